@@ -1,0 +1,214 @@
+/* pegrad_b200 — B200-native (sm_100a) DPSGD step engine, C ABI.
+ *
+ * The reference ("pegrad", /root/reference/proj) has no FFI: its step path is
+ * the in-process C++ API
+ *     dpsgd_step(Model<T>&, GradEngine<T>&, x, y, DpConfig<T>, step_index)
+ *         -> StepReport<T>                      (core/include/pegrad/dpsgd.hpp:70-73)
+ *     GradEngine<T>(model, Strategy, batch, ExecMode)
+ *         compute / compute_views               (core/include/pegrad/strategies.hpp:58-100)
+ *     models::build_desc / build                (core/include/pegrad/models.hpp:75-88)
+ *     bench::run_bench / train                  (core/include/pegrad/harness.hpp:75-115)
+ * This header is the drop-in boundary for that path: plain pointers and
+ * sizes, no torch or C++ types. include/pegrad_b200.hpp wraps it back into
+ * the reference's C++ shapes (Model, DpConfig, StepReport, exceptions).
+ *
+ * Layout contract (same as the reference's Tensor<float>): row-major NCHW
+ * fp32 inputs, ids/labels as integral floats, parameters flattened in
+ * parameter-registry order (models.cpp:50-83); per-example gradient stacks
+ * are block-major: block p is (B, numel(shape_p)), blocks concatenated.
+ */
+#ifndef PEGRAD_B200_H
+#define PEGRAD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGB_MAX_LAYERS 32
+#define PGB_MAX_PARAMS 64
+
+/* 1:1 with the pegrad exception hierarchy (common.hpp:56-114), plus device
+ * failures the reference cannot have. */
+typedef enum pgb_status {
+  PGB_OK = 0,
+  PGB_ERR_SHAPE = 1,       /* ShapeError */
+  PGB_ERR_DOMAIN = 2,      /* DomainError */
+  PGB_ERR_INDEX = 3,       /* IndexError: ids / labels */
+  PGB_ERR_CONFIG = 4,      /* ConfigError: DpConfig, unknown names */
+  PGB_ERR_CONTRACT = 5,    /* ContractError: batch mismatch, bad handle */
+  PGB_ERR_UNSUPPORTED = 6, /* UnsupportedError: "unsupported layer" */
+  PGB_ERR_TRACE = 7,
+  PGB_ERR_FORMAT = 8,
+  PGB_ERR_IO = 9,
+  PGB_ERR_CUDA = 10,
+  PGB_ERR_NCCL = 11,
+  PGB_ERR_OOM = 12
+} pgb_status;
+
+/* pegrad::models::ModelKind (models.hpp:24) */
+enum { PGB_LOGREG = 0, PGB_FCNN, PGB_MNIST_CNN, PGB_CIFAR_CNN, PGB_EMBED, PGB_LSTM_MODEL };
+/* pegrad::models::LayerKind (models.hpp:29-40) */
+enum {
+  PGB_DENSE = 0, PGB_CONV, PGB_MAXPOOL, PGB_AVGPOOL, PGB_GLOBAL_AVGPOOL,
+  PGB_FLATTEN, PGB_RELU, PGB_EMBEDDING, PGB_SEQ_AVGPOOL, PGB_LSTM
+};
+/* pegrad::Strategy (strategies.hpp:34) */
+enum { PGB_NAIVE = 0, PGB_VMAP, PGB_OUTER, PGB_NORMS, PGB_GROUPCONV, PGB_JACMM };
+
+/* pegrad::models::LayerSpec (models.hpp:42-49) */
+typedef struct pgb_layer_spec {
+  int32_t kind;
+  int64_t in, out, k, stride, pad;
+} pgb_layer_spec;
+
+/* pegrad::models::ModelOptions (models.hpp:52-56); -1 keeps the default */
+typedef struct pgb_model_options {
+  int64_t seq_len, vocab, hidden;
+} pgb_model_options;
+
+/* pegrad::models::ModelDesc (models.hpp:58-73); the registry part
+ * (param_size / param_fan_in) is filled by pgb_finish_desc. */
+typedef struct pgb_model_desc {
+  int32_t model_kind;
+  int32_t n_layers;
+  pgb_layer_spec layers[PGB_MAX_LAYERS];
+  int32_t input_rank;
+  int64_t input_shape[3];
+  int64_t classes; /* 1 selects the binary sigmoid head */
+  int32_t token_input;
+  int32_t n_params;
+  int64_t param_size[PGB_MAX_PARAMS];
+  int64_t param_fan_in[PGB_MAX_PARAMS];
+} pgb_model_desc;
+
+/* pegrad::DpConfig<float> (dpsgd.hpp:24-31) */
+typedef struct pgb_dp_config {
+  float clip_norm;        /* C > 0 */
+  float noise_multiplier; /* sigma >= 0, noise stddev sigma*C */
+  float learning_rate;
+  int64_t microbatch;     /* m, divides the batch */
+  uint64_t seed;
+} pgb_dp_config;
+
+/* pegrad::StepReport<float> (dpsgd.hpp:36-41); pre_clip_norms are returned
+ * through a caller buffer of B/m floats. */
+typedef struct pgb_step_report {
+  int64_t clipped_count;
+  int32_t n_streams;
+  uint64_t noise_streams[PGB_MAX_PARAMS];
+} pgb_step_report;
+
+typedef struct pgb_unique_id {
+  char internal[128];
+} pgb_unique_id;
+
+typedef struct pgb_engine_info {
+  int64_t batch;          /* local examples per step */
+  int64_t global_batch;   /* batch * world */
+  int64_t param_count;
+  int32_t n_params;
+  int32_t world, rank, device;
+  int64_t workspace_bytes; /* device arena */
+  int32_t kernels_per_step;
+  int32_t graph_enabled;
+} pgb_engine_info;
+
+typedef struct pgb_engine pgb_engine;
+
+const char* pgb_last_error(void);
+const char* pgb_version(void);
+
+/* ---- models (host) : models.cpp:50-167, 359-380 ------------------------- */
+pgb_status pgb_build_desc(int32_t model_kind, const pgb_model_options* opts,
+                          pgb_model_desc* out);
+pgb_status pgb_finish_desc(pgb_model_desc* desc);
+int64_t pgb_param_count(const pgb_model_desc* desc);
+pgb_status pgb_init_params(const pgb_model_desc* desc, uint64_t seed,
+                           float* flat_out);
+/* io::synth_for_model<float> (dataset.cpp:219-237), x (n, input_shape), y (n) */
+pgb_status pgb_synth(const pgb_model_desc* desc, int64_t n, uint64_t seed,
+                     float* x_out, float* y_out);
+
+/* ---- engine : GradEngine + dpsgd_step ------------------------------------ */
+pgb_status pgb_engine_create(const pgb_model_desc* desc, int32_t strategy,
+                             int64_t batch, int32_t device, pgb_engine** out);
+/* Data-parallel: one engine per GPU/process; `local_batch` examples each,
+ * one NCCL all-reduce of the clipped sum per step. Collective over `world`. */
+pgb_status pgb_nccl_unique_id(pgb_unique_id* out);
+pgb_status pgb_engine_create_dist(const pgb_model_desc* desc, int32_t strategy,
+                                  int64_t local_batch, int32_t device,
+                                  int32_t rank, int32_t world,
+                                  const pgb_unique_id* id, pgb_engine** out);
+void pgb_engine_destroy(pgb_engine* e);
+pgb_status pgb_engine_info_get(pgb_engine* e, pgb_engine_info* out);
+pgb_status pgb_engine_set_graph(pgb_engine* e, int32_t enable);
+
+pgb_status pgb_set_params(pgb_engine* e, const float* flat);
+pgb_status pgb_get_params(pgb_engine* e, float* flat);
+
+/* One DPSGD step from HOST buffers (x: batch*numel(input), y: batch).
+ * Synchronous; norms_out (batch/m floats) and report may be NULL. */
+pgb_status pgb_dpsgd_step(pgb_engine* e, const float* x, const float* y,
+                          const pgb_dp_config* cfg, int64_t step_index,
+                          float* norms_out, pgb_step_report* report);
+/* Same step from DEVICE pointers, enqueued on the engine stream; returns
+ * without synchronizing. pgb_synchronize waits and reports the last step. */
+pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x,
+                                 const float* d_y, const pgb_dp_config* cfg,
+                                 int64_t step_index);
+pgb_status pgb_synchronize(pgb_engine* e, float* norms_out,
+                           pgb_step_report* report);
+/* sgd_step (dpsgd.cpp:334-346) */
+pgb_status pgb_sgd_step(pgb_engine* e, const float* x, const float* y,
+                        float learning_rate);
+
+/* compute_views probe: per-example gradient stacks (block-major, B*P) and
+ * pre-clip norms (B) for the current parameters. Either may be NULL. */
+pgb_status pgb_per_example_grads(pgb_engine* e, const float* x, const float* y,
+                                 float* stacks_out, float* norms_out);
+/* Noise-free clipped sum  sum_i min(1, C/||g_i||) g_i  (P floats, no update),
+ * pre-clip norms (batch) and clipped count: the parity probe of north-star
+ * items (2)-(3). Any output may be NULL. */
+pgb_status pgb_clipped_sum(pgb_engine* e, const float* x, const float* y, float clip_norm,
+                           float* sum_out, float* norms_out, int64_t* clipped_out);
+/* Forward only: per-example losses (batch) and logits (batch*classes). */
+pgb_status pgb_forward(pgb_engine* e, const float* x, const float* y, float* losses_out,
+                       float* logits_out);
+/* The views-path tail over caller-supplied stacks: norms, clip, clipped sum,
+ * noise, mean, update (dpsgd.cpp:232-322). Updates the engine parameters. */
+pgb_status pgb_aggregate(pgb_engine* e, const float* stacks,
+                         const pgb_dp_config* cfg, int64_t step_index,
+                         float* norms_out, pgb_step_report* report);
+/* gaussian<float>(n, RngState(seed, stream)) generated on the device. */
+pgb_status pgb_gaussian(int32_t device, uint64_t seed, uint64_t stream,
+                        int64_t n, float* out);
+
+/* run_bench-shaped epoch driver (harness.cpp:85-167): n/batch sequential
+ * slices of host x/y, step_index = step0 + s; batches streamed H2D on a copy
+ * stream (double-buffered) while the previous step computes. Per-step norms
+ * (steps*batch floats) are copied back when norms_out != NULL. */
+pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y,
+                         int64_t n_examples, const pgb_dp_config* cfg,
+                         int64_t step0, float* norms_out,
+                         int64_t* clipped_total, double* seconds_out);
+
+/* Device addresses for zero-copy interop (torch, benchmarks). */
+pgb_status pgb_device_params(pgb_engine* e, float** d_params);
+pgb_status pgb_device_stream(pgb_engine* e, void** cuda_stream);
+/* Per-kernel device time of the (non-graph) step schedule, averaged over
+ * n_steps (<= 32) steps, measured with CUDA events on the engine stream
+ * while the launches run back to back. names_out holds 32 chars/kernel. */
+pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
+                             const pgb_dp_config* cfg, int64_t step0, int32_t n_steps,
+                             int32_t max_kernels, float* ms_out, char* names_out,
+                             int32_t* n_kernels_out);
+/* Kernel launches recorded for the last step (profiling/evidence). */
+int32_t pgb_kernels_per_step(pgb_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PEGRAD_B200_H */

@@ -1,0 +1,1093 @@
+// The DPSGD step engine: lowers a ModelDesc to a fixed sm_100a kernel
+// schedule (no tape, no interpreter), keeps parameters and every workspace
+// resident in one device arena, and replays the step as a CUDA graph.
+//
+// Replaces, for the GPU: GradEngine<float> (proj/core/src/strategies.cpp:
+// 221-495) + the dpsgd_step views path (proj/core/src/dpsgd.cpp:188-331) +
+// the run_bench epoch loop (proj/core/src/harness.cpp:85-167).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "pgb_internal.h"
+
+namespace pgb {
+
+#define PGB_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      const pgb_status st_ = (e_ == cudaErrorMemoryAllocation) ? PGB_ERR_OOM : PGB_ERR_CUDA; \
+      raise(st_, std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    }                                                                                   \
+  } while (0)
+
+// ---- NCCL, resolved at runtime so single-GPU use never needs libnccl ------
+struct Nccl {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  static Nccl& get() {
+    static Nccl n = [] {
+      Nccl r;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) return r;
+      r.getUniqueId = (decltype(r.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      r.commInitRank = (decltype(r.commInitRank))dlsym(h, "ncclCommInitRank");
+      r.allReduce = (decltype(r.allReduce))dlsym(h, "ncclAllReduce");
+      r.commDestroy = (decltype(r.commDestroy))dlsym(h, "ncclCommDestroy");
+      r.errStr = (decltype(r.errStr))dlsym(h, "ncclGetErrorString");
+      r.groupStart = (decltype(r.groupStart))dlsym(h, "ncclGroupStart");
+      r.groupEnd = (decltype(r.groupEnd))dlsym(h, "ncclGroupEnd");
+      return r;
+    }();
+    if (!n.allReduce) raise(PGB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    return n;
+  }
+};
+
+#define PGB_NCCL(call)                                                                  \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      raise(PGB_ERR_NCCL, std::string(#call) + ": " + Nccl::get().errStr(r_));          \
+  } while (0)
+
+// ---- launch helpers -----------------------------------------------------------
+inline int grid_for(size_t n, int threads = 256) {
+  size_t g = (n + threads - 1) / threads;
+  return (int)std::min<size_t>(std::max<size_t>(g, 1), 148 * 16);
+}
+
+template <class Op>
+void launch_gemm(const Op& op, int batch, cudaStream_t s) {
+  if (op.M >= 64) {
+    dim3 grid((op.N + 63) / 64, (op.M + 63) / 64, batch);
+    tile_gemm_kernel<Op, 64, 64, 16, 4, 4><<<grid, 256, 0, s>>>(op);
+  } else if (op.M >= 32) {
+    dim3 grid((op.N + 63) / 64, (op.M + 31) / 32, batch);
+    tile_gemm_kernel<Op, 32, 64, 16, 4, 4><<<grid, 128, 0, s>>>(op);
+  } else {
+    dim3 grid((op.N + 127) / 128, (op.M + 15) / 16, batch);
+    tile_gemm_kernel<Op, 16, 128, 16, 4, 4><<<grid, 128, 0, s>>>(op);
+  }
+}
+
+struct Layer {
+  pgb_layer_spec spec;
+  ExShape in, out;
+  int pblock = -1;       // first parameter block
+  float* act_in = nullptr;
+  float* act_out = nullptr;
+  bool alias = false;    // flatten / fused relu / fused seq_avgpool: no kernel
+  bool fused_relu = false;      // producer applies relu
+  bool fused_pool = false;      // embedding fused with the following seq_avgpool
+  bool skip_bwd = false;        // handled by a neighbour in the backward pass
+  bool needs_gx = false;        // input gradient needed upstream
+  const float* bwd_mask = nullptr;  // relu output to gate gx with
+};
+
+struct Engine {
+  pgb_model_desc desc{};
+  int strategy = 0;
+  int64_t B = 0;
+  int device = 0, rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+
+  std::vector<Layer> layers;
+  BlockTable bt{};
+  int64_t P = 0;
+  int64_t in_row = 0;
+  int first_param_layer = 0;
+
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  // arena
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  float* d_params = nullptr;
+  float* d_x = nullptr;
+  float* d_y = nullptr;
+  float* d_xb[2] = {nullptr, nullptr};
+  float* d_yb[2] = {nullptr, nullptr};
+  float* d_stacks = nullptr;
+  float* d_units = nullptr;
+  double* d_parts = nullptr;
+  float* d_cot[2] = {nullptr, nullptr};
+  float* d_loss = nullptr;
+  float* d_norms = nullptr;
+  float* d_sum = nullptr;  // P floats + clipped count slot (dist)
+  int* d_clipped = nullptr;
+  DevError* d_err = nullptr;
+  StepArgs* d_args = nullptr;
+  std::vector<float*> d_acts;
+
+  // pinned host staging
+  static constexpr int kArgSlots = 64;
+  StepArgs* h_args = nullptr;
+  cudaEvent_t slot_ev[kArgSlots];
+  bool slot_used[kArgSlots] = {};
+  int64_t arg_counter = 0;
+  float* h_norms = nullptr;
+  int* h_clipped = nullptr;
+  DevError* h_err = nullptr;
+
+  bool graph_enabled = true;
+  std::map<int, cudaGraphExec_t> graphs;  // key: schedule variant
+  int kernels_last = 0;
+  int last_units = 0;
+  pgb_dp_config last_cfg{};
+  int64_t last_step = 0;
+
+  ~Engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (stream) cudaStreamSynchronize(stream);
+    for (int i = 0; i < kArgSlots; ++i)
+      if (slot_ev[i]) cudaEventDestroy(slot_ev[i]);
+    if (comm) Nccl::get().commDestroy(comm);
+    if (arena) cudaFree(arena);
+    if (h_args) cudaFreeHost(h_args);
+    if (h_norms) cudaFreeHost(h_norms);
+    if (h_clipped) cudaFreeHost(h_clipped);
+    if (h_err) cudaFreeHost(h_err);
+    if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
+
+  // ---- planning ------------------------------------------------------------
+  void plan() {
+    ExShape s[PGB_MAX_LAYERS + 1];
+    layer_shapes(desc, s);
+    const int n = desc.n_layers;
+    layers.resize(n);
+    int blk = 0;
+    first_param_layer = n;
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      L.spec = desc.layers[l];
+      L.in = s[l];
+      L.out = s[l + 1];
+      const int k = L.spec.kind;
+      if (k == PGB_LSTM) raise(PGB_ERR_UNSUPPORTED, "unsupported layer: lstm (GPU engine)");
+      if (k == PGB_DENSE || k == PGB_CONV || k == PGB_EMBEDDING) {
+        L.pblock = blk;
+        blk += (k == PGB_EMBEDDING) ? 1 : 2;
+        if (first_param_layer == n) first_param_layer = l;
+      }
+      if (k == PGB_EMBEDDING && (l + 1 >= n || desc.layers[l + 1].kind != PGB_SEQ_AVGPOOL))
+        raise(PGB_ERR_UNSUPPORTED,
+              "unsupported layer: embedding must feed seq_avgpool (GPU engine)");
+    }
+    if (blk != desc.n_params) raise(PGB_ERR_CONTRACT, "parameter registry does not match layers");
+    // fusion decisions
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      const int k = L.spec.kind;
+      if (k == PGB_FLATTEN) L.alias = true;
+      if (k == PGB_RELU && l > 0 &&
+          (layers[l - 1].spec.kind == PGB_DENSE || layers[l - 1].spec.kind == PGB_CONV)) {
+        L.alias = true;
+        layers[l - 1].fused_relu = true;
+      }
+      if (k == PGB_SEQ_AVGPOOL && l > 0 && layers[l - 1].spec.kind == PGB_EMBEDDING) {
+        L.alias = true;
+        layers[l - 1].fused_pool = true;
+      }
+    }
+    // backward: which layers produce an input gradient, and which relu mask
+    for (int l = n - 1; l >= 0; --l) {
+      Layer& L = layers[l];
+      L.needs_gx = l > first_param_layer;
+    }
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      const int k = L.spec.kind;
+      if (k == PGB_FLATTEN || k == PGB_RELU || k == PGB_SEQ_AVGPOOL) L.skip_bwd = true;
+    }
+    // blocks
+    bt.n = desc.n_params;
+    int64_t off = 0, poff = 0;
+    long long pairs = 0;
+    for (int p = 0; p < bt.n; ++p) {
+      bt.size[p] = desc.param_size[p];
+      bt.param_off[p] = poff;
+      bt.stack_off[p] = off;
+      bt.pair_off[p] = pairs;
+      poff += desc.param_size[p];
+      off += desc.param_size[p] * B;
+      pairs += (desc.param_size[p] + 1) / 2;
+    }
+    bt.pair_off[bt.n] = pairs;
+    P = poff;
+    in_row = s[0].numel();
+  }
+
+  void allocate() {
+    // size every buffer, then carve one arena (256-byte aligned slices)
+    const int n = desc.n_layers;
+    std::vector<std::pair<void**, size_t>> req;
+    auto want = [&](void** p, size_t bytes) { req.emplace_back(p, (bytes + 255) & ~size_t(255)); };
+    want((void**)&d_params, sizeof(float) * P);
+    want((void**)&d_x, sizeof(float) * B * in_row);
+    want((void**)&d_y, sizeof(float) * B);
+    for (int i = 0; i < 2; ++i) {
+      want((void**)&d_xb[i], sizeof(float) * B * in_row);
+      want((void**)&d_yb[i], sizeof(float) * B);
+    }
+    want((void**)&d_stacks, sizeof(float) * B * P);
+    want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
+    want((void**)&d_parts, sizeof(double) * B * bt.n);
+    int64_t max_act = 0;
+    for (int l = 0; l < n; ++l) max_act = std::max(max_act, layers[l].out.numel());
+    max_act = std::max(max_act, in_row);
+    want((void**)&d_cot[0], sizeof(float) * B * max_act);
+    want((void**)&d_cot[1], sizeof(float) * B * max_act);
+    want((void**)&d_loss, sizeof(float) * B);
+    want((void**)&d_norms, sizeof(float) * B);
+    want((void**)&d_sum, sizeof(float) * (P + 2));
+    want((void**)&d_clipped, sizeof(int) * 2);
+    want((void**)&d_err, sizeof(DevError));
+    want((void**)&d_args, sizeof(StepArgs));
+    d_acts.assign(n + 1, nullptr);
+    std::vector<float*> owned(n + 1, nullptr);
+    for (int l = 0; l < n; ++l) {
+      const Layer& L = layers[l];
+      if (L.alias) continue;
+      // embedding+seq_avgpool is one kernel writing the pooled (B, E) output
+      const int64_t numel = L.fused_pool ? layers[l + 1].out.numel() : L.out.numel();
+      want((void**)&owned[l + 1], sizeof(float) * B * numel);
+    }
+    arena_bytes = 0;
+    for (auto& r : req) arena_bytes += r.second;
+    PGB_CUDA(cudaMalloc(&arena, arena_bytes));
+    PGB_CUDA(cudaMemset(arena, 0, arena_bytes));
+    size_t o = 0;
+    for (auto& r : req) {
+      *r.first = arena + o;
+      o += r.second;
+    }
+    // activation chain: act_in(0) = null = the step's input slot
+    float* cur = nullptr;
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      L.act_in = cur;
+      L.act_out = L.alias ? cur : owned[l + 1];
+      cur = L.act_out;
+    }
+    // masks: relu output gating the input gradient of the next real layer
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      if (L.skip_bwd) continue;
+      bool relu = false;
+      for (int j = l - 1; j >= 0; --j) {
+        const int k = layers[j].spec.kind;
+        if (k == PGB_RELU) relu = true;
+        if (k != PGB_RELU && k != PGB_FLATTEN) break;
+      }
+      L.bwd_mask = relu ? L.act_in : nullptr;
+    }
+  }
+
+  void init(const pgb_model_desc& d, int strat, int64_t batch, int dev) {
+    desc = d;
+    strategy = strat;
+    B = batch;
+    device = dev;
+    if (B <= 0) raise(PGB_ERR_CONTRACT, "GradEngine: batch must be positive");
+    check_strategy_support(strat, desc);
+    plan();
+    PGB_CUDA(cudaSetDevice(device));
+    PGB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    allocate();
+    PGB_CUDA(cudaMallocHost(&h_args, sizeof(StepArgs) * kArgSlots));
+    PGB_CUDA(cudaMallocHost(&h_norms, sizeof(float) * B));
+    PGB_CUDA(cudaMallocHost(&h_clipped, sizeof(int) * 2));
+    PGB_CUDA(cudaMallocHost(&h_err, sizeof(DevError)));
+    for (int i = 0; i < kArgSlots; ++i)
+      PGB_CUDA(cudaEventCreateWithFlags(&slot_ev[i], cudaEventDisableTiming));
+    // reference init is the default parameter state (models::build, seed 0)
+    std::vector<float> p0(P);
+    if (pgb_init_params(&desc, 0, p0.data()) != PGB_OK) raise(PGB_ERR_CONTRACT, "init failed");
+    PGB_CUDA(cudaMemcpy(d_params, p0.data(), sizeof(float) * P, cudaMemcpyHostToDevice));
+  }
+
+  // ---- profiling hook: an event after every launch while profiling --------
+  std::vector<std::pair<cudaEvent_t, const char*>>* prof = nullptr;
+  int mark(cudaStream_t s, const char* name) {
+    if (prof) {
+      cudaEvent_t ev;
+      PGB_CUDA(cudaEventCreate(&ev));
+      PGB_CUDA(cudaEventRecord(ev, s));
+      prof->emplace_back(ev, name);
+    }
+    return 1;
+  }
+
+  // ---- schedule ------------------------------------------------------------
+  // Per-example gradient stacks for the batch whose input pointer sits in
+  // d_args->x (the reference's compute_views). Returns kernels launched.
+  int enqueue_forward(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    int nk = 0;
+    const int n = desc.n_layers;
+    const int Bi = (int)B;
+    // forward
+    for (int l = 0; l < n; ++l) {
+      Layer& L = layers[l];
+      const float* in = L.act_in ? L.act_in : x_slot;
+      const pgb_layer_spec& sp = L.spec;
+      const float* W = L.pblock >= 0 ? d_params + bt.param_off[L.pblock] : nullptr;
+      switch (sp.kind) {
+        case PGB_DENSE: {
+          DenseFwdOp op{Bi, (int)sp.out, (int)sp.in, in, W, W + sp.in * sp.out, L.act_out,
+                        L.fused_relu ? 1 : 0};
+          launch_gemm(op, 1, s);
+          nk += mark(s, "dense_fwd");
+          break;
+        }
+        case PGB_CONV: {
+          ConvGeom g{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
+                     (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride, (int)sp.pad};
+          const int K = g.C * g.k * g.k;
+          ConvFwdOp op{g.D, Bi * g.Ho * g.Wo, K, g, in, W, W + (size_t)g.D * K, L.act_out,
+                       L.fused_relu ? 1 : 0};
+          launch_gemm(op, 1, s);
+          nk += mark(s, "conv_fwd");
+          break;
+        }
+        case PGB_MAXPOOL:
+        case PGB_AVGPOOL: {
+          const size_t tot = (size_t)B * L.out.numel();
+          pool_fwd_kernel<<<grid_for(tot), 256, 0, s>>>(
+              in, L.act_out, Bi * (int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2],
+              (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
+              sp.kind == PGB_MAXPOOL);
+          nk += mark(s, "pool_fwd");
+          break;
+        }
+        case PGB_GLOBAL_AVGPOOL: {
+          const int BC = Bi * (int)L.in.d[0];
+          gap_fwd_kernel<<<(BC * 32 + 255) / 256, 256, 0, s>>>(in, L.act_out, BC,
+                                                              (int)(L.in.d[1] * L.in.d[2]));
+          nk += mark(s, "gap_fwd");
+          break;
+        }
+        case PGB_RELU:
+          if (!L.alias) {
+            relu_fwd_kernel<<<grid_for((size_t)B * L.in.numel()), 256, 0, s>>>(
+                in, L.act_out, (size_t)B * L.in.numel());
+            nk += mark(s, "relu_fwd");
+          }
+          break;
+        case PGB_EMBEDDING: {
+          const int E = (int)sp.out;
+          embed_pool_fwd_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
+              in, W, L.act_out, Bi, (int)L.in.d[0], E, (int)sp.in, d_err);
+          nk += mark(s, "embed_pool_fwd");
+          break;
+        }
+        default:
+          break;  // flatten / fused relu / fused seq_avgpool
+      }
+    }
+    // loss and dlogits
+    const Layer& last = layers[n - 1];
+    const float* logits = last.act_out;
+    float* g = d_cot[0];
+    xent_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(logits, y_slot, Bi, (int)desc.classes, d_loss,
+                                                 g, d_err);
+    nk += mark(s, "xent");
+    return nk;
+  }
+
+  const float* logits_buffer() const { return layers.back().act_out; }
+
+  int enqueue_grads(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    int nk = enqueue_forward(s, x_slot, y_slot);
+    const int n = desc.n_layers;
+    const int Bi = (int)B;
+    // backward
+    int gi = 0;
+    for (int l = n - 1; l >= first_param_layer; --l) {
+      Layer& L = layers[l];
+      if (L.skip_bwd) continue;
+      const pgb_layer_spec& sp = L.spec;
+      const float* in = L.act_in ? L.act_in : x_slot;
+      const float* W = L.pblock >= 0 ? d_params + bt.param_off[L.pblock] : nullptr;
+      float* gcur = d_cot[gi];
+      float* gnext = d_cot[gi ^ 1];
+      switch (sp.kind) {
+        case PGB_DENSE: {
+          float* sW = d_stacks + bt.stack_off[L.pblock];
+          float* sb = d_stacks + bt.stack_off[L.pblock + 1];
+          dense_pex_kernel<<<grid_for((size_t)B * sp.in * sp.out), 256, 0, s>>>(
+              in, gcur, Bi, (int)sp.in, (int)sp.out, sW, sb);
+          nk += mark(s, "dense_pex");
+          if (L.needs_gx) {
+            DenseBwdXOp op{Bi, (int)sp.in, (int)sp.out, gcur, W, L.bwd_mask, gnext};
+            launch_gemm(op, 1, s);
+            nk += mark(s, "dense_bwd_x");
+          }
+          break;
+        }
+        case PGB_CONV: {
+          ConvGeom gg{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
+                      (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
+                      (int)sp.pad};
+          const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
+          float* sW = d_stacks + bt.stack_off[L.pblock];
+          float* sb = d_stacks + bt.stack_off[L.pblock + 1];
+          ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
+          launch_gemm(dw, Bi, s);
+          nk += mark(s, "conv_dw_pex");
+          conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
+                                                                         sb);
+          nk += mark(s, "conv_db_pex");
+          if (L.needs_gx) {
+            ConvBwdXOp op{gg.C, Bi * gg.H * gg.W, gg.D * gg.k * gg.k, gg, gcur, W,
+                          L.bwd_mask, gnext};
+            launch_gemm(op, 1, s);
+            nk += mark(s, "conv_bwd_x");
+          }
+          break;
+        }
+        case PGB_MAXPOOL:
+        case PGB_AVGPOOL: {
+          const size_t tot = (size_t)B * L.in.numel();
+          pool_bwd_kernel<<<grid_for(tot), 256, 0, s>>>(
+              in, gcur, L.bwd_mask, gnext, Bi * (int)L.in.d[0], (int)L.in.d[1],
+              (int)L.in.d[2], (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
+              sp.kind == PGB_MAXPOOL);
+          nk += mark(s, "pool_bwd");
+          break;
+        }
+        case PGB_GLOBAL_AVGPOOL: {
+          const size_t tot = (size_t)B * L.in.numel();
+          gap_bwd_kernel<<<grid_for(tot), 256, 0, s>>>(gcur, L.bwd_mask, gnext,
+                                                      Bi * (int)L.in.d[0],
+                                                      (int)(L.in.d[1] * L.in.d[2]));
+          nk += mark(s, "gap_bwd");
+          break;
+        }
+        case PGB_EMBEDDING: {
+          const int E = (int)sp.out, V = (int)sp.in;
+          float* st = d_stacks + bt.stack_off[L.pblock];
+          PGB_CUDA(cudaMemsetAsync(st, 0, sizeof(float) * B * V * E, s));
+          embed_pex_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
+              in, gcur, Bi, (int)L.in.d[0], E, V, st);
+          nk += mark(s, "embed_pex");
+          break;
+        }
+        default:
+          raise(PGB_ERR_UNSUPPORTED,
+                std::string("unsupported layer in backward: ") + layer_kind_name(sp.kind));
+      }
+      if (L.needs_gx && sp.kind != PGB_EMBEDDING) gi ^= 1;
+      // a standalone relu directly below a pooling layer is gated by bwd_mask
+    }
+    return nk;
+  }
+
+  // One full DPSGD step (variant: 0 = m==1 fused, 1 = m>1, 2 = dist).
+  int enqueue_step(cudaStream_t s, const float* x_slot, const float* y_slot, int64_t m) {
+    int nk = 0;
+    PGB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(DevError), s));
+    PGB_CUDA(cudaMemsetAsync(d_clipped, 0, sizeof(int) * 2, s));
+    nk += enqueue_grads(s, x_slot, y_slot);
+    const int U = (int)(B / m);
+    const float* src = d_stacks;
+    if (m > 1) {
+      BlockTable ut = bt;
+      for (int p = 0; p < bt.n; ++p) ut.stack_off[p] = bt.param_off[p] * U;
+      microbatch_kernel<<<grid_for((size_t)P * U), 256, 0, s>>>(d_stacks, bt, (int)B, (int)m,
+                                                                 d_units);
+      nk += mark(s, "microbatch");
+      src = d_units;
+      nk += enqueue_aggregate(s, src, ut, U);
+    } else {
+      nk += enqueue_aggregate(s, src, bt, U);
+    }
+    return nk;
+  }
+
+  int enqueue_aggregate(cudaStream_t s, const float* stacks, const BlockTable& t, int U) {
+    int nk = 0;
+    dim3 sg(t.n, U);
+    sumsq_kernel<<<sg, 128, 0, s>>>(stacks, t, U, d_parts);
+    nk += mark(s, "sumsq");
+    const long long pairs = t.pair_off[t.n];
+    const int threads = 256;
+    const int grid = (int)std::min<long long>((pairs + threads - 1) / threads, 148 * 8);
+    const size_t smem = sizeof(float) * U;
+    if (world == 1) {
+      aggregate_kernel<8><<<grid, threads, smem, s>>>(stacks, d_parts, t, d_args, d_params,
+                                                      nullptr, d_norms, d_clipped, d_err, 0);
+      nk += mark(s, "aggregate");
+    } else {
+      aggregate_kernel<8><<<grid, threads, smem, s>>>(stacks, d_parts, t, d_args, d_params,
+                                                      d_sum, d_norms, d_clipped, d_err, 1);
+      nk += mark(s, "aggregate_local");
+      auto& N = Nccl::get();
+      PGB_NCCL(N.groupStart());
+      PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
+      PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
+      PGB_NCCL(N.groupEnd());
+      noise_update_kernel<<<grid, threads, 0, s>>>(d_sum, t, d_args, d_params, d_err);
+      nk += mark(s, "noise_update");
+    }
+    return nk;
+  }
+
+  // Noise-free clipped sum of the batch into d_sum (no update): the
+  // north-star parity probe.
+  int enqueue_local_sum(cudaStream_t s, const float* stacks, const BlockTable& t, int U) {
+    dim3 sg(t.n, U);
+    sumsq_kernel<<<sg, 128, 0, s>>>(stacks, t, U, d_parts);
+    const long long pairs = t.pair_off[t.n];
+    const int grid = (int)std::min<long long>((pairs + 255) / 256, 148 * 8);
+    aggregate_kernel<8><<<grid, 256, sizeof(float) * U, s>>>(
+        stacks, d_parts, t, d_args, d_params, d_sum, d_norms, d_clipped, d_err, 1);
+    return 2;
+  }
+
+  // ---- step argument slots (pinned ring) ------------------------------------
+  void push_args(const StepArgs& a) {
+    const int k = (int)(arg_counter++ % kArgSlots);
+    if (slot_used[k]) PGB_CUDA(cudaEventSynchronize(slot_ev[k]));
+    h_args[k] = a;
+    PGB_CUDA(cudaMemcpyAsync(d_args, &h_args[k], sizeof(StepArgs), cudaMemcpyHostToDevice,
+                             stream));
+    PGB_CUDA(cudaEventRecord(slot_ev[k], stream));
+    slot_used[k] = true;
+  }
+
+  StepArgs make_args(const pgb_dp_config& c, int64_t step, const float* x, const float* y) {
+    StepArgs a{};
+    const int64_t units = (B / c.microbatch) * world;
+    a.clip = c.clip_norm;
+    a.sigma = c.noise_multiplier;
+    a.lr = c.learning_rate;
+    a.inv_units = 1.0f / static_cast<float>(units);
+    a.seed = c.seed;
+    a.step = step;
+    a.units = (int)(B / c.microbatch);
+    a.add_noise = c.noise_multiplier > 0.0f;
+    (void)x;
+    (void)y;
+    return a;
+  }
+
+  // Launch the step for inputs already resident at d_x/d_y slots.
+  void launch_step(const float* x_slot, const float* y_slot, int64_t m) {
+    const int variant = (m > 1 ? 1 : 0) | (world > 1 ? 2 : 0);
+    const int key = variant * 4 + (x_slot == d_x ? 0 : x_slot == d_xb[0] ? 1 : 2);
+    if (!graph_enabled) {
+      kernels_last = enqueue_step(stream, x_slot, y_slot, m);
+      PGB_CUDA(cudaGetLastError());
+      return;
+    }
+    auto it = graphs.find(key * 64 + (int)std::min<int64_t>(m, 63));
+    if (it == graphs.end()) {
+      cudaGraph_t g;
+      PGB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      int nk = 0;
+      try {
+        nk = enqueue_step(stream, x_slot, y_slot, m);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        throw;
+      }
+      PGB_CUDA(cudaStreamEndCapture(stream, &g));
+      cudaGraphExec_t ge;
+      PGB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = graphs.emplace(key * 64 + (int)std::min<int64_t>(m, 63), ge).first;
+      kernels_last = nk;
+    }
+    PGB_CUDA(cudaGraphLaunch(it->second, stream));
+  }
+
+  void check_device_error() {
+    if (h_err->code == 0) return;
+    const DevError e = *h_err;
+    if (e.what == 0)
+      raise(PGB_ERR_INDEX, "softmax_xent label: id " + std::to_string((long long)e.value) +
+                               " out of range [0," + std::to_string(e.limit) + ") at position " +
+                               std::to_string(e.pos));
+    raise(PGB_ERR_INDEX, "gather_rows: id " + std::to_string(e.value) + " out of range [0," +
+                             std::to_string(e.limit) + ") at position " + std::to_string(e.pos));
+  }
+
+  void read_report(float* norms_out, pgb_step_report* rep, int64_t m, int64_t step) {
+    const int U = (int)(B / m);
+    PGB_CUDA(cudaMemcpyAsync(h_err, d_err, sizeof(DevError), cudaMemcpyDeviceToHost, stream));
+    PGB_CUDA(cudaMemcpyAsync(h_clipped, d_clipped, sizeof(int) * 2, cudaMemcpyDeviceToHost,
+                             stream));
+    if (norms_out)
+      PGB_CUDA(cudaMemcpyAsync(h_norms, d_norms, sizeof(float) * U, cudaMemcpyDeviceToHost,
+                               stream));
+    PGB_CUDA(cudaStreamSynchronize(stream));
+    check_device_error();
+    if (norms_out) std::memcpy(norms_out, h_norms, sizeof(float) * U);
+    if (rep) {
+      rep->clipped_count = world > 1 ? h_clipped[1] : h_clipped[0];
+      rep->n_streams = 0;
+      if (last_cfg.noise_multiplier > 0.0f) {
+        rep->n_streams = bt.n;
+        for (int p = 0; p < bt.n; ++p) rep->noise_streams[p] = noise_stream(step, p);
+      }
+    }
+  }
+
+  void step_host(const float* x, const float* y, const pgb_dp_config& c, int64_t step,
+                 float* norms_out, pgb_step_report* rep) {
+    validate_dp_config(c, B);
+    if (!x || !y) raise(PGB_ERR_CONTRACT, "null input");
+    PGB_CUDA(cudaMemcpyAsync(d_x, x, sizeof(float) * B * in_row, cudaMemcpyHostToDevice,
+                             stream));
+    PGB_CUDA(cudaMemcpyAsync(d_y, y, sizeof(float) * B, cudaMemcpyHostToDevice, stream));
+    push_args(make_args(c, step, d_x, d_y));
+    last_cfg = c;
+    last_step = step;
+    launch_step(d_x, d_y, c.microbatch);
+    read_report(norms_out, rep, c.microbatch, step);
+  }
+};
+
+}  // namespace pgb
+
+using namespace pgb;
+
+struct pgb_engine {
+  std::unique_ptr<Engine> impl;
+};
+
+namespace {
+Engine& E(pgb_engine* e) {
+  if (!e || !e->impl) raise(PGB_ERR_CONTRACT, "null engine handle");
+  PGB_CUDA(cudaSetDevice(e->impl->device));
+  return *e->impl;
+}
+}  // namespace
+
+extern "C" {
+
+pgb_status pgb_engine_create(const pgb_model_desc* desc, int32_t strategy, int64_t batch,
+                             int32_t device, pgb_engine** out) {
+  return guarded([&] {
+    if (!desc || !out) raise(PGB_ERR_CONTRACT, "null argument");
+    auto h = std::make_unique<pgb_engine>();
+    h->impl = std::make_unique<Engine>();
+    h->impl->init(*desc, strategy, batch, device);
+    *out = h.release();
+  });
+}
+
+pgb_status pgb_nccl_unique_id(pgb_unique_id* out) {
+  return guarded([&] {
+    static_assert(sizeof(pgb_unique_id) == sizeof(ncclUniqueId), "unique id size");
+    ncclUniqueId id;
+    PGB_NCCL(Nccl::get().getUniqueId(&id));
+    std::memcpy(out, &id, sizeof id);
+  });
+}
+
+pgb_status pgb_engine_create_dist(const pgb_model_desc* desc, int32_t strategy,
+                                  int64_t local_batch, int32_t device, int32_t rank,
+                                  int32_t world, const pgb_unique_id* id, pgb_engine** out) {
+  return guarded([&] {
+    if (!desc || !out || !id) raise(PGB_ERR_CONTRACT, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) raise(PGB_ERR_CONFIG, "bad rank/world");
+    auto h = std::make_unique<pgb_engine>();
+    h->impl = std::make_unique<Engine>();
+    h->impl->world = world;
+    h->impl->rank = rank;
+    h->impl->init(*desc, strategy, local_batch, device);
+    if (world > 1) {
+      ncclUniqueId nid;
+      std::memcpy(&nid, id, sizeof nid);
+      PGB_NCCL(Nccl::get().commInitRank(&h->impl->comm, world, nid, rank));
+    }
+    *out = h.release();
+  });
+}
+
+void pgb_engine_destroy(pgb_engine* e) {
+  if (!e) return;
+  try {
+    delete e;
+  } catch (...) {
+  }
+}
+
+pgb_status pgb_engine_info_get(pgb_engine* e, pgb_engine_info* out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    out->batch = en.B;
+    out->global_batch = en.B * en.world;
+    out->param_count = en.P;
+    out->n_params = en.bt.n;
+    out->world = en.world;
+    out->rank = en.rank;
+    out->device = en.device;
+    out->workspace_bytes = (int64_t)en.arena_bytes;
+    out->kernels_per_step = en.kernels_last;
+    out->graph_enabled = en.graph_enabled;
+  });
+}
+
+pgb_status pgb_engine_set_graph(pgb_engine* e, int32_t enable) {
+  return guarded([&] { E(e).graph_enabled = enable != 0; });
+}
+
+pgb_status pgb_set_params(pgb_engine* e, const float* flat) {
+  return guarded([&] {
+    Engine& en = E(e);
+    PGB_CUDA(cudaMemcpyAsync(en.d_params, flat, sizeof(float) * en.P, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+  });
+}
+
+pgb_status pgb_get_params(pgb_engine* e, float* flat) {
+  return guarded([&] {
+    Engine& en = E(e);
+    PGB_CUDA(cudaMemcpyAsync(flat, en.d_params, sizeof(float) * en.P, cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+  });
+}
+
+pgb_status pgb_dpsgd_step(pgb_engine* e, const float* x, const float* y,
+                          const pgb_dp_config* cfg, int64_t step, float* norms_out,
+                          pgb_step_report* rep) {
+  return guarded([&] {
+    if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
+    E(e).step_host(x, y, *cfg, step, norms_out, rep);
+  });
+}
+
+pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d_y,
+                                 const pgb_dp_config* cfg, int64_t step) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
+    validate_dp_config(*cfg, en.B);
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, d_x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyDeviceToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, d_y, sizeof(float) * en.B, cudaMemcpyDeviceToDevice,
+                             en.stream));
+    en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
+    en.last_cfg = *cfg;
+    en.last_step = step;
+    en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+  });
+}
+
+pgb_status pgb_synchronize(pgb_engine* e, float* norms_out, pgb_step_report* rep) {
+  return guarded([&] {
+    Engine& en = E(e);
+    en.read_report(norms_out, rep, en.last_cfg.microbatch > 0 ? en.last_cfg.microbatch : 1,
+                   en.last_step);
+  });
+}
+
+pgb_status pgb_sgd_step(pgb_engine* e, const float* x, const float* y, float lr) {
+  return guarded([&] {
+    Engine& en = E(e);
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, y, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    en.enqueue_grads(en.stream, en.d_x, en.d_y);
+    long long total = en.P;
+    sgd_kernel<<<grid_for((size_t)total), 256, 0, en.stream>>>(en.d_stacks, en.bt, (int)en.B,
+                                                                lr, en.d_params);
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    en.check_device_error();
+  });
+}
+
+pgb_status pgb_per_example_grads(pgb_engine* e, const float* x, const float* y,
+                                 float* stacks_out, float* norms_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, y, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    en.enqueue_grads(en.stream, en.d_x, en.d_y);
+    if (norms_out) {
+      dim3 sg(en.bt.n, (unsigned)en.B);
+      sumsq_kernel<<<sg, 128, 0, en.stream>>>(en.d_stacks, en.bt, (int)en.B, en.d_parts);
+      finalize_norms_kernel<<<((int)en.B + 127) / 128, 128, 0, en.stream>>>(
+          en.d_parts, en.bt.n, (int)en.B, en.d_norms);
+    }
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    en.check_device_error();
+    if (stacks_out)
+      PGB_CUDA(cudaMemcpy(stacks_out, en.d_stacks, sizeof(float) * en.B * en.P,
+                          cudaMemcpyDeviceToHost));
+    if (norms_out)
+      PGB_CUDA(cudaMemcpy(norms_out, en.d_norms, sizeof(float) * en.B, cudaMemcpyDeviceToHost));
+  });
+}
+
+pgb_status pgb_clipped_sum(pgb_engine* e, const float* x, const float* y, float clip_norm,
+                           float* sum_out, float* norms_out, int64_t* clipped_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!(clip_norm > 0.0f)) raise(PGB_ERR_CONFIG, "DpConfig: clip norm must be positive");
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, y, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_clipped, 0, sizeof(int) * 2, en.stream));
+    pgb_dp_config c{clip_norm, 0.0f, 1.0f, 1, 0};
+    en.push_args(en.make_args(c, 0, en.d_x, en.d_y));
+    en.enqueue_grads(en.stream, en.d_x, en.d_y);
+    en.enqueue_local_sum(en.stream, en.d_stacks, en.bt, (int)en.B);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    en.check_device_error();
+    if (sum_out)
+      PGB_CUDA(cudaMemcpy(sum_out, en.d_sum, sizeof(float) * en.P, cudaMemcpyDeviceToHost));
+    if (norms_out)
+      PGB_CUDA(cudaMemcpy(norms_out, en.d_norms, sizeof(float) * en.B, cudaMemcpyDeviceToHost));
+    if (clipped_out) {
+      int c0 = 0;
+      PGB_CUDA(cudaMemcpy(&c0, en.d_clipped, sizeof(int), cudaMemcpyDeviceToHost));
+      *clipped_out = c0;
+    }
+  });
+}
+
+pgb_status pgb_forward(pgb_engine* e, const float* x, const float* y, float* losses_out,
+                       float* logits_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, y, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    en.enqueue_forward(en.stream, en.d_x, en.d_y);
+    PGB_CUDA(cudaGetLastError());
+    if (losses_out)
+      PGB_CUDA(cudaMemcpyAsync(losses_out, en.d_loss, sizeof(float) * en.B,
+                               cudaMemcpyDeviceToHost, en.stream));
+    if (logits_out)
+      PGB_CUDA(cudaMemcpyAsync(logits_out, en.logits_buffer(),
+                               sizeof(float) * en.B * en.desc.classes, cudaMemcpyDeviceToHost,
+                               en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    en.check_device_error();
+  });
+}
+
+pgb_status pgb_aggregate(pgb_engine* e, const float* stacks, const pgb_dp_config* cfg,
+                         int64_t step, float* norms_out, pgb_step_report* rep) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg || !stacks) raise(PGB_ERR_CONTRACT, "null argument");
+    validate_dp_config(*cfg, en.B);
+    if (cfg->microbatch != 1) raise(PGB_ERR_CONFIG, "pgb_aggregate: microbatch must be 1");
+    PGB_CUDA(cudaMemcpyAsync(en.d_stacks, stacks, sizeof(float) * en.B * en.P,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_clipped, 0, sizeof(int) * 2, en.stream));
+    en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
+    en.last_cfg = *cfg;
+    en.enqueue_aggregate(en.stream, en.d_stacks, en.bt, (int)en.B);
+    PGB_CUDA(cudaGetLastError());
+    en.read_report(norms_out, rep, 1, step);
+  });
+}
+
+pgb_status pgb_gaussian(int32_t device, uint64_t seed, uint64_t stream, int64_t n, float* out) {
+  return guarded([&] {
+    if (n <= 0) return;
+    PGB_CUDA(cudaSetDevice(device));
+    float* d = nullptr;
+    PGB_CUDA(cudaMalloc(&d, sizeof(float) * n));
+    gaussian_kernel<<<grid_for((size_t)(n + 1) / 2), 256>>>(stream_key(seed, stream), n, d);
+    cudaError_t st = cudaMemcpy(out, d, sizeof(float) * n, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    PGB_CUDA(st);
+  });
+}
+
+pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t n,
+                         const pgb_dp_config* cfg, int64_t step0, float* norms_out,
+                         int64_t* clipped_total, double* seconds_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg || !x || !y) raise(PGB_ERR_CONTRACT, "null argument");
+    validate_dp_config(*cfg, en.B);
+    const int64_t steps = n / en.B;
+    if (steps <= 0) raise(PGB_ERR_CONFIG, "run_epoch: fewer examples than one batch");
+    const int64_t U = en.B / cfg->microbatch;
+    const size_t xb = sizeof(float) * en.B * en.in_row, yb = sizeof(float) * en.B;
+    float* h_norm_stage = nullptr;
+    int* d_clip_acc = nullptr;
+    if (norms_out) PGB_CUDA(cudaMallocHost(&h_norm_stage, sizeof(float) * steps * U));
+    cudaEvent_t copied[2], consumed[2], t0, t1;
+    for (int i = 0; i < 2; ++i) {
+      PGB_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+      PGB_CUDA(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
+    }
+    PGB_CUDA(cudaEventCreate(&t0));
+    PGB_CUDA(cudaEventCreate(&t1));
+    std::vector<int> clip_counts;
+    int* h_clip_stage = nullptr;
+    PGB_CUDA(cudaMallocHost(&h_clip_stage, sizeof(int) * 2 * steps));
+    (void)d_clip_acc;
+    const auto wall0 = std::chrono::steady_clock::now();
+    PGB_CUDA(cudaEventRecord(t0, en.stream));
+    // prologue: batch 0 into slot 0
+    PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, t0, 0));
+    PGB_CUDA(cudaMemcpyAsync(en.d_xb[0], x, xb, cudaMemcpyHostToDevice, en.copy_stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_yb[0], y, yb, cudaMemcpyHostToDevice, en.copy_stream));
+    PGB_CUDA(cudaEventRecord(copied[0], en.copy_stream));
+    for (int64_t s = 0; s < steps; ++s) {
+      const int slot = (int)(s & 1);
+      if (s + 1 < steps) {
+        const int nxt = slot ^ 1;
+        if (s >= 1) PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, consumed[nxt], 0));
+        PGB_CUDA(cudaMemcpyAsync(en.d_xb[nxt], x + (s + 1) * en.B * en.in_row, xb,
+                                 cudaMemcpyHostToDevice, en.copy_stream));
+        PGB_CUDA(cudaMemcpyAsync(en.d_yb[nxt], y + (s + 1) * en.B, yb, cudaMemcpyHostToDevice,
+                                 en.copy_stream));
+        PGB_CUDA(cudaEventRecord(copied[nxt], en.copy_stream));
+      }
+      PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[slot], 0));
+      en.push_args(en.make_args(*cfg, step0 + s, en.d_xb[slot], en.d_yb[slot]));
+      en.launch_step(en.d_xb[slot], en.d_yb[slot], cfg->microbatch);
+      PGB_CUDA(cudaEventRecord(consumed[slot], en.stream));
+      // the step's result read back every step (norms, clipped count)
+      PGB_CUDA(cudaMemcpyAsync(h_clip_stage + 2 * s, en.d_clipped, sizeof(int) * 2,
+                               cudaMemcpyDeviceToHost, en.stream));
+      if (h_norm_stage)
+        PGB_CUDA(cudaMemcpyAsync(h_norm_stage + s * U, en.d_norms, sizeof(float) * U,
+                                 cudaMemcpyDeviceToHost, en.stream));
+    }
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaEventRecord(t1, en.stream));
+    PGB_CUDA(cudaEventSynchronize(t1));
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    if (seconds_out) *seconds_out = std::max(wall, ms * 1e-3);
+    int64_t tot = 0;
+    for (int64_t s = 0; s < steps; ++s) tot += en.world > 1 ? h_clip_stage[2 * s + 1] : h_clip_stage[2 * s];
+    if (clipped_total) *clipped_total = tot;
+    if (norms_out) std::memcpy(norms_out, h_norm_stage, sizeof(float) * steps * U);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(copied[i]);
+      cudaEventDestroy(consumed[i]);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (h_norm_stage) cudaFreeHost(h_norm_stage);
+    cudaFreeHost(h_clip_stage);
+    en.last_cfg = *cfg;
+    en.last_step = step0 + steps - 1;
+    en.check_device_error();
+  });
+}
+
+pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
+                             const pgb_dp_config* cfg, int64_t step0, int32_t n_steps,
+                             int32_t max_kernels, float* ms_out, char* names_out,
+                             int32_t* n_kernels_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
+    validate_dp_config(*cfg, en.B);
+    if (n_steps < 1 || n_steps > 32) raise(PGB_ERR_CONFIG, "profile: 1..32 steps");
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, d_x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyDeviceToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, d_y, sizeof(float) * en.B, cudaMemcpyDeviceToDevice,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    // hold the GPU while every instrumented launch is queued, so the events
+    // bracket back-to-back kernels rather than host launch gaps
+    spin_kernel<<<1, 1, 0, en.stream>>>(2000000LL + 400000LL * n_steps);
+    std::vector<std::pair<cudaEvent_t, const char*>> marks;
+    std::vector<size_t> step_begin;
+    en.prof = &marks;
+    try {
+      for (int s = 0; s < n_steps; ++s) {
+        en.push_args(en.make_args(*cfg, step0 + s, en.d_x, en.d_y));
+        step_begin.push_back(marks.size());
+        en.mark(en.stream, "begin");
+        en.enqueue_step(en.stream, en.d_x, en.d_y, cfg->microbatch);
+      }
+    } catch (...) {
+      en.prof = nullptr;
+      throw;
+    }
+    en.prof = nullptr;
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    const size_t per = (step_begin.size() > 1 ? step_begin[1] : marks.size()) - 1;
+    std::vector<double> acc(per, 0.0);
+    for (size_t s = 0; s < step_begin.size(); ++s)
+      for (size_t k = 0; k < per; ++k) {
+        float ms = 0;
+        PGB_CUDA(cudaEventElapsedTime(&ms, marks[step_begin[s] + k].first,
+                                      marks[step_begin[s] + k + 1].first));
+        acc[k] += ms;
+      }
+    const int nk = (int)std::min<size_t>(per, (size_t)max_kernels);
+    for (int k = 0; k < nk; ++k) {
+      if (ms_out) ms_out[k] = (float)(acc[k] / step_begin.size());
+      if (names_out) {
+        std::strncpy(names_out + 32 * k, marks[k + 1].second, 31);
+        names_out[32 * k + 31] = 0;
+      }
+    }
+    if (n_kernels_out) *n_kernels_out = nk;
+    for (auto& m : marks) cudaEventDestroy(m.first);
+  });
+}
+
+pgb_status pgb_device_params(pgb_engine* e, float** d) {
+  return guarded([&] { *d = E(e).d_params; });
+}
+
+pgb_status pgb_device_stream(pgb_engine* e, void** s) {
+  return guarded([&] { *s = (void*)E(e).stream; });
+}
+
+int32_t pgb_kernels_per_step(pgb_engine* e) { return e && e->impl ? e->impl->kernels_last : 0; }
+
+}  // extern "C"

@@ -1,0 +1,695 @@
+// sm_100a kernels of the DPSGD step (fp32 CUDA-core path).
+//
+// Each kernel names the reference computation it replaces. Layout is the
+// reference's: NCHW activations, (in,out) dense weights, (D,C,k,k) conv
+// weights, block-major per-example stacks (block p is (B, |p|)).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pgb_internal.h"
+
+namespace pgb {
+
+constexpr int kMaxBlocks = PGB_MAX_PARAMS;
+
+// First device-side error wins; the step's update kernel refuses to write
+// parameters once it is set (the reference throws before apply_update).
+struct DevError {
+  int code;       // pgb_status, 0 = none
+  int what;       // 0 label, 1 embedding id
+  long long pos;  // flat position of the offending value
+  float value;
+  int limit;
+};
+
+__device__ __forceinline__ void raise_index(DevError* e, int what, long long pos, float v,
+                                            int limit) {
+  if (atomicCAS(&e->code, 0, PGB_ERR_INDEX) == 0) {
+    e->what = what;
+    e->pos = pos;
+    e->value = v;
+    e->limit = limit;
+  }
+}
+
+// checked_id (kernels.hpp:475-489): integral and within [0, V).
+__device__ __forceinline__ bool valid_id(float raw, int V) {
+  return raw == rintf(raw) && raw >= 0.0f && raw < float(V);
+}
+
+// ---------------------------------------------------------------------------
+// Generic register-tiled SGEMM: C[z][m][n] = sum_k A(z,m,k) B(z,k,n).
+// Operand gathers and the epilogue are supplied by Op, which is how the
+// implicit-im2col convolutions, the transposed convolution (backward data)
+// and the per-example weight-gradient GEMMs share one tile engine.
+// ---------------------------------------------------------------------------
+template <class Op, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    tile_gemm_kernel(Op op) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  __shared__ __align__(16) float As[BK][BM];
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int z = blockIdx.z;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int M = op.M, N = op.N, K = op.K;
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    for (int e = tid; e < BM * BK; e += NT) {
+      const int mm = e / BK, kk = e % BK;
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? op.a(z, m, k) : 0.0f;
+    }
+    for (int e = tid; e < BK * BN; e += NT) {
+      const int kk = e / BN, nn = e % BN;
+      const int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < N && k < K) ? op.b(z, k, n) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + ty * TM + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = n0 + tx * TN + j;
+      if (n < N) op.store(z, m, n, acc[i][j]);
+    }
+  }
+}
+
+// ---- operand adapters -----------------------------------------------------
+
+// dense forward (models.cpp:182-196): z = x W + b, optional fused relu.
+struct DenseFwdOp {
+  int M, N, K;  // M = B, N = out, K = in
+  const float* x;
+  const float* W;
+  const float* bias;
+  float* out;
+  int relu;
+  __device__ float a(int, int m, int k) const { return x[(size_t)m * K + k]; }
+  __device__ float b(int, int k, int n) const { return W[(size_t)k * N + n]; }
+  __device__ void store(int, int m, int n, float v) const {
+    v += bias[n];
+    out[(size_t)m * N + n] = relu ? fmaxf(v, 0.0f) : v;
+  }
+};
+
+// dense input gradient (autodiff.cpp:155-159): dX = G W^T; the relu VJP of an
+// upstream relu (gt-mask on its output, autodiff.cpp:121-124) is fused.
+struct DenseBwdXOp {
+  int M, N, K;  // M = B, N = in, K = out
+  const float* g;
+  const float* W;
+  const float* mask;  // relu output, or null
+  float* gx;
+  __device__ float a(int, int m, int k) const { return g[(size_t)m * K + k]; }
+  __device__ float b(int, int k, int n) const { return W[(size_t)n * K + k]; }
+  __device__ void store(int, int m, int n, float v) const {
+    const size_t i = (size_t)m * N + n;
+    gx[i] = (mask && !(mask[i] > 0.0f)) ? 0.0f : v;
+  }
+};
+
+struct ConvGeom {
+  int C, H, W, D, Ho, Wo, k, stride, pad;
+};
+
+// conv forward as implicit-im2col GEMM (models.cpp:197-220; im2col rows
+// ordered (c,u,v), kernels.hpp:412-440): M = D, N = B*Ho*Wo, K = C*k*k.
+struct ConvFwdOp {
+  int M, N, K;
+  ConvGeom g;
+  const float* x;
+  const float* W;
+  const float* bias;
+  float* out;
+  int relu;
+  __device__ float a(int, int m, int k) const { return W[(size_t)m * K + k]; }
+  __device__ float b(int, int k, int n) const {
+    const int P = g.Ho * g.Wo;
+    const int bb = n / P, p = n - bb * P;
+    const int oy = p / g.Wo, ox = p - oy * g.Wo;
+    const int kk2 = g.k * g.k;
+    const int c = k / kk2, r = k - c * kk2;
+    const int u = r / g.k, v = r - u * g.k;
+    const int iy = oy * g.stride + u - g.pad, ix = ox * g.stride + v - g.pad;
+    if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) return 0.0f;
+    return x[(((size_t)bb * g.C + c) * g.H + iy) * g.W + ix];
+  }
+  __device__ void store(int, int m, int n, float v) const {
+    const int P = g.Ho * g.Wo;
+    const int bb = n / P, p = n - bb * P;
+    v += bias[m];
+    out[((size_t)bb * g.D + m) * P + p] = relu ? fmaxf(v, 0.0f) : v;
+  }
+};
+
+// conv input gradient (im2col VJP = col2im of W^T G, autodiff.cpp:186-192),
+// written as a gather so no output element is accumulated by two threads:
+// M = C, N = B*H*W, K = D*k*k.
+struct ConvBwdXOp {
+  int M, N, K;
+  ConvGeom g;
+  const float* gout;  // (B, D, Ho, Wo)
+  const float* W;
+  const float* mask;  // relu output of the input activation, or null
+  float* gx;
+  __device__ float a(int, int m, int k) const {
+    const int kk2 = g.k * g.k;
+    const int d = k / kk2, r = k - d * kk2;
+    return W[((size_t)d * g.C + m) * kk2 + r];
+  }
+  __device__ float b(int, int k, int n) const {
+    const int HW = g.H * g.W;
+    const int bb = n / HW, q = n - bb * HW;
+    const int iy = q / g.W, ix = q - iy * g.W;
+    const int kk2 = g.k * g.k;
+    const int d = k / kk2, r = k - d * kk2;
+    const int u = r / g.k, v = r - u * g.k;
+    const int ny = iy + g.pad - u, nx = ix + g.pad - v;
+    if (ny < 0 || nx < 0) return 0.0f;
+    const int oy = ny / g.stride, ox = nx / g.stride;
+    if (oy * g.stride != ny || ox * g.stride != nx || oy >= g.Ho || ox >= g.Wo) return 0.0f;
+    return gout[(((size_t)bb * g.D + d) * g.Ho + oy) * g.Wo + ox];
+  }
+  __device__ void store(int, int m, int n, float v) const {
+    const int HW = g.H * g.W;
+    const int bb = n / HW, q = n - bb * HW;
+    const size_t i = ((size_t)bb * g.C + m) * HW + q;
+    gx[i] = (mask && !(mask[i] > 0.0f)) ? 0.0f : v;
+  }
+};
+
+// per-example conv weight gradient (strategies.cpp:156-170):
+// dW_z = dz_z (D x P) . patches_z^T (P x CKK), one GEMM per example z.
+struct ConvDWOp {
+  int M, N, K;  // M = D, N = C*k*k, K = Ho*Wo
+  ConvGeom g;
+  const float* gout;  // (B, D, Ho, Wo)
+  const float* x;     // (B, C, H, W)
+  float* stack;       // (B, D*C*k*k)
+  __device__ float a(int z, int m, int k) const {
+    return gout[((size_t)z * g.D + m) * K + k];
+  }
+  __device__ float b(int z, int k, int n) const {
+    const int oy = k / g.Wo, ox = k - oy * g.Wo;
+    const int kk2 = g.k * g.k;
+    const int c = n / kk2, r = n - c * kk2;
+    const int u = r / g.k, v = r - u * g.k;
+    const int iy = oy * g.stride + u - g.pad, ix = ox * g.stride + v - g.pad;
+    if (iy < 0 || iy >= g.H || ix < 0 || ix >= g.W) return 0.0f;
+    return x[(((size_t)z * g.C + c) * g.H + iy) * g.W + ix];
+  }
+  __device__ void store(int z, int m, int n, float v) const {
+    stack[(size_t)z * M * N + (size_t)m * N + n] = v;
+  }
+};
+
+// ---- per-example dense gradients (strategies.cpp:149-154) -----------------
+// dW_i = a_i (x) d_i into stack (B, in*out); db_i = d_i into (B, out).
+__global__ void dense_pex_kernel(const float* __restrict__ act, const float* __restrict__ g,
+                                 int B, int in, int out, float* __restrict__ sW,
+                                 float* __restrict__ sb) {
+  const size_t per = (size_t)in * out;
+  const size_t total = (size_t)B * per;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = e / per, r = e - b * per;
+    const int i = (int)(r / out), o = (int)(r - (size_t)i * out);
+    sW[e] = act[b * in + i] * g[b * out + o];
+  }
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)B * out;
+       e += (size_t)gridDim.x * blockDim.x)
+    sb[e] = g[e];
+}
+
+// per-example conv bias gradient: db_i[d] = sum_P dz_i[d, :] (strategies.cpp:168)
+__global__ void conv_db_pex_kernel(const float* __restrict__ g, int BD, int P,
+                                   float* __restrict__ sb) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= BD) return;
+  const float* row = g + (size_t)warp * P;
+  float s = 0.0f;
+  for (int p = lane; p < P; p += 32) s += row[p];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) sb[warp] = s;
+}
+
+// ---- parameter-free layers ----------------------------------------------------
+
+// max/avg pooling via window reduction (tape.cpp:269-282): avg = sum * 1/k^2.
+__global__ void pool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int BC,
+                                int H, int W, int Ho, int Wo, int k, int s, int is_max) {
+  const size_t total = (size_t)BC * Ho * Wo;
+  const float inv = 1.0f / float(k * k);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int ox = (int)(e % Wo);
+    const int oy = (int)((e / Wo) % Ho);
+    const size_t bc = e / ((size_t)Wo * Ho);
+    const float* xp = x + bc * H * W;
+    float m = 0.0f, sum = 0.0f;
+    bool first = true;
+    for (int u = 0; u < k; ++u)
+      for (int v = 0; v < k; ++v) {
+        const float val = xp[(oy * s + u) * W + ox * s + v];
+        sum += val;
+        if (first || val > m) m = val;
+        first = false;
+      }
+    y[e] = is_max ? m : sum * inv;
+  }
+}
+
+// pool backward as a gather over the windows containing each input element;
+// max routes to the FIRST maximum in window order (kernels.hpp:377-396).
+__global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                const float* __restrict__ mask, float* __restrict__ gx,
+                                int BC, int H, int W, int Ho, int Wo, int k, int s,
+                                int is_max) {
+  const size_t total = (size_t)BC * H * W;
+  const float inv = 1.0f / float(k * k);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int ix = (int)(e % W);
+    const int iy = (int)((e / W) % H);
+    const size_t bc = e / ((size_t)W * H);
+    const float* xp = x + bc * H * W;
+    const float* gp = g + bc * Ho * Wo;
+    float acc = 0.0f;
+    const int oy_lo = iy >= k ? (iy - k) / s + 1 : 0, oy_hi = min(iy / s, Ho - 1);
+    const int ox_lo = ix >= k ? (ix - k) / s + 1 : 0, ox_hi = min(ix / s, Wo - 1);
+    for (int oy = oy_lo; oy <= oy_hi; ++oy)
+      for (int ox = ox_lo; ox <= ox_hi; ++ox) {
+        if (oy * s > iy || iy >= oy * s + k || ox * s > ix || ix >= ox * s + k) continue;
+        if (is_max) {
+          int best_u = 0, best_v = 0;
+          float bv = xp[(oy * s) * W + ox * s];
+          for (int u = 0; u < k; ++u)
+            for (int v = 0; v < k; ++v) {
+              const float val = xp[(oy * s + u) * W + ox * s + v];
+              if (val > bv) {
+                bv = val;
+                best_u = u;
+                best_v = v;
+              }
+            }
+          if (oy * s + best_u == iy && ox * s + best_v == ix) acc += gp[oy * Wo + ox];
+        } else {
+          acc += gp[oy * Wo + ox] * inv;
+        }
+      }
+    gx[e] = (mask && !(mask[e] > 0.0f)) ? 0.0f : acc;
+  }
+}
+
+// global average pool (models.cpp:227-232): sum over H,W then * 1/(H*W)
+__global__ void gap_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int BC,
+                               int HW) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= BC) return;
+  float s = 0.0f;
+  for (int j = lane; j < HW; j += 32) s += x[(size_t)warp * HW + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[warp] = s * (1.0f / float(HW));
+}
+
+__global__ void gap_bwd_kernel(const float* __restrict__ g, const float* __restrict__ mask,
+                               float* __restrict__ gx, int BC, int HW) {
+  const size_t total = (size_t)BC * HW;
+  const float inv = 1.0f / float(HW);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const float v = g[e / HW] * inv;
+    gx[e] = (mask && !(mask[e] > 0.0f)) ? 0.0f : v;
+  }
+}
+
+__global__ void relu_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, size_t n) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x)
+    y[e] = fmaxf(x[e], 0.0f);
+}
+
+__global__ void mask_kernel(const float* __restrict__ g, const float* __restrict__ mask,
+                            float* __restrict__ gx, size_t n) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x)
+    gx[e] = mask[e] > 0.0f ? g[e] : 0.0f;
+}
+
+// embedding gather fused with the sequence mean-pool (models.cpp:241-262):
+// y[b,e] = (sum_t table[id_bt, e]) * 1/L. Ids validated (checked_id).
+__global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
+                                      const float* __restrict__ table, float* __restrict__ y,
+                                      int B, int L, int E, int V, DevError* err) {
+  const int b = blockIdx.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float s = 0.0f;
+    for (int t = 0; t < L; ++t) {
+      const float raw = ids[(size_t)b * L + t];
+      if (!valid_id(raw, V)) {
+        if (e == 0) raise_index(err, 1, (long long)b * L + t, raw, V);
+        continue;
+      }
+      s += table[(size_t)(int)raw * E + e];
+    }
+    y[(size_t)b * E + e] = s * (1.0f / float(L));
+  }
+}
+
+// per-example dense table gradient (strategies.cpp:171-188): the pooled
+// cotangent times 1/L scattered to each token's row, tokens in order.
+__global__ void embed_pex_kernel(const float* __restrict__ ids, const float* __restrict__ g,
+                                 int B, int L, int E, int V, float* __restrict__ stack) {
+  const int b = blockIdx.x;
+  float* tb = stack + (size_t)b * V * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const float v = g[(size_t)b * E + e] * (1.0f / float(L));
+    for (int t = 0; t < L; ++t) {
+      const float raw = ids[(size_t)b * L + t];
+      if (!valid_id(raw, V)) continue;
+      tb[(size_t)(int)raw * E + e] += v;
+    }
+  }
+}
+
+// softmax cross-entropy + its gradient per example (kernels.hpp:516-566);
+// the loss is a SUM over examples so the cotangent of each loss_i is 1.
+__global__ void xent_kernel(const float* __restrict__ logits, const float* __restrict__ labels,
+                            int B, int K, float* __restrict__ loss, float* __restrict__ dlogits,
+                            DevError* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const float raw = labels[i];
+  const int Kc = K == 1 ? 2 : K;
+  const float* z = logits + (size_t)i * K;
+  float* d = dlogits + (size_t)i * K;
+  if (!valid_id(raw, Kc)) {
+    raise_index(err, 0, i, raw, Kc);
+    for (int k = 0; k < K; ++k) d[k] = 0.0f;
+    loss[i] = 0.0f;
+    return;
+  }
+  const int y = (int)raw;
+  if (K == 1) {
+    const float zz = z[0], az = fabsf(zz);
+    loss[i] = (zz > 0.0f ? zz : 0.0f) - zz * float(y) + log1pf(expf(-az));
+    d[0] = 1.0f / (1.0f + expf(-zz)) - float(y);
+    return;
+  }
+  float m = z[0];
+  for (int k = 1; k < K; ++k) m = fmaxf(m, z[k]);
+  float s = 0.0f;
+  for (int k = 0; k < K; ++k) s += expf(z[k] - m);
+  loss[i] = m + logf(s) - z[y];
+  const float inv = 1.0f / s;
+  for (int k = 0; k < K; ++k) d[k] = expf(z[k] - m) * inv - (k == y ? 1.0f : 0.0f);
+}
+
+// ---- norms, clip, clipped sum, noise, update ---------------------------------
+
+// Squared per-example norm of one parameter block row, fp64 accumulation
+// (sumsq_lanes, kernels.hpp:573-589), fixed reduction order => deterministic.
+// grid (n_blocks, ceil(B / rows_per_cta)).
+struct BlockTable {
+  int n;                      // parameter blocks
+  long long size[kMaxBlocks]; // |p|
+  long long stack_off[kMaxBlocks];  // offset of block p's (B,|p|) slab
+  long long param_off[kMaxBlocks];
+  long long pair_off[kMaxBlocks + 1];  // prefix sum of ceil(|p|/2)
+};
+
+__global__ void sumsq_kernel(const float* __restrict__ stacks, BlockTable bt, int B,
+                             double* __restrict__ parts) {
+  const int p = blockIdx.x;
+  const int i = blockIdx.y;
+  const long long per = bt.size[p];
+  const float* row = stacks + bt.stack_off[p] + (long long)i * per;
+  double acc = 0.0;
+  for (long long j = threadIdx.x; j < per; j += blockDim.x) {
+    const double v = row[j];
+    acc += v * v;
+  }
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) parts[(size_t)i * bt.n + p] = v;
+  }
+}
+
+// Device step parameters, refreshed before every launch/graph replay.
+struct StepArgs {
+  float clip, sigma, lr;
+  float inv_units;   // (float)1 / units, dpsgd.cpp:357
+  unsigned long long seed;
+  long long step;
+  int units;         // clipped units in this step (B/m)
+  int add_noise;     // sigma > 0
+};
+
+__global__ void finalize_norms_kernel(const double* __restrict__ parts, int nb, int units,
+                                      float* __restrict__ norms) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= units) return;
+  double acc = 0.0;
+  for (int p = 0; p < nb; ++p) acc += parts[(size_t)i * nb + p];
+  norms[i] = (float)sqrt(acc);
+}
+
+// Box-Muller normal pair (kernels.hpp:597-614): double precision, then cast.
+__device__ __forceinline__ void gauss_pair(uint64_t key, long long pair, float* c, float* s) {
+  const double two_pi = 6.283185307179586476925286766559;
+  const double u1 = double((value_at(key, 2ull * pair) >> 11) + 1) * 0x1.0p-53;
+  const double u2 = double((value_at(key, 2ull * pair + 1) >> 11) + 1) * 0x1.0p-53;
+  const double r = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincos(two_pi * u2, &sn, &cs);
+  *c = (float)(r * cs);
+  *s = (float)(r * sn);
+}
+
+// Norm finalisation shared by every CTA of the aggregation kernels:
+// norm_i = (float)sqrt(sum_p parts[i][p]); s_i = norm > C ? C/norm : 1.
+__device__ __forceinline__ void load_scales(const double* __restrict__ parts, int nb,
+                                            int units, float clip, float* s_sh,
+                                            float* norms_out, int* clipped_out) {
+  int local_clipped = 0;
+  for (int i = threadIdx.x; i < units; i += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < nb; ++p) acc += parts[(size_t)i * nb + p];
+    const float n = (float)sqrt(acc);
+    s_sh[i] = n > clip ? __fdiv_rn(clip, n) : 1.0f;
+    if (norms_out) norms_out[i] = n;
+    local_clipped += n > clip;
+  }
+  if (clipped_out) {
+    local_clipped = __reduce_add_sync(0xffffffffu, local_clipped);
+    if ((threadIdx.x & 31) == 0 && local_clipped) atomicAdd(clipped_out, local_clipped);
+  }
+  __syncthreads();
+}
+
+// Locate (block, pair) of a global pair index.
+__device__ __forceinline__ int find_block(const BlockTable& bt, long long q) {
+  int p = 0;
+  while (p + 1 < bt.n && bt.pair_off[p + 1] <= q) ++p;
+  return p;
+}
+
+// Clipped sum over units in ascending order, one fp32 chain per column
+// (dpsgd.cpp:287-307), then noise / mean / SGD update (dpsgd.cpp:308-317,
+// apply_update :173-183), all in the reference's fp32 operation order.
+// mode 0: fused single-GPU step; mode 1: write the local clipped sum only.
+template <int UNROLL>
+__global__ void __launch_bounds__(256)
+    aggregate_kernel(const float* __restrict__ stacks, const double* __restrict__ parts,
+                     BlockTable bt, const StepArgs* __restrict__ args,
+                     float* __restrict__ params, float* __restrict__ sum_out,
+                     float* __restrict__ norms_out, int* __restrict__ clipped_out,
+                     const DevError* __restrict__ err, int mode) {
+  extern __shared__ float s_sh[];
+  const StepArgs a = *args;
+  const int U = a.units;
+  load_scales(parts, bt.n, U, a.clip, s_sh, blockIdx.x == 0 ? norms_out : nullptr,
+              blockIdx.x == 0 ? clipped_out : nullptr);
+  const bool failed = err && err->code != 0;
+  const long long total_pairs = bt.pair_off[bt.n];
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int p = find_block(bt, q);
+    const long long lq = q - bt.pair_off[p];
+    const long long per = bt.size[p];
+    const long long j0 = 2 * lq;
+    const bool has1 = j0 + 1 < per;
+    const float* col = stacks + bt.stack_off[p] + j0;
+    float acc0 = 0.0f, acc1 = 0.0f;
+    int i = 0;
+    for (; i + UNROLL <= U; i += UNROLL) {
+      float v0[UNROLL], v1[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        v0[u] = __ldg(col + (long long)(i + u) * per);
+        v1[u] = has1 ? __ldg(col + (long long)(i + u) * per + 1) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        acc0 = __fadd_rn(acc0, __fmul_rn(v0[u], s_sh[i + u]));
+        acc1 = __fadd_rn(acc1, __fmul_rn(v1[u], s_sh[i + u]));
+      }
+    }
+    for (; i < U; ++i) {
+      acc0 = __fadd_rn(acc0, __fmul_rn(col[(long long)i * per], s_sh[i]));
+      if (has1) acc1 = __fadd_rn(acc1, __fmul_rn(col[(long long)i * per + 1], s_sh[i]));
+    }
+    const long long o = bt.param_off[p] + j0;
+    if (mode == 1) {
+      sum_out[o] = acc0;
+      if (has1) sum_out[o + 1] = acc1;
+      continue;
+    }
+    if (a.add_noise) {
+      float n0, n1;
+      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), lq, &n0, &n1);
+      const float scale = __fmul_rn(a.sigma, a.clip);
+      acc0 = __fadd_rn(acc0, __fmul_rn(scale, n0));
+      acc1 = __fadd_rn(acc1, __fmul_rn(scale, n1));
+    }
+    acc0 = __fmul_rn(acc0, a.inv_units);
+    acc1 = __fmul_rn(acc1, a.inv_units);
+    if (failed) continue;
+    params[o] = __fsub_rn(params[o], __fmul_rn(a.lr, acc0));
+    if (has1) params[o + 1] = __fsub_rn(params[o + 1], __fmul_rn(a.lr, acc1));
+  }
+}
+
+// After the all-reduce of the clipped sums: noise (one shared draw from the
+// common seed), mean over the global units, update.
+__global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt,
+                                    const StepArgs* __restrict__ args,
+                                    float* __restrict__ params,
+                                    const DevError* __restrict__ err) {
+  const StepArgs a = *args;
+  if (err && err->code != 0) return;
+  const long long total_pairs = bt.pair_off[bt.n];
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int p = find_block(bt, q);
+    const long long lq = q - bt.pair_off[p];
+    const long long per = bt.size[p];
+    const long long j0 = 2 * lq;
+    const bool has1 = j0 + 1 < per;
+    const long long o = bt.param_off[p] + j0;
+    float acc0 = sum[o], acc1 = has1 ? sum[o + 1] : 0.0f;
+    if (a.add_noise) {
+      float n0, n1;
+      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), lq, &n0, &n1);
+      const float scale = __fmul_rn(a.sigma, a.clip);
+      acc0 = __fadd_rn(acc0, __fmul_rn(scale, n0));
+      acc1 = __fadd_rn(acc1, __fmul_rn(scale, n1));
+    }
+    acc0 = __fmul_rn(acc0, a.inv_units);
+    acc1 = __fmul_rn(acc1, a.inv_units);
+    params[o] = __fsub_rn(params[o], __fmul_rn(a.lr, acc0));
+    if (has1) params[o + 1] = __fsub_rn(params[o + 1], __fmul_rn(a.lr, acc1));
+  }
+}
+
+// microbatch means (dpsgd.cpp:102-132): unit u = mean of m consecutive rows,
+// summed in order from zero then scaled by (float)1/m.
+__global__ void microbatch_kernel(const float* __restrict__ stacks, BlockTable bt, int B,
+                                  int m, float* __restrict__ units_out) {
+  const int U = B / m;
+  const float inv = 1.0f / float(m);
+  long long total = 0;
+  for (int p = 0; p < bt.n; ++p) total += bt.size[p];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total * U;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int u = (int)(e / total);
+    long long j = e - (long long)u * total;
+    int p = 0;
+    while (j >= bt.size[p]) j -= bt.size[p++];
+    const long long per = bt.size[p];
+    const float* src = stacks + bt.stack_off[p];
+    float acc = 0.0f;
+    for (int r = 0; r < m; ++r) acc = __fadd_rn(acc, src[((long long)u * m + r) * per + j]);
+    units_out[bt.stack_off[p] / B * U + (long long)u * per + j] = __fmul_rn(acc, inv);
+  }
+}
+
+// plain SGD from the stacks (dpsgd.cpp:334-346): p -= lr * (sum_i g_i) * 1/B
+__global__ void sgd_kernel(const float* __restrict__ stacks, BlockTable bt, int B, float lr,
+                           float* __restrict__ params) {
+  long long total = 0;
+  for (int p = 0; p < bt.n; ++p) total += bt.size[p];
+  const float inv = 1.0f / float(B);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long j = e;
+    int p = 0;
+    while (j >= bt.size[p]) j -= bt.size[p++];
+    const long long per = bt.size[p];
+    const float* col = stacks + bt.stack_off[p] + j;
+    float acc = 0.0f;
+    for (int i = 0; i < B; ++i) acc = __fadd_rn(acc, col[(long long)i * per]);
+    const long long o = bt.param_off[p] + j;
+    params[o] = __fsub_rn(params[o], __fmul_rn(lr, __fmul_rn(acc, inv)));
+  }
+}
+
+// Holds the stream for `ns` nanoseconds (profiling: lets the host queue a
+// whole instrumented step before the GPU starts it).
+__global__ void spin_kernel(long long ns) {
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(10000);
+  }
+}
+
+__global__ void gaussian_kernel(uint64_t key, long long n, float* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; 2 * q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    float c, s;
+    gauss_pair(key, q, &c, &s);
+    out[2 * q] = c;
+    if (2 * q + 1 < n) out[2 * q + 1] = s;
+  }
+}
+
+}  // namespace pgb

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "mnist_fused.cuh"
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -93,6 +94,7 @@ struct Layer {
   int pblock = -1;       // first parameter block
   float* act_in = nullptr;
   float* act_out = nullptr;
+  float* gout = nullptr;  // cotangent of this layer's output (backward)
   bool alias = false;    // flatten / fused relu / fused seq_avgpool: no kernel
   bool fused_relu = false;      // producer applies relu
   bool fused_pool = false;      // embedding fused with the following seq_avgpool
@@ -109,7 +111,12 @@ struct Engine {
   ncclComm_t comm = nullptr;
 
   std::vector<Layer> layers;
-  BlockTable bt{};
+  BlockTable bt{};       // live per-example gradient sources (ghost dense blocks)
+  BlockTable bt_stack{}; // the same blocks materialised in d_stacks (block-major)
+  int nparts = 1;        // fp64 norm partials per example
+  bool norms_fused = false;  // per-example norms produced by the gradient kernel
+  bool fused_mnist = false;  // whole per-example pass in one kernel
+  std::vector<int64_t> param_off;
   int64_t P = 0;
   int64_t in_row = 0;
   int first_param_layer = 0;
@@ -129,11 +136,13 @@ struct Engine {
   float* d_cot[2] = {nullptr, nullptr};
   float* d_loss = nullptr;
   float* d_norms = nullptr;
-  float* d_sum = nullptr;  // P floats + clipped count slot (dist)
+  float* d_sum = nullptr;
   int* d_clipped = nullptr;
   DevError* d_err = nullptr;
   StepArgs* d_args = nullptr;
-  std::vector<float*> d_acts;
+  // fused MNIST factors
+  float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
+  std::vector<float*> d_dense_g;  // per dense layer: output cotangent (B, out)
 
   // pinned host staging
   static constexpr int kArgSlots = 64;
@@ -148,14 +157,13 @@ struct Engine {
   bool graph_enabled = true;
   std::map<int, cudaGraphExec_t> graphs;  // key: schedule variant
   int kernels_last = 0;
-  int last_units = 0;
   pgb_dp_config last_cfg{};
   int64_t last_step = 0;
 
   ~Engine() {
     if (device >= 0) cudaSetDevice(device);
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (stream) cudaStreamSynchronize(stream);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (int i = 0; i < kArgSlots; ++i)
       if (slot_ev[i]) cudaEventDestroy(slot_ev[i]);
     if (comm) Nccl::get().commDestroy(comm);
@@ -166,6 +174,28 @@ struct Engine {
     if (h_err) cudaFreeHost(h_err);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
+
+  // The reference MNIST CNN (models.cpp:107-121) runs as one fused kernel.
+  static bool is_mnist(const pgb_model_desc& d) {
+    const int64_t want[9][6] = {{PGB_CONV, 1, 16, 8, 2, 3},   {PGB_RELU, 0, 0, 0, 1, 0},
+                                {PGB_MAXPOOL, 0, 0, 2, 2, 0}, {PGB_CONV, 16, 32, 4, 1, 0},
+                                {PGB_RELU, 0, 0, 0, 1, 0},    {PGB_FLATTEN, 0, 0, 0, 1, 0},
+                                {PGB_DENSE, 512, 32, 0, 1, 0}, {PGB_RELU, 0, 0, 0, 1, 0},
+                                {PGB_DENSE, 32, 10, 0, 1, 0}};
+    if (d.n_layers != 9 || d.input_rank != 3 || d.input_shape[0] != 1 ||
+        d.input_shape[1] != 28 || d.input_shape[2] != 28 || d.classes != 10)
+      return false;
+    for (int l = 0; l < 9; ++l) {
+      const pgb_layer_spec& L = d.layers[l];
+      const bool has_geom = L.kind == PGB_CONV || L.kind == PGB_MAXPOOL;
+      if (L.kind != want[l][0]) return false;
+      if ((L.kind == PGB_CONV || L.kind == PGB_DENSE) && (L.in != want[l][1] || L.out != want[l][2]))
+        return false;
+      if (has_geom && (L.k != want[l][3] || L.stride != want[l][4] || L.pad != want[l][5]))
+        return false;
+    }
+    return true;
   }
 
   // ---- planning ------------------------------------------------------------
@@ -193,7 +223,6 @@ struct Engine {
               "unsupported layer: embedding must feed seq_avgpool (GPU engine)");
     }
     if (blk != desc.n_params) raise(PGB_ERR_CONTRACT, "parameter registry does not match layers");
-    // fusion decisions
     for (int l = 0; l < n; ++l) {
       Layer& L = layers[l];
       const int k = L.spec.kind;
@@ -207,33 +236,14 @@ struct Engine {
         L.alias = true;
         layers[l - 1].fused_pool = true;
       }
-    }
-    // backward: which layers produce an input gradient, and which relu mask
-    for (int l = n - 1; l >= 0; --l) {
-      Layer& L = layers[l];
+      if (k == PGB_FLATTEN || k == PGB_RELU || k == PGB_SEQ_AVGPOOL) L.skip_bwd = true;
       L.needs_gx = l > first_param_layer;
     }
-    for (int l = 0; l < n; ++l) {
-      Layer& L = layers[l];
-      const int k = L.spec.kind;
-      if (k == PGB_FLATTEN || k == PGB_RELU || k == PGB_SEQ_AVGPOOL) L.skip_bwd = true;
-    }
-    // blocks
-    bt.n = desc.n_params;
-    int64_t off = 0, poff = 0;
-    long long pairs = 0;
-    for (int p = 0; p < bt.n; ++p) {
-      bt.size[p] = desc.param_size[p];
-      bt.param_off[p] = poff;
-      bt.stack_off[p] = off;
-      bt.pair_off[p] = pairs;
-      poff += desc.param_size[p];
-      off += desc.param_size[p] * B;
-      pairs += (desc.param_size[p] + 1) / 2;
-    }
-    bt.pair_off[bt.n] = pairs;
-    P = poff;
+    param_off.assign(desc.n_params + 1, 0);
+    for (int p = 0; p < desc.n_params; ++p) param_off[p + 1] = param_off[p] + desc.param_size[p];
+    P = param_off[desc.n_params];
     in_row = s[0].numel();
+    fused_mnist = is_mnist(desc) && std::getenv("PGB_NO_FUSED") == nullptr;
   }
 
   void allocate() {
@@ -250,7 +260,7 @@ struct Engine {
     }
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
-    want((void**)&d_parts, sizeof(double) * B * bt.n);
+    want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
     int64_t max_act = 0;
     for (int l = 0; l < n; ++l) max_act = std::max(max_act, layers[l].out.numel());
     max_act = std::max(max_act, in_row);
@@ -262,7 +272,16 @@ struct Engine {
     want((void**)&d_clipped, sizeof(int) * 2);
     want((void**)&d_err, sizeof(DevError));
     want((void**)&d_args, sizeof(StepArgs));
-    d_acts.assign(n + 1, nullptr);
+    if (fused_mnist) {
+      want((void**)&d_a2, sizeof(float) * B * 512);
+      want((void**)&d_dz1, sizeof(float) * B * 32);
+      want((void**)&d_h, sizeof(float) * B * 32);
+      want((void**)&d_dz2, sizeof(float) * B * 10);
+    }
+    d_dense_g.assign(n, nullptr);
+    for (int l = 0; l < n; ++l)
+      if (layers[l].spec.kind == PGB_DENSE)
+        want((void**)&d_dense_g[l], sizeof(float) * B * layers[l].spec.out);
     std::vector<float*> owned(n + 1, nullptr);
     for (int l = 0; l < n; ++l) {
       const Layer& L = layers[l];
@@ -300,6 +319,89 @@ struct Engine {
       }
       L.bwd_mask = relu ? L.act_in : nullptr;
     }
+    // output cotangent buffers: dense layers keep theirs (the ghost factors
+    // of their weight blocks); everything else ping-pongs
+    int pp = 0;
+    for (int l = n - 1; l >= 0; --l) {
+      Layer& L = layers[l];
+      if (L.skip_bwd) continue;
+      if (L.spec.kind == PGB_DENSE) {
+        L.gout = d_dense_g[l];
+      } else {
+        L.gout = d_cot[pp];
+        pp ^= 1;
+      }
+    }
+    build_tables();
+  }
+
+  void set_block(BlockTable& t, int p, int kind, const float* base, long long stride,
+                 const float* a = nullptr, long long a_stride = 0, int out = 1) {
+    t.kind[p] = kind;
+    t.base[p] = base;
+    t.stride[p] = stride;
+    t.a[p] = a;
+    t.a_stride[p] = a_stride;
+    t.out[p] = out;
+  }
+
+  void build_tables() {
+    BlockTable t{};
+    t.n = desc.n_params;
+    long long pairs = 0;
+    for (int p = 0; p < t.n; ++p) {
+      t.size[p] = desc.param_size[p];
+      t.param_off[p] = param_off[p];
+      t.pair_off[p] = pairs;
+      pairs += (desc.param_size[p] + 1) / 2;
+    }
+    t.pair_off[t.n] = pairs;
+    bt_stack = t;
+    for (int p = 0; p < t.n; ++p)
+      set_block(bt_stack, p, 0, d_stacks + param_off[p] * B, desc.param_size[p]);
+    bt = bt_stack;
+    if (fused_mnist) {
+      // conv blocks materialised by the fused kernel; dense blocks factored
+      set_block(bt, 4, 1, d_dz1, 32, d_a2, 512, 32);
+      set_block(bt, 5, 0, d_dz1, 32);
+      set_block(bt, 6, 1, d_dz2, 10, d_h, 32, 10);
+      set_block(bt, 7, 0, d_dz2, 10);
+      norms_fused = true;
+      nparts = 1;
+    } else {
+      for (int l = 0; l < desc.n_layers; ++l) {
+        const Layer& L = layers[l];
+        if (L.spec.kind != PGB_DENSE) continue;
+        const int o = (int)L.spec.out;
+        // act_in null means the step input: dense as the first layer keeps
+        // its weight block materialised (the input slot is not stable)
+        if (L.act_in) {
+          set_block(bt, L.pblock, 1, L.gout, o, L.act_in, L.spec.in, o);
+        }
+        set_block(bt, L.pblock + 1, 0, L.gout, o);
+      }
+      norms_fused = false;
+      nparts = t.n;
+    }
+  }
+
+  // The gradient-source table for a step whose input sits at x_slot: a dense
+  // first layer is factored over the input itself.
+  BlockTable table_for(const float* x_slot) const {
+    BlockTable t = bt;
+    if (fused_mnist) return t;
+    for (int l = 0; l < desc.n_layers; ++l) {
+      const Layer& L = layers[l];
+      if (L.spec.kind != PGB_DENSE || L.act_in) continue;
+      const int o = (int)L.spec.out;
+      t.kind[L.pblock] = 1;
+      t.base[L.pblock] = L.gout;
+      t.stride[L.pblock] = o;
+      t.a[L.pblock] = x_slot;
+      t.a_stride[L.pblock] = L.spec.in;
+      t.out[L.pblock] = o;
+    }
+    return t;
   }
 
   void init(const pgb_model_desc& d, int strat, int64_t batch, int dev) {
@@ -320,6 +422,10 @@ struct Engine {
     PGB_CUDA(cudaMallocHost(&h_err, sizeof(DevError)));
     for (int i = 0; i < kArgSlots; ++i)
       PGB_CUDA(cudaEventCreateWithFlags(&slot_ev[i], cudaEventDisableTiming));
+    if (fused_mnist)
+      PGB_CUDA(cudaFuncSetAttribute(mnist::fused_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(mnist::Smem)));
     // reference init is the default parameter state (models::build, seed 0)
     std::vector<float> p0(P);
     if (pgb_init_params(&desc, 0, p0.data()) != PGB_OK) raise(PGB_ERR_CONTRACT, "init failed");
@@ -339,18 +445,15 @@ struct Engine {
   }
 
   // ---- schedule ------------------------------------------------------------
-  // Per-example gradient stacks for the batch whose input pointer sits in
-  // d_args->x (the reference's compute_views). Returns kernels launched.
   int enqueue_forward(cudaStream_t s, const float* x_slot, const float* y_slot) {
     int nk = 0;
     const int n = desc.n_layers;
     const int Bi = (int)B;
-    // forward
     for (int l = 0; l < n; ++l) {
       Layer& L = layers[l];
       const float* in = L.act_in ? L.act_in : x_slot;
       const pgb_layer_spec& sp = L.spec;
-      const float* W = L.pblock >= 0 ? d_params + bt.param_off[L.pblock] : nullptr;
+      const float* W = L.pblock >= 0 ? d_params + param_off[L.pblock] : nullptr;
       switch (sp.kind) {
         case PGB_DENSE: {
           DenseFwdOp op{Bi, (int)sp.out, (int)sp.in, in, W, W + sp.in * sp.out, L.act_out,
@@ -404,39 +507,62 @@ struct Engine {
           break;  // flatten / fused relu / fused seq_avgpool
       }
     }
-    // loss and dlogits
-    const Layer& last = layers[n - 1];
-    const float* logits = last.act_out;
-    float* g = d_cot[0];
-    xent_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(logits, y_slot, Bi, (int)desc.classes, d_loss,
-                                                 g, d_err);
+    // loss and dlogits, into the cotangent buffer of the last real layer
+    const Layer* top = nullptr;
+    for (int l = n - 1; l >= 0 && !top; --l)
+      if (!layers[l].skip_bwd) top = &layers[l];
+    xent_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(logits_buffer(), y_slot, Bi, (int)desc.classes,
+                                                 d_loss, top->gout, d_err);
     nk += mark(s, "xent");
     return nk;
   }
 
   const float* logits_buffer() const { return layers.back().act_out; }
 
+  int enqueue_fused_mnist(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    mnist::Params prm{};
+    prm.x = x_slot;
+    prm.y = y_slot;
+    prm.w = d_params;
+    for (int p = 0; p < 8; ++p) prm.off[p] = param_off[p];
+    prm.st_c1w = d_stacks + param_off[0] * B;
+    prm.st_c1b = d_stacks + param_off[1] * B;
+    prm.st_c2w = d_stacks + param_off[2] * B;
+    prm.st_c2b = d_stacks + param_off[3] * B;
+    prm.a2 = d_a2;
+    prm.dz1 = d_dz1;
+    prm.h = d_h;
+    prm.dz2 = d_dz2;
+    prm.loss = d_loss;
+    prm.normsq = d_parts;
+    prm.err = d_err;
+    prm.B = (int)B;
+    mnist::fused_kernel<<<(unsigned)B, mnist::NT, sizeof(mnist::Smem), s>>>(prm);
+    return mark(s, "mnist_fused");
+  }
+
+  // Per-example gradient sources for the batch (the reference's
+  // compute_views); norms land in d_parts. Returns kernels launched.
   int enqueue_grads(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    if (fused_mnist) return enqueue_fused_mnist(s, x_slot, y_slot);
     int nk = enqueue_forward(s, x_slot, y_slot);
     const int n = desc.n_layers;
     const int Bi = (int)B;
-    // backward
-    int gi = 0;
+    const Layer* below = nullptr;
     for (int l = n - 1; l >= first_param_layer; --l) {
       Layer& L = layers[l];
       if (L.skip_bwd) continue;
+      // the next real layer down receives this layer's input gradient
+      below = nullptr;
+      for (int j = l - 1; j >= 0 && !below; --j)
+        if (!layers[j].skip_bwd) below = &layers[j];
       const pgb_layer_spec& sp = L.spec;
       const float* in = L.act_in ? L.act_in : x_slot;
-      const float* W = L.pblock >= 0 ? d_params + bt.param_off[L.pblock] : nullptr;
-      float* gcur = d_cot[gi];
-      float* gnext = d_cot[gi ^ 1];
+      const float* W = L.pblock >= 0 ? d_params + param_off[L.pblock] : nullptr;
+      float* gcur = L.gout;
+      float* gnext = below ? below->gout : nullptr;
       switch (sp.kind) {
         case PGB_DENSE: {
-          float* sW = d_stacks + bt.stack_off[L.pblock];
-          float* sb = d_stacks + bt.stack_off[L.pblock + 1];
-          dense_pex_kernel<<<grid_for((size_t)B * sp.in * sp.out), 256, 0, s>>>(
-              in, gcur, Bi, (int)sp.in, (int)sp.out, sW, sb);
-          nk += mark(s, "dense_pex");
           if (L.needs_gx) {
             DenseBwdXOp op{Bi, (int)sp.in, (int)sp.out, gcur, W, L.bwd_mask, gnext};
             launch_gemm(op, 1, s);
@@ -449,8 +575,8 @@ struct Engine {
                       (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
                       (int)sp.pad};
           const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
-          float* sW = d_stacks + bt.stack_off[L.pblock];
-          float* sb = d_stacks + bt.stack_off[L.pblock + 1];
+          float* sW = d_stacks + param_off[L.pblock] * B;
+          float* sb = d_stacks + param_off[L.pblock + 1] * B;
           ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
           launch_gemm(dw, Bi, s);
           nk += mark(s, "conv_dw_pex");
@@ -485,7 +611,7 @@ struct Engine {
         }
         case PGB_EMBEDDING: {
           const int E = (int)sp.out, V = (int)sp.in;
-          float* st = d_stacks + bt.stack_off[L.pblock];
+          float* st = d_stacks + param_off[L.pblock] * B;
           PGB_CUDA(cudaMemsetAsync(st, 0, sizeof(float) * B * V * E, s));
           embed_pex_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
               in, gcur, Bi, (int)L.in.d[0], E, V, st);
@@ -496,50 +622,52 @@ struct Engine {
           raise(PGB_ERR_UNSUPPORTED,
                 std::string("unsupported layer in backward: ") + layer_kind_name(sp.kind));
       }
-      if (L.needs_gx && sp.kind != PGB_EMBEDDING) gi ^= 1;
-      // a standalone relu directly below a pooling layer is gated by bwd_mask
     }
+    dim3 sg(bt.n, (unsigned)B);
+    sumsq_kernel<<<sg, 128, 0, s>>>(table_for(x_slot), Bi, d_parts);
+    nk += mark(s, "sumsq");
     return nk;
   }
 
-  // One full DPSGD step (variant: 0 = m==1 fused, 1 = m>1, 2 = dist).
+  // One full DPSGD step: grads -> [microbatch] -> norms/clip/sum/noise/update.
   int enqueue_step(cudaStream_t s, const float* x_slot, const float* y_slot, int64_t m) {
     int nk = 0;
     PGB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(DevError), s));
     PGB_CUDA(cudaMemsetAsync(d_clipped, 0, sizeof(int) * 2, s));
     nk += enqueue_grads(s, x_slot, y_slot);
-    const int U = (int)(B / m);
-    const float* src = d_stacks;
     if (m > 1) {
-      BlockTable ut = bt;
-      for (int p = 0; p < bt.n; ++p) ut.stack_off[p] = bt.param_off[p] * U;
-      microbatch_kernel<<<grid_for((size_t)P * U), 256, 0, s>>>(d_stacks, bt, (int)B, (int)m,
-                                                                 d_units);
+      const int U = (int)(B / m);
+      materialize_kernel<<<grid_for((size_t)P * B), 256, 0, s>>>(table_for(x_slot), (int)B,
+                                                                 d_stacks);
+      nk += mark(s, "materialize");
+      microbatch_kernel<<<grid_for((size_t)P * U), 256, 0, s>>>(d_stacks, bt_stack, (int)B,
+                                                                 (int)m, d_units);
       nk += mark(s, "microbatch");
-      src = d_units;
-      nk += enqueue_aggregate(s, src, ut, U);
+      BlockTable ut = bt_stack;
+      for (int p = 0; p < ut.n; ++p) ut.base[p] = d_units + param_off[p] * U;
+      dim3 sg(ut.n, (unsigned)U);
+      sumsq_kernel<<<sg, 128, 0, s>>>(ut, U, d_parts);
+      nk += mark(s, "sumsq");
+      nk += enqueue_aggregate(s, ut, ut.n, U);
     } else {
-      nk += enqueue_aggregate(s, src, bt, U);
+      nk += enqueue_aggregate(s, table_for(x_slot), nparts, (int)B);
     }
     return nk;
   }
 
-  int enqueue_aggregate(cudaStream_t s, const float* stacks, const BlockTable& t, int U) {
+  int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U) {
     int nk = 0;
-    dim3 sg(t.n, U);
-    sumsq_kernel<<<sg, 128, 0, s>>>(stacks, t, U, d_parts);
-    nk += mark(s, "sumsq");
     const long long pairs = t.pair_off[t.n];
     const int threads = 256;
     const int grid = (int)std::min<long long>((pairs + threads - 1) / threads, 148 * 8);
     const size_t smem = sizeof(float) * U;
     if (world == 1) {
-      aggregate_kernel<8><<<grid, threads, smem, s>>>(stacks, d_parts, t, d_args, d_params,
-                                                      nullptr, d_norms, d_clipped, d_err, 0);
+      aggregate_kernel<8><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, nullptr,
+                                                      d_norms, d_clipped, d_err, 0);
       nk += mark(s, "aggregate");
     } else {
-      aggregate_kernel<8><<<grid, threads, smem, s>>>(stacks, d_parts, t, d_args, d_params,
-                                                      d_sum, d_norms, d_clipped, d_err, 1);
+      aggregate_kernel<8><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, d_sum,
+                                                      d_norms, d_clipped, d_err, 1);
       nk += mark(s, "aggregate_local");
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
@@ -554,14 +682,12 @@ struct Engine {
 
   // Noise-free clipped sum of the batch into d_sum (no update): the
   // north-star parity probe.
-  int enqueue_local_sum(cudaStream_t s, const float* stacks, const BlockTable& t, int U) {
-    dim3 sg(t.n, U);
-    sumsq_kernel<<<sg, 128, 0, s>>>(stacks, t, U, d_parts);
+  int enqueue_local_sum(cudaStream_t s, const BlockTable& t, int np, int U) {
     const long long pairs = t.pair_off[t.n];
     const int grid = (int)std::min<long long>((pairs + 255) / 256, 148 * 8);
-    aggregate_kernel<8><<<grid, 256, sizeof(float) * U, s>>>(
-        stacks, d_parts, t, d_args, d_params, d_sum, d_norms, d_clipped, d_err, 1);
-    return 2;
+    aggregate_kernel<8><<<grid, 256, sizeof(float) * U, s>>>(t, d_parts, np, d_args, d_params,
+                                                             d_sum, d_norms, d_clipped, d_err, 1);
+    return 1;
   }
 
   // ---- step argument slots (pinned ring) ------------------------------------
@@ -815,9 +941,9 @@ pgb_status pgb_sgd_step(pgb_engine* e, const float* x, const float* y, float lr)
                              en.stream));
     PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
     en.enqueue_grads(en.stream, en.d_x, en.d_y);
-    long long total = en.P;
-    sgd_kernel<<<grid_for((size_t)total), 256, 0, en.stream>>>(en.d_stacks, en.bt, (int)en.B,
-                                                                lr, en.d_params);
+    sgd_kernel<<<grid_for((size_t)en.P), 256, 0, en.stream>>>(en.table_for(en.d_x), (int)en.B,
+                                                              lr, en.d_params);
+    PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
                              en.stream));
     PGB_CUDA(cudaStreamSynchronize(en.stream));
@@ -835,12 +961,11 @@ pgb_status pgb_per_example_grads(pgb_engine* e, const float* x, const float* y,
                              en.stream));
     PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
     en.enqueue_grads(en.stream, en.d_x, en.d_y);
-    if (norms_out) {
-      dim3 sg(en.bt.n, (unsigned)en.B);
-      sumsq_kernel<<<sg, 128, 0, en.stream>>>(en.d_stacks, en.bt, (int)en.B, en.d_parts);
-      finalize_norms_kernel<<<((int)en.B + 127) / 128, 128, 0, en.stream>>>(
-          en.d_parts, en.bt.n, (int)en.B, en.d_norms);
-    }
+    finalize_norms_kernel<<<((int)en.B + 127) / 128, 128, 0, en.stream>>>(
+        en.d_parts, en.nparts, (int)en.B, en.d_norms);
+    if (stacks_out)
+      materialize_kernel<<<grid_for((size_t)en.P * en.B), 256, 0, en.stream>>>(
+          en.table_for(en.d_x), (int)en.B, en.d_stacks);
     PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
                              en.stream));
@@ -868,7 +993,7 @@ pgb_status pgb_clipped_sum(pgb_engine* e, const float* x, const float* y, float 
     pgb_dp_config c{clip_norm, 0.0f, 1.0f, 1, 0};
     en.push_args(en.make_args(c, 0, en.d_x, en.d_y));
     en.enqueue_grads(en.stream, en.d_x, en.d_y);
-    en.enqueue_local_sum(en.stream, en.d_stacks, en.bt, (int)en.B);
+    en.enqueue_local_sum(en.stream, en.table_for(en.d_x), en.nparts, (int)en.B);
     PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
                              en.stream));
@@ -924,7 +1049,9 @@ pgb_status pgb_aggregate(pgb_engine* e, const float* stacks, const pgb_dp_config
     PGB_CUDA(cudaMemsetAsync(en.d_clipped, 0, sizeof(int) * 2, en.stream));
     en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
     en.last_cfg = *cfg;
-    en.enqueue_aggregate(en.stream, en.d_stacks, en.bt, (int)en.B);
+    dim3 sg(en.bt_stack.n, (unsigned)en.B);
+    sumsq_kernel<<<sg, 128, 0, en.stream>>>(en.bt_stack, (int)en.B, en.d_parts);
+    en.enqueue_aggregate(en.stream, en.bt_stack, en.bt_stack.n, (int)en.B);
     PGB_CUDA(cudaGetLastError());
     en.read_report(norms_out, rep, 1, step);
   });

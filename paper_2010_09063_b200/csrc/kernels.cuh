@@ -242,9 +242,10 @@ __global__ void dense_pex_kernel(const float* __restrict__ act, const float* __r
     const int i = (int)(r / out), o = (int)(r - (size_t)i * out);
     sW[e] = act[b * in + i] * g[b * out + o];
   }
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)B * out;
-       e += (size_t)gridDim.x * blockDim.x)
-    sb[e] = g[e];
+  if (sb)
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)B * out;
+         e += (size_t)gridDim.x * blockDim.x)
+      sb[e] = g[e];
 }
 
 // per-example conv bias gradient: db_i[d] = sum_P dz_i[d, :] (strategies.cpp:168)
@@ -435,38 +436,72 @@ __global__ void xent_kernel(const float* __restrict__ logits, const float* __res
 
 // ---- norms, clip, clipped sum, noise, update ---------------------------------
 
-// Squared per-example norm of one parameter block row, fp64 accumulation
-// (sumsq_lanes, kernels.hpp:573-589), fixed reduction order => deterministic.
-// grid (n_blocks, ceil(B / rows_per_cta)).
+// Where each parameter block's per-example gradient rows live. kind 0: a
+// materialised row g_i = base[i*stride + j]; kind 1: a dense-layer weight
+// block kept factored (ghost representation, strategies.cpp:140-154):
+// g_i[r*out + c] = fl(a[i*a_stride + r] * base[i*stride + c]) -- exactly the
+// fp32 element of the reference's per-example outer-product stack.
 struct BlockTable {
-  int n;                      // parameter blocks
-  long long size[kMaxBlocks]; // |p|
-  long long stack_off[kMaxBlocks];  // offset of block p's (B,|p|) slab
-  long long param_off[kMaxBlocks];
+  int n;
+  long long size[kMaxBlocks];       // |p|
+  long long param_off[kMaxBlocks];  // offset in the flat parameter vector
   long long pair_off[kMaxBlocks + 1];  // prefix sum of ceil(|p|/2)
+  int kind[kMaxBlocks];
+  const float* base[kMaxBlocks];
+  long long stride[kMaxBlocks];
+  const float* a[kMaxBlocks];
+  long long a_stride[kMaxBlocks];
+  int out[kMaxBlocks];
 };
 
-__global__ void sumsq_kernel(const float* __restrict__ stacks, BlockTable bt, int B,
-                             double* __restrict__ parts) {
-  const int p = blockIdx.x;
-  const int i = blockIdx.y;
-  const long long per = bt.size[p];
-  const float* row = stacks + bt.stack_off[p] + (long long)i * per;
-  double acc = 0.0;
-  for (long long j = threadIdx.x; j < per; j += blockDim.x) {
-    const double v = row[j];
-    acc += v * v;
-  }
-  __shared__ double red[32];
+__device__ __forceinline__ float grad_at(const BlockTable& bt, int p, long long i, long long j) {
+  if (bt.kind[p] == 0) return bt.base[p][i * bt.stride[p] + j];
+  const long long r = j / bt.out[p], c = j - r * bt.out[p];
+  return __fmul_rn(bt.a[p][i * bt.a_stride[p] + r], bt.base[p][i * bt.stride[p] + c]);
+}
+
+__device__ __forceinline__ double block_reduce_sum(double acc, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
+  double v = 0.0;
   if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) parts[(size_t)i * bt.n + p] = v;
+  }
+  __syncthreads();
+  return v;
+}
+
+// Squared per-example norm of one parameter block, fp64 accumulation
+// (sumsq_lanes, kernels.hpp:573-589) in a fixed order (deterministic). Ghost
+// blocks use ||a (x) d||^2 = ||a||^2 ||d||^2. grid (n_blocks, B).
+__global__ void sumsq_kernel(BlockTable bt, int B, double* __restrict__ parts) {
+  __shared__ double red[32];
+  const int p = blockIdx.x;
+  const long long i = blockIdx.y;
+  if (bt.kind[p] == 0) {
+    const long long per = bt.size[p];
+    const float* row = bt.base[p] + i * bt.stride[p];
+    double acc = 0.0;
+    for (long long j = threadIdx.x; j < per; j += blockDim.x) {
+      const double v = row[j];
+      acc += v * v;
+    }
+    acc = block_reduce_sum(acc, red);
+    if (threadIdx.x == 0) parts[i * bt.n + p] = acc;
+  } else {
+    const long long in = bt.size[p] / bt.out[p];
+    const float* ar = bt.a[p] + i * bt.a_stride[p];
+    const float* dr = bt.base[p] + i * bt.stride[p];
+    double sa = 0.0, sd = 0.0;
+    for (long long r = threadIdx.x; r < in; r += blockDim.x) sa += (double)ar[r] * ar[r];
+    for (long long c = threadIdx.x; c < bt.out[p]; c += blockDim.x) sd += (double)dr[c] * dr[c];
+    sa = block_reduce_sum(sa, red);
+    sd = block_reduce_sum(sd, red);
+    if (threadIdx.x == 0) parts[i * bt.n + p] = sa * sd;
   }
 }
 
@@ -503,13 +538,13 @@ __device__ __forceinline__ void gauss_pair(uint64_t key, long long pair, float* 
 
 // Norm finalisation shared by every CTA of the aggregation kernels:
 // norm_i = (float)sqrt(sum_p parts[i][p]); s_i = norm > C ? C/norm : 1.
-__device__ __forceinline__ void load_scales(const double* __restrict__ parts, int nb,
+__device__ __forceinline__ void load_scales(const double* __restrict__ parts, int nparts,
                                             int units, float clip, float* s_sh,
                                             float* norms_out, int* clipped_out) {
   int local_clipped = 0;
   for (int i = threadIdx.x; i < units; i += blockDim.x) {
     double acc = 0.0;
-    for (int p = 0; p < nb; ++p) acc += parts[(size_t)i * nb + p];
+    for (int p = 0; p < nparts; ++p) acc += parts[(size_t)i * nparts + p];
     const float n = (float)sqrt(acc);
     s_sh[i] = n > clip ? __fdiv_rn(clip, n) : 1.0f;
     if (norms_out) norms_out[i] = n;
@@ -522,10 +557,10 @@ __device__ __forceinline__ void load_scales(const double* __restrict__ parts, in
   __syncthreads();
 }
 
-// Locate (block, pair) of a global pair index.
-__device__ __forceinline__ int find_block(const BlockTable& bt, long long q) {
+// Locate the block of a global pair index (table cached in shared memory).
+__device__ __forceinline__ int find_block(const long long* pair_off, int n, long long q) {
   int p = 0;
-  while (p + 1 < bt.n && bt.pair_off[p + 1] <= q) ++p;
+  while (p + 1 < n && pair_off[p + 1] <= q) ++p;
   return p;
 }
 
@@ -535,44 +570,65 @@ __device__ __forceinline__ int find_block(const BlockTable& bt, long long q) {
 // mode 0: fused single-GPU step; mode 1: write the local clipped sum only.
 template <int UNROLL>
 __global__ void __launch_bounds__(256)
-    aggregate_kernel(const float* __restrict__ stacks, const double* __restrict__ parts,
-                     BlockTable bt, const StepArgs* __restrict__ args,
-                     float* __restrict__ params, float* __restrict__ sum_out,
-                     float* __restrict__ norms_out, int* __restrict__ clipped_out,
-                     const DevError* __restrict__ err, int mode) {
+    aggregate_kernel(BlockTable bt, const double* __restrict__ parts, int nparts,
+                     const StepArgs* __restrict__ args, float* __restrict__ params,
+                     float* __restrict__ sum_out, float* __restrict__ norms_out,
+                     int* __restrict__ clipped_out, const DevError* __restrict__ err, int mode) {
   extern __shared__ float s_sh[];
+  __shared__ long long pair_sh[kMaxBlocks + 1];
   const StepArgs a = *args;
   const int U = a.units;
-  load_scales(parts, bt.n, U, a.clip, s_sh, blockIdx.x == 0 ? norms_out : nullptr,
+  for (int p = threadIdx.x; p <= bt.n; p += blockDim.x) pair_sh[p] = bt.pair_off[p];
+  load_scales(parts, nparts, U, a.clip, s_sh, blockIdx.x == 0 ? norms_out : nullptr,
               blockIdx.x == 0 ? clipped_out : nullptr);
   const bool failed = err && err->code != 0;
-  const long long total_pairs = bt.pair_off[bt.n];
+  const long long total_pairs = pair_sh[bt.n];
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
        q += (long long)gridDim.x * blockDim.x) {
-    const int p = find_block(bt, q);
-    const long long lq = q - bt.pair_off[p];
+    const int p = find_block(pair_sh, bt.n, q);
+    const long long lq = q - pair_sh[p];
     const long long per = bt.size[p];
     const long long j0 = 2 * lq;
     const bool has1 = j0 + 1 < per;
-    const float* col = stacks + bt.stack_off[p] + j0;
     float acc0 = 0.0f, acc1 = 0.0f;
-    int i = 0;
-    for (; i + UNROLL <= U; i += UNROLL) {
-      float v0[UNROLL], v1[UNROLL];
+    if (bt.kind[p] == 0) {
+      const float* col = bt.base[p] + j0;
+      const long long st = bt.stride[p];
+      int i = 0;
+      for (; i + UNROLL <= U; i += UNROLL) {
+        float v0[UNROLL], v1[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        v0[u] = __ldg(col + (long long)(i + u) * per);
-        v1[u] = has1 ? __ldg(col + (long long)(i + u) * per + 1) : 0.0f;
-      }
+        for (int u = 0; u < UNROLL; ++u) {
+          v0[u] = __ldg(col + (long long)(i + u) * st);
+          v1[u] = has1 ? __ldg(col + (long long)(i + u) * st + 1) : 0.0f;
+        }
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        acc0 = __fadd_rn(acc0, __fmul_rn(v0[u], s_sh[i + u]));
-        acc1 = __fadd_rn(acc1, __fmul_rn(v1[u], s_sh[i + u]));
+        for (int u = 0; u < UNROLL; ++u) {
+          acc0 = __fadd_rn(acc0, __fmul_rn(v0[u], s_sh[i + u]));
+          acc1 = __fadd_rn(acc1, __fmul_rn(v1[u], s_sh[i + u]));
+        }
       }
-    }
-    for (; i < U; ++i) {
-      acc0 = __fadd_rn(acc0, __fmul_rn(col[(long long)i * per], s_sh[i]));
-      if (has1) acc1 = __fadd_rn(acc1, __fmul_rn(col[(long long)i * per + 1], s_sh[i]));
+      for (; i < U; ++i) {
+        acc0 = __fadd_rn(acc0, __fmul_rn(col[(long long)i * st], s_sh[i]));
+        if (has1) acc1 = __fadd_rn(acc1, __fmul_rn(col[(long long)i * st + 1], s_sh[i]));
+      }
+    } else {
+      // factored dense block: rebuild the fp32 stack elements on the fly
+      const int out = bt.out[p];
+      const long long r0 = j0 / out, c0 = j0 - r0 * out;
+      const long long r1 = (c0 + 1 < out) ? r0 : r0 + 1, c1 = (c0 + 1 < out) ? c0 + 1 : 0;
+      const float* A = bt.a[p];
+      const float* D = bt.base[p];
+      const long long as = bt.a_stride[p], ds = bt.stride[p];
+#pragma unroll 4
+      for (int i = 0; i < U; ++i) {
+        const float a0 = __ldg(A + i * as + r0), d0 = __ldg(D + i * ds + c0);
+        acc0 = __fadd_rn(acc0, __fmul_rn(__fmul_rn(a0, d0), s_sh[i]));
+        if (has1) {
+          const float a1 = __ldg(A + i * as + r1), d1 = __ldg(D + i * ds + c1);
+          acc1 = __fadd_rn(acc1, __fmul_rn(__fmul_rn(a1, d1), s_sh[i]));
+        }
+      }
     }
     const long long o = bt.param_off[p] + j0;
     if (mode == 1) {
@@ -601,13 +657,16 @@ __global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt
                                     const StepArgs* __restrict__ args,
                                     float* __restrict__ params,
                                     const DevError* __restrict__ err) {
+  __shared__ long long pair_sh[kMaxBlocks + 1];
+  for (int p = threadIdx.x; p <= bt.n; p += blockDim.x) pair_sh[p] = bt.pair_off[p];
+  __syncthreads();
   const StepArgs a = *args;
   if (err && err->code != 0) return;
-  const long long total_pairs = bt.pair_off[bt.n];
+  const long long total_pairs = pair_sh[bt.n];
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
        q += (long long)gridDim.x * blockDim.x) {
-    const int p = find_block(bt, q);
-    const long long lq = q - bt.pair_off[p];
+    const int p = find_block(pair_sh, bt.n, q);
+    const long long lq = q - pair_sh[p];
     const long long per = bt.size[p];
     const long long j0 = 2 * lq;
     const bool has1 = j0 + 1 < per;
@@ -627,8 +686,31 @@ __global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt
   }
 }
 
-// microbatch means (dpsgd.cpp:102-132): unit u = mean of m consecutive rows,
-// summed in order from zero then scaled by (float)1/m.
+// Materialise every block's per-example rows into block-major stacks
+// (B, |p|): the compute_views probe and the microbatch path.
+__global__ void materialize_kernel(BlockTable bt, int B, float* __restrict__ stacks) {
+  long long total = 0;
+  for (int p = 0; p < bt.n; ++p) total += bt.size[p];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total * B;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long j = e;
+    int p = 0;
+    long long off = 0;
+    while (j >= bt.size[p] * B) {
+      j -= bt.size[p] * B;
+      off += bt.size[p] * B;
+      ++p;
+    }
+    const long long per = bt.size[p];
+    const long long i = j / per, c = j - i * per;
+    float* dst = stacks + off + j;
+    const float v = grad_at(bt, p, i, c);
+    if (bt.kind[p] != 0 || bt.base[p] + i * bt.stride[p] + c != dst) *dst = v;
+  }
+}
+
+// microbatch means (dpsgd.cpp:102-132) over materialised stacks: unit u =
+// mean of m consecutive rows, summed in order from zero then * (float)1/m.
 __global__ void microbatch_kernel(const float* __restrict__ stacks, BlockTable bt, int B,
                                   int m, float* __restrict__ units_out) {
   const int U = B / m;
@@ -642,16 +724,15 @@ __global__ void microbatch_kernel(const float* __restrict__ stacks, BlockTable b
     int p = 0;
     while (j >= bt.size[p]) j -= bt.size[p++];
     const long long per = bt.size[p];
-    const float* src = stacks + bt.stack_off[p];
+    const float* src = stacks + bt.param_off[p] * B;
     float acc = 0.0f;
     for (int r = 0; r < m; ++r) acc = __fadd_rn(acc, src[((long long)u * m + r) * per + j]);
-    units_out[bt.stack_off[p] / B * U + (long long)u * per + j] = __fmul_rn(acc, inv);
+    units_out[bt.param_off[p] * U + (long long)u * per + j] = __fmul_rn(acc, inv);
   }
 }
 
-// plain SGD from the stacks (dpsgd.cpp:334-346): p -= lr * (sum_i g_i) * 1/B
-__global__ void sgd_kernel(const float* __restrict__ stacks, BlockTable bt, int B, float lr,
-                           float* __restrict__ params) {
+// plain SGD (dpsgd.cpp:334-346): p -= lr * (sum_i g_i) * 1/B
+__global__ void sgd_kernel(BlockTable bt, int B, float lr, float* __restrict__ params) {
   long long total = 0;
   for (int p = 0; p < bt.n; ++p) total += bt.size[p];
   const float inv = 1.0f / float(B);
@@ -660,10 +741,8 @@ __global__ void sgd_kernel(const float* __restrict__ stacks, BlockTable bt, int 
     long long j = e;
     int p = 0;
     while (j >= bt.size[p]) j -= bt.size[p++];
-    const long long per = bt.size[p];
-    const float* col = stacks + bt.stack_off[p] + j;
     float acc = 0.0f;
-    for (int i = 0; i < B; ++i) acc = __fadd_rn(acc, col[(long long)i * per]);
+    for (int i = 0; i < B; ++i) acc = __fadd_rn(acc, grad_at(bt, p, i, j));
     const long long o = bt.param_off[p] + j;
     params[o] = __fsub_rn(params[o], __fmul_rn(lr, __fmul_rn(acc, inv)));
   }

@@ -142,6 +142,7 @@ struct Engine {
   StepArgs* d_args = nullptr;
   // fused MNIST factors
   float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
+  float* d_w2t = nullptr;  // conv2 weights kept transposed [k][d] for the fused kernel
   std::vector<float*> d_dense_g;  // per dense layer: output cotangent (B, out)
 
   // pinned host staging
@@ -277,6 +278,7 @@ struct Engine {
       want((void**)&d_dz1, sizeof(float) * B * 32);
       want((void**)&d_h, sizeof(float) * B * 32);
       want((void**)&d_dz2, sizeof(float) * B * 10);
+      want((void**)&d_w2t, sizeof(float) * 32 * 256);
     }
     d_dense_g.assign(n, nullptr);
     for (int l = 0; l < n; ++l)
@@ -366,6 +368,10 @@ struct Engine {
       set_block(bt, 5, 0, d_dz1, 32);
       set_block(bt, 6, 1, d_dz2, 10, d_h, 32, 10);
       set_block(bt, 7, 0, d_dz2, 10);
+      bt.shadow[2] = d_w2t;  // conv2 W (32, 256) -> [256][32]
+      bt.shadow_rows[2] = 32;
+      bt_stack.shadow[2] = d_w2t;
+      bt_stack.shadow_rows[2] = 32;
       norms_fused = true;
       nparts = 1;
     } else {
@@ -430,6 +436,18 @@ struct Engine {
     std::vector<float> p0(P);
     if (pgb_init_params(&desc, 0, p0.data()) != PGB_OK) raise(PGB_ERR_CONTRACT, "init failed");
     PGB_CUDA(cudaMemcpy(d_params, p0.data(), sizeof(float) * P, cudaMemcpyHostToDevice));
+    refresh_shadows(stream);
+    PGB_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  // Keep transposed shadows in step with host-uploaded parameters.
+  void refresh_shadows(cudaStream_t s) {
+    for (int p = 0; p < bt.n; ++p)
+      if (bt.shadow[p]) {
+        const int rows = bt.shadow_rows[p], cols = (int)(bt.size[p] / rows);
+        transpose_kernel<<<grid_for((size_t)rows * cols), 256, 0, s>>>(
+            d_params + param_off[p], rows, cols, bt.shadow[p]);
+      }
   }
 
   // ---- profiling hook: an event after every launch while profiling --------
@@ -524,6 +542,7 @@ struct Engine {
     prm.x = x_slot;
     prm.y = y_slot;
     prm.w = d_params;
+    prm.w2t = d_w2t;
     for (int p = 0; p < 8; ++p) prm.off[p] = param_off[p];
     prm.st_c1w = d_stacks + param_off[0] * B;
     prm.st_c1b = d_stacks + param_off[1] * B;
@@ -657,16 +676,15 @@ struct Engine {
 
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U) {
     int nk = 0;
-    const long long pairs = t.pair_off[t.n];
-    const int threads = 256;
-    const int grid = (int)std::min<long long>((pairs + threads - 1) / threads, 148 * 8);
+    const int threads = 32 * kChunks;
+    const int grid = (int)std::min<long long>((P + 31) / 32, 148 * 16);
     const size_t smem = sizeof(float) * U;
     if (world == 1) {
-      aggregate_kernel<8><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, nullptr,
+      aggregate_kernel<16><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, nullptr,
                                                       d_norms, d_clipped, d_err, 0);
       nk += mark(s, "aggregate");
     } else {
-      aggregate_kernel<8><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, d_sum,
+      aggregate_kernel<16><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, d_sum,
                                                       d_norms, d_clipped, d_err, 1);
       nk += mark(s, "aggregate_local");
       auto& N = Nccl::get();
@@ -674,7 +692,7 @@ struct Engine {
       PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
       PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
       PGB_NCCL(N.groupEnd());
-      noise_update_kernel<<<grid, threads, 0, s>>>(d_sum, t, d_args, d_params, d_err);
+      noise_update_kernel<<<grid_for((size_t)P), 256, 0, s>>>(d_sum, t, d_args, d_params, d_err);
       nk += mark(s, "noise_update");
     }
     return nk;
@@ -683,9 +701,8 @@ struct Engine {
   // Noise-free clipped sum of the batch into d_sum (no update): the
   // north-star parity probe.
   int enqueue_local_sum(cudaStream_t s, const BlockTable& t, int np, int U) {
-    const long long pairs = t.pair_off[t.n];
-    const int grid = (int)std::min<long long>((pairs + 255) / 256, 148 * 8);
-    aggregate_kernel<8><<<grid, 256, sizeof(float) * U, s>>>(t, d_parts, np, d_args, d_params,
+    const int grid = (int)std::min<long long>((P + 31) / 32, 148 * 16);
+    aggregate_kernel<16><<<grid, 32 * kChunks, sizeof(float) * U, s>>>(t, d_parts, np, d_args, d_params,
                                                              d_sum, d_norms, d_clipped, d_err, 1);
     return 1;
   }
@@ -885,6 +902,7 @@ pgb_status pgb_set_params(pgb_engine* e, const float* flat) {
     Engine& en = E(e);
     PGB_CUDA(cudaMemcpyAsync(en.d_params, flat, sizeof(float) * en.P, cudaMemcpyHostToDevice,
                              en.stream));
+    en.refresh_shadows(en.stream);
     PGB_CUDA(cudaStreamSynchronize(en.stream));
   });
 }

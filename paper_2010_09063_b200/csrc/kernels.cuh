@@ -452,7 +452,21 @@ struct BlockTable {
   const float* a[kMaxBlocks];
   long long a_stride[kMaxBlocks];
   int out[kMaxBlocks];
+  // optional transposed copy of the parameter block kept in step with the
+  // update (row-major (rows, cols) block -> shadow[c * rows + r])
+  float* shadow[kMaxBlocks];
+  int shadow_rows[kMaxBlocks];
 };
+
+__device__ __forceinline__ void write_param(const BlockTable& bt, int p, long long j,
+                                            float* params, float v) {
+  params[bt.param_off[p] + j] = v;
+  if (bt.shadow[p]) {
+    const long long cols = bt.size[p] / bt.shadow_rows[p];
+    const long long r = j / cols, c = j - r * cols;
+    bt.shadow[p][c * bt.shadow_rows[p] + r] = v;
+  }
+}
 
 __device__ __forceinline__ float grad_at(const BlockTable& bt, int p, long long i, long long j) {
   if (bt.kind[p] == 0) return bt.base[p][i * bt.stride[p] + j];
@@ -564,90 +578,111 @@ __device__ __forceinline__ int find_block(const long long* pair_off, int n, long
   return p;
 }
 
-// Clipped sum over units in ascending order, one fp32 chain per column
-// (dpsgd.cpp:287-307), then noise / mean / SGD update (dpsgd.cpp:308-317,
-// apply_update :173-183), all in the reference's fp32 operation order.
+// Clipped sum over the units (dpsgd.cpp:287-307), then noise / mean / SGD
+// update (dpsgd.cpp:308-317, apply_update :173-183) with the reference's fp32
+// operation order per element. The sum over units runs as kChunks ordered
+// partial sums (each in ascending unit order) combined in chunk order: a
+// fixed, run-to-run deterministic order that keeps kChunks x more loads in
+// flight than one sequential chain per column (the reference's strictly
+// ascending chain differs only by fp32 re-association, ~1e-7 relative).
+// CTA = 32 columns x kChunks warps; lanes take consecutive columns.
 // mode 0: fused single-GPU step; mode 1: write the local clipped sum only.
+constexpr int kChunks = 8;
+
 template <int UNROLL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * kChunks)
     aggregate_kernel(BlockTable bt, const double* __restrict__ parts, int nparts,
                      const StepArgs* __restrict__ args, float* __restrict__ params,
                      float* __restrict__ sum_out, float* __restrict__ norms_out,
                      int* __restrict__ clipped_out, const DevError* __restrict__ err, int mode) {
   extern __shared__ float s_sh[];
-  __shared__ long long pair_sh[kMaxBlocks + 1];
+  __shared__ long long off_sh[kMaxBlocks + 1];
+  __shared__ float part_sh[kChunks][33];
   const StepArgs a = *args;
   const int U = a.units;
-  for (int p = threadIdx.x; p <= bt.n; p += blockDim.x) pair_sh[p] = bt.pair_off[p];
+  if (threadIdx.x == 0) {
+    long long o = 0;
+    for (int p = 0; p < bt.n; ++p) {
+      off_sh[p] = o;
+      o += bt.size[p];
+    }
+    off_sh[bt.n] = o;
+  }
   load_scales(parts, nparts, U, a.clip, s_sh, blockIdx.x == 0 ? norms_out : nullptr,
               blockIdx.x == 0 ? clipped_out : nullptr);
   const bool failed = err && err->code != 0;
-  const long long total_pairs = pair_sh[bt.n];
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
-       q += (long long)gridDim.x * blockDim.x) {
-    const int p = find_block(pair_sh, bt.n, q);
-    const long long lq = q - pair_sh[p];
-    const long long per = bt.size[p];
-    const long long j0 = 2 * lq;
-    const bool has1 = j0 + 1 < per;
-    float acc0 = 0.0f, acc1 = 0.0f;
-    if (bt.kind[p] == 0) {
-      const float* col = bt.base[p] + j0;
-      const long long st = bt.stride[p];
-      int i = 0;
-      for (; i + UNROLL <= U; i += UNROLL) {
-        float v0[UNROLL], v1[UNROLL];
+  const long long total = off_sh[bt.n];
+  const int lane = threadIdx.x & 31, chunk = threadIdx.x >> 5;
+  const int rows = (U + kChunks - 1) / kChunks;
+  const int i0 = min(U, chunk * rows), i1 = min(U, i0 + rows);
+  for (long long base = (long long)blockIdx.x * 32; base < total;
+       base += (long long)gridDim.x * 32) {
+    const long long q = base + lane;
+    float acc = 0.0f;
+    int p = 0;
+    long long j = 0;
+    if (q < total) {
+      p = find_block(off_sh, bt.n, q);
+      j = q - off_sh[p];
+      if (bt.kind[p] == 0) {
+        const float* col = bt.base[p] + j;
+        const long long st = bt.stride[p];
+        int i = i0;
+        for (; i + UNROLL <= i1; i += UNROLL) {
+          float v[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          v0[u] = __ldg(col + (long long)(i + u) * st);
-          v1[u] = has1 ? __ldg(col + (long long)(i + u) * st + 1) : 0.0f;
-        }
+          for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(col + (long long)(i + u) * st);
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          acc0 = __fadd_rn(acc0, __fmul_rn(v0[u], s_sh[i + u]));
-          acc1 = __fadd_rn(acc1, __fmul_rn(v1[u], s_sh[i + u]));
+          for (int u = 0; u < UNROLL; ++u) acc = __fadd_rn(acc, __fmul_rn(v[u], s_sh[i + u]));
+        }
+        for (; i < i1; ++i) acc = __fadd_rn(acc, __fmul_rn(__ldg(col + (long long)i * st), s_sh[i]));
+      } else {
+        // factored dense block: rebuild the fp32 stack element fl(a_r * d_c)
+        const int out = bt.out[p];
+        const long long r = j / out, c = j - r * out;
+        const float* A = bt.a[p] + r;
+        const float* D = bt.base[p] + c;
+        const long long as = bt.a_stride[p], ds = bt.stride[p];
+        int i = i0;
+        for (; i + UNROLL <= i1; i += UNROLL) {
+          float av[UNROLL], dv[UNROLL];
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            av[u] = __ldg(A + (long long)(i + u) * as);
+            dv[u] = __ldg(D + (long long)(i + u) * ds);
+          }
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u)
+            acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(av[u], dv[u]), s_sh[i + u]));
+        }
+        for (; i < i1; ++i)
+          acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__ldg(A + (long long)i * as),
+                                                   __ldg(D + (long long)i * ds)), s_sh[i]));
+      }
+    }
+    part_sh[chunk][lane] = acc;
+    __syncthreads();
+    if (chunk == 0 && q < total) {
+      float sum = part_sh[0][lane];
+#pragma unroll
+      for (int c = 1; c < kChunks; ++c) sum = __fadd_rn(sum, part_sh[c][lane]);
+      if (mode == 1) {
+        sum_out[bt.param_off[p] + j] = sum;
+      } else {
+        if (a.add_noise) {
+          float n0, n1;
+          gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
+          const float scale = __fmul_rn(a.sigma, a.clip);
+          sum = __fadd_rn(sum, __fmul_rn(scale, (j & 1) ? n1 : n0));
+        }
+        sum = __fmul_rn(sum, a.inv_units);
+        if (!failed) {
+          const float cur = params[bt.param_off[p] + j];
+          write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
         }
       }
-      for (; i < U; ++i) {
-        acc0 = __fadd_rn(acc0, __fmul_rn(col[(long long)i * st], s_sh[i]));
-        if (has1) acc1 = __fadd_rn(acc1, __fmul_rn(col[(long long)i * st + 1], s_sh[i]));
-      }
-    } else {
-      // factored dense block: rebuild the fp32 stack elements on the fly
-      const int out = bt.out[p];
-      const long long r0 = j0 / out, c0 = j0 - r0 * out;
-      const long long r1 = (c0 + 1 < out) ? r0 : r0 + 1, c1 = (c0 + 1 < out) ? c0 + 1 : 0;
-      const float* A = bt.a[p];
-      const float* D = bt.base[p];
-      const long long as = bt.a_stride[p], ds = bt.stride[p];
-#pragma unroll 4
-      for (int i = 0; i < U; ++i) {
-        const float a0 = __ldg(A + i * as + r0), d0 = __ldg(D + i * ds + c0);
-        acc0 = __fadd_rn(acc0, __fmul_rn(__fmul_rn(a0, d0), s_sh[i]));
-        if (has1) {
-          const float a1 = __ldg(A + i * as + r1), d1 = __ldg(D + i * ds + c1);
-          acc1 = __fadd_rn(acc1, __fmul_rn(__fmul_rn(a1, d1), s_sh[i]));
-        }
-      }
     }
-    const long long o = bt.param_off[p] + j0;
-    if (mode == 1) {
-      sum_out[o] = acc0;
-      if (has1) sum_out[o + 1] = acc1;
-      continue;
-    }
-    if (a.add_noise) {
-      float n0, n1;
-      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), lq, &n0, &n1);
-      const float scale = __fmul_rn(a.sigma, a.clip);
-      acc0 = __fadd_rn(acc0, __fmul_rn(scale, n0));
-      acc1 = __fadd_rn(acc1, __fmul_rn(scale, n1));
-    }
-    acc0 = __fmul_rn(acc0, a.inv_units);
-    acc1 = __fmul_rn(acc1, a.inv_units);
-    if (failed) continue;
-    params[o] = __fsub_rn(params[o], __fmul_rn(a.lr, acc0));
-    if (has1) params[o + 1] = __fsub_rn(params[o + 1], __fmul_rn(a.lr, acc1));
+    __syncthreads();
   }
 }
 
@@ -657,32 +692,33 @@ __global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt
                                     const StepArgs* __restrict__ args,
                                     float* __restrict__ params,
                                     const DevError* __restrict__ err) {
-  __shared__ long long pair_sh[kMaxBlocks + 1];
-  for (int p = threadIdx.x; p <= bt.n; p += blockDim.x) pair_sh[p] = bt.pair_off[p];
+  __shared__ long long off_sh[kMaxBlocks + 1];
+  if (threadIdx.x == 0) {
+    long long o = 0;
+    for (int p = 0; p < bt.n; ++p) {
+      off_sh[p] = o;
+      o += bt.size[p];
+    }
+    off_sh[bt.n] = o;
+  }
   __syncthreads();
   const StepArgs a = *args;
   if (err && err->code != 0) return;
-  const long long total_pairs = pair_sh[bt.n];
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total_pairs;
+  const long long total = off_sh[bt.n];
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
-    const int p = find_block(pair_sh, bt.n, q);
-    const long long lq = q - pair_sh[p];
-    const long long per = bt.size[p];
-    const long long j0 = 2 * lq;
-    const bool has1 = j0 + 1 < per;
-    const long long o = bt.param_off[p] + j0;
-    float acc0 = sum[o], acc1 = has1 ? sum[o + 1] : 0.0f;
+    const int p = find_block(off_sh, bt.n, q);
+    const long long j = q - off_sh[p];
+    float acc = sum[bt.param_off[p] + j];
     if (a.add_noise) {
       float n0, n1;
-      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), lq, &n0, &n1);
+      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
       const float scale = __fmul_rn(a.sigma, a.clip);
-      acc0 = __fadd_rn(acc0, __fmul_rn(scale, n0));
-      acc1 = __fadd_rn(acc1, __fmul_rn(scale, n1));
+      acc = __fadd_rn(acc, __fmul_rn(scale, (j & 1) ? n1 : n0));
     }
-    acc0 = __fmul_rn(acc0, a.inv_units);
-    acc1 = __fmul_rn(acc1, a.inv_units);
-    params[o] = __fsub_rn(params[o], __fmul_rn(a.lr, acc0));
-    if (has1) params[o + 1] = __fsub_rn(params[o + 1], __fmul_rn(a.lr, acc1));
+    acc = __fmul_rn(acc, a.inv_units);
+    const float cur = params[bt.param_off[p] + j];
+    write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, acc)));
   }
 }
 
@@ -743,8 +779,17 @@ __global__ void sgd_kernel(BlockTable bt, int B, float lr, float* __restrict__ p
     while (j >= bt.size[p]) j -= bt.size[p++];
     float acc = 0.0f;
     for (int i = 0; i < B; ++i) acc = __fadd_rn(acc, grad_at(bt, p, i, j));
-    const long long o = bt.param_off[p] + j;
-    params[o] = __fsub_rn(params[o], __fmul_rn(lr, __fmul_rn(acc, inv)));
+    const float cur = params[bt.param_off[p] + j];
+    write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(lr, __fmul_rn(acc, inv))));
+  }
+}
+
+// shadow[c * rows + r] = block[r * cols + c] (after a host parameter upload)
+__global__ void transpose_kernel(const float* __restrict__ src, int rows, int cols,
+                                 float* __restrict__ dst) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    dst[c * rows + r] = src[e];
   }
 }
 

@@ -205,6 +205,10 @@ pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
                              const pgb_dp_config* cfg, int64_t step0, int32_t n_steps,
                              int32_t max_kernels, float* ms_out, char* names_out,
                              int32_t* n_kernels_out);
+/* Self-test of the tcgen05 3xTF32 GEMM block: C (MxN) = A (MxK) . B (NxK)^T,
+ * host buffers. */
+pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
+                             const float* B, float* C);
 /* Kernel launches recorded for the last step (profiling/evidence). */
 int32_t pgb_kernels_per_step(pgb_engine* e);
 

@@ -97,6 +97,8 @@ EXPORTS = {
     "pgb_profile_steps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(DpConfigC),
                                     C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.POINTER(C.c_int32)]),
+    "pgb_debug_tc_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]),
     "pgb_device_params": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_device_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_kernels_per_step": (C.c_int32, [C.c_void_p]),

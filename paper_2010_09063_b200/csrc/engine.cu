@@ -19,6 +19,7 @@
 
 #include "kernels.cuh"
 #include "mnist_fused.cuh"
+#include "tc.cuh"
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -1222,6 +1223,32 @@ pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
     }
     if (n_kernels_out) *n_kernels_out = nk;
     for (auto& m : marks) cudaEventDestroy(m.first);
+  });
+}
+
+pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
+                             const float* Bm, float* Cout) {
+  return guarded([&] {
+    PGB_CUDA(cudaSetDevice(device));
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    PGB_CUDA(cudaMalloc(&dA, sizeof(float) * (size_t)M * K));
+    PGB_CUDA(cudaMalloc(&dB, sizeof(float) * (size_t)N * K));
+    PGB_CUDA(cudaMalloc(&dC, sizeof(float) * (size_t)M * N));
+    PGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * (size_t)M * K, cudaMemcpyHostToDevice));
+    PGB_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * (size_t)N * K, cudaMemcpyHostToDevice));
+    tc::PlainOp op{M, N, K, dA, dB, dC};
+    constexpr int BN = 64;
+    const size_t smem = tc::tc_smem_bytes<tc::PlainOp, BN>();
+    PGB_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<tc::PlainOp, BN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((N + BN - 1) / BN, (M + tc::kBM - 1) / tc::kBM, 1);
+    tc::tc_gemm_kernel<tc::PlainOp, BN><<<grid, tc::kThreads, smem>>>(op);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaDeviceSynchronize());
+    PGB_CUDA(cudaMemcpy(Cout, dC, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
   });
 }
 

@@ -1,0 +1,264 @@
+// tcgen05 (5th-generation tensor core) building blocks for sm_100a:
+// TMEM allocation, UMMA shared-memory descriptors (K-major, no swizzle),
+// kind::tf32 MMA issue, commit-to-mbarrier, TMEM -> register loads.
+//
+// fp32 accuracy comes from the 3xTF32 split: x = hi + lo with
+// hi = rna_tf32(x), lo = x - hi; D += Ahi.Bhi + Ahi.Blo + Alo.Bhi gives
+// ~1e-7 normwise error (1xTF32 gives ~3e-4 and fails the 1e-5 parity bar,
+// SURVEY 8(d)).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pgb {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_NONE, K-major canonical
+// layout ((8,m),(4,2)) : ((16B, SBO), (4B, LBO)) -- core matrices of
+// 8 rows x 16 bytes, LBO between the two K-adjacent core matrices of one MMA,
+// SBO between 8-row groups.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, both operands K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4)                       // D format f32
+         | (2u << 7)                     // A format tf32
+         | (2u << 10)                    // B format tf32
+         | ((uint32_t)(N >> 3) << 17)    // N / 8
+         | ((uint32_t)(M >> 4) << 24);   // M / 16
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Arrive on `bar` once every previously issued tcgen05.mma of this thread
+// has completed (implies tcgen05.fence::before_thread_sync).
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+      :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void fence_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One full warp: allocate `ncols` TMEM columns (power of 2 >= 32); the base
+// address lands in *slot.
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+               :: "r"(smem_u32(slot)), "r"(ncols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+               :: "r"(taddr), "r"(ncols) : "memory");
+}
+
+// Warp w reads TMEM lanes 32w..32w+31 (one accumulator row per thread),
+// 8 consecutive 32-bit columns starting at `taddr`'s column.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// 3xTF32 split.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  lo = x - hi;
+}
+
+// Float offset of element (r, k) inside one K-major canonical tile whose K
+// extent is BK: 8x4 core matrices, K-adjacent cores 32 floats apart (LBO =
+// 128 B), 8-row groups BK*8 floats apart (SBO = BK*32 B).
+template <int BK>
+__device__ __forceinline__ int canon_off(int r, int k) {
+  return (r & 7) * 4 + (k & 3) + (r >> 3) * (BK * 8) + (k >> 2) * 32;
+}
+
+// ---------------------------------------------------------------------------
+// Generic tcgen05 GEMM with gathered operands:
+//   C[z][m][n] = sum_k A(z,m,k) * B(z,n,k)       (then op.store)
+// BM = 128 rows per CTA (UMMA_M = 128, one accumulator row per TMEM lane),
+// BN columns (multiple of 16, <= 256), BK = 32 per pipeline stage, 2 stages.
+// 128 threads: all gather (fp32 -> hi/lo tf32 in canonical layout), thread 0
+// issues 4 k-steps x 3 MMAs per stage and commits to the stage's mbarrier,
+// the gather of the next stage overlaps the tensor core; epilogue reads the
+// accumulator from TMEM with tcgen05.ld.
+// ---------------------------------------------------------------------------
+constexpr int kBM = 128, kBK = 32, kThreads = 128;
+
+template <int BN>
+struct TcSmem {
+  float ahi[2][kBM * kBK], alo[2][kBM * kBK];
+  float bhi[2][BN * kBK], blo[2][BN * kBK];
+  uint64_t bar[2];
+  uint32_t tmem;
+};
+
+template <class Op, int BN>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(Op op) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  TcSmem<BN>& S = *reinterpret_cast<TcSmem<BN>*>(raw);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int z = blockIdx.z;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
+  const int M = op.M, N = op.N, K = op.K;
+  // three accumulators: hi.hi for even / odd K chunks, and the small
+  // hi.lo + lo.hi correction -- shorter fp32 accumulation chains in TMEM
+  constexpr uint32_t kCols = 3 * BN <= 32 ? 32 : 3 * BN <= 64 ? 64 : 3 * BN <= 128 ? 128
+                             : 3 * BN <= 256 ? 256 : 512;
+  static_assert(3 * BN <= 512, "BN too large for three TMEM accumulators");
+  if (warp == 0) tmem_alloc(&S.tmem, kCols);
+  if (t == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = S.tmem;
+  constexpr uint32_t idesc = idesc_tf32(kBM, BN);
+  const int nk = (K + kBK - 1) / kBK;
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
+    const int k0 = kc * kBK;
+    // gather A: lanes cover one 8x4 core matrix (conflict-free 128 B stores)
+    for (int e = t; e < kBM * kBK; e += kThreads) {
+      const int core = e >> 5, in = e & 31;
+      const int r = (core % (kBM / 8)) * 8 + (in >> 2);
+      const int k = (core / (kBM / 8)) * 4 + (in & 3);
+      const int m = m0 + r, kk = k0 + k;
+      const float v = (m < M && kk < K) ? op.a(z, m, kk) : 0.0f;
+      float hi, lo;
+      split_tf32(v, hi, lo);
+      const int o = canon_off<kBK>(r, k);
+      S.ahi[s][o] = hi;
+      S.alo[s][o] = lo;
+    }
+    for (int e = t; e < BN * kBK; e += kThreads) {
+      const int core = e >> 5, in = e & 31;
+      const int r = (core % (BN / 8)) * 8 + (in >> 2);
+      const int k = (core / (BN / 8)) * 4 + (in & 3);
+      const int n = n0 + r, kk = k0 + k;
+      const float v = (n < N && kk < K) ? op.b(z, n, kk) : 0.0f;
+      float hi, lo;
+      split_tf32(v, hi, lo);
+      const int o = canon_off<kBK>(r, k);
+      S.bhi[s][o] = hi;
+      S.blo[s][o] = lo;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0) {
+      fence_after_sync();
+      const uint32_t ah = smem_u32(S.ahi[s]), al = smem_u32(S.alo[s]);
+      const uint32_t bh = smem_u32(S.bhi[s]), bl = smem_u32(S.blo[s]);
+#pragma unroll
+      for (int ks = 0; ks < kBK / 8; ++ks) {
+        const uint32_t off = ks * 256;  // two 128-B core matrices per k-step
+        const uint64_t dah = make_desc(ah + off, 128, kBK * 32);
+        const uint64_t dal = make_desc(al + off, 128, kBK * 32);
+        const uint64_t dbh = make_desc(bh + off, 128, kBK * 32);
+        const uint64_t dbl = make_desc(bl + off, 128, kBK * 32);
+        const uint32_t main = tmem + (uint32_t)((kc & 1) * BN), corr = tmem + 2 * BN;
+        mma_tf32(main, dah, dbh, idesc, (kc > 1 || ks > 0) ? 1u : 0u);
+        mma_tf32(corr, dah, dbl, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
+        mma_tf32(corr, dal, dbh, idesc, 1u);
+      }
+      commit(&S.bar[s]);
+    }
+  }
+  // all MMAs done once the last commit lands (they complete in issue order)
+  mbar_wait(&S.bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  fence_after_sync();
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 8) {
+    float v[8], v1[8], vc[8];
+    tmem_ld8(lane_base + (uint32_t)c0, v);
+    tmem_ld8(lane_base + (uint32_t)(2 * BN + c0), vc);
+    if (nk > 1) {
+      tmem_ld8(lane_base + (uint32_t)(BN + c0), v1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += v1[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] += vc[j];
+    if (row < M) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (n0 + c0 + j < N) op.store(z, row, n0 + c0 + j, v[j]);
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kCols);
+}
+
+template <class Op, int BN>
+inline size_t tc_smem_bytes() {
+  return sizeof(TcSmem<BN>);
+}
+
+// Plain row-major test GEMM: C (M x N) = A (M x K) . B (N x K)^T.
+struct PlainOp {
+  int M, N, K;
+  const float* A;
+  const float* Bm;
+  float* C;
+  __device__ float a(int, int m, int k) const { return A[(size_t)m * K + k]; }
+  __device__ float b(int, int n, int k) const { return Bm[(size_t)n * K + k]; }
+  __device__ void store(int, int m, int n, float v) const { C[(size_t)m * N + n] = v; }
+};
+
+}  // namespace tc
+}  // namespace pgb

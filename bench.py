@@ -1,20 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark: DPSGD examples/sec, MNIST CNN (reference topology, P=26,010),
-batch 256 per GPU, C=1.0, sigma=1.1, lr=0.1, synthetic MNIST-shaped data.
+"""Benchmark: DPSGD examples/sec at batch 256 (MNIST CNN, reference topology,
+P=26,010), C=1.0, sigma=1.1, lr=0.1, synthetic MNIST-shaped data.
 
-    python bench.py [--gpus N --steps K --warmup W]           # our engine
-    python bench.py --impl reference ...                       # reference CPU path
+    python bench.py [--gpus N --steps K --warmup W] [--model cifar_cnn ...]
+    python bench.py --impl reference ...          # the reference's CPU path
 
 Under torchrun each rank drives one GPU with 256 examples per step (weak
 scaling: global DP batch 256*N, one NCCL all-reduce of the clipped sum per
-step). Prints ONE JSON line on rank 0.
+step inside the engine's CUDA graph). Prints ONE JSON line on rank 0.
 
-value  : device-resident inputs (a 60,000-example synthetic dataset, 188 MB >
-         the 126 MB L2, cycled batch by batch), K steps timed with CUDA events
-         on the engine stream, max over ranks.
+value  : device-resident inputs (a synthetic dataset larger than the 126 MB
+         L2 -- 60,000 MNIST images, 188 MB -- cycled batch by batch), K steps
+         timed with CUDA events on the engine stream, max over ranks.
 e2e    : the public epoch driver pgb_run_epoch on PINNED HOST batches: every
          step copies its batch H2D and reads its result (per-example norms +
          clipped count) back D2H; wall time, max over ranks.
+roofline: per-kernel device times from CUDA events around each launch of the
+         same schedule (pgb_profile_steps), algorithmic work per SURVEY 8(d).
 """
 from __future__ import annotations
 
@@ -30,11 +32,25 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "DPSGD examples/sec at batch 256 (MNIST CNN); median epoch time vs CPU ref"
 UNIT = "examples/s"
-BATCH = 256
 CLIP, SIGMA, LR, SEED = 1.0, 1.1, 0.1, 0
-DATA_N = 60000  # the paper's MNIST epoch; 188 MB of fp32 pixels > L2
+
+# model -> (ModelKind, options, strategy, per-GPU batch, dataset size, metric, MFLOP/ex)
+MODELS = {
+    "mnist_cnn": (2, {}, 4, 256, 60000,
+                  "DPSGD examples/sec at batch 256 (MNIST CNN); median epoch time vs CPU ref",
+                  1.689, "reference topology conv16 8x8/2 p3, maxpool2, conv32 4x4, "
+                         "fc512-32, fc32-10; P=26,010"),
+    "cifar_cnn": (3, {}, 4, 256, 12800, "DPSGD examples/sec at batch 256 (CIFAR-10 CNN)",
+                  260.6, "8 conv3x3 + 3 avgpool + GAP; P=605,226"),
+    "fcnn": (1, {}, 2, 256, 200000, "DPSGD examples/sec at batch 256 (FCNN 104-50-10)",
+             0.0238, "dense 104-50-10; P=5,760"),
+    "logreg": (0, {}, 2, 256, 300000, "DPSGD examples/sec at batch 256 (logistic regression)",
+               0.0006, "dense 104-1, sigmoid head; P=105"),
+    "embed": (4, {"hidden": 100}, 5, 512, 1024,
+              "DPSGD examples/sec at batch 512 (IMDb-shaped embedding)", 0.05,
+              "embedding 10,004x100, mean-pool, dense 100-2; P=1,000,602"),
+}
 
 
 def peaks():
@@ -101,47 +117,62 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+def workload_config(model, world):
+    kind, opts, strat, batch, data_n, _, _, arch = MODELS[model]
+    return {"workload": f"{model} DPSGD step ({arch})", "model": model,
+            "global_batch": batch * world, "per_gpu_batch": batch, "seq_len": None,
+            "parallelism": f"dp{world}", "clip_norm": CLIP, "noise_multiplier": SIGMA,
+            "learning_rate": LR,
+            "l2": f"inputs larger than L2 where the dataset allows: {data_n}-example resident "
+                  "synthetic dataset cycled one batch per step"}
+
+
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref = the unmodified reference library compiled here)
 # ---------------------------------------------------------------------------
 
-def _ref_worker(steps, warmup, time_cap, q):
+def _ref_worker(model, steps, warmup, time_cap, q):
     import numpy as np
     import oracle as O
-    d = O.build_desc(O.MNIST_CNN)
+    kind, opts, strat, batch, _, _, _, _ = MODELS[model]
+    strat = {4: O.GROUPCONV, 2: O.OUTER, 5: O.JACMM}.get(strat, strat)
+    if model == "fcnn":
+        strat = O.NORMS  # the reference's fastest FCNN strategy
+    d = O.build_desc(kind, **opts)
     p = O.ref_init_params(d, SEED, np.float32)
-    nb = 16
-    x, y = O.ref_synth(d, BATCH * nb, SEED, np.float32)
-    R = O.RefModel(d, O.GROUPCONV, BATCH, p, np.float32)
+    nb = 4
+    x, y = O.ref_synth(d, batch * nb, SEED, np.float32)
+    R = O.RefModel(d, strat, batch, p, np.float32)
     for s in range(warmup):
         b = s % nb
-        R.step(x[b * BATCH:(b + 1) * BATCH], y[b * BATCH:(b + 1) * BATCH], CLIP, SIGMA, LR, 1,
+        R.step(x[b * batch:(b + 1) * batch], y[b * batch:(b + 1) * batch], CLIP, SIGMA, LR, 1,
                SEED, s)
     t0 = time.perf_counter()
     done = 0
     while done < steps and (time.perf_counter() - t0) < time_cap:
         b = done % nb
-        R.step(x[b * BATCH:(b + 1) * BATCH], y[b * BATCH:(b + 1) * BATCH], CLIP, SIGMA, LR, 1,
+        R.step(x[b * batch:(b + 1) * batch], y[b * batch:(b + 1) * batch], CLIP, SIGMA, LR, 1,
                SEED, warmup + done)
         done += 1
     q.put((done, time.perf_counter() - t0))
 
 
-def cpu_reference(steps, procs, warmup=1, time_cap=20.0):
-    """The reference's own dpsgd_step (groupconv strategy, graph mode, fp32,
+def cpu_reference(model, steps, procs, warmup=1, time_cap=20.0):
+    """The reference's own dpsgd_step (its fastest strategy, graph mode, fp32,
     its 2-thread intra-op split) on `procs` independent processes, each over
     its own batches; returns (aggregate ex/s, steps per process, seconds)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_ref_worker, args=(steps, warmup, time_cap, q))
+    ps = [ctx.Process(target=_ref_worker, args=(model, steps, warmup, time_cap, q))
           for _ in range(procs)]
     for p in ps:
         p.start()
     res = [q.get() for _ in ps]
     for p in ps:
         p.join()
-    value = sum(n * BATCH / t for n, t in res)
+    batch = MODELS[model][3]
+    value = sum(n * batch / t for n, t in res if n)
     return value, [n for n, _ in res], max(t for _, t in res)
 
 
@@ -151,18 +182,19 @@ def run_reference_arm(args):
         return
     ncpu = os.cpu_count() or 1
     procs = max(1, ncpu // 2)
-    value, nsteps, t = cpu_reference(args.steps, procs, warmup=args.warmup,
+    value, nsteps, t = cpu_reference(args.model, args.steps, procs, warmup=args.warmup,
                                      time_cap=args.ref_seconds)
+    batch = MODELS[args.model][3]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "metric": MODELS[args.model][5], "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": int(min(nsteps)), "warmup": args.warmup,
         "ms_per_step": 1e3 * t / max(1, min(nsteps)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (io::synth_for_model, seed 0)", "impl": "reference",
-        "config": workload_config(world),
+        "config": workload_config(args.model, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 2 * procs, "kind": "reference",
                          "sample": f"{procs} processes x up to {args.steps} reference "
-                                   f"dpsgd_step(B=256, groupconv, graph, fp32) capped at "
+                                   f"dpsgd_step(B={batch}, graph, fp32) capped at "
                                    f"{args.ref_seconds:.0f} s each (ran {nsteps}); host "
                                    f"nproc={ncpu}; 2 threads per process, the reference's "
                                    f"maximum (parallel.cpp:30-75)"},
@@ -171,28 +203,53 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(world):
-    return {"workload": "mnist_cnn DPSGD step (reference topology conv16 8x8/2 p3, maxpool2, "
-                        "conv32 4x4, fc512-32, fc32-10; P=26,010)",
-            "model": "mnist_cnn", "global_batch": BATCH * world, "per_gpu_batch": BATCH,
-            "seq_len": None, "parallelism": f"dp{world}",
-            "clip_norm": CLIP, "noise_multiplier": SIGMA, "learning_rate": LR,
-            "l2": f"inputs larger than L2: {DATA_N}-example resident dataset (188 MB) cycled "
-                  "one batch per step"}
-
-
 # ---------------------------------------------------------------------------
 # our engine
 # ---------------------------------------------------------------------------
 
-def algorithmic(name, B, P, nb):
-    """Algorithmic bytes per launch for the HBM-bound kernels:
-    per-example stacks are B*P fp32 values."""
-    if name == "aggregate":
-        return B * P * 4 + 2 * P * 4 + B * nb * 8 + B * 4
-    if name == "sumsq":
-        return B * P * 4 + B * nb * 8
-    return None
+def conv_gemm_flops(desc, B):
+    """Algorithmic FLOPs of the convolution GEMMs of one step: forward,
+    per-example dW and input gradient (2*M*N*K each, single pass; the 3xTF32
+    split is not counted as work)."""
+    from paper_2010_09063_b200 import LayerKind
+    shape = tuple(desc.input_shape)
+    first = True
+    total = 0
+    for l in desc.layers:
+        if l.kind == LayerKind.conv:
+            C_, H, W = shape
+            Ho = (H + 2 * l.pad - l.k) // l.stride + 1
+            Wo = (W + 2 * l.pad - l.k) // l.stride + 1
+            mnk = B * Ho * Wo * l.out * C_ * l.k * l.k
+            total += 2 * mnk * (2 if first else 3)
+            shape = (l.out, Ho, Wo)
+            first = False
+        elif l.kind in (LayerKind.maxpool, LayerKind.avgpool):
+            shape = (shape[0], (shape[1] - l.k) // l.stride + 1, (shape[2] - l.k) // l.stride + 1)
+        elif l.kind == LayerKind.global_avgpool:
+            shape = (shape[0],)
+    return total
+
+
+def aggregate_bytes(desc, B, fused):
+    """Bytes the aggregation kernel must read/write: per-example gradient
+    sources (materialised rows: B*|p|*4; factored dense blocks: B*(in+out)*4),
+    the parameters (read + write), norms partials."""
+    from paper_2010_09063_b200 import LayerKind
+    total = 0
+    pi = 0
+    for l in desc.layers:
+        if l.kind == LayerKind.dense:
+            total += B * (l.in_ + l.out) * 4 + B * l.out * 4
+            pi += 2
+        elif l.kind == LayerKind.conv:
+            total += B * (l.out * l.in_ * l.k * l.k + l.out) * 4
+            pi += 2
+        elif l.kind == LayerKind.embedding:
+            total += B * l.in_ * l.out * 4
+            pi += 1
+    P = desc.param_count()
+    return total + 2 * P * 4 + B * 8 * (1 if fused else pi) + B * 4
 
 
 def run_ours(args):
@@ -202,30 +259,26 @@ def run_ours(args):
 
     import paper_2010_09063_b200 as Pk
     from paper_2010_09063_b200 import _lib
+    from paper_2010_09063_b200.dist import exchange_unique_id
 
+    kind, opts, strat, BATCH, DATA_N, METRIC, MFLOP, _ = MODELS[args.model]
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     dev = local
-    desc = Pk.build_desc(Pk.ModelKind.mnist_cnn)
-    model = Pk.build(Pk.ModelKind.mnist_cnn, SEED)
+    desc = Pk.build_desc(Pk.ModelKind(kind), Pk.ModelOptions(**opts))
+    model = Pk.build_from_desc(desc, SEED)
     if world > 1:
-        uid = bytearray(128)
-        if rank == 0:
-            u = _lib.UniqueIdC()
-            _lib.check(_lib.lib.pgb_nccl_unique_id(C.byref(u)))
-            uid = bytearray(bytes(u)[:128])
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0)
-        engine = Pk.GradEngine(model, Pk.Strategy.groupconv, BATCH, device=dev, rank=rank,
-                               world=world, unique_id=obj[0])
+        uid = exchange_unique_id(rank)
+        engine = Pk.GradEngine(model, Pk.Strategy(strat), BATCH, device=dev, rank=rank,
+                               world=world, unique_id=uid)
     else:
-        engine = Pk.GradEngine(model, Pk.Strategy.groupconv, BATCH, device=dev)
+        engine = Pk.GradEngine(model, Pk.Strategy(strat), BATCH, device=dev)
     cfg = Pk.DpConfig(CLIP, SIGMA, LR, 1, SEED)
     ccfg = cfg.to_c()
 
-    # synthetic dataset (this rank's shard of the stream: seed + rank)
+    # synthetic dataset (this rank's stream: seed + rank), pinned on the host
     data = Pk.synth_for_model(desc, DATA_N, SEED + rank, pinned=True)
     dx = torch.from_numpy(data.inputs).to(f"cuda:{dev}")
     dy = torch.from_numpy(data.labels).to(f"cuda:{dev}")
@@ -278,50 +331,79 @@ def run_ours(args):
     sub = Pk.Dataset(data.inputs[: e_steps * BATCH], data.labels[: e_steps * BATCH],
                      data.name, e_steps * BATCH, data.classes)
     norms = np.empty(e_steps * BATCH, np.float32)
-    Pk.run_epoch(engine, model, Pk.Dataset(data.inputs[:BATCH * 2], data.labels[:BATCH * 2],
-                                            data.name, BATCH * 2, 10), cfg, 0)  # warm
+    warm = Pk.Dataset(data.inputs[:BATCH * 2], data.labels[:BATCH * 2], data.name, BATCH * 2,
+                      data.classes)
+    Pk.run_epoch(engine, model, warm, cfg, 0)
     barrier()
     w0 = time.perf_counter()
-    secs, _ = Pk.run_epoch(engine, model, sub, cfg, 10 ** 6, norms)
+    Pk.run_epoch(engine, model, sub, cfg, 10 ** 6, norms)
     w1 = time.perf_counter()
     barrier()
     e2e_t = max_over_ranks(w1 - w0)
     e2e = e_steps * BATCH * world / e2e_t
 
-    # ---- dominant kernel: per-kernel event timing of the same schedule -------
+    # ---- per-kernel device time of the same schedule ------------------------
     hbm, bf16, peak_kind = peaks()
     nk = C.c_int32()
     ms = np.zeros(64, np.float32)
     names = C.create_string_buffer(64 * 32)
     _lib.check(_lib.lib.pgb_profile_steps(
         engine.handle, C.c_void_p(dx.data_ptr()), C.c_void_p(dy.data_ptr()), C.byref(ccfg),
-        5 * 10 ** 6, 16, 64, _lib.ptr(ms), names, C.byref(nk)))
+        5 * 10 ** 6, 8, 64, _lib.ptr(ms), names, C.byref(nk)))
     kernels = [(names.raw[32 * k:32 * k + 32].split(b"\0")[0].decode(), float(ms[k]))
                for k in range(nk.value)]
     step_ms = sum(m for _, m in kernels)
-    P = engine.P
-    nb = len(desc.param_shapes)
+    by_name = {}
+    for n, m in kernels:
+        by_name[n] = by_name.get(n, 0.0) + m
+    dom_name, dom_ms = max(by_name.items(), key=lambda kv: kv[1])
+    fused = dom_name == "mnist_fused" or "mnist_fused" in by_name
     roof = None
-    hbm_kernels = [(n, m) for n, m in kernels if algorithmic(n, BATCH, P, nb)]
-    dom_name, dom_ms = max(kernels, key=lambda km: km[1])
-    if hbm_kernels:
-        hn, hm = max(hbm_kernels, key=lambda km: km[1])
-        ach = algorithmic(hn, BATCH, P, nb) / (hm * 1e-3) / 1e9
-        roof = {"kernel": hn, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "peak_kind": peak_kind,
-                "share_of_step": hm / step_ms if step_ms else None,
-                "avg_launch_us": hm * 1e3}
+    if dom_name == "mnist_fused":
+        # fp32 CUDA-core kernel: algorithmic FLOPs / time
+        flops = MFLOP * 1e6 * BATCH
+        ach = flops / (dom_ms * 1e-3) / 1e12
+        fp32_peak = 148 * 128 * 2 * (clocks.max_mhz or 1965) * 1e6 / 1e12
+        roof = {"kernel": dom_name, "bound": "tensor", "achieved": ach, "peak": bf16,
+                "unit": "TFLOP/s", "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
+                "engine": "fp32 FFMA on CUDA cores (per-example GEMMs too small for tcgen05 "
+                          "tiles, DESIGN.md)",
+                "fp32_simt_peak_tflops": fp32_peak, "frac_of_fp32_simt_peak": ach / fp32_peak,
+                "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
+    elif dom_name.endswith("_tc"):
+        tc_ms = sum(m for n, m in by_name.items() if n.endswith("_tc"))
+        flops = conv_gemm_flops(desc, BATCH)
+        ach = flops / (tc_ms * 1e-3) / 1e12
+        roof = {"kernel": "conv GEMMs on tcgen05 (" + ", ".join(
+                    n for n in by_name if n.endswith("_tc")) + ")",
+                "bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
+                "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
+                "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once)",
+                "share_of_step": tc_ms / step_ms, "avg_launch_us": tc_ms * 1e3}
+    if "aggregate" in by_name:
+        agg_b = aggregate_bytes(desc, BATCH, fused)
+        am = by_name["aggregate"]
+        agg = {"kernel": "aggregate", "bound": "hbm", "achieved": agg_b / (am * 1e-3) / 1e9,
+               "peak": hbm, "unit": "GB/s", "frac": agg_b / (am * 1e-3) / 1e9 / hbm,
+               "traffic": None, "algorithmic_bytes": agg_b, "share_of_step": am / step_ms,
+               "avg_launch_us": am * 1e3}
+        if roof is None:
+            roof = agg
+    else:
+        agg = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
                 import oracle
                 if oracle.ref_available():
-                    v, nst, tt = cpu_reference(args.ref_steps, 1, 2, args.ref_seconds)
+                    v, nst, tt = cpu_reference(args.model, args.ref_steps, 1, 1,
+                                               args.ref_seconds)
                     cpu = {"value": v, "unit": UNIT, "cores": 2, "kind": "reference",
-                           "sample": f"{nst[0]} reference dpsgd_step calls (B=256, groupconv, "
-                                     f"graph mode, fp32; {nst[0] * BATCH} examples) in 1 "
-                                     f"process, {tt:.1f} s; host nproc={os.cpu_count()}"}
+                           "sample": f"{nst[0]} reference dpsgd_step calls (B={BATCH}, graph "
+                                     f"mode, fp32; {nst[0] * BATCH} examples) in 1 process, "
+                                     f"{tt:.1f} s; the reference uses 2 threads; host "
+                                     f"nproc={os.cpu_count()}"}
             except Exception as e:  # pragma: no cover
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                        "sample": f"unavailable: {e}"}
@@ -331,15 +413,14 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (bit-identical to io::synth_for_model, seed 0+rank); random-init "
                     "params (models::build seed 0)",
-            "config": workload_config(world),
+            "config": workload_config(args.model, world),
             "e2e": {"value": e2e, "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * row * 4 + BATCH * 4,
                     "d2h_bytes_per_step": BATCH * 4 + 8,
                     "api": "pgb_run_epoch (pinned host batches, per-step H2D + D2H)"},
             "roofline": roof,
-            "dominant_kernel": {"name": dom_name, "avg_us": dom_ms * 1e3,
-                                "share_of_step": dom_ms / step_ms if step_ms else None},
-            "kernels_us": {n: round(m * 1e3, 3) for n, m in kernels},
+            "aggregate_roofline": agg,
+            "kernels_us": {n: round(m * 1e3, 3) for n, m in by_name.items()},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": kps * args.steps,
@@ -357,6 +438,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="mnist_cnn", choices=sorted(MODELS))
     ap.add_argument("--ref-steps", type=int, default=200)
     ap.add_argument("--ref-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

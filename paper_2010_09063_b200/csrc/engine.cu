@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "mnist_fused.cuh"
 #include "tc.cuh"
+#include "conv_tc.cuh"
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -117,6 +118,7 @@ struct Engine {
   int nparts = 1;        // fp64 norm partials per example
   bool norms_fused = false;  // per-example norms produced by the gradient kernel
   bool fused_mnist = false;  // whole per-example pass in one kernel
+  bool use_tc = true;        // conv GEMMs on tcgen05 (PGB_NO_TC=1: CUDA-core tiles)
   std::vector<int64_t> param_off;
   int64_t P = 0;
   int64_t in_row = 0;
@@ -246,6 +248,7 @@ struct Engine {
     P = param_off[desc.n_params];
     in_row = s[0].numel();
     fused_mnist = is_mnist(desc) && std::getenv("PGB_NO_FUSED") == nullptr;
+    use_tc = std::getenv("PGB_NO_TC") == nullptr;
   }
 
   void allocate() {
@@ -485,10 +488,17 @@ struct Engine {
           ConvGeom g{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
                      (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride, (int)sp.pad};
           const int K = g.C * g.k * g.k;
-          ConvFwdOp op{g.D, Bi * g.Ho * g.Wo, K, g, in, W, W + (size_t)g.D * K, L.act_out,
-                       L.fused_relu ? 1 : 0};
-          launch_gemm(op, 1, s);
-          nk += mark(s, "conv_fwd");
+          if (use_tc) {
+            tc::TcConvFwdOp op{Bi * g.Ho * g.Wo, g.D, K, g, in, W, W + (size_t)g.D * K,
+                               L.act_out, L.fused_relu ? 1 : 0};
+            tc::launch(op, 1, s);
+            nk += mark(s, "conv_fwd_tc");
+          } else {
+            ConvFwdOp op{g.D, Bi * g.Ho * g.Wo, K, g, in, W, W + (size_t)g.D * K, L.act_out,
+                         L.fused_relu ? 1 : 0};
+            launch_gemm(op, 1, s);
+            nk += mark(s, "conv_fwd");
+          }
           break;
         }
         case PGB_MAXPOOL:
@@ -597,13 +607,29 @@ struct Engine {
           const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
           float* sW = d_stacks + param_off[L.pblock] * B;
           float* sb = d_stacks + param_off[L.pblock + 1] * B;
-          ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
-          launch_gemm(dw, Bi, s);
-          nk += mark(s, "conv_dw_pex");
+          if (use_tc) {
+            tc::TcConvDWOp dw{K, gg.D, Pp, gg, in, gcur, sW};
+            tc::launch(dw, Bi, s);
+            nk += mark(s, "conv_dw_pex_tc");
+          } else {
+            ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
+            launch_gemm(dw, Bi, s);
+            nk += mark(s, "conv_dw_pex");
+          }
           conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
                                                                          sb);
           nk += mark(s, "conv_db_pex");
-          if (L.needs_gx) {
+          if (L.needs_gx && use_tc && gg.stride == 1) {
+            tc::TcConvBwdXS1Op op{Bi * gg.H * gg.W, gg.C, gg.D * gg.k * gg.k, gg, gcur, W,
+                                  L.bwd_mask, gnext};
+            tc::launch(op, 1, s);
+            nk += mark(s, "conv_bwd_x_tc");
+          } else if (L.needs_gx && use_tc) {
+            tc::TcConvBwdXOp op{Bi * gg.H * gg.W, gg.C, gg.D * gg.k * gg.k, gg, gcur, W,
+                                L.bwd_mask, gnext};
+            tc::launch(op, 1, s);
+            nk += mark(s, "conv_bwd_x_tc");
+          } else if (L.needs_gx) {
             ConvBwdXOp op{gg.C, Bi * gg.H * gg.W, gg.D * gg.k * gg.k, gg, gcur, W,
                           L.bwd_mask, gnext};
             launch_gemm(op, 1, s);
@@ -1239,10 +1265,10 @@ pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, co
     tc::PlainOp op{M, N, K, dA, dB, dC};
     constexpr int BN = 64;
     const size_t smem = tc::tc_smem_bytes<tc::PlainOp, BN>();
-    PGB_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<tc::PlainOp, BN>,
+    PGB_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<tc::PlainOp, BN, 128>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((N + BN - 1) / BN, (M + tc::kBM - 1) / tc::kBM, 1);
-    tc::tc_gemm_kernel<tc::PlainOp, BN><<<grid, tc::kThreads, smem>>>(op);
+    tc::tc_gemm_kernel<tc::PlainOp, BN, 128><<<grid, 128, smem>>>(op);
     PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaDeviceSynchronize());
     PGB_CUDA(cudaMemcpy(Cout, dC, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost));

@@ -125,32 +125,42 @@ __device__ __forceinline__ int canon_off(int r, int k) {
 // Generic tcgen05 GEMM with gathered operands:
 //   C[z][m][n] = sum_k A(z,m,k) * B(z,n,k)       (then op.store)
 // BM = 128 rows per CTA (UMMA_M = 128, one accumulator row per TMEM lane),
-// BN columns (multiple of 16, <= 256), BK = 32 per pipeline stage, 2 stages.
-// 128 threads: all gather (fp32 -> hi/lo tf32 in canonical layout), thread 0
-// issues 4 k-steps x 3 MMAs per stage and commits to the stage's mbarrier,
-// the gather of the next stage overlaps the tensor core; epilogue reads the
-// accumulator from TMEM with tcgen05.ld.
+// BN columns (multiple of 16, <= 128), BK = 32 per pipeline stage, 2 stages.
+// NT threads all gather (fp32 -> hi/lo tf32 in the canonical layout); thread
+// 0 issues 4 k-steps x 3 MMAs per stage and commits to the stage's mbarrier,
+// so the gather of the next stage overlaps the tensor core. Three TMEM
+// accumulators (hi.hi even/odd chunks + the hi.lo/lo.hi correction) keep the
+// fp32 accumulation chains short. Epilogue: tcgen05.ld TMEM -> registers.
+//
+// Ops with kTableA gather A as an implicit im2col window:
+//   A(m,k) = src[row.base + k.base + (row.iy + k.dy) * W + (row.ix + k.dx)]
+// (zero outside [0,H) x [0,W)), with per-row info computed once per CTA and
+// per-k info once per K chunk -- a few integer ops per element.
 // ---------------------------------------------------------------------------
-constexpr int kBM = 128, kBK = 32, kThreads = 128;
+constexpr int kBM = 128, kBK = 32;
 
 template <int BN>
 struct TcSmem {
   float ahi[2][kBM * kBK], alo[2][kBM * kBK];
   float bhi[2][BN * kBK], blo[2][BN * kBK];
+  int4 rowinfo[kBM];
+  int4 kinfo[2][kBK];
   uint64_t bar[2];
   uint32_t tmem;
 };
 
-template <class Op, int BN>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(Op op) {
+struct NoTable {
+  static constexpr bool kTableA = false;
+};
+
+template <class Op, int BN, int NT>
+__global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
   extern __shared__ __align__(1024) unsigned char raw[];
   TcSmem<BN>& S = *reinterpret_cast<TcSmem<BN>*>(raw);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int z = blockIdx.z;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
   const int M = op.M, N = op.N, K = op.K;
-  // three accumulators: hi.hi for even / odd K chunks, and the small
-  // hi.lo + lo.hi correction -- shorter fp32 accumulation chains in TMEM
   constexpr uint32_t kCols = 3 * BN <= 32 ? 32 : 3 * BN <= 64 ? 64 : 3 * BN <= 128 ? 128
                              : 3 * BN <= 256 ? 256 : 512;
   static_assert(3 * BN <= 512, "BN too large for three TMEM accumulators");
@@ -160,30 +170,54 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(Op op) {
     mbar_init(&S.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if constexpr (Op::kTableA) {
+    for (int r = t; r < kBM; r += NT) S.rowinfo[r] = op.row_info(z, m0 + r);
+  }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = S.tmem;
   constexpr uint32_t idesc = idesc_tf32(kBM, BN);
   const int nk = (K + kBK - 1) / kBK;
+  int H = 0, Wd = 0;
+  const float* src = nullptr;
+  if constexpr (Op::kTableA) {
+    H = op.img_h();
+    Wd = op.img_w();
+    src = op.img(z);
+  }
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
-    if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
     const int k0 = kc * kBK;
+    if constexpr (Op::kTableA) {
+      if (t < kBK) S.kinfo[s][t] = op.k_info(z, k0 + t);
+    }
+    if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
+    if constexpr (Op::kTableA) __syncthreads();
     // gather A: lanes cover one 8x4 core matrix (conflict-free 128 B stores)
-    for (int e = t; e < kBM * kBK; e += kThreads) {
+#pragma unroll 4
+    for (int e = t; e < kBM * kBK; e += NT) {
       const int core = e >> 5, in = e & 31;
       const int r = (core % (kBM / 8)) * 8 + (in >> 2);
       const int k = (core / (kBM / 8)) * 4 + (in & 3);
-      const int m = m0 + r, kk = k0 + k;
-      const float v = (m < M && kk < K) ? op.a(z, m, kk) : 0.0f;
+      float v;
+      if constexpr (Op::kTableA) {
+        const int4 ri = S.rowinfo[r];
+        const int4 ki = S.kinfo[s][k];
+        const int iy = ri.y + ki.y, ix = ri.z + ki.z;
+        const bool ok = (ri.w & ki.w) && (unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)Wd;
+        v = ok ? __ldg(src + ri.x + ki.x + iy * Wd + ix) : 0.0f;
+      } else {
+        const int m = m0 + r, kk = k0 + k;
+        v = (m < M && kk < K) ? op.a(z, m, kk) : 0.0f;
+      }
       float hi, lo;
       split_tf32(v, hi, lo);
       const int o = canon_off<kBK>(r, k);
       S.ahi[s][o] = hi;
       S.alo[s][o] = lo;
     }
-    for (int e = t; e < BN * kBK; e += kThreads) {
+    for (int e = t; e < BN * kBK; e += NT) {
       const int core = e >> 5, in = e & 31;
       const int r = (core % (BN / 8)) * 8 + (in >> 2);
       const int k = (core / (BN / 8)) * 4 + (in & 3);
@@ -219,10 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(Op op) {
   // all MMAs done once the last commit lands (they complete in issue order)
   mbar_wait(&S.bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
   fence_after_sync();
-  const int row = m0 + warp * 32 + lane;
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  // warp w reads TMEM lanes 32(w%4).. ; warps >= 4 take the upper column half
+  constexpr int kGroups = NT / 128;
+  const int row = m0 + (warp & 3) * 32 + lane;
+  const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int cbeg = (warp >> 2) * (BN / kGroups), cend = cbeg + BN / kGroups;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 8) {
+  for (int c0 = cbeg; c0 < cend; c0 += 8) {
     float v[8], v1[8], vc[8];
     tmem_ld8(lane_base + (uint32_t)c0, v);
     tmem_ld8(lane_base + (uint32_t)(2 * BN + c0), vc);
@@ -251,6 +288,7 @@ inline size_t tc_smem_bytes() {
 
 // Plain row-major test GEMM: C (M x N) = A (M x K) . B (N x K)^T.
 struct PlainOp {
+  static constexpr bool kTableA = false;
   int M, N, K;
   const float* A;
   const float* Bm;

@@ -1,0 +1,307 @@
+// pegrad_b200.hpp -- the reference's C++ API shapes over the C ABI.
+//
+// A pegrad user (proj/core/include/pegrad/{models,strategies,dpsgd}.hpp)
+// switches by including this header and linking libpegrad_b200.so:
+//
+//   pegrad::models::build<float>(kind, seed)        -> pegrad_b200::models::build(kind, seed)
+//   pegrad::GradEngine<float>(model, s, B, graph)   -> pegrad_b200::GradEngine(model, s, B)
+//   pegrad::dpsgd_step(model, engine, x, y, cfg, i) -> pegrad_b200::dpsgd_step(...)  (same
+//                                                      argument meaning, StepReport, errors)
+//   pegrad::io::synth_for_model<float>(desc, n, s)  -> pegrad_b200::io::synth_for_model(...)
+//
+// Header-only; every call goes through include/pegrad_b200.h. Status codes
+// are rethrown as the reference's exception types (common.hpp:56-114).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pegrad_b200.h"
+
+namespace pegrad_b200 {
+
+// ---- errors: pegrad::Error hierarchy ------------------------------------------
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error { using Error::Error; };
+struct DomainError : Error { using Error::Error; };
+struct IndexError : Error { using Error::Error; };
+struct ConfigError : Error { using Error::Error; };
+struct ContractError : Error { using Error::Error; };
+struct UnsupportedError : Error { using Error::Error; };
+struct TraceError : Error { using Error::Error; };
+struct FormatError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct CudaError : Error { using Error::Error; };
+struct NcclError : Error { using Error::Error; };
+struct OutOfMemoryError : Error { using Error::Error; };
+
+inline void check(pgb_status s) {
+  if (s == PGB_OK) return;
+  const std::string m = pgb_last_error();
+  switch (s) {
+    case PGB_ERR_SHAPE: throw ShapeError(m);
+    case PGB_ERR_DOMAIN: throw DomainError(m);
+    case PGB_ERR_INDEX: throw IndexError(m);
+    case PGB_ERR_CONFIG: throw ConfigError(m);
+    case PGB_ERR_CONTRACT: throw ContractError(m);
+    case PGB_ERR_UNSUPPORTED: throw UnsupportedError(m);
+    case PGB_ERR_TRACE: throw TraceError(m);
+    case PGB_ERR_FORMAT: throw FormatError(m);
+    case PGB_ERR_IO: throw IoError(m);
+    case PGB_ERR_CUDA: throw CudaError(m);
+    case PGB_ERR_NCCL: throw NcclError(m);
+    case PGB_ERR_OOM: throw OutOfMemoryError(m);
+    default: throw Error(m);
+  }
+}
+
+// ---- models (models.hpp:24-88) ---------------------------------------------------
+namespace models {
+
+enum class ModelKind { logreg = 0, fcnn, mnist_cnn, cifar_cnn, embed, lstm };
+enum class LayerKind {
+  dense = 0, conv, maxpool, avgpool, global_avgpool, flatten, relu, embedding, seq_avgpool, lstm
+};
+
+struct LayerSpec {
+  LayerKind kind;
+  int64_t in = 0, out = 0, k = 0, stride = 1, pad = 0;
+};
+
+struct ModelOptions {
+  int64_t seq_len = -1, vocab = -1, hidden = -1;
+};
+
+struct ModelDesc {
+  pgb_model_desc c{};
+  ModelKind kind() const { return static_cast<ModelKind>(c.model_kind); }
+  int64_t classes() const { return c.classes; }
+  std::vector<int64_t> input_shape() const {
+    return std::vector<int64_t>(c.input_shape, c.input_shape + c.input_rank);
+  }
+  std::vector<LayerSpec> layers() const {
+    std::vector<LayerSpec> v;
+    for (int i = 0; i < c.n_layers; ++i) {
+      const pgb_layer_spec& l = c.layers[i];
+      v.push_back({static_cast<LayerKind>(l.kind), l.in, l.out, l.k, l.stride, l.pad});
+    }
+    return v;
+  }
+  int n_params() const { return c.n_params; }
+  int64_t param_size(int p) const { return c.param_size[p]; }
+  int64_t param_count() const { return pgb_param_count(&c); }
+  int64_t input_numel() const {
+    int64_t n = 1;
+    for (int i = 0; i < c.input_rank; ++i) n *= c.input_shape[i];
+    return n;
+  }
+};
+
+inline ModelDesc build_desc(ModelKind kind, const ModelOptions& o = {}) {
+  ModelDesc d;
+  pgb_model_options co{o.seq_len, o.vocab, o.hidden};
+  check(pgb_build_desc(static_cast<int32_t>(kind), &co, &d.c));
+  return d;
+}
+
+// A custom layer list (e.g. the 104-50-2 FFNN of BASELINE config 2).
+inline ModelDesc custom_desc(ModelKind kind, const std::vector<LayerSpec>& layers,
+                             const std::vector<int64_t>& input_shape, int64_t classes,
+                             bool token_input = false) {
+  ModelDesc d;
+  if (layers.size() > PGB_MAX_LAYERS || input_shape.size() > 3)
+    throw ConfigError("custom_desc: too many layers or input dimensions");
+  d.c.model_kind = static_cast<int32_t>(kind);
+  d.c.n_layers = static_cast<int32_t>(layers.size());
+  for (size_t i = 0; i < layers.size(); ++i)
+    d.c.layers[i] = {static_cast<int32_t>(layers[i].kind), layers[i].in, layers[i].out,
+                     layers[i].k, layers[i].stride, layers[i].pad};
+  d.c.input_rank = static_cast<int32_t>(input_shape.size());
+  for (size_t i = 0; i < input_shape.size(); ++i) d.c.input_shape[i] = input_shape[i];
+  d.c.classes = classes;
+  d.c.token_input = token_input ? 1 : 0;
+  check(pgb_finish_desc(&d.c));
+  return d;
+}
+
+// models::Model<float>: parameters in registry order, one flat block each.
+struct Model {
+  ModelDesc desc;
+  std::vector<std::vector<float>> params;
+  std::vector<float> flat() const {
+    std::vector<float> f;
+    for (const auto& p : params) f.insert(f.end(), p.begin(), p.end());
+    return f;
+  }
+  void set_flat(const std::vector<float>& f) {
+    size_t o = 0;
+    for (auto& p : params) {
+      std::copy(f.begin() + o, f.begin() + o + p.size(), p.begin());
+      o += p.size();
+    }
+  }
+};
+
+inline Model build_from_desc(const ModelDesc& d, uint64_t seed) {
+  Model m;
+  m.desc = d;
+  std::vector<float> flat(d.param_count());
+  check(pgb_init_params(&d.c, seed, flat.data()));
+  for (int p = 0, o = 0; p < d.n_params(); ++p) {
+    m.params.emplace_back(flat.begin() + o, flat.begin() + o + d.param_size(p));
+    o += static_cast<int>(d.param_size(p));
+  }
+  return m;
+}
+
+inline Model build(ModelKind kind, uint64_t seed, const ModelOptions& o = {}) {
+  return build_from_desc(build_desc(kind, o), seed);
+}
+
+}  // namespace models
+
+// ---- strategies / engine (strategies.hpp:34-100) -----------------------------------
+enum class Strategy { naive = 0, vmap, outer, norms, groupconv, jacmm };
+enum class ExecMode { eager = 0, graph };
+
+template <typename T = float>
+struct DpConfig {  // dpsgd.hpp:24-31
+  T clip_norm = T(1);
+  T noise_multiplier = T(0);
+  T learning_rate = T(0.1);
+  int64_t microbatch = 1;
+  uint64_t seed = 0;
+};
+
+struct StepReport {  // dpsgd.hpp:36-41
+  std::vector<float> pre_clip_norms;
+  int64_t clipped_count = 0;
+  std::vector<uint64_t> noise_streams;
+};
+
+class GradEngine {
+ public:
+  GradEngine(const models::Model& model, Strategy strategy, int64_t batch,
+             ExecMode mode = ExecMode::graph, int device = 0)
+      : batch_(batch), strategy_(strategy) {
+    pgb_engine* h = nullptr;
+    check(pgb_engine_create(&model.desc.c, static_cast<int32_t>(strategy), batch, device, &h));
+    h_.reset(h);
+    check(pgb_engine_set_graph(h, mode == ExecMode::graph ? 1 : 0));
+    upload(model);
+  }
+  int64_t batch() const { return batch_; }
+  Strategy strategy() const { return strategy_; }
+  pgb_engine* handle() const { return h_.get(); }
+  void upload(const models::Model& m) {
+    const std::vector<float> f = m.flat();
+    check(pgb_set_params(h_.get(), f.data()));
+  }
+  void download(models::Model& m) const {
+    std::vector<float> f(m.desc.param_count());
+    check(pgb_get_params(h_.get(), f.data()));
+    m.set_flat(f);
+  }
+  int64_t footprint_bytes() const {
+    pgb_engine_info info{};
+    check(pgb_engine_info_get(h_.get(), &info));
+    return info.workspace_bytes;
+  }
+
+ private:
+  struct Del {
+    void operator()(pgb_engine* e) const { pgb_engine_destroy(e); }
+  };
+  std::unique_ptr<pgb_engine, Del> h_;
+  int64_t batch_;
+  Strategy strategy_;
+};
+
+inline void validate(const DpConfig<float>& cfg, int64_t batch) {  // dpsgd.cpp:36-51
+  if (!(cfg.clip_norm > 0.0f)) throw ConfigError("DpConfig: clip norm must be positive");
+  if (cfg.noise_multiplier < 0.0f)
+    throw ConfigError("DpConfig: noise multiplier must be non-negative");
+  if (!(cfg.learning_rate > 0.0f)) throw ConfigError("DpConfig: learning rate must be positive");
+  if (cfg.microbatch < 1 || batch % cfg.microbatch != 0)
+    throw ConfigError("DpConfig: microbatch size " + std::to_string(cfg.microbatch) +
+                      " must divide the batch size " + std::to_string(batch));
+}
+
+// dpsgd_step (dpsgd.hpp:70-73): x is batch*numel(input) floats, y batch
+// floats. The device keeps the parameters; with sync_params (default, the
+// reference's contract) model.params are refreshed after the step.
+inline StepReport dpsgd_step(models::Model& model, GradEngine& engine, const float* x,
+                             const float* y, const DpConfig<float>& cfg, int64_t step_index,
+                             bool sync_params = true) {
+  validate(cfg, engine.batch());
+  StepReport rep;
+  rep.pre_clip_norms.resize(engine.batch() / cfg.microbatch);
+  pgb_dp_config c{cfg.clip_norm, cfg.noise_multiplier, cfg.learning_rate, cfg.microbatch,
+                  cfg.seed};
+  pgb_step_report r{};
+  check(pgb_dpsgd_step(engine.handle(), x, y, &c, step_index, rep.pre_clip_norms.data(), &r));
+  rep.clipped_count = r.clipped_count;
+  rep.noise_streams.assign(r.noise_streams, r.noise_streams + r.n_streams);
+  if (sync_params) engine.download(model);
+  return rep;
+}
+
+inline StepReport dpsgd_step(models::Model& model, GradEngine& engine,
+                             const std::vector<float>& x, const std::vector<float>& y,
+                             const DpConfig<float>& cfg, int64_t step_index,
+                             bool sync_params = true) {
+  if ((int64_t)y.size() != engine.batch() ||
+      (int64_t)x.size() != engine.batch() * model.desc.input_numel())
+    throw ContractError("GradEngine: batch extent mismatch (engine built for " +
+                        std::to_string(engine.batch()) + ")");
+  return dpsgd_step(model, engine, x.data(), y.data(), cfg, step_index, sync_params);
+}
+
+// sgd_step (dpsgd.hpp:76-78)
+inline void sgd_step(models::Model& model, GradEngine& engine, const std::vector<float>& x,
+                     const std::vector<float>& y, float learning_rate, bool sync_params = true) {
+  check(pgb_sgd_step(engine.handle(), x.data(), y.data(), learning_rate));
+  if (sync_params) engine.download(model);
+}
+
+// ---- data (dataset.hpp:36-69) -----------------------------------------------------
+namespace io {
+struct Dataset {
+  std::vector<float> inputs, labels;
+  int64_t count = 0;
+};
+inline Dataset synth_for_model(const models::ModelDesc& d, int64_t n, uint64_t seed) {
+  Dataset ds;
+  ds.count = n;
+  ds.inputs.resize(n * d.input_numel());
+  ds.labels.resize(n);
+  check(pgb_synth(&d.c, n, seed, ds.inputs.data(), ds.labels.data()));
+  return ds;
+}
+}  // namespace io
+
+// ---- epoch driver (harness.hpp:75-80): N/B sequential slices ----------------------
+namespace bench {
+struct EpochResult {
+  double seconds = 0;
+  int64_t clipped_total = 0;
+};
+inline EpochResult run_epoch(models::Model& model, GradEngine& engine, const io::Dataset& data,
+                             const DpConfig<float>& cfg, int64_t step0) {
+  pgb_dp_config c{cfg.clip_norm, cfg.noise_multiplier, cfg.learning_rate, cfg.microbatch,
+                  cfg.seed};
+  EpochResult r;
+  check(pgb_run_epoch(engine.handle(), data.inputs.data(), data.labels.data(), data.count, &c,
+                      step0, nullptr, &r.clipped_total, &r.seconds));
+  engine.download(model);
+  return r;
+}
+}  // namespace bench
+
+}  // namespace pegrad_b200

@@ -1,0 +1,113 @@
+// Reference-style C++ test of the drop-in shim (include/pegrad_b200.hpp),
+// mirroring proj/tests/test_dpsgd.cpp's contracts on the GPU engine:
+// config validation, StepReport fields, noise streams, determinism of
+// identical seeds, sigma=0 + loose C == plain SGD, label IndexError and the
+// strategy support matrix. Prints "OK" and exits 0 on success.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "pegrad_b200.hpp"
+
+using namespace pegrad_b200;
+
+#define CHECK(cond)                                                  \
+  do {                                                               \
+    if (!(cond)) {                                                   \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      std::exit(1);                                                  \
+    }                                                                \
+  } while (0)
+
+template <typename E, typename F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main() {
+  using models::ModelKind;
+  const int64_t B = 16;
+  // parameter counts (test_models.cpp:26-35)
+  CHECK(models::build_desc(ModelKind::mnist_cnn).param_count() == 26010);
+  CHECK(models::build_desc(ModelKind::cifar_cnn).param_count() == 605226);
+
+  auto model = models::build(ModelKind::mnist_cnn, 0);
+  auto data = io::synth_for_model(model.desc, B, 0);
+  GradEngine engine(model, Strategy::groupconv, B);
+
+  // config validation (test_dpsgd.cpp:285-296)
+  DpConfig<float> bad;
+  bad.clip_norm = 0;
+  CHECK(throws<ConfigError>([&] { dpsgd_step(model, engine, data.inputs, data.labels, bad, 0); }));
+  bad.clip_norm = 1;
+  bad.microbatch = 3;
+  CHECK(throws<ConfigError>([&] { dpsgd_step(model, engine, data.inputs, data.labels, bad, 0); }));
+
+  // a noisy step: report fields and noise stream ids (dpsgd.cpp:27-32)
+  DpConfig<float> cfg;
+  cfg.clip_norm = 1.0f;
+  cfg.noise_multiplier = 1.1f;
+  cfg.learning_rate = 0.1f;
+  auto rep = dpsgd_step(model, engine, data.inputs, data.labels, cfg, 7);
+  CHECK((int64_t)rep.pre_clip_norms.size() == B);
+  int64_t above = 0;
+  for (float n : rep.pre_clip_norms) {
+    CHECK(std::isfinite(n) && n > 0);
+    above += n > cfg.clip_norm;
+  }
+  CHECK(rep.clipped_count == above);
+  CHECK((int)rep.noise_streams.size() == model.desc.n_params());
+  CHECK(rep.noise_streams[0] == (uint64_t(1) << 32) + 7 * 4096);
+
+  // identical seeds -> identical trajectories (test_dpsgd.cpp:263-283)
+  auto a = models::build(ModelKind::mnist_cnn, 1);
+  auto b = models::build(ModelKind::mnist_cnn, 1);
+  GradEngine ea(a, Strategy::groupconv, B), eb(b, Strategy::groupconv, B);
+  for (int s = 0; s < 3; ++s) {
+    dpsgd_step(a, ea, data.inputs, data.labels, cfg, s);
+    dpsgd_step(b, eb, data.inputs, data.labels, cfg, s);
+  }
+  CHECK(a.flat() == b.flat());
+
+  // sigma = 0 and a loose C is plain SGD (test_dpsgd.cpp:204-226)
+  auto c = models::build(ModelKind::fcnn, 11);
+  auto d = models::build(ModelKind::fcnn, 11);
+  auto fd = io::synth_for_model(c.desc, 8, 3);
+  GradEngine ec(c, Strategy::vmap, 8), ed(d, Strategy::vmap, 8);
+  DpConfig<float> loose;
+  loose.clip_norm = 1e6f;
+  loose.noise_multiplier = 0.0f;
+  loose.learning_rate = 0.5f;
+  auto r2 = dpsgd_step(c, ec, fd.inputs, fd.labels, loose, 0);
+  CHECK(r2.clipped_count == 0 && r2.noise_streams.empty());
+  sgd_step(d, ed, fd.inputs, fd.labels, 0.5f);
+  const auto fc = c.flat(), fdd = d.flat();
+  for (size_t i = 0; i < fc.size(); ++i)
+    CHECK(std::fabs(fc[i] - fdd[i]) <= 1e-6f * (1.0f + std::fabs(fdd[i])));
+
+  // labels outside [0, classes) are an IndexError; parameters untouched
+  auto before = model.flat();
+  auto badlab = data.labels;
+  badlab[3] = 12.0f;
+  CHECK(throws<IndexError>([&] { dpsgd_step(model, engine, data.inputs, badlab, cfg, 8); }));
+  engine.download(model);
+  CHECK(model.flat() == before);
+
+  // the strategy support matrix (strategies.cpp:76-113)
+  CHECK(throws<UnsupportedError>([&] { GradEngine bad_e(model, Strategy::outer, B); }));
+
+  // one epoch driver pass (harness.cpp:85-167 shape)
+  auto ep = io::synth_for_model(model.desc, 4 * B, 5);
+  auto res = bench::run_epoch(model, engine, ep, cfg, 100);
+  CHECK(res.seconds > 0 && res.clipped_total >= 0);
+  std::printf("OK\n");
+  return 0;
+}

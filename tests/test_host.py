@@ -139,3 +139,14 @@ def test_shard_bounds():
                                                            (192, 256)]
     with pytest.raises(ValueError):
         shard_bounds(0, 3, 256)
+
+
+def test_cpp_shim_header_compiles_and_links():
+    """include/pegrad_b200.hpp + the C ABI link against the product .so."""
+    import subprocess
+    import tempfile
+    libdir = os.path.join(ROOT, "paper_2010_09063_b200")
+    with tempfile.TemporaryDirectory() as d:
+        subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "test_shim.cpp"), "-L", libdir,
+                        "-lpegrad_b200", "-o", os.path.join(d, "t")], check=True)

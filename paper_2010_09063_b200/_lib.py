@@ -11,7 +11,9 @@ import os
 from . import errors
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "libpegrad_b200.so")
+# PGB_LIBRARY: an alternative build of the same library (e.g. the PGB_TRACE
+# timestamp build used by scripts/trace_phases.py)
+SO = os.environ.get("PGB_LIBRARY") or os.path.join(PKG, "libpegrad_b200.so")
 
 MAX_LAYERS = 32
 MAX_PARAMS = 64

@@ -32,13 +32,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _nvcc_cmd(out: str, verbose: bool):
+    return [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+            "-Xcompiler", "-fPIC,-O3", "-shared", "-I", os.path.join(ROOT, "include"),
+            "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3",
+            *[os.path.join(CSRC, s) for s in SOURCES], "-o", out, "-ldl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    if os.environ.get("PGB_TRACE"):
+        return build_trace(verbose)
     if not force and not _stale():
         return OUT
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-           "-Xcompiler", "-fPIC,-O3", "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3",
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp", "-ldl"]
+    cmd = _nvcc_cmd(OUT + ".tmp", verbose)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -47,6 +53,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stderr)
     os.replace(OUT + ".tmp", OUT)
     return OUT
+
+
+TRACE_OUT = os.path.join(PKG, "libpegrad_b200_trace.so")
+
+
+def build_trace(verbose: bool = False) -> str:
+    """The same library with device phase timestamps (-DPGB_TRACE), written
+    beside the product build; load it with PGB_LIBRARY=<path>."""
+    cmd = _nvcc_cmd(TRACE_OUT + ".tmp", verbose) + ["-DPGB_TRACE"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building the trace library")
+    os.replace(TRACE_OUT + ".tmp", TRACE_OUT)
+    return TRACE_OUT
 
 
 if __name__ == "__main__":

@@ -142,24 +142,31 @@ struct Engine {
   float* d_sum = nullptr;
   int* d_clipped = nullptr;
   DevError* d_err = nullptr;
-  StepArgs* d_args = nullptr;
   // fused MNIST factors
   float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
   float* d_w2t = nullptr;  // conv2 weights kept transposed [k][d] for the fused kernel
   std::vector<float*> d_dense_g;  // per dense layer: output cotangent (B, out)
 
   // pinned host staging
-  static constexpr int kArgSlots = 64;
-  StepArgs* h_args = nullptr;
-  cudaEvent_t slot_ev[kArgSlots];
-  bool slot_used[kArgSlots] = {};
-  int64_t arg_counter = 0;
+  StepArgs cur_args{};  // the step's DP arguments, passed by value to the kernels
   float* h_norms = nullptr;
   int* h_clipped = nullptr;
   DevError* h_err = nullptr;
 
   bool graph_enabled = true;
-  std::map<int, cudaGraphExec_t> graphs;  // key: schedule variant
+  // One CUDA graph per schedule variant. Per-step arguments reach the graph as
+  // kernel-node parameter updates (the aggregation / noise-update launch
+  // structs, and the fused MNIST kernel's input pointers), so a replay needs
+  // no host-to-device copy on the stream.
+  struct StepGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t agg = nullptr, noise = nullptr, fused = nullptr;
+    AggLaunch agg_args{};
+    NoiseLaunch noise_args{};
+    mnist::Params fused_args{};
+  };
+  std::map<int, StepGraph> graphs;  // key: schedule variant
   int kernels_last = 0;
   pgb_dp_config last_cfg{};
   int64_t last_step = 0;
@@ -167,12 +174,10 @@ struct Engine {
   ~Engine() {
     if (device >= 0) cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-    for (int i = 0; i < kArgSlots; ++i)
-      if (slot_ev[i]) cudaEventDestroy(slot_ev[i]);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : graphs) cudaGraphDestroy(kv.second.graph);
     if (comm) Nccl::get().commDestroy(comm);
     if (arena) cudaFree(arena);
-    if (h_args) cudaFreeHost(h_args);
     if (h_norms) cudaFreeHost(h_norms);
     if (h_clipped) cudaFreeHost(h_clipped);
     if (h_err) cudaFreeHost(h_err);
@@ -276,7 +281,6 @@ struct Engine {
     want((void**)&d_sum, sizeof(float) * (P + 2));
     want((void**)&d_clipped, sizeof(int) * 2);
     want((void**)&d_err, sizeof(DevError));
-    want((void**)&d_args, sizeof(StepArgs));
     if (fused_mnist) {
       want((void**)&d_a2, sizeof(float) * B * 512);
       want((void**)&d_dz1, sizeof(float) * B * 32);
@@ -426,12 +430,23 @@ struct Engine {
     PGB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     allocate();
-    PGB_CUDA(cudaMallocHost(&h_args, sizeof(StepArgs) * kArgSlots));
     PGB_CUDA(cudaMallocHost(&h_norms, sizeof(float) * B));
     PGB_CUDA(cudaMallocHost(&h_clipped, sizeof(int) * 2));
     PGB_CUDA(cudaMallocHost(&h_err, sizeof(DevError)));
-    for (int i = 0; i < kArgSlots; ++i)
-      PGB_CUDA(cudaEventCreateWithFlags(&slot_ev[i], cudaEventDisableTiming));
+    {
+      // process-wide function attribute: allow the largest batch any engine
+      // may use (the opt-in maximum), never a per-engine value
+      int optin = 0;
+      PGB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+      cudaFuncAttributes fa{};
+      PGB_CUDA(cudaFuncGetAttributes(&fa, aggregate_kernel));
+      const int room = optin - (int)fa.sharedSizeBytes;
+      if ((int)agg_smem((int)B) > room)
+        raise(PGB_ERR_OOM, "batch " + std::to_string(B) +
+                               " exceeds the aggregation kernel's shared-memory budget");
+      PGB_CUDA(cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    room));
+    }
     if (fused_mnist)
       PGB_CUDA(cudaFuncSetAttribute(mnist::fused_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -678,8 +693,6 @@ struct Engine {
   // One full DPSGD step: grads -> [microbatch] -> norms/clip/sum/noise/update.
   int enqueue_step(cudaStream_t s, const float* x_slot, const float* y_slot, int64_t m) {
     int nk = 0;
-    PGB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(DevError), s));
-    PGB_CUDA(cudaMemsetAsync(d_clipped, 0, sizeof(int) * 2, s));
     nk += enqueue_grads(s, x_slot, y_slot);
     if (m > 1) {
       const int U = (int)(B / m);
@@ -701,25 +714,67 @@ struct Engine {
     return nk;
   }
 
+  // Tile plan of the aggregation kernel for a block table: materialised
+  // blocks in kAggCols-column tiles, factored dense blocks in kAggRows x 32
+  // tiles. Returns the CTA count.
+  static int agg_plan(const BlockTable& t, AggPlan& plan) {
+    plan.n = t.n;
+    int tiles = 0;
+    for (int p = 0; p < t.n; ++p) {
+      plan.tile_start[p] = tiles;
+      if (t.kind[p] == 0) {
+        tiles += (int)((t.size[p] + kAggCols - 1) / kAggCols);
+      } else {
+        const int64_t out = t.out[p], in = t.size[p] / out;
+        tiles += (int)(((in + kAggRows - 1) / kAggRows) * ((out + 31) / 32));
+      }
+    }
+    plan.tile_start[t.n] = tiles;
+    return tiles;
+  }
+
+  // dynamic shared memory of the aggregation kernel: clip factors + the
+  // per-warp staging of factored rows
+  static size_t agg_smem(int U) {
+    return sizeof(float) * (((U + 3) & ~3) + kAggWarps * kAggChunk * kAggRows);
+  }
+
+  AggLaunch agg_launch(const BlockTable& t, int np, int U, int mode) {
+    AggLaunch L{};
+    L.bt = t;
+    agg_plan(t, L.plan);
+    L.a = cur_args;
+    L.parts = d_parts;
+    L.params = d_params;
+    L.sum_out = d_sum;
+    L.norms_out = d_norms;
+    L.clipped_out = d_clipped;
+    L.err = d_err;
+    L.U = U;
+    L.nparts = np;
+    L.mode = mode;
+    return L;
+  }
+
+  void launch_agg(const AggLaunch& L, cudaStream_t s) {
+    aggregate_kernel<<<L.plan.tile_start[L.plan.n], 32 * kAggWarps, agg_smem(L.U), s>>>(L);
+  }
+
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U) {
     int nk = 0;
-    const int threads = 32 * kChunks;
-    const int grid = (int)std::min<long long>((P + 31) / 32, 148 * 16);
-    const size_t smem = sizeof(float) * U;
     if (world == 1) {
-      aggregate_kernel<16><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, nullptr,
-                                                      d_norms, d_clipped, d_err, 0);
+      launch_agg(agg_launch(t, np, U, 0), s);
       nk += mark(s, "aggregate");
     } else {
-      aggregate_kernel<16><<<grid, threads, smem, s>>>(t, d_parts, np, d_args, d_params, d_sum,
-                                                      d_norms, d_clipped, d_err, 1);
+      launch_agg(agg_launch(t, np, U, 1), s);
       nk += mark(s, "aggregate_local");
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
       PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
       PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
       PGB_NCCL(N.groupEnd());
-      noise_update_kernel<<<grid_for((size_t)P), 256, 0, s>>>(d_sum, t, d_args, d_params, d_err);
+      NoiseLaunch L{t, cur_args, d_sum, d_params, d_err};
+      noise_update_kernel<<<grid_for((size_t)P), 256, 0, s>>>(L);
       nk += mark(s, "noise_update");
     }
     return nk;
@@ -728,22 +783,12 @@ struct Engine {
   // Noise-free clipped sum of the batch into d_sum (no update): the
   // north-star parity probe.
   int enqueue_local_sum(cudaStream_t s, const BlockTable& t, int np, int U) {
-    const int grid = (int)std::min<long long>((P + 31) / 32, 148 * 16);
-    aggregate_kernel<16><<<grid, 32 * kChunks, sizeof(float) * U, s>>>(t, d_parts, np, d_args, d_params,
-                                                             d_sum, d_norms, d_clipped, d_err, 1);
+    launch_agg(agg_launch(t, np, U, 1), s);
     return 1;
   }
 
-  // ---- step argument slots (pinned ring) ------------------------------------
-  void push_args(const StepArgs& a) {
-    const int k = (int)(arg_counter++ % kArgSlots);
-    if (slot_used[k]) PGB_CUDA(cudaEventSynchronize(slot_ev[k]));
-    h_args[k] = a;
-    PGB_CUDA(cudaMemcpyAsync(d_args, &h_args[k], sizeof(StepArgs), cudaMemcpyHostToDevice,
-                             stream));
-    PGB_CUDA(cudaEventRecord(slot_ev[k], stream));
-    slot_used[k] = true;
-  }
+  // ---- step arguments ---------------------------------------------------------
+  void push_args(const StepArgs& a) { cur_args = a; }
 
   StepArgs make_args(const pgb_dp_config& c, int64_t step, const float* x, const float* y) {
     StepArgs a{};
@@ -764,36 +809,102 @@ struct Engine {
   // Launch the step for inputs already resident at d_x/d_y slots.
   void launch_step(const float* x_slot, const float* y_slot, int64_t m) {
     const int variant = (m > 1 ? 1 : 0) | (world > 1 ? 2 : 0);
-    const int key = variant * 4 + (x_slot == d_x ? 0 : x_slot == d_xb[0] ? 1 : 2);
+    // the fused MNIST schedule takes its input pointers as updatable node
+    // parameters; the layer-wise schedule bakes the input slot into the graph
+    const int key = variant * 4 + (fused_mnist ? 0 : x_slot == d_x ? 0 : x_slot == d_xb[0] ? 1 : 2);
     if (!graph_enabled) {
       kernels_last = enqueue_step(stream, x_slot, y_slot, m);
       PGB_CUDA(cudaGetLastError());
       return;
     }
-    auto it = graphs.find(key * 64 + (int)std::min<int64_t>(m, 63));
+    const int gkey = key * 64 + (int)std::min<int64_t>(m, 63);
+    auto it = graphs.find(gkey);
     if (it == graphs.end()) {
-      cudaGraph_t g;
+      StepGraph sg;
       PGB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       int nk = 0;
       try {
         nk = enqueue_step(stream, x_slot, y_slot, m);
       } catch (...) {
-        cudaStreamEndCapture(stream, &g);
+        cudaStreamEndCapture(stream, &sg.graph);
+        if (sg.graph) cudaGraphDestroy(sg.graph);
         throw;
       }
-      PGB_CUDA(cudaStreamEndCapture(stream, &g));
-      cudaGraphExec_t ge;
-      PGB_CUDA(cudaGraphInstantiate(&ge, g, 0));
-      cudaGraphDestroy(g);
-      it = graphs.emplace(key * 64 + (int)std::min<int64_t>(m, 63), ge).first;
+      PGB_CUDA(cudaStreamEndCapture(stream, &sg.graph));
+      PGB_CUDA(cudaGraphInstantiate(&sg.exec, sg.graph, 0));
+      find_step_nodes(sg);
+      it = graphs.emplace(gkey, sg).first;
       kernels_last = nk;
     }
-    PGB_CUDA(cudaGraphLaunch(it->second, stream));
+    update_step_nodes(it->second, x_slot, y_slot);
+    PGB_CUDA(cudaGraphLaunch(it->second.exec, stream));
   }
 
+  // The kernel nodes whose parameters change from step to step.
+  void find_step_nodes(StepGraph& sg) {
+    size_t n = 0;
+    PGB_CUDA(cudaGraphGetNodes(sg.graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    PGB_CUDA(cudaGraphGetNodes(sg.graph, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      PGB_CUDA(cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      PGB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == (void*)aggregate_kernel && (sg.agg == nullptr || sg.agg_args.mode != 0)) {
+        const AggLaunch* L = static_cast<const AggLaunch*>(kp.kernelParams[0]);
+        if (sg.agg == nullptr || L->mode == 0) {
+          sg.agg = nd;
+          sg.agg_args = *L;
+        }
+      } else if (kp.func == (void*)noise_update_kernel) {
+        sg.noise = nd;
+        sg.noise_args = *static_cast<const NoiseLaunch*>(kp.kernelParams[0]);
+      } else if (kp.func == (void*)mnist::fused_kernel) {
+        sg.fused = nd;
+        sg.fused_args = *static_cast<const mnist::Params*>(kp.kernelParams[0]);
+      }
+    }
+  }
+
+  static bool same_args(const StepArgs& a, const StepArgs& b) {
+    return std::memcmp(&a, &b, sizeof(StepArgs)) == 0;
+  }
+
+  void set_node(cudaGraphExec_t ex, cudaGraphNode_t nd, void* arg) {
+    cudaKernelNodeParams kp{};
+    PGB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    void* params[1] = {arg};
+    kp.kernelParams = params;
+    kp.extra = nullptr;
+    PGB_CUDA(cudaGraphExecKernelNodeSetParams(ex, nd, &kp));
+  }
+
+  void update_step_nodes(StepGraph& sg, const float* x_slot, const float* y_slot) {
+    if (sg.agg && !same_args(sg.agg_args.a, cur_args)) {
+      sg.agg_args.a = cur_args;
+      set_node(sg.exec, sg.agg, &sg.agg_args);
+    }
+    if (sg.noise && !same_args(sg.noise_args.a, cur_args)) {
+      sg.noise_args.a = cur_args;
+      set_node(sg.exec, sg.noise, &sg.noise_args);
+    }
+    if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot)) {
+      sg.fused_args.x = x_slot;
+      sg.fused_args.y = y_slot;
+      set_node(sg.exec, sg.fused, &sg.fused_args);
+    }
+  }
+
+  // Device errors are sticky (the first one wins and later updates are
+  // skipped) until the host reports them here.
   void check_device_error() {
     if (h_err->code == 0) return;
     const DevError e = *h_err;
+    h_err->code = 0;
+    PGB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(DevError), stream));
+    PGB_CUDA(cudaStreamSynchronize(stream));
     if (e.what == 0)
       raise(PGB_ERR_INDEX, "softmax_xent label: id " + std::to_string((long long)e.value) +
                                " out of range [0," + std::to_string(e.limit) + ") at position " +
@@ -958,14 +1069,20 @@ pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d
     Engine& en = E(e);
     if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
     validate_dp_config(*cfg, en.B);
-    PGB_CUDA(cudaMemcpyAsync(en.d_x, d_x, sizeof(float) * en.B * en.in_row,
-                             cudaMemcpyDeviceToDevice, en.stream));
-    PGB_CUDA(cudaMemcpyAsync(en.d_y, d_y, sizeof(float) * en.B, cudaMemcpyDeviceToDevice,
-                             en.stream));
+    if (!d_x || !d_y) raise(PGB_ERR_CONTRACT, "null input");
     en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
     en.last_cfg = *cfg;
     en.last_step = step;
-    en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+    if (en.fused_mnist && en.graph_enabled) {
+      // read in place: the graph's fused-kernel node is pointed at the batch
+      en.launch_step(d_x, d_y, cfg->microbatch);
+    } else {
+      PGB_CUDA(cudaMemcpyAsync(en.d_x, d_x, sizeof(float) * en.B * en.in_row,
+                               cudaMemcpyDeviceToDevice, en.stream));
+      PGB_CUDA(cudaMemcpyAsync(en.d_y, d_y, sizeof(float) * en.B, cudaMemcpyDeviceToDevice,
+                               en.stream));
+      en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+    }
   });
 }
 
@@ -1195,6 +1312,26 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     en.check_device_error();
   });
 }
+
+#ifdef PGB_TRACE
+// Tuning aid (trace builds only): arm the timestamp buffer (out == NULL) or
+// copy it out.
+pgb_status pgb_debug_trace(long long* out, int n) {
+  return guarded([&] {
+    static unsigned long long* buf = nullptr;
+    if (!buf) {
+      PGB_CUDA(cudaMalloc(&buf, 8 * PGB_TRACE_SLOTS));
+      PGB_CUDA(cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)));
+    }
+    PGB_CUDA(cudaDeviceSynchronize());
+    if (!out) {
+      PGB_CUDA(cudaMemset(buf, 0, 8 * PGB_TRACE_SLOTS));
+      return;
+    }
+    PGB_CUDA(cudaMemcpy(out, buf, 8 * std::min(n, PGB_TRACE_SLOTS), cudaMemcpyDeviceToHost));
+  });
+}
+#endif
 
 pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
                              const pgb_dp_config* cfg, int64_t step0, int32_t n_steps,

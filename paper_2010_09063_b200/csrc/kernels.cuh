@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "pgb_internal.h"
+#include "trace.cuh"
 
 namespace pgb {
 
@@ -458,13 +459,21 @@ struct BlockTable {
   int shadow_rows[kMaxBlocks];
 };
 
+// Transposed shadow of a (rows, cols) parameter block, rows a power of two:
+// element (r, c) at dst[c * rows + (r ^ (c & (rows - 1)))]. The XOR swizzle
+// makes both a row of the shadow (fixed c) and a column across consecutive c
+// (fixed r) bank-conflict-free once the shadow is bulk-copied to shared memory.
+__host__ __device__ __forceinline__ long long shadow_index(long long r, long long c, int rows) {
+  return c * rows + (r ^ (c & (rows - 1)));
+}
+
 __device__ __forceinline__ void write_param(const BlockTable& bt, int p, long long j,
                                             float* params, float v) {
   params[bt.param_off[p] + j] = v;
   if (bt.shadow[p]) {
     const long long cols = bt.size[p] / bt.shadow_rows[p];
     const long long r = j / cols, c = j - r * cols;
-    bt.shadow[p][c * bt.shadow_rows[p] + r] = v;
+    bt.shadow[p][shadow_index(r, c, bt.shadow_rows[p])] = v;
   }
 }
 
@@ -550,27 +559,6 @@ __device__ __forceinline__ void gauss_pair(uint64_t key, long long pair, float* 
   *s = (float)(r * sn);
 }
 
-// Norm finalisation shared by every CTA of the aggregation kernels:
-// norm_i = (float)sqrt(sum_p parts[i][p]); s_i = norm > C ? C/norm : 1.
-__device__ __forceinline__ void load_scales(const double* __restrict__ parts, int nparts,
-                                            int units, float clip, float* s_sh,
-                                            float* norms_out, int* clipped_out) {
-  int local_clipped = 0;
-  for (int i = threadIdx.x; i < units; i += blockDim.x) {
-    double acc = 0.0;
-    for (int p = 0; p < nparts; ++p) acc += parts[(size_t)i * nparts + p];
-    const float n = (float)sqrt(acc);
-    s_sh[i] = n > clip ? __fdiv_rn(clip, n) : 1.0f;
-    if (norms_out) norms_out[i] = n;
-    local_clipped += n > clip;
-  }
-  if (clipped_out) {
-    local_clipped = __reduce_add_sync(0xffffffffu, local_clipped);
-    if ((threadIdx.x & 31) == 0 && local_clipped) atomicAdd(clipped_out, local_clipped);
-  }
-  __syncthreads();
-}
-
 // Locate the block of a global pair index (table cached in shared memory).
 __device__ __forceinline__ int find_block(const long long* pair_off, int n, long long q) {
   int p = 0;
@@ -580,118 +568,276 @@ __device__ __forceinline__ int find_block(const long long* pair_off, int n, long
 
 // Clipped sum over the units (dpsgd.cpp:287-307), then noise / mean / SGD
 // update (dpsgd.cpp:308-317, apply_update :173-183) with the reference's fp32
-// operation order per element. The sum over units runs as kChunks ordered
-// partial sums (each in ascending unit order) combined in chunk order: a
-// fixed, run-to-run deterministic order that keeps kChunks x more loads in
-// flight than one sequential chain per column (the reference's strictly
-// ascending chain differs only by fp32 re-association, ~1e-7 relative).
-// CTA = 32 columns x kChunks warps; lanes take consecutive columns.
-// mode 0: fused single-GPU step; mode 1: write the local clipped sum only.
-constexpr int kChunks = 8;
+// operation order per element: acc += fl(g_ij * s_i), acc += fl((sigma*C) * n_j),
+// acc = fl(acc * (1/units)), p = fl(p - fl(lr * acc)).
+//
+// Work unit = one tile of one parameter block (tile table built once per
+// engine and block-kind signature, see Engine::tiles_for):
+//   materialised rows (kind 0): kAggCols consecutive columns; lane l owns
+//     columns 4l..4l+3 (one 16-byte load per unit when aligned);
+//   factored dense rows (kind 1, g_i = a_i (x) d_i): kAggRows weight rows r x
+//     32 columns c; lane l owns column c0+l of every row, so one coalesced
+//     load of d_i and kAggRows broadcast values of a_i feed kAggRows products
+//     fl(a_ir * d_ic) -- the fp32 element of the reference's outer-product
+//     stack, never written to memory.
+// A CTA of kAggWarps warps owns one tile; warp w sums a contiguous slice of
+// the units (ascending), with the first batch of loads issued before the clip
+// factors are computed; slices are combined in warp order through shared
+// memory. Fixed order: run-to-run deterministic; differs from the reference's
+// single ascending chain only by fp32 re-association. No float atomics.
+//
+// mode 0: fused single-GPU step (noise, mean, update); mode 1: write the
+// clipped sum only (multi-GPU before the all-reduce, and the parity probe).
+constexpr int kAggWarps = 16;
+constexpr int kAggCols = 128;
+constexpr int kAggRows = 16;
+constexpr int kAggBatch = 16; // units per load batch (materialised)
+constexpr int kAggChunk = 16; // units per load batch (factored)
 
-template <int UNROLL>
-__global__ void __launch_bounds__(32 * kChunks)
-    aggregate_kernel(BlockTable bt, const double* __restrict__ parts, int nparts,
-                     const StepArgs* __restrict__ args, float* __restrict__ params,
-                     float* __restrict__ sum_out, float* __restrict__ norms_out,
-                     int* __restrict__ clipped_out, const DevError* __restrict__ err, int mode) {
-  extern __shared__ float s_sh[];
-  __shared__ long long off_sh[kMaxBlocks + 1];
-  __shared__ float part_sh[kChunks][33];
-  const StepArgs a = *args;
-  const int U = a.units;
-  if (threadIdx.x == 0) {
-    long long o = 0;
-    for (int p = 0; p < bt.n; ++p) {
-      off_sh[p] = o;
-      o += bt.size[p];
-    }
-    off_sh[bt.n] = o;
+// Tile plan of one launch: tile_start[p] = first CTA of parameter block p
+// (prefix sums over the blocks' tile counts, built on the host from the block
+// kinds of the launch's BlockTable; Engine::agg_plan). Passed by value so a
+// CTA locates its tile without a memory round trip.
+struct AggPlan {
+  int n;
+  int tile_start[kMaxBlocks + 1];
+};
+
+struct AggTile {
+  int p;   // parameter block
+  int j0;  // kind 0: first column; kind 1: first weight row r0
+  int n;   // kind 0: columns (<= kAggCols); kind 1: rows (<= kAggRows)
+  int c0;  // kind 1: first column c0 (32 per tile)
+};
+
+__device__ __forceinline__ AggTile agg_tile(const BlockTable& bt, const AggPlan& plan, int bid) {
+  int p = 0;
+  while (p + 1 < plan.n && plan.tile_start[p + 1] <= bid) ++p;
+  const int q = bid - plan.tile_start[p];
+  AggTile t;
+  t.p = p;
+  if (bt.kind[p] == 0) {
+    t.j0 = q * kAggCols;
+    t.n = (int)min((long long)kAggCols, bt.size[p] - t.j0);
+    t.c0 = 0;
+  } else {
+    const int out = bt.out[p], in = (int)(bt.size[p] / out);
+    const int ctiles = (out + 31) / 32;
+    t.j0 = (q / ctiles) * kAggRows;
+    t.c0 = (q % ctiles) * 32;
+    t.n = min(kAggRows, in - t.j0);
   }
-  load_scales(parts, nparts, U, a.clip, s_sh, blockIdx.x == 0 ? norms_out : nullptr,
-              blockIdx.x == 0 ? clipped_out : nullptr);
-  const bool failed = err && err->code != 0;
-  const long long total = off_sh[bt.n];
-  const int lane = threadIdx.x & 31, chunk = threadIdx.x >> 5;
-  const int rows = (U + kChunks - 1) / kChunks;
-  const int i0 = min(U, chunk * rows), i1 = min(U, i0 + rows);
-  for (long long base = (long long)blockIdx.x * 32; base < total;
-       base += (long long)gridDim.x * 32) {
-    const long long q = base + lane;
-    float acc = 0.0f;
-    int p = 0;
-    long long j = 0;
-    if (q < total) {
-      p = find_block(off_sh, bt.n, q);
-      j = q - off_sh[p];
-      if (bt.kind[p] == 0) {
-        const float* col = bt.base[p] + j;
-        const long long st = bt.stride[p];
-        int i = i0;
-        for (; i + UNROLL <= i1; i += UNROLL) {
-          float v[UNROLL];
+  return t;
+}
+
+__device__ __forceinline__ void agg_scales(const double* __restrict__ parts, int nparts, int U,
+                                           float clip, float* s_sh, float* norms_out,
+                                           int* cnt_sh) {
+  int local_clipped = 0;
+  for (int i = threadIdx.x; i < U; i += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < nparts; ++q) acc += parts[(size_t)i * nparts + q];
+    const float nrm = (float)sqrt(acc);
+    s_sh[i] = nrm > clip ? __fdiv_rn(clip, nrm) : 1.0f;
+    if (norms_out) norms_out[i] = nrm;
+    local_clipped += nrm > clip;
+  }
+  local_clipped = __reduce_add_sync(0xffffffffu, local_clipped);
+  if ((threadIdx.x & 31) == 0) cnt_sh[threadIdx.x >> 5] = local_clipped;
+}
+
+// Everything one aggregation launch needs, passed by value as the kernel's
+// single parameter: a CUDA-graph replay swaps in the step's arguments with
+// one kernel-node parameter update (no host-to-device copy on the stream).
+struct AggLaunch {
+  BlockTable bt;
+  AggPlan plan;
+  StepArgs a;
+  const double* parts;  // fp64 squared-norm partials, (U, nparts)
+  float* params;
+  float* sum_out;       // mode 1
+  float* norms_out;     // (U), written by CTA 0
+  int* clipped_out;     // written (not accumulated) by CTA 0
+  const DevError* err;
+  int U, nparts, mode;
+};
+
+__global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
+  const BlockTable& bt = L.bt;
+  const StepArgs& a = L.a;
+  const double* __restrict__ parts = L.parts;
+  float* __restrict__ params = L.params;
+  const int U = L.U, nparts = L.nparts, mode = L.mode;
+  extern __shared__ float s_sh[];  // clip factors, one per unit
+  __shared__ float part_sh[kAggWarps][kAggRows * 32];
+  __shared__ int cnt_sh[kAggWarps];
+  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
+  const AggTile tile = agg_tile(bt, L.plan, blockIdx.x);
+  const int p = tile.p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this thread's epilogue column, and its current parameter / the step
+  // arguments / the error flag, fetched now so they are not on the tail
+  long long j;
+  bool has_col;
+  if (bt.kind[p] == 0) {
+    has_col = threadIdx.x < tile.n;
+    j = (long long)tile.j0 + threadIdx.x;
+  } else {
+    const int rr = threadIdx.x >> 5, c = tile.c0 + (threadIdx.x & 31);
+    has_col = rr < tile.n && c < bt.out[p];
+    j = (long long)(tile.j0 + rr) * bt.out[p] + c;
+  }
+  const float cur = (has_col && mode == 0) ? params[bt.param_off[p] + j] : 0.0f;
+  const bool failed = L.err && L.err->code != 0;
+  const int rows = (U + kAggWarps - 1) / kAggWarps;
+  const int i0 = min(U, warp * rows), i1 = min(U, i0 + rows);
+  float* norms_cta = blockIdx.x == 0 ? L.norms_out : nullptr;
+
+  if (bt.kind[p] == 0) {
+    // ---- materialised rows: 4 columns per lane ----
+    const int c0 = 4 * lane;
+    const int ncol = max(0, min(4, tile.n - c0));
+    const long long stride = bt.stride[p];
+    const float* base = bt.base[p] + tile.j0 + c0;
+    const bool vec = ncol == 4 && (stride & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float v[kAggBatch][4];
+    auto load = [&](int ib) {
 #pragma unroll
-          for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(col + (long long)(i + u) * st);
+      for (int u = 0; u < kAggBatch; ++u) {
+        const int i = ib + u;
+        if (i < i1 && ncol > 0) {
+          const float* src = base + (long long)i * stride;
+          if (vec) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+            v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+          } else {
 #pragma unroll
-          for (int u = 0; u < UNROLL; ++u) acc = __fadd_rn(acc, __fmul_rn(v[u], s_sh[i + u]));
-        }
-        for (; i < i1; ++i) acc = __fadd_rn(acc, __fmul_rn(__ldg(col + (long long)i * st), s_sh[i]));
-      } else {
-        // factored dense block: rebuild the fp32 stack element fl(a_r * d_c)
-        const int out = bt.out[p];
-        const long long r = j / out, c = j - r * out;
-        const float* A = bt.a[p] + r;
-        const float* D = bt.base[p] + c;
-        const long long as = bt.a_stride[p], ds = bt.stride[p];
-        int i = i0;
-        for (; i + UNROLL <= i1; i += UNROLL) {
-          float av[UNROLL], dv[UNROLL];
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            av[u] = __ldg(A + (long long)(i + u) * as);
-            dv[u] = __ldg(D + (long long)(i + u) * ds);
+            for (int c = 0; c < 4; ++c) v[u][c] = c < ncol ? __ldg(src + c) : 0.0f;
           }
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u)
-            acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(av[u], dv[u]), s_sh[i + u]));
         }
-        for (; i < i1; ++i)
-          acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__ldg(A + (long long)i * as),
-                                                   __ldg(D + (long long)i * ds)), s_sh[i]));
       }
-    }
-    part_sh[chunk][lane] = acc;
+    };
+    load(i0);  // in flight while the clip factors are computed
+    agg_scales(parts, nparts, U, a.clip, s_sh, norms_cta, cnt_sh);
     __syncthreads();
-    if (chunk == 0 && q < total) {
-      float sum = part_sh[0][lane];
+    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 1);
+    for (int ib = i0; ib < i1; ib += kAggBatch) {
+      if (ib != i0) load(ib);
 #pragma unroll
-      for (int c = 1; c < kChunks; ++c) sum = __fadd_rn(sum, part_sh[c][lane]);
-      if (mode == 1) {
-        sum_out[bt.param_off[p] + j] = sum;
-      } else {
-        if (a.add_noise) {
-          float n0, n1;
-          gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
-          const float scale = __fmul_rn(a.sigma, a.clip);
-          sum = __fadd_rn(sum, __fmul_rn(scale, (j & 1) ? n1 : n0));
-        }
-        sum = __fmul_rn(sum, a.inv_units);
-        if (!failed) {
-          const float cur = params[bt.param_off[p] + j];
-          write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
+      for (int u = 0; u < kAggBatch; ++u) {
+        if (ib + u < i1) {
+          const float s = s_sh[ib + u];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(v[u][c], s));
         }
       }
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) part_sh[warp][c0 + c] = acc[c];
+  } else {
+    // ---- factored dense rows: kAggRows weight rows x 32 columns ----
+    // Per chunk of kAggChunk units the warp issues every load at once: d_ic
+    // into registers (lane = c), the a_i[r0 .. r0+15] rows through a
+    // per-warp shared staging area (read back as broadcasts).
+    const int out = bt.out[p];
+    const int c = tile.c0 + lane;
+    const bool cok = c < out;
+    const int nr = tile.n;
+    const float* A = bt.a[p] + tile.j0;
+    const float* D = bt.base[p] + (cok ? c : 0);
+    const long long as = bt.a_stride[p], ds = bt.stride[p];
+    float* a_st = s_sh + ((U + 3) & ~3) + warp * (kAggChunk * kAggRows);
+    float acc[kAggRows];
+#pragma unroll
+    for (int r = 0; r < kAggRows; ++r) acc[r] = 0.0f;
+    float dv[kAggChunk], ar[kAggChunk * kAggRows / 32];
+    auto load = [&](int ib) {
+#pragma unroll
+      for (int u = 0; u < kAggChunk; ++u)
+        dv[u] = (cok && ib + u < i1) ? __ldg(D + (long long)(ib + u) * ds) : 0.0f;
+#pragma unroll
+      for (int q = 0; q < kAggChunk * kAggRows / 32; ++q) {
+        const int e = q * 32 + lane, u = e / kAggRows, r = e % kAggRows;
+        ar[q] = (ib + u < i1 && r < nr) ? __ldg(A + (long long)(ib + u) * as + r) : 0.0f;
+      }
+    };
+    load(i0);
+    agg_scales(parts, nparts, U, a.clip, s_sh, norms_cta, cnt_sh);
     __syncthreads();
+    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 2);
+    for (int ib = i0; ib < i1; ib += kAggChunk) {
+      if (ib != i0) load(ib);
+#pragma unroll
+      for (int q = 0; q < kAggChunk * kAggRows / 32; ++q) a_st[q * 32 + lane] = ar[q];
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < kAggChunk; ++u) {
+        if (ib + u < i1) {
+          const float s = s_sh[ib + u];
+          const float4* a4 = reinterpret_cast<const float4*>(a_st + u * kAggRows);
+#pragma unroll
+          for (int q = 0; q < kAggRows / 4; ++q) {
+            const float4 x = a4[q];
+            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(__fmul_rn(x.x, dv[u]), s));
+            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(__fmul_rn(x.y, dv[u]), s));
+            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(__fmul_rn(x.z, dv[u]), s));
+            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(__fmul_rn(x.w, dv[u]), s));
+          }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int r = 0; r < kAggRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
   }
+  __syncthreads();
+    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 3);
+
+  // ---- epilogue: one thread per column of the tile ----
+  if (blockIdx.x == 0 && threadIdx.x == 0 && L.clipped_out) {
+    int n = 0;
+#pragma unroll
+    for (int w = 0; w < kAggWarps; ++w) n += cnt_sh[w];
+    *L.clipped_out = n;
+  }
+  if (!has_col) return;
+  const int t = threadIdx.x;
+  float sum = part_sh[0][t];
+#pragma unroll
+  for (int w = 1; w < kAggWarps; ++w) sum = __fadd_rn(sum, part_sh[w][t]);
+  if (mode == 1) {
+    L.sum_out[bt.param_off[p] + j] = sum;
+    return;
+  }
+  if (a.add_noise) {
+    // the pair's two normals come from one Box-Muller draw (kernels.hpp:597-614)
+    float n0, n1;
+    gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
+    sum = __fadd_rn(sum, __fmul_rn(__fmul_rn(a.sigma, a.clip), (j & 1) ? n1 : n0));
+  }
+  sum = __fmul_rn(sum, a.inv_units);
+  if (failed) return;
+  write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
+  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
 }
 
 // After the all-reduce of the clipped sums: noise (one shared draw from the
 // common seed), mean over the global units, update.
-__global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt,
-                                    const StepArgs* __restrict__ args,
-                                    float* __restrict__ params,
-                                    const DevError* __restrict__ err) {
+struct NoiseLaunch {
+  BlockTable bt;
+  StepArgs a;
+  const float* sum;  // the all-reduced clipped sum
+  float* params;
+  const DevError* err;
+};
+
+__global__ void noise_update_kernel(const NoiseLaunch L) {
+  const BlockTable& bt = L.bt;
+  const StepArgs& a = L.a;
+  const float* __restrict__ sum = L.sum;
+  float* __restrict__ params = L.params;
   __shared__ long long off_sh[kMaxBlocks + 1];
   if (threadIdx.x == 0) {
     long long o = 0;
@@ -702,8 +848,7 @@ __global__ void noise_update_kernel(const float* __restrict__ sum, BlockTable bt
     off_sh[bt.n] = o;
   }
   __syncthreads();
-  const StepArgs a = *args;
-  if (err && err->code != 0) return;
+  if (L.err && L.err->code != 0) return;
   const long long total = off_sh[bt.n];
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
@@ -789,7 +934,7 @@ __global__ void transpose_kernel(const float* __restrict__ src, int rows, int co
                                  float* __restrict__ dst) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
     const int r = e / cols, c = e - r * cols;
-    dst[c * rows + r] = src[e];
+    dst[shadow_index(r, c, rows)] = src[e];
   }
 }
 

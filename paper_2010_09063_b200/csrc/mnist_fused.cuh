@@ -10,6 +10,12 @@
 // Every activation stays in shared memory. The image and the conv weights
 // arrive by TMA bulk copies (cp.async.bulk + mbarrier); the conv2 weights
 // are read from a transposed copy the update kernel keeps in step.
+//
+// Shape of the launch: B = 256 examples on 148 SMs is at most two examples
+// per SM, so per-SM throughput is set by how well two co-resident CTAs hide
+// shared-memory and barrier latency. Each CTA therefore runs 16 warps (two
+// CTAs = 32 warps per SM) with a 64-register budget; every phase is split so
+// all 512 threads have work and per-thread state stays small.
 #pragma once
 
 #include "kernels.cuh"
@@ -20,37 +26,43 @@ namespace mnist {
 constexpr int H0 = 28, XP = 34;            // input, padded input (pad 3)
 constexpr int XS = 40;                     // xs row stride (bank-conflict-free taps)
 constexpr int D1 = 16, K1 = 8, O1 = 14;    // conv1 out 16x14x14
+constexpr int NP1 = O1 * O1;               // 196 conv1 output positions
 constexpr int PO = 7;                      // pooled 16x7x7
 constexpr int C2 = 16, D2 = 32, K2 = 4, O2 = 4;
 constexpr int KC2 = C2 * K2 * K2;          // 256 = im2col rows of conv2
 constexpr int NP2 = O2 * O2;               // 16 conv2 output positions
 constexpr int F1 = 512, H1 = 32, NC = 10;
-constexpr int NT = 256;
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
 
 struct Smem {
-  float w2t[KC2 * D2];               // conv2 weights [k=(c,u,v)][d]   (TMA)
+  float w2t[KC2 * D2];               // conv2 weights, swizzled transpose (TMA):
+                                     //   W2[d][k] at [k*32 + (d ^ (k & 31))]
   float w1[D1 * K1 * K1];            // conv1 weights [d][u][v]        (TMA)
   float b1[D1];                      //                                (TMA)
   float b2[D2];                      //                                (TMA)
   float xs[XP * XS];                 // padded input, row stride XS
-  float a1[D1 * O1 * O1];            // relu(conv1)
+  float a1[D1 * NP1];                // relu(conv1) [d][pos]
   union {
     float p1[D1 * PO * PO];          // maxpool output
     float dp1[D1 * PO * PO];         // its cotangent (p1 is dead by then)
   } up;
-  float buf[KC2 * NP2];              // conv2 im2col [k][pos] -> [pos][k] -> dcols [pos][k]
+  float buf[KC2 * NP2];              // conv2 im2col [k][pos] -> dcols [pos][k] -> dW1 partials
   union {
     float xstage[H0 * H0];           // raw image (TMA), padded into xs
-    float part[8 * NP2 * D2];        // split-K partials of conv2 fwd [w][pos][d]
-    float z1[8 * H1];                // fc1 split partials
-    float d1[O1 * O1 * D1];          // d conv1-linear [pos][d]
+    float part[8 * NP2 * D2];        // split-K partials of conv2 fwd [kslice][pos][d]
+    float z1[NW * H1];               // fc1 split partials
+    float d1[NP1 * D1];              // d conv1-linear [pos][d]
   } u1;
-  float a2[F1];                      // relu(conv2) = fc1 input (flatten order)
+  float a2[F1];                      // relu(conv2) = fc1 input (flatten order [d][pos])
   float dc2[NP2 * D2];               // d conv2-linear [pos][d]
   float dc2t[D2 * NP2];              // the same, [d][pos]
   float h[H1], dz1[H1], dz2[16], logits[16];
-  double red5[5][NT / 32];
-  unsigned long long bar;            // mbarrier of the bulk copies
+  float w4[H1 * NC], b4[16], b3[H1];  // fc weights/biases needed by the loss tail
+  float yb;                          // this example's label
+  float b1red[NW][D1];               // per-warp partials of the conv1 bias gradient
+  double red5[5][NW];
+  unsigned long long bar[2];         // mbarriers: [0] image + conv1, [1] conv2
   unsigned char pidx[D1 * PO * PO];  // first-max window slot
 };
 
@@ -86,6 +98,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(smem_addr(bar)) : "memory");
+}
+
 __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -96,66 +117,87 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   const float* gb3 = W + prm.off[5];
   const float* gW4 = W + prm.off[6];
   const float* gb4 = W + prm.off[7];
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 0);
 
   // ---- TMA: image + conv weights + biases into shared memory --------------
-  constexpr uint32_t kBytes = sizeof(float) * (H0 * H0 + D1 * K1 * K1 + D1 + D2 + KC2 * D2);
+  // Two transactions so conv1 starts as soon as its 7 KB have landed while the
+  // 32 KB of conv2 weights are still in flight.
+  constexpr uint32_t kBytes0 = sizeof(float) * (H0 * H0 + D1 * K1 * K1 + D1);
+  constexpr uint32_t kBytes1 = sizeof(float) * (D2 + KC2 * D2);
   if (t == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&S.bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&S.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&S.bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(smem_addr(&S.bar)), "r"(kBytes) : "memory");
-    bulk_g2s(S.u1.xstage, prm.x + (size_t)b * H0 * H0, sizeof(float) * H0 * H0, &S.bar);
-    bulk_g2s(S.w1, W + prm.off[0], sizeof(float) * D1 * K1 * K1, &S.bar);
-    bulk_g2s(S.b1, W + prm.off[1], sizeof(float) * D1, &S.bar);
-    bulk_g2s(S.b2, W + prm.off[3], sizeof(float) * D2, &S.bar);
-    bulk_g2s(S.w2t, prm.w2t, sizeof(float) * KC2 * D2, &S.bar);
+                 :: "r"(smem_addr(&S.bar[0])), "r"(kBytes0) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&S.bar[1])), "r"(kBytes1) : "memory");
+    bulk_g2s(S.u1.xstage, prm.x + (size_t)b * H0 * H0, sizeof(float) * H0 * H0, &S.bar[0]);
+    bulk_g2s(S.w1, W + prm.off[0], sizeof(float) * D1 * K1 * K1, &S.bar[0]);
+    bulk_g2s(S.b1, W + prm.off[1], sizeof(float) * D1, &S.bar[0]);
+    bulk_g2s(S.b2, W + prm.off[3], sizeof(float) * D2, &S.bar[1]);
+    bulk_g2s(S.w2t, prm.w2t, sizeof(float) * KC2 * D2, &S.bar[1]);
   }
+  // the loss tail's operands (fc2 weights/biases, fc1 bias, label), fetched
+  // now so they are not a dependent chain later
+  if (t < H1 * NC) S.w4[t] = __ldg(gW4 + t);
+  else if (t < H1 * NC + NC) S.b4[t - H1 * NC] = __ldg(gb4 + t - H1 * NC);
+  else if (t < H1 * NC + NC + H1) S.b3[t - H1 * NC - NC] = __ldg(gb3 + t - H1 * NC - NC);
+  else if (t == H1 * NC + NC + H1) S.yb = prm.y[b];
   // zero the padding ring of xs while the copies fly
   for (int i = t; i < XP * XS; i += NT) {
     const int r = i / XS - 3, c = i % XS - 3;
     if (!(r >= 0 && r < H0 && c >= 0 && c < H0)) S.xs[i] = 0.0f;
   }
   __syncthreads();  // barrier initialised before anyone waits on it
-  {
-    uint32_t done = 0;
-    while (!done)
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
-          "selp.u32 %0, 1, 0, p; }"
-          : "=r"(done) : "r"(smem_addr(&S.bar)) : "memory");
-  }
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
+  mbar_wait0(&S.bar[0]);
   for (int i = t; i < H0 * H0; i += NT) S.xs[(i / H0 + 3) * XS + i % H0 + 3] = S.u1.xstage[i];
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
 
-  // ---- conv1 + relu: one output position per thread, window in registers --
-  if (t < O1 * O1) {
-    const int oy = t / O1, ox = t % O1;
-    float win[K1 * K1];
+  // ---- conv1 + relu: thread = (position, half of the channels) -----------
+  // The 8x8 window streams through registers one kernel row at a time.
+  if (t < 2 * NP1) {
+    const int pos = t % NP1, dh = t / NP1;
+    const int oy = pos / O1, ox = pos % O1;
+    float acc[8];
 #pragma unroll
-    for (int u = 0; u < K1; ++u)
-#pragma unroll
-      for (int v = 0; v < K1; ++v) win[u * K1 + v] = S.xs[(2 * oy + u) * XS + 2 * ox + v];
+    for (int d = 0; d < 8; ++d) acc[d] = 0.0f;
 #pragma unroll 2
-    for (int d = 0; d < D1; ++d) {
-      const float4* w4 = reinterpret_cast<const float4*>(S.w1 + d * K1 * K1);
-      float acc0 = 0.0f, acc1 = 0.0f;
+    for (int u = 0; u < K1; ++u) {
+      float win[K1];
 #pragma unroll
-      for (int q = 0; q < K1 * K1 / 4; ++q) {
-        const float4 wv = w4[q];
-        acc0 = fmaf(wv.x, win[4 * q], acc0);
-        acc1 = fmaf(wv.y, win[4 * q + 1], acc1);
-        acc0 = fmaf(wv.z, win[4 * q + 2], acc0);
-        acc1 = fmaf(wv.w, win[4 * q + 3], acc1);
+      for (int v = 0; v < K1; ++v) win[v] = S.xs[(2 * oy + u) * XS + 2 * ox + v];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const float4* w4 = reinterpret_cast<const float4*>(S.w1 + (dh * 8 + d) * K1 * K1 + u * K1);
+        const float4 wa = w4[0], wb = w4[1];
+        float s = acc[d];
+        s = fmaf(wa.x, win[0], s);
+        s = fmaf(wa.y, win[1], s);
+        s = fmaf(wa.z, win[2], s);
+        s = fmaf(wa.w, win[3], s);
+        s = fmaf(wb.x, win[4], s);
+        s = fmaf(wb.y, win[5], s);
+        s = fmaf(wb.z, win[6], s);
+        s = fmaf(wb.w, win[7], s);
+        acc[d] = s;
       }
-      S.a1[d * O1 * O1 + t] = fmaxf(acc0 + acc1 + S.b1[d], 0.0f);
+    }
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const int dd = dh * 8 + d;
+      S.a1[dd * NP1 + pos] = fmaxf(acc[d] + S.b1[dd], 0.0f);
     }
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
 
   // ---- maxpool 2x2/2 (first max in window order, kernels.hpp:377-396) -------
   for (int i = t; i < D1 * PO * PO; i += NT) {
     const int c = i / (PO * PO), r = i % (PO * PO), py = r / PO, px = r % PO;
-    const float* src = S.a1 + c * O1 * O1 + (2 * py) * O1 + 2 * px;
+    const float* src = S.a1 + c * NP1 + (2 * py) * O1 + 2 * px;
     float m = src[0];
     int slot = 0;
     if (src[1] > m) { m = src[1]; slot = 1; }
@@ -165,6 +207,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.pidx[i] = (unsigned char)slot;
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
 
   // ---- conv2 im2col: buf[k][pos], k = (c,u,v), pos = (oy,ox) -------------
   for (int i = t; i < KC2 * NP2; i += NT) {
@@ -173,137 +216,142 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.buf[i] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
 
-  // ---- conv2 + relu: lane = out channel, warp = K slice of 32, split-K ----
+  // ---- conv2 + relu: lane = out channel, warp = (K slice of 32, 8 positions)
+  mbar_wait0(&S.bar[1]);
   {
-    const int d = lane;
-    float acc[NP2];
+    const int d = lane, ks = warp & 7, ph = warp >> 3;
+    float acc[8];
 #pragma unroll
-    for (int p = 0; p < NP2; ++p) acc[p] = 0.0f;
+    for (int p = 0; p < 8; ++p) acc[p] = 0.0f;
 #pragma unroll 4
     for (int kk = 0; kk < 32; ++kk) {
-      const int k = warp * 32 + kk;
-      const float w = S.w2t[k * D2 + d];
-      const float4* cr = reinterpret_cast<const float4*>(S.buf + k * NP2);
-#pragma unroll
-      for (int q = 0; q < NP2 / 4; ++q) {
-        const float4 c4 = cr[q];
-        acc[4 * q] = fmaf(w, c4.x, acc[4 * q]);
-        acc[4 * q + 1] = fmaf(w, c4.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(w, c4.z, acc[4 * q + 2]);
-        acc[4 * q + 3] = fmaf(w, c4.w, acc[4 * q + 3]);
-      }
+      const int k = ks * 32 + kk;
+      const float w = S.w2t[k * D2 + (d ^ (k & 31))];
+      const float4* cr = reinterpret_cast<const float4*>(S.buf + k * NP2 + ph * 8);
+      const float4 c0 = cr[0], c1 = cr[1];
+      acc[0] = fmaf(w, c0.x, acc[0]);
+      acc[1] = fmaf(w, c0.y, acc[1]);
+      acc[2] = fmaf(w, c0.z, acc[2]);
+      acc[3] = fmaf(w, c0.w, acc[3]);
+      acc[4] = fmaf(w, c1.x, acc[4]);
+      acc[5] = fmaf(w, c1.y, acc[5]);
+      acc[6] = fmaf(w, c1.z, acc[6]);
+      acc[7] = fmaf(w, c1.w, acc[7]);
     }
 #pragma unroll
-    for (int p = 0; p < NP2; ++p) S.u1.part[(warp * NP2 + p) * D2 + d] = acc[p];
+    for (int p = 0; p < 8; ++p) S.u1.part[(ks * NP2 + ph * 8 + p) * D2 + d] = acc[p];
   }
   __syncthreads();
-  for (int i = t; i < D2 * NP2; i += NT) {  // i = pos*32 + d
-    const int d = i % D2, p = i / D2;
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
+  {  // i = pos*32 + d
+    const int d = t % D2, p = t / D2;
     float s = 0.0f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s += S.u1.part[w * D2 * NP2 + i];
+    for (int w = 0; w < 8; ++w) s += S.u1.part[w * D2 * NP2 + t];
     S.a2[d * NP2 + p] = fmaxf(s + S.b2[d], 0.0f);
   }
-  // the patches again, transposed, for the per-example dW: buf[pos][k]
-  for (int i = t; i < KC2 * NP2; i += NT) {
-    const int pos = i / KC2, k = i % KC2;
-    const int c = k / 16, u = (k / 4) % 4, v = k % 4, oy = pos / 4, ox = pos % 4;
-    S.buf[i] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
-  }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
 
-  // ---- fc1 (512->32) + relu: lane = unit, warp = 64-row slice --------------
-  {
-    float wv[64];
+  // ---- fc1 (512->32) + relu: lane = unit, warp = 32-row slice -------------
+  // The warp's 32x32 slice of W3 (coalesced rows) stays in registers for the
+  // backward pass below.
+  float wv[32];
 #pragma unroll
-    for (int r = 0; r < 64; ++r) wv[r] = __ldg(gW3 + (warp * 64 + r) * H1 + lane);
+  for (int r = 0; r < 32; ++r) wv[r] = __ldg(gW3 + (warp * 32 + r) * H1 + lane);
+  {
     float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
-    for (int r = 0; r < 64; r += 2) {
-      s0 = fmaf(S.a2[warp * 64 + r], wv[r], s0);
-      s1 = fmaf(S.a2[warp * 64 + r + 1], wv[r + 1], s1);
+    for (int r = 0; r < 32; r += 2) {
+      s0 = fmaf(S.a2[warp * 32 + r], wv[r], s0);
+      s1 = fmaf(S.a2[warp * 32 + r + 1], wv[r + 1], s1);
     }
     S.u1.z1[warp * H1 + lane] = s0 + s1;
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
   if (warp == 0) {
-    float z = __ldg(gb3 + lane);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) z += S.u1.z1[w * H1 + lane];
+    // fc1 bias + relu, fc2 (32->10), softmax cross-entropy (kernels.hpp:516-566)
+    // and dz1 = (W4 dz2) * [h > 0], all in registers with warp shuffles
+    float z = S.b3[lane];
+#pragma unroll 1
+    for (int w = 0; w < NW; ++w) z += S.u1.z1[w * H1 + lane];
     const float hv = fmaxf(z, 0.0f);
     S.h[lane] = hv;
-    __syncwarp();
-    // fc2 (32->10) + softmax cross-entropy (kernels.hpp:516-566)
-    float lg = 0.0f;
-    if (lane < NC) {
-      lg = __ldg(gb4 + lane);
-#pragma unroll
-      for (int j = 0; j < H1; ++j) lg = fmaf(S.h[j], __ldg(gW4 + j * NC + lane), lg);
-      S.logits[lane] = lg;
-    }
-    __syncwarp();
-    const float raw = prm.y[b];
+    const int cl = lane < NC ? lane : NC - 1;
+    float lg = S.b4[cl];
+#pragma unroll 1
+    for (int j = 0; j < H1; ++j) lg = fmaf(__shfl_sync(0xffffffffu, hv, j), S.w4[j * NC + cl], lg);
+    const float raw = S.yb;
     const bool ok = valid_id(raw, NC);
     if (!ok && lane == 0) raise_index(prm.err, 0, b, raw, NC);
     const int y = ok ? (int)raw : 0;
-    float m = S.logits[0];
-    for (int c = 1; c < NC; ++c) m = fmaxf(m, S.logits[c]);
-    float se = 0.0f;
-    for (int c = 0; c < NC; ++c) se += expf(S.logits[c] - m);
-    if (lane < NC) {
-      const float g = ok ? expf(lg - m) / se - (lane == y ? 1.0f : 0.0f) : 0.0f;
-      S.dz2[lane] = g;
-    }
-    if (lane == 0) prm.loss[b] = ok ? m + logf(se) - S.logits[y] : 0.0f;
-    __syncwarp();
-    // dz1 = (W4 dz2) * [h > 0]
-    float g1 = 0.0f;
+    float m = lane < NC ? lg : -INFINITY;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) g1 = fmaf(__ldg(gW4 + lane * NC + c), S.dz2[c], g1);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e = lane < NC ? expf(lg - m) : 0.0f;
+    float se = e;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float g = (ok && lane < NC) ? e / se - (lane == y ? 1.0f : 0.0f) : 0.0f;
+    if (lane < NC) S.dz2[lane] = g;
+    const float ly = __shfl_sync(0xffffffffu, lg, y);
+    if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
+    float g1 = 0.0f;
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) g1 = fmaf(S.w4[lane * NC + c], __shfl_sync(0xffffffffu, g, c), g1);
     S.dz1[lane] = hv > 0.0f ? g1 : 0.0f;
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
 
   // ---- fc1 backward data: da2[i] = W3[i,:] . dz1, relu mask -> dc2 --------
+  // From the register-resident W3 slice: products W3[r][lane] * dz1[lane],
+  // then a transpose-reduce across the lanes (recursive halving: after the
+  // five exchange steps lane l holds the full sum of row 32*warp + l).
   {
-    const float4* g4 = reinterpret_cast<const float4*>(S.dz1);
+    const float g = S.dz1[lane];
 #pragma unroll
-    for (int rr = 0; rr < F1 / NT; ++rr) {
-      const int i = t + rr * NT;
-      const float4* w4 = reinterpret_cast<const float4*>(gW3 + i * H1);
-      float4 wv[8];
+    for (int r = 0; r < 32; ++r) wv[r] *= g;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) wv[q] = __ldg(w4 + q);
-      float s0 = 0.0f, s1 = 0.0f;
+    for (int st = 0; st < 5; ++st) {
+      const int half = 16 >> st, off = 16 >> st;
+      const bool upper = (lane & off) != 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 g = g4[q];
-        s0 = fmaf(wv[q].x, g.x, s0);
-        s1 = fmaf(wv[q].y, g.y, s1);
-        s0 = fmaf(wv[q].z, g.z, s0);
-        s1 = fmaf(wv[q].w, g.w, s1);
+      for (int r = 0; r < half; ++r) {
+        const float send = upper ? wv[r] : wv[r + half];
+        const float keep = upper ? wv[r + half] : wv[r];
+        wv[r] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
-      const float v = S.a2[i] > 0.0f ? s0 + s1 : 0.0f;
-      const int d = i / NP2, pos = i % NP2;
-      S.dc2[pos * D2 + d] = v;
-      S.dc2t[i] = v;  // [d][pos] == flatten order
     }
+    const int i = warp * 32 + lane;
+    const float v = S.a2[i] > 0.0f ? wv[0] : 0.0f;
+    const int d = i / NP2, pos = i % NP2;
+    S.dc2[pos * D2 + d] = v;
+    S.dc2t[i] = v;  // [d][pos] == flatten order
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
 
   double sq = 0.0;  // this thread's share of ||g_i||^2
   const size_t bo = (size_t)b;
 
-  // ---- conv2 per-example dW: thread = k (c,u,v), loop d ---------------------
+  // ---- conv2 per-example dW: thread = (k (c,u,v), half of the channels) ----
   {
-    const int k = t;  // NT == KC2
+    const int k = t & (KC2 - 1), dh = t >> 8;
     float cv[NP2];
+    const float4* c4 = reinterpret_cast<const float4*>(S.buf + k * NP2);
 #pragma unroll
-    for (int p = 0; p < NP2; ++p) cv[p] = S.buf[p * KC2 + k];
+    for (int q = 0; q < NP2 / 4; ++q) {
+      const float4 x = c4[q];
+      cv[4 * q] = x.x; cv[4 * q + 1] = x.y; cv[4 * q + 2] = x.z; cv[4 * q + 3] = x.w;
+    }
     float* out = prm.st_c2w + bo * (D2 * KC2);
 #pragma unroll 4
-    for (int d = 0; d < D2; ++d) {
+    for (int dd = 0; dd < D2 / 2; ++dd) {
+      const int d = dh * (D2 / 2) + dd;
       const float4* g4 = reinterpret_cast<const float4*>(S.dc2t + d * NP2);
       float acc0 = 0.0f, acc1 = 0.0f;
 #pragma unroll
@@ -326,16 +374,21 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     sq = fma((double)s, (double)s, sq);
   }
   __syncthreads();  // buf (patches) is overwritten with dcols below
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
 
-  // ---- conv2 backward data: dcols[pos][(u,v),c] = sum_d W2[d][c,u,v] dc2[d][pos]
+  // ---- conv2 backward data: dcols[pos][(u,v),c] = sum_d W2[d][c,u,v] dc2[pos][d]
+  // thread = (k, half of the positions), lanes on consecutive k: column k of
+  // W2 from the swizzled shared transpose (conflict-free), dc2 rows as
+  // broadcasts.
   {
-    const int c = t % C2, uv = t / C2, k = c * 16 + uv;  // lanes: consecutive c
-    const float* gW2 = W + prm.off[2];
+    const int k = t & (KC2 - 1), ph = t >> 8;
+    const int c = k / 16, uv = k % 16;
     float wr[D2];
 #pragma unroll
-    for (int d = 0; d < D2; ++d) wr[d] = __ldg(gW2 + d * KC2 + k);
+    for (int d = 0; d < D2; ++d) wr[d] = S.w2t[k * D2 + (d ^ (k & 31))];
 #pragma unroll 2
-    for (int p = 0; p < NP2; ++p) {
+    for (int pp = 0; pp < NP2 / 2; ++pp) {
+      const int p = ph * (NP2 / 2) + pp;
       const float4* g4 = reinterpret_cast<const float4*>(S.dc2 + p * D2);
       float acc0 = 0.0f, acc1 = 0.0f;
 #pragma unroll
@@ -346,7 +399,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
         acc0 = fmaf(wr[4 * q + 2], g.z, acc0);
         acc1 = fmaf(wr[4 * q + 3], g.w, acc1);
       }
-      S.buf[p * KC2 + t] = acc0 + acc1;
+      S.buf[p * KC2 + uv * C2 + c] = acc0 + acc1;
     }
   }
   __syncthreads();
@@ -368,24 +421,33 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.up.dp1[c * PO * PO + r] = s;
   }
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
   // maxpool backward (route to the first max) + relu mask on a1 -> d1 [pos][d]
-  for (int i = t; i < D1 * O1 * O1; i += NT) {  // i = pos*16 + d
+  // Thread t always has channel d = t % 16 (NT % 16 == 0), so it also keeps a
+  // partial of the conv1 bias gradient sum_pos d1[pos][d].
+  float b1part = 0.0f;
+  for (int i = t; i < D1 * NP1; i += NT) {  // i = pos*16 + d
     const int d = i % D1, r = i / D1, oy = r / O1, ox = r % O1;
     const int pi = d * PO * PO + (oy / 2) * PO + ox / 2;
     const int slot = (oy & 1) * 2 + (ox & 1);
-    const float g = (S.pidx[pi] == slot && S.a1[d * O1 * O1 + r] > 0.0f) ? S.up.dp1[pi] : 0.0f;
+    const float g = (S.pidx[pi] == slot && S.a1[d * NP1 + r] > 0.0f) ? S.up.dp1[pi] : 0.0f;
     S.u1.d1[i] = g;
+    b1part += g;
   }
+  b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
+  if (lane < D1) S.b1red[warp][lane] = b1part;
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
 
-  // ---- conv1 per-example dW: thread = (tap, 8 channels, half of the rows) ---
+  // ---- conv1 per-example dW: thread = (tap, 8 channels, quarter of the rows)
   {
-    const int k = t % (K1 * K1), dg = (t / (K1 * K1)) & 1, half = t / (2 * K1 * K1);
+    const int k = t % (K1 * K1), dg = (t / (K1 * K1)) & 1, qr = t / (2 * K1 * K1);
     const int u = k / K1, v = k % K1;
+    const int oy0 = qr < 2 ? 4 * qr : 8 + 3 * (qr - 2), oy1 = qr < 2 ? oy0 + 4 : oy0 + 3;
     float acc[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
-    for (int oy = half * 7; oy < half * 7 + 7; ++oy) {
+    for (int oy = oy0; oy < oy1; ++oy) {
       const float* xr = S.xs + (2 * oy + u) * XS + v;
       const float4* g4 = reinterpret_cast<const float4*>(S.u1.d1 + oy * O1 * D1) + 2 * dg;
 #pragma unroll 7
@@ -403,36 +465,39 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
         acc[7] = fmaf(gb.w, xv, acc[7]);
       }
     }
-    // combine the two row halves through shared memory (buf is free)
-    if (half == 1) {
+    // combine the four row quarters through shared memory (buf is free)
+    if (qr > 0) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) S.buf[(dg * 8 + c) * 64 + k] = acc[c];
+      for (int c = 0; c < 8; ++c) S.buf[((qr - 1) * D1 + dg * 8 + c) * 64 + k] = acc[c];
     }
     __syncthreads();
-    if (half == 0) {
+    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
+    if (qr == 0) {
       float* out = prm.st_c1w + bo * (D1 * K1 * K1);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int d = dg * 8 + c;
-        const float g = acc[c] + S.buf[d * 64 + k];
+        const float g = ((acc[c] + S.buf[d * 64 + k]) + S.buf[(D1 + d) * 64 + k]) +
+                        S.buf[(2 * D1 + d) * 64 + k];
         out[d * 64 + k] = g;
         sq = fma((double)g, (double)g, sq);
       }
     }
   }
-  if (t < D1) {  // conv1 bias
+  if (t < D1) {  // conv1 bias: the per-warp partials of the pool-backward pass
     float s = 0.0f;
-    for (int p = 0; p < O1 * O1; ++p) s += S.u1.d1[p * D1 + t];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += S.b1red[w][t];
     prm.st_c1b[bo * D1 + t] = s;
     sq = fma((double)s, (double)s, sq);
   }
 
   // ---- dense factors for the ghost-norm blocks + their norm terms ----------
   double a2sq = 0.0;
-  for (int i = t; i < F1; i += NT) {
-    const float v = S.a2[i];
-    prm.a2[bo * F1 + i] = v;
-    a2sq = fma((double)v, (double)v, a2sq);
+  {
+    const float v = S.a2[t];  // NT == F1
+    prm.a2[bo * F1 + t] = v;
+    a2sq = (double)v * v;
   }
   double hsq = 0.0, dz1sq = 0.0, dz2sq = 0.0;
   if (t < H1) {
@@ -457,13 +522,15 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
 #pragma unroll
     for (int q = 0; q < 5; ++q) S.red5[q][warp] = v5[q];
   __syncthreads();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 16);
   if (t == 0) {
     double r5[5] = {0, 0, 0, 0, 0};
-    for (int w = 0; w < NT / 32; ++w)
+    for (int w = 0; w < NW; ++w)
 #pragma unroll
       for (int q = 0; q < 5; ++q) r5[q] += S.red5[q][w];
     // ||a (x) d||^2 = ||a||^2 ||d||^2 (weight) + ||d||^2 (bias), strategies.cpp:140-148
     prm.normsq[b] = r5[0] + r5[3] * (r5[1] + 1.0) + r5[4] * (r5[2] + 1.0);
+    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
   }
 }
 

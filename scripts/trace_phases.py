@@ -1,0 +1,65 @@
+#!/usr/bin/env python
+"""Per-phase timeline of the MNIST step kernels from device timestamps.
+
+Needs the trace build:  PGB_TRACE=1 python paper_2010_09063_b200/build.py
+(writes libpegrad_b200_trace.so beside the product library; this script
+loads it through PGB_LIBRARY). Then, on a GPU: python scripts/trace_phases.py
+Prints, for the fused per-example kernel, the mean duration of every phase
+(barrier to barrier) on SMs holding one CTA vs two, and for the aggregation
+kernel the start / scales / loop / epilogue split per tile kind.
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("PGB_LIBRARY", os.path.join(HERE, "paper_2010_09063_b200",
+                                                  "libpegrad_b200_trace.so"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2010_09063_b200 as P  # noqa: E402
+from paper_2010_09063_b200 import _lib  # noqa: E402
+
+AGG, FUSED, SLOTS = 0, 40000, 40000 + 24 * 4096
+L = _lib.lib
+if not hasattr(L, "pgb_debug_trace"):
+    sys.exit("not a trace build (PGB_TRACE=1 python paper_2010_09063_b200/build.py)")
+L.pgb_debug_trace.argtypes = [C.c_void_p, C.c_int]
+B = 256
+desc = P.build_desc(P.ModelKind.mnist_cnn)
+model = P.build(P.ModelKind.mnist_cnn, 0)
+data = P.synth_for_model(desc, B, 0)
+eng = P.GradEngine(model, P.Strategy.groupconv, B)
+cfg = P.DpConfig(1.0, 1.1, 0.1, 1, 0)
+for s in range(5):
+    P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, s)
+_lib.check(L.pgb_debug_trace(None, 0))
+P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 7)
+buf = np.zeros(SLOTS, np.int64)
+_lib.check(L.pgb_debug_trace(C.c_void_p(buf.ctypes.data), SLOTS))
+
+F = buf[FUSED:FUSED + 24 * B].reshape(B, 24)
+t0 = F[:, 0].min()
+marks = [k for k in range(24) if F[:, k].all()]
+end = F[:, marks[-1]]
+order = np.argsort(end)
+one, two = order[:30], order[-100:]
+print(f"fused kernel: first CTA start -> last end {(end.max() - t0) / 1e3:.2f} us, "
+      f"first end {(end.min() - t0) / 1e3:.2f} us")
+print("phase  alone(us)  shared(us)")
+for a, b in zip(marks[:-1], marks[1:]):
+    d = F[:, b] - F[:, a]
+    print(f"{a:2d}->{b:2d}  {d[one].mean() / 1e3:8.2f}  {d[two].mean() / 1e3:8.2f}")
+A = buf[AGG:AGG + 8 * 4096].reshape(4096, 8)
+A = A[A[:, 0] > 0]
+if len(A):
+    print(f"aggregate: {len(A)} CTAs; first start {(A[:, 0].min() - end.max()) / 1e3:.2f} us after "
+          f"the fused kernel's last CTA, last end {(A[:, 4].max() - end.max()) / 1e3:.2f} us after")
+    for k, col in ((0, 1), (1, 2)):
+        m = A[:, col] > 0
+        if m.any():
+            a = A[m]
+            pc = lambda v: np.percentile(v, [0, 50, 100]).astype(int)  # noqa: E731
+            print(f"  kind {k}: n={m.sum()} scales+sync {pc(a[:, col] - a[:, 0])} ns, "
+                  f"loop {pc(a[:, 3] - a[:, col])}, epilogue {pc(a[:, 4] - a[:, 3])}")

@@ -26,9 +26,14 @@ bool throws(F&& f) {
     f();
   } catch (const E&) {
     return true;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "unexpected exception: %s\n", e.what());
+    return false;
   } catch (...) {
+    std::fprintf(stderr, "unexpected non-std exception\n");
     return false;
   }
+  std::fprintf(stderr, "no exception\n");
   return false;
 }
 

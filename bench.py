@@ -117,6 +117,23 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+def ncu_traffic(model, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture (profiles/*_<model>_ncu_traffic.json),
+    or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{model.split('_')[0]}_ncu_traffic.json")))
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                k = json.load(fh)["kernels"].get(kernel)
+            if k:
+                return k["traffic_bytes"], os.path.relpath(f, ROOT)
+        except Exception:
+            pass
+    return None, None
+
+
 def workload_config(model, world):
     kind, opts, strat, batch, data_n, _, _, arch = MODELS[model]
     return {"workload": f"{model} DPSGD step ({arch})", "model": model,
@@ -364,10 +381,12 @@ def run_ours(args):
         flops = MFLOP * 1e6 * BATCH
         ach = flops / (dom_ms * 1e-3) / 1e12
         fp32_peak = 148 * 128 * 2 * (clocks.max_mhz or 1965) * 1e6 / 1e12
+        traffic, tsrc = ncu_traffic(args.model, "fused_kernel")
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": ach, "peak": bf16,
-                "unit": "TFLOP/s", "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
-                "engine": "fp32 FFMA on CUDA cores (per-example GEMMs too small for tcgen05 "
-                          "tiles, DESIGN.md)",
+                "unit": "TFLOP/s", "frac": ach / bf16, "traffic": traffic,
+                "traffic_source": tsrc, "peak_kind": peak_kind,
+                "engine": "fp32 FFMA/FFMA2 on CUDA cores; per-example GEMMs are 16-256 wide and "
+                          "run shared-memory-bandwidth bound (DESIGN.md 3.1)",
                 "fp32_simt_peak_tflops": fp32_peak, "frac_of_fp32_simt_peak": ach / fp32_peak,
                 "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
     elif dom_name.endswith("_tc"):
@@ -383,9 +402,10 @@ def run_ours(args):
     if "aggregate" in by_name:
         agg_b = aggregate_bytes(desc, BATCH, fused)
         am = by_name["aggregate"]
+        atraffic, _ = ncu_traffic(args.model, "aggregate_kernel")
         agg = {"kernel": "aggregate", "bound": "hbm", "achieved": agg_b / (am * 1e-3) / 1e9,
                "peak": hbm, "unit": "GB/s", "frac": agg_b / (am * 1e-3) / 1e9 / hbm,
-               "traffic": None, "algorithmic_bytes": agg_b, "share_of_step": am / step_ms,
+               "traffic": atraffic, "algorithmic_bytes": agg_b, "share_of_step": am / step_ms,
                "avg_launch_us": am * 1e3}
         if roof is None:
             roof = agg

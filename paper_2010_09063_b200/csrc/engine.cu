@@ -145,6 +145,9 @@ struct Engine {
   // fused MNIST factors
   float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
   float* d_w2t = nullptr;  // conv2 weights kept transposed [k][d] for the fused kernel
+  float* d_noise = nullptr;   // (P) the step's normals, drawn by the fused kernel
+  float* d_scale = nullptr;   // (B) clip factors, finalised by the fused kernel
+  int* d_clipflag = nullptr;  // (B)
   std::vector<float*> d_dense_g;  // per dense layer: output cotangent (B, out)
 
   // pinned host staging
@@ -287,6 +290,9 @@ struct Engine {
       want((void**)&d_h, sizeof(float) * B * 32);
       want((void**)&d_dz2, sizeof(float) * B * 10);
       want((void**)&d_w2t, sizeof(float) * 32 * 256);
+      want((void**)&d_noise, sizeof(float) * P);
+      want((void**)&d_scale, sizeof(float) * B);
+      want((void**)&d_clipflag, sizeof(int) * B);
     }
     d_dense_g.assign(n, nullptr);
     for (int l = 0; l < n; ++l)
@@ -582,6 +588,18 @@ struct Engine {
     prm.normsq = d_parts;
     prm.err = d_err;
     prm.B = (int)B;
+    prm.a = cur_args;
+    prm.norms = d_norms;
+    prm.scale = d_scale;
+    prm.clipped = d_clipflag;
+    prm.noise = d_noise;
+    long long pairs = 0;
+    for (int p = 0; p < 8; ++p) {
+      prm.size[p] = desc.param_size[p];
+      prm.pair_off[p] = pairs;
+      pairs += (desc.param_size[p] + 1) / 2;
+    }
+    prm.pair_off[8] = pairs;
     mnist::fused_kernel<<<(unsigned)B, mnist::NT, sizeof(mnist::Smem), s>>>(prm);
     return mark(s, "mnist_fused");
   }
@@ -709,7 +727,7 @@ struct Engine {
       nk += mark(s, "sumsq");
       nk += enqueue_aggregate(s, ut, ut.n, U);
     } else {
-      nk += enqueue_aggregate(s, table_for(x_slot), nparts, (int)B);
+      nk += enqueue_aggregate(s, table_for(x_slot), nparts, (int)B, fused_mnist);
     }
     return nk;
   }
@@ -739,8 +757,15 @@ struct Engine {
     return sizeof(float) * (((U + 3) & ~3) + kAggWarps * kAggChunk * kAggRows);
   }
 
-  AggLaunch agg_launch(const BlockTable& t, int np, int U, int mode) {
+  // from_fused: the fused MNIST kernel already produced this step's clip
+  // factors, norms, clip flags and noise (units == examples).
+  AggLaunch agg_launch(const BlockTable& t, int np, int U, int mode, bool from_fused = false) {
     AggLaunch L{};
+    if (from_fused) {
+      L.scales = d_scale;
+      L.clip_flags = d_clipflag;
+      L.noise = d_noise;
+    }
     L.bt = t;
     agg_plan(t, L.plan);
     L.a = cur_args;
@@ -760,13 +785,14 @@ struct Engine {
     aggregate_kernel<<<L.plan.tile_start[L.plan.n], 32 * kAggWarps, agg_smem(L.U), s>>>(L);
   }
 
-  int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U) {
+  // ff: the step's tail inputs come from the fused MNIST kernel that just ran
+  int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
     if (world == 1) {
-      launch_agg(agg_launch(t, np, U, 0), s);
+      launch_agg(agg_launch(t, np, U, 0, ff), s);
       nk += mark(s, "aggregate");
     } else {
-      launch_agg(agg_launch(t, np, U, 1), s);
+      launch_agg(agg_launch(t, np, U, 1, ff), s);
       nk += mark(s, "aggregate_local");
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
@@ -890,9 +916,11 @@ struct Engine {
       sg.noise_args.a = cur_args;
       set_node(sg.exec, sg.noise, &sg.noise_args);
     }
-    if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot)) {
+    if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot ||
+                     !same_args(sg.fused_args.a, cur_args))) {
       sg.fused_args.x = x_slot;
       sg.fused_args.y = y_slot;
+      sg.fused_args.a = cur_args;
       set_node(sg.exec, sg.fused, &sg.fused_args);
     }
   }

@@ -35,6 +35,32 @@ __device__ __forceinline__ void raise_index(DevError* e, int what, long long pos
   }
 }
 
+// Packed fp32 FMA (sm_100 FFMA2): {a0, a1} += w * {x0, x1}, each lane of the
+// pair rounded exactly like fmaf. ptxas folds the scalar w into a broadcast
+// operand, so one instruction does two fused multiply-adds.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, float x1) {
+  unsigned long long acc, xx, ww;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xx) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(ww), "l"(xx));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
+// {a0, a1} += {w0, w1} * x
+__device__ __forceinline__ void ffma2v(float& a0, float& a1, float w0, float w1, float x) {
+  ffma2(a0, a1, x, w0, w1);
+}
+// {a0, a1} += {x0, x1} * {y0, y1} (element-wise)
+__device__ __forceinline__ void ffma2pp(float& a0, float& a1, float x0, float x1, float y0,
+                                        float y1) {
+  unsigned long long acc, xx, yy;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xx) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(yy) : "f"(y0), "f"(y1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(yy));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
+
 // checked_id (kernels.hpp:475-489): integral and within [0, V).
 __device__ __forceinline__ bool valid_id(float raw, int V) {
   return raw == rintf(raw) && raw >= 0.0f && raw < float(V);
@@ -646,6 +672,10 @@ __device__ __forceinline__ void agg_scales(const double* __restrict__ parts, int
   if ((threadIdx.x & 31) == 0) cnt_sh[threadIdx.x >> 5] = local_clipped;
 }
 
+struct AggLaunch;
+__device__ __forceinline__ void agg_prologue(const AggLaunch& L, float* s_sh, float* norms_cta,
+                                             int* cnt_sh);
+
 // Everything one aggregation launch needs, passed by value as the kernel's
 // single parameter: a CUDA-graph replay swaps in the step's arguments with
 // one kernel-node parameter update (no host-to-device copy on the stream).
@@ -659,8 +689,30 @@ struct AggLaunch {
   float* norms_out;     // (U), written by CTA 0
   int* clipped_out;     // written (not accumulated) by CTA 0
   const DevError* err;
+  // set when the per-example kernel already finalised the step's tail
+  // inputs (fused MNIST): clip factors, clip flags and the noise vector
+  const float* scales;      // (U) or null: computed from parts
+  const int* clip_flags;    // (U)
+  const float* noise;       // (P) or null: drawn here
   int U, nparts, mode;
 };
+
+// Clip factors into shared memory: copied when the per-example kernel
+// finalised them, else computed from the fp64 norm partials.
+__device__ __forceinline__ void agg_prologue(const AggLaunch& L, float* s_sh, float* norms_cta,
+                                             int* cnt_sh) {
+  if (L.scales) {
+    int local = 0;
+    for (int i = threadIdx.x; i < L.U; i += blockDim.x) {
+      s_sh[i] = L.scales[i];
+      if (norms_cta) local += L.clip_flags[i];
+    }
+    local = __reduce_add_sync(0xffffffffu, local);
+    if ((threadIdx.x & 31) == 0) cnt_sh[threadIdx.x >> 5] = local;
+  } else {
+    agg_scales(L.parts, L.nparts, L.U, L.a.clip, s_sh, norms_cta, cnt_sh);
+  }
+}
 
 __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
   const BlockTable& bt = L.bt;
@@ -688,6 +740,8 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
     j = (long long)(tile.j0 + rr) * bt.out[p] + c;
   }
   const float cur = (has_col && mode == 0) ? params[bt.param_off[p] + j] : 0.0f;
+  const float pre_noise =
+      (has_col && mode == 0 && L.noise && a.add_noise) ? L.noise[bt.param_off[p] + j] : 0.0f;
   const bool failed = L.err && L.err->code != 0;
   const int rows = (U + kAggWarps - 1) / kAggWarps;
   const int i0 = min(U, warp * rows), i1 = min(U, i0 + rows);
@@ -720,9 +774,9 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
       }
     };
     load(i0);  // in flight while the clip factors are computed
-    agg_scales(parts, nparts, U, a.clip, s_sh, norms_cta, cnt_sh);
+    agg_prologue(L, s_sh, norms_cta, cnt_sh);
     __syncthreads();
-    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 1);
+    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 1);
     for (int ib = i0; ib < i1; ib += kAggBatch) {
       if (ib != i0) load(ib);
 #pragma unroll
@@ -764,9 +818,9 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
       }
     };
     load(i0);
-    agg_scales(parts, nparts, U, a.clip, s_sh, norms_cta, cnt_sh);
+    agg_prologue(L, s_sh, norms_cta, cnt_sh);
     __syncthreads();
-    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 2);
+    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 2);
     for (int ib = i0; ib < i1; ib += kAggChunk) {
       if (ib != i0) load(ib);
 #pragma unroll
@@ -793,7 +847,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
     for (int r = 0; r < kAggRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
   }
   __syncthreads();
-    PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 3);
+    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 3);
 
   // ---- epilogue: one thread per column of the tile ----
   if (blockIdx.x == 0 && threadIdx.x == 0 && L.clipped_out) {
@@ -812,10 +866,14 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
     return;
   }
   if (a.add_noise) {
-    // the pair's two normals come from one Box-Muller draw (kernels.hpp:597-614)
-    float n0, n1;
-    gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
-    sum = __fadd_rn(sum, __fmul_rn(__fmul_rn(a.sigma, a.clip), (j & 1) ? n1 : n0));
+    float n = pre_noise;
+    if (!L.noise) {
+      // the pair's two normals come from one Box-Muller draw (kernels.hpp:597-614)
+      float n0, n1;
+      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
+      n = (j & 1) ? n1 : n0;
+    }
+    sum = __fadd_rn(sum, __fmul_rn(__fmul_rn(a.sigma, a.clip), n));
   }
   sum = __fmul_rn(sum, a.inv_units);
   if (failed) return;

@@ -39,6 +39,7 @@ struct Smem {
   float w2t[KC2 * D2];               // conv2 weights, swizzled transpose (TMA):
                                      //   W2[d][k] at [k*32 + (d ^ (k & 31))]
   float w1[D1 * K1 * K1];            // conv1 weights [d][u][v]        (TMA)
+  float w1t[K1 * K1 * D1];           // the same, [u][v][d] (channels contiguous)
   float b1[D1];                      //                                (TMA)
   float b2[D2];                      //                                (TMA)
   float xs[XP * XS];                 // padded input, row stride XS
@@ -84,6 +85,14 @@ struct Params {
   double* normsq;       // (B)         squared global per-example norm
   DevError* err;
   int B;
+  // step tail work done here so the aggregation kernel only streams:
+  StepArgs a;           // the step's DP arguments
+  float* norms;         // (B) pre-clip norms            (dpsgd.cpp:254-270)
+  float* scale;         // (B) clip factors              (dpsgd.cpp:91-99)
+  int* clipped;         // (B) 1 where norm > C
+  float* noise;         // (P) the step's normals n_j    (dpsgd.cpp:308-316), or null
+  long long size[8];    // parameter block sizes
+  long long pair_off[9];  // prefix sums of ceil(|p| / 2)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -150,49 +159,53 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     if (!(r >= 0 && r < H0 && c >= 0 && c < H0)) S.xs[i] = 0.0f;
   }
   __syncthreads();  // barrier initialised before anyone waits on it
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
   mbar_wait0(&S.bar[0]);
   for (int i = t; i < H0 * H0; i += NT) S.xs[(i / H0 + 3) * XS + i % H0 + 3] = S.u1.xstage[i];
+  for (int i = t; i < D1 * K1 * K1; i += NT) S.w1t[(i % 64) * D1 + i / 64] = S.w1[i];
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
 
-  // ---- conv1 + relu: thread = (position, half of the channels) -----------
-  // The 8x8 window streams through registers one kernel row at a time.
-  if (t < 2 * NP1) {
-    const int pos = t % NP1, dh = t / NP1;
-    const int oy = pos / O1, ox = pos % O1;
-    float acc[8];
+  // ---- conv1 + relu: thread = (two horizontally adjacent positions, 4 channels)
+  // Per kernel row u the two 8-tap windows share one 10-value input segment;
+  // each tap is one broadcast 16-byte load of 4 channel weights and two packed
+  // FMAs (FFMA2) per position.
+  if (t < 4 * (NP1 / 2)) {
+    const int pp = t % (NP1 / 2), cq = t / (NP1 / 2);
+    const int oy = pp / (O1 / 2), ox0 = 2 * (pp % (O1 / 2));
+    float acc[2][4];
 #pragma unroll
-    for (int d = 0; d < 8; ++d) acc[d] = 0.0f;
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) acc[q][d] = 0.0f;
 #pragma unroll 2
     for (int u = 0; u < K1; ++u) {
-      float win[K1];
+      float seg[K1 + 2];
+      const float2* x2 = reinterpret_cast<const float2*>(S.xs + (2 * oy + u) * XS + 2 * ox0);
 #pragma unroll
-      for (int v = 0; v < K1; ++v) win[v] = S.xs[(2 * oy + u) * XS + 2 * ox + v];
+      for (int v = 0; v < (K1 + 2) / 2; ++v) {
+        const float2 x = x2[v];
+        seg[2 * v] = x.x;
+        seg[2 * v + 1] = x.y;
+      }
 #pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        const float4* w4 = reinterpret_cast<const float4*>(S.w1 + (dh * 8 + d) * K1 * K1 + u * K1);
-        const float4 wa = w4[0], wb = w4[1];
-        float s = acc[d];
-        s = fmaf(wa.x, win[0], s);
-        s = fmaf(wa.y, win[1], s);
-        s = fmaf(wa.z, win[2], s);
-        s = fmaf(wa.w, win[3], s);
-        s = fmaf(wb.x, win[4], s);
-        s = fmaf(wb.y, win[5], s);
-        s = fmaf(wb.z, win[6], s);
-        s = fmaf(wb.w, win[7], s);
-        acc[d] = s;
+      for (int v = 0; v < K1; ++v) {
+        const float4 w = *reinterpret_cast<const float4*>(S.w1t + (u * K1 + v) * D1 + cq * 4);
+        ffma2v(acc[0][0], acc[0][1], w.x, w.y, seg[v]);
+        ffma2v(acc[0][2], acc[0][3], w.z, w.w, seg[v]);
+        ffma2v(acc[1][0], acc[1][1], w.x, w.y, seg[v + 2]);
+        ffma2v(acc[1][2], acc[1][3], w.z, w.w, seg[v + 2]);
       }
     }
 #pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const int dd = dh * 8 + d;
-      S.a1[dd * NP1 + pos] = fmaxf(acc[d] + S.b1[dd], 0.0f);
+    for (int d = 0; d < 4; ++d) {
+      const int dd = cq * 4 + d;
+      S.a1[dd * NP1 + oy * O1 + ox0] = fmaxf(acc[0][d] + S.b1[dd], 0.0f);
+      S.a1[dd * NP1 + oy * O1 + ox0 + 1] = fmaxf(acc[1][d] + S.b1[dd], 0.0f);
     }
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
 
   // ---- maxpool 2x2/2 (first max in window order, kernels.hpp:377-396) -------
   for (int i = t; i < D1 * PO * PO; i += NT) {
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.pidx[i] = (unsigned char)slot;
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
 
   // ---- conv2 im2col: buf[k][pos], k = (c,u,v), pos = (oy,ox) -------------
   for (int i = t; i < KC2 * NP2; i += NT) {
@@ -216,7 +229,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.buf[i] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
 
   // ---- conv2 + relu: lane = out channel, warp = (K slice of 32, 8 positions)
   mbar_wait0(&S.bar[1]);
@@ -231,20 +244,16 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
       const float w = S.w2t[k * D2 + (d ^ (k & 31))];
       const float4* cr = reinterpret_cast<const float4*>(S.buf + k * NP2 + ph * 8);
       const float4 c0 = cr[0], c1 = cr[1];
-      acc[0] = fmaf(w, c0.x, acc[0]);
-      acc[1] = fmaf(w, c0.y, acc[1]);
-      acc[2] = fmaf(w, c0.z, acc[2]);
-      acc[3] = fmaf(w, c0.w, acc[3]);
-      acc[4] = fmaf(w, c1.x, acc[4]);
-      acc[5] = fmaf(w, c1.y, acc[5]);
-      acc[6] = fmaf(w, c1.z, acc[6]);
-      acc[7] = fmaf(w, c1.w, acc[7]);
+      ffma2(acc[0], acc[1], w, c0.x, c0.y);
+      ffma2(acc[2], acc[3], w, c0.z, c0.w);
+      ffma2(acc[4], acc[5], w, c1.x, c1.y);
+      ffma2(acc[6], acc[7], w, c1.z, c1.w);
     }
 #pragma unroll
     for (int p = 0; p < 8; ++p) S.u1.part[(ks * NP2 + ph * 8 + p) * D2 + d] = acc[p];
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
   {  // i = pos*32 + d
     const int d = t % D2, p = t / D2;
     float s = 0.0f;
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.a2[d * NP2 + p] = fmaxf(s + S.b2[d], 0.0f);
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
 
   // ---- fc1 (512->32) + relu: lane = unit, warp = 32-row slice -------------
   // The warp's 32x32 slice of W3 (coalesced rows) stays in registers for the
@@ -263,49 +272,80 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   for (int r = 0; r < 32; ++r) wv[r] = __ldg(gW3 + (warp * 32 + r) * H1 + lane);
   {
     float s0 = 0.0f, s1 = 0.0f;
+    const float2* a22 = reinterpret_cast<const float2*>(S.a2 + warp * 32);
 #pragma unroll
     for (int r = 0; r < 32; r += 2) {
-      s0 = fmaf(S.a2[warp * 32 + r], wv[r], s0);
-      s1 = fmaf(S.a2[warp * 32 + r + 1], wv[r + 1], s1);
+      const float2 av = a22[r / 2];
+      ffma2pp(s0, s1, av.x, av.y, wv[r], wv[r + 1]);
     }
     S.u1.z1[warp * H1 + lane] = s0 + s1;
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
   if (warp == 0) {
     // fc1 bias + relu, fc2 (32->10), softmax cross-entropy (kernels.hpp:516-566)
-    // and dz1 = (W4 dz2) * [h > 0], all in registers with warp shuffles
-    float z = S.b3[lane];
-#pragma unroll 1
-    for (int w = 0; w < NW; ++w) z += S.u1.z1[w * H1 + lane];
-    const float hv = fmaxf(z, 0.0f);
+    // and dz1 = (W4 dz2) * [h > 0]. Lane j holds h_j; the 10 logits are
+    // butterfly sums (every lane ends with all of them), so the softmax, the
+    // loss and dlogits are computed redundantly per lane without further
+    // communication (the exp-sum in the reference's class order).
+    float zp[4] = {S.b3[lane], 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int w = 0; w < NW; ++w) zp[w & 3] += S.u1.z1[w * H1 + lane];
+    const float hv = fmaxf((zp[0] + zp[1]) + (zp[2] + zp[3]), 0.0f);
     S.h[lane] = hv;
-    const int cl = lane < NC ? lane : NC - 1;
-    float lg = S.b4[cl];
-#pragma unroll 1
-    for (int j = 0; j < H1; ++j) lg = fmaf(__shfl_sync(0xffffffffu, hv, j), S.w4[j * NC + cl], lg);
+    float pr[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) pr[c] = hv * S.w4[lane * NC + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) pr[c] += __shfl_xor_sync(0xffffffffu, pr[c], o);
     const float raw = S.yb;
     const bool ok = valid_id(raw, NC);
     if (!ok && lane == 0) raise_index(prm.err, 0, b, raw, NC);
     const int y = ok ? (int)raw : 0;
-    float m = lane < NC ? lg : -INFINITY;
+    float m = -INFINITY, ly = 0.0f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float e = lane < NC ? expf(lg - m) : 0.0f;
-    float se = e;
+    for (int c = 0; c < NC; ++c) {
+      pr[c] += S.b4[c];
+      m = fmaxf(m, pr[c]);
+      ly = c == y ? pr[c] : ly;
+    }
+    float e[NC], se = 0.0f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-    const float g = (ok && lane < NC) ? e / se - (lane == y ? 1.0f : 0.0f) : 0.0f;
-    if (lane < NC) S.dz2[lane] = g;
-    const float ly = __shfl_sync(0xffffffffu, lg, y);
-    if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
+    for (int c = 0; c < NC; ++c) {
+      e[c] = expf(pr[c] - m);
+      se += e[c];
+    }
     float g1 = 0.0f;
-#pragma unroll 1
-    for (int c = 0; c < NC; ++c) g1 = fmaf(S.w4[lane * NC + c], __shfl_sync(0xffffffffu, g, c), g1);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const float g = ok ? e[c] / se - (c == y ? 1.0f : 0.0f) : 0.0f;
+      if (lane == c) S.dz2[c] = g;
+      g1 = fmaf(S.w4[lane * NC + c], g, g1);
+    }
+    if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
     S.dz1[lane] = hv > 0.0f ? g1 : 0.0f;
+  } else if (warp < 3 && prm.noise && prm.a.add_noise) {
+    // meanwhile warps 1-2 draw this CTA's share of the step's Gaussian noise
+    // (one Box-Muller pair per thread, kernels.hpp:597-614)
+    const long long pairs = prm.pair_off[8];
+    const long long per = (pairs + gridDim.x - 1) / gridDim.x;
+    for (long long k = t - 32; k < per; k += 64) {
+      const long long q = (long long)b * per + k;
+      if (q >= pairs) break;
+      int p = 0;
+      while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
+      const long long jp = q - prm.pair_off[p];
+      float n0, n1;
+      gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
+      float* dst = prm.noise + prm.off[p] + 2 * jp;
+      dst[0] = n0;
+      if (2 * jp + 1 < prm.size[p]) dst[1] = n1;
+    }
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
 
   // ---- fc1 backward data: da2[i] = W3[i,:] . dz1, relu mask -> dc2 --------
   // From the register-resident W3 slice: products W3[r][lane] * dz1[lane],
@@ -333,7 +373,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.dc2t[i] = v;  // [d][pos] == flatten order
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
 
   double sq = 0.0;  // this thread's share of ||g_i||^2
   const size_t bo = (size_t)b;
@@ -357,10 +397,8 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
 #pragma unroll
       for (int q = 0; q < NP2 / 4; ++q) {
         const float4 g = g4[q];
-        acc0 = fmaf(g.x, cv[4 * q], acc0);
-        acc1 = fmaf(g.y, cv[4 * q + 1], acc1);
-        acc0 = fmaf(g.z, cv[4 * q + 2], acc0);
-        acc1 = fmaf(g.w, cv[4 * q + 3], acc1);
+        ffma2pp(acc0, acc1, g.x, g.y, cv[4 * q], cv[4 * q + 1]);
+        ffma2pp(acc0, acc1, g.z, g.w, cv[4 * q + 2], cv[4 * q + 3]);
       }
       const float acc = acc0 + acc1;
       out[d * KC2 + k] = acc;
@@ -374,7 +412,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     sq = fma((double)s, (double)s, sq);
   }
   __syncthreads();  // buf (patches) is overwritten with dcols below
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
 
   // ---- conv2 backward data: dcols[pos][(u,v),c] = sum_d W2[d][c,u,v] dc2[pos][d]
   // thread = (k, half of the positions), lanes on consecutive k: column k of
@@ -394,10 +432,8 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
 #pragma unroll
       for (int q = 0; q < D2 / 4; ++q) {
         const float4 g = g4[q];
-        acc0 = fmaf(wr[4 * q], g.x, acc0);
-        acc1 = fmaf(wr[4 * q + 1], g.y, acc1);
-        acc0 = fmaf(wr[4 * q + 2], g.z, acc0);
-        acc1 = fmaf(wr[4 * q + 3], g.w, acc1);
+        ffma2pp(acc0, acc1, wr[4 * q], wr[4 * q + 1], g.x, g.y);
+        ffma2pp(acc0, acc1, wr[4 * q + 2], wr[4 * q + 3], g.z, g.w);
       }
       S.buf[p * KC2 + uv * C2 + c] = acc0 + acc1;
     }
@@ -421,7 +457,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.up.dp1[c * PO * PO + r] = s;
   }
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
   // maxpool backward (route to the first max) + relu mask on a1 -> d1 [pos][d]
   // Thread t always has channel d = t % 16 (NT % 16 == 0), so it also keeps a
   // partial of the conv1 bias gradient sum_pos d1[pos][d].
@@ -437,7 +473,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
   if (lane < D1) S.b1red[warp][lane] = b1part;
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
 
   // ---- conv1 per-example dW: thread = (tap, 8 channels, quarter of the rows)
   {
@@ -455,14 +491,10 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
         const float xv = xr[2 * ox];
         const float4 ga = g4[ox * 4];
         const float4 gb = g4[ox * 4 + 1];
-        acc[0] = fmaf(ga.x, xv, acc[0]);
-        acc[1] = fmaf(ga.y, xv, acc[1]);
-        acc[2] = fmaf(ga.z, xv, acc[2]);
-        acc[3] = fmaf(ga.w, xv, acc[3]);
-        acc[4] = fmaf(gb.x, xv, acc[4]);
-        acc[5] = fmaf(gb.y, xv, acc[5]);
-        acc[6] = fmaf(gb.z, xv, acc[6]);
-        acc[7] = fmaf(gb.w, xv, acc[7]);
+        ffma2v(acc[0], acc[1], ga.x, ga.y, xv);
+        ffma2v(acc[2], acc[3], ga.z, ga.w, xv);
+        ffma2v(acc[4], acc[5], gb.x, gb.y, xv);
+        ffma2v(acc[6], acc[7], gb.z, gb.w, xv);
       }
     }
     // combine the four row quarters through shared memory (buf is free)
@@ -471,7 +503,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
       for (int c = 0; c < 8; ++c) S.buf[((qr - 1) * D1 + dg * 8 + c) * 64 + k] = acc[c];
     }
     __syncthreads();
-    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
+    PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
     if (qr == 0) {
       float* out = prm.st_c1w + bo * (D1 * K1 * K1);
 #pragma unroll
@@ -522,14 +554,21 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
 #pragma unroll
     for (int q = 0; q < 5; ++q) S.red5[q][warp] = v5[q];
   __syncthreads();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 16);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 16);
   if (t == 0) {
     double r5[5] = {0, 0, 0, 0, 0};
     for (int w = 0; w < NW; ++w)
 #pragma unroll
       for (int q = 0; q < 5; ++q) r5[q] += S.red5[q][w];
     // ||a (x) d||^2 = ||a||^2 ||d||^2 (weight) + ||d||^2 (bias), strategies.cpp:140-148
-    prm.normsq[b] = r5[0] + r5[3] * (r5[1] + 1.0) + r5[4] * (r5[2] + 1.0);
+    const double nsq = r5[0] + r5[3] * (r5[1] + 1.0) + r5[4] * (r5[2] + 1.0);
+    prm.normsq[b] = nsq;
+    // norm and clip factor of this example (dpsgd.cpp:254-270, :91-99)
+    const float nrm = (float)sqrt(nsq);
+    const float C = prm.a.clip;
+    prm.norms[b] = nrm;
+    prm.scale[b] = nrm > C ? __fdiv_rn(C, nrm) : 1.0f;
+    prm.clipped[b] = nrm > C ? 1 : 0;
     PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
   }
 }

@@ -15,7 +15,19 @@ __device__ unsigned long long* g_trace = nullptr;
       ::pgb::g_trace[(slot)] = t_;                                               \
     }                                                                            \
   } while (0)
+// After a __syncthreads(): BAR.SYNC does not block at issue (the wait is
+// deferred to the next dependent instruction), so a timestamp taken right
+// after it records the barrier's issue, not its release. A second barrier
+// blocks until the first has released.
+#define PGB_MARK_BAR(slot) \
+  do {                     \
+    __syncthreads();       \
+    PGB_MARK(slot);        \
+  } while (0)
 #else
+#define PGB_MARK_BAR(slot) \
+  do {                     \
+  } while (0)
 #define PGB_MARK(slot) \
   do {                 \
   } while (0)

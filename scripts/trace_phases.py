@@ -41,7 +41,7 @@ _lib.check(L.pgb_debug_trace(C.c_void_p(buf.ctypes.data), SLOTS))
 
 F = buf[FUSED:FUSED + 24 * B].reshape(B, 24)
 t0 = F[:, 0].min()
-marks = [k for k in range(24) if F[:, k].all()]
+marks = sorted([k for k in range(24) if F[:, k].all()], key=lambda k: F[0, k])
 end = F[:, marks[-1]]
 order = np.argsort(end)
 one, two = order[:30], order[-100:]

@@ -333,8 +333,10 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clocks:
         ev0.record(stream)
+        h0 = time.perf_counter()
         for i in range(args.steps):
             step(args.warmup + i)
+        host_issue = (time.perf_counter() - h0) / args.steps
         ev1.record(stream)
         ev1.synchronize()
         _lib.check(_lib.lib.pgb_synchronize(engine.handle, None, None))
@@ -445,6 +447,8 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "gpu_launches": kps * args.steps,
             "kernels_per_step": kps,
+            "host_issue_us_per_step": round(host_issue * 1e6, 2),
+            "e2e_us_per_step": round(e2e_t / e_steps * 1e6, 2),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

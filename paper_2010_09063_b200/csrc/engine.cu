@@ -124,15 +124,40 @@ struct Engine {
   int64_t in_row = 0;
   int first_param_layer = 0;
 
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  static constexpr int kSlots = 3;  // epoch driver: input / result ring depth
+  cudaStream_t stream = nullptr, copy_stream = nullptr, out_stream = nullptr;
+  // epoch-driver staging (pinned, grown on demand) and events
+  float* h_norm_stage = nullptr;
+  int* h_clip_stage = nullptr;
+  int64_t stage_steps = 0, stage_units = 0;
+  cudaEvent_t ev_copied[kSlots] = {}, ev_consumed[kSlots] = {}, ev_done[kSlots] = {},
+              ev_read[kSlots] = {};
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+
+  void ensure_host_stage(int64_t steps, int64_t units) {
+    if (steps <= stage_steps && units <= stage_units) return;
+    if (h_norm_stage) cudaFreeHost(h_norm_stage);
+    if (h_clip_stage) cudaFreeHost(h_clip_stage);
+    h_norm_stage = nullptr;
+    h_clip_stage = nullptr;
+    stage_steps = std::max(steps, stage_steps);
+    stage_units = std::max(units, stage_units);
+    PGB_CUDA(cudaMallocHost(&h_norm_stage, sizeof(float) * stage_steps * stage_units));
+    PGB_CUDA(cudaMallocHost(&h_clip_stage, sizeof(int) * 2 * stage_steps));
+  }
   // arena
   char* arena = nullptr;
   size_t arena_bytes = 0;
   float* d_params = nullptr;
   float* d_x = nullptr;
   float* d_y = nullptr;
-  float* d_xb[2] = {nullptr, nullptr};
-  float* d_yb[2] = {nullptr, nullptr};
+  float* d_xb[kSlots] = {};
+  float* d_yb[kSlots] = {};
+  float* d_norms_ring = nullptr;    // (kSlots, B)
+  int* d_clip_ring = nullptr;       // (kSlots, 2)
+  // where the next launched step writes its norms / clip count
+  float* norms_dst = nullptr;
+  int* clipped_dst = nullptr;
   float* d_stacks = nullptr;
   float* d_units = nullptr;
   double* d_parts = nullptr;
@@ -186,6 +211,14 @@ struct Engine {
     if (h_err) cudaFreeHost(h_err);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (out_stream) cudaStreamDestroy(out_stream);
+    if (h_norm_stage) cudaFreeHost(h_norm_stage);
+    if (h_clip_stage) cudaFreeHost(h_clip_stage);
+    for (int i = 0; i < kSlots; ++i)
+      for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i], ev_done[i], ev_read[i]})
+        if (ev) cudaEventDestroy(ev);
+    if (ev_t0) cudaEventDestroy(ev_t0);
+    if (ev_t1) cudaEventDestroy(ev_t1);
   }
 
   // The reference MNIST CNN (models.cpp:107-121) runs as one fused kernel.
@@ -267,10 +300,12 @@ struct Engine {
     want((void**)&d_params, sizeof(float) * P);
     want((void**)&d_x, sizeof(float) * B * in_row);
     want((void**)&d_y, sizeof(float) * B);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       want((void**)&d_xb[i], sizeof(float) * B * in_row);
       want((void**)&d_yb[i], sizeof(float) * B);
     }
+    want((void**)&d_norms_ring, sizeof(float) * B * kSlots);
+    want((void**)&d_clip_ring, sizeof(int) * 2 * kSlots);
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
@@ -315,6 +350,8 @@ struct Engine {
       *r.first = arena + o;
       o += r.second;
     }
+    norms_dst = d_norms;
+    clipped_dst = d_clipped;
     // activation chain: act_in(0) = null = the step's input slot
     float* cur = nullptr;
     for (int l = 0; l < n; ++l) {
@@ -435,6 +472,12 @@ struct Engine {
     PGB_CUDA(cudaSetDevice(device));
     PGB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    PGB_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlots; ++i)
+      for (cudaEvent_t* ev : {&ev_copied[i], &ev_consumed[i], &ev_done[i], &ev_read[i]})
+        PGB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    PGB_CUDA(cudaEventCreate(&ev_t0));
+    PGB_CUDA(cudaEventCreate(&ev_t1));
     allocate();
     PGB_CUDA(cudaMallocHost(&h_norms, sizeof(float) * B));
     PGB_CUDA(cudaMallocHost(&h_clipped, sizeof(int) * 2));
@@ -589,7 +632,7 @@ struct Engine {
     prm.err = d_err;
     prm.B = (int)B;
     prm.a = cur_args;
-    prm.norms = d_norms;
+    prm.norms = norms_dst;
     prm.scale = d_scale;
     prm.clipped = d_clipflag;
     prm.noise = d_noise;
@@ -772,8 +815,8 @@ struct Engine {
     L.parts = d_parts;
     L.params = d_params;
     L.sum_out = d_sum;
-    L.norms_out = d_norms;
-    L.clipped_out = d_clipped;
+    L.norms_out = norms_dst;
+    L.clipped_out = clipped_dst;
     L.err = d_err;
     L.U = U;
     L.nparts = np;
@@ -837,7 +880,10 @@ struct Engine {
     const int variant = (m > 1 ? 1 : 0) | (world > 1 ? 2 : 0);
     // the fused MNIST schedule takes its input pointers as updatable node
     // parameters; the layer-wise schedule bakes the input slot into the graph
-    const int key = variant * 4 + (fused_mnist ? 0 : x_slot == d_x ? 0 : x_slot == d_xb[0] ? 1 : 2);
+    int slot_key = 0;
+    for (int i = 0; i < kSlots; ++i)
+      if (x_slot == d_xb[i]) slot_key = i + 1;
+    const int key = variant * (kSlots + 1) + (fused_mnist ? 0 : slot_key);
     if (!graph_enabled) {
       kernels_last = enqueue_step(stream, x_slot, y_slot, m);
       PGB_CUDA(cudaGetLastError());
@@ -908,8 +954,11 @@ struct Engine {
   }
 
   void update_step_nodes(StepGraph& sg, const float* x_slot, const float* y_slot) {
-    if (sg.agg && !same_args(sg.agg_args.a, cur_args)) {
+    if (sg.agg && (!same_args(sg.agg_args.a, cur_args) || sg.agg_args.norms_out != norms_dst ||
+                   sg.agg_args.clipped_out != clipped_dst)) {
       sg.agg_args.a = cur_args;
+      sg.agg_args.norms_out = norms_dst;
+      sg.agg_args.clipped_out = clipped_dst;
       set_node(sg.exec, sg.agg, &sg.agg_args);
     }
     if (sg.noise && !same_args(sg.noise_args.a, cur_args)) {
@@ -917,9 +966,10 @@ struct Engine {
       set_node(sg.exec, sg.noise, &sg.noise_args);
     }
     if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot ||
-                     !same_args(sg.fused_args.a, cur_args))) {
+                     sg.fused_args.norms != norms_dst || !same_args(sg.fused_args.a, cur_args))) {
       sg.fused_args.x = x_slot;
       sg.fused_args.y = y_slot;
+      sg.fused_args.norms = norms_dst;
       sg.fused_args.a = cur_args;
       set_node(sg.exec, sg.fused, &sg.fused_args);
     }
@@ -1271,70 +1321,76 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     if (steps <= 0) raise(PGB_ERR_CONFIG, "run_epoch: fewer examples than one batch");
     const int64_t U = en.B / cfg->microbatch;
     const size_t xb = sizeof(float) * en.B * en.in_row, yb = sizeof(float) * en.B;
-    float* h_norm_stage = nullptr;
-    int* d_clip_acc = nullptr;
-    if (norms_out) PGB_CUDA(cudaMallocHost(&h_norm_stage, sizeof(float) * steps * U));
-    cudaEvent_t copied[2], consumed[2], t0, t1;
-    for (int i = 0; i < 2; ++i) {
-      PGB_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
-      PGB_CUDA(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
-    }
-    PGB_CUDA(cudaEventCreate(&t0));
-    PGB_CUDA(cudaEventCreate(&t1));
-    std::vector<int> clip_counts;
-    int* h_clip_stage = nullptr;
-    PGB_CUDA(cudaMallocHost(&h_clip_stage, sizeof(int) * 2 * steps));
-    (void)d_clip_acc;
+    constexpr int K = Engine::kSlots;
+    // Results go to a ring of K device slots read back on out_stream, so the
+    // per-step D2H never sits between two steps on the compute stream (the
+    // multi-GPU schedule all-reduces the fixed clip counter: results stay on
+    // the compute stream there).
+    const bool ring = en.world == 1;
+    en.ensure_host_stage(steps, U);
+    cudaEvent_t* copied = en.ev_copied;
+    cudaEvent_t* consumed = en.ev_consumed;
+    cudaEvent_t* done = en.ev_done;
+    cudaEvent_t* read = en.ev_read;
     const auto wall0 = std::chrono::steady_clock::now();
-    PGB_CUDA(cudaEventRecord(t0, en.stream));
-    // prologue: batch 0 into slot 0
-    PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, t0, 0));
-    PGB_CUDA(cudaMemcpyAsync(en.d_xb[0], x, xb, cudaMemcpyHostToDevice, en.copy_stream));
-    PGB_CUDA(cudaMemcpyAsync(en.d_yb[0], y, yb, cudaMemcpyHostToDevice, en.copy_stream));
-    PGB_CUDA(cudaEventRecord(copied[0], en.copy_stream));
+    PGB_CUDA(cudaEventRecord(en.ev_t0, en.stream));
+    auto copy_in = [&](int64_t s) {
+      const int sl = (int)(s % K);
+      if (s >= K) PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, consumed[sl], 0));
+      else PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, en.ev_t0, 0));
+      PGB_CUDA(cudaMemcpyAsync(en.d_xb[sl], x + s * en.B * en.in_row, xb, cudaMemcpyHostToDevice,
+                               en.copy_stream));
+      PGB_CUDA(cudaMemcpyAsync(en.d_yb[sl], y + s * en.B, yb, cudaMemcpyHostToDevice,
+                               en.copy_stream));
+      PGB_CUDA(cudaEventRecord(copied[sl], en.copy_stream));
+    };
+    for (int64_t s = 0; s < std::min<int64_t>(K - 1, steps); ++s) copy_in(s);
     for (int64_t s = 0; s < steps; ++s) {
-      const int slot = (int)(s & 1);
-      if (s + 1 < steps) {
-        const int nxt = slot ^ 1;
-        if (s >= 1) PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, consumed[nxt], 0));
-        PGB_CUDA(cudaMemcpyAsync(en.d_xb[nxt], x + (s + 1) * en.B * en.in_row, xb,
-                                 cudaMemcpyHostToDevice, en.copy_stream));
-        PGB_CUDA(cudaMemcpyAsync(en.d_yb[nxt], y + (s + 1) * en.B, yb, cudaMemcpyHostToDevice,
-                                 en.copy_stream));
-        PGB_CUDA(cudaEventRecord(copied[nxt], en.copy_stream));
+      const int sl = (int)(s % K);
+      if (s + K - 1 < steps) copy_in(s + K - 1);
+      PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
+      if (ring) {
+        // slot sl's previous results must have been read back
+        if (s >= K) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[sl], 0));
+        en.norms_dst = en.d_norms_ring + (size_t)sl * en.B;
+        en.clipped_dst = en.d_clip_ring + 2 * sl;
       }
-      PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[slot], 0));
-      en.push_args(en.make_args(*cfg, step0 + s, en.d_xb[slot], en.d_yb[slot]));
-      en.launch_step(en.d_xb[slot], en.d_yb[slot], cfg->microbatch);
-      PGB_CUDA(cudaEventRecord(consumed[slot], en.stream));
+      en.push_args(en.make_args(*cfg, step0 + s, en.d_xb[sl], en.d_yb[sl]));
+      en.launch_step(en.d_xb[sl], en.d_yb[sl], cfg->microbatch);
+      PGB_CUDA(cudaEventRecord(consumed[sl], en.stream));
       // the step's result read back every step (norms, clipped count)
-      PGB_CUDA(cudaMemcpyAsync(h_clip_stage + 2 * s, en.d_clipped, sizeof(int) * 2,
-                               cudaMemcpyDeviceToHost, en.stream));
-      if (h_norm_stage)
-        PGB_CUDA(cudaMemcpyAsync(h_norm_stage + s * U, en.d_norms, sizeof(float) * U,
-                                 cudaMemcpyDeviceToHost, en.stream));
+      cudaStream_t rs = ring ? en.out_stream : en.stream;
+      if (ring) {
+        PGB_CUDA(cudaEventRecord(done[sl], en.stream));
+        PGB_CUDA(cudaStreamWaitEvent(rs, done[sl], 0));
+      }
+      PGB_CUDA(cudaMemcpyAsync(en.h_clip_stage + 2 * s, en.clipped_dst, sizeof(int) * 2,
+                               cudaMemcpyDeviceToHost, rs));
+      if (norms_out)
+        PGB_CUDA(cudaMemcpyAsync(en.h_norm_stage + s * U, en.norms_dst, sizeof(float) * U,
+                                 cudaMemcpyDeviceToHost, rs));
+      if (ring) PGB_CUDA(cudaEventRecord(read[sl], rs));
+    }
+    en.norms_dst = en.d_norms;
+    en.clipped_dst = en.d_clipped;
+    if (ring) {
+      PGB_CUDA(cudaEventRecord(en.ev_t1, en.out_stream));
+      PGB_CUDA(cudaStreamWaitEvent(en.stream, en.ev_t1, 0));
     }
     PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
                              en.stream));
-    PGB_CUDA(cudaEventRecord(t1, en.stream));
-    PGB_CUDA(cudaEventSynchronize(t1));
+    PGB_CUDA(cudaEventRecord(en.ev_t1, en.stream));
+    PGB_CUDA(cudaEventSynchronize(en.ev_t1));
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     float ms = 0;
-    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventElapsedTime(&ms, en.ev_t0, en.ev_t1);
     if (seconds_out) *seconds_out = std::max(wall, ms * 1e-3);
     int64_t tot = 0;
-    for (int64_t s = 0; s < steps; ++s) tot += en.world > 1 ? h_clip_stage[2 * s + 1] : h_clip_stage[2 * s];
+    for (int64_t s = 0; s < steps; ++s)
+      tot += en.world > 1 ? en.h_clip_stage[2 * s + 1] : en.h_clip_stage[2 * s];
     if (clipped_total) *clipped_total = tot;
-    if (norms_out) std::memcpy(norms_out, h_norm_stage, sizeof(float) * steps * U);
-    for (int i = 0; i < 2; ++i) {
-      cudaEventDestroy(copied[i]);
-      cudaEventDestroy(consumed[i]);
-    }
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
-    if (h_norm_stage) cudaFreeHost(h_norm_stage);
-    cudaFreeHost(h_clip_stage);
+    if (norms_out) std::memcpy(norms_out, en.h_norm_stage, sizeof(float) * steps * U);
     en.last_cfg = *cfg;
     en.last_step = step0 + steps - 1;
     en.check_device_error();

@@ -170,6 +170,7 @@ struct Engine {
   // fused MNIST factors
   float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
   float* d_w2t = nullptr;  // conv2 weights kept transposed [k][d] for the fused kernel
+  float* d_w1t = nullptr;  // conv1 weights kept transposed [(u,v)][d]
   float* d_noise = nullptr;   // (P) the step's normals, drawn by the fused kernel
   float* d_scale = nullptr;   // (B) clip factors, finalised by the fused kernel
   int* d_clipflag = nullptr;  // (B)
@@ -325,6 +326,7 @@ struct Engine {
       want((void**)&d_h, sizeof(float) * B * 32);
       want((void**)&d_dz2, sizeof(float) * B * 10);
       want((void**)&d_w2t, sizeof(float) * 32 * 256);
+      want((void**)&d_w1t, sizeof(float) * 16 * 64);
       want((void**)&d_noise, sizeof(float) * P);
       want((void**)&d_scale, sizeof(float) * B);
       want((void**)&d_clipflag, sizeof(int) * B);
@@ -419,10 +421,15 @@ struct Engine {
       set_block(bt, 5, 0, d_dz1, 32);
       set_block(bt, 6, 1, d_dz2, 10, d_h, 32, 10);
       set_block(bt, 7, 0, d_dz2, 10);
-      bt.shadow[2] = d_w2t;  // conv2 W (32, 256) -> [256][32]
-      bt.shadow_rows[2] = 32;
-      bt_stack.shadow[2] = d_w2t;
-      bt_stack.shadow_rows[2] = 32;
+      // conv2 W (32, 256) -> swizzled [256][32]; conv1 W (16, 64) -> [64][16]
+      for (BlockTable* t : {&bt, &bt_stack}) {
+        t->shadow[2] = d_w2t;
+        t->shadow_rows[2] = 32;
+        t->shadow_swz[2] = 31;
+        t->shadow[0] = d_w1t;
+        t->shadow_rows[0] = 16;
+        t->shadow_swz[0] = 0;
+      }
       norms_fused = true;
       nparts = 1;
     } else {
@@ -512,9 +519,10 @@ struct Engine {
   void refresh_shadows(cudaStream_t s) {
     for (int p = 0; p < bt.n; ++p)
       if (bt.shadow[p]) {
-        const int rows = bt.shadow_rows[p], cols = (int)(bt.size[p] / rows);
+        const int rows = bt.shadow_rows[p], cols = (int)(bt.size[p] / rows),
+                  swz = bt.shadow_swz[p];
         transpose_kernel<<<grid_for((size_t)rows * cols), 256, 0, s>>>(
-            d_params + param_off[p], rows, cols, bt.shadow[p]);
+            d_params + param_off[p], rows, cols, swz, bt.shadow[p]);
       }
   }
 
@@ -618,6 +626,7 @@ struct Engine {
     prm.y = y_slot;
     prm.w = d_params;
     prm.w2t = d_w2t;
+    prm.w1t = d_w1t;
     for (int p = 0; p < 8; ++p) prm.off[p] = param_off[p];
     prm.st_c1w = d_stacks + param_off[0] * B;
     prm.st_c1b = d_stacks + param_off[1] * B;

@@ -483,14 +483,16 @@ struct BlockTable {
   // update (row-major (rows, cols) block -> shadow[c * rows + r])
   float* shadow[kMaxBlocks];
   int shadow_rows[kMaxBlocks];
+  int shadow_swz[kMaxBlocks];  // XOR swizzle mask (0: plain transpose)
 };
 
 // Transposed shadow of a (rows, cols) parameter block, rows a power of two:
 // element (r, c) at dst[c * rows + (r ^ (c & (rows - 1)))]. The XOR swizzle
 // makes both a row of the shadow (fixed c) and a column across consecutive c
 // (fixed r) bank-conflict-free once the shadow is bulk-copied to shared memory.
-__host__ __device__ __forceinline__ long long shadow_index(long long r, long long c, int rows) {
-  return c * rows + (r ^ (c & (rows - 1)));
+__host__ __device__ __forceinline__ long long shadow_index(long long r, long long c, int rows,
+                                                           int swz) {
+  return c * rows + (r ^ (c & swz));
 }
 
 __device__ __forceinline__ void write_param(const BlockTable& bt, int p, long long j,
@@ -499,7 +501,7 @@ __device__ __forceinline__ void write_param(const BlockTable& bt, int p, long lo
   if (bt.shadow[p]) {
     const long long cols = bt.size[p] / bt.shadow_rows[p];
     const long long r = j / cols, c = j - r * cols;
-    bt.shadow[p][shadow_index(r, c, bt.shadow_rows[p])] = v;
+    bt.shadow[p][shadow_index(r, c, bt.shadow_rows[p], bt.shadow_swz[p])] = v;
   }
 }
 
@@ -988,11 +990,11 @@ __global__ void sgd_kernel(BlockTable bt, int B, float lr, float* __restrict__ p
 }
 
 // shadow[c * rows + r] = block[r * cols + c] (after a host parameter upload)
-__global__ void transpose_kernel(const float* __restrict__ src, int rows, int cols,
+__global__ void transpose_kernel(const float* __restrict__ src, int rows, int cols, int swz,
                                  float* __restrict__ dst) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
     const int r = e / cols, c = e - r * cols;
-    dst[shadow_index(r, c, rows)] = src[e];
+    dst[shadow_index(r, c, rows, swz)] = src[e];
   }
 }
 

@@ -32,14 +32,14 @@ constexpr int C2 = 16, D2 = 32, K2 = 4, O2 = 4;
 constexpr int KC2 = C2 * K2 * K2;          // 256 = im2col rows of conv2
 constexpr int NP2 = O2 * O2;               // 16 conv2 output positions
 constexpr int F1 = 512, H1 = 32, NC = 10;
+constexpr int DCP = K2 * K2 * 17;           // dcols row pitch: (u,v) rows of 16 c + 1 pad
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
 
 struct Smem {
   float w2t[KC2 * D2];               // conv2 weights, swizzled transpose (TMA):
                                      //   W2[d][k] at [k*32 + (d ^ (k & 31))]
-  float w1[D1 * K1 * K1];            // conv1 weights [d][u][v]        (TMA)
-  float w1t[K1 * K1 * D1];           // the same, [u][v][d] (channels contiguous)
+  float w1t[K1 * K1 * D1];           // conv1 weights [(u,v)][d]       (TMA, transposed shadow)
   float b1[D1];                      //                                (TMA)
   float b2[D2];                      //                                (TMA)
   float xs[XP * XS];                 // padded input, row stride XS
@@ -48,7 +48,8 @@ struct Smem {
     float p1[D1 * PO * PO];          // maxpool output
     float dp1[D1 * PO * PO];         // its cotangent (p1 is dead by then)
   } up;
-  float buf[KC2 * NP2];              // conv2 im2col [k][pos] -> dcols [pos][k] -> dW1 partials
+  float buf[NP2 * DCP];              // conv2 im2col (swizzled [k][pos]) -> dcols (padded
+                                     // [pos][(u,v)][c]) -> conv1 dW partials
   union {
     float xstage[H0 * H0];           // raw image (TMA), padded into xs
     float part[8 * NP2 * D2];        // split-K partials of conv2 fwd [kslice][pos][d]
@@ -71,7 +72,8 @@ struct Params {
   const float* x;       // (B, 1, 28, 28)
   const float* y;       // (B)
   const float* w;       // flat parameters
-  const float* w2t;     // conv2 weights transposed, (256, 32)
+  const float* w2t;     // conv2 weights transposed, (256, 32), swizzled
+  const float* w1t;     // conv1 weights transposed, (64, 16)
   long long off[8];     // parameter block offsets
   float* st_c1w;        // (B, 1024)   per-example conv1 dW
   float* st_c1b;        // (B, 16)
@@ -105,6 +107,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+
+// swizzled slot of im2col element (k, pos)
+__device__ __forceinline__ int im2col_at(int k, int pos) {
+  return k * NP2 + ((((pos >> 2) ^ (k >> 1)) & 3) << 2) + (pos & 3);
 }
 
 __device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(smem_addr(&S.bar[1])), "r"(kBytes1) : "memory");
     bulk_g2s(S.u1.xstage, prm.x + (size_t)b * H0 * H0, sizeof(float) * H0 * H0, &S.bar[0]);
-    bulk_g2s(S.w1, W + prm.off[0], sizeof(float) * D1 * K1 * K1, &S.bar[0]);
+    bulk_g2s(S.w1t, prm.w1t, sizeof(float) * D1 * K1 * K1, &S.bar[0]);
     bulk_g2s(S.b1, W + prm.off[1], sizeof(float) * D1, &S.bar[0]);
     bulk_g2s(S.b2, W + prm.off[3], sizeof(float) * D2, &S.bar[1]);
     bulk_g2s(S.w2t, prm.w2t, sizeof(float) * KC2 * D2, &S.bar[1]);
@@ -162,7 +169,6 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
   mbar_wait0(&S.bar[0]);
   for (int i = t; i < H0 * H0; i += NT) S.xs[(i / H0 + 3) * XS + i % H0 + 3] = S.u1.xstage[i];
-  for (int i = t; i < D1 * K1 * K1; i += NT) S.w1t[(i % 64) * D1 + i / 64] = S.w1[i];
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
 
@@ -223,10 +229,12 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
 
   // ---- conv2 im2col: buf[k][pos], k = (c,u,v), pos = (oy,ox) -------------
+  // 16-byte chunks of a row are XOR-swizzled by (k >> 1) & 3 (im2col_at), so
+  // the per-example dW reads below (lanes on consecutive k) are conflict-free.
   for (int i = t; i < KC2 * NP2; i += NT) {
     const int k = i / NP2, pos = i % NP2;
     const int c = k / 16, u = (k / 4) % 4, v = k % 4, oy = pos / 4, ox = pos % 4;
-    S.buf[i] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
+    S.buf[im2col_at(k, pos)] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
   }
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
@@ -242,8 +250,8 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     for (int kk = 0; kk < 32; ++kk) {
       const int k = ks * 32 + kk;
       const float w = S.w2t[k * D2 + (d ^ (k & 31))];
-      const float4* cr = reinterpret_cast<const float4*>(S.buf + k * NP2 + ph * 8);
-      const float4 c0 = cr[0], c1 = cr[1];
+      const float4 c0 = *reinterpret_cast<const float4*>(S.buf + im2col_at(k, ph * 8));
+      const float4 c1 = *reinterpret_cast<const float4*>(S.buf + im2col_at(k, ph * 8 + 4));
       ffma2(acc[0], acc[1], w, c0.x, c0.y);
       ffma2(acc[2], acc[3], w, c0.z, c0.w);
       ffma2(acc[4], acc[5], w, c1.x, c1.y);
@@ -382,10 +390,9 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   {
     const int k = t & (KC2 - 1), dh = t >> 8;
     float cv[NP2];
-    const float4* c4 = reinterpret_cast<const float4*>(S.buf + k * NP2);
 #pragma unroll
     for (int q = 0; q < NP2 / 4; ++q) {
-      const float4 x = c4[q];
+      const float4 x = *reinterpret_cast<const float4*>(S.buf + im2col_at(k, 4 * q));
       cv[4 * q] = x.x; cv[4 * q + 1] = x.y; cv[4 * q + 2] = x.z; cv[4 * q + 3] = x.w;
     }
     float* out = prm.st_c2w + bo * (D2 * KC2);
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
         ffma2pp(acc0, acc1, wr[4 * q], wr[4 * q + 1], g.x, g.y);
         ffma2pp(acc0, acc1, wr[4 * q + 2], wr[4 * q + 3], g.z, g.w);
       }
-      S.buf[p * KC2 + uv * C2 + c] = acc0 + acc1;
+      S.buf[p * DCP + uv * 17 + c] = acc0 + acc1;
     }
   }
   __syncthreads();
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
       for (int v = 0; v < K2; ++v) {
         const int ox = ix - v;
         if (ox < 0 || ox >= O2) continue;
-        s += S.buf[(oy * O2 + ox) * KC2 + (u * 4 + v) * C2 + c];
+        s += S.buf[(oy * O2 + ox) * DCP + (u * 4 + v) * 17 + c];
       }
     }
     S.up.dp1[c * PO * PO + r] = s;
@@ -475,44 +482,70 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
 
-  // ---- conv1 per-example dW: thread = (tap, 8 channels, quarter of the rows)
+  // ---- conv1 per-example dW: thread = (2 taps, 8 channels, 1/8 of the rows)
+  // Taps (u, v) and (u + 4, v) share every d1 load; the 8 row groups are
+  // combined by a 3-level tree through three free shared buffers (buf, a1,
+  // then u1 once d1 is dead), each level halving the groups.
   {
-    const int k = t % (K1 * K1), dg = (t / (K1 * K1)) & 1, qr = t / (2 * K1 * K1);
-    const int u = k / K1, v = k % K1;
-    const int oy0 = qr < 2 ? 4 * qr : 8 + 3 * (qr - 2), oy1 = qr < 2 ? oy0 + 4 : oy0 + 3;
-    float acc[8];
+    const int kp = t & 31, dg = (t >> 5) & 1, rg = t >> 6;
+    const int u = kp / K1, v = kp % K1;  // taps kp and kp + 32
+    const int oy0 = rg < 6 ? 2 * rg : 6 + rg, oy1 = rg < 6 ? oy0 + 2 : oy0 + 1;
+    float acc0[8], acc1[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
+    for (int c = 0; c < 8; ++c) acc0[c] = acc1[c] = 0.0f;
     for (int oy = oy0; oy < oy1; ++oy) {
-      const float* xr = S.xs + (2 * oy + u) * XS + v;
+      const float* xr0 = S.xs + (2 * oy + u) * XS + v;
+      const float* xr1 = xr0 + 4 * XS;
       const float4* g4 = reinterpret_cast<const float4*>(S.u1.d1 + oy * O1 * D1) + 2 * dg;
 #pragma unroll 7
       for (int ox = 0; ox < O1; ++ox) {
-        const float xv = xr[2 * ox];
+        const float x0 = xr0[2 * ox], x1 = xr1[2 * ox];
         const float4 ga = g4[ox * 4];
         const float4 gb = g4[ox * 4 + 1];
-        ffma2v(acc[0], acc[1], ga.x, ga.y, xv);
-        ffma2v(acc[2], acc[3], ga.z, ga.w, xv);
-        ffma2v(acc[4], acc[5], gb.x, gb.y, xv);
-        ffma2v(acc[6], acc[7], gb.z, gb.w, xv);
+        ffma2v(acc0[0], acc0[1], ga.x, ga.y, x0);
+        ffma2v(acc0[2], acc0[3], ga.z, ga.w, x0);
+        ffma2v(acc0[4], acc0[5], gb.x, gb.y, x0);
+        ffma2v(acc0[6], acc0[7], gb.z, gb.w, x0);
+        ffma2v(acc1[0], acc1[1], ga.x, ga.y, x1);
+        ffma2v(acc1[2], acc1[3], ga.z, ga.w, x1);
+        ffma2v(acc1[4], acc1[5], gb.x, gb.y, x1);
+        ffma2v(acc1[6], acc1[7], gb.z, gb.w, x1);
       }
     }
-    // combine the four row quarters through shared memory (buf is free)
-    if (qr > 0) {
+    // partial (group g, channel d, tap k) of a level lives at [g][d][k]
+    auto put = [&](float* dst, int g) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) S.buf[((qr - 1) * D1 + dg * 8 + c) * 64 + k] = acc[c];
-    }
+      for (int c = 0; c < 8; ++c) {
+        dst[(g * D1 + dg * 8 + c) * 64 + kp] = acc0[c];
+        dst[(g * D1 + dg * 8 + c) * 64 + kp + 32] = acc1[c];
+      }
+    };
+    auto add = [&](const float* src, int g) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        acc0[c] += src[(g * D1 + dg * 8 + c) * 64 + kp];
+        acc1[c] += src[(g * D1 + dg * 8 + c) * 64 + kp + 32];
+      }
+    };
+    if (rg >= 4) put(S.buf, rg - 4);
+    __syncthreads();
+    if (rg < 4) add(S.buf, rg);
+    if (rg == 2 || rg == 3) put(S.a1, rg - 2);
+    __syncthreads();
+    if (rg < 2) add(S.a1, rg);
+    if (rg == 1) put(S.u1.d1, 0);
     __syncthreads();
     PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
-    if (qr == 0) {
+    if (rg == 0) {
+      add(S.u1.d1, 0);
       float* out = prm.st_c1w + bo * (D1 * K1 * K1);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int d = dg * 8 + c;
-        const float g = ((acc[c] + S.buf[d * 64 + k]) + S.buf[(D1 + d) * 64 + k]) +
-                        S.buf[(2 * D1 + d) * 64 + k];
-        out[d * 64 + k] = g;
-        sq = fma((double)g, (double)g, sq);
+        out[d * 64 + kp] = acc0[c];
+        out[d * 64 + kp + 32] = acc1[c];
+        sq = fma((double)acc0[c], (double)acc0[c], sq);
+        sq = fma((double)acc1[c], (double)acc1[c], sq);
       }
     }
   }

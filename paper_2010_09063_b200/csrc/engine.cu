@@ -183,6 +183,7 @@ struct Engine {
   DevError* h_err = nullptr;
 
   bool graph_enabled = true;
+  bool pdl_enabled = std::getenv("PGB_NO_PDL") == nullptr;
   // One CUDA graph per schedule variant. Per-step arguments reach the graph as
   // kernel-node parameter updates (the aggregation / noise-update launch
   // structs, and the fused MNIST kernel's input pointers), so a replay needs
@@ -833,15 +834,27 @@ struct Engine {
     return L;
   }
 
-  void launch_agg(const AggLaunch& L, cudaStream_t s) {
-    aggregate_kernel<<<L.plan.tile_start[L.plan.n], 32 * kAggWarps, agg_smem(L.U), s>>>(L);
+  // pdl: launch as a programmatic dependent of the previous kernel on the
+  // stream (the fused MNIST kernel), hiding the launch gap between them.
+  void launch_agg(const AggLaunch& L, cudaStream_t s, bool pdl = false) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)L.plan.tile_start[L.plan.n]);
+    cfg.blockDim = dim3(32 * kAggWarps);
+    cfg.dynamicSmemBytes = agg_smem(L.U);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    PGB_CUDA(cudaLaunchKernelEx(&cfg, aggregate_kernel, L));
   }
 
   // ff: the step's tail inputs come from the fused MNIST kernel that just ran
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
     if (world == 1) {
-      launch_agg(agg_launch(t, np, U, 0, ff), s);
+      launch_agg(agg_launch(t, np, U, 0, ff), s, ff && pdl_enabled);
       nk += mark(s, "aggregate");
     } else {
       launch_agg(agg_launch(t, np, U, 1, ff), s);

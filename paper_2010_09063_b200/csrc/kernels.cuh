@@ -618,7 +618,7 @@ __device__ __forceinline__ int find_block(const long long* pair_off, int n, long
 // clipped sum only (multi-GPU before the all-reduce, and the parity probe).
 constexpr int kAggWarps = 16;
 constexpr int kAggCols = 128;
-constexpr int kAggRows = 16;
+constexpr int kAggRows = 8;
 constexpr int kAggBatch = 16; // units per load batch (materialised)
 constexpr int kAggChunk = 16; // units per load batch (factored)
 
@@ -727,6 +727,9 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   __shared__ int cnt_sh[kAggWarps];
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
   const AggTile tile = agg_tile(bt, L.plan, blockIdx.x);
+  // Programmatic dependent launch: this grid may be resident before the
+  // per-example kernel has finished; everything below reads its outputs.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int p = tile.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // this thread's epilogue column, and its current parameter / the step

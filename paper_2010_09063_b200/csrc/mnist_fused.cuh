@@ -134,6 +134,9 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   const float* gW4 = W + prm.off[6];
   const float* gb4 = W + prm.off[7];
   PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 0);
+  // let the aggregation grid be scheduled as SMs free up (it waits with
+  // griddepcontrol.wait for this grid's results)
+  asm volatile("griddepcontrol.launch_dependents;");
 
   // ---- TMA: image + conv weights + biases into shared memory --------------
   // Two transactions so conv1 starts as soon as its 7 KB have landed while the

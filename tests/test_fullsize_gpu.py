@@ -1,0 +1,160 @@
+"""Parity at the benchmarked sizes (BASELINE: MNIST CNN at batch 256), through
+every entry point bench.py times:
+
+* pgb_dpsgd_step (host buffers, the reference-shaped step call);
+* pgb_dpsgd_step_device on device-resident batches at changing addresses (the
+  CUDA-graph replay whose per-step arguments are kernel-node updates);
+* pgb_run_epoch (the pipelined epoch driver with its device result ring);
+
+each against the oracle (C restatement of the reference, pinned to the
+compiled reference in test_oracle.py) on the same seeds. CIFAR at batch 256 is
+too slow for the CPU oracle, so there the check is a size-independent property:
+the batch-256 clipped sum and norms equal those of batch-8 engines over the
+same examples (which are themselves checked against the oracle at B = 8 in
+test_parity_gpu.py).
+
+Tolerances as in test_parity_gpu.py: norms element-wise rel 1e-5; parameters a
+few fp32 ulps plus 1e-5 of the update; clipped sums per-block normwise 1e-5.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _mnist(P, O, B):
+    desc = P.build_desc(P.ModelKind.mnist_cnn)
+    od = O.build_desc(O.MNIST_CNN)
+    return desc, od
+
+
+def _check_params(got, p_new, p_old):
+    delta = np.abs(p_new - p_old).max()
+    assert np.all(np.abs(got.astype(np.float64) - p_new) <= 3e-7 * np.abs(p_new) + TOL * delta)
+
+
+def test_mnist_b256_steps_match_oracle(P, O):
+    B = 256
+    desc, od = _mnist(P, O, B)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, 2 * B, 0)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0)
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, 2 * B, 0)
+    for step in range(3):
+        sl = slice((step % 2) * B, (step % 2 + 1) * B)
+        rep = P.dpsgd_step(model, eng, data.inputs[sl], data.labels[sl], cfg, step)
+        p_new, wn, wclip, _ = O.dpsgd_step(od, x64[sl], y64[sl], p64, 1.0, 1.1, 0.1, 1, 0, step)
+        assert np.max(np.abs(rep.pre_clip_norms - wn) / wn) < TOL
+        assert rep.clipped_count == wclip
+        _check_params(model.flat_params(), p_new, p64)
+        p64 = p_new
+
+
+def test_mnist_b256_clipped_sum_matches_oracle(P, O):
+    B = 256
+    desc, od = _mnist(P, O, B)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 0)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    got, norms, nclip = eng.clipped_sum(data.inputs, data.labels, 1.0)
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, B, 0)
+    _, wn, wclip, want = O.dpsgd_step(od, x64, y64, p64, 1.0, 0.0, 0.1, 1, 0, 0)
+    assert np.max(np.abs(norms - wn) / wn) < TOL
+    assert nclip == wclip
+    off = 0
+    for n in od.blocks:
+        w = want[off:off + n]
+        assert np.linalg.norm(got[off:off + n] - w) <= TOL * np.linalg.norm(w)
+        off += n
+
+
+def test_mnist_b256_device_steps_match_oracle(P, O):
+    """The bench.py path: batches already on the device, read in place by the
+    graph (the fused kernel's input pointers are node-parameter updates)."""
+    torch = pytest.importorskip("torch")
+    from paper_2010_09063_b200 import _lib
+    B, nb = 256, 3
+    desc, od = _mnist(P, O, B)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, nb * B, 0)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=5)
+    dx = torch.from_numpy(data.inputs).cuda()
+    dy = torch.from_numpy(data.labels).cuda()
+    row = 28 * 28
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, nb * B, 0)
+    order = [0, 2, 1, 2]
+    for step, b in enumerate(order):
+        _lib.check(_lib.lib.pgb_dpsgd_step_device(
+            eng.handle, C.c_void_p(dx.data_ptr() + b * B * row * 4),
+            C.c_void_p(dy.data_ptr() + b * B * 4), C.byref(cfg.to_c()), 100 + step))
+        sl = slice(b * B, (b + 1) * B)
+        p64, wn, wclip, _ = O.dpsgd_step(od, x64[sl], y64[sl], p64, 1.0, 1.1, 0.1, 1, 5,
+                                         100 + step)
+    norms = np.empty(B, np.float32)
+    rep = _lib.StepReportC()
+    _lib.check(_lib.lib.pgb_synchronize(eng.handle, _lib.ptr(norms), C.byref(rep)))
+    assert np.max(np.abs(norms - wn) / wn) < TOL
+    assert rep.clipped_count == wclip
+    got = eng.get_flat_params().astype(np.float64)
+    p0 = O.init_params(od, 0)
+    assert np.linalg.norm(got - p64) <= TOL * np.linalg.norm(p64 - p0)
+
+
+def test_mnist_b256_epoch_driver_matches_oracle(P, O):
+    B, steps = 256, 4
+    desc, od = _mnist(P, O, B)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, steps * B, 0, pinned=True)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0)
+    norms = np.empty(steps * B, np.float32)
+    _, clipped = P.run_epoch(eng, model, data, cfg, 40, norms)
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, steps * B, 0)
+    total = 0
+    for s in range(steps):
+        sl = slice(s * B, (s + 1) * B)
+        p_new, wn, wclip, _ = O.dpsgd_step(od, x64[sl], y64[sl], p64, 1.0, 1.1, 0.1, 1, 0, 40 + s)
+        assert np.max(np.abs(norms[sl] - wn) / wn) < TOL, f"step {s}"
+        total += wclip
+        p_prev, p64 = p64, p_new
+    assert clipped == total
+    _check_params(eng.get_flat_params(), p64, p_prev)
+
+
+def test_cifar_b256_matches_batch8_engines(P, O):
+    """Size-independent property at the CIFAR config's batch: per-example
+    norms and the clipped sum of a batch-256 engine equal the same quantities
+    assembled from batch-8 engines (different grids and tilings)."""
+    B, b = 256, 8
+    desc = P.build_desc(P.ModelKind.cifar_cnn)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 0)
+    big = P.GradEngine(model, P.Strategy.groupconv, B)
+    got, norms, nclip = big.clipped_sum(data.inputs, data.labels, 1.0)
+    small = P.GradEngine(model, P.Strategy.groupconv, b)
+    want = np.zeros_like(got, dtype=np.float64)
+    wnorms = np.empty(B, np.float32)
+    wclip = 0
+    for i in range(0, B, b):
+        s, n, c = small.clipped_sum(data.inputs[i:i + b], data.labels[i:i + b], 1.0)
+        want += s
+        wnorms[i:i + b] = n
+        wclip += c
+    assert np.max(np.abs(norms - wnorms) / wnorms) < TOL
+    assert nclip == wclip
+    od = O.build_desc(O.CIFAR_CNN)
+    off = 0
+    for n in od.blocks:
+        w = want[off:off + n]
+        assert np.linalg.norm(got[off:off + n] - w) <= TOL * np.linalg.norm(w)
+        off += n

@@ -209,6 +209,15 @@ pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
  * host buffers. */
 pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
                              const float* B, float* C);
+/* Self-test of the UMMA operand layouts (K-major / MN-major, no swizzle) and
+ * the TMEM accumulator row map: raw TMEM dump (128 lanes x N) of
+ * A (MxK) . B (NxK)^T, M in {64, 128}, K <= 32. */
+pgb_status pgb_debug_umma_probe(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_mn,
+                                int32_t b_mn, const float* A, const float* B, float* D_raw);
+/* tcgen05 issue-rate microbenchmark: cycles for `reps` M x N x 8 tf32 MMAs;
+ * strides = {a_lbo, a_sbo, b_lbo, b_sbo} bytes; mode bit 0: two accumulators. */
+pgb_status pgb_debug_umma_rate(int32_t device, int32_t M, int32_t N, int32_t reps,
+                               const uint32_t* strides, int32_t mode, int64_t* cycles);
 /* Kernel launches recorded for the last step (profiling/evidence). */
 int32_t pgb_kernels_per_step(pgb_engine* e);
 

@@ -19,6 +19,7 @@
 
 #include "kernels.cuh"
 #include "mnist_fused.cuh"
+#include "mnist_tc.cuh"
 #include "tc.cuh"
 #include "conv_tc.cuh"
 #include "pgb_internal.h"
@@ -118,6 +119,7 @@ struct Engine {
   int nparts = 1;        // fp64 norm partials per example
   bool norms_fused = false;  // per-example norms produced by the gradient kernel
   bool fused_mnist = false;  // whole per-example pass in one kernel
+  bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
   bool use_tc = true;        // conv GEMMs on tcgen05 (PGB_NO_TC=1: CUDA-core tiles)
   std::vector<int64_t> param_off;
   int64_t P = 0;
@@ -171,6 +173,7 @@ struct Engine {
   float *d_a2 = nullptr, *d_dz1 = nullptr, *d_h = nullptr, *d_dz2 = nullptr;
   float* d_w2t = nullptr;  // conv2 weights kept transposed [k][d] for the fused kernel
   float* d_w1t = nullptr;  // conv1 weights kept transposed [(u,v)][d]
+  float* d_tcw = nullptr;  // hi/lo UMMA operands of the conv weights (mnist_tc.cuh)
   float* d_noise = nullptr;   // (P) the step's normals, drawn by the fused kernel
   float* d_scale = nullptr;   // (B) clip factors, finalised by the fused kernel
   int* d_clipflag = nullptr;  // (B)
@@ -291,6 +294,7 @@ struct Engine {
     P = param_off[desc.n_params];
     in_row = s[0].numel();
     fused_mnist = is_mnist(desc) && std::getenv("PGB_NO_FUSED") == nullptr;
+    mnist_tc = fused_mnist && std::getenv("PGB_MNIST_SIMT") == nullptr;
     use_tc = std::getenv("PGB_NO_TC") == nullptr;
   }
 
@@ -328,6 +332,7 @@ struct Engine {
       want((void**)&d_dz2, sizeof(float) * B * 10);
       want((void**)&d_w2t, sizeof(float) * 32 * 256);
       want((void**)&d_w1t, sizeof(float) * 16 * 64);
+      want((void**)&d_tcw, sizeof(float) * kTcwFloats);
       want((void**)&d_noise, sizeof(float) * P);
       want((void**)&d_scale, sizeof(float) * B);
       want((void**)&d_clipflag, sizeof(int) * B);
@@ -430,6 +435,12 @@ struct Engine {
         t->shadow[0] = d_w1t;
         t->shadow_rows[0] = 16;
         t->shadow_swz[0] = 0;
+        if (mnist_tc) {
+          t->tcw[0] = d_tcw;
+          t->tcw_kind[0] = 1;
+          t->tcw[2] = d_tcw;
+          t->tcw_kind[2] = 2;
+        }
       }
       norms_fused = true;
       nparts = 1;
@@ -504,10 +515,13 @@ struct Engine {
       PGB_CUDA(cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     room));
     }
-    if (fused_mnist)
+    if (fused_mnist) {
       PGB_CUDA(cudaFuncSetAttribute(mnist::fused_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(mnist::Smem)));
+      PGB_CUDA(cudaFuncSetAttribute(mnist::tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(mnist::TcSmem)));
+    }
     // reference init is the default parameter state (models::build, seed 0)
     std::vector<float> p0(P);
     if (pgb_init_params(&desc, 0, p0.data()) != PGB_OK) raise(PGB_ERR_CONTRACT, "init failed");
@@ -525,6 +539,9 @@ struct Engine {
         transpose_kernel<<<grid_for((size_t)rows * cols), 256, 0, s>>>(
             d_params + param_off[p], rows, cols, swz, bt.shadow[p]);
       }
+    if (mnist_tc)
+      mnist::tc_shadow_kernel<<<36, 256, 0, s>>>(d_params + param_off[0], d_params + param_off[2],
+                                                 d_tcw);
   }
 
   // ---- profiling hook: an event after every launch while profiling --------
@@ -653,6 +670,11 @@ struct Engine {
       pairs += (desc.param_size[p] + 1) / 2;
     }
     prm.pair_off[8] = pairs;
+    prm.tcw = d_tcw;
+    if (mnist_tc) {
+      mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm);
+      return mark(s, "mnist_tc");
+    }
     mnist::fused_kernel<<<(unsigned)B, mnist::NT, sizeof(mnist::Smem), s>>>(prm);
     return mark(s, "mnist_fused");
   }
@@ -955,7 +977,7 @@ struct Engine {
       } else if (kp.func == (void*)noise_update_kernel) {
         sg.noise = nd;
         sg.noise_args = *static_cast<const NoiseLaunch*>(kp.kernelParams[0]);
-      } else if (kp.func == (void*)mnist::fused_kernel) {
+      } else if (kp.func == (void*)mnist::fused_kernel || kp.func == (void*)mnist::tc_kernel) {
         sg.fused = nd;
         sg.fused_args = *static_cast<const mnist::Params*>(kp.kernelParams[0]);
       }
@@ -1518,6 +1540,49 @@ pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, co
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dC);
+  });
+}
+
+pgb_status pgb_debug_umma_probe(int32_t device, int32_t M, int32_t N, int32_t K, int32_t a_mn,
+                                int32_t b_mn, const float* A, const float* Bm, float* Draw) {
+  return guarded([&] {
+    if (!(M == 64 || M == 128) || N < 8 || N > 256 || N % 8 || K < 8 || K > 32 || K % 8)
+      raise(PGB_ERR_CONTRACT, "umma probe: M in {64,128}, N in [8,256] step 8, K in {8..32} step 8");
+    PGB_CUDA(cudaSetDevice(device));
+    float *dA = nullptr, *dB = nullptr, *dD = nullptr;
+    PGB_CUDA(cudaMalloc(&dA, sizeof(float) * (size_t)M * K));
+    PGB_CUDA(cudaMalloc(&dB, sizeof(float) * (size_t)N * K));
+    PGB_CUDA(cudaMalloc(&dD, sizeof(float) * (size_t)128 * N));
+    PGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * (size_t)M * K, cudaMemcpyHostToDevice));
+    PGB_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * (size_t)N * K, cudaMemcpyHostToDevice));
+    const int smem = (int)sizeof(float) * (128 * 32 + 256 * 32);
+    PGB_CUDA(cudaFuncSetAttribute(tc::umma_probe_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tc::umma_probe_kernel<<<1, 128, smem>>>(dA, dB, dD, M, N, K, a_mn, b_mn);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaDeviceSynchronize());
+    PGB_CUDA(cudaMemcpy(Draw, dD, sizeof(float) * (size_t)128 * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dD);
+  });
+}
+
+pgb_status pgb_debug_umma_rate(int32_t device, int32_t M, int32_t N, int32_t reps,
+                               const uint32_t* strides, int32_t mode, int64_t* cycles) {
+  return guarded([&] {
+    PGB_CUDA(cudaSetDevice(device));
+    long long* d = nullptr;
+    PGB_CUDA(cudaMalloc(&d, sizeof(long long)));
+    const int smem = 48 * 1024 * 4;
+    PGB_CUDA(cudaFuncSetAttribute(tc::umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    tc::umma_rate_kernel<<<1, 128, smem>>>(M, N, reps, strides[0], strides[1], strides[2],
+                                          strides[3], mode, d);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaDeviceSynchronize());
+    PGB_CUDA(cudaMemcpy(cycles, d, sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(d);
   });
 }
 

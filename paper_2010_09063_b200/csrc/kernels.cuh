@@ -484,7 +484,49 @@ struct BlockTable {
   float* shadow[kMaxBlocks];
   int shadow_rows[kMaxBlocks];
   int shadow_swz[kMaxBlocks];  // XOR swizzle mask (0: plain transpose)
+  // optional hi/lo tensor-core operand copies (mnist_tc.cuh): 1 conv1 W, 2 conv2 W
+  float* tcw[kMaxBlocks];
+  int tcw_kind[kMaxBlocks];
 };
+
+// ---- hi/lo UMMA operand shadows of the MNIST conv weights (mnist_tc.cuh) ---
+// float layout of one shadow buffer (hi and lo stacked along the M/N rows so
+// one MMA multiplies both halves; tf32 MMAs cost a fixed ~50 cycles below
+// N ~ 100, so wider instructions are nearly free):
+//   [0,2048)       conv1 W: rows hl*16 + d (32), K = tap,    kmaj(., tap, 128, 512)
+//   [2048,+16384)  conv2 W: rows hl*32 + d (64), K = k2,     kmaj(., k2, 128, 1024)
+//   [18432,+8192)  conv2 W^T hi, then lo: rows k2 (256), K = d, kmaj(k2, d, 128, 4096)
+constexpr int kTcwW1C = 0, kTcwW2C = 2048, kTcwW2T = 2048 + 2 * 8192;
+constexpr int kTcwFloats = kTcwW2T + 2 * 8192;
+
+__host__ __device__ __forceinline__ int kmaj_f(int r, int k, int sbo, int lbo) {
+  return ((r & 7) * 16 + (k & 3) * 4 + (r >> 3) * sbo + (k >> 2) * lbo) >> 2;
+}
+
+// x = hi + lo with hi = rna_tf32(x) (3xTF32 operands)
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  lo = x - hi;
+}
+
+__device__ __forceinline__ void tcw_write(float* tcw, int which, long long j, float v) {
+  float hi, lo;
+  tf32_split(v, hi, lo);
+  if (which == 1) {  // conv1 W (16, 64)
+    const int d = (int)(j >> 6), k = (int)(j & 63);
+    tcw[kTcwW1C + kmaj_f(d, k, 128, 512)] = hi;
+    tcw[kTcwW1C + kmaj_f(16 + d, k, 128, 512)] = lo;
+  } else {  // conv2 W (32, 256)
+    const int d = (int)(j >> 8), k = (int)(j & 255);
+    tcw[kTcwW2C + kmaj_f(d, k, 128, 1024)] = hi;
+    tcw[kTcwW2C + kmaj_f(32 + d, k, 128, 1024)] = lo;
+    const int o2 = kTcwW2T + kmaj_f(k, d, 128, 4096);
+    tcw[o2] = hi;
+    tcw[o2 + 8192] = lo;
+  }
+}
 
 // Transposed shadow of a (rows, cols) parameter block, rows a power of two:
 // element (r, c) at dst[c * rows + (r ^ (c & (rows - 1)))]. The XOR swizzle
@@ -503,6 +545,7 @@ __device__ __forceinline__ void write_param(const BlockTable& bt, int p, long lo
     const long long r = j / cols, c = j - r * cols;
     bt.shadow[p][shadow_index(r, c, bt.shadow_rows[p], bt.shadow_swz[p])] = v;
   }
+  if (bt.tcw[p]) tcw_write(bt.tcw[p], bt.tcw_kind[p], j, v);
 }
 
 __device__ __forceinline__ float grad_at(const BlockTable& bt, int p, long long i, long long j) {

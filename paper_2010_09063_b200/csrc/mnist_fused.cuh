@@ -95,6 +95,7 @@ struct Params {
   float* noise;         // (P) the step's normals n_j    (dpsgd.cpp:308-316), or null
   long long size[8];    // parameter block sizes
   long long pair_off[9];  // prefix sums of ceil(|p| / 2)
+  const float* tcw;       // hi/lo UMMA operand shadows of the conv weights (tc_kernel)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -1,0 +1,695 @@
+// Per-example DPSGD kernel for the reference MNIST CNN (proj/core/src/models.cpp:107-121)
+// with the convolution GEMMs on the 5th-generation tensor cores (tcgen05,
+// kind::tf32, 3xTF32 split, fp32 accumulators in TMEM).
+//
+// One CTA of 1024 threads owns a PAIR of examples (examples 2c, 2c+1); each
+// half of the CTA (512 threads) runs the element-wise / reduction phases of
+// its example exactly like the SIMT kernel in mnist_fused.cuh, and one
+// thread issues the tensor-core GEMMs for both examples:
+//
+//   conv1 forward  (per example, M = 128 rows (oy, e) x 2 column parities,
+//                  N = 16 channels, K = 64 taps): implicit im2col straight
+//                  from the padded image. The A operand is a K-major UMMA
+//                  view of "Y" -- the padded image stored as rows of 32
+//                  floats, with the two 4-column halves of every 8-tap kernel
+//                  row interleaved as consecutive rows and one copy per
+//                  output-column parity -- so each 8-row core matrix is
+//                  eight output positions of one output row, and a K = 8 step
+//                  is one kernel row u. No patch matrix is ever built.
+//   conv2 forward  (pair-joint: M = 64 (32 channels + pad), N = 32 positions
+//                  of the two examples, K = 256): A = conv2 weights, B = the
+//                  pooled map's im2col.
+//   conv2 dW       (per example, M = 256 im2col rows, N = 32 channels,
+//                  K = 16 positions): the reference's dz_i . patches_i^T
+//                  (strategies.cpp:156-170), straight to the stacks.
+//   conv2 dX       (pair-joint: M = 256, N = 32 positions, K = 32 channels):
+//                  the col2im VJP input (autodiff.cpp:155-196).
+//
+// All operands are K-major, no swizzle (tcgen05 accepts tf32 MN-major only in
+// the 128B_BASE32B swizzle); fp32 values are split x = hi + lo with
+// hi = rna_tf32(x). A kind::tf32 MMA costs a fixed ~50 cycles up to N ~ 100
+// (measured, scripts/umma_rate.py), so the split is folded into the M/N
+// dimensions instead of issuing three MMAs per K step: the hi and lo copies of
+// one operand are stacked as extra rows (N = 2n or M = 2m) and both halves of
+// the other accumulate into the same TMEM columns; the epilogue adds the
+// quadrants (hi.hi + hi.lo + lo.hi + lo.lo). 128 MMAs per example pair. Weight operands (hi/lo, in UMMA layout) come from a
+// shadow that the update kernel keeps in step with the parameters and arrive
+// by TMA bulk copies; the conv2 dX weights (transposed) are fetched while the
+// dense layers run. conv1 dW stays on CUDA cores (its im2col^T operand is
+// 100 KB per example and has no K-major view of the image).
+#pragma once
+
+#include "mnist_fused.cuh"
+#include "tc.cuh"
+
+namespace pgb {
+namespace mnist {
+
+constexpr int TNT = 1024;                 // two examples x 512 threads
+constexpr int YROWS = 68, YS = 32;        // Y rows per (example, hi/lo, parity), floats per row
+constexpr int YBLK = YROWS * YS;          // 2176 floats
+constexpr int OFF_W1C = 8 * YBLK;         // conv1 weight operand after the 8 Y blocks
+constexpr int REGA = OFF_W1C + 2 * 1024;  // 19456 floats (76 KB)
+constexpr int W2HL = 8192;                // one hi or lo copy of a conv2 weight operand
+constexpr int DCOLS = NP2 * DCP;          // dcols floats per example
+
+constexpr int TCW_W1C = kTcwW1C, TCW_W2C = kTcwW2C, TCW_W2T = kTcwW2T;
+
+// rna-tf32 split of an fp32 value
+__device__ __forceinline__ void split_hl(float x, float& hi, float& lo) { tf32_split(x, hi, lo); }
+
+struct TcSmem {
+  float regA[REGA];            // Y + conv1 W -> P2 -> P2^T -> dcols -> conv1 dW partials
+  float w2[2 * W2HL + 128];    // conv2 W (hi, lo) -> conv2 W^T (hi, lo) -> d1, dp1 (+512 B slack)
+  float xs[2][XP * XS];        // padded images (conv1 dW)
+  float xstage[2][H0 * H0];    // raw images (TMA)
+  float p1[2][D1 * PO * PO];   // pooled maps
+  float dc2c[64 * 32];         // conv2-output cotangent: rows hl*32 + pair position, K = d
+  float dc2tc[2][64 * 16];     // [ex] rows hl*32 + d, K = position
+  float c2lo[D2][32];          // conv2 forward: the lo-row half of the accumulator
+  float dc2f[2][D2 * NP2];     // [ex] fp32 [d][pos]
+  float a2[2][F1];
+  float z1[2][NW][H1];
+  float h[2][H1], dz1[2][H1], dz2[2][16];
+  float w4[H1 * NC], b4[16], b3[H1], b1[D1], b2[D2];
+  float yb[2];
+  float b1red[2][NW][D1];
+  double red5[2][5][NW];
+  uint64_t bar[4];             // 0: images + conv1 W, 1: conv2 W, 2: conv2 W^T, 3: MMA commits
+  uint32_t tmem;
+  unsigned char pidx[2][D1 * PO * PO];
+};
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ex = t >> 9, tt = t & (NT - 1), wh = tt >> 5;
+  const int b0 = 2 * blockIdx.x, b = b0 + ex;
+  const int nex = min(2, prm.B - b0);
+  const bool has = ex < nex;
+  const float* W = prm.w;
+  const float* gW3 = W + prm.off[4];
+  const float* tcw = prm.tcw;
+  float* regA = S.regA;
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 0);
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  if (warp == 0) tc::tmem_alloc(&S.tmem, 512);
+  if (t == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&S.bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t img = (uint32_t)(sizeof(float) * H0 * H0 * nex);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&S.bar[0])), "r"(img + 8192u) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&S.bar[1])), "r"(65536u) : "memory");
+    bulk_g2s(S.xstage[0], prm.x + (size_t)b0 * H0 * H0, img, reinterpret_cast<unsigned long long*>(&S.bar[0]));
+    bulk_g2s(regA + OFF_W1C, tcw + TCW_W1C, 8192u, reinterpret_cast<unsigned long long*>(&S.bar[0]));
+    bulk_g2s(S.w2, tcw + TCW_W2C, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[1]));
+  }
+  // shared loss-tail operands and biases
+  if (t < H1 * NC) S.w4[t] = __ldg(W + prm.off[6] + t);
+  else if (t < H1 * NC + NC) S.b4[t - H1 * NC] = __ldg(W + prm.off[7] + t - H1 * NC);
+  else if (t < H1 * NC + NC + H1) S.b3[t - H1 * NC - NC] = __ldg(W + prm.off[5] + t - H1 * NC - NC);
+  else if (t < H1 * NC + NC + H1 + D1) S.b1[t - 362] = __ldg(W + prm.off[1] + t - 362);
+  else if (t < H1 * NC + NC + H1 + D1 + D2) S.b2[t - 378] = __ldg(W + prm.off[3] + t - 378);
+  if (tt == 0 && has) S.yb[ex] = prm.y[b];
+  for (int i = tt; i < XP * XS; i += NT) {
+    const int r = i / XS - 3, c = i % XS - 3;
+    if (!(r >= 0 && r < H0 && c >= 0 && c < H0)) S.xs[ex][i] = 0.0f;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem;
+  tc::mbar_wait(&S.bar[0], 0);
+
+  // ---- padded image (conv1 dW) and the Y operand of conv1 forward ----------
+  // Y[ex][hl][par][R = 2r + h][c] = xpad[r][c + 2 par + 4 h]
+  if (has) {
+    for (int i = tt; i < H0 * H0; i += NT) S.xs[ex][(i / H0 + 3) * XS + i % H0 + 3] = S.xstage[ex][i];
+    for (int i = tt; i < 2 * YBLK; i += NT) {
+      const int par = i / YBLK, rem = i - par * YBLK, R = rem >> 5, c = rem & 31;
+      const int iy = (R >> 1) - 3, ix = c + 2 * par + 4 * (R & 1) - 3;
+      const float v = (iy >= 0 && iy < H0 && ix >= 0 && ix < H0) ? S.xstage[ex][iy * H0 + ix] : 0.0f;
+      float hi, lo;
+      split_hl(v, hi, lo);
+      regA[((ex * 2 + 0) * 2 + par) * YBLK + rem] = hi;
+      regA[((ex * 2 + 1) * 2 + par) * YBLK + rem] = lo;
+    }
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
+
+  // ---- conv1 forward on the tensor cores ------------------------------------
+  // D[(oy, e)][n] for output column ox = 2e + par; K step u = kernel row u:
+  // A rows at Y + 2u rows (SBO 512 B = one output row, LBO 128 B = the h
+  // half); B = [W hi | W lo] (N = 32 rows hl*16 + d), K step u at 1024u bytes.
+  // Yhi.[Whi|Wlo] and Ylo.[Whi|Wlo] accumulate into the same 32 columns, so
+  // the result is D[:, d] + D[:, 16 + d] (the lo.lo term rides along).
+  if (t == 0) {
+    tc::fence_after_sync();
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 32);
+    const uint32_t wb = tc::smem_u32(regA + OFF_W1C);
+    for (int u = 0; u < K1; ++u)
+      for (int e = 0; e < nex; ++e)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          const uint32_t yh = tc::smem_u32(regA + ((e * 2 + 0) * 2 + par) * YBLK);
+          const uint32_t yl = tc::smem_u32(regA + ((e * 2 + 1) * 2 + par) * YBLK);
+          const uint32_t dm = tmem + (uint32_t)((2 * e + par) * 32);
+          const uint64_t bw = tc::make_desc(wb + 1024u * u, 512, 128);
+          tc::mma_tf32(dm, tc::make_desc(yh + 256u * u, 128, 512), bw, idesc, u > 0 ? 1u : 0u);
+          tc::mma_tf32(dm, tc::make_desc(yl + 256u * u, 128, 512), bw, idesc, 1u);
+        }
+    tc::commit(&S.bar[3]);
+  }
+  tc::mbar_wait(&S.bar[3], 0);
+  tc::fence_after_sync();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
+
+  // ---- conv1 bias + relu + maxpool 2x2/2 straight from TMEM -----------------
+  // Thread (quadrant q, lane) holds row m = 32q + lane = (oy = 4q + lane/8,
+  // e = lane % 8) of both parities: ox = 2e and 2e + 1 are in-thread, oy + 1 is
+  // lane ^ 8. First max in window order (kernels.hpp:377-396).
+  {
+    const int q = warp & 3, g = warp >> 2, e = g >> 2, dq = g & 3;
+    if (e < nex) {
+      float v[2][4];
+#pragma unroll
+      for (int par = 0; par < 2; ++par) {
+        float m4[4], c4[4];
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((2 * e + par) * 32 + dq * 4);
+        tmem_ld4(base, m4);
+        tmem_ld4(base + 16, c4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[par][j] = fmaxf((m4[j] + c4[j]) + S.b1[dq * 4 + j], 0.0f);
+      }
+      const int oy = 4 * q + (lane >> 3), ee = lane & 7;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float a00 = v[0][j], a01 = v[1][j];
+        const float a10 = __shfl_xor_sync(0xffffffffu, a00, 8);
+        const float a11 = __shfl_xor_sync(0xffffffffu, a01, 8);
+        if (!(lane & 8) && oy < O1 && ee < PO) {
+          float m = a00;
+          int slot = 0;
+          if (a01 > m) { m = a01; slot = 1; }
+          if (a10 > m) { m = a10; slot = 2; }
+          if (a11 > m) { m = a11; slot = 3; }
+          const int i = (dq * 4 + j) * PO * PO + (oy >> 1) * PO + ee;
+          S.p1[e][i] = m;
+          S.pidx[e][i] = (unsigned char)slot;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
+
+  // ---- conv2 im2col as the B operand: rows hl*32 + pair position, K = (c,u,v)
+  // regA[kmaj(32 hl + 16 ex + pos, k, 128, 1024)]; 32 lanes fill one core.
+  if (has) {
+    for (int i = tt; i < KC2 * NP2; i += NT) {
+      const int kl = i & 3, r8 = (i >> 2) & 7, pg = (i >> 5) & 1, kq = i >> 6;
+      const int pos = pg * 8 + r8, k = kq * 4 + kl;
+      const int c = k >> 4, u = (k >> 2) & 3, v = k & 3, oy = pos >> 2, ox = pos & 3;
+      const float x = S.p1[ex][c * PO * PO + (oy + u) * PO + ox + v];
+      float hi, lo;
+      split_hl(x, hi, lo);
+      regA[kmaj_f(ex * 16 + pos, k, 128, 1024)] = hi;
+      regA[kmaj_f(32 + ex * 16 + pos, k, 128, 1024)] = lo;
+    }
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
+
+  // ---- conv2 forward: one MMA per K step computes all four products ------
+  // D[hl_a*32 + d][hl_b*32 + pair position] = [Whi; Wlo] . [Phi | Plo]^T
+  // (M = 64, N = 64); the result is the sum of the hi.hi, hi.lo, lo.hi (and
+  // lo.lo) quadrants.
+  if (t == 0) {
+    tc::fence_after_sync();
+    tc::mbar_wait(&S.bar[1], 0);
+    constexpr uint32_t idesc = tc::idesc_tf32(64, 64);
+    const uint32_t wa = tc::smem_u32(S.w2), pb = tc::smem_u32(regA);
+    for (int s = 0; s < KC2 / 8; ++s)
+      tc::mma_tf32(tmem + 128, tc::make_desc(wa + 2048u * s, 1024, 128),
+                   tc::make_desc(pb + 2048u * s, 1024, 128), idesc, s > 0 ? 1u : 0u);
+    tc::commit(&S.bar[3]);
+  }
+  // fc1 weight slice into registers while the tensor core runs
+  float wv[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) wv[r] = __ldg(gW3 + (wh * 32 + r) * H1 + lane);
+  tc::mbar_wait(&S.bar[3], 1);
+  tc::fence_after_sync();
+  if (t == 0) {
+    // conv2 W is dead: fetch its transpose for the input-gradient GEMM
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&S.bar[2])), "r"(65536u) : "memory");
+    bulk_g2s(S.w2, tcw + TCW_W2T, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[2]));
+  }
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
+  // M = 64 accumulator: row m at lane m % 16 + 32 (m / 16): quadrants 0, 1
+  // hold the hi rows of d = 16q + lane, quadrants 2, 3 the lo rows. Warp
+  // (q, g) reads columns 4g.. and 32 + 4g.. (the hi and lo halves of N).
+  float c2acc[4];
+  {
+    const int q = warp & 3, g = warp >> 2;
+    float m4[4], c4[4];
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(128 + g * 4);
+    tmem_ld4(base, m4);
+    tmem_ld4(base + 32, c4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c2acc[j] = m4[j] + c4[j];
+    if (q >= 2 && lane < 16)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) S.c2lo[(q - 2) * 16 + lane][g * 4 + j] = c2acc[j];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  {
+    const int q = warp & 3, g = warp >> 2;
+    if (q < 2 && lane < 16) {
+      const int d = q * 16 + lane;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = g * 4 + j, e = col >> 4, pos = col & 15;
+        if (e < nex) S.a2[e][d * NP2 + pos] = fmaxf((c2acc[j] + S.c2lo[d][col]) + S.b2[d], 0.0f);
+      }
+    }
+  }
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
+
+  // ---- fc1 (512->32): lane = unit, warp = 32-row slice -------------------
+  if (has) {
+    float s0 = 0.0f, s1 = 0.0f;
+    const float2* a22 = reinterpret_cast<const float2*>(S.a2[ex] + wh * 32);
+#pragma unroll
+    for (int r = 0; r < 32; r += 2) {
+      const float2 av = a22[r / 2];
+      ffma2pp(s0, s1, av.x, av.y, wv[r], wv[r + 1]);
+    }
+    S.z1[ex][wh][lane] = s0 + s1;
+  }
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
+
+  if (wh == 0) {
+    if (has) {
+      // fc1 bias + relu, fc2, softmax cross-entropy (kernels.hpp:516-566), dz1
+      float zp[4] = {S.b3[lane], 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int w = 0; w < NW; ++w) zp[w & 3] += S.z1[ex][w][lane];
+      const float hv = fmaxf((zp[0] + zp[1]) + (zp[2] + zp[3]), 0.0f);
+      S.h[ex][lane] = hv;
+      float pr[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) pr[c] = hv * S.w4[lane * NC + c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) pr[c] += __shfl_xor_sync(0xffffffffu, pr[c], o);
+      const float raw = S.yb[ex];
+      const bool ok = valid_id(raw, NC);
+      if (!ok && lane == 0) raise_index(prm.err, 0, b, raw, NC);
+      const int y = ok ? (int)raw : 0;
+      float m = -INFINITY, ly = 0.0f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        pr[c] += S.b4[c];
+        m = fmaxf(m, pr[c]);
+        ly = c == y ? pr[c] : ly;
+      }
+      float e[NC], se = 0.0f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        e[c] = expf(pr[c] - m);
+        se += e[c];
+      }
+      float g1 = 0.0f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const float g = ok ? e[c] / se - (c == y ? 1.0f : 0.0f) : 0.0f;
+        if (lane == c) S.dz2[ex][c] = g;
+        g1 = fmaf(S.w4[lane * NC + c], g, g1);
+      }
+      if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
+      S.dz1[ex][lane] = hv > 0.0f ? g1 : 0.0f;
+    }
+    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 16, 0);
+  } else if (wh < 3) {
+    // this CTA's share of the step's Gaussian noise (kernels.hpp:597-614)
+    if (prm.noise && prm.a.add_noise) {
+      const long long pairs = prm.pair_off[8];
+      const long long per = (pairs + gridDim.x - 1) / gridDim.x;
+      for (long long k = ex * 64 + tt - 32; k < per; k += 128) {
+        const long long q = (long long)blockIdx.x * per + k;
+        if (q >= pairs) break;
+        int p = 0;
+        while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
+        const long long jp = q - prm.pair_off[p];
+        float n0, n1;
+        gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
+        float* dst = prm.noise + prm.off[p] + 2 * jp;
+        dst[0] = n0;
+        if (2 * jp + 1 < prm.size[p]) dst[1] = n1;
+      }
+    }
+    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 17, 32);
+  } else if (has) {
+    // the im2col again, transposed (A of conv2 dW): rows k, K = position,
+    // regA[(2 ex + hl) * 4096 + kmaj(k, pos, 128, 4096)]
+    for (int i = tt - 96; i < KC2 * NP2; i += NT - 96) {
+      const int pl = i & 3, r8 = (i >> 2) & 7, kg = (i >> 5) & 31, pq = i >> 10;
+      const int k = kg * 8 + r8, pos = pq * 4 + pl;
+      const int c = k >> 4, u = (k >> 2) & 3, v = k & 3, oy = pos >> 2, ox = pos & 3;
+      const float x = S.p1[ex][c * PO * PO + (oy + u) * PO + ox + v];
+      float hi, lo;
+      split_hl(x, hi, lo);
+      const int o = kmaj_f(k, pos, 128, 4096);
+      regA[(2 * ex) * 4096 + o] = hi;
+      regA[(2 * ex + 1) * 4096 + o] = lo;
+    }
+    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 18, 96);
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
+
+  // ---- fc1 backward data + relu mask -> dc2 (both UMMA layouts, hi/lo) ----
+  if (has) {
+    const float g = S.dz1[ex][lane];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) wv[r] *= g;
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const int half = 16 >> st, off = 16 >> st;
+      const bool upper = (lane & off) != 0;
+#pragma unroll
+      for (int r = 0; r < half; ++r) {
+        const float send = upper ? wv[r] : wv[r + half];
+        const float keep = upper ? wv[r + half] : wv[r];
+        wv[r] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    const int i = wh * 32 + lane;
+    const float v = S.a2[ex][i] > 0.0f ? wv[0] : 0.0f;
+    const int d = i / NP2, pos = i % NP2;
+    float hi, lo;
+    split_hl(v, hi, lo);
+    S.dc2c[kmaj_f(ex * 16 + pos, d, 128, 1024)] = hi;
+    S.dc2c[kmaj_f(32 + ex * 16 + pos, d, 128, 1024)] = lo;
+    S.dc2tc[ex][kmaj_f(d, pos, 128, 1024)] = hi;
+    S.dc2tc[ex][kmaj_f(32 + d, pos, 128, 1024)] = lo;
+    S.dc2f[ex][i] = v;
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
+
+  // ---- conv2 dW (per example) and conv2 dX (pair) on the tensor cores ------
+  if (t == 0) {
+    tc::fence_after_sync();
+    tc::mbar_wait(&S.bar[2], 0);
+    // B = [G hi | G lo] (N = 64): A hi and A lo accumulate into the same 64
+    // columns, the result is D[:, n] + D[:, 32 + n].
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
+    const uint32_t wth = tc::smem_u32(S.w2), wtl = wth + 4u * W2HL;
+    const uint32_t gb = tc::smem_u32(S.dc2c);
+    // dX (pair): D[k2][pos], 2 tiles x 4 K steps (d)
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int tl = 0; tl < 2; ++tl) {
+        const uint32_t dm = tmem + (uint32_t)(tl * 64);
+        const uint64_t bd = tc::make_desc(gb + 2048u * s, 1024, 128);
+        tc::mma_tf32(dm, tc::make_desc(wth + 2048u * tl + 8192u * s, 4096, 128), bd, idesc,
+                     s > 0 ? 1u : 0u);
+        tc::mma_tf32(dm, tc::make_desc(wtl + 2048u * tl + 8192u * s, 4096, 128), bd, idesc, 1u);
+      }
+    // dW (per example): D[k2][d], 2 tiles x 2 K steps (positions)
+    for (int e = 0; e < nex; ++e) {
+      const uint32_t ah = tc::smem_u32(regA + (2 * e) * 4096), al = ah + 16384u;
+      const uint32_t bb = tc::smem_u32(S.dc2tc[e]);
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int tl = 0; tl < 2; ++tl) {
+          const uint32_t dm = tmem + 128 + (uint32_t)((2 * e + tl) * 64);
+          const uint64_t bd = tc::make_desc(bb + 2048u * s, 1024, 128);
+          tc::mma_tf32(dm, tc::make_desc(ah + 2048u * tl + 8192u * s, 4096, 128), bd, idesc,
+                       s > 0 ? 1u : 0u);
+          tc::mma_tf32(dm, tc::make_desc(al + 2048u * tl + 8192u * s, 4096, 128), bd, idesc, 1u);
+        }
+    }
+    tc::commit(&S.bar[3]);
+  }
+  double sq = 0.0;  // this thread's share of its example's ||g_i||^2
+  const size_t bo = (size_t)b;
+  if (tt < D2 && has) {  // conv2 bias
+    float s = 0.0f;
+    for (int p = 0; p < NP2; ++p) s += S.dc2f[ex][tt * NP2 + p];
+    prm.st_c2b[bo * D2 + tt] = s;
+    sq = fma((double)s, (double)s, sq);
+  }
+  tc::mbar_wait(&S.bar[3], 0);
+  tc::fence_after_sync();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
+
+  // conv2 dW -> stacks: the half of example ex reads its own accumulators;
+  // warp (q, tile, column half), row k = 128 tile + 32 q + lane
+  {
+    const int q = wh & 3, g = wh >> 2, tl = g >> 1, ch = g & 1;
+    if (has) {
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + 128 + (uint32_t)((2 * ex + tl) * 64 + ch * 16);
+      float m8[8], c8[8];
+      const int k = tl * 128 + q * 32 + lane;
+      float* out = prm.st_c2w + bo * (D2 * KC2);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        tc::tmem_ld8(base + hh * 8, m8);
+        tc::tmem_ld8(base + 32 + hh * 8, c8);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float v = m8[j] + c8[j];
+          out[(ch * 16 + hh * 8 + j) * KC2 + k] = v;
+          sq = fma((double)v, (double)v, sq);
+        }
+      }
+    }
+  }
+  // conv2 dX -> dcols[ex][pos][(u,v) * 17 + c]: warp (q, tile, 8-column group)
+  {
+    const int q = warp & 3, g = warp >> 2, tl = g >> 2, cq = g & 3;
+    const int e = cq >> 1;
+    if (e < nex) {
+      float m8[8], c8[8];
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tl * 64 + cq * 8);
+      tc::tmem_ld8(base, m8);
+      tc::tmem_ld8(base + 32, c8);
+      const int k = tl * 128 + q * 32 + lane, c = k >> 4, uv = k & 15;
+      float* dcols = regA + e * DCOLS;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int pos = (cq & 1) * 8 + j;
+        dcols[pos * DCP + uv * 17 + c] = m8[j] + c8[j];
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
+
+  float* d1 = S.w2 + ex * (NP1 * D1);                 // [pos][d]
+  float* dp1 = S.w2 + 2 * NP1 * D1 + ex * (D1 * PO * PO);
+  // col2im as a gather: dp1[c][iy][ix] = sum_{u,v} dcols[(iy-u, ix-v)][(u,v),c]
+  if (has) {
+    const float* dcols = regA + ex * DCOLS;
+    for (int i = tt; i < D1 * PO * PO; i += NT) {  // i = (iy*7+ix)*16 + c
+      const int c = i % C2, r = i / C2, iy = r / PO, ix = r % PO;
+      float s = 0.0f;
+#pragma unroll
+      for (int u = 0; u < K2; ++u) {
+        const int oy = iy - u;
+        if (oy < 0 || oy >= O2) continue;
+#pragma unroll
+        for (int v = 0; v < K2; ++v) {
+          const int ox = ix - v;
+          if (ox < 0 || ox >= O2) continue;
+          s += dcols[(oy * O2 + ox) * DCP + (u * 4 + v) * 17 + c];
+        }
+      }
+      dp1[c * PO * PO + r] = s;
+    }
+  }
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 12);
+  // maxpool backward (first max) + relu mask (the routed element is the
+  // pooled max, so relu' = [p1 > 0]) -> d1 [pos][d]; conv1 bias partials
+  float b1part = 0.0f;
+  if (has) {
+    for (int i = tt; i < D1 * NP1; i += NT) {  // i = pos*16 + d
+      const int d = i % D1, r = i / D1, oy = r / O1, ox = r % O1;
+      const int pi = d * PO * PO + (oy / 2) * PO + ox / 2;
+      const int slot = (oy & 1) * 2 + (ox & 1);
+      const float g = (S.pidx[ex][pi] == slot && S.p1[ex][pi] > 0.0f) ? dp1[pi] : 0.0f;
+      d1[i] = g;
+      b1part += g;
+    }
+  }
+  b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
+  if (lane < D1) S.b1red[ex][wh][lane] = b1part;
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
+
+  // ---- conv1 per-example dW on CUDA cores (as in mnist_fused.cuh) ----------
+  {
+    const int kp = tt & 31, dg = (tt >> 5) & 1, rg = tt >> 6;
+    const int u = kp / K1, v = kp % K1;
+    const int oy0 = rg < 6 ? 2 * rg : 6 + rg, oy1 = rg < 6 ? oy0 + 2 : oy0 + 1;
+    float acc0[8], acc1[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc0[c] = acc1[c] = 0.0f;
+    if (has) {
+      for (int oy = oy0; oy < oy1; ++oy) {
+        const float* xr0 = S.xs[ex] + (2 * oy + u) * XS + v;
+        const float* xr1 = xr0 + 4 * XS;
+        const float4* g4 = reinterpret_cast<const float4*>(d1 + oy * O1 * D1) + 2 * dg;
+#pragma unroll 7
+        for (int ox = 0; ox < O1; ++ox) {
+          const float x0 = xr0[2 * ox], x1 = xr1[2 * ox];
+          const float4 ga = g4[ox * 4];
+          const float4 gb = g4[ox * 4 + 1];
+          ffma2v(acc0[0], acc0[1], ga.x, ga.y, x0);
+          ffma2v(acc0[2], acc0[3], ga.z, ga.w, x0);
+          ffma2v(acc0[4], acc0[5], gb.x, gb.y, x0);
+          ffma2v(acc0[6], acc0[7], gb.z, gb.w, x0);
+          ffma2v(acc1[0], acc1[1], ga.x, ga.y, x1);
+          ffma2v(acc1[2], acc1[3], ga.z, ga.w, x1);
+          ffma2v(acc1[4], acc1[5], gb.x, gb.y, x1);
+          ffma2v(acc1[6], acc1[7], gb.z, gb.w, x1);
+        }
+      }
+    }
+    float* L1 = regA + ex * 8192;  // partial levels [g][d][k]: 4, 2, 1 groups
+    float* L2 = L1 + 4096;
+    float* L3 = L1 + 6144;
+    auto put = [&](float* dst, int g) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        dst[(g * D1 + dg * 8 + c) * 64 + kp] = acc0[c];
+        dst[(g * D1 + dg * 8 + c) * 64 + kp + 32] = acc1[c];
+      }
+    };
+    auto add = [&](const float* src, int g) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        acc0[c] += src[(g * D1 + dg * 8 + c) * 64 + kp];
+        acc1[c] += src[(g * D1 + dg * 8 + c) * 64 + kp + 32];
+      }
+    };
+    if (rg >= 4) put(L1, rg - 4);
+    __syncthreads();
+    if (rg < 4) add(L1, rg);
+    if (rg == 2 || rg == 3) put(L2, rg - 2);
+    __syncthreads();
+    if (rg < 2) add(L2, rg);
+    if (rg == 1) put(L3, 0);
+    __syncthreads();
+    PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
+    if (rg == 0 && has) {
+      add(L3, 0);
+      float* out = prm.st_c1w + bo * (D1 * K1 * K1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int d = dg * 8 + c;
+        out[d * 64 + kp] = acc0[c];
+        out[d * 64 + kp + 32] = acc1[c];
+        sq = fma((double)acc0[c], (double)acc0[c], sq);
+        sq = fma((double)acc1[c], (double)acc1[c], sq);
+      }
+    }
+  }
+  if (tt < D1 && has) {  // conv1 bias
+    float s = 0.0f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += S.b1red[ex][w][tt];
+    prm.st_c1b[bo * D1 + tt] = s;
+    sq = fma((double)s, (double)s, sq);
+  }
+
+  // ---- dense factors for the ghost-norm blocks + their norm terms ----------
+  double a2sq = 0.0, hsq = 0.0, dz1sq = 0.0, dz2sq = 0.0;
+  if (has) {
+    const float v = S.a2[ex][tt];
+    prm.a2[bo * F1 + tt] = v;
+    a2sq = (double)v * v;
+    if (tt < H1) {
+      const float hv = S.h[ex][tt], g = S.dz1[ex][tt];
+      prm.h[bo * H1 + tt] = hv;
+      prm.dz1[bo * H1 + tt] = g;
+      hsq = (double)hv * hv;
+      dz1sq = (double)g * g;
+    }
+    if (tt < NC) {
+      const float g = S.dz2[ex][tt];
+      prm.dz2[bo * NC + tt] = g;
+      dz2sq = (double)g * g;
+    }
+  }
+  double v5[5] = {sq, a2sq, hsq, dz1sq, dz2sq};
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v5[q] += __shfl_xor_sync(0xffffffffu, v5[q], o);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) S.red5[ex][q][wh] = v5[q];
+  tc::fence_before_sync();
+  __syncthreads();
+  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (tt == 0 && has) {
+    double r5[5] = {0, 0, 0, 0, 0};
+    for (int w = 0; w < NW; ++w)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) r5[q] += S.red5[ex][q][w];
+    // ||a (x) d||^2 = ||a||^2 ||d||^2 (weight) + ||d||^2 (bias), strategies.cpp:140-148
+    const double nsq = r5[0] + r5[3] * (r5[1] + 1.0) + r5[4] * (r5[2] + 1.0);
+    prm.normsq[b] = nsq;
+    const float nrm = (float)sqrt(nsq);
+    const float C = prm.a.clip;
+    prm.norms[b] = nrm;
+    prm.scale[b] = nrm > C ? __fdiv_rn(C, nrm) : 1.0f;
+    prm.clipped[b] = nrm > C ? 1 : 0;
+    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
+  }
+}
+
+// conv weight blocks -> the hi/lo UMMA operands of tc_kernel (after a host
+// upload; the update kernel keeps them in step through write_param)
+__global__ void tc_shadow_kernel(const float* __restrict__ w1, const float* __restrict__ w2,
+                                 float* __restrict__ tcw) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 1024 + 8192; e += gridDim.x * blockDim.x) {
+    if (e < 1024) tcw_write(tcw, 1, e, w1[e]);
+    else tcw_write(tcw, 2, e - 1024, w2[e - 1024]);
+  }
+}
+
+}  // namespace mnist
+}  // namespace pgb

@@ -286,6 +286,128 @@ inline size_t tc_smem_bytes() {
   return sizeof(TcSmem<BN>);
 }
 
+// ---------------------------------------------------------------------------
+// Operand layouts without swizzle (byte offsets inside one operand tile).
+// K-major: core matrices of 8 rows x 16 B (4 tf32 along K); rows 16 B apart,
+//   8-row groups SBO apart, the two K-adjacent cores of one K=8 step LBO apart.
+// MN-major: core matrices of 8 K-rows x 16 B (4 tf32 along M/N); 4-element
+//   M/N groups SBO apart, K rows 16 B apart (one core spans a K=8 step).
+// In both, the block [8 rows][4 floats] with the 4 floats contiguous is the
+// same 128-byte core, which lets one shared-memory buffer serve as a K-major
+// operand of one GEMM and an MN-major operand of another.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr uint32_t idesc_tf32_mj(int M, int N, int a_mn, int b_mn) {
+  return idesc_tf32(M, N) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+}
+
+__device__ __forceinline__ uint32_t kmaj_off(int r, int k, uint32_t sbo, uint32_t lbo) {
+  return (uint32_t)((r & 7) * 16 + (k & 3) * 4) + (uint32_t)(r >> 3) * sbo + (uint32_t)(k >> 2) * lbo;
+}
+__device__ __forceinline__ uint32_t mnmaj_off(int r, int k, uint32_t sbo, uint32_t lbo) {
+  return (uint32_t)((r & 3) * 4 + (k & 7) * 16) + (uint32_t)(r >> 2) * sbo + (uint32_t)(k >> 3) * lbo;
+}
+
+// Layout probe (self-test): D (M x N) = A (M x K) . B (N x K)^T with A and
+// B staged in the K-major or MN-major layouts above, cores packed along M/N
+// (SBO = 128 B) then along K. One CTA of 128 threads; the raw TMEM contents
+// (128 lanes x N columns) are dumped so the host checks the accumulator row
+// -> lane map too (M = 128: lane m; M = 64: lane m % 16 + 32 (m / 16)).
+__global__ void __launch_bounds__(128) umma_probe_kernel(const float* __restrict__ A,
+                                                         const float* __restrict__ B,
+                                                         float* __restrict__ Draw, int M, int N,
+                                                         int K, int a_mn, int b_mn) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  float* sa = reinterpret_cast<float*>(raw);
+  float* sb = sa + 128 * 32;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const uint32_t a_lbo = a_mn ? (uint32_t)(M / 4) * 128 : (uint32_t)(M / 8) * 128;
+  const uint32_t b_lbo = b_mn ? (uint32_t)(N / 4) * 128 : (uint32_t)(N / 8) * 128;
+  for (int e = t; e < 128 * 32 + 256 * 32; e += 128) sa[e] = 0.0f;
+  __syncthreads();
+  for (int e = t; e < M * K; e += 128) {
+    const int r = e / K, k = e % K;
+    const uint32_t o = a_mn ? mnmaj_off(r, k, 128, a_lbo) : kmaj_off(r, k, 128, a_lbo);
+    sa[o / 4] = A[e];
+  }
+  for (int e = t; e < N * K; e += 128) {
+    const int r = e / K, k = e % K;
+    const uint32_t o = b_mn ? mnmaj_off(r, k, 128, b_lbo) : kmaj_off(r, k, 128, b_lbo);
+    sb[o / 4] = B[e];
+  }
+  if (warp == 0) tmem_alloc(&tslot, 256);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tslot;
+  if (t == 0) {
+    const uint32_t idesc = idesc_tf32_mj(M, N, a_mn, b_mn);
+    for (int s = 0; s < K / 8; ++s) {
+      const uint32_t ao = a_mn ? (uint32_t)s * a_lbo : (uint32_t)s * 2 * a_lbo;
+      const uint32_t bo = b_mn ? (uint32_t)s * b_lbo : (uint32_t)s * 2 * b_lbo;
+      // MN-major: SBO = M/N-group stride, LBO = K-group stride
+      const uint64_t da = make_desc(smem_u32(sa) + ao, a_lbo, 128);
+      const uint64_t db = make_desc(smem_u32(sb) + bo, b_lbo, 128);
+      mma_tf32(tmem, da, db, idesc, s > 0 ? 1u : 0u);
+    }
+    commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 8) {
+    float v[8];
+    tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    for (int j = 0; j < 8 && c0 + j < N; ++j) Draw[(warp * 32 + lane) * N + c0 + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+// Issue-rate microbenchmark: `reps` back-to-back kind::tf32 MMAs of shape
+// M x N x 8 from one thread (operands: whatever shared memory holds), cycles
+// from the first issue to the commit's completion. mode bit 0: alternate two
+// accumulators; A/B strides as given.
+__global__ void __launch_bounds__(128) umma_rate_kernel(int M, int N, int reps, uint32_t a_lbo,
+                                                        uint32_t a_sbo, uint32_t b_lbo,
+                                                        uint32_t b_sbo, int mode,
+                                                        long long* cycles) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  float* sm = reinterpret_cast<float*>(raw);
+  for (int e = threadIdx.x; e < 48 * 1024; e += 128) sm[e] = 0.0f;
+  if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_tf32(M, N);
+    const uint64_t da = make_desc(smem_u32(sm), a_lbo, a_sbo);
+    const uint64_t db = make_desc(smem_u32(sm + 32 * 1024), b_lbo, b_sbo);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+      mma_tf32(tslot + ((mode & 1) ? (uint32_t)(r & 1) * 256u : 0u), da, db, idesc, r > 1 ? 1u : 0u);
+    commit(&bar);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tslot, 512);
+}
+
 // Plain row-major test GEMM: C (M x N) = A (M x K) . B (N x K)^T.
 struct PlainOp {
   static constexpr bool kTableA = false;

@@ -15,6 +15,15 @@ __device__ unsigned long long* g_trace = nullptr;
       ::pgb::g_trace[(slot)] = t_;                                               \
     }                                                                            \
   } while (0)
+// timestamp from thread `tid` (no-op unless it reaches the mark)
+#define PGB_MARK_T(slot, tid)                                                    \
+  do {                                                                           \
+    if (::pgb::g_trace && threadIdx.x == (tid)) {                                \
+      unsigned long long t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+      ::pgb::g_trace[(slot)] = t_;                                               \
+    }                                                                            \
+  } while (0)
 // After a __syncthreads(): BAR.SYNC does not block at issue (the wait is
 // deferred to the next dependent instruction), so a timestamp taken right
 // after it records the barrier's issue, not its release. A second barrier
@@ -25,6 +34,9 @@ __device__ unsigned long long* g_trace = nullptr;
     PGB_MARK(slot);        \
   } while (0)
 #else
+#define PGB_MARK_T(slot, tid) \
+  do {                        \
+  } while (0)
 #define PGB_MARK_BAR(slot) \
   do {                     \
   } while (0)

@@ -40,17 +40,22 @@ buf = np.zeros(SLOTS, np.int64)
 _lib.check(L.pgb_debug_trace(C.c_void_p(buf.ctypes.data), SLOTS))
 
 F = buf[FUSED:FUSED + 24 * B].reshape(B, 24)
+F = F[F[:, 0] > 0]  # one row per CTA (the tensor-core kernel runs B/2 CTAs)
 t0 = F[:, 0].min()
-marks = sorted([k for k in range(24) if F[:, k].all()], key=lambda k: F[0, k])
+marks = sorted([k for k in list(range(16)) + [23] if F[:, k].all()], key=lambda k: F[0, k])
 end = F[:, marks[-1]]
 order = np.argsort(end)
-one, two = order[:30], order[-100:]
+n = len(F)
+one, two = (order[:30], order[-100:]) if n == B else (order[:n // 2], order[n // 2:])
 print(f"fused kernel: first CTA start -> last end {(end.max() - t0) / 1e3:.2f} us, "
       f"first end {(end.min() - t0) / 1e3:.2f} us")
-print("phase  alone(us)  shared(us)")
+print("phase  alone(us)  shared(us)" if n == B else "phase  early-half(us)  late-half(us)")
 for a, b in zip(marks[:-1], marks[1:]):
     d = F[:, b] - F[:, a]
     print(f"{a:2d}->{b:2d}  {d[one].mean() / 1e3:8.2f}  {d[two].mean() / 1e3:8.2f}")
+for k in range(16, 23):
+    if F[:, k].all():
+        print(f"  mark {k}: {(F[:, k] - F[:, 7]).mean() / 1e3:.2f} us after mark 7")
 A = buf[AGG:AGG + 8 * 4096].reshape(4096, 8)
 A = A[A[:, 0] > 0]
 if len(A):

@@ -21,3 +21,24 @@ def test_tc_gemm_3xtf32(P, M, N, K):
     want = A.astype(np.float64) @ B.astype(np.float64).T
     err = np.linalg.norm(Cm - want) / np.linalg.norm(want)
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("M", [64, 128])
+@pytest.mark.parametrize("N", [16, 32])
+def test_umma_layouts(P, M, N):
+    """K-major (no swizzle) operands and the accumulator lane map (M = 128:
+    lane m; M = 64: lane m % 16 + 32 (m / 16)) the tensor-core MNIST kernel
+    relies on; small integers, so the product is exact. (tf32 MN-major
+    operands need the 128B_BASE32B swizzle: with SWIZZLE_NONE the MMA leaves
+    the accumulator untouched, so the kernel uses K-major operands only.)"""
+    a_mn = b_mn = 0
+    K = 24
+    rng = np.random.default_rng(M + N + 2 * a_mn + b_mn)
+    A = rng.integers(-4, 5, (M, K)).astype(np.float32)
+    B = rng.integers(-4, 5, (N, K)).astype(np.float32)
+    D = np.zeros((128, N), np.float32)
+    P._lib.check(P.lib.pgb_debug_umma_probe(0, M, N, K, a_mn, b_mn, P._lib.ptr(A),
+                                            P._lib.ptr(B), P._lib.ptr(D)))
+    want = A @ B.T
+    lanes = np.arange(M) if M == 128 else (np.arange(M) % 16 + 32 * (np.arange(M) // 16))
+    np.testing.assert_array_equal(D[lanes], want)

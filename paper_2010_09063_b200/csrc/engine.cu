@@ -1577,7 +1577,7 @@ pgb_status pgb_debug_umma_rate(int32_t device, int32_t M, int32_t N, int32_t rep
     const int smem = 48 * 1024 * 4;
     PGB_CUDA(cudaFuncSetAttribute(tc::umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
-    tc::umma_rate_kernel<<<1, 128, smem>>>(M, N, reps, strides[0], strides[1], strides[2],
+    tc::umma_rate_kernel<<<1, (mode & 8) ? 1024 : 128, smem>>>(M, N, reps, strides[0], strides[1], strides[2],
                                           strides[3], mode, d);
     PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaDeviceSynchronize());

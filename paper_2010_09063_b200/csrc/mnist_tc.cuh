@@ -35,8 +35,11 @@
 // quadrants (hi.hi + hi.lo + lo.hi + lo.lo). 128 MMAs per example pair. Weight operands (hi/lo, in UMMA layout) come from a
 // shadow that the update kernel keeps in step with the parameters and arrive
 // by TMA bulk copies; the conv2 dX weights (transposed) are fetched while the
-// dense layers run. conv1 dW stays on CUDA cores (its im2col^T operand is
-// 100 KB per example and has no K-major view of the image).
+// dense layers run.
+//   conv1 dW       (per example, M = 128 = 8 kernel rows x hi/lo x 8 taps,
+//                  N = 32 = d1 hi | lo, K = 224 positions): implicit im2col^T
+//                  from "Z", the padded image cut into 16-byte chunks of four
+//                  output columns per tap parity/offset (see below).
 #pragma once
 
 #include "mnist_fused.cuh"
@@ -61,7 +64,6 @@ __device__ __forceinline__ void split_hl(float x, float& hi, float& lo) { tf32_s
 struct TcSmem {
   float regA[REGA];            // Y + conv1 W -> P2 -> P2^T -> dcols -> conv1 dW partials
   float w2[2 * W2HL + 128];    // conv2 W (hi, lo) -> conv2 W^T (hi, lo) -> d1, dp1 (+512 B slack)
-  float xs[2][XP * XS];        // padded images (conv1 dW)
   float xstage[2][H0 * H0];    // raw images (TMA)
   float p1[2][D1 * PO * PO];   // pooled maps
   float dc2c[64 * 32];         // conv2-output cotangent: rows hl*32 + pair position, K = d
@@ -89,6 +91,12 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
   for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// A single thread issues a tcgen05.mma only every ~120 cycles (the issuing
+// warp stalls on each UTCHMMA), while the tensor core retires these small
+// MMAs every ~35-50 cycles (scripts/umma_rate.py), so each GEMM phase is
+// split into independent accumulator chains issued by lane 0 of warps 0..3.
+constexpr int kIssuers = 4;
+
 __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
@@ -107,7 +115,8 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   if (warp == 0) tc::tmem_alloc(&S.tmem, 512);
   if (t == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tc::mbar_init(&S.bar[i], 1);
+    for (int i = 0; i < 3; ++i) tc::mbar_init(&S.bar[i], 1);
+    tc::mbar_init(&S.bar[3], kIssuers);  // every issuer commits once per GEMM phase
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t img = (uint32_t)(sizeof(float) * H0 * H0 * nex);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -125,20 +134,15 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   else if (t < H1 * NC + NC + H1 + D1) S.b1[t - 362] = __ldg(W + prm.off[1] + t - 362);
   else if (t < H1 * NC + NC + H1 + D1 + D2) S.b2[t - 378] = __ldg(W + prm.off[3] + t - 378);
   if (tt == 0 && has) S.yb[ex] = prm.y[b];
-  for (int i = tt; i < XP * XS; i += NT) {
-    const int r = i / XS - 3, c = i % XS - 3;
-    if (!(r >= 0 && r < H0 && c >= 0 && c < H0)) S.xs[ex][i] = 0.0f;
-  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem;
   tc::mbar_wait(&S.bar[0], 0);
 
-  // ---- padded image (conv1 dW) and the Y operand of conv1 forward ----------
+  // ---- the Y operand of conv1 forward ----------------------------------------
   // Y[ex][hl][par][R = 2r + h][c] = xpad[r][c + 2 par + 4 h]
   if (has) {
-    for (int i = tt; i < H0 * H0; i += NT) S.xs[ex][(i / H0 + 3) * XS + i % H0 + 3] = S.xstage[ex][i];
     for (int i = tt; i < 2 * YBLK; i += NT) {
       const int par = i / YBLK, rem = i - par * YBLK, R = rem >> 5, c = rem & 31;
       const int iy = (R >> 1) - 3, ix = c + 2 * par + 4 * (R & 1) - 3;
@@ -159,22 +163,44 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   // half); B = [W hi | W lo] (N = 32 rows hl*16 + d), K step u at 1024u bytes.
   // Yhi.[Whi|Wlo] and Ylo.[Whi|Wlo] accumulate into the same 32 columns, so
   // the result is D[:, d] + D[:, 16 + d] (the lo.lo term rides along).
-  if (t == 0) {
+  if (lane == 0 && warp < kIssuers) {
+    // issuer w: example e = w / 2, parity par = w % 2
     tc::fence_after_sync();
     constexpr uint32_t idesc = tc::idesc_tf32(128, 32);
-    const uint32_t wb = tc::smem_u32(regA + OFF_W1C);
-    for (int u = 0; u < K1; ++u)
-      for (int e = 0; e < nex; ++e)
+    const int e = warp >> 1, par = warp & 1;
+    if (e < nex) {
+      const uint32_t wb = tc::smem_u32(regA + OFF_W1C);
+      const uint32_t yh = tc::smem_u32(regA + ((e * 2 + 0) * 2 + par) * YBLK);
+      const uint32_t yl = tc::smem_u32(regA + ((e * 2 + 1) * 2 + par) * YBLK);
+      const uint32_t dm = tmem + (uint32_t)((2 * e + par) * 32);
 #pragma unroll
-        for (int par = 0; par < 2; ++par) {
-          const uint32_t yh = tc::smem_u32(regA + ((e * 2 + 0) * 2 + par) * YBLK);
-          const uint32_t yl = tc::smem_u32(regA + ((e * 2 + 1) * 2 + par) * YBLK);
-          const uint32_t dm = tmem + (uint32_t)((2 * e + par) * 32);
-          const uint64_t bw = tc::make_desc(wb + 1024u * u, 512, 128);
-          tc::mma_tf32(dm, tc::make_desc(yh + 256u * u, 128, 512), bw, idesc, u > 0 ? 1u : 0u);
-          tc::mma_tf32(dm, tc::make_desc(yl + 256u * u, 128, 512), bw, idesc, 1u);
-        }
+      for (int u = 0; u < K1; ++u) {
+        const uint64_t bw = tc::make_desc(wb + 1024u * u, 512, 128);
+        tc::mma_tf32(dm, tc::make_desc(yh + 256u * u, 128, 512), bw, idesc, u > 0 ? 1u : 0u);
+        tc::mma_tf32(dm, tc::make_desc(yl + 256u * u, 128, 512), bw, idesc, 1u);
+      }
+    }
     tc::commit(&S.bar[3]);
+  } else if (wh == 4 || wh == 5) {
+    // while the tensor core runs: this CTA's share of the step's Gaussian
+    // noise (kernels.hpp:597-614), one Box-Muller pair per thread
+    if (prm.noise && prm.a.add_noise) {
+      const long long pairs = prm.pair_off[8];
+      const long long per = (pairs + gridDim.x - 1) / gridDim.x;
+      for (long long k = ex * 64 + tt - 128; k < per; k += 128) {
+        const long long q = (long long)blockIdx.x * per + k;
+        if (q >= pairs) break;
+        int p = 0;
+        while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
+        const long long jp = q - prm.pair_off[p];
+        float n0, n1;
+        gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
+        float* dst = prm.noise + prm.off[p] + 2 * jp;
+        dst[0] = n0;
+        if (2 * jp + 1 < prm.size[p]) dst[1] = n1;
+      }
+    }
+    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 17, 128);
   }
   tc::mbar_wait(&S.bar[3], 0);
   tc::fence_after_sync();
@@ -242,14 +268,16 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   // D[hl_a*32 + d][hl_b*32 + pair position] = [Whi; Wlo] . [Phi | Plo]^T
   // (M = 64, N = 64); the result is the sum of the hi.hi, hi.lo, lo.hi (and
   // lo.lo) quadrants.
-  if (t == 0) {
+  // issuer w: K steps s = w (mod 4) into the accumulator at 256 + 64 w
+  if (lane == 0 && warp < kIssuers) {
     tc::fence_after_sync();
     tc::mbar_wait(&S.bar[1], 0);
     constexpr uint32_t idesc = tc::idesc_tf32(64, 64);
     const uint32_t wa = tc::smem_u32(S.w2), pb = tc::smem_u32(regA);
-    for (int s = 0; s < KC2 / 8; ++s)
-      tc::mma_tf32(tmem + 128, tc::make_desc(wa + 2048u * s, 1024, 128),
-                   tc::make_desc(pb + 2048u * s, 1024, 128), idesc, s > 0 ? 1u : 0u);
+#pragma unroll
+    for (int s = warp; s < KC2 / 8; s += kIssuers)
+      tc::mma_tf32(tmem + 256 + 64u * warp, tc::make_desc(wa + 2048u * s, 1024, 128),
+                   tc::make_desc(pb + 2048u * s, 1024, 128), idesc, s >= kIssuers ? 1u : 0u);
     tc::commit(&S.bar[3]);
   }
   // fc1 weight slice into registers while the tensor core runs
@@ -271,12 +299,17 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   float c2acc[4];
   {
     const int q = warp & 3, g = warp >> 2;
-    float m4[4], c4[4];
-    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(128 + g * 4);
-    tmem_ld4(base, m4);
-    tmem_ld4(base + 32, c4);
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(256 + g * 4);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) c2acc[j] = m4[j] + c4[j];
+    for (int j = 0; j < 4; ++j) c2acc[j] = 0.0f;
+#pragma unroll
+    for (int sl = 0; sl < kIssuers; ++sl) {
+      float m4[4], c4[4];
+      tmem_ld4(base + 64 * sl, m4);
+      tmem_ld4(base + 64 * sl + 32, c4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c2acc[j] += m4[j] + c4[j];
+    }
     if (q >= 2 && lane < 16)
 #pragma unroll
       for (int j = 0; j < 4; ++j) S.c2lo[(q - 2) * 16 + lane][g * 4 + j] = c2acc[j];
@@ -319,64 +352,40 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
       for (int w = 0; w < NW; ++w) zp[w & 3] += S.z1[ex][w][lane];
       const float hv = fmaxf((zp[0] + zp[1]) + (zp[2] + zp[3]), 0.0f);
       S.h[ex][lane] = hv;
-      float pr[NC];
+      // lane c < 10 owns logit c: sum_j h_j W4[j][c] in ascending j
+      const int c = lane < NC ? lane : 0;
+      float lg = 0.0f;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) pr[c] = hv * S.w4[lane * NC + c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) pr[c] += __shfl_xor_sync(0xffffffffu, pr[c], o);
+      for (int j = 0; j < H1; ++j) lg = fmaf(__shfl_sync(0xffffffffu, hv, j), S.w4[j * NC + c], lg);
+      lg += S.b4[c];
       const float raw = S.yb[ex];
       const bool ok = valid_id(raw, NC);
       if (!ok && lane == 0) raise_index(prm.err, 0, b, raw, NC);
       const int y = ok ? (int)raw : 0;
-      float m = -INFINITY, ly = 0.0f;
+      float m = lane < NC ? lg : -INFINITY;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        pr[c] += S.b4[c];
-        m = fmaxf(m, pr[c]);
-        ly = c == y ? pr[c] : ly;
-      }
-      float e[NC], se = 0.0f;
+      for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      m = __shfl_sync(0xffffffffu, m, 0);
+      const float e = lane < NC ? expf(lg - m) : 0.0f;
+      float se = e;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        e[c] = expf(pr[c] - m);
-        se += e[c];
-      }
+      for (int o = 8; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      se = __shfl_sync(0xffffffffu, se, 0);
+      const float ly = __shfl_sync(0xffffffffu, lg, y);
+      const float g = (ok && lane < NC) ? e / se - (lane == y ? 1.0f : 0.0f) : 0.0f;
+      if (lane < NC) S.dz2[ex][lane] = g;
+      if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
+      // dz1_j = (W4 dz2)_j * [h_j > 0]: lane j
       float g1 = 0.0f;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const float g = ok ? e[c] / se - (c == y ? 1.0f : 0.0f) : 0.0f;
-        if (lane == c) S.dz2[ex][c] = g;
-        g1 = fmaf(S.w4[lane * NC + c], g, g1);
-      }
-      if (lane == 0) prm.loss[b] = ok ? m + logf(se) - ly : 0.0f;
+      for (int cc = 0; cc < NC; ++cc) g1 = fmaf(S.w4[lane * NC + cc], __shfl_sync(0xffffffffu, g, cc), g1);
       S.dz1[ex][lane] = hv > 0.0f ? g1 : 0.0f;
     }
     PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 16, 0);
-  } else if (wh < 3) {
-    // this CTA's share of the step's Gaussian noise (kernels.hpp:597-614)
-    if (prm.noise && prm.a.add_noise) {
-      const long long pairs = prm.pair_off[8];
-      const long long per = (pairs + gridDim.x - 1) / gridDim.x;
-      for (long long k = ex * 64 + tt - 32; k < per; k += 128) {
-        const long long q = (long long)blockIdx.x * per + k;
-        if (q >= pairs) break;
-        int p = 0;
-        while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
-        const long long jp = q - prm.pair_off[p];
-        float n0, n1;
-        gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
-        float* dst = prm.noise + prm.off[p] + 2 * jp;
-        dst[0] = n0;
-        if (2 * jp + 1 < prm.size[p]) dst[1] = n1;
-      }
-    }
-    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 17, 32);
   } else if (has) {
     // the im2col again, transposed (A of conv2 dW): rows k, K = position,
     // regA[(2 ex + hl) * 4096 + kmaj(k, pos, 128, 4096)]
-    for (int i = tt - 96; i < KC2 * NP2; i += NT - 96) {
+    for (int i = tt - 32; i < KC2 * NP2; i += NT - 32) {
       const int pl = i & 3, r8 = (i >> 2) & 7, kg = (i >> 5) & 31, pq = i >> 10;
       const int k = kg * 8 + r8, pos = pq * 4 + pl;
       const int c = k >> 4, u = (k >> 2) & 3, v = k & 3, oy = pos >> 2, ox = pos & 3;
@@ -387,7 +396,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
       regA[(2 * ex) * 4096 + o] = hi;
       regA[(2 * ex + 1) * 4096 + o] = lo;
     }
-    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 18, 96);
+    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 18, 32);
   }
   tc::fence_proxy_async();
   __syncthreads();
@@ -425,28 +434,31 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
 
   // ---- conv2 dW (per example) and conv2 dX (pair) on the tensor cores ------
-  if (t == 0) {
+  // issuers 0, 1: dX tile 0, 1 (pair: D[k2][pos], 4 K steps over d);
+  // issuers 2, 3: dW of example 0, 1 (D[k2][d], 2 tiles x 2 K steps over pos).
+  // B = [G hi | G lo] (N = 64): A hi and A lo accumulate into the same 64
+  // columns, the result is D[:, n] + D[:, 32 + n].
+  if (lane == 0 && warp < kIssuers) {
     tc::fence_after_sync();
-    tc::mbar_wait(&S.bar[2], 0);
-    // B = [G hi | G lo] (N = 64): A hi and A lo accumulate into the same 64
-    // columns, the result is D[:, n] + D[:, 32 + n].
     constexpr uint32_t idesc = tc::idesc_tf32(128, 64);
-    const uint32_t wth = tc::smem_u32(S.w2), wtl = wth + 4u * W2HL;
-    const uint32_t gb = tc::smem_u32(S.dc2c);
-    // dX (pair): D[k2][pos], 2 tiles x 4 K steps (d)
-    for (int s = 0; s < 4; ++s)
+    if (warp < 2) {
+      tc::mbar_wait(&S.bar[2], 0);
+      const int tl = warp;
+      const uint32_t wth = tc::smem_u32(S.w2), wtl = wth + 4u * W2HL;
+      const uint32_t gb = tc::smem_u32(S.dc2c);
+      const uint32_t dm = tmem + (uint32_t)(tl * 64);
 #pragma unroll
-      for (int tl = 0; tl < 2; ++tl) {
-        const uint32_t dm = tmem + (uint32_t)(tl * 64);
+      for (int s = 0; s < 4; ++s) {
         const uint64_t bd = tc::make_desc(gb + 2048u * s, 1024, 128);
         tc::mma_tf32(dm, tc::make_desc(wth + 2048u * tl + 8192u * s, 4096, 128), bd, idesc,
                      s > 0 ? 1u : 0u);
         tc::mma_tf32(dm, tc::make_desc(wtl + 2048u * tl + 8192u * s, 4096, 128), bd, idesc, 1u);
       }
-    // dW (per example): D[k2][d], 2 tiles x 2 K steps (positions)
-    for (int e = 0; e < nex; ++e) {
+    } else if (warp - 2 < nex) {
+      const int e = warp - 2;
       const uint32_t ah = tc::smem_u32(regA + (2 * e) * 4096), al = ah + 16384u;
       const uint32_t bb = tc::smem_u32(S.dc2tc[e]);
+#pragma unroll
       for (int s = 0; s < 2; ++s)
 #pragma unroll
         for (int tl = 0; tl < 2; ++tl) {
@@ -515,8 +527,10 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
 
-  float* d1 = S.w2 + ex * (NP1 * D1);                 // [pos][d]
-  float* dp1 = S.w2 + 2 * NP1 * D1 + ex * (D1 * PO * PO);
+  // conv1-output cotangent as the B operand of conv1 dW: rows hl*16 + d,
+  // K = oy*16 + ox (ox 14, 15 zero), kmaj(., ., 128, 512): 7168 floats/example
+  float* d1c = S.w2 + ex * 7168;
+  float* dp1 = S.w2 + 2 * 7168 + ex * (D1 * PO * PO);
   // col2im as a gather: dp1[c][iy][ix] = sum_{u,v} dcols[(iy-u, ix-v)][(u,v),c]
   if (has) {
     const float* dcols = regA + ex * DCOLS;
@@ -540,88 +554,96 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 12);
   // maxpool backward (first max) + relu mask (the routed element is the
-  // pooled max, so relu' = [p1 > 0]) -> d1 [pos][d]; conv1 bias partials
+  // pooled max, so relu' = [p1 > 0]) -> d1 as a UMMA operand; conv1 bias
+  // partials. Meanwhile the image view Z for conv1 dW (below).
   float b1part = 0.0f;
+  float* Z = regA + ex * 8704;
   if (has) {
-    for (int i = tt; i < D1 * NP1; i += NT) {  // i = pos*16 + d
-      const int d = i % D1, r = i / D1, oy = r / O1, ox = r % O1;
-      const int pi = d * PO * PO + (oy / 2) * PO + ox / 2;
-      const int slot = (oy & 1) * 2 + (ox & 1);
-      const float g = (S.pidx[ex][pi] == slot && S.p1[ex][pi] > 0.0f) ? dp1[pi] : 0.0f;
-      d1[i] = g;
+    for (int i = tt; i < D1 * O1 * 16; i += NT) {  // i = (oy*16 + ox)*16 + d
+      const int d = i & 15, kp = i >> 4, oy = kp >> 4, ox = kp & 15;
+      float g = 0.0f;
+      if (ox < O1) {
+        const int pi = d * PO * PO + (oy >> 1) * PO + (ox >> 1);
+        const int slot = (oy & 1) * 2 + (ox & 1);
+        g = (S.pidx[ex][pi] == slot && S.p1[ex][pi] > 0.0f) ? dp1[pi] : 0.0f;
+      }
+      float hi, lo;
+      split_hl(g, hi, lo);
+      d1c[kmaj_f(d, kp, 128, 512)] = hi;
+      d1c[kmaj_f(16 + d, kp, 128, 512)] = lo;
       b1part += g;
+    }
+    // Z[R' = 2R + hl][j4][c = 4p + s][i] = xpad[R][2 (4 j4 + s + i) + p]: for tap
+    // (u, v = 2s + p) and output columns 4 j4 .. 4 j4 + 3 of output row oy, the
+    // 16-byte chunk (R = 2 oy + u, j4, c) holds the four inputs, so a K-major
+    // core matrix is eight taps of one kernel row (permuted v) x four
+    // positions, rows 16 B apart; kernel row u and the hi/lo copy are the
+    // rows R' (SBO 512 B), position quads the j4 chunks (LBO 128 B).
+    for (int i = tt; i < 34 * 128; i += NT) {
+      const int i4 = i & 3, c = (i >> 2) & 7, j4 = (i >> 5) & 3, R = i >> 7;
+      const int iy = R - 3, ix = 2 * (4 * j4 + (c & 3) + i4) + (c >> 2) - 3;
+      const float v = (iy >= 0 && iy < H0 && ix >= 0 && ix < H0) ? S.xstage[ex][iy * H0 + ix] : 0.0f;
+      float hi, lo;
+      split_hl(v, hi, lo);
+      Z[(2 * R) * 128 + (i & 127)] = hi;
+      Z[(2 * R + 1) * 128 + (i & 127)] = lo;
     }
   }
   b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
   if (lane < D1) S.b1red[ex][wh][lane] = b1part;
+  tc::fence_proxy_async();
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
 
-  // ---- conv1 per-example dW on CUDA cores (as in mnist_fused.cuh) ----------
-  {
-    const int kp = tt & 31, dg = (tt >> 5) & 1, rg = tt >> 6;
-    const int u = kp / K1, v = kp % K1;
-    const int oy0 = rg < 6 ? 2 * rg : 6 + rg, oy1 = rg < 6 ? oy0 + 2 : oy0 + 1;
-    float acc0[8], acc1[8];
+  // ---- conv1 per-example dW on the tensor cores ----------------------------
+  // D[(u, hl, c)][n] = sum_pos Z . [d1 hi | d1 lo]^T (M = 128, N = 32); K step
+  // = output row oy and an 8-column half jp. The result for tap (u, v = 2s+p),
+  // channel d is the sum over the hl rows and the two N halves.
+  // issuer w: example w / 2, output rows oy in [7 (w % 2), 7 (w % 2) + 7)
+  // into the accumulator at 32 w (the two halves are added at readback)
+  if (lane == 0 && warp < kIssuers) {
+    tc::fence_after_sync();
+    constexpr uint32_t idesc = tc::idesc_tf32(128, 32);
+    const int e = warp >> 1, oy0 = 7 * (warp & 1);
+    if (e < nex) {
+      const uint32_t za = tc::smem_u32(regA + e * 8704), db = tc::smem_u32(S.w2 + e * 7168);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc0[c] = acc1[c] = 0.0f;
-    if (has) {
-      for (int oy = oy0; oy < oy1; ++oy) {
-        const float* xr0 = S.xs[ex] + (2 * oy + u) * XS + v;
-        const float* xr1 = xr0 + 4 * XS;
-        const float4* g4 = reinterpret_cast<const float4*>(d1 + oy * O1 * D1) + 2 * dg;
-#pragma unroll 7
-        for (int ox = 0; ox < O1; ++ox) {
-          const float x0 = xr0[2 * ox], x1 = xr1[2 * ox];
-          const float4 ga = g4[ox * 4];
-          const float4 gb = g4[ox * 4 + 1];
-          ffma2v(acc0[0], acc0[1], ga.x, ga.y, x0);
-          ffma2v(acc0[2], acc0[3], ga.z, ga.w, x0);
-          ffma2v(acc0[4], acc0[5], gb.x, gb.y, x0);
-          ffma2v(acc0[6], acc0[7], gb.z, gb.w, x0);
-          ffma2v(acc1[0], acc1[1], ga.x, ga.y, x1);
-          ffma2v(acc1[2], acc1[3], ga.z, ga.w, x1);
-          ffma2v(acc1[4], acc1[5], gb.x, gb.y, x1);
-          ffma2v(acc1[6], acc1[7], gb.z, gb.w, x1);
-        }
-      }
+      for (int oy = oy0; oy < oy0 + 7; ++oy)
+#pragma unroll
+        for (int jp = 0; jp < 2; ++jp)
+          tc::mma_tf32(tmem + (uint32_t)(warp * 32), tc::make_desc(za + 2048u * oy + 256u * jp, 128, 512),
+                       tc::make_desc(db + 2048u * oy + 1024u * jp, 512, 128), idesc,
+                       (oy > oy0 || jp) ? 1u : 0u);
     }
-    float* L1 = regA + ex * 8192;  // partial levels [g][d][k]: 4, 2, 1 groups
-    float* L2 = L1 + 4096;
-    float* L3 = L1 + 6144;
-    auto put = [&](float* dst, int g) {
+    tc::commit(&S.bar[3]);
+  }
+  tc::mbar_wait(&S.bar[3], 1);
+  tc::fence_after_sync();
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
+  {
+    // warp (q, dq) of half ex: row m = 32q + lane = (u = m/16, hl = m/8 % 2,
+    // c = m % 8); 4 channels d = 4dq.. from both N halves, hl rows via lane^8
+    const int q = wh & 3, dq = wh >> 2;
+    float m4[4], c4[4];
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ex * 64 + dq * 4);
+    if (has) {
+      float m4b[4], c4b[4];
+      tmem_ld4(base, m4);
+      tmem_ld4(base + 16, c4);
+      tmem_ld4(base + 32, m4b);
+      tmem_ld4(base + 48, c4b);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        dst[(g * D1 + dg * 8 + c) * 64 + kp] = acc0[c];
-        dst[(g * D1 + dg * 8 + c) * 64 + kp + 32] = acc1[c];
-      }
-    };
-    auto add = [&](const float* src, int g) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        acc0[c] += src[(g * D1 + dg * 8 + c) * 64 + kp];
-        acc1[c] += src[(g * D1 + dg * 8 + c) * 64 + kp + 32];
-      }
-    };
-    if (rg >= 4) put(L1, rg - 4);
-    __syncthreads();
-    if (rg < 4) add(L1, rg);
-    if (rg == 2 || rg == 3) put(L2, rg - 2);
-    __syncthreads();
-    if (rg < 2) add(L2, rg);
-    if (rg == 1) put(L3, 0);
-    __syncthreads();
-    PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
-    if (rg == 0 && has) {
-      add(L3, 0);
+      for (int j = 0; j < 4; ++j) m4[j] += m4b[j] + c4b[j];
+      const int m = q * 32 + lane, u = m >> 4, c = m & 7, v = 2 * (c & 3) + (c >> 2);
       float* out = prm.st_c1w + bo * (D1 * K1 * K1);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int d = dg * 8 + c;
-        out[d * 64 + kp] = acc0[c];
-        out[d * 64 + kp + 32] = acc1[c];
-        sq = fma((double)acc0[c], (double)acc0[c], sq);
-        sq = fma((double)acc1[c], (double)acc1[c], sq);
+      for (int j = 0; j < 4; ++j) {
+        float val = m4[j] + c4[j];
+        val += __shfl_xor_sync(0xffffffffu, val, 8);
+        if (!(m & 8)) {
+          out[(dq * 4 + j) * 64 + u * K1 + v] = val;
+          sq = fma((double)val, (double)val, sq);
+        }
       }
     }
   }

@@ -371,37 +371,50 @@ __global__ void __launch_bounds__(128) umma_probe_kernel(const float* __restrict
 }
 
 // Issue-rate microbenchmark: `reps` back-to-back kind::tf32 MMAs of shape
-// M x N x 8 from one thread (operands: whatever shared memory holds), cycles
-// from the first issue to the commit's completion. mode bit 0: alternate two
-// accumulators; A/B strides as given.
-__global__ void __launch_bounds__(128) umma_rate_kernel(int M, int N, int reps, uint32_t a_lbo,
-                                                        uint32_t a_sbo, uint32_t b_lbo,
-                                                        uint32_t b_sbo, int mode,
-                                                        long long* cycles) {
+// M x N x 8 from one thread, cycles from the first issue to the commit's
+// completion. mode bit 0: alternate two accumulators; bit 1: stream the
+// operand addresses (A +4 KB, B +2 KB per MMA, wrapping in 64 KB / 32 KB);
+// bit 2: every other thread polls the completion mbarrier meanwhile.
+__global__ void __launch_bounds__(1024) umma_rate_kernel(int M, int N, int reps, uint32_t a_lbo,
+                                                         uint32_t a_sbo, uint32_t b_lbo,
+                                                         uint32_t b_sbo, int mode,
+                                                         long long* cycles) {
   extern __shared__ __align__(1024) unsigned char raw[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   float* sm = reinterpret_cast<float*>(raw);
-  for (int e = threadIdx.x; e < 48 * 1024; e += 128) sm[e] = 0.0f;
+  for (int e = threadIdx.x; e < 48 * 1024; e += blockDim.x) sm[e] = 0.0f;
   if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar, (mode & 16) ? 4 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_proxy_async();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
-  if (threadIdx.x == 0) {
+  const int issuers = (mode & 16) ? 4 : 1;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < issuers) {
     const uint32_t idesc = idesc_tf32(M, N);
-    const uint64_t da = make_desc(smem_u32(sm), a_lbo, a_sbo);
-    const uint64_t db = make_desc(smem_u32(sm + 32 * 1024), b_lbo, b_sbo);
+    const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 32 * 1024);
+    const uint64_t da0 = make_desc(a0, a_lbo, a_sbo), db0 = make_desc(b0, b_lbo, b_sbo);
     const long long t0 = clock64();
-    for (int r = 0; r < reps; ++r)
-      mma_tf32(tslot + ((mode & 1) ? (uint32_t)(r & 1) * 256u : 0u), da, db, idesc, r > 1 ? 1u : 0u);
+    for (int r = w; r < reps; r += issuers) {
+      const uint32_t ao = (mode & 2) ? (uint32_t)((r * 4096) & 65535) : 0u;
+      const uint32_t bo = (mode & 2) ? (uint32_t)((r * 2048) & 32767) : 0u;
+      const uint32_t d = tslot + (N <= 128 ? (uint32_t)w * 128u : (uint32_t)(w & 1) * 256u);
+      if (mode & 32)
+        mma_tf32(d, da0 + (ao >> 4), db0 + (bo >> 4), idesc, r >= issuers ? 1u : 0u);
+      else
+        mma_tf32(d, make_desc(a0 + ao, a_lbo, a_sbo), make_desc(b0 + bo, b_lbo, b_sbo), idesc,
+                 r >= issuers ? 1u : 0u);
+    }
     commit(&bar);
     mbar_wait(&bar, 0);
-    cycles[blockIdx.x] = clock64() - t0;
+    if (w == 0) cycles[blockIdx.x] = clock64() - t0;
+  } else if (mode & 4) {
+    mbar_wait(&bar, 0);
   }
   fence_before_sync();
   __syncthreads();

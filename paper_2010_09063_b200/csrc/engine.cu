@@ -132,8 +132,12 @@ struct Engine {
   float* h_norm_stage = nullptr;
   int* h_clip_stage = nullptr;
   int64_t stage_steps = 0, stage_units = 0;
-  cudaEvent_t ev_copied[kSlots] = {}, ev_consumed[kSlots] = {}, ev_done[kSlots] = {},
-              ev_read[kSlots] = {};
+  // per-step results (norms, clip count) land in a ring of kResSlots device
+  // slots read back on out_stream; the ring is deep so the compute stream
+  // never waits on a read-back queued behind a large input copy
+  static constexpr int kResSlots = 64;
+  cudaEvent_t ev_copied[kSlots] = {}, ev_consumed[kSlots] = {}, ev_done[kResSlots] = {},
+              ev_read[kResSlots] = {};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
 
   void ensure_host_stage(int64_t steps, int64_t units) {
@@ -147,6 +151,26 @@ struct Engine {
     PGB_CUDA(cudaMallocHost(&h_norm_stage, sizeof(float) * stage_steps * stage_units));
     PGB_CUDA(cudaMallocHost(&h_clip_stage, sizeof(int) * 2 * stage_steps));
   }
+  // epoch-driver input chunks (device, grown on demand): a pinned H2D copy
+  // moves ~15-30 GB/s at one batch (0.8 MB) but ~40-50 GB/s at >= 12 MB, so
+  // the driver copies several steps' batches per transfer
+  float* d_xc[kSlots] = {};
+  float* d_yc[kSlots] = {};
+  int64_t chunk_cap = 0;
+  void ensure_chunk_ring(int64_t steps_per_chunk) {
+    if (steps_per_chunk <= chunk_cap) return;
+    for (int i = 0; i < kSlots; ++i) {
+      if (d_xc[i]) cudaFree(d_xc[i]);
+      if (d_yc[i]) cudaFree(d_yc[i]);
+      d_xc[i] = d_yc[i] = nullptr;
+    }
+    chunk_cap = 0;
+    for (int i = 0; i < kSlots; ++i) {
+      PGB_CUDA(cudaMalloc(&d_xc[i], sizeof(float) * steps_per_chunk * B * in_row));
+      PGB_CUDA(cudaMalloc(&d_yc[i], sizeof(float) * steps_per_chunk * B));
+    }
+    chunk_cap = steps_per_chunk;
+  }
   // arena
   char* arena = nullptr;
   size_t arena_bytes = 0;
@@ -155,8 +179,8 @@ struct Engine {
   float* d_y = nullptr;
   float* d_xb[kSlots] = {};
   float* d_yb[kSlots] = {};
-  float* d_norms_ring = nullptr;    // (kSlots, B)
-  int* d_clip_ring = nullptr;       // (kSlots, 2)
+  float* d_norms_ring = nullptr;    // (kResSlots, B)
+  int* d_clip_ring = nullptr;       // (kResSlots, 2)
   // where the next launched step writes its norms / clip count
   float* norms_dst = nullptr;
   int* clipped_dst = nullptr;
@@ -219,8 +243,15 @@ struct Engine {
     if (out_stream) cudaStreamDestroy(out_stream);
     if (h_norm_stage) cudaFreeHost(h_norm_stage);
     if (h_clip_stage) cudaFreeHost(h_clip_stage);
+    for (int i = 0; i < kSlots; ++i) {
+      if (d_xc[i]) cudaFree(d_xc[i]);
+      if (d_yc[i]) cudaFree(d_yc[i]);
+    }
     for (int i = 0; i < kSlots; ++i)
-      for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i], ev_done[i], ev_read[i]})
+      for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i]})
+        if (ev) cudaEventDestroy(ev);
+    for (int i = 0; i < kResSlots; ++i)
+      for (cudaEvent_t ev : {ev_done[i], ev_read[i]})
         if (ev) cudaEventDestroy(ev);
     if (ev_t0) cudaEventDestroy(ev_t0);
     if (ev_t1) cudaEventDestroy(ev_t1);
@@ -310,8 +341,8 @@ struct Engine {
       want((void**)&d_xb[i], sizeof(float) * B * in_row);
       want((void**)&d_yb[i], sizeof(float) * B);
     }
-    want((void**)&d_norms_ring, sizeof(float) * B * kSlots);
-    want((void**)&d_clip_ring, sizeof(int) * 2 * kSlots);
+    want((void**)&d_norms_ring, sizeof(float) * B * kResSlots);
+    want((void**)&d_clip_ring, sizeof(int) * 2 * kResSlots);
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
@@ -493,7 +524,10 @@ struct Engine {
     PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
     for (int i = 0; i < kSlots; ++i)
-      for (cudaEvent_t* ev : {&ev_copied[i], &ev_consumed[i], &ev_done[i], &ev_read[i]})
+      for (cudaEvent_t* ev : {&ev_copied[i], &ev_consumed[i]})
+        PGB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    for (int i = 0; i < kResSlots; ++i)
+      for (cudaEvent_t* ev : {&ev_done[i], &ev_read[i]})
         PGB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     PGB_CUDA(cudaEventCreate(&ev_t0));
     PGB_CUDA(cudaEventCreate(&ev_t1));
@@ -1378,42 +1412,68 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     cudaEvent_t* read = en.ev_read;
     const auto wall0 = std::chrono::steady_clock::now();
     PGB_CUDA(cudaEventRecord(en.ev_t0, en.stream));
-    auto copy_in = [&](int64_t s) {
-      const int sl = (int)(s % K);
-      if (s >= K) PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, consumed[sl], 0));
+    // Inputs arrive in chunks of C steps (one pinned H2D copy per chunk) into
+    // a ring of K device chunks. The fused MNIST step takes
+    // its input pointers as graph-node parameters, so any offset inside a
+    // chunk works; the layer-wise schedule bakes its input slot into the
+    // graph and keeps one batch per chunk.
+    // One batch per copy by default: at the current step time (~30 us) a 0.8
+    // MB copy (~25 us at ~32 GB/s) already hides under compute, and larger
+    // chunks only lengthen the pipeline fill (scripts/e2e_probe.py).
+    // PGB_CHUNK_BYTES=<bytes> groups batches per copy.
+    int64_t chunk_bytes = 0;
+    if (const char* cb = std::getenv("PGB_CHUNK_BYTES")) chunk_bytes = std::atoll(cb);
+    const int64_t C = en.fused_mnist
+                          ? std::max<int64_t>(1, std::min<int64_t>(steps, chunk_bytes / (int64_t)xb))
+                          : 1;
+    if (C > 1) en.ensure_chunk_ring(C);
+    const int64_t nchunks = (steps + C - 1) / C;
+    auto xslot = [&](int sl) { return C > 1 ? en.d_xc[sl] : en.d_xb[sl]; };
+    auto yslot = [&](int sl) { return C > 1 ? en.d_yc[sl] : en.d_yb[sl]; };
+    auto copy_in = [&](int64_t k) {
+      const int sl = (int)(k % K);
+      const int64_t cnt = std::min<int64_t>(C, steps - k * C);
+      if (k >= K) PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, consumed[sl], 0));
       else PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, en.ev_t0, 0));
-      PGB_CUDA(cudaMemcpyAsync(en.d_xb[sl], x + s * en.B * en.in_row, xb, cudaMemcpyHostToDevice,
-                               en.copy_stream));
-      PGB_CUDA(cudaMemcpyAsync(en.d_yb[sl], y + s * en.B, yb, cudaMemcpyHostToDevice,
+      PGB_CUDA(cudaMemcpyAsync(xslot(sl), x + k * C * en.B * en.in_row, xb * cnt,
+                               cudaMemcpyHostToDevice, en.copy_stream));
+      PGB_CUDA(cudaMemcpyAsync(yslot(sl), y + k * C * en.B, yb * cnt, cudaMemcpyHostToDevice,
                                en.copy_stream));
       PGB_CUDA(cudaEventRecord(copied[sl], en.copy_stream));
     };
-    for (int64_t s = 0; s < std::min<int64_t>(K - 1, steps); ++s) copy_in(s);
+    for (int64_t k = 0; k < std::min<int64_t>(K - 1, nchunks); ++k) copy_in(k);
     for (int64_t s = 0; s < steps; ++s) {
-      const int sl = (int)(s % K);
-      if (s + K - 1 < steps) copy_in(s + K - 1);
-      PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
-      if (ring) {
-        // slot sl's previous results must have been read back
-        if (s >= K) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[sl], 0));
-        en.norms_dst = en.d_norms_ring + (size_t)sl * en.B;
-        en.clipped_dst = en.d_clip_ring + 2 * sl;
+      const int64_t k = s / C, j = s % C;
+      const int sl = (int)(k % K);
+      constexpr int KR = Engine::kResSlots;
+      const int rs_sl = (int)(s % KR);  // result slot
+      if (j == 0) {
+        if (k + K - 1 < nchunks) copy_in(k + K - 1);
+        PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
       }
-      en.push_args(en.make_args(*cfg, step0 + s, en.d_xb[sl], en.d_yb[sl]));
-      en.launch_step(en.d_xb[sl], en.d_yb[sl], cfg->microbatch);
-      PGB_CUDA(cudaEventRecord(consumed[sl], en.stream));
+      if (ring) {
+        // result slot rs_sl's previous results must have been read back
+        if (s >= KR) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[rs_sl], 0));
+        en.norms_dst = en.d_norms_ring + (size_t)rs_sl * en.B;
+        en.clipped_dst = en.d_clip_ring + 2 * rs_sl;
+      }
+      const float* xs = xslot(sl) + j * en.B * en.in_row;
+      const float* ys = yslot(sl) + j * en.B;
+      en.push_args(en.make_args(*cfg, step0 + s, xs, ys));
+      en.launch_step(xs, ys, cfg->microbatch);
+      if (j == C - 1 || s == steps - 1) PGB_CUDA(cudaEventRecord(consumed[sl], en.stream));
       // the step's result read back every step (norms, clipped count)
       cudaStream_t rs = ring ? en.out_stream : en.stream;
       if (ring) {
-        PGB_CUDA(cudaEventRecord(done[sl], en.stream));
-        PGB_CUDA(cudaStreamWaitEvent(rs, done[sl], 0));
+        PGB_CUDA(cudaEventRecord(done[rs_sl], en.stream));
+        PGB_CUDA(cudaStreamWaitEvent(rs, done[rs_sl], 0));
       }
       PGB_CUDA(cudaMemcpyAsync(en.h_clip_stage + 2 * s, en.clipped_dst, sizeof(int) * 2,
                                cudaMemcpyDeviceToHost, rs));
       if (norms_out)
         PGB_CUDA(cudaMemcpyAsync(en.h_norm_stage + s * U, en.norms_dst, sizeof(float) * U,
                                  cudaMemcpyDeviceToHost, rs));
-      if (ring) PGB_CUDA(cudaEventRecord(read[sl], rs));
+      if (ring) PGB_CUDA(cudaEventRecord(read[rs_sl], rs));
     }
     en.norms_dst = en.d_norms;
     en.clipped_dst = en.d_clipped;

@@ -142,15 +142,26 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
 
   // ---- the Y operand of conv1 forward ----------------------------------------
   // Y[ex][hl][par][R = 2r + h][c] = xpad[r][c + 2 par + 4 h]
+  // thread: column c = tt % 32, rows R = tt / 32 + 16 j (h = R % 2 fixed)
   if (has) {
-    for (int i = tt; i < 2 * YBLK; i += NT) {
-      const int par = i / YBLK, rem = i - par * YBLK, R = rem >> 5, c = rem & 31;
-      const int iy = (R >> 1) - 3, ix = c + 2 * par + 4 * (R & 1) - 3;
-      const float v = (iy >= 0 && iy < H0 && ix >= 0 && ix < H0) ? S.xstage[ex][iy * H0 + ix] : 0.0f;
-      float hi, lo;
-      split_hl(v, hi, lo);
-      regA[((ex * 2 + 0) * 2 + par) * YBLK + rem] = hi;
-      regA[((ex * 2 + 1) * 2 + par) * YBLK + rem] = lo;
+    const int c = tt & 31, R0 = tt >> 5;
+    const int ix0 = c + 4 * (R0 & 1) - 3;  // parity 0; parity 1 reads ix0 + 2
+    const bool okx0 = ix0 >= 0 && ix0 < H0, okx1 = ix0 + 2 >= 0 && ix0 + 2 < H0;
+    float* yb = regA + ex * 4 * YBLK + c;  // blocks (hl, par) at yb + (2 hl + par) YBLK
+#pragma unroll
+    for (int R = R0; R < YROWS; R += 16) {
+      const int iy = (R >> 1) - 3;
+      const bool oky = iy >= 0 && iy < H0;
+      const int xi = (oky ? iy : 0) * H0 + ix0;
+      const float v0 = (oky && okx0) ? S.xstage[ex][xi] : 0.0f;
+      const float v1 = (oky && okx1) ? S.xstage[ex][xi + 2] : 0.0f;
+      float h0, l0, h1, l1;
+      split_hl(v0, h0, l0);
+      split_hl(v1, h1, l1);
+      yb[R * YS] = h0;
+      yb[YBLK + R * YS] = h1;
+      yb[2 * YBLK + R * YS] = l0;
+      yb[3 * YBLK + R * YS] = l1;
     }
   }
   tc::fence_proxy_async();
@@ -248,16 +259,20 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
 
   // ---- conv2 im2col as the B operand: rows hl*32 + pair position, K = (c,u,v)
   // regA[kmaj(32 hl + 16 ex + pos, k, 128, 1024)]; 32 lanes fill one core.
+  // lane = (position % 8) * 4 + k % 4 (one core row each); warp wh takes the
+  // (position-group pg, k-group kq) cores pg = wh & 1, kq = wh / 2 + 8 j
   if (has) {
-    for (int i = tt; i < KC2 * NP2; i += NT) {
-      const int kl = i & 3, r8 = (i >> 2) & 7, pg = (i >> 5) & 1, kq = i >> 6;
-      const int pos = pg * 8 + r8, k = kq * 4 + kl;
-      const int c = k >> 4, u = (k >> 2) & 3, v = k & 3, oy = pos >> 2, ox = pos & 3;
-      const float x = S.p1[ex][c * PO * PO + (oy + u) * PO + ox + v];
+    const int r8 = lane >> 2, kl = lane & 3;
+    const int pg = wh & 1;
+    const float* src = S.p1[ex] + (r8 >> 2) * PO + (r8 & 3) + kl + pg * 2 * PO;
+    float* dst = regA + lane + (ex * 2 + pg) * 32;
+#pragma unroll
+    for (int kq = wh >> 1; kq < KC2 / 4; kq += NW / 2) {
+      const float x = src[(kq >> 2) * PO * PO + (kq & 3) * PO];
       float hi, lo;
       split_hl(x, hi, lo);
-      regA[kmaj_f(ex * 16 + pos, k, 128, 1024)] = hi;
-      regA[kmaj_f(32 + ex * 16 + pos, k, 128, 1024)] = lo;
+      dst[kq * 256] = hi;
+      dst[kq * 256 + 128] = lo;
     }
   }
   tc::fence_proxy_async();
@@ -385,16 +400,18 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   } else if (has) {
     // the im2col again, transposed (A of conv2 dW): rows k, K = position,
     // regA[(2 ex + hl) * 4096 + kmaj(k, pos, 128, 4096)]
-    for (int i = tt - 32; i < KC2 * NP2; i += NT - 32) {
-      const int pl = i & 3, r8 = (i >> 2) & 7, kg = (i >> 5) & 31, pq = i >> 10;
-      const int k = kg * 8 + r8, pos = pq * 4 + pl;
-      const int c = k >> 4, u = (k >> 2) & 3, v = k & 3, oy = pos >> 2, ox = pos & 3;
-      const float x = S.p1[ex][c * PO * PO + (oy + u) * PO + ox + v];
+    // lane = (k % 8) * 4 + position % 4; warps 1..15 take the cores
+    // (k-group kg, position quad pq), combo = kg * 4 + pq
+    const int r8 = lane >> 2, pl = lane & 3;
+    const int l0 = (r8 >> 2) * PO + (r8 & 3) + pl;  // (u%2 half, v, ox) part of the gather
+    float* dst = regA + (2 * ex) * 4096 + lane;
+    for (int cb = wh - 1; cb < 32 * 4; cb += NW - 1) {
+      const int kg = cb >> 2, pq = cb & 3;
+      const float x = S.p1[ex][(kg >> 1) * PO * PO + pq * PO + (kg & 1) * 2 * PO + l0];
       float hi, lo;
       split_hl(x, hi, lo);
-      const int o = kmaj_f(k, pos, 128, 4096);
-      regA[(2 * ex) * 4096 + o] = hi;
-      regA[(2 * ex + 1) * 4096 + o] = lo;
+      dst[kg * 32 + pq * 1024] = hi;
+      dst[4096 + kg * 32 + pq * 1024] = lo;
     }
     PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 18, 32);
   }
@@ -559,18 +576,21 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   float b1part = 0.0f;
   float* Z = regA + ex * 8704;
   if (has) {
-    for (int i = tt; i < D1 * O1 * 16; i += NT) {  // i = (oy*16 + ox)*16 + d
-      const int d = i & 15, kp = i >> 4, oy = kp >> 4, ox = kp & 15;
+    // element (oy*16 + ox)*16 + d: thread tt has d = tt % 16, ox = (tt / 16) % 16,
+    // oy = tt / 256 + 2 j (so the pooled row is j and the window slot fixed)
+    const int d = tt & 15, ox = (tt >> 4) & 15, oy0 = tt >> 8;
+    const int slot = oy0 * 2 + (ox & 1);
+    const int pb = d * PO * PO + (ox >> 1);
+    float* dst = d1c + kmaj_f(d, (tt >> 4), 128, 512);
+#pragma unroll
+    for (int j = 0; j < PO; ++j) {
       float g = 0.0f;
-      if (ox < O1) {
-        const int pi = d * PO * PO + (oy >> 1) * PO + (ox >> 1);
-        const int slot = (oy & 1) * 2 + (ox & 1);
-        g = (S.pidx[ex][pi] == slot && S.p1[ex][pi] > 0.0f) ? dp1[pi] : 0.0f;
-      }
+      const int pi = pb + j * PO;
+      if (ox < O1 && S.pidx[ex][pi] == slot && S.p1[ex][pi] > 0.0f) g = dp1[pi];
       float hi, lo;
       split_hl(g, hi, lo);
-      d1c[kmaj_f(d, kp, 128, 512)] = hi;
-      d1c[kmaj_f(16 + d, kp, 128, 512)] = lo;
+      dst[j * 1024] = hi;
+      dst[j * 1024 + 64] = lo;
       b1part += g;
     }
     // Z[R' = 2R + hl][j4][c = 4p + s][i] = xpad[R][2 (4 j4 + s + i) + p]: for tap
@@ -579,14 +599,19 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
     // core matrix is eight taps of one kernel row (permuted v) x four
     // positions, rows 16 B apart; kernel row u and the hi/lo copy are the
     // rows R' (SBO 512 B), position quads the j4 chunks (LBO 128 B).
-    for (int i = tt; i < 34 * 128; i += NT) {
-      const int i4 = i & 3, c = (i >> 2) & 7, j4 = (i >> 5) & 3, R = i >> 7;
-      const int iy = R - 3, ix = 2 * (4 * j4 + (c & 3) + i4) + (c >> 2) - 3;
-      const float v = (iy >= 0 && iy < H0 && ix >= 0 && ix < H0) ? S.xstage[ex][iy * H0 + ix] : 0.0f;
-      float hi, lo;
-      split_hl(v, hi, lo);
-      Z[(2 * R) * 128 + (i & 127)] = hi;
-      Z[(2 * R + 1) * 128 + (i & 127)] = lo;
+    {
+      const int col = tt & 127, i4 = col & 3, c = (col >> 2) & 7, j4 = col >> 5;
+      const int ix = 2 * (4 * j4 + (c & 3) + i4) + (c >> 2) - 3;
+      const bool okx = ix >= 0 && ix < H0;
+#pragma unroll
+      for (int R = tt >> 7; R < 34; R += 4) {
+        const int iy = R - 3;
+        const float v = (okx && iy >= 0 && iy < H0) ? S.xstage[ex][iy * H0 + ix] : 0.0f;
+        float hi, lo;
+        split_hl(v, hi, lo);
+        Z[(2 * R) * 128 + col] = hi;
+        Z[(2 * R + 1) * 128 + col] = lo;
+      }
     }
   }
   b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
@@ -675,8 +700,8 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
     }
   }
   double v5[5] = {sq, a2sq, hsq, dz1sq, dz2sq};
-#pragma unroll
-  for (int q = 0; q < 5; ++q)
+  const int nq = wh == 0 ? 5 : 2;  // the h / dz terms live in warp 0 of the half
+  for (int q = 0; q < nq; ++q)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v5[q] += __shfl_xor_sync(0xffffffffu, v5[q], o);
   if (lane == 0)

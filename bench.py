@@ -306,11 +306,15 @@ def run_ours(args):
     _lib.check(_lib.lib.pgb_device_stream(engine.handle, C.byref(sp)))
     stream = torch.cuda.ExternalStream(sp.value, device=f"cuda:{dev}")
 
-    def step(i):
-        b = i % nbatches
-        _lib.check(_lib.lib.pgb_dpsgd_step_device(
-            engine.handle, C.c_void_p(dx.data_ptr() + b * BATCH * row * 4),
-            C.c_void_p(dy.data_ptr() + b * BATCH * 4), C.byref(ccfg), i))
+    def run_steps(i0, n):
+        """n steps from step index i0; step i reads resident batch i mod nbatches
+        (pgb_run_steps_device: static multi-step CUDA graphs for the fused MNIST
+        schedule, one pgb_dpsgd_step_device-equivalent step each)."""
+        launches = C.c_int64()
+        _lib.check(_lib.lib.pgb_run_steps_device(
+            engine.handle, C.c_void_p(dx.data_ptr()), C.c_void_p(dy.data_ptr()), nbatches, n,
+            C.byref(ccfg), i0, C.byref(launches)))
+        return launches.value
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -325,8 +329,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for i in range(args.warmup):
-        step(i)
+    run_steps(0, args.warmup)
     _lib.check(_lib.lib.pgb_synchronize(engine.handle, None, None))
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -334,8 +337,7 @@ def run_ours(args):
     with ClockSampler(dev) as clocks:
         ev0.record(stream)
         h0 = time.perf_counter()
-        for i in range(args.steps):
-            step(args.warmup + i)
+        timed_launches = run_steps(args.warmup, args.steps)
         host_issue = (time.perf_counter() - h0) / args.steps
         ev1.record(stream)
         ev1.synchronize()
@@ -350,8 +352,10 @@ def run_ours(args):
     sub = Pk.Dataset(data.inputs[: e_steps * BATCH], data.labels[: e_steps * BATCH],
                      data.name, e_steps * BATCH, data.classes)
     norms = np.empty(e_steps * BATCH, np.float32)
-    warm = Pk.Dataset(data.inputs[:BATCH * 2], data.labels[:BATCH * 2], data.name, BATCH * 2,
-                      data.classes)
+    # warm-up epoch long enough to build the driver's multi-step graphs for
+    # every input-chunk slot (one-time setup, outside the timed region)
+    wn = min(nbatches, 32) * BATCH
+    warm = Pk.Dataset(data.inputs[:wn], data.labels[:wn], data.name, wn, data.classes)
     Pk.run_epoch(engine, model, warm, cfg, 0)
     barrier()
     w0 = time.perf_counter()
@@ -439,13 +443,13 @@ def run_ours(args):
             "e2e": {"value": e2e, "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * row * 4 + BATCH * 4,
                     "d2h_bytes_per_step": BATCH * 4 + 8,
-                    "api": "pgb_run_epoch (pinned host batches, per-step H2D + D2H)"},
+                    "api": "pgb_run_epoch (pinned host batches; every step's inputs copied H2D and its norms + clip count read back D2H inside the timed region, 8 steps per copy / graph launch)"},
             "roofline": roof,
             "aggregate_roofline": agg,
             "kernels_us": {n: round(m * 1e3, 3) for n, m in by_name.items()},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
-            "gpu_launches": kps * args.steps,
+            "gpu_launches": timed_launches,
             "kernels_per_step": kps,
             "host_issue_us_per_step": round(host_issue * 1e6, 2),
             "e2e_us_per_step": round(e2e_t / e_steps * 1e6, 2),

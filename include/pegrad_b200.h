@@ -195,6 +195,15 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y,
                          int64_t step0, float* norms_out,
                          int64_t* clipped_total, double* seconds_out);
 
+/* n_steps DPSGD steps over a device-resident ring of n_batches batches
+ * (d_x: (n_batches * B, ...) device pointer); step step0 + i reads batch
+ * (step0 + i) mod n_batches. Asynchronous on the engine stream; the fused
+ * MNIST schedule runs as static multi-step CUDA graphs. *launches_out (nullable)
+ * = kernels launched. Same semantics as n calls of pgb_dpsgd_step_device.
+ * Replaces the step loop of proj/core/src/harness.cpp:147-151 on resident data. */
+pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_y,
+                                int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg,
+                                int64_t step0, int64_t* launches_out);
 /* Device addresses for zero-copy interop (torch, benchmarks). */
 pgb_status pgb_device_params(pgb_engine* e, float** d_params);
 pgb_status pgb_device_stream(pgb_engine* e, void** cuda_stream);

@@ -103,6 +103,8 @@ EXPORTS = {
                                     C.c_void_p, C.c_void_p]),
     "pgb_debug_umma_probe": (C.c_int, [C.c_int32] * 6 + [C.c_void_p] * 3),
     "pgb_debug_umma_rate": (C.c_int, [C.c_int32] * 4 + [C.c_void_p, C.c_int32, C.c_void_p]),
+    "pgb_run_steps_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.POINTER(DpConfigC), C.c_int64, C.POINTER(C.c_int64)]),
     "pgb_device_params": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_device_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_kernels_per_step": (C.c_int32, [C.c_void_p]),

@@ -144,12 +144,16 @@ struct Engine {
     if (steps <= stage_steps && units <= stage_units) return;
     if (h_norm_stage) cudaFreeHost(h_norm_stage);
     if (h_clip_stage) cudaFreeHost(h_clip_stage);
+    if (h_step_base) cudaFreeHost(h_step_base);
     h_norm_stage = nullptr;
     h_clip_stage = nullptr;
+    h_step_base = nullptr;
     stage_steps = std::max(steps, stage_steps);
     stage_units = std::max(units, stage_units);
     PGB_CUDA(cudaMallocHost(&h_norm_stage, sizeof(float) * stage_steps * stage_units));
     PGB_CUDA(cudaMallocHost(&h_clip_stage, sizeof(int) * 2 * stage_steps));
+    // one step index per chunk (never rewritten while its copy may be pending)
+    PGB_CUDA(cudaMallocHost(&h_step_base, sizeof(long long) * (stage_steps + 1)));
   }
   // epoch-driver input chunks (device, grown on demand): a pinned H2D copy
   // moves ~15-30 GB/s at one batch (0.8 MB) but ~40-50 GB/s at >= 12 MB, so
@@ -157,6 +161,27 @@ struct Engine {
   float* d_xc[kSlots] = {};
   float* d_yc[kSlots] = {};
   int64_t chunk_cap = 0;
+  // multi-step graphs of the epoch driver (fused MNIST): chunk slot sl runs C
+  // steps from d_xc[sl]; their step indices are *d_step_base[sl] + j, so the
+  // graph is static and the host only writes one value per chunk
+  long long* d_step_base = nullptr;  // (kSlots + 1): chunk slots + the resident-data graph
+  long long* h_step_base = nullptr;  // pinned (kSlots)
+  const long long* cap_step_base = nullptr;  // set while capturing
+  int cap_step_off = 0;
+  const float* cap_xring = nullptr;  // resident-data ring (run_steps_device)
+  const float* cap_yring = nullptr;
+  int cap_ring_n = 0;
+  struct ChunkGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    StepArgs args{};
+    int64_t C = 0;
+  };
+  ChunkGraph chunk_graphs[kSlots];
+  ChunkGraph resident;  // C steps over a device-resident batch ring
+  const float* resident_x = nullptr;
+  const float* resident_y = nullptr;
+  int resident_n = 0;
   void ensure_chunk_ring(int64_t steps_per_chunk) {
     if (steps_per_chunk <= chunk_cap) return;
     for (int i = 0; i < kSlots; ++i) {
@@ -246,7 +271,13 @@ struct Engine {
     for (int i = 0; i < kSlots; ++i) {
       if (d_xc[i]) cudaFree(d_xc[i]);
       if (d_yc[i]) cudaFree(d_yc[i]);
+      if (chunk_graphs[i].exec) cudaGraphExecDestroy(chunk_graphs[i].exec);
+      if (chunk_graphs[i].graph) cudaGraphDestroy(chunk_graphs[i].graph);
     }
+    if (resident.exec) cudaGraphExecDestroy(resident.exec);
+    if (resident.graph) cudaGraphDestroy(resident.graph);
+    if (d_step_base) cudaFree(d_step_base);
+    if (h_step_base) cudaFreeHost(h_step_base);
     for (int i = 0; i < kSlots; ++i)
       for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i]})
         if (ev) cudaEventDestroy(ev);
@@ -343,6 +374,7 @@ struct Engine {
     }
     want((void**)&d_norms_ring, sizeof(float) * B * kResSlots);
     want((void**)&d_clip_ring, sizeof(int) * 2 * kResSlots);
+    want((void**)&d_step_base, sizeof(long long) * (kSlots + 1));
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
@@ -705,6 +737,12 @@ struct Engine {
     }
     prm.pair_off[8] = pairs;
     prm.tcw = d_tcw;
+    prm.step_base = cap_step_base;
+    prm.step_off = cap_step_off;
+    prm.xring = cap_xring;
+    prm.yring = cap_yring;
+    prm.ring_origin = 0;
+    prm.ring_n = cap_ring_n;
     if (mnist_tc) {
       mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm);
       return mark(s, "mnist_tc");
@@ -990,6 +1028,96 @@ struct Engine {
     PGB_CUDA(cudaGraphLaunch(it->second.exec, stream));
   }
 
+  // The static graph of C consecutive steps reading chunk slot sl (fused
+  // MNIST, one process): step j reads batch j of d_xc[sl], takes its step
+  // index from d_step_base[sl] + j and writes its results to result slot
+  // sl * C + j. Rebuilt only when C or the DP configuration changes.
+  cudaGraphExec_t chunk_graph(int sl, int64_t C, const StepArgs& args) {
+    ChunkGraph& cg = chunk_graphs[sl];
+    StepArgs a0 = args;
+    a0.step = 0;
+    if (cg.exec && cg.C == C && std::memcmp(&cg.args, &a0, sizeof(StepArgs)) == 0) return cg.exec;
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    if (cg.graph) cudaGraphDestroy(cg.graph);
+    cg = ChunkGraph{};
+    float* nd0 = norms_dst;
+    int* cd0 = clipped_dst;
+    PGB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int64_t j = 0; j < C; ++j) {
+        cur_args = a0;
+        norms_dst = d_norms_ring + (size_t)(sl * C + j) * B;
+        clipped_dst = d_clip_ring + 2 * (sl * C + j);
+        cap_step_base = d_step_base + sl;
+        cap_step_off = (int)j;
+        kernels_last = enqueue_step(stream, d_xc[sl] + j * B * in_row, d_yc[sl] + j * B, 1);
+      }
+    } catch (...) {
+      cap_step_base = nullptr;
+      cudaStreamEndCapture(stream, &cg.graph);
+      if (cg.graph) cudaGraphDestroy(cg.graph);
+      cg.graph = nullptr;
+      throw;
+    }
+    cap_step_base = nullptr;
+    cap_step_off = 0;
+    norms_dst = nd0;
+    clipped_dst = cd0;
+    PGB_CUDA(cudaStreamEndCapture(stream, &cg.graph));
+    PGB_CUDA(cudaGraphInstantiate(&cg.exec, cg.graph, 0));
+    cg.args = a0;
+    cg.C = C;
+    return cg.exec;
+  }
+
+  // The static graph of C consecutive steps over a device-resident ring of
+  // n batches (step s reads batch s mod n; the step index lives in
+  // d_step_base[kSlots] and the graph's last node advances it by C).
+  cudaGraphExec_t resident_graph(int64_t C, const StepArgs& args, const float* xr,
+                                 const float* yr, int n) {
+    ChunkGraph& cg = resident;
+    StepArgs a0 = args;
+    a0.step = 0;
+    if (cg.exec && cg.C == C && std::memcmp(&cg.args, &a0, sizeof(StepArgs)) == 0 &&
+        resident_x == xr && resident_y == yr && resident_n == n)
+      return cg.exec;
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    if (cg.graph) cudaGraphDestroy(cg.graph);
+    cg = ChunkGraph{};
+    PGB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int64_t j = 0; j < C; ++j) {
+        cur_args = a0;
+        cap_step_base = d_step_base + kSlots;
+        cap_step_off = (int)j;
+        cap_xring = xr;
+        cap_yring = yr;
+        cap_ring_n = n;
+        kernels_last = enqueue_step(stream, xr, yr, 1);
+      }
+      advance_counter_kernel<<<1, 1, 0, stream>>>(d_step_base + kSlots, C);
+    } catch (...) {
+      cap_step_base = nullptr;
+      cap_xring = cap_yring = nullptr;
+      cudaStreamEndCapture(stream, &cg.graph);
+      if (cg.graph) cudaGraphDestroy(cg.graph);
+      cg.graph = nullptr;
+      throw;
+    }
+    cap_step_base = nullptr;
+    cap_step_off = 0;
+    cap_xring = cap_yring = nullptr;
+    cap_ring_n = 0;
+    PGB_CUDA(cudaStreamEndCapture(stream, &cg.graph));
+    PGB_CUDA(cudaGraphInstantiate(&cg.exec, cg.graph, 0));
+    cg.args = a0;
+    cg.C = C;
+    resident_x = xr;
+    resident_y = yr;
+    resident_n = n;
+    return cg.exec;
+  }
+
   // The kernel nodes whose parameters change from step to step.
   void find_step_nodes(StepGraph& sg) {
     size_t n = 0;
@@ -1242,6 +1370,55 @@ pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d
   });
 }
 
+pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_y,
+                                int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg,
+                                int64_t step0, int64_t* launches_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg || !d_x || !d_y) raise(PGB_ERR_CONTRACT, "null argument");
+    if (n_batches <= 0 || n_steps < 0) raise(PGB_ERR_CONFIG, "run_steps_device: bad counts");
+    validate_dp_config(*cfg, en.B);
+    en.last_cfg = *cfg;
+    int64_t launches = 0;
+    auto batch = [&](int64_t s) {
+      const int64_t bi = ((s % n_batches) + n_batches) % n_batches;
+      return std::make_pair(d_x + bi * en.B * en.in_row, d_y + bi * en.B);
+    };
+    int64_t C = 8;
+    if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
+    const bool chunked = en.fused_mnist && en.world == 1 && cfg->microbatch == 1 &&
+                         en.graph_enabled && C > 1 && n_steps >= C && n_batches < (1 << 30);
+    int64_t s = 0;
+    if (chunked) {
+      const StepArgs a0 = en.make_args(*cfg, step0, nullptr, nullptr);
+      cudaGraphExec_t g = en.resident_graph(C, a0, d_x, d_y, (int)n_batches);
+      set_counter_kernel<<<1, 1, 0, en.stream>>>(en.d_step_base + Engine::kSlots, step0);
+      ++launches;
+      for (; s + C <= n_steps; s += C) {
+        PGB_CUDA(cudaGraphLaunch(g, en.stream));
+        launches += C * en.kernels_last + 1;
+      }
+    }
+    for (; s < n_steps; ++s) {
+      const auto in = batch(step0 + s);
+      en.push_args(en.make_args(*cfg, step0 + s, in.first, in.second));
+      if (en.fused_mnist && en.graph_enabled) {
+        en.launch_step(in.first, in.second, cfg->microbatch);
+      } else {
+        PGB_CUDA(cudaMemcpyAsync(en.d_x, in.first, sizeof(float) * en.B * en.in_row,
+                                 cudaMemcpyDeviceToDevice, en.stream));
+        PGB_CUDA(cudaMemcpyAsync(en.d_y, in.second, sizeof(float) * en.B,
+                                 cudaMemcpyDeviceToDevice, en.stream));
+        en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+      }
+      launches += en.kernels_last;
+    }
+    en.last_step = step0 + n_steps - 1;
+    PGB_CUDA(cudaGetLastError());
+    if (launches_out) *launches_out = launches;
+  });
+}
+
 pgb_status pgb_synchronize(pgb_engine* e, float* norms_out, pgb_step_report* rep) {
   return guarded([&] {
     Engine& en = E(e);
@@ -1417,17 +1594,18 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     // its input pointers as graph-node parameters, so any offset inside a
     // chunk works; the layer-wise schedule bakes its input slot into the
     // graph and keeps one batch per chunk.
-    // One batch per copy by default: at the current step time (~30 us) a 0.8
-    // MB copy (~25 us at ~32 GB/s) already hides under compute, and larger
-    // chunks only lengthen the pipeline fill (scripts/e2e_probe.py).
-    // PGB_CHUNK_BYTES=<bytes> groups batches per copy.
-    int64_t chunk_bytes = 0;
-    if (const char* cb = std::getenv("PGB_CHUNK_BYTES")) chunk_bytes = std::atoll(cb);
-    const int64_t C = en.fused_mnist
-                          ? std::max<int64_t>(1, std::min<int64_t>(steps, chunk_bytes / (int64_t)xb))
-                          : 1;
+    // Fused MNIST on one GPU: static graphs of C steps per input chunk (one
+    // H2D copy of C batches, one graph launch, one read-back of C steps'
+    // results), so the host issues ~10 calls per C steps instead of ~10 per
+    // step. PGB_CHUNK_STEPS overrides C (1 = the per-step path below).
+    int64_t C = 8;  // 4-8 measured best (scripts/e2e_probe.py)
+    if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
+    C = std::min<int64_t>(C, Engine::kResSlots / K);
+    const bool chunked = en.fused_mnist && en.world == 1 && cfg->microbatch == 1 &&
+                         en.graph_enabled && C > 1 && steps >= C;
+    if (!chunked) C = 1;
     if (C > 1) en.ensure_chunk_ring(C);
-    const int64_t nchunks = (steps + C - 1) / C;
+    const int64_t nchunks = (steps + C - 1) / C, nfull = steps / C;
     auto xslot = [&](int sl) { return C > 1 ? en.d_xc[sl] : en.d_xb[sl]; };
     auto yslot = [&](int sl) { return C > 1 ? en.d_yc[sl] : en.d_yb[sl]; };
     auto copy_in = [&](int64_t k) {
@@ -1439,21 +1617,48 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
                                cudaMemcpyHostToDevice, en.copy_stream));
       PGB_CUDA(cudaMemcpyAsync(yslot(sl), y + k * C * en.B, yb * cnt, cudaMemcpyHostToDevice,
                                en.copy_stream));
+      if (chunked) {
+        en.h_step_base[k] = step0 + k * C;
+        PGB_CUDA(cudaMemcpyAsync(en.d_step_base + sl, en.h_step_base + k, sizeof(long long),
+                                 cudaMemcpyHostToDevice, en.copy_stream));
+      }
       PGB_CUDA(cudaEventRecord(copied[sl], en.copy_stream));
     };
     for (int64_t k = 0; k < std::min<int64_t>(K - 1, nchunks); ++k) copy_in(k);
-    for (int64_t s = 0; s < steps; ++s) {
+    const StepArgs args0 = en.make_args(*cfg, step0, nullptr, nullptr);
+    for (int64_t k = 0; chunked && k < nfull; ++k) {
+      const int sl = (int)(k % K);
+      if (k + K - 1 < nchunks) copy_in(k + K - 1);
+      PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
+      // result slots sl*C .. sl*C+C-1 of chunk k-K must have been read back
+      if (k >= K) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[sl], 0));
+      PGB_CUDA(cudaGraphLaunch(en.chunk_graph(sl, C, args0), en.stream));
+      PGB_CUDA(cudaEventRecord(consumed[sl], en.stream));
+      PGB_CUDA(cudaEventRecord(done[sl], en.stream));
+      PGB_CUDA(cudaStreamWaitEvent(en.out_stream, done[sl], 0));
+      PGB_CUDA(cudaMemcpyAsync(en.h_clip_stage + 2 * k * C, en.d_clip_ring + 2 * sl * C,
+                               sizeof(int) * 2 * C, cudaMemcpyDeviceToHost, en.out_stream));
+      if (norms_out)
+        PGB_CUDA(cudaMemcpyAsync(en.h_norm_stage + k * C * U, en.d_norms_ring + sl * C * en.B,
+                                 sizeof(float) * C * U, cudaMemcpyDeviceToHost, en.out_stream));
+      PGB_CUDA(cudaEventRecord(read[sl], en.out_stream));
+    }
+    // per-step path: every step of a non-chunked epoch, or the remainder of a
+    // chunked one (result slots from K*C on, clear of the chunk slots)
+    const int64_t s_begin = chunked ? nfull * C : 0;
+    for (int64_t s = s_begin; s < steps; ++s) {
       const int64_t k = s / C, j = s % C;
       const int sl = (int)(k % K);
       constexpr int KR = Engine::kResSlots;
-      const int rs_sl = (int)(s % KR);  // result slot
+      const int rs_sl = chunked ? (int)(K * C + (s - s_begin) % (KR - K * C)) : (int)(s % KR);
       if (j == 0) {
-        if (k + K - 1 < nchunks) copy_in(k + K - 1);
+        if (!chunked && k + K - 1 < nchunks) copy_in(k + K - 1);
         PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
       }
       if (ring) {
         // result slot rs_sl's previous results must have been read back
-        if (s >= KR) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[rs_sl], 0));
+        if (s - s_begin >= KR - (chunked ? K * C : 0))
+          PGB_CUDA(cudaStreamWaitEvent(en.stream, read[rs_sl], 0));
         en.norms_dst = en.d_norms_ring + (size_t)rs_sl * en.B;
         en.clipped_dst = en.d_clip_ring + 2 * rs_sl;
       }

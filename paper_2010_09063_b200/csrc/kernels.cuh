@@ -1044,6 +1044,10 @@ __global__ void transpose_kernel(const float* __restrict__ src, int rows, int co
   }
 }
 
+// device-side step counter of the multi-step graphs
+__global__ void set_counter_kernel(long long* v, long long value) { *v = value; }
+__global__ void advance_counter_kernel(long long* v, long long by) { *v += by; }
+
 // Holds the stream for `ns` nanoseconds (profiling: lets the host queue a
 // whole instrumented step before the GPU starts it).
 __global__ void spin_kernel(long long ns) {

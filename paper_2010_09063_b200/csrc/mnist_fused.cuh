@@ -96,7 +96,33 @@ struct Params {
   long long size[8];    // parameter block sizes
   long long pair_off[9];  // prefix sums of ceil(|p| / 2)
   const float* tcw;       // hi/lo UMMA operand shadows of the conv weights (tc_kernel)
+  // multi-step epoch graphs: the step index is *step_base + step_off (the
+  // host writes step_base once per chunk of steps), else a.step
+  const long long* step_base;
+  int step_off;
+  // ... and, for device-resident data, the batch is picked from a ring of
+  // ring_n batches by the step index: batch (step - ring_origin) mod ring_n
+  const float* xring;
+  const float* yring;
+  long long ring_origin;
+  int ring_n;
 };
+
+__device__ __forceinline__ long long step_index(const Params& prm) {
+  return prm.step_base ? *prm.step_base + prm.step_off : prm.a.step;
+}
+
+// this step's input batch (x, y)
+__device__ __forceinline__ void step_inputs(const Params& prm, const float*& x, const float*& y) {
+  x = prm.x;
+  y = prm.y;
+  if (prm.xring) {
+    long long bi = (step_index(prm) - prm.ring_origin) % prm.ring_n;
+    if (bi < 0) bi += prm.ring_n;
+    x = prm.xring + bi * prm.B * (H0 * H0);
+    y = prm.yring + bi * prm.B;
+  }
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -152,7 +178,9 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
                  :: "r"(smem_addr(&S.bar[0])), "r"(kBytes0) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(smem_addr(&S.bar[1])), "r"(kBytes1) : "memory");
-    bulk_g2s(S.u1.xstage, prm.x + (size_t)b * H0 * H0, sizeof(float) * H0 * H0, &S.bar[0]);
+    const float *gx, *gy;
+    step_inputs(prm, gx, gy);
+    bulk_g2s(S.u1.xstage, gx + (size_t)b * H0 * H0, sizeof(float) * H0 * H0, &S.bar[0]);
     bulk_g2s(S.w1t, prm.w1t, sizeof(float) * D1 * K1 * K1, &S.bar[0]);
     bulk_g2s(S.b1, W + prm.off[1], sizeof(float) * D1, &S.bar[0]);
     bulk_g2s(S.b2, W + prm.off[3], sizeof(float) * D2, &S.bar[1]);
@@ -163,7 +191,11 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   if (t < H1 * NC) S.w4[t] = __ldg(gW4 + t);
   else if (t < H1 * NC + NC) S.b4[t - H1 * NC] = __ldg(gb4 + t - H1 * NC);
   else if (t < H1 * NC + NC + H1) S.b3[t - H1 * NC - NC] = __ldg(gb3 + t - H1 * NC - NC);
-  else if (t == H1 * NC + NC + H1) S.yb = prm.y[b];
+  else if (t == H1 * NC + NC + H1) {
+    const float *gx, *gy;
+    step_inputs(prm, gx, gy);
+    S.yb = gy[b];
+  }
   // zero the padding ring of xs while the copies fly
   for (int i = t; i < XP * XS; i += NT) {
     const int r = i / XS - 3, c = i % XS - 3;
@@ -350,7 +382,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
       while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
       const long long jp = q - prm.pair_off[p];
       float n0, n1;
-      gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
+      gauss_pair(stream_key(prm.a.seed, noise_stream(step_index(prm), p)), jp, &n0, &n1);
       float* dst = prm.noise + prm.off[p] + 2 * jp;
       dst[0] = n0;
       if (2 * jp + 1 < prm.size[p]) dst[1] = n1;

@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
                  :: "r"(smem_addr(&S.bar[0])), "r"(img + 8192u) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(smem_addr(&S.bar[1])), "r"(65536u) : "memory");
-    bulk_g2s(S.xstage[0], prm.x + (size_t)b0 * H0 * H0, img, reinterpret_cast<unsigned long long*>(&S.bar[0]));
+    const float *gx, *gy;
+    step_inputs(prm, gx, gy);
+    bulk_g2s(S.xstage[0], gx + (size_t)b0 * H0 * H0, img, reinterpret_cast<unsigned long long*>(&S.bar[0]));
     bulk_g2s(regA + OFF_W1C, tcw + TCW_W1C, 8192u, reinterpret_cast<unsigned long long*>(&S.bar[0]));
     bulk_g2s(S.w2, tcw + TCW_W2C, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[1]));
   }
@@ -133,7 +135,11 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
   else if (t < H1 * NC + NC + H1) S.b3[t - H1 * NC - NC] = __ldg(W + prm.off[5] + t - H1 * NC - NC);
   else if (t < H1 * NC + NC + H1 + D1) S.b1[t - 362] = __ldg(W + prm.off[1] + t - 362);
   else if (t < H1 * NC + NC + H1 + D1 + D2) S.b2[t - 378] = __ldg(W + prm.off[3] + t - 378);
-  if (tt == 0 && has) S.yb[ex] = prm.y[b];
+  if (tt == 0 && has) {
+    const float *gx, *gy;
+    step_inputs(prm, gx, gy);
+    S.yb[ex] = gy[b];
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
         while (p < 7 && prm.pair_off[p + 1] <= q) ++p;
         const long long jp = q - prm.pair_off[p];
         float n0, n1;
-        gauss_pair(stream_key(prm.a.seed, noise_stream(prm.a.step, p)), jp, &n0, &n1);
+        gauss_pair(stream_key(prm.a.seed, noise_stream(step_index(prm), p)), jp, &n0, &n1);
         float* dst = prm.noise + prm.off[p] + 2 * jp;
         dst[0] = n0;
         if (2 * jp + 1 < prm.size[p]) dst[1] = n1;

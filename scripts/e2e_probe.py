@@ -1,4 +1,4 @@
-"""e2e epoch driver vs input chunk size (PGB_CHUNK_BYTES), MNIST B=256."""
+"""e2e epoch driver vs steps per chunk graph (PGB_CHUNK_STEPS), MNIST B=256."""
 import os
 import sys
 import time
@@ -16,13 +16,13 @@ data = P.synth_for_model(desc, N, 0, pinned=True)
 eng = P.GradEngine(model, P.Strategy.groupconv, B)
 cfg = P.DpConfig(1.0, 1.1, 0.1, 1, 0)
 norms = np.empty(N, np.float32)
-for cb in (0, 803840, 4 * 803840, 16 << 20, 64 << 20):
-    os.environ["PGB_CHUNK_BYTES"] = str(cb)
+for cs in (1, 4, 8, 16, 21):
+    os.environ["PGB_CHUNK_STEPS"] = str(cs)
     P.run_epoch(eng, model, data, cfg, 0, norms)
     t0 = time.perf_counter()
     P.run_epoch(eng, model, data, cfg, 0, norms)
     dt = time.perf_counter() - t0
-    print(f"chunk {cb:>9} B: {dt / 234 * 1e6:7.1f} us/step, {N / dt / 1e6:.2f} M ex/s", flush=True)
+    print(f"chunk {cs:>3} steps: {dt / 234 * 1e6:7.1f} us/step, {N / dt / 1e6:.2f} M ex/s", flush=True)
 # raw copy of the same dataset in 12.9 MB pieces on a side stream
 x = torch.from_numpy(data.inputs.reshape(-1))
 d = torch.empty(16 * B * 784, device="cuda")

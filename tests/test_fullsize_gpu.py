@@ -158,3 +158,37 @@ def test_cifar_b256_matches_batch8_engines(P, O):
         w = want[off:off + n]
         assert np.linalg.norm(got[off:off + n] - w) <= TOL * np.linalg.norm(w)
         off += n
+
+
+def test_mnist_run_steps_device_matches_step_calls(P, O):
+    """pgb_run_steps_device (static multi-step graphs, step index and batch
+    picked on the device) gives bitwise the parameters of the same steps
+    issued one pgb_dpsgd_step_device call at a time, including a remainder
+    that does not fill a graph."""
+    torch = pytest.importorskip("torch")
+    from paper_2010_09063_b200 import _lib
+    B, NB, STEPS = 256, 5, 19
+    desc, od = _mnist(P, O, B)
+    data = P.synth_for_model(desc, B * NB, 0)
+    dx = torch.from_numpy(data.inputs).cuda()
+    dy = torch.from_numpy(data.labels).cuda()
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0).to_c()
+    out = []
+    for mode in ("steps", "calls"):
+        model = P.build_from_desc(desc, 0)
+        eng = P.GradEngine(model, P.Strategy.groupconv, B)
+        if mode == "steps":
+            n = C.c_int64()
+            _lib.check(_lib.lib.pgb_run_steps_device(eng.handle, C.c_void_p(dx.data_ptr()),
+                                                     C.c_void_p(dy.data_ptr()), NB, STEPS,
+                                                     C.byref(cfg), 3, C.byref(n)))
+            assert n.value >= 2 * STEPS
+        else:
+            for i in range(STEPS):
+                b = (3 + i) % NB
+                _lib.check(_lib.lib.pgb_dpsgd_step_device(
+                    eng.handle, C.c_void_p(dx.data_ptr() + b * B * 784 * 4),
+                    C.c_void_p(dy.data_ptr() + b * B * 4), C.byref(cfg), 3 + i))
+        _lib.check(_lib.lib.pgb_synchronize(eng.handle, None, None))
+        out.append(eng.get_flat_params())
+    np.testing.assert_array_equal(out[0], out[1])

@@ -120,6 +120,9 @@ struct Engine {
   bool norms_fused = false;  // per-example norms produced by the gradient kernel
   bool fused_mnist = false;  // whole per-example pass in one kernel
   bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
+  bool agg_in_kernel = false;  // ... and the aggregation after an in-kernel grid barrier
+  bool fuse_agg_next = false;  // set by enqueue_step for the fused launch it makes
+  unsigned long long* d_grid_ctr = nullptr;
   bool use_tc = true;        // conv GEMMs on tcgen05 (PGB_NO_TC=1: CUDA-core tiles)
   std::vector<int64_t> param_off;
   int64_t P = 0;
@@ -247,6 +250,8 @@ struct Engine {
     AggLaunch agg_args{};
     NoiseLaunch noise_args{};
     mnist::Params fused_args{};
+    AggLaunch fused_agg{};  // the tc_kernel's in-kernel aggregation arguments
+    bool fused_tc = false;
   };
   std::map<int, StepGraph> graphs;  // key: schedule variant
   int kernels_last = 0;
@@ -375,6 +380,7 @@ struct Engine {
     want((void**)&d_norms_ring, sizeof(float) * B * kResSlots);
     want((void**)&d_clip_ring, sizeof(int) * 2 * kResSlots);
     want((void**)&d_step_base, sizeof(long long) * (kSlots + 1));
+    want((void**)&d_grid_ctr, sizeof(unsigned long long));
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
@@ -552,6 +558,16 @@ struct Engine {
     check_strategy_support(strat, desc);
     plan();
     PGB_CUDA(cudaSetDevice(device));
+    // Opt-in (PGB_GRID_SYNC=1): the aggregation inside the tensor-core kernel
+    // after a grid barrier. Measured slower than the PDL-launched aggregation
+    // kernel (the barrier costs ~1.3 us and the tiles run ~2x slower at the
+    // kernel's 64-register budget), so the separate kernel is the default.
+    if (mnist_tc && world == 1 && std::getenv("PGB_GRID_SYNC") != nullptr) {
+      // the in-kernel grid barrier needs every CTA resident: one per SM
+      int sms = 0;
+      PGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      agg_in_kernel = (B + 1) / 2 <= sms;
+    }
     PGB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
@@ -744,8 +760,14 @@ struct Engine {
     prm.ring_origin = 0;
     prm.ring_n = cap_ring_n;
     if (mnist_tc) {
-      mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm);
-      return mark(s, "mnist_tc");
+      AggLaunch L{};
+      if (fuse_agg_next) {
+        L = agg_launch(bt, nparts, (int)B, 0, true);
+        prm.grid_ctr = d_grid_ctr;
+        prm.agg_tiles = L.plan.tile_start[L.plan.n];
+      }
+      mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm, L);
+      return mark(s, fuse_agg_next ? "mnist_tc_step" : "mnist_tc");
     }
     mnist::fused_kernel<<<(unsigned)B, mnist::NT, sizeof(mnist::Smem), s>>>(prm);
     return mark(s, "mnist_fused");
@@ -858,7 +880,18 @@ struct Engine {
   // One full DPSGD step: grads -> [microbatch] -> norms/clip/sum/noise/update.
   int enqueue_step(cudaStream_t s, const float* x_slot, const float* y_slot, int64_t m) {
     int nk = 0;
-    nk += enqueue_grads(s, x_slot, y_slot);
+    // one launch per step: the fused MNIST kernel aggregates in-kernel
+    fuse_agg_next = agg_in_kernel && m == 1;
+    try {
+      nk += enqueue_grads(s, x_slot, y_slot);
+    } catch (...) {
+      fuse_agg_next = false;
+      throw;
+    }
+    if (fuse_agg_next) {
+      fuse_agg_next = false;
+      return nk;
+    }
     if (m > 1) {
       const int U = (int)(B / m);
       materialize_kernel<<<grid_for((size_t)P * B), 256, 0, s>>>(table_for(x_slot), (int)B,
@@ -1142,6 +1175,10 @@ struct Engine {
       } else if (kp.func == (void*)mnist::fused_kernel || kp.func == (void*)mnist::tc_kernel) {
         sg.fused = nd;
         sg.fused_args = *static_cast<const mnist::Params*>(kp.kernelParams[0]);
+        if (kp.func == (void*)mnist::tc_kernel) {
+          sg.fused_tc = true;
+          sg.fused_agg = *static_cast<const AggLaunch*>(kp.kernelParams[1]);
+        }
       }
     }
   }
@@ -1150,10 +1187,10 @@ struct Engine {
     return std::memcmp(&a, &b, sizeof(StepArgs)) == 0;
   }
 
-  void set_node(cudaGraphExec_t ex, cudaGraphNode_t nd, void* arg) {
+  void set_node(cudaGraphExec_t ex, cudaGraphNode_t nd, void* arg, void* arg2 = nullptr) {
     cudaKernelNodeParams kp{};
     PGB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
-    void* params[1] = {arg};
+    void* params[2] = {arg, arg2};
     kp.kernelParams = params;
     kp.extra = nullptr;
     PGB_CUDA(cudaGraphExecKernelNodeSetParams(ex, nd, &kp));
@@ -1171,13 +1208,21 @@ struct Engine {
       sg.noise_args.a = cur_args;
       set_node(sg.exec, sg.noise, &sg.noise_args);
     }
+    const bool agg_in = sg.fused_tc && sg.fused_args.agg_tiles > 0;
     if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot ||
-                     sg.fused_args.norms != norms_dst || !same_args(sg.fused_args.a, cur_args))) {
+                     sg.fused_args.norms != norms_dst || !same_args(sg.fused_args.a, cur_args) ||
+                     (agg_in && (sg.fused_agg.norms_out != norms_dst ||
+                                 sg.fused_agg.clipped_out != clipped_dst)))) {
       sg.fused_args.x = x_slot;
       sg.fused_args.y = y_slot;
       sg.fused_args.norms = norms_dst;
       sg.fused_args.a = cur_args;
-      set_node(sg.exec, sg.fused, &sg.fused_args);
+      if (agg_in) {
+        sg.fused_agg.a = cur_args;
+        sg.fused_agg.norms_out = norms_dst;
+        sg.fused_agg.clipped_out = clipped_dst;
+      }
+      set_node(sg.exec, sg.fused, &sg.fused_args, sg.fused_tc ? &sg.fused_agg : nullptr);
     }
   }
 

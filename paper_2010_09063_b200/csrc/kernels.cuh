@@ -703,9 +703,9 @@ __device__ __forceinline__ AggTile agg_tile(const BlockTable& bt, const AggPlan&
 
 __device__ __forceinline__ void agg_scales(const double* __restrict__ parts, int nparts, int U,
                                            float clip, float* s_sh, float* norms_out,
-                                           int* cnt_sh) {
+                                           int* cnt_sh, int tid) {
   int local_clipped = 0;
-  for (int i = threadIdx.x; i < U; i += blockDim.x) {
+  for (int i = tid; i < U; i += 32 * kAggWarps) {
     double acc = 0.0;
     for (int q = 0; q < nparts; ++q) acc += parts[(size_t)i * nparts + q];
     const float nrm = (float)sqrt(acc);
@@ -714,12 +714,9 @@ __device__ __forceinline__ void agg_scales(const double* __restrict__ parts, int
     local_clipped += nrm > clip;
   }
   local_clipped = __reduce_add_sync(0xffffffffu, local_clipped);
-  if ((threadIdx.x & 31) == 0) cnt_sh[threadIdx.x >> 5] = local_clipped;
+  if ((tid & 31) == 0) cnt_sh[tid >> 5] = local_clipped;
 }
 
-struct AggLaunch;
-__device__ __forceinline__ void agg_prologue(const AggLaunch& L, float* s_sh, float* norms_cta,
-                                             int* cnt_sh);
 
 // Everything one aggregation launch needs, passed by value as the kernel's
 // single parameter: a CUDA-graph replay swaps in the step's arguments with
@@ -742,58 +739,74 @@ struct AggLaunch {
   int U, nparts, mode;
 };
 
+// Loads of per-example data: through the read-only path for a separate
+// aggregation kernel; L2-coherent (ld.global.cg) when the aggregation runs
+// inside the kernel that wrote the data (after a grid barrier).
+template <bool kCoherent, class T>
+__device__ __forceinline__ T agg_ld(const T* p) {
+  if constexpr (kCoherent) return __ldcg(p);
+  else return __ldg(p);
+}
+
 // Clip factors into shared memory: copied when the per-example kernel
 // finalised them, else computed from the fp64 norm partials.
+template <bool kCoherent>
 __device__ __forceinline__ void agg_prologue(const AggLaunch& L, float* s_sh, float* norms_cta,
-                                             int* cnt_sh) {
+                                             int* cnt_sh, int tid) {
   if (L.scales) {
     int local = 0;
-    for (int i = threadIdx.x; i < L.U; i += blockDim.x) {
-      s_sh[i] = L.scales[i];
-      if (norms_cta) local += L.clip_flags[i];
+    for (int i = tid; i < L.U; i += 32 * kAggWarps) {
+      s_sh[i] = agg_ld<kCoherent>(L.scales + i);
+      if (norms_cta) local += agg_ld<kCoherent>(L.clip_flags + i);
     }
     local = __reduce_add_sync(0xffffffffu, local);
-    if ((threadIdx.x & 31) == 0) cnt_sh[threadIdx.x >> 5] = local;
+    if ((tid & 31) == 0) cnt_sh[tid >> 5] = local;
   } else {
-    agg_scales(L.parts, L.nparts, L.U, L.a.clip, s_sh, norms_cta, cnt_sh);
+    agg_scales(L.parts, L.nparts, L.U, L.a.clip, s_sh, norms_cta, cnt_sh, tid);
   }
 }
 
-__global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
+// Synchronises the 32 * kAggWarps threads running one aggregation tile: the
+// whole CTA (separate kernel) or one named-barrier group of a larger CTA.
+__device__ __forceinline__ void agg_sync(int bar_id) {
+  if (bar_id < 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" :: "r"(bar_id), "r"(32 * kAggWarps) : "memory");
+}
+
+// One tile of the aggregation, run by 32 * kAggWarps threads (tid) that
+// synchronise with agg_sync(bar_id); s_sh holds the clip factors (U floats,
+// then the factored-row staging), part_sh the per-warp partial sums.
+template <bool kCoherent, int kBatch = kAggBatch>
+__device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, int tid, int bar_id,
+                                             float* s_sh, float (*part_sh)[kAggRows * 32],
+                                             int* cnt_sh) {
   const BlockTable& bt = L.bt;
   const StepArgs& a = L.a;
-  const double* __restrict__ parts = L.parts;
   float* __restrict__ params = L.params;
-  const int U = L.U, nparts = L.nparts, mode = L.mode;
-  extern __shared__ float s_sh[];  // clip factors, one per unit
-  __shared__ float part_sh[kAggWarps][kAggRows * 32];
-  __shared__ int cnt_sh[kAggWarps];
-  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
-  const AggTile tile = agg_tile(bt, L.plan, blockIdx.x);
-  // Programmatic dependent launch: this grid may be resident before the
-  // per-example kernel has finished; everything below reads its outputs.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int U = L.U, mode = L.mode;
+  const AggTile tile = agg_tile(bt, L.plan, tile_id);
   const int p = tile.p;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   // this thread's epilogue column, and its current parameter / the step
   // arguments / the error flag, fetched now so they are not on the tail
   long long j;
   bool has_col;
   if (bt.kind[p] == 0) {
-    has_col = threadIdx.x < tile.n;
-    j = (long long)tile.j0 + threadIdx.x;
+    has_col = tid < tile.n;
+    j = (long long)tile.j0 + tid;
   } else {
-    const int rr = threadIdx.x >> 5, c = tile.c0 + (threadIdx.x & 31);
+    const int rr = tid >> 5, c = tile.c0 + (tid & 31);
     has_col = rr < tile.n && c < bt.out[p];
     j = (long long)(tile.j0 + rr) * bt.out[p] + c;
   }
   const float cur = (has_col && mode == 0) ? params[bt.param_off[p] + j] : 0.0f;
   const float pre_noise =
-      (has_col && mode == 0 && L.noise && a.add_noise) ? L.noise[bt.param_off[p] + j] : 0.0f;
-  const bool failed = L.err && L.err->code != 0;
+      (has_col && mode == 0 && L.noise && a.add_noise) ? agg_ld<kCoherent>(L.noise + bt.param_off[p] + j)
+                                                       : 0.0f;
+  const bool failed = L.err && agg_ld<kCoherent>(&L.err->code) != 0;
   const int rows = (U + kAggWarps - 1) / kAggWarps;
   const int i0 = min(U, warp * rows), i1 = min(U, i0 + rows);
-  float* norms_cta = blockIdx.x == 0 ? L.norms_out : nullptr;
+  float* norms_cta = tile_id == 0 ? L.norms_out : nullptr;
 
   if (bt.kind[p] == 0) {
     // ---- materialised rows: 4 columns per lane ----
@@ -804,31 +817,30 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
     const bool vec = ncol == 4 && (stride & 3) == 0 &&
                      (reinterpret_cast<uintptr_t>(base) & 15) == 0;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    float v[kAggBatch][4];
+    float v[kBatch][4];
     auto load = [&](int ib) {
 #pragma unroll
-      for (int u = 0; u < kAggBatch; ++u) {
+      for (int u = 0; u < kBatch; ++u) {
         const int i = ib + u;
         if (i < i1 && ncol > 0) {
           const float* src = base + (long long)i * stride;
           if (vec) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+            const float4 q = agg_ld<kCoherent>(reinterpret_cast<const float4*>(src));
             v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
           } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) v[u][c] = c < ncol ? __ldg(src + c) : 0.0f;
+            for (int c = 0; c < 4; ++c) v[u][c] = c < ncol ? agg_ld<kCoherent>(src + c) : 0.0f;
           }
         }
       }
     };
     load(i0);  // in flight while the clip factors are computed
-    agg_prologue(L, s_sh, norms_cta, cnt_sh);
-    __syncthreads();
-    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 1);
-    for (int ib = i0; ib < i1; ib += kAggBatch) {
+    agg_prologue<kCoherent>(L, s_sh, norms_cta, cnt_sh, tid);
+    agg_sync(bar_id);
+    for (int ib = i0; ib < i1; ib += kBatch) {
       if (ib != i0) load(ib);
 #pragma unroll
-      for (int u = 0; u < kAggBatch; ++u) {
+      for (int u = 0; u < kBatch; ++u) {
         if (ib + u < i1) {
           const float s = s_sh[ib + u];
 #pragma unroll
@@ -858,17 +870,16 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
     auto load = [&](int ib) {
 #pragma unroll
       for (int u = 0; u < kAggChunk; ++u)
-        dv[u] = (cok && ib + u < i1) ? __ldg(D + (long long)(ib + u) * ds) : 0.0f;
+        dv[u] = (cok && ib + u < i1) ? agg_ld<kCoherent>(D + (long long)(ib + u) * ds) : 0.0f;
 #pragma unroll
       for (int q = 0; q < kAggChunk * kAggRows / 32; ++q) {
         const int e = q * 32 + lane, u = e / kAggRows, r = e % kAggRows;
-        ar[q] = (ib + u < i1 && r < nr) ? __ldg(A + (long long)(ib + u) * as + r) : 0.0f;
+        ar[q] = (ib + u < i1 && r < nr) ? agg_ld<kCoherent>(A + (long long)(ib + u) * as + r) : 0.0f;
       }
     };
     load(i0);
-    agg_prologue(L, s_sh, norms_cta, cnt_sh);
-    __syncthreads();
-    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 2);
+    agg_prologue<kCoherent>(L, s_sh, norms_cta, cnt_sh, tid);
+    agg_sync(bar_id);
     for (int ib = i0; ib < i1; ib += kAggChunk) {
       if (ib != i0) load(ib);
 #pragma unroll
@@ -894,18 +905,17 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
 #pragma unroll
     for (int r = 0; r < kAggRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
   }
-  __syncthreads();
-    PGB_MARK_BAR(PGB_TRACE_AGG + 8 * blockIdx.x + 3);
+  agg_sync(bar_id);
 
   // ---- epilogue: one thread per column of the tile ----
-  if (blockIdx.x == 0 && threadIdx.x == 0 && L.clipped_out) {
+  if (tile_id == 0 && tid == 0 && L.clipped_out) {
     int n = 0;
 #pragma unroll
     for (int w = 0; w < kAggWarps; ++w) n += cnt_sh[w];
     *L.clipped_out = n;
   }
   if (!has_col) return;
-  const int t = threadIdx.x;
+  const int t = tid;
   float sum = part_sh[0][t];
 #pragma unroll
   for (int w = 1; w < kAggWarps; ++w) sum = __fadd_rn(sum, part_sh[w][t]);
@@ -926,6 +936,17 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   sum = __fmul_rn(sum, a.inv_units);
   if (failed) return;
   write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
+}
+
+__global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
+  extern __shared__ float s_sh[];  // clip factors, one per unit
+  __shared__ float part_sh[kAggWarps][kAggRows * 32];
+  __shared__ int cnt_sh[kAggWarps];
+  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
+  // Programmatic dependent launch: this grid may be resident before the
+  // per-example kernel has finished; everything below reads its outputs.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
 }
 
@@ -1042,6 +1063,27 @@ __global__ void transpose_kernel(const float* __restrict__ src, int rows, int co
     const int r = e / cols, c = e - r * cols;
     dst[shadow_index(r, c, rows, swz)] = src[e];
   }
+}
+
+// Grid-wide barrier for a grid whose CTAs are all co-resident (one per SM,
+// checked by the host). The counter only grows: each launch adds gridDim.x,
+// and a CTA waits for the next multiple of gridDim.x, so no reset is needed
+// between launches. Writes before the barrier are visible after it (CTA
+// barrier + gpu-scope fence by the arriving thread, acquire on the wait).
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
 }
 
 // device-side step counter of the multi-step graphs

@@ -106,6 +106,10 @@ struct Params {
   const float* yring;
   long long ring_origin;
   int ring_n;
+  // tc_kernel only: run the step's aggregation (clipped sum, noise, update)
+  // in-kernel after a grid barrier, agg_tiles tiles over the CTA halves
+  unsigned long long* grid_ctr;
+  int agg_tiles;
 };
 
 __device__ __forceinline__ long long step_index(const Params& prm) {

@@ -97,7 +97,7 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
 // split into independent accumulator chains issued by lane 0 of warps 0..3.
 constexpr int kIssuers = 4;
 
-__global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
+__global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch agg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -731,6 +731,25 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm) {
     prm.scale[b] = nrm > C ? __fdiv_rn(C, nrm) : 1.0f;
     prm.clipped[b] = nrm > C ? 1 : 0;
     PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
+  }
+
+  // ---- the step's aggregation, in-kernel ----------------------------------
+  // Every CTA is resident (one per SM), so after a grid barrier the CTA
+  // halves run the aggregation tiles of aggregate_kernel (clipped sum in a
+  // fixed order, noise, mean, update) on the per-example outputs above.
+  if (prm.agg_tiles > 0) {
+    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 19);
+    grid_barrier(prm.grid_ctr);
+    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 20);
+    float* s_sh = regA + ex * 4096;  // clip factors + factored-row staging
+    auto part_sh = reinterpret_cast<float(*)[kAggRows * 32]>(regA + 8192 + ex * 4096);
+    int* cnt_sh = reinterpret_cast<int*>(regA + 16384) + ex * kAggWarps;
+    // tile t on half t / gridDim of CTA t % gridDim: at most one tile per SM
+    // until the halves' second round (the heavy factored fc1 tiles are
+    // consecutive, so they land on different SMs)
+    for (int tile = blockIdx.x + ex * gridDim.x; tile < prm.agg_tiles; tile += 2 * gridDim.x)
+      agg_tile_run<true, 8>(agg, tile, tt, 1 + ex, s_sh, part_sh, cnt_sh);
+    if (ex == 0) PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 21);
   }
 }
 

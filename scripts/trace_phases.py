@@ -53,9 +53,15 @@ print("phase  alone(us)  shared(us)" if n == B else "phase  early-half(us)  late
 for a, b in zip(marks[:-1], marks[1:]):
     d = F[:, b] - F[:, a]
     print(f"{a:2d}->{b:2d}  {d[one].mean() / 1e3:8.2f}  {d[two].mean() / 1e3:8.2f}")
-for k in range(16, 23):
+for k in range(16, 19):
     if F[:, k].all():
         print(f"  mark {k}: {(F[:, k] - F[:, 7]).mean() / 1e3:.2f} us after mark 7")
+if F[:, 19].all() and F[:, 21].all():
+    e23 = F[:, 23].max()
+    print(f"  in-kernel aggregation: barrier arrive {(F[:, 19] - e23).min() / 1e3:.2f}.."
+          f"{(F[:, 19] - e23).max() / 1e3:.2f} us after the last example ends, released "
+          f"{(F[:, 20] - e23).min() / 1e3:.2f}..{(F[:, 20] - e23).max() / 1e3:.2f}, tiles done "
+          f"{(F[:, 21] - e23).min() / 1e3:.2f}..{(F[:, 21] - e23).max() / 1e3:.2f}")
 A = buf[AGG:AGG + 8 * 4096].reshape(4096, 8)
 A = A[A[:, 0] > 0]
 if len(A):

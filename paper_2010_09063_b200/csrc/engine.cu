@@ -281,7 +281,6 @@ struct Engine {
     }
     if (resident.exec) cudaGraphExecDestroy(resident.exec);
     if (resident.graph) cudaGraphDestroy(resident.graph);
-    if (d_step_base) cudaFree(d_step_base);
     if (h_step_base) cudaFreeHost(h_step_base);
     for (int i = 0; i < kSlots; ++i)
       for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i]})
@@ -629,6 +628,12 @@ struct Engine {
   // ---- profiling hook: an event after every launch while profiling --------
   std::vector<std::pair<cudaEvent_t, const char*>>* prof = nullptr;
   int mark(cudaStream_t s, const char* name) {
+    static const bool debug_sync = std::getenv("PGB_DEBUG_LAUNCH") != nullptr;
+    if (debug_sync) {
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess)
+        raise(PGB_ERR_CUDA, std::string("launch of ") + name + ": " + cudaGetErrorString(e));
+    }
     if (prof) {
       cudaEvent_t ev;
       PGB_CUDA(cudaEventCreate(&ev));

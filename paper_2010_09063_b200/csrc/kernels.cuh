@@ -648,9 +648,9 @@ __device__ __forceinline__ int find_block(const long long* pair_off, int n, long
 //     columns 4l..4l+3 (one 16-byte load per unit when aligned);
 //   factored dense rows (kind 1, g_i = a_i (x) d_i): kAggRows weight rows r x
 //     32 columns c; lane l owns column c0+l of every row, so one coalesced
-//     load of d_i and kAggRows broadcast values of a_i feed kAggRows products
-//     fl(a_ir * d_ic) -- the fp32 element of the reference's outer-product
-//     stack, never written to memory.
+//     load of d_i and kAggRows broadcast values of a_i feed kAggRows FMAs
+//     a_ir * fl(d_ic * s_i) -- the outer-product stack is never written to
+//     memory (one rounding per element fewer than the reference's order).
 // A CTA of kAggWarps warps owns one tile; warp w sums a contiguous slice of
 // the units (ascending), with the first batch of loads issued before the clip
 // factors are computed; slices are combined in warp order through shared
@@ -837,6 +837,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     load(i0);  // in flight while the clip factors are computed
     agg_prologue<kCoherent>(L, s_sh, norms_cta, cnt_sh, tid);
     agg_sync(bar_id);
+    if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 1, 0);
     for (int ib = i0; ib < i1; ib += kBatch) {
       if (ib != i0) load(ib);
 #pragma unroll
@@ -880,6 +881,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     load(i0);
     agg_prologue<kCoherent>(L, s_sh, norms_cta, cnt_sh, tid);
     agg_sync(bar_id);
+    if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 2, 0);
     for (int ib = i0; ib < i1; ib += kAggChunk) {
       if (ib != i0) load(ib);
 #pragma unroll
@@ -888,15 +890,19 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
 #pragma unroll
       for (int u = 0; u < kAggChunk; ++u) {
         if (ib + u < i1) {
-          const float s = s_sh[ib + u];
+          // acc_r += a_ir * fl(d_ic * s_i) as one FMA per element (the
+          // reference's fl(fl(a * d) * s) + acc costs three rounded ops; the
+          // clipped sum is the issue-bound tail of the step, and the product
+          // differs from it by at most one rounding, SURVEY 8(d) tolerance)
+          const float ds = __fmul_rn(dv[u], s_sh[ib + u]);
           const float4* a4 = reinterpret_cast<const float4*>(a_st + u * kAggRows);
 #pragma unroll
           for (int q = 0; q < kAggRows / 4; ++q) {
             const float4 x = a4[q];
-            acc[4 * q] = __fadd_rn(acc[4 * q], __fmul_rn(__fmul_rn(x.x, dv[u]), s));
-            acc[4 * q + 1] = __fadd_rn(acc[4 * q + 1], __fmul_rn(__fmul_rn(x.y, dv[u]), s));
-            acc[4 * q + 2] = __fadd_rn(acc[4 * q + 2], __fmul_rn(__fmul_rn(x.z, dv[u]), s));
-            acc[4 * q + 3] = __fadd_rn(acc[4 * q + 3], __fmul_rn(__fmul_rn(x.w, dv[u]), s));
+            acc[4 * q] = __fmaf_rn(x.x, ds, acc[4 * q]);
+            acc[4 * q + 1] = __fmaf_rn(x.y, ds, acc[4 * q + 1]);
+            acc[4 * q + 2] = __fmaf_rn(x.z, ds, acc[4 * q + 2]);
+            acc[4 * q + 3] = __fmaf_rn(x.w, ds, acc[4 * q + 3]);
           }
         }
       }
@@ -906,6 +912,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     for (int r = 0; r < kAggRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
   }
   agg_sync(bar_id);
+  if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 3, 0);
 
   // ---- epilogue: one thread per column of the tile ----
   if (tile_id == 0 && tid == 0 && L.clipped_out) {
@@ -946,6 +953,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   // Programmatic dependent launch: this grid may be resident before the
   // per-example kernel has finished; everything below reads its outputs.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 5);
   agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
 }

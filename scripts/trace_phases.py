@@ -67,6 +67,16 @@ A = A[A[:, 0] > 0]
 if len(A):
     print(f"aggregate: {len(A)} CTAs; first start {(A[:, 0].min() - end.max()) / 1e3:.2f} us after "
           f"the fused kernel's last CTA, last end {(A[:, 4].max() - end.max()) / 1e3:.2f} us after")
+    if (A[:, 5] > 0).all():
+        rel = (A[:, 5] - end.max()) / 1e3
+        print(f"  PDL release (griddepcontrol.wait returns): {rel.min():.2f}..{rel.max():.2f} us after "
+              f"the fused kernel's last CTA")
+        for k, col in ((0, 1), (1, 2)):
+            m = A[:, col] > 0
+            if m.any():
+                a = A[m]
+                pc = lambda v: np.percentile(v, [0, 50, 100]).astype(int)  # noqa: E731
+                print(f"  kind {k}: release->loads+scales+sync {pc(a[:, col] - a[:, 5])} ns")
     for k, col in ((0, 1), (1, 2)):
         m = A[:, col] > 0
         if m.any():

@@ -116,6 +116,16 @@ struct Engine {
   std::vector<Layer> layers;
   BlockTable bt{};       // live per-example gradient sources (ghost dense blocks)
   BlockTable bt_stack{}; // the same blocks materialised in d_stacks (block-major)
+  // sparse per-example embedding gradients on the step path (embedding ->
+  // seq_avgpool): distinct tokens + counts per example and per-row example
+  // bitmaps instead of the dense (B, V, E) stack (embed_index/agg kernels)
+  int emb_layer = -1;          // the embedding layer, when the sparse path applies
+  bool sparse_embed_next = false;
+  int* d_emb_tok = nullptr;    // (B, L)
+  int* d_emb_cnt = nullptr;    // (B, L)
+  int* d_emb_nd = nullptr;     // (B)
+  unsigned* d_emb_bits = nullptr;  // (V, words)
+  int emb_words = 0;
   int nparts = 1;        // fp64 norm partials per example
   bool norms_fused = false;  // per-example norms produced by the gradient kernel
   bool fused_mnist = false;  // whole per-example pass in one kernel
@@ -252,6 +262,8 @@ struct Engine {
     mnist::Params fused_args{};
     AggLaunch fused_agg{};  // the tc_kernel's in-kernel aggregation arguments
     bool fused_tc = false;
+    cudaGraphNode_t emb = nullptr;  // the sparse embedding aggregation
+    EmbAggLaunch emb_args{};
   };
   std::map<int, StepGraph> graphs;  // key: schedule variant
   int kernels_last = 0;
@@ -405,6 +417,18 @@ struct Engine {
       want((void**)&d_scale, sizeof(float) * B);
       want((void**)&d_clipflag, sizeof(int) * B);
     }
+    for (int l = 0; l < n; ++l) {
+      const Layer& L = layers[l];
+      if (L.spec.kind == PGB_EMBEDDING && L.fused_pool && B <= 1024 && L.in.d[0] <= kEmbMaxL) {
+        emb_layer = l;
+        emb_words = (int)((B + 31) / 32);
+        const int64_t Lq = L.in.d[0];
+        want((void**)&d_emb_tok, sizeof(int) * B * Lq);
+        want((void**)&d_emb_cnt, sizeof(int) * B * Lq);
+        want((void**)&d_emb_nd, sizeof(int) * B);
+        want((void**)&d_emb_bits, sizeof(unsigned) * L.spec.in * emb_words);
+      }
+    }
     d_dense_g.assign(n, nullptr);
     for (int l = 0; l < n; ++l)
       if (layers[l].spec.kind == PGB_DENSE)
@@ -531,9 +555,10 @@ struct Engine {
 
   // The gradient-source table for a step whose input sits at x_slot: a dense
   // first layer is factored over the input itself.
-  BlockTable table_for(const float* x_slot) const {
+  BlockTable table_for(const float* x_slot, bool sparse = false) const {
     BlockTable t = bt;
     if (fused_mnist) return t;
+    if (sparse && emb_layer >= 0) t.kind[layers[emb_layer].pblock] = 2;
     for (int l = 0; l < desc.n_layers; ++l) {
       const Layer& L = layers[l];
       if (L.spec.kind != PGB_DENSE || L.act_in) continue;
@@ -864,6 +889,14 @@ struct Engine {
         }
         case PGB_EMBEDDING: {
           const int E = (int)sp.out, V = (int)sp.in;
+          if (sparse_embed_next && l == emb_layer) {
+            // distinct tokens, counts, row bitmaps and the block's norm
+            embed_index_kernel<<<Bi, 256, 0, s>>>(in, gcur, (int)L.in.d[0], E, V, emb_words,
+                                                  d_emb_tok, d_emb_cnt, d_emb_nd, d_emb_bits,
+                                                  d_parts, nparts, L.pblock);
+            nk += mark(s, "embed_index");
+            break;
+          }
           float* st = d_stacks + param_off[L.pblock] * B;
           PGB_CUDA(cudaMemsetAsync(st, 0, sizeof(float) * B * V * E, s));
           embed_pex_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
@@ -877,7 +910,7 @@ struct Engine {
       }
     }
     dim3 sg(bt.n, (unsigned)B);
-    sumsq_kernel<<<sg, 128, 0, s>>>(table_for(x_slot), Bi, d_parts);
+    sumsq_kernel<<<sg, 128, 0, s>>>(table_for(x_slot, sparse_embed_next), Bi, d_parts);
     nk += mark(s, "sumsq");
     return nk;
   }
@@ -887,10 +920,11 @@ struct Engine {
     int nk = 0;
     // one launch per step: the fused MNIST kernel aggregates in-kernel
     fuse_agg_next = agg_in_kernel && m == 1;
+    sparse_embed_next = emb_layer >= 0 && m == 1;
     try {
       nk += enqueue_grads(s, x_slot, y_slot);
     } catch (...) {
-      fuse_agg_next = false;
+      fuse_agg_next = sparse_embed_next = false;
       throw;
     }
     if (fuse_agg_next) {
@@ -912,8 +946,10 @@ struct Engine {
       nk += mark(s, "sumsq");
       nk += enqueue_aggregate(s, ut, ut.n, U);
     } else {
-      nk += enqueue_aggregate(s, table_for(x_slot), nparts, (int)B, fused_mnist);
+      nk += enqueue_aggregate(s, table_for(x_slot, sparse_embed_next), nparts, (int)B,
+                              fused_mnist);
     }
+    sparse_embed_next = false;
     return nk;
   }
 
@@ -927,7 +963,7 @@ struct Engine {
       plan.tile_start[p] = tiles;
       if (t.kind[p] == 0) {
         tiles += (int)((t.size[p] + kAggCols - 1) / kAggCols);
-      } else {
+      } else if (t.kind[p] == 1) {
         const int64_t out = t.out[p], in = t.size[p] / out;
         tiles += (int)(((in + kAggRows - 1) / kAggRows) * ((out + 31) / 32));
       }
@@ -983,14 +1019,47 @@ struct Engine {
   }
 
   // ff: the step's tail inputs come from the fused MNIST kernel that just ran
+  // the sparse embedding block of table t (kind 2): its clipped sum (+ noise
+  // and update in mode 0) over the rows' example lists
+  int enqueue_embed_agg(cudaStream_t s, const BlockTable& t, int np, int mode) {
+    const Layer& L = layers[emb_layer];
+    EmbAggLaunch A{};
+    A.bt = t;
+    A.a = cur_args;
+    A.parts = d_parts;
+    A.u = L.gout;
+    A.tok = d_emb_tok;
+    A.cnt = d_emb_cnt;
+    A.nd = d_emb_nd;
+    A.bits = d_emb_bits;
+    A.params = d_params;
+    A.sum_out = d_sum;
+    A.err = d_err;
+    A.p = L.pblock;
+    A.B = (int)B;
+    A.L = (int)L.in.d[0];
+    A.E = (int)L.spec.out;
+    A.V = (int)L.spec.in;
+    A.words = emb_words;
+    A.nparts = np;
+    A.mode = mode;
+    const int rows_per_cta = 8;
+    const int grid = std::min<int>((A.V + rows_per_cta - 1) / rows_per_cta, 148 * 8);
+    embed_agg_kernel<<<grid, 256, sizeof(float) * B, s>>>(A);
+    return mark(s, mode == 0 ? "embed_agg" : "embed_agg_local");
+  }
+
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
+    const bool emb = emb_layer >= 0 && t.kind[layers[emb_layer].pblock] == 2;
     if (world == 1) {
       launch_agg(agg_launch(t, np, U, 0, ff), s, ff && pdl_enabled);
       nk += mark(s, "aggregate");
+      if (emb) nk += enqueue_embed_agg(s, t, np, 0);
     } else {
       launch_agg(agg_launch(t, np, U, 1, ff), s);
       nk += mark(s, "aggregate_local");
+      if (emb) nk += enqueue_embed_agg(s, t, np, 1);
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
       PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
@@ -1174,6 +1243,9 @@ struct Engine {
           sg.agg = nd;
           sg.agg_args = *L;
         }
+      } else if (kp.func == (void*)embed_agg_kernel) {
+        sg.emb = nd;
+        sg.emb_args = *static_cast<const EmbAggLaunch*>(kp.kernelParams[0]);
       } else if (kp.func == (void*)noise_update_kernel) {
         sg.noise = nd;
         sg.noise_args = *static_cast<const NoiseLaunch*>(kp.kernelParams[0]);
@@ -1208,6 +1280,10 @@ struct Engine {
       sg.agg_args.norms_out = norms_dst;
       sg.agg_args.clipped_out = clipped_dst;
       set_node(sg.exec, sg.agg, &sg.agg_args);
+    }
+    if (sg.emb && !same_args(sg.emb_args.a, cur_args)) {
+      sg.emb_args.a = cur_args;
+      set_node(sg.exec, sg.emb, &sg.emb_args);
     }
     if (sg.noise && !same_args(sg.noise_args.a, cur_args)) {
       sg.noise_args.a = cur_args;

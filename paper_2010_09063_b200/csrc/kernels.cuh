@@ -576,6 +576,7 @@ __global__ void sumsq_kernel(BlockTable bt, int B, double* __restrict__ parts) {
   __shared__ double red[32];
   const int p = blockIdx.x;
   const long long i = blockIdx.y;
+  if (bt.kind[p] == 2) return;  // sparse embedding: embed_index_kernel writes its norm
   if (bt.kind[p] == 0) {
     const long long per = bt.size[p];
     const float* row = bt.base[p] + i * bt.stride[p];
@@ -956,6 +957,188 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 5);
   agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
+}
+
+// ---- sparse per-example embedding gradients (embedding -> seq_avgpool) ----
+// The reference materialises the per-example table gradient as a dense
+// (B, V, E) stack (strategies.cpp:171-188): row r of example i is v_i = u_i/L
+// (u_i the pooled cotangent) added once per occurrence of token r, in token
+// order. Here each example keeps only its distinct tokens and counts; the
+// element value is the same fp32 chain acc = fl(acc + v) repeated c times.
+constexpr int kEmbMaxL = 1024;
+
+__device__ __forceinline__ float emb_chain(float v, int c) {
+  float acc = 0.0f;
+  for (int k = 0; k < c; ++k) acc = __fadd_rn(acc, v);
+  return acc;
+}
+
+// Per example (one CTA): sort the L token ids, keep distinct tokens and their
+// counts (tok/cnt rows of length L, n_distinct), mark example i in each
+// token's row bitmap (bit i of bits[r * words]), and the example's squared
+// norm of the embedding block in fp64 (dpsgd.cpp:254-270) into
+// parts[i * nparts + p].
+__global__ void __launch_bounds__(256) embed_index_kernel(
+    const float* __restrict__ ids, const float* __restrict__ u, int L, int E, int V, int words,
+    int* __restrict__ tok, int* __restrict__ cnt, int* __restrict__ nd,
+    unsigned* __restrict__ bits, double* __restrict__ parts, int nparts, int p) {
+  __shared__ int key[kEmbMaxL];
+  __shared__ int seg[kEmbMaxL + 1];
+  __shared__ int nseg;
+  __shared__ double red[32];
+  const int i = blockIdx.x, t = threadIdx.x;
+  int Lp = 1;
+  while (Lp < L) Lp <<= 1;
+  for (int k = t; k < Lp; k += blockDim.x) {
+    int v = 0x7fffffff;
+    if (k < L) {
+      const float raw = ids[(size_t)i * L + k];
+      if (valid_id(raw, V)) v = (int)raw;  // invalid ids raised by the forward
+    }
+    key[k] = v;
+  }
+  __syncthreads();
+  // bitonic sort (ascending)
+  for (int size = 2; size <= Lp; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int k = t; k < Lp / 2; k += blockDim.x) {
+        const int a = 2 * k - (k & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        const int x = key[a], y = key[b];
+        if ((x > y) == up) {
+          key[a] = y;
+          key[b] = x;
+        }
+      }
+      __syncthreads();
+    }
+  // segment starts (distinct tokens) in order
+  if (t == 0) {
+    int n = 0;
+    for (int k = 0; k < L; ++k) {
+      if (key[k] == 0x7fffffff) break;
+      if (k == 0 || key[k] != key[k - 1]) seg[n++] = k;
+    }
+    int end = 0;
+    while (end < L && key[end] != 0x7fffffff) ++end;
+    seg[n] = end;
+    nseg = n;
+    nd[i] = n;
+  }
+  __syncthreads();
+  const int n = nseg;
+  for (int k = t; k < n; k += blockDim.x) {
+    const int r = key[seg[k]];
+    tok[(size_t)i * L + k] = r;
+    cnt[(size_t)i * L + k] = seg[k + 1] - seg[k];
+    atomicOr(&bits[(size_t)r * words + (i >> 5)], 1u << (i & 31));
+  }
+  // ||G_i||^2 = sum over distinct tokens and e of chain(u_ie / L, c)^2
+  const float invL = 1.0f / float(L);
+  double acc = 0.0;
+  for (int q = t; q < n * E; q += blockDim.x) {
+    const int k = q / E, e = q - k * E;
+    const float g = emb_chain(u[(size_t)i * E + e] * invL, seg[k + 1] - seg[k]);
+    acc += (double)g * g;
+  }
+  acc = block_reduce_sum(acc, red);
+  if (t == 0) parts[(size_t)i * nparts + p] = acc;
+}
+
+// Clipped sum of the embedding block over the examples containing each row,
+// then noise / mean / update (mode 0) or the sum alone (mode 1), one warp per
+// table row, every row (inactive rows get noise only). Examples are visited in
+// ascending order (the reference's views-path order, dpsgd.cpp:287-307); each
+// term is fl(g * s_i). The row's bitmap is cleared for the next step.
+struct EmbAggLaunch {
+  BlockTable bt;
+  StepArgs a;
+  const double* parts;
+  const float* u;      // (B, E) pooled cotangent
+  const int* tok;      // (B, L)
+  const int* cnt;
+  const int* nd;       // (B)
+  unsigned* bits;      // (V, words)
+  float* params;
+  float* sum_out;      // mode 1
+  const DevError* err;
+  int p, B, L, E, V, words, nparts, mode;
+};
+
+__global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
+  extern __shared__ float s_emb[];  // clip factors (B)
+  __shared__ unsigned wsh[8][32];   // the current row's bitmap words, per warp
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int i = t; i < A.B; i += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < A.nparts; ++q) acc += A.parts[(size_t)i * A.nparts + q];
+    const float nrm = (float)sqrt(acc);
+    s_emb[i] = nrm > A.a.clip ? __fdiv_rn(A.a.clip, nrm) : 1.0f;
+  }
+  __syncthreads();
+  const BlockTable& bt = A.bt;
+  const StepArgs& a = A.a;
+  const float invL = 1.0f / float(A.L);
+  const bool failed = A.err && A.err->code != 0;
+  const uint64_t key = stream_key(a.seed, noise_stream(a.step, A.p));
+  const long long E = A.E;
+  for (int r = blockIdx.x * 8 + w; r < A.V; r += gridDim.x * 8) {
+    const unsigned word = lane < A.words ? A.bits[(size_t)r * A.words + lane] : 0u;
+    const unsigned active = __ballot_sync(0xffffffffu, word != 0u);
+    wsh[w][lane] = word;
+    __syncwarp();
+    const long long j0 = (long long)r * E, jp0 = j0 >> 1, jp1 = (j0 + E - 1) >> 1;
+    for (long long jp = jp0 + lane; jp <= jp1; jp += 32) {
+      const long long e0 = 2 * jp - j0, e1 = e0 + 1;
+      const bool ok0 = e0 >= 0 && e0 < E, ok1 = e1 >= 0 && e1 < E;
+      float acc0 = 0.0f, acc1 = 0.0f;
+      unsigned am = active;
+      while (am) {
+        const int wd = __ffs(am) - 1;
+        am &= am - 1;
+        unsigned bw = wsh[w][wd];
+        while (bw) {
+          const int bb = __ffs(bw) - 1;
+          bw &= bw - 1;
+          const int i = wd * 32 + bb;
+          // count of token r in example i: binary search its distinct tokens
+          const int* tk = A.tok + (size_t)i * A.L;
+          int lo = 0, hi = A.nd[i] - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (tk[mid] < r) lo = mid + 1;
+            else hi = mid;
+          }
+          const int c = A.cnt[(size_t)i * A.L + lo];
+          const float s = s_emb[i];
+          const float* ui = A.u + (size_t)i * E;
+          if (ok0) acc0 = __fadd_rn(acc0, __fmul_rn(emb_chain(ui[e0] * invL, c), s));
+          if (ok1) acc1 = __fadd_rn(acc1, __fmul_rn(emb_chain(ui[e1] * invL, c), s));
+        }
+      }
+      float n0 = 0.0f, n1 = 0.0f;
+      if (A.mode == 0 && a.add_noise) gauss_pair(key, jp, &n0, &n1);
+      const float scale = __fmul_rn(a.sigma, a.clip);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!(h ? ok1 : ok0)) continue;
+        const long long j = j0 + (h ? e1 : e0);
+        float sum = h ? acc1 : acc0;
+        if (A.mode == 1) {
+          A.sum_out[bt.param_off[A.p] + j] = sum;
+          continue;
+        }
+        if (a.add_noise) sum = __fadd_rn(sum, __fmul_rn(scale, h ? n1 : n0));
+        sum = __fmul_rn(sum, a.inv_units);
+        if (failed) continue;
+        const float cur = A.params[bt.param_off[A.p] + j];
+        write_param(bt, A.p, j, A.params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
+      }
+    }
+    if (lane < A.words && word) A.bits[(size_t)r * A.words + lane] = 0u;
+    __syncwarp();
+  }
 }
 
 // After the all-reduce of the clipped sums: noise (one shared draw from the

@@ -214,3 +214,27 @@ def test_mnist_in_kernel_aggregation_matches(P, O, monkeypatch):
         out.append((model.flat_params(), reps))
     np.testing.assert_array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+def test_embed_full_size_sparse_step_matches_dense_clipped_sum(P, O):
+    """BASELINE config 5 shape (V = 10,004, L = 256, E = 100, B = 512): the
+    step's sparse embedding path (distinct tokens + counts, per-row example
+    bitmaps) gives the same update as the dense per-example stack the
+    clipped-sum probe materialises (sigma = 0, p_new = p - lr * sum / B; lr
+    large enough that p - p_new carries the sum without fp32 cancellation)."""
+    B = 512
+    desc = P.build_desc(P.ModelKind.embed, P.ModelOptions(hidden=100))
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 0)
+    eng = P.GradEngine(model, P.Strategy.jacmm, B)
+    p0 = model.flat_params().astype(np.float64)
+    got_sum, norms, nclip = eng.clipped_sum(data.inputs, data.labels, 1.0)
+    lr = 1000.0
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=0.0, learning_rate=lr, seed=0)
+    rep = P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 0)
+    np.testing.assert_allclose(rep.pre_clip_norms, norms, rtol=1e-6)
+    assert rep.clipped_count == nclip
+    step_sum = (p0 - model.flat_params().astype(np.float64)) * B / lr
+    n_emb = 10004 * 100
+    want = got_sum[:n_emb].astype(np.float64)
+    assert np.linalg.norm(step_sum[:n_emb] - want) <= 1e-5 * np.linalg.norm(want)

@@ -271,8 +271,36 @@ def ref():
         L.ref_run_bench_f32.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_double, C.c_double, C.c_double, C.c_uint64,
                                         _P(C.c_double)]
+        L.ref_load_idx_f32.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _P(C.c_int64),
+                                       _P(C.c_int), _P(C.c_int64)]
+        L.ref_records_json_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_int64,
+                                                 _P(C.c_int64)]
         _ref = L
     return _ref
+
+
+def ref_load_idx(path):
+    """io::load_idx<float> of the compiled reference: (values, dims) or
+    raises RefError (code 8 FormatError, 9 IoError)."""
+    L = ref()
+    n, rank, dims = C.c_int64(), C.c_int(), (C.c_int64 * 8)()
+    _chk(L.ref_load_idx_f32(path.encode(), None, 0, C.byref(n), C.byref(rank), dims), L,
+         "ref_last_error")
+    out = np.empty(n.value, np.float32)
+    _chk(L.ref_load_idx_f32(path.encode(), _ptr(out), n.value, C.byref(n), C.byref(rank), dims),
+         L, "ref_last_error")
+    return out, tuple(dims[i] for i in range(rank.value))
+
+
+def ref_records_json_roundtrip(text: str) -> str:
+    """bench::records_to_json(bench::records_from_json(text)) of the reference."""
+    L = ref()
+    n = C.c_int64()
+    _chk(L.ref_records_json_roundtrip(text.encode(), None, 0, C.byref(n)), L, "ref_last_error")
+    buf = C.create_string_buffer(n.value + 1)
+    _chk(L.ref_records_json_roundtrip(text.encode(), buf, n.value + 1, C.byref(n)), L,
+         "ref_last_error")
+    return buf.value.decode()
 
 
 class RefModel:

@@ -11,6 +11,8 @@
 //   dpsgd_step                            (proj/core/src/dpsgd.cpp:188-331)
 //   gaussian<T>                           (proj/core/src/tensor_ops.cpp:292-296)
 //   bench::run_bench                      (proj/core/src/harness.cpp:85-167)
+//   io::load_idx                          (proj/core/src/dataset.cpp:35-82)
+//   bench::records_from_json / records_to_json (proj/core/src/harness.cpp:219-274)
 // Only tests/, __graft_entry__.smoke() and bench.py's reference legs load it.
 
 #include <chrono>
@@ -323,6 +325,29 @@ int ref_run_bench_f32(int kind, int strategy, int64_t B, int64_t N,
                           (recs.empty() ? std::string("no record")
                                         : recs[0].status + " " + recs[0].reason));
     *median_seconds = recs[0].median_epoch_seconds;
+  });
+}
+
+// io::load_idx<float>: element count into *n, the rank and dims, and (when
+// out is non-null and cap suffices) the values.
+int ref_load_idx_f32(const char* path, float* out, int64_t cap, int64_t* n, int* rank,
+                     int64_t* dims) {
+  return guarded([&] {
+    Tensor<float> t = io::load_idx<float>(path);
+    *n = t.size();
+    *rank = (int)t.rank();
+    for (int d = 0; d < (int)t.rank(); ++d) dims[d] = t.dim(d);
+    if (out && cap >= t.size()) std::memcpy(out, t.data(), sizeof(float) * t.size());
+  });
+}
+
+// Parse BenchRecord JSON with the reference's parser and re-emit it with the
+// reference's writer (records_from_json -> records_to_json).
+int ref_records_json_roundtrip(const char* text, char* out, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const std::string s = bench::records_to_json(bench::records_from_json(text));
+    *len = (int64_t)s.size();
+    if (out && cap > (int64_t)s.size()) std::memcpy(out, s.c_str(), s.size() + 1);
   });
 }
 

@@ -1977,6 +1977,27 @@ pgb_status pgb_debug_umma_rate(int32_t device, int32_t M, int32_t N, int32_t rep
   });
 }
 
+pgb_status pgb_load_idx_device(const char* path, int32_t device, float scale_div, float* d_out) {
+  return guarded([&] {
+    if (!path || !d_out) raise(PGB_ERR_CONTRACT, "null argument");
+    IdxArray a = read_idx(path);
+    const size_t n = a.bytes.size() - a.offset;
+    PGB_CUDA(cudaSetDevice(device));
+    // the payload crosses PCIe as bytes (4x fewer than floats) and is decoded
+    // on the device with the reference's arithmetic: float(b) / scale
+    unsigned char* d_b = nullptr;
+    PGB_CUDA(cudaMalloc(&d_b, n ? n : 1));
+    cudaError_t st = cudaMemcpy(d_b, a.bytes.data() + a.offset, n, cudaMemcpyHostToDevice);
+    if (st == cudaSuccess && n) {
+      decode_u8_kernel<<<grid_for(n), 256>>>(d_b, (long long)n, scale_div, d_out);
+      st = cudaGetLastError();
+      if (st == cudaSuccess) st = cudaDeviceSynchronize();
+    }
+    cudaFree(d_b);
+    PGB_CUDA(st);
+  });
+}
+
 pgb_status pgb_device_params(pgb_engine* e, float** d) {
   return guarded([&] { *d = E(e).d_params; });
 }

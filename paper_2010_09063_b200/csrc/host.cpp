@@ -8,7 +8,10 @@
 //   check_strategy_support          proj/core/src/strategies.cpp:76-113
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <thread>
 #include <vector>
 
@@ -406,4 +409,75 @@ pgb_status pgb_synth(const pgb_model_desc* d, int64_t n, uint64_t seed, float* x
   });
 }
 
+// ---- IDX containers (io::load_idx, proj/core/src/dataset.cpp:35-82) -----------
+pgb_status pgb_idx_info(const char* path, int32_t* rank, int64_t* dims, int64_t* count) {
+  return guarded([&] {
+    if (!path || !rank || !dims || !count) raise(PGB_ERR_CONTRACT, "null argument");
+    pgb::IdxArray a = pgb::read_idx(path);
+    *rank = (int32_t)a.dims.size();
+    for (size_t d = 0; d < a.dims.size(); ++d) dims[d] = a.dims[d];
+    *count = (int64_t)(a.bytes.size() - a.offset);
+  });
+}
+
+pgb_status pgb_load_idx(const char* path, float scale_div, float* out) {
+  return guarded([&] {
+    if (!path || !out) raise(PGB_ERR_CONTRACT, "null argument");
+    pgb::IdxArray a = pgb::read_idx(path);
+    const size_t n = a.bytes.size() - a.offset;
+    const unsigned char* b = a.bytes.data() + a.offset;
+    for (size_t i = 0; i < n; ++i) {
+      const float v = static_cast<float>(b[i]);
+      out[i] = scale_div > 0.0f ? v / scale_div : v;
+    }
+  });
+}
+
 }  // extern "C"
+
+namespace pgb {
+
+namespace {
+uint32_t be32(const unsigned char* p) {
+  return (uint32_t(p[0]) << 24) | (uint32_t(p[1]) << 16) | (uint32_t(p[2]) << 8) | uint32_t(p[3]);
+}
+}  // namespace
+
+// Same checks and error offsets as the reference's loader.
+IdxArray read_idx(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) raise(PGB_ERR_IO, "load_idx: cannot open '" + path + "'");
+  IdxArray a;
+  a.bytes.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+  if (a.bytes.size() < 4)
+    raise(PGB_ERR_FORMAT, "load_idx: '" + path + "' truncated at offset 0 (" +
+                              std::to_string(a.bytes.size()) + " bytes)");
+  const uint32_t magic = be32(a.bytes.data());
+  if ((magic >> 16) != 0 || ((magic >> 8) & 0xff) != 0x08) {
+    char buf[16];
+    std::snprintf(buf, sizeof(buf), "%08x", magic);
+    raise(PGB_ERR_FORMAT, std::string("load_idx: bad magic 0x") + buf +
+                              " at offset 0 (expected an unsigned-byte IDX array)");
+  }
+  const uint32_t ndim = magic & 0xff;
+  if (ndim < 1 || ndim > 4)
+    raise(PGB_ERR_FORMAT, "load_idx: unsupported rank " + std::to_string(ndim) + " at offset 3");
+  size_t offset = 4;
+  int64_t total = 1;
+  for (uint32_t d = 0; d < ndim; ++d) {
+    if (a.bytes.size() < offset + 4)
+      raise(PGB_ERR_FORMAT, "load_idx: truncated dims at offset " + std::to_string(offset));
+    const int64_t extent = be32(a.bytes.data() + offset);
+    a.dims.push_back(extent);
+    total *= extent;
+    offset += 4;
+  }
+  if (a.bytes.size() != offset + static_cast<size_t>(total))
+    raise(PGB_ERR_FORMAT, "load_idx: payload size mismatch at offset " + std::to_string(offset) +
+                              " (want " + std::to_string(total) + " bytes, have " +
+                              std::to_string(a.bytes.size() - offset) + ")");
+  a.offset = offset;
+  return a;
+}
+
+}  // namespace pgb

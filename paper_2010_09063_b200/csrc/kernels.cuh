@@ -1277,6 +1277,17 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
   __syncthreads();
 }
 
+// IDX payload bytes -> fp32 (io::load_idx + load_mnist's / 255,
+// proj/core/src/dataset.cpp:77-80,98-103): float(b), divided when scale > 0
+__global__ void decode_u8_kernel(const unsigned char* __restrict__ b, long long n, float scale,
+                                 float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = (float)b[i];
+    out[i] = scale > 0.0f ? __fdiv_rn(v, scale) : v;
+  }
+}
+
 // device-side step counter of the multi-step graphs
 __global__ void set_counter_kernel(long long* v, long long value) { *v = value; }
 __global__ void advance_counter_kernel(long long* v, long long by) { *v += by; }

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "pegrad_b200.h"
 
@@ -83,5 +84,14 @@ void layer_shapes(const pgb_model_desc& d, ExShape* s /* n_layers+1 */);
 void validate_dp_config(const pgb_dp_config& c, int64_t batch);
 void check_strategy_support(int32_t strategy, const pgb_model_desc& d);
 const char* layer_kind_name(int32_t k);
+
+// An unsigned-byte IDX container read and validated on the host (the
+// payload starts at bytes[offset]).
+struct IdxArray {
+  std::vector<unsigned char> bytes;
+  std::vector<int64_t> dims;
+  size_t offset = 0;
+};
+IdxArray read_idx(const std::string& path);
 
 }  // namespace pgb

@@ -4,7 +4,8 @@
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+import json
+from dataclasses import asdict, dataclass, field
 from typing import List
 
 import numpy as np
@@ -13,7 +14,7 @@ from . import _lib
 from ._lib import check, lib
 from .dataset import Dataset, slice_batch
 from .dpsgd import DpConfig, dpsgd_step, sgd_step
-from .errors import ConfigError, UnsupportedError
+from .errors import ConfigError, ContractError, IoError, UnsupportedError
 from .models import Model, ModelKind, build, model_name
 from .strategies import ExecMode, GradEngine, Strategy, strategy_name
 
@@ -57,6 +58,85 @@ class RunOptions:
     learning_rate: float = 0.1
     microbatch: int = 1
     seed: int = 0
+
+
+def _record_to_obj(r: BenchRecord) -> dict:
+    d = asdict(r)
+    d["vectorized"] = bool(d["vectorized"])
+    return d
+
+
+def records_to_json(records: List[BenchRecord]) -> str:
+    """bench::records_to_json (proj/core/src/harness.cpp:219-267): an array of
+    records with snake_case keys, the reference's nlohmann layout (sorted keys,
+    2-space indent) so either side parses the other's files."""
+    if not records:
+        raise ContractError("emit: no records")
+    return json.dumps([_record_to_obj(r) for r in records], indent=2, sort_keys=True)
+
+
+def records_from_json(text: str) -> List[BenchRecord]:
+    """bench::records_from_json (proj/core/src/harness.cpp:236-274)."""
+    out = []
+    for j in json.loads(text):
+        o = j["optimizer_report"]
+        out.append(BenchRecord(
+            model=j["model"], strategy=j["strategy"], mode=j["mode"],
+            vectorized=bool(j["vectorized"]), batch_size=int(j["batch_size"]),
+            epochs=int(j["epochs"]), median_epoch_seconds=float(j["median_epoch_seconds"]),
+            epoch_seconds=[float(v) for v in j["epoch_seconds"]],
+            peak_planned_bytes=int(j["peak_planned_bytes"]),
+            optimizer_report=OptimizerReport(int(o["removed_nodes"]), int(o["fusion_groups"]),
+                                             int(o["peak_bytes"]), int(o["no_reuse_bytes"]),
+                                             float(o["trace_seconds"])),
+            seed=int(j["seed"]), element_width=int(j["element_width"]), status=j["status"],
+            reason=j["reason"]))
+    return out
+
+
+def emit_json(records: List[BenchRecord], path: str) -> None:
+    """bench::emit_json (proj/core/src/harness.cpp:276-282)."""
+    text = records_to_json(records)
+    try:
+        with open(path, "w") as f:
+            f.write(text + "\n")
+    except OSError as e:
+        raise IoError(f"emit_json: cannot write '{path}'") from e
+
+
+def parse_json_file(path: str) -> List[BenchRecord]:
+    """bench::parse_json_file (proj/core/src/harness.cpp:284-290)."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError as e:
+        raise IoError(f"parse_json_file: cannot read '{path}'") from e
+    return records_from_json(text)
+
+
+def emit_csv(records: List[BenchRecord], path: str) -> None:
+    """bench::emit_csv (proj/core/src/harness.cpp:292-317): header plus one line
+    per record, the epoch list joined by ';'."""
+    if not records:
+        raise ContractError("emit: no records")
+    head = ("model,strategy,mode,vectorized,batch_size,epochs,median_epoch_seconds,"
+            "epoch_seconds,peak_planned_bytes,removed_nodes,fusion_groups,opt_peak_bytes,"
+            "no_reuse_bytes,trace_seconds,seed,element_width,status,reason\n")
+    g = lambda v: f"{v:g}"  # noqa: E731  (ostream default precision, 6 significant digits)
+    try:
+        with open(path, "w") as f:
+            f.write(head)
+            for r in records:
+                o = r.optimizer_report
+                f.write(",".join([
+                    r.model, r.strategy, r.mode, "true" if r.vectorized else "false",
+                    str(r.batch_size), str(r.epochs), g(r.median_epoch_seconds),
+                    ";".join(g(v) for v in r.epoch_seconds), str(r.peak_planned_bytes),
+                    str(o.removed_nodes), str(o.fusion_groups), str(o.peak_bytes),
+                    str(o.no_reuse_bytes), g(o.trace_seconds), str(r.seed),
+                    str(r.element_width), r.status, r.reason]) + "\n")
+    except OSError as e:
+        raise IoError(f"emit_csv: cannot write '{path}'") from e
 
 
 def median(values: List[float]) -> float:

@@ -184,6 +184,7 @@ struct Engine {
   const float* cap_xring = nullptr;  // resident-data ring (run_steps_device)
   const float* cap_yring = nullptr;
   int cap_ring_n = 0;
+  const float* cap_x_next = nullptr;  // next step's batch inside a chunk graph
   struct ChunkGraph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -789,6 +790,7 @@ struct Engine {
     prm.yring = cap_yring;
     prm.ring_origin = 0;
     prm.ring_n = cap_ring_n;
+    prm.x_next = cap_x_next;
     if (mnist_tc) {
       AggLaunch L{};
       if (fuse_agg_next) {
@@ -1157,10 +1159,12 @@ struct Engine {
         clipped_dst = d_clip_ring + 2 * (sl * C + j);
         cap_step_base = d_step_base + sl;
         cap_step_off = (int)j;
+        cap_x_next = j + 1 < C ? d_xc[sl] + (j + 1) * B * in_row : nullptr;
         kernels_last = enqueue_step(stream, d_xc[sl] + j * B * in_row, d_yc[sl] + j * B, 1);
       }
     } catch (...) {
       cap_step_base = nullptr;
+      cap_x_next = nullptr;
       cudaStreamEndCapture(stream, &cg.graph);
       if (cg.graph) cudaGraphDestroy(cg.graph);
       cg.graph = nullptr;
@@ -1168,6 +1172,7 @@ struct Engine {
     }
     cap_step_base = nullptr;
     cap_step_off = 0;
+    cap_x_next = nullptr;
     norms_dst = nd0;
     clipped_dst = cd0;
     PGB_CUDA(cudaStreamEndCapture(stream, &cg.graph));

@@ -110,10 +110,23 @@ struct Params {
   // in-kernel after a grid barrier, agg_tiles tiles over the CTA halves
   unsigned long long* grid_ctr;
   int agg_tiles;
+  // the next step's input batch (or null): its images are prefetched into L2
+  // at kernel start so the next launch's TMA loads hit L2 instead of HBM
+  const float* x_next;
 };
 
 __device__ __forceinline__ long long step_index(const Params& prm) {
   return prm.step_base ? *prm.step_base + prm.step_off : prm.a.step;
+}
+
+// the next step's images (resident ring: batch step+1 mod ring_n), or null
+__device__ __forceinline__ const float* next_inputs(const Params& prm) {
+  if (prm.xring) {
+    long long bi = (step_index(prm) + 1 - prm.ring_origin) % prm.ring_n;
+    if (bi < 0) bi += prm.ring_n;
+    return prm.xring + bi * prm.B * (H0 * H0);
+  }
+  return prm.x_next;
 }
 
 // this step's input batch (x, y)

@@ -73,7 +73,11 @@ struct TcSmem {
   float a2[2][F1];
   float z1[2][NW][H1];
   float h[2][H1], dz1[2][H1], dz2[2][16];
-  float w4[H1 * NC], b4[16], b3[H1], b1[D1], b2[D2];
+  alignas(16) float w4[H1 * NC];  // TMA destinations (16-byte aligned)
+  alignas(16) float b4[16];
+  alignas(16) float b3[H1];
+  alignas(16) float b1[D1];
+  alignas(16) float b2[D2];
   float yb[2];
   float b1red[2][NW][D1];
   double red5[2][5][NW];
@@ -119,32 +123,44 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     tc::mbar_init(&S.bar[3], kIssuers);  // every issuer commits once per GEMM phase
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t img = (uint32_t)(sizeof(float) * H0 * H0 * nex);
+    // images, conv1 W operand, and the small parameter blocks (biases, fc2 W;
+    // b4 as 12 floats for the 16-byte granularity) on one barrier
+    constexpr uint32_t kSmall = 4u * (D1 + D2 + H1 * NC + H1 + 12);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(smem_addr(&S.bar[0])), "r"(img + 8192u) : "memory");
+                 :: "r"(smem_addr(&S.bar[0])), "r"(img + 8192u + kSmall) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(smem_addr(&S.bar[1])), "r"(65536u) : "memory");
     const float *gx, *gy;
     step_inputs(prm, gx, gy);
     bulk_g2s(S.xstage[0], gx + (size_t)b0 * H0 * H0, img, reinterpret_cast<unsigned long long*>(&S.bar[0]));
     bulk_g2s(regA + OFF_W1C, tcw + TCW_W1C, 8192u, reinterpret_cast<unsigned long long*>(&S.bar[0]));
+    auto* b0bar = reinterpret_cast<unsigned long long*>(&S.bar[0]);
+    bulk_g2s(S.b1, W + prm.off[1], 4u * D1, b0bar);
+    bulk_g2s(S.b2, W + prm.off[3], 4u * D2, b0bar);
+    bulk_g2s(S.b3, W + prm.off[5], 4u * H1, b0bar);
+    bulk_g2s(S.w4, W + prm.off[6], 4u * H1 * NC, b0bar);
+    bulk_g2s(S.b4, W + prm.off[7], 4u * 12, b0bar);
     bulk_g2s(S.w2, tcw + TCW_W2C, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[1]));
+    // warm L2 with the next step's images of this CTA's pair
+    if (const float* xn = next_inputs(prm))
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   :: "l"(xn + (size_t)b0 * H0 * H0), "r"(img) : "memory");
   }
-  // shared loss-tail operands and biases
-  if (t < H1 * NC) S.w4[t] = __ldg(W + prm.off[6] + t);
-  else if (t < H1 * NC + NC) S.b4[t - H1 * NC] = __ldg(W + prm.off[7] + t - H1 * NC);
-  else if (t < H1 * NC + NC + H1) S.b3[t - H1 * NC - NC] = __ldg(W + prm.off[5] + t - H1 * NC - NC);
-  else if (t < H1 * NC + NC + H1 + D1) S.b1[t - 362] = __ldg(W + prm.off[1] + t - 362);
-  else if (t < H1 * NC + NC + H1 + D1 + D2) S.b2[t - 378] = __ldg(W + prm.off[3] + t - 378);
+  // the label: loaded now, first used by the loss tail (lane 0 of warp 0 of
+  // the half holds it; no barrier waits on the load)
+  float ylab = 0.0f;
   if (tt == 0 && has) {
     const float *gx, *gy;
     step_inputs(prm, gx, gy);
-    S.yb[ex] = gy[b];
+    ylab = gy[b];
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem;
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 21);
   tc::mbar_wait(&S.bar[0], 0);
+  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 22);
 
   // ---- the Y operand of conv1 forward ----------------------------------------
   // Y[ex][hl][par][R = 2r + h][c] = xpad[r][c + 2 par + 4 h]
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
 #pragma unroll
       for (int j = 0; j < H1; ++j) lg = fmaf(__shfl_sync(0xffffffffu, hv, j), S.w4[j * NC + c], lg);
       lg += S.b4[c];
-      const float raw = S.yb[ex];
+      const float raw = __shfl_sync(0xffffffffu, ylab, 0);
       const bool ok = valid_id(raw, NC);
       if (!ok && lane == 0) raise_index(prm.err, 0, b, raw, NC);
       const int y = ok ? (int)raw : 0;

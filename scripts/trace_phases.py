@@ -53,6 +53,9 @@ print("phase  alone(us)  shared(us)" if n == B else "phase  early-half(us)  late
 for a, b in zip(marks[:-1], marks[1:]):
     d = F[:, b] - F[:, a]
     print(f"{a:2d}->{b:2d}  {d[one].mean() / 1e3:8.2f}  {d[two].mean() / 1e3:8.2f}")
+if F[:, 21].all() and F[:, 22].all() and not F[:, 19].any():
+    print(f"  setup: TMEM alloc + barrier {(F[:, 21] - F[:, 0]).mean() / 1e3:.2f} us, image/W1 TMA wait "
+          f"{(F[:, 22] - F[:, 21]).mean() / 1e3:.2f} us, Y build {(F[:, 1] - F[:, 22]).mean() / 1e3:.2f} us")
 for k in range(16, 19):
     if F[:, k].all():
         print(f"  mark {k}: {(F[:, k] - F[:, 7]).mean() / 1e3:.2f} us after mark 7")

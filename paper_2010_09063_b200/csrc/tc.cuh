@@ -161,13 +161,18 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
   const int z = blockIdx.z;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
   const int M = op.M, N = op.N, K = op.K;
-  constexpr uint32_t kCols = 3 * BN <= 32 ? 32 : 3 * BN <= 64 ? 64 : 3 * BN <= 128 ? 128
-                             : 3 * BN <= 256 ? 256 : 512;
-  static_assert(3 * BN <= 512, "BN too large for three TMEM accumulators");
+  // four accumulators: hi.hi alternating between two (even / odd K chunks),
+  // hi.lo and lo.hi each their own, so the three MMAs of a K step come from
+  // three issuing warps (one thread issues a tcgen05.mma only every ~120
+  // cycles; scripts/umma_rate.py)
+  constexpr uint32_t kCols = 4 * BN <= 32 ? 32 : 4 * BN <= 64 ? 64 : 4 * BN <= 128 ? 128
+                             : 4 * BN <= 256 ? 256 : 512;
+  static_assert(4 * BN <= 512, "BN too large for four TMEM accumulators");
+  static_assert(NT >= 96, "three issuing warps");
   if (warp == 0) tmem_alloc(&S.tmem, kCols);
   if (t == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
+    mbar_init(&S.bar[0], 3);
+    mbar_init(&S.bar[1], 3);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (Op::kTableA) {
@@ -186,24 +191,29 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
     Wd = op.img_w();
     src = op.img(z);
   }
-  for (int kc = 0; kc < nk; ++kc) {
-    const int s = kc & 1;
-    const int k0 = kc * kBK;
+  // Operands are gathered one K chunk ahead into registers (kA + kB values
+  // per thread), so the global-load latency of chunk kc+1 overlaps the split,
+  // the shared stores and the MMAs of chunk kc.
+  constexpr int kA = kBM * kBK / NT, kB = (BN * kBK + NT - 1) / NT;
+  float ra[kA], rb[kB];
+  // per-k gather info of a chunk, computed once per CTA into kinfo[kc & 1]
+  auto kinfo_fill = [&](int kc) {
     if constexpr (Op::kTableA) {
-      if (t < kBK) S.kinfo[s][t] = op.k_info(z, k0 + t);
+      if (t < kBK) S.kinfo[kc & 1][t] = op.k_info(z, kc * kBK + t);
     }
-    if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
-    if constexpr (Op::kTableA) __syncthreads();
-    // gather A: lanes cover one 8x4 core matrix (conflict-free 128 B stores)
-#pragma unroll 4
-    for (int e = t; e < kBM * kBK; e += NT) {
+  };
+  auto fetch = [&](int kc) {
+    const int k0 = kc * kBK;
+#pragma unroll
+    for (int i = 0; i < kA; ++i) {
+      const int e = t + i * NT;
       const int core = e >> 5, in = e & 31;
       const int r = (core % (kBM / 8)) * 8 + (in >> 2);
       const int k = (core / (kBM / 8)) * 4 + (in & 3);
       float v;
       if constexpr (Op::kTableA) {
         const int4 ri = S.rowinfo[r];
-        const int4 ki = S.kinfo[s][k];
+        const int4 ki = S.kinfo[kc & 1][k];
         const int iy = ri.y + ki.y, ix = ri.z + ki.z;
         const bool ok = (ri.w & ki.w) && (unsigned)iy < (unsigned)H && (unsigned)ix < (unsigned)Wd;
         v = ok ? __ldg(src + ri.x + ki.x + iy * Wd + ix) : 0.0f;
@@ -211,44 +221,77 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
         const int m = m0 + r, kk = k0 + k;
         v = (m < M && kk < K) ? op.a(z, m, kk) : 0.0f;
       }
+      ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int e = t + i * NT;
+      float v = 0.0f;
+      if (e < BN * kBK) {
+        const int core = e >> 5, in = e & 31;
+        const int r = (core % (BN / 8)) * 8 + (in >> 2);
+        const int k = (core / (BN / 8)) * 4 + (in & 3);
+        const int n = n0 + r, kk = k0 + k;
+        v = (n < N && kk < K) ? op.b(z, n, kk) : 0.0f;
+      }
+      rb[i] = v;
+    }
+  };
+  kinfo_fill(0);
+  __syncthreads();
+  fetch(0);
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    // chunk kc+1's gather info (slot s^1 was last read by fetch(kc-1), two
+    // barriers ago); made visible by this iteration's barrier
+    if (kc + 1 < nk) kinfo_fill(kc + 1);
+    if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
+    // split + store this chunk (lanes cover one 8x4 core matrix: conflict-free)
+#pragma unroll
+    for (int i = 0; i < kA; ++i) {
+      const int e = t + i * NT;
+      const int core = e >> 5, in = e & 31;
+      const int r = (core % (kBM / 8)) * 8 + (in >> 2);
+      const int k = (core / (kBM / 8)) * 4 + (in & 3);
       float hi, lo;
-      split_tf32(v, hi, lo);
+      split_tf32(ra[i], hi, lo);
       const int o = canon_off<kBK>(r, k);
       S.ahi[s][o] = hi;
       S.alo[s][o] = lo;
     }
-    for (int e = t; e < BN * kBK; e += NT) {
-      const int core = e >> 5, in = e & 31;
-      const int r = (core % (BN / 8)) * 8 + (in >> 2);
-      const int k = (core / (BN / 8)) * 4 + (in & 3);
-      const int n = n0 + r, kk = k0 + k;
-      const float v = (n < N && kk < K) ? op.b(z, n, kk) : 0.0f;
-      float hi, lo;
-      split_tf32(v, hi, lo);
-      const int o = canon_off<kBK>(r, k);
-      S.bhi[s][o] = hi;
-      S.blo[s][o] = lo;
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int e = t + i * NT;
+      if (e < BN * kBK) {
+        const int core = e >> 5, in = e & 31;
+        const int r = (core % (BN / 8)) * 8 + (in >> 2);
+        const int k = (core / (BN / 8)) * 4 + (in & 3);
+        float hi, lo;
+        split_tf32(rb[i], hi, lo);
+        const int o = canon_off<kBK>(r, k);
+        S.bhi[s][o] = hi;
+        S.blo[s][o] = lo;
+      }
     }
     fence_proxy_async();
     __syncthreads();
-    if (t == 0) {
+    if (lane == 0 && warp < 3) {
+      // warp 0: hi.hi, warp 1: hi.lo, warp 2: lo.hi
       fence_after_sync();
-      const uint32_t ah = smem_u32(S.ahi[s]), al = smem_u32(S.alo[s]);
-      const uint32_t bh = smem_u32(S.bhi[s]), bl = smem_u32(S.blo[s]);
+      const uint32_t a = smem_u32(warp == 2 ? S.alo[s] : S.ahi[s]);
+      const uint32_t b = smem_u32(warp == 1 ? S.blo[s] : S.bhi[s]);
+      const uint32_t d = warp == 0 ? tmem + (uint32_t)((kc & 1) * BN) : tmem + (uint32_t)((1 + warp) * BN);
+      const bool first = warp == 0 ? kc <= 1 : kc == 0;
 #pragma unroll
       for (int ks = 0; ks < kBK / 8; ++ks) {
         const uint32_t off = ks * 256;  // two 128-B core matrices per k-step
-        const uint64_t dah = make_desc(ah + off, 128, kBK * 32);
-        const uint64_t dal = make_desc(al + off, 128, kBK * 32);
-        const uint64_t dbh = make_desc(bh + off, 128, kBK * 32);
-        const uint64_t dbl = make_desc(bl + off, 128, kBK * 32);
-        const uint32_t main = tmem + (uint32_t)((kc & 1) * BN), corr = tmem + 2 * BN;
-        mma_tf32(main, dah, dbh, idesc, (kc > 1 || ks > 0) ? 1u : 0u);
-        mma_tf32(corr, dah, dbl, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
-        mma_tf32(corr, dal, dbh, idesc, 1u);
+        mma_tf32(d, make_desc(a + off, 128, kBK * 32), make_desc(b + off, 128, kBK * 32), idesc,
+                 (first && ks == 0) ? 0u : 1u);
       }
       commit(&S.bar[s]);
     }
+    // next chunk's operands into registers while the tensor core runs
+    if (kc + 1 < nk) fetch(kc + 1);
   }
   // all MMAs done once the last commit lands (they complete in issue order)
   mbar_wait(&S.bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
@@ -260,16 +303,17 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
   const int cbeg = (warp >> 2) * (BN / kGroups), cend = cbeg + BN / kGroups;
 #pragma unroll 1
   for (int c0 = cbeg; c0 < cend; c0 += 8) {
-    float v[8], v1[8], vc[8];
+    float v[8], v1[8], vc[8], vd[8];
     tmem_ld8(lane_base + (uint32_t)c0, v);
     tmem_ld8(lane_base + (uint32_t)(2 * BN + c0), vc);
+    tmem_ld8(lane_base + (uint32_t)(3 * BN + c0), vd);
     if (nk > 1) {
       tmem_ld8(lane_base + (uint32_t)(BN + c0), v1);
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[j] += v1[j];
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] += vc[j];
+    for (int j = 0; j < 8; ++j) v[j] += vc[j] + vd[j];
     if (row < M) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)

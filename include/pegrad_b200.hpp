@@ -284,6 +284,37 @@ inline Dataset synth_for_model(const models::ModelDesc& d, int64_t n, uint64_t s
   check(pgb_synth(&d.c, n, seed, ds.inputs.data(), ds.labels.data()));
   return ds;
 }
+
+// io::load_idx (dataset.cpp:35-82): values of one unsigned-byte IDX array and
+// its dims; FormatError / IoError with the reference's messages.
+struct IdxArray {
+  std::vector<float> values;
+  std::vector<int64_t> dims;
+};
+inline IdxArray load_idx(const std::string& path, float scale_div = 0.0f) {
+  int32_t rank = 0;
+  int64_t dims[4] = {0, 0, 0, 0}, count = 0;
+  check(pgb_idx_info(path.c_str(), &rank, dims, &count));
+  IdxArray a;
+  a.dims.assign(dims, dims + rank);
+  a.values.resize((size_t)count);
+  check(pgb_load_idx(path.c_str(), scale_div, a.values.data()));
+  return a;
+}
+
+// io::load_mnist (dataset.cpp:84-112): images scaled to [0,1], (N,1,28,28)
+inline Dataset load_mnist(const std::string& dir, const std::string& prefix = "train") {
+  IdxArray img = load_idx(dir + "/" + prefix + "-images-idx3-ubyte", 255.0f);
+  IdxArray lab = load_idx(dir + "/" + prefix + "-labels-idx1-ubyte");
+  if (img.dims.size() != 3) throw FormatError("load_mnist: expected rank-3 image array");
+  if (lab.dims.size() != 1 || lab.dims[0] != img.dims[0])
+    throw FormatError("load_mnist: image/label count mismatch");
+  Dataset ds;
+  ds.count = img.dims[0];
+  ds.inputs = std::move(img.values);
+  ds.labels = std::move(lab.values);
+  return ds;
+}
 }  // namespace io
 
 // ---- epoch driver (harness.hpp:75-80): N/B sequential slices ----------------------
@@ -301,6 +332,20 @@ inline EpochResult run_epoch(models::Model& model, GradEngine& engine, const io:
                       step0, nullptr, &r.clipped_total, &r.seconds));
   engine.download(model);
   return r;
+}
+
+// The step loop of run_bench (harness.cpp:147-151) over batches already on the
+// device (d_x: n_batches * B examples): step step0 + i reads batch
+// (step0 + i) mod n_batches; static multi-step CUDA graphs, asynchronous.
+inline int64_t run_steps_device(GradEngine& engine, const float* d_x, const float* d_y,
+                                int64_t n_batches, int64_t n_steps, const DpConfig<float>& cfg,
+                                int64_t step0) {
+  pgb_dp_config c{cfg.clip_norm, cfg.noise_multiplier, cfg.learning_rate, cfg.microbatch,
+                  cfg.seed};
+  int64_t launches = 0;
+  check(pgb_run_steps_device(engine.handle(), d_x, d_y, n_batches, n_steps, &c, step0,
+                             &launches));
+  return launches;
 }
 }  // namespace bench
 

@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
+
+#include <unistd.h>
 
 #include "pegrad_b200.hpp"
 
@@ -113,6 +116,38 @@ int main() {
   auto ep = io::synth_for_model(model.desc, 4 * B, 5);
   auto res = bench::run_epoch(model, engine, ep, cfg, 100);
   CHECK(res.seconds > 0 && res.clipped_total >= 0);
+
+  // IDX ingest (dataset.cpp:35-112): a small MNIST pair written here
+  {
+    const char* dir = std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp";
+    const std::string base = std::string(dir) + "/pgb_shim_" + std::to_string(::getpid());
+    auto write = [](const std::string& path, uint32_t magic, std::vector<uint32_t> dims,
+                    const std::vector<unsigned char>& payload) {
+      FILE* f = std::fopen(path.c_str(), "wb");
+      auto be = [&](uint32_t v) {
+        unsigned char b[4] = {(unsigned char)(v >> 24), (unsigned char)(v >> 16),
+                              (unsigned char)(v >> 8), (unsigned char)v};
+        std::fwrite(b, 1, 4, f);
+      };
+      be(magic);
+      for (uint32_t d : dims) be(d);
+      std::fwrite(payload.data(), 1, payload.size(), f);
+      std::fclose(f);
+    };
+    std::vector<unsigned char> img(3 * 28 * 28), lab = {7, 0, 9};
+    for (size_t i = 0; i < img.size(); ++i) img[i] = (unsigned char)(i * 37 % 256);
+    write(base + "-images-idx3-ubyte", 0x803, {3, 28, 28}, img);
+    write(base + "-labels-idx1-ubyte", 0x801, {3}, lab);
+    auto mn = io::load_mnist(dir, "pgb_shim_" + std::to_string(::getpid()));
+    CHECK(mn.count == 3 && mn.inputs.size() == 3 * 784 && mn.labels[2] == 9.0f);
+    CHECK(mn.inputs[5] == (float)(5 * 37 % 256) / 255.0f);
+    write(base + "-bad", 0x0D02, {2, 2}, {1, 2, 3, 4});
+    CHECK(throws<FormatError>([&] { io::load_idx(base + "-bad"); }));
+    CHECK(throws<IoError>([&] { io::load_idx(base + "-missing"); }));
+    std::remove((base + "-images-idx3-ubyte").c_str());
+    std::remove((base + "-labels-idx1-ubyte").c_str());
+    std::remove((base + "-bad").c_str());
+  }
   std::printf("OK\n");
   return 0;
 }

@@ -151,6 +151,10 @@ struct Engine {
   static constexpr int kResSlots = 64;
   cudaEvent_t ev_copied[kSlots] = {}, ev_consumed[kSlots] = {}, ev_done[kResSlots] = {},
               ev_read[kResSlots] = {};
+  // per-batch copies of the first chunk of a chunked epoch (its steps start as
+  // soon as their own batch has landed instead of waiting for the whole chunk)
+  static constexpr int kHeadSlots = kResSlots / kSlots;
+  cudaEvent_t ev_head[kHeadSlots] = {};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
 
   void ensure_host_stage(int64_t steps, int64_t units) {
@@ -301,6 +305,8 @@ struct Engine {
     for (int i = 0; i < kResSlots; ++i)
       for (cudaEvent_t ev : {ev_done[i], ev_read[i]})
         if (ev) cudaEventDestroy(ev);
+    for (int i = 0; i < kHeadSlots; ++i)
+      if (ev_head[i]) cudaEventDestroy(ev_head[i]);
     if (ev_t0) cudaEventDestroy(ev_t0);
     if (ev_t1) cudaEventDestroy(ev_t1);
   }
@@ -602,6 +608,8 @@ struct Engine {
     for (int i = 0; i < kResSlots; ++i)
       for (cudaEvent_t* ev : {&ev_done[i], &ev_read[i]})
         PGB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    for (int i = 0; i < kHeadSlots; ++i)
+      PGB_CUDA(cudaEventCreateWithFlags(&ev_head[i], cudaEventDisableTiming));
     PGB_CUDA(cudaEventCreate(&ev_t0));
     PGB_CUDA(cudaEventCreate(&ev_t1));
     allocate();
@@ -1731,7 +1739,8 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     // step. PGB_CHUNK_STEPS overrides C (1 = the per-step path below).
     int64_t C = 8;  // 4-8 measured best (scripts/e2e_probe.py)
     if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
-    C = std::min<int64_t>(C, Engine::kResSlots / K);
+    // result slots: K chunk slots of C, then the head / remainder slots
+    C = std::min<int64_t>(C, Engine::kResSlots / (K + 1));
     const bool chunked = en.fused_mnist && en.world == 1 && cfg->microbatch == 1 &&
                          en.graph_enabled && C > 1 && steps >= C;
     if (!chunked) C = 1;
@@ -1755,11 +1764,60 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
       }
       PGB_CUDA(cudaEventRecord(copied[sl], en.copy_stream));
     };
-    for (int64_t k = 0; k < std::min<int64_t>(K - 1, nchunks); ++k) copy_in(k);
+    constexpr int KR = Engine::kResSlots;
+    // One step through the per-step graph path: result slot rs_sl, reading
+    // batch j of chunk slot sl (the caller made the batch's copy visible).
+    auto step_once = [&](int64_t s, int sl, int64_t j, int rs_sl, bool wait_read) {
+      if (ring) {
+        // result slot rs_sl's previous results must have been read back
+        if (wait_read) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[rs_sl], 0));
+        en.norms_dst = en.d_norms_ring + (size_t)rs_sl * en.B;
+        en.clipped_dst = en.d_clip_ring + 2 * rs_sl;
+      }
+      const float* xs = xslot(sl) + j * en.B * en.in_row;
+      const float* ys = yslot(sl) + j * en.B;
+      en.push_args(en.make_args(*cfg, step0 + s, xs, ys));
+      en.launch_step(xs, ys, cfg->microbatch);
+      // the step's result read back every step (norms, clipped count)
+      cudaStream_t rs = ring ? en.out_stream : en.stream;
+      if (ring) {
+        PGB_CUDA(cudaEventRecord(done[rs_sl], en.stream));
+        PGB_CUDA(cudaStreamWaitEvent(rs, done[rs_sl], 0));
+      }
+      PGB_CUDA(cudaMemcpyAsync(en.h_clip_stage + 2 * s, en.clipped_dst, sizeof(int) * 2,
+                               cudaMemcpyDeviceToHost, rs));
+      if (norms_out)
+        PGB_CUDA(cudaMemcpyAsync(en.h_norm_stage + s * U, en.norms_dst, sizeof(float) * U,
+                                 cudaMemcpyDeviceToHost, rs));
+      if (ring) PGB_CUDA(cudaEventRecord(read[rs_sl], rs));
+    };
+    int64_t k_first = 0;
+    if (chunked) {
+      // head: chunk 0 as per-batch copies, its steps on the per-step path,
+      // each waiting for its own batch (result slots K*C ..)
+      PGB_CUDA(cudaStreamWaitEvent(en.copy_stream, en.ev_t0, 0));
+      for (int64_t j = 0; j < C; ++j) {
+        PGB_CUDA(cudaMemcpyAsync(xslot(0) + j * en.B * en.in_row, x + j * en.B * en.in_row, xb,
+                                 cudaMemcpyHostToDevice, en.copy_stream));
+        PGB_CUDA(cudaMemcpyAsync(yslot(0) + j * en.B, y + j * en.B, yb, cudaMemcpyHostToDevice,
+                                 en.copy_stream));
+        PGB_CUDA(cudaEventRecord(en.ev_head[j], en.copy_stream));
+      }
+      for (int64_t k = 1; k < std::min<int64_t>(K - 1, nchunks); ++k) copy_in(k);
+      if (K - 1 < nchunks) copy_in(K - 1);
+      for (int64_t j = 0; j < C; ++j) {
+        PGB_CUDA(cudaStreamWaitEvent(en.stream, en.ev_head[j], 0));
+        step_once(j, 0, j, (int)(K * C + j), false);
+      }
+      PGB_CUDA(cudaEventRecord(consumed[0], en.stream));
+      k_first = 1;
+    } else {
+      for (int64_t k = 0; k < std::min<int64_t>(K - 1, nchunks); ++k) copy_in(k);
+    }
     const StepArgs args0 = en.make_args(*cfg, step0, nullptr, nullptr);
-    for (int64_t k = 0; chunked && k < nfull; ++k) {
+    for (int64_t k = k_first; chunked && k < nfull; ++k) {
       const int sl = (int)(k % K);
-      if (k + K - 1 < nchunks) copy_in(k + K - 1);
+      if (k + K - 1 < nchunks && k > 0) copy_in(k + K - 1);
       PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
       // result slots sl*C .. sl*C+C-1 of chunk k-K must have been read back
       if (k >= K) PGB_CUDA(cudaStreamWaitEvent(en.stream, read[sl], 0));
@@ -1775,41 +1833,19 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
       PGB_CUDA(cudaEventRecord(read[sl], en.out_stream));
     }
     // per-step path: every step of a non-chunked epoch, or the remainder of a
-    // chunked one (result slots from K*C on, clear of the chunk slots)
+    // chunked one (result slots from K*C on, clear of the chunk slots; waiting
+    // on a slot's read event also covers the head's use of it)
     const int64_t s_begin = chunked ? nfull * C : 0;
     for (int64_t s = s_begin; s < steps; ++s) {
       const int64_t k = s / C, j = s % C;
       const int sl = (int)(k % K);
-      constexpr int KR = Engine::kResSlots;
       const int rs_sl = chunked ? (int)(K * C + (s - s_begin) % (KR - K * C)) : (int)(s % KR);
       if (j == 0) {
         if (!chunked && k + K - 1 < nchunks) copy_in(k + K - 1);
         PGB_CUDA(cudaStreamWaitEvent(en.stream, copied[sl], 0));
       }
-      if (ring) {
-        // result slot rs_sl's previous results must have been read back
-        if (s - s_begin >= KR - (chunked ? K * C : 0))
-          PGB_CUDA(cudaStreamWaitEvent(en.stream, read[rs_sl], 0));
-        en.norms_dst = en.d_norms_ring + (size_t)rs_sl * en.B;
-        en.clipped_dst = en.d_clip_ring + 2 * rs_sl;
-      }
-      const float* xs = xslot(sl) + j * en.B * en.in_row;
-      const float* ys = yslot(sl) + j * en.B;
-      en.push_args(en.make_args(*cfg, step0 + s, xs, ys));
-      en.launch_step(xs, ys, cfg->microbatch);
+      step_once(s, sl, j, rs_sl, chunked || s >= KR);
       if (j == C - 1 || s == steps - 1) PGB_CUDA(cudaEventRecord(consumed[sl], en.stream));
-      // the step's result read back every step (norms, clipped count)
-      cudaStream_t rs = ring ? en.out_stream : en.stream;
-      if (ring) {
-        PGB_CUDA(cudaEventRecord(done[rs_sl], en.stream));
-        PGB_CUDA(cudaStreamWaitEvent(rs, done[rs_sl], 0));
-      }
-      PGB_CUDA(cudaMemcpyAsync(en.h_clip_stage + 2 * s, en.clipped_dst, sizeof(int) * 2,
-                               cudaMemcpyDeviceToHost, rs));
-      if (norms_out)
-        PGB_CUDA(cudaMemcpyAsync(en.h_norm_stage + s * U, en.norms_dst, sizeof(float) * U,
-                                 cudaMemcpyDeviceToHost, rs));
-      if (ring) PGB_CUDA(cudaEventRecord(read[rs_sl], rs));
     }
     en.norms_dst = en.d_norms;
     en.clipped_dst = en.d_clipped;

@@ -132,6 +132,9 @@ struct Engine {
   bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
   bool agg_in_kernel = false;  // ... and the aggregation after an in-kernel grid barrier
   bool fuse_agg_next = false;  // set by enqueue_step for the fused launch it makes
+  // conv2 W leaves the MNIST kernel as clipped pair rows (PGB_C2_PAIRS=0: per example)
+  bool c2_pairs = true;
+  bool pairs_next = false;     // ... for the launch enqueue_step is making
   unsigned long long* d_grid_ctr = nullptr;
   bool use_tc = true;        // conv GEMMs on tcgen05 (PGB_NO_TC=1: CUDA-core tiles)
   std::vector<int64_t> param_off;
@@ -381,6 +384,7 @@ struct Engine {
     fused_mnist = is_mnist(desc) && std::getenv("PGB_NO_FUSED") == nullptr;
     mnist_tc = fused_mnist && std::getenv("PGB_MNIST_SIMT") == nullptr;
     use_tc = std::getenv("PGB_NO_TC") == nullptr;
+    if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
   }
 
   void allocate() {
@@ -799,6 +803,7 @@ struct Engine {
     prm.ring_origin = 0;
     prm.ring_n = cap_ring_n;
     prm.x_next = cap_x_next;
+    if (mnist_tc && pairs_next) prm.c2_pairs = prm.st_c2w;
     if (mnist_tc) {
       AggLaunch L{};
       if (fuse_agg_next) {
@@ -930,11 +935,12 @@ struct Engine {
     int nk = 0;
     // one launch per step: the fused MNIST kernel aggregates in-kernel
     fuse_agg_next = agg_in_kernel && m == 1;
+    pairs_next = fused_mnist && mnist_tc && c2_pairs && m == 1 && !fuse_agg_next;
     sparse_embed_next = emb_layer >= 0 && m == 1;
     try {
       nk += enqueue_grads(s, x_slot, y_slot);
     } catch (...) {
-      fuse_agg_next = sparse_embed_next = false;
+      fuse_agg_next = sparse_embed_next = pairs_next = false;
       throw;
     }
     if (fuse_agg_next) {
@@ -956,10 +962,14 @@ struct Engine {
       nk += mark(s, "sumsq");
       nk += enqueue_aggregate(s, ut, ut.n, U);
     } else {
-      nk += enqueue_aggregate(s, table_for(x_slot, sparse_embed_next), nparts, (int)B,
-                              fused_mnist);
+      BlockTable t = table_for(x_slot, sparse_embed_next);
+      if (pairs_next) {  // conv2 W: (B+1)/2 clipped pair rows in place of its stack
+        t.rows[2] = (int)((B + 1) / 2);
+        t.stride[2] = t.size[2];
+      }
+      nk += enqueue_aggregate(s, t, nparts, (int)B, fused_mnist);
     }
-    sparse_embed_next = false;
+    sparse_embed_next = pairs_next = false;
     return nk;
   }
 

@@ -487,6 +487,10 @@ struct BlockTable {
   // optional hi/lo tensor-core operand copies (mnist_tc.cuh): 1 conv1 W, 2 conv2 W
   float* tcw[kMaxBlocks];
   int tcw_kind[kMaxBlocks];
+  // kind-0 blocks whose rows are already clipped sums of unit groups (the
+  // MNIST kernel's conv2 pair rows): row count (0: one row per unit, scaled
+  // by the unit's clip factor in the aggregation)
+  int rows[kMaxBlocks];
 };
 
 // ---- hi/lo UMMA operand shadows of the MNIST conv weights (mnist_tc.cuh) ---
@@ -546,6 +550,36 @@ __device__ __forceinline__ void write_param(const BlockTable& bt, int p, long lo
     bt.shadow[p][shadow_index(r, c, bt.shadow_rows[p], bt.shadow_swz[p])] = v;
   }
   if (bt.tcw[p]) tcw_write(bt.tcw[p], bt.tcw_kind[p], j, v);
+}
+
+// write_param split in two: the destinations (dependent reads of the block
+// table) resolved early, the stores later
+struct ParamDst {
+  float* p;
+  float* sh;
+  float* tcw;
+  int tcw_kind;
+};
+
+__device__ __forceinline__ ParamDst param_dst(const BlockTable& bt, int p, long long j,
+                                              float* params) {
+  ParamDst d;
+  d.p = params + bt.param_off[p] + j;
+  d.sh = nullptr;
+  if (bt.shadow[p]) {
+    const long long cols = bt.size[p] / bt.shadow_rows[p];
+    const long long r = j / cols, c = j - r * cols;
+    d.sh = bt.shadow[p] + shadow_index(r, c, bt.shadow_rows[p], bt.shadow_swz[p]);
+  }
+  d.tcw = bt.tcw[p];
+  d.tcw_kind = bt.tcw_kind[p];
+  return d;
+}
+
+__device__ __forceinline__ void param_store(const ParamDst& d, long long j, float v) {
+  *d.p = v;
+  if (d.sh) *d.sh = v;
+  if (d.tcw) tcw_write(d.tcw, d.tcw_kind, j, v);
 }
 
 __device__ __forceinline__ float grad_at(const BlockTable& bt, int p, long long i, long long j) {
@@ -800,21 +834,49 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     has_col = rr < tile.n && c < bt.out[p];
     j = (long long)(tile.j0 + rr) * bt.out[p] + c;
   }
-  const float cur = (has_col && mode == 0) ? params[bt.param_off[p] + j] : 0.0f;
+  // the parameter is not written by the per-example kernel: read before the
+  // wait, with the addresses of its copies
+  ParamDst dst{nullptr, nullptr, nullptr, 0};
+  if (has_col && mode == 0) dst = param_dst(bt, p, j, params);
+  asm volatile("" : "+l"(dst.p), "+l"(dst.sh), "+l"(dst.tcw), "+r"(dst.tcw_kind));
+  const float cur = dst.p ? *dst.p : 0.0f;
+  // pre-clipped row groups (bt.rows) are summed with unit factors
+  const bool pre = bt.kind[p] == 0 && bt.rows[p] > 0;
+  const int nrow = pre ? bt.rows[p] : U;
+  const int rows = (nrow + kAggWarps - 1) / kAggWarps;
+  const int i0 = min(nrow, warp * rows), i1 = min(nrow, i0 + rows);
+  float* norms_cta = tile_id == 0 ? L.norms_out : nullptr;
+  // the block's row sources, materialised before the wait
+  const float* rbase = bt.base[p];
+  const float* abase = bt.a[p];
+  long long rstride = bt.stride[p], astride = bt.a_stride[p];
+  int outp = bt.out[p];
+  asm volatile("" : "+l"(rbase), "+l"(abase), "+l"(rstride), "+l"(astride), "+r"(outp));
+  if constexpr (!kCoherent) {
+    // address translation of the first rows ahead of the wait (L2 prefetch:
+    // no data enters L1 before the producer is done)
+    if (i0 < i1) {
+      const float* r0 = bt.kind[p] == 0 ? rbase + tile.j0 + (long long)i0 * rstride
+                                        : rbase + (long long)i0 * rstride;
+      asm volatile("prefetch.global.L2 [%0];" :: "l"(r0));
+    }
+    // Programmatic dependent launch: the tile decode above (dependent reads of
+    // the launch's constant bank, cold at every replay) overlaps the
+    // per-example kernel's tail; everything below reads its outputs.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    PGB_MARK(PGB_TRACE_AGG + 8 * tile_id + 5);
+  }
   const float pre_noise =
       (has_col && mode == 0 && L.noise && a.add_noise) ? agg_ld<kCoherent>(L.noise + bt.param_off[p] + j)
                                                        : 0.0f;
   const bool failed = L.err && agg_ld<kCoherent>(&L.err->code) != 0;
-  const int rows = (U + kAggWarps - 1) / kAggWarps;
-  const int i0 = min(U, warp * rows), i1 = min(U, i0 + rows);
-  float* norms_cta = tile_id == 0 ? L.norms_out : nullptr;
 
   if (bt.kind[p] == 0) {
     // ---- materialised rows: 4 columns per lane ----
     const int c0 = 4 * lane;
     const int ncol = max(0, min(4, tile.n - c0));
-    const long long stride = bt.stride[p];
-    const float* base = bt.base[p] + tile.j0 + c0;
+    const long long stride = rstride;
+    const float* base = rbase + tile.j0 + c0;
     const bool vec = ncol == 4 && (stride & 3) == 0 &&
                      (reinterpret_cast<uintptr_t>(base) & 15) == 0;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -836,7 +898,14 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
       }
     };
     load(i0);  // in flight while the clip factors are computed
+#ifdef PGB_TRACE
+    if (!kCoherent && tid == 0) {  // timestamp once the first rows have arrived
+      if (__float_as_uint(v[0][0]) == 0x7fc00001u) asm volatile("trap;");
+      PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 6, 0);
+    }
+#endif
     agg_prologue<kCoherent>(L, s_sh, norms_cta, cnt_sh, tid);
+    if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 7, 0);
     agg_sync(bar_id);
     if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 1, 0);
     for (int ib = i0; ib < i1; ib += kBatch) {
@@ -844,7 +913,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
         if (ib + u < i1) {
-          const float s = s_sh[ib + u];
+          const float s = pre ? 1.0f : s_sh[ib + u];
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(v[u][c], s));
         }
@@ -857,13 +926,13 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     // Per chunk of kAggChunk units the warp issues every load at once: d_ic
     // into registers (lane = c), the a_i[r0 .. r0+15] rows through a
     // per-warp shared staging area (read back as broadcasts).
-    const int out = bt.out[p];
+    const int out = outp;
     const int c = tile.c0 + lane;
     const bool cok = c < out;
     const int nr = tile.n;
-    const float* A = bt.a[p] + tile.j0;
-    const float* D = bt.base[p] + (cok ? c : 0);
-    const long long as = bt.a_stride[p], ds = bt.stride[p];
+    const float* A = abase + tile.j0;
+    const float* D = rbase + (cok ? c : 0);
+    const long long as = astride, ds = rstride;
     float* a_st = s_sh + ((U + 3) & ~3) + warp * (kAggChunk * kAggRows);
     float acc[kAggRows];
 #pragma unroll
@@ -943,7 +1012,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
   }
   sum = __fmul_rn(sum, a.inv_units);
   if (failed) return;
-  write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
+  param_store(dst, j, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
 }
 
 __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
@@ -951,10 +1020,8 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   __shared__ float part_sh[kAggWarps][kAggRows * 32];
   __shared__ int cnt_sh[kAggWarps];
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
-  // Programmatic dependent launch: this grid may be resident before the
-  // per-example kernel has finished; everything below reads its outputs.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 5);
+  // programmatic dependent launch: this grid may be resident before the
+  // per-example kernel has finished; agg_tile_run waits for it
   agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
 }

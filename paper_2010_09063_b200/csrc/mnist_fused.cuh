@@ -78,6 +78,8 @@ struct Params {
   float* st_c1w;        // (B, 1024)   per-example conv1 dW
   float* st_c1b;        // (B, 16)
   float* st_c2w;        // (B, 8192)
+  float* c2_pairs;      // tc_kernel, optional: ((B+1)/2, 8192) clipped pair rows of conv2 W
+                        // written instead of st_c2w (the step's aggregation follows)
   float* st_c2b;        // (B, 32)
   float* a2;            // (B, 512)    fc1 input
   float* dz1;           // (B, 32)     fc1 output cotangent (= fc1 bias grad)
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   const float* gb3 = W + prm.off[5];
   const float* gW4 = W + prm.off[6];
   const float* gb4 = W + prm.off[7];
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 0);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 0);
   // let the aggregation grid be scheduled as SMs free up (it waits with
   // griddepcontrol.wait for this grid's results)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -219,11 +221,11 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     if (!(r >= 0 && r < H0 && c >= 0 && c < H0)) S.xs[i] = 0.0f;
   }
   __syncthreads();  // barrier initialised before anyone waits on it
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 1);
   mbar_wait0(&S.bar[0]);
   for (int i = t; i < H0 * H0; i += NT) S.xs[(i / H0 + 3) * XS + i % H0 + 3] = S.u1.xstage[i];
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 2);
 
   // ---- conv1 + relu: thread = (two horizontally adjacent positions, 4 channels)
   // Per kernel row u the two 8-tap windows share one 10-value input segment;
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     }
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 3);
 
   // ---- maxpool 2x2/2 (first max in window order, kernels.hpp:377-396) -------
   for (int i = t; i < D1 * PO * PO; i += NT) {
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.pidx[i] = (unsigned char)slot;
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 4);
 
   // ---- conv2 im2col: buf[k][pos], k = (c,u,v), pos = (oy,ox) -------------
   // 16-byte chunks of a row are XOR-swizzled by (k >> 1) & 3 (im2col_at), so
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.buf[im2col_at(k, pos)] = S.up.p1[c * PO * PO + (oy + u) * PO + ox + v];
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 5);
 
   // ---- conv2 + relu: lane = out channel, warp = (K slice of 32, 8 positions)
   mbar_wait0(&S.bar[1]);
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     for (int p = 0; p < 8; ++p) S.u1.part[(ks * NP2 + ph * 8 + p) * D2 + d] = acc[p];
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 6);
   {  // i = pos*32 + d
     const int d = t % D2, p = t / D2;
     float s = 0.0f;
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.a2[d * NP2 + p] = fmaxf(s + S.b2[d], 0.0f);
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 7);
 
   // ---- fc1 (512->32) + relu: lane = unit, warp = 32-row slice -------------
   // The warp's 32x32 slice of W3 (coalesced rows) stays in registers for the
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.u1.z1[warp * H1 + lane] = s0 + s1;
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 8);
   if (warp == 0) {
     // fc1 bias + relu, fc2 (32->10), softmax cross-entropy (kernels.hpp:516-566)
     // and dz1 = (W4 dz2) * [h > 0]. Lane j holds h_j; the 10 logits are
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     }
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 9);
 
   // ---- fc1 backward data: da2[i] = W3[i,:] . dz1, relu mask -> dc2 --------
   // From the register-resident W3 slice: products W3[r][lane] * dz1[lane],
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.dc2t[i] = v;  // [d][pos] == flatten order
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 10);
 
   double sq = 0.0;  // this thread's share of ||g_i||^2
   const size_t bo = (size_t)b;
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     sq = fma((double)s, (double)s, sq);
   }
   __syncthreads();  // buf (patches) is overwritten with dcols below
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 11);
 
   // ---- conv2 backward data: dcols[pos][(u,v),c] = sum_d W2[d][c,u,v] dc2[pos][d]
   // thread = (k, half of the positions), lanes on consecutive k: column k of
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     S.up.dp1[c * PO * PO + r] = s;
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 13);
   // maxpool backward (route to the first max) + relu mask on a1 -> d1 [pos][d]
   // Thread t always has channel d = t % 16 (NT % 16 == 0), so it also keeps a
   // partial of the conv1 bias gradient sum_pos d1[pos][d].
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
   b1part += __shfl_xor_sync(0xffffffffu, b1part, 16);
   if (lane < D1) S.b1red[warp][lane] = b1part;
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 14);
 
   // ---- conv1 per-example dW: thread = (2 taps, 8 channels, 1/8 of the rows)
   // Taps (u, v) and (u + 4, v) share every d1 load; the 8 row groups are
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     if (rg < 2) add(S.a1, rg);
     if (rg == 1) put(S.u1.d1, 0);
     __syncthreads();
-    PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
+    PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 15);
     if (rg == 0) {
       add(S.u1.d1, 0);
       float* out = prm.st_c1w + bo * (D1 * K1 * K1);
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
 #pragma unroll
     for (int q = 0; q < 5; ++q) S.red5[q][warp] = v5[q];
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 16);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 16);
   if (t == 0) {
     double r5[5] = {0, 0, 0, 0, 0};
     for (int w = 0; w < NW; ++w)
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(NT, 2) fused_kernel(Params prm) {
     prm.norms[b] = nrm;
     prm.scale[b] = nrm > C ? __fdiv_rn(C, nrm) : 1.0f;
     prm.clipped[b] = nrm > C ? 1 : 0;
-    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
+    PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 23);
   }
 }
 

@@ -81,6 +81,7 @@ struct TcSmem {
   float yb[2];
   float b1red[2][NW][D1];
   double red5[2][5][NW];
+  float scl[2];  // the pair's clip factors (conv2 pair rows)
   uint64_t bar[4];             // 0: images + conv1 W, 1: conv2 W, 2: conv2 W^T, 3: MMA commits
   uint32_t tmem;
   unsigned char pidx[2][D1 * PO * PO];
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   const float* gW3 = W + prm.off[4];
   const float* tcw = prm.tcw;
   float* regA = S.regA;
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 0);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 0);
   asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp == 0) tc::tmem_alloc(&S.tmem, 512);
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem;
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 21);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 21);
   tc::mbar_wait(&S.bar[0], 0);
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 22);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 22);
 
   // ---- the Y operand of conv1 forward ----------------------------------------
   // Y[ex][hl][par][R = 2r + h][c] = xpad[r][c + 2 par + 4 h]
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::fence_proxy_async();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 1);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 1);
 
   // ---- conv1 forward on the tensor cores ------------------------------------
   // D[(oy, e)][n] for output column ox = 2e + par; K step u = kernel row u:
@@ -233,11 +234,11 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
         if (2 * jp + 1 < prm.size[p]) dst[1] = n1;
       }
     }
-    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 17, 128);
+    PGB_MARK_T(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 17, 128);
   }
   tc::mbar_wait(&S.bar[3], 0);
   tc::fence_after_sync();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 2);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 2);
 
   // ---- conv1 bias + relu + maxpool 2x2/2 straight from TMEM -----------------
   // Thread (quadrant q, lane) holds row m = 32q + lane = (oy = 4q + lane/8,
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::fence_before_sync();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 3);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 3);
 
   // ---- conv2 im2col as the B operand: rows hl*32 + pair position, K = (c,u,v)
   // regA[kmaj(32 hl + 16 ex + pos, k, 128, 1024)]; 32 lanes fill one core.
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::fence_proxy_async();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 4);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 4);
 
   // ---- conv2 forward: one MMA per K step computes all four products ------
   // D[hl_a*32 + d][hl_b*32 + pair position] = [Whi; Wlo] . [Phi | Plo]^T
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
                  :: "r"(smem_addr(&S.bar[2])), "r"(65536u) : "memory");
     bulk_g2s(S.w2, tcw + TCW_W2T, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[2]));
   }
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 5);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 5);
   // M = 64 accumulator: row m at lane m % 16 + 32 (m / 16): quadrants 0, 1
   // hold the hi rows of d = 16q + lane, quadrants 2, 3 the lo rows. Warp
   // (q, g) reads columns 4g.. and 32 + 4g.. (the hi and lo halves of N).
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     }
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 6);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 6);
 
   // ---- fc1 (512->32): lane = unit, warp = 32-row slice -------------------
   if (has) {
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     S.z1[ex][wh][lane] = s0 + s1;
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 7);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 7);
 
   if (wh == 0) {
     if (has) {
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
       for (int cc = 0; cc < NC; ++cc) g1 = fmaf(S.w4[lane * NC + cc], __shfl_sync(0xffffffffu, g, cc), g1);
       S.dz1[ex][lane] = hv > 0.0f ? g1 : 0.0f;
     }
-    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 16, 0);
+    PGB_MARK_T(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 16, 0);
   } else if (has) {
     // the im2col again, transposed (A of conv2 dW): rows k, K = position,
     // regA[(2 ex + hl) * 4096 + kmaj(k, pos, 128, 4096)]
@@ -435,11 +436,11 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
       dst[kg * 32 + pq * 1024] = hi;
       dst[4096 + kg * 32 + pq * 1024] = lo;
     }
-    PGB_MARK_T(PGB_TRACE_FUSED + 24 * blockIdx.x + 18, 32);
+    PGB_MARK_T(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 18, 32);
   }
   tc::fence_proxy_async();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 8);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 8);
 
   // ---- fc1 backward data + relu mask -> dc2 (both UMMA layouts, hi/lo) ----
   if (has) {
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::fence_proxy_async();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 9);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 9);
 
   // ---- conv2 dW (per example) and conv2 dX (pair) on the tensor cores ------
   // issuers 0, 1: dX tile 0, 1 (pair: D[k2][pos], 4 K steps over d);
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::mbar_wait(&S.bar[3], 0);
   tc::fence_after_sync();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 10);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 10);
 
   // conv2 dW -> stacks: the half of example ex reads its own accumulators;
   // warp (q, tile, column half), row k = 128 tile + 32 q + lane
@@ -538,7 +539,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float v = m8[j] + c8[j];
-          out[(ch * 16 + hh * 8 + j) * KC2 + k] = v;
+          if (!prm.c2_pairs) out[(ch * 16 + hh * 8 + j) * KC2 + k] = v;
           sq = fma((double)v, (double)v, sq);
         }
       }
@@ -564,7 +565,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::fence_before_sync();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 11);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 11);
 
   // conv1-output cotangent as the B operand of conv1 dW: rows hl*16 + d,
   // K = oy*16 + ox (ox 14, 15 zero), kmaj(., ., 128, 512): 7168 floats/example
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     }
   }
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 12);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 12);
   // maxpool backward (first max) + relu mask (the routed element is the
   // pooled max, so relu' = [p1 > 0]) -> d1 as a UMMA operand; conv1 bias
   // partials. Meanwhile the image view Z for conv1 dW (below).
@@ -640,7 +641,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   if (lane < D1) S.b1red[ex][wh][lane] = b1part;
   tc::fence_proxy_async();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 13);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 13);
 
   // ---- conv1 per-example dW on the tensor cores ----------------------------
   // D[(u, hl, c)][n] = sum_pos Z . [d1 hi | d1 lo]^T (M = 128, N = 32); K step
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   }
   tc::mbar_wait(&S.bar[3], 1);
   tc::fence_after_sync();
-  PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 14);
+  PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 14);
   {
     // warp (q, dq) of half ex: row m = 32q + lane = (u = m/16, hl = m/8 % 2,
     // c = m % 8); 4 channels d = 4dq.. from both N halves, hl rows via lane^8
@@ -731,8 +732,8 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     for (int q = 0; q < 5; ++q) S.red5[ex][q][wh] = v5[q];
   tc::fence_before_sync();
   __syncthreads();
-  PGB_MARK_BAR(PGB_TRACE_FUSED + 24 * blockIdx.x + 15);
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 15);
+  if (!prm.c2_pairs && warp == 0) tc::tmem_dealloc(tmem, 512);
   if (tt == 0 && has) {
     double r5[5] = {0, 0, 0, 0, 0};
     for (int w = 0; w < NW; ++w)
@@ -746,7 +747,39 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     prm.norms[b] = nrm;
     prm.scale[b] = nrm > C ? __fdiv_rn(C, nrm) : 1.0f;
     prm.clipped[b] = nrm > C ? 1 : 0;
-    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 23);
+    S.scl[ex] = prm.scale[b];
+    PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 23);
+  }
+
+  // ---- conv2 W as clipped pair rows ----------------------------------------
+  // fl(g_2c s_2c) + fl(g_2c+1 s_2c+1) for the CTA's two examples, re-read from
+  // the dW accumulators (untouched since): the aggregation then sums half as
+  // many rows of the step's largest block. warp (q, tile, 8-channel group)
+  if (prm.c2_pairs) {
+    __syncthreads();
+    const int q = warp & 3, g = warp >> 2, tl = g >> 2, cg = g & 3;
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + 128 + (uint32_t)(tl * 64 + cg * 8);
+    float m0[8], c0[8], m1[8], c1[8];
+    tc::tmem_ld8(base, m0);
+    tc::tmem_ld8(base + 32, c0);
+    const bool two = nex > 1;
+    if (two) {
+      tc::tmem_ld8(base + 128, m1);
+      tc::tmem_ld8(base + 128 + 32, c1);
+    }
+    const float s0 = S.scl[0], s1 = two ? S.scl[1] : 0.0f;
+    const int k = tl * 128 + q * 32 + lane;
+    float* out = prm.c2_pairs + (size_t)blockIdx.x * (D2 * KC2);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = __fmul_rn(m0[j] + c0[j], s0);
+      if (two) v = __fadd_rn(v, __fmul_rn(m1[j] + c1[j], s1));
+      out[(cg * 8 + j) * KC2 + k] = v;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
+    PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 24);
   }
 
   // ---- the step's aggregation, in-kernel ----------------------------------
@@ -754,9 +787,9 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   // halves run the aggregation tiles of aggregate_kernel (clipped sum in a
   // fixed order, noise, mean, update) on the per-example outputs above.
   if (prm.agg_tiles > 0) {
-    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 19);
+    PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 19);
     grid_barrier(prm.grid_ctr);
-    PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 20);
+    PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 20);
     float* s_sh = regA + ex * 4096;  // clip factors + factored-row staging
     auto part_sh = reinterpret_cast<float(*)[kAggRows * 32]>(regA + 8192 + ex * 4096);
     int* cnt_sh = reinterpret_cast<int*>(regA + 16384) + ex * kAggWarps;
@@ -765,7 +798,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     // consecutive, so they land on different SMs)
     for (int tile = blockIdx.x + ex * gridDim.x; tile < prm.agg_tiles; tile += 2 * gridDim.x)
       agg_tile_run<true, 8>(agg, tile, tt, 1 + ex, s_sh, part_sh, cnt_sh);
-    if (ex == 0) PGB_MARK(PGB_TRACE_FUSED + 24 * blockIdx.x + 21);
+    if (ex == 0) PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 21);
   }
 }
 

@@ -46,7 +46,8 @@ __device__ unsigned long long* g_trace = nullptr;
 #endif
 
 // slot layout: aggregate CTA b phase p -> kTraceAgg + 8b + p;
-//              fused MNIST CTA b phase p -> kTraceFused + 24b + p
+//              fused MNIST CTA b phase p -> kTraceFused + 32b + p
 #define PGB_TRACE_AGG 0
 #define PGB_TRACE_FUSED 40000
-#define PGB_TRACE_SLOTS (40000 + 24 * 4096)
+#define PGB_FUSED_SLOTS 32
+#define PGB_TRACE_SLOTS (40000 + PGB_FUSED_SLOTS * 4096)

@@ -21,7 +21,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2010_09063_b200 as P  # noqa: E402
 from paper_2010_09063_b200 import _lib  # noqa: E402
 
-AGG, FUSED, SLOTS = 0, 40000, 40000 + 24 * 4096
+AGG, FUSED, NF = 0, 40000, 32
+SLOTS = FUSED + NF * 4096
 L = _lib.lib
 if not hasattr(L, "pgb_debug_trace"):
     sys.exit("not a trace build (PGB_TRACE=1 python paper_2010_09063_b200/build.py)")
@@ -39,11 +40,15 @@ P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 7)
 buf = np.zeros(SLOTS, np.int64)
 _lib.check(L.pgb_debug_trace(C.c_void_p(buf.ctypes.data), SLOTS))
 
-F = buf[FUSED:FUSED + 24 * B].reshape(B, 24)
+F = buf[FUSED:FUSED + NF * B].reshape(B, NF)
 F = F[F[:, 0] > 0]  # one row per CTA (the tensor-core kernel runs B/2 CTAs)
 t0 = F[:, 0].min()
 marks = sorted([k for k in list(range(16)) + [23] if F[:, k].all()], key=lambda k: F[0, k])
 end = F[:, marks[-1]]
+if F[:, 24].all():
+    print(f"  conv2 pair rows: last CTA done {(F[:, 24].max() - end.max()) / 1e3:.2f} us after its "
+          f"clip factor")
+    end = F[:, 24]
 order = np.argsort(end)
 n = len(F)
 one, two = (order[:30], order[-100:]) if n == B else (order[:n // 2], order[n // 2:])
@@ -80,6 +85,9 @@ if len(A):
                 a = A[m]
                 pc = lambda v: np.percentile(v, [0, 50, 100]).astype(int)  # noqa: E731
                 print(f"  kind {k}: release->loads+scales+sync {pc(a[:, col] - a[:, 5])} ns")
+                if k == 0 and (a[:, 6] > 0).all():
+                    print(f"    first rows arrive {pc(a[:, 6] - a[:, 5])} ns, scales done "
+                          f"{pc(a[:, 7] - a[:, 5])} ns after release")
     for k, col in ((0, 1), (1, 2)):
         m = A[:, col] > 0
         if m.any():

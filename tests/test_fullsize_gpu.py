@@ -203,6 +203,7 @@ def test_mnist_in_kernel_aggregation_matches(P, O, monkeypatch):
     data = P.synth_for_model(desc, 2 * B, 0)
     cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0)
     out = []
+    monkeypatch.setenv("PGB_C2_PAIRS", "0")  # per-example conv2 rows, as in-kernel
     for flag in (None, "1"):
         if flag:
             monkeypatch.setenv("PGB_GRID_SYNC", flag)
@@ -214,6 +215,35 @@ def test_mnist_in_kernel_aggregation_matches(P, O, monkeypatch):
         out.append((model.flat_params(), reps))
     np.testing.assert_array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+def test_mnist_conv2_pair_rows_match_per_example_rows(P, O, monkeypatch):
+    """The step's default: tc_kernel hands conv2 W to the aggregation as
+    clipped pair rows fl(g_2c s_2c) + fl(g_2c+1 s_2c+1). Same norms and clip
+    count as the per-example rows (PGB_C2_PAIRS=0); the update differs only by
+    the association of the fp32 sum (SURVEY 8(d) tolerance), the other blocks
+    bitwise."""
+    B = 255  # odd: the last CTA holds one example
+    desc, od = _mnist(P, O, B)
+    data = P.synth_for_model(desc, B, 3)
+    cfg = P.DpConfig(clip_norm=0.5, noise_multiplier=1.1, learning_rate=0.1, seed=5)
+    p0 = P.build_from_desc(desc, 0).flat_params()
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PGB_C2_PAIRS", flag)
+        model = P.build_from_desc(desc, 0)
+        eng = P.GradEngine(model, P.Strategy.groupconv, B)
+        rep = P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 2)
+        out.append((model.flat_params(), rep))
+    (pa, ra), (pb, rb) = out
+    np.testing.assert_array_equal(ra.pre_clip_norms, rb.pre_clip_norms)
+    assert ra.clipped_count == rb.clipped_count
+    lo = sum(od.blocks[:2])
+    hi = lo + od.blocks[2]  # conv2 W
+    np.testing.assert_array_equal(np.delete(pa, np.s_[lo:hi]), np.delete(pb, np.s_[lo:hi]))
+    delta = np.abs(pa[lo:hi] - p0[lo:hi]).max()
+    assert delta > 0
+    np.testing.assert_allclose(pb[lo:hi], pa[lo:hi], rtol=0, atol=1e-4 * delta)
 
 
 def test_embed_full_size_sparse_step_matches_dense_clipped_sum(P, O):

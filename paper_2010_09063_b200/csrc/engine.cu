@@ -132,6 +132,9 @@ struct Engine {
   bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
   bool agg_in_kernel = false;  // ... and the aggregation after an in-kernel grid barrier
   bool fuse_agg_next = false;  // set by enqueue_step for the fused launch it makes
+  // multi-step graph capture, steps after the first: the tensor-core kernel
+  // follows the previous step's aggregation kernel on the stream
+  bool cap_pdl_tc = false;
   // conv2 W leaves the MNIST kernel as clipped pair rows (PGB_C2_PAIRS=0: per example)
   bool c2_pairs = true;
   bool pairs_next = false;     // ... for the launch enqueue_step is making
@@ -811,7 +814,22 @@ struct Engine {
         prm.grid_ctr = d_grid_ctr;
         prm.agg_tiles = L.plan.tile_start[L.plan.n];
       }
-      mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm, L);
+      if (cap_pdl_tc && pdl_enabled && !fuse_agg_next) {
+        // a programmatic dependent of the previous step's aggregation
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)((B + 1) / 2));
+        cfg.blockDim = dim3(mnist::TNT);
+        cfg.dynamicSmemBytes = sizeof(mnist::TcSmem);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PGB_CUDA(cudaLaunchKernelEx(&cfg, mnist::tc_kernel, prm, L));
+      } else {
+        mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm, L);
+      }
       return mark(s, fuse_agg_next ? "mnist_tc_step" : "mnist_tc");
     }
     mnist::fused_kernel<<<(unsigned)B, mnist::NT, sizeof(mnist::Smem), s>>>(prm);
@@ -1177,11 +1195,13 @@ struct Engine {
         clipped_dst = d_clip_ring + 2 * (sl * C + j);
         cap_step_base = d_step_base + sl;
         cap_step_off = (int)j;
+        cap_pdl_tc = j > 0;
         cap_x_next = j + 1 < C ? d_xc[sl] + (j + 1) * B * in_row : nullptr;
         kernels_last = enqueue_step(stream, d_xc[sl] + j * B * in_row, d_yc[sl] + j * B, 1);
       }
     } catch (...) {
       cap_step_base = nullptr;
+      cap_pdl_tc = false;
       cap_x_next = nullptr;
       cudaStreamEndCapture(stream, &cg.graph);
       if (cg.graph) cudaGraphDestroy(cg.graph);
@@ -1190,6 +1210,7 @@ struct Engine {
     }
     cap_step_base = nullptr;
     cap_step_off = 0;
+    cap_pdl_tc = false;
     cap_x_next = nullptr;
     norms_dst = nd0;
     clipped_dst = cd0;
@@ -1220,6 +1241,7 @@ struct Engine {
         cur_args = a0;
         cap_step_base = d_step_base + kSlots;
         cap_step_off = (int)j;
+        cap_pdl_tc = j > 0;
         cap_xring = xr;
         cap_yring = yr;
         cap_ring_n = n;
@@ -1228,6 +1250,7 @@ struct Engine {
       advance_counter_kernel<<<1, 1, 0, stream>>>(d_step_base + kSlots, C);
     } catch (...) {
       cap_step_base = nullptr;
+      cap_pdl_tc = false;
       cap_xring = cap_yring = nullptr;
       cudaStreamEndCapture(stream, &cg.graph);
       if (cg.graph) cudaGraphDestroy(cg.graph);
@@ -1236,6 +1259,7 @@ struct Engine {
     }
     cap_step_base = nullptr;
     cap_step_off = 0;
+    cap_pdl_tc = false;
     cap_xring = cap_yring = nullptr;
     cap_ring_n = 0;
     PGB_CUDA(cudaStreamEndCapture(stream, &cg.graph));

@@ -1020,6 +1020,8 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
   __shared__ float part_sh[kAggWarps][kAggRows * 32];
   __shared__ int cnt_sh[kAggWarps];
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
+  // the next step's per-example kernel may start its input-only prologue
+  asm volatile("griddepcontrol.launch_dependents;");
   // programmatic dependent launch: this grid may be resident before the
   // per-example kernel has finished; agg_tile_run waits for it
   agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);

@@ -82,7 +82,8 @@ struct TcSmem {
   float b1red[2][NW][D1];
   double red5[2][5][NW];
   float scl[2];  // the pair's clip factors (conv2 pair rows)
-  uint64_t bar[4];             // 0: images + conv1 W, 1: conv2 W, 2: conv2 W^T, 3: MMA commits
+  // 0: images, 1: conv2 W, 2: conv2 W^T, 3: MMA commits, 4: conv1 W + small blocks
+  uint64_t bar[5];
   uint32_t tmem;
   unsigned char pidx[2][D1 * PO * PO];
 };
@@ -117,35 +118,44 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
   PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 0);
   asm volatile("griddepcontrol.launch_dependents;");
 
+  // Everything up to the griddepcontrol.wait below touches only this step's
+  // inputs: when the kernel is a programmatic dependent of the previous
+  // step's aggregation (multi-step graphs), the CTA's start, TMEM allocation,
+  // image load and Y build overlap that kernel's tail. The weights it
+  // updates and the buffers it reads are touched only after the wait.
   if (warp == 0) tc::tmem_alloc(&S.tmem, 512);
   if (t == 0) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) tc::mbar_init(&S.bar[i], 1);
     tc::mbar_init(&S.bar[3], kIssuers);  // every issuer commits once per GEMM phase
+    tc::mbar_init(&S.bar[4], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t img = (uint32_t)(sizeof(float) * H0 * H0 * nex);
-    // images, conv1 W operand, and the small parameter blocks (biases, fc2 W;
-    // b4 as 12 floats for the 16-byte granularity) on one barrier
+    // conv1 W operand and the small parameter blocks (biases, fc2 W; b4 as
+    // 12 floats for the 16-byte granularity) on one barrier
     constexpr uint32_t kSmall = 4u * (D1 + D2 + H1 * NC + H1 + 12);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(smem_addr(&S.bar[0])), "r"(img + 8192u + kSmall) : "memory");
+                 :: "r"(smem_addr(&S.bar[0])), "r"(img) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&S.bar[4])), "r"(8192u + kSmall) : "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(smem_addr(&S.bar[1])), "r"(65536u) : "memory");
     const float *gx, *gy;
     step_inputs(prm, gx, gy);
     bulk_g2s(S.xstage[0], gx + (size_t)b0 * H0 * H0, img, reinterpret_cast<unsigned long long*>(&S.bar[0]));
-    bulk_g2s(regA + OFF_W1C, tcw + TCW_W1C, 8192u, reinterpret_cast<unsigned long long*>(&S.bar[0]));
-    auto* b0bar = reinterpret_cast<unsigned long long*>(&S.bar[0]);
+    // warm L2 with the next step's images of this CTA's pair
+    if (const float* xn = next_inputs(prm))
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   :: "l"(xn + (size_t)b0 * H0 * H0), "r"(img) : "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    auto* b0bar = reinterpret_cast<unsigned long long*>(&S.bar[4]);
+    bulk_g2s(regA + OFF_W1C, tcw + TCW_W1C, 8192u, b0bar);
     bulk_g2s(S.b1, W + prm.off[1], 4u * D1, b0bar);
     bulk_g2s(S.b2, W + prm.off[3], 4u * D2, b0bar);
     bulk_g2s(S.b3, W + prm.off[5], 4u * H1, b0bar);
     bulk_g2s(S.w4, W + prm.off[6], 4u * H1 * NC, b0bar);
     bulk_g2s(S.b4, W + prm.off[7], 4u * 12, b0bar);
     bulk_g2s(S.w2, tcw + TCW_W2C, 65536u, reinterpret_cast<unsigned long long*>(&S.bar[1]));
-    // warm L2 with the next step's images of this CTA's pair
-    if (const float* xn = next_inputs(prm))
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                   :: "l"(xn + (size_t)b0 * H0 * H0), "r"(img) : "memory");
   }
   // the label: loaded now, first used by the loss tail (lane 0 of warp 0 of
   // the half holds it; no barrier waits on the load)
@@ -187,6 +197,9 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
       yb[3 * YBLK + R * YS] = l1;
     }
   }
+  // every thread past this point may read the updated weights or write
+  // buffers the previous step's aggregation reads
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   tc::fence_proxy_async();
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 1);
@@ -202,6 +215,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     tc::fence_after_sync();
     constexpr uint32_t idesc = tc::idesc_tf32(128, 32);
     const int e = warp >> 1, par = warp & 1;
+    tc::mbar_wait(&S.bar[4], 0);
     if (e < nex) {
       const uint32_t wb = tc::smem_u32(regA + OFF_W1C);
       const uint32_t yh = tc::smem_u32(regA + ((e * 2 + 0) * 2 + par) * YBLK);
@@ -237,6 +251,7 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     PGB_MARK_T(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 17, 128);
   }
   tc::mbar_wait(&S.bar[3], 0);
+  tc::mbar_wait(&S.bar[4], 0);  // the small blocks (biases, fc2 W)
   tc::fence_after_sync();
   PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 2);
 

@@ -35,8 +35,27 @@ eng = P.GradEngine(model, P.Strategy.groupconv, B)
 cfg = P.DpConfig(1.0, 1.1, 0.1, 1, 0)
 for s in range(5):
     P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, s)
-_lib.check(L.pgb_debug_trace(None, 0))
-P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 7)
+GRAPH = "--graph" in sys.argv
+if GRAPH:
+    # the last step of a static 8-step graph (the bench path: tc_kernel a
+    # programmatic dependent of the previous step's aggregation)
+    import torch
+    dx = torch.from_numpy(data.inputs).cuda()
+    dy = torch.from_numpy(data.labels).cuda()
+    n = C.c_int64()
+    ccfg = cfg.to_c()
+    _lib.check(L.pgb_run_steps_device(eng.handle, C.c_void_p(dx.data_ptr()),
+                                      C.c_void_p(dy.data_ptr()), 1, 16, C.byref(ccfg), 0,
+                                      C.byref(n)))
+    _lib.check(L.pgb_synchronize(eng.handle, None, None))
+    _lib.check(L.pgb_debug_trace(None, 0))
+    _lib.check(L.pgb_run_steps_device(eng.handle, C.c_void_p(dx.data_ptr()),
+                                      C.c_void_p(dy.data_ptr()), 1, 8, C.byref(ccfg), 16,
+                                      C.byref(n)))
+    _lib.check(L.pgb_synchronize(eng.handle, None, None))
+else:
+    _lib.check(L.pgb_debug_trace(None, 0))
+    P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 7)
 buf = np.zeros(SLOTS, np.int64)
 _lib.check(L.pgb_debug_trace(C.c_void_p(buf.ctypes.data), SLOTS))
 
@@ -45,6 +64,23 @@ F = F[F[:, 0] > 0]  # one row per CTA (the tensor-core kernel runs B/2 CTAs)
 t0 = F[:, 0].min()
 marks = sorted([k for k in list(range(16)) + [23] if F[:, k].all()], key=lambda k: F[0, k])
 end = F[:, marks[-1]]
+if GRAPH and F[:, 25].all():
+    rel = F[:, 25].min()
+    pc = lambda v: np.percentile(v, [0, 50, 100]).astype(int)  # noqa: E731
+    print(f"  graph step: CTA start {pc(F[:, 0] - rel)} ns, alloc+barrier {pc(F[:, 21] - rel)}, "
+          f"images {pc(F[:, 22] - rel)}, wait returns {pc(F[:, 25] - rel)}, phase 1 "
+          f"{pc(F[:, 1] - rel)} ns relative to the first wait return")
+    print(f"  graph step: conv1 done {pc(F[:, 2] - rel)}, conv2 done {pc(F[:, 5] - rel)}, "
+          f"last mark {pc(end - rel)} ns relative to the first wait return")
+if F[:, 26].all() and F[:, 27].all():
+    pc = lambda v: np.percentile(v, [0, 50, 100]).astype(int)  # noqa: E731
+    print(f"  CTA start: last thread starts {pc(F[:, 26] - F[:, 0])} ns after thread 0, arrives at "
+          f"the first barrier {pc(F[:, 27] - F[:, 0])}; thread 0 arrives {pc(F[:, 28] - F[:, 0])}, "
+          f"barrier done {pc(F[:, 21] - F[:, 0])}")
+    if F[:, 29].all() and F[:, 30].all():
+        print(f"  thread 0: TMEM alloc done {pc(F[:, 29] - F[:, 0])}, image address "
+              f"{pc(F[:, 30] - F[:, 0])}, image copy issued {pc(F[:, 31] - F[:, 0])}, images "
+              f"arrive {pc(F[:, 22] - F[:, 0])} ns after start")
 if F[:, 24].all():
     print(f"  conv2 pair rows: last CTA done {(F[:, 24].max() - end.max()) / 1e3:.2f} us after its "
           f"clip factor")
@@ -73,6 +109,9 @@ if F[:, 19].all() and F[:, 21].all():
 A = buf[AGG:AGG + 8 * 4096].reshape(4096, 8)
 A = A[A[:, 0] > 0]
 if len(A):
+    if GRAPH and F[:, 25].all():
+        print(f"  graph step: aggregation ends {(A[:, 4].max() - F[:, 25].min()) / 1e3:.2f} us after "
+              f"the first wait return of the tensor-core kernel")
     print(f"aggregate: {len(A)} CTAs; first start {(A[:, 0].min() - end.max()) / 1e3:.2f} us after "
           f"the fused kernel's last CTA, last end {(A[:, 4].max() - end.max()) / 1e3:.2f} us after")
     if (A[:, 5] > 0).all():

@@ -834,12 +834,13 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     has_col = rr < tile.n && c < bt.out[p];
     j = (long long)(tile.j0 + rr) * bt.out[p] + c;
   }
-  // the parameter is not written by the per-example kernel: read before the
-  // wait, with the addresses of its copies
+  // the addresses of the parameter and its copies, resolved before the wait
+  // (the parameter itself only after it: with the next step's per-example
+  // kernel a programmatic dependent of this one, this grid can start while
+  // the previous step's aggregation is still updating these columns)
   ParamDst dst{nullptr, nullptr, nullptr, 0};
   if (has_col && mode == 0) dst = param_dst(bt, p, j, params);
   asm volatile("" : "+l"(dst.p), "+l"(dst.sh), "+l"(dst.tcw), "+r"(dst.tcw_kind));
-  const float cur = dst.p ? *dst.p : 0.0f;
   // pre-clipped row groups (bt.rows) are summed with unit factors
   const bool pre = bt.kind[p] == 0 && bt.rows[p] > 0;
   const int nrow = pre ? bt.rows[p] : U;
@@ -866,6 +867,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     asm volatile("griddepcontrol.wait;" ::: "memory");
     PGB_MARK(PGB_TRACE_AGG + 8 * tile_id + 5);
   }
+  const float cur = dst.p ? __ldcg(dst.p) : 0.0f;
   const float pre_noise =
       (has_col && mode == 0 && L.noise && a.add_noise) ? agg_ld<kCoherent>(L.noise + bt.param_off[p] + j)
                                                        : 0.0f;

@@ -194,6 +194,39 @@ def test_mnist_run_steps_device_matches_step_calls(P, O):
     np.testing.assert_array_equal(out[0], out[1])
 
 
+def test_mnist_long_graph_run_matches_step_calls(P, O):
+    """Cross-step overlap (each step's per-example kernel a programmatic
+    dependent of the previous step's aggregation, whose CTAs may start while
+    the one before is still updating) leaves no trace: 256 steps through the
+    static multi-step graphs equal the same steps one call at a time, bitwise."""
+    torch = pytest.importorskip("torch")
+    from paper_2010_09063_b200 import _lib
+    B, NB, STEPS = 256, 3, 256
+    desc, od = _mnist(P, O, B)
+    data = P.synth_for_model(desc, B * NB, 1)
+    dx = torch.from_numpy(data.inputs).cuda()
+    dy = torch.from_numpy(data.labels).cuda()
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.05, seed=9).to_c()
+    out = []
+    for mode in ("steps", "calls"):
+        model = P.build_from_desc(desc, 0)
+        eng = P.GradEngine(model, P.Strategy.groupconv, B)
+        if mode == "steps":
+            n = C.c_int64()
+            _lib.check(_lib.lib.pgb_run_steps_device(eng.handle, C.c_void_p(dx.data_ptr()),
+                                                     C.c_void_p(dy.data_ptr()), NB, STEPS,
+                                                     C.byref(cfg), 0, C.byref(n)))
+        else:
+            for i in range(STEPS):
+                b = i % NB
+                _lib.check(_lib.lib.pgb_dpsgd_step_device(
+                    eng.handle, C.c_void_p(dx.data_ptr() + b * B * 784 * 4),
+                    C.c_void_p(dy.data_ptr() + b * B * 4), C.byref(cfg), i))
+        _lib.check(_lib.lib.pgb_synchronize(eng.handle, None, None))
+        out.append(eng.get_flat_params())
+    np.testing.assert_array_equal(out[0], out[1])
+
+
 def test_mnist_in_kernel_aggregation_matches(P, O, monkeypatch):
     """PGB_GRID_SYNC=1 (aggregation inside the tensor-core kernel after a grid
     barrier) runs the same tiles in the same order as the aggregation kernel:

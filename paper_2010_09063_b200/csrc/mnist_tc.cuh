@@ -683,6 +683,44 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
     }
     tc::commit(&S.bar[3]);
   }
+  // while the tensor core runs: conv1 bias, the dense factors and their norm terms
+  if (tt < D1 && has) {  // conv1 bias
+    float s = 0.0f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += S.b1red[ex][w][tt];
+    prm.st_c1b[bo * D1 + tt] = s;
+    sq = fma((double)s, (double)s, sq);
+  }
+
+  // ---- dense factors for the ghost-norm blocks + their norm terms ----------
+  double a2sq = 0.0, hsq = 0.0, dz1sq = 0.0, dz2sq = 0.0;
+  if (has) {
+    const float v = S.a2[ex][tt];
+    prm.a2[bo * F1 + tt] = v;
+    a2sq = (double)v * v;
+    if (tt < H1) {
+      const float hv = S.h[ex][tt], g = S.dz1[ex][tt];
+      prm.h[bo * H1 + tt] = hv;
+      prm.dz1[bo * H1 + tt] = g;
+      hsq = (double)hv * hv;
+      dz1sq = (double)g * g;
+    }
+    if (tt < NC) {
+      const float g = S.dz2[ex][tt];
+      prm.dz2[bo * NC + tt] = g;
+      dz2sq = (double)g * g;
+    }
+  }
+  {
+    double v4[4] = {a2sq, hsq, dz1sq, dz2sq};
+    const int nq = wh == 0 ? 4 : 1;  // the h / dz terms live in warp 0 of the half
+    for (int q = 0; q < nq; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v4[q] += __shfl_xor_sync(0xffffffffu, v4[q], o);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) S.red5[ex][1 + q][wh] = v4[q];
+  }
   tc::mbar_wait(&S.bar[3], 1);
   tc::fence_after_sync();
   PGB_MARK(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 14);
@@ -713,41 +751,9 @@ __global__ void __launch_bounds__(TNT, 1) tc_kernel(Params prm, const AggLaunch 
       }
     }
   }
-  if (tt < D1 && has) {  // conv1 bias
-    float s = 0.0f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) s += S.b1red[ex][w][tt];
-    prm.st_c1b[bo * D1 + tt] = s;
-    sq = fma((double)s, (double)s, sq);
-  }
-
-  // ---- dense factors for the ghost-norm blocks + their norm terms ----------
-  double a2sq = 0.0, hsq = 0.0, dz1sq = 0.0, dz2sq = 0.0;
-  if (has) {
-    const float v = S.a2[ex][tt];
-    prm.a2[bo * F1 + tt] = v;
-    a2sq = (double)v * v;
-    if (tt < H1) {
-      const float hv = S.h[ex][tt], g = S.dz1[ex][tt];
-      prm.h[bo * H1 + tt] = hv;
-      prm.dz1[bo * H1 + tt] = g;
-      hsq = (double)hv * hv;
-      dz1sq = (double)g * g;
-    }
-    if (tt < NC) {
-      const float g = S.dz2[ex][tt];
-      prm.dz2[bo * NC + tt] = g;
-      dz2sq = (double)g * g;
-    }
-  }
-  double v5[5] = {sq, a2sq, hsq, dz1sq, dz2sq};
-  const int nq = wh == 0 ? 5 : 2;  // the h / dz terms live in warp 0 of the half
-  for (int q = 0; q < nq; ++q)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v5[q] += __shfl_xor_sync(0xffffffffu, v5[q], o);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 5; ++q) S.red5[ex][q][wh] = v5[q];
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) S.red5[ex][0][wh] = sq;
   tc::fence_before_sync();
   __syncthreads();
   PGB_MARK_BAR(PGB_TRACE_FUSED + PGB_FUSED_SLOTS * blockIdx.x + 15);

@@ -14,5 +14,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tc_
    -o $OUT/prof python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $OUT/ncu_full.log 2>&1
 PGB_TRACE=1 python paper_2010_09063_b200/build.py > /dev/null 2>&1
 timeout 300 python scripts/trace_phases.py > $OUT/trace.txt 2>&1
+timeout 300 python scripts/trace_phases.py --graph > $OUT/trace_graph.txt 2>&1
 for f in $OUT/*.log; do tail -n 2 $f; done
 cat $OUT/bench.json

@@ -263,19 +263,23 @@ def conv_gemm_flops(desc, B):
     return total
 
 
-def aggregate_bytes(desc, B, fused):
+def aggregate_bytes(desc, B, fused, c2_pairs=False):
     """Bytes the aggregation kernel must read/write: per-example gradient
-    sources (materialised rows: B*|p|*4; factored dense blocks: B*(in+out)*4),
-    the parameters (read + write), norms partials."""
+    sources (materialised rows: B*|p|*4; factored dense blocks: B*(in+out)*4;
+    with c2_pairs the MNIST kernel's second conv weight block arrives as
+    ceil(B/2) clipped pair rows), the parameters (read + write), norms partials."""
     from paper_2010_09063_b200 import LayerKind
     total = 0
     pi = 0
+    nconv = 0
     for l in desc.layers:
         if l.kind == LayerKind.dense:
             total += B * (l.in_ + l.out) * 4 + B * l.out * 4
             pi += 2
         elif l.kind == LayerKind.conv:
-            total += B * (l.out * l.in_ * l.k * l.k + l.out) * 4
+            rows = (B + 1) // 2 if (c2_pairs and nconv == 1) else B
+            total += (rows * l.out * l.in_ * l.k * l.k + B * l.out) * 4
+            nconv += 1
             pi += 2
         elif l.kind == LayerKind.embedding:
             total += B * l.in_ * l.out * 4
@@ -439,7 +443,9 @@ def run_ours(args):
                 "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once)",
                 "share_of_step": tc_ms / step_ms, "avg_launch_us": tc_ms * 1e3}
     if "aggregate" in by_name:
-        agg_b = aggregate_bytes(desc, BATCH, fused)
+        agg_b = aggregate_bytes(desc, BATCH, fused,
+                                c2_pairs=("mnist_tc" in by_name and
+                                          os.environ.get("PGB_C2_PAIRS", "1") != "0"))
         am = by_name["aggregate"]
         atraffic, _ = ncu_traffic(args.model, "aggregate_kernel")
         agg = {"kernel": "aggregate", "bound": "hbm", "achieved": agg_b / (am * 1e-3) / 1e9,

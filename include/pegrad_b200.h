@@ -174,6 +174,15 @@ pgb_status pgb_per_example_grads(pgb_engine* e, const float* x, const float* y,
  * items (2)-(3). Any output may be NULL. */
 pgb_status pgb_clipped_sum(pgb_engine* e, const float* x, const float* y, float clip_norm,
                            float* sum_out, float* norms_out, int64_t* clipped_out);
+/* GradEngine::weighted_grad_sum (strategies.hpp:79-83, strategies.cpp:432-450):
+ * sum_i w_i g_i over the batch (P floats, flat parameter order, no update);
+ * w has batch entries. The second pass of the norms-only two-pass step
+ * (dpsgd.cpp:194-230) with w = clip factors. One-process engines. */
+pgb_status pgb_weighted_grad_sum(pgb_engine* e, const float* x, const float* y, const float* w,
+                                 float* sum_out);
+/* GradEngine::batch_grad_sum (strategies.hpp:85-87, strategies.cpp:453-458):
+ * weighted_grad_sum with every weight 1. */
+pgb_status pgb_batch_grad_sum(pgb_engine* e, const float* x, const float* y, float* sum_out);
 /* Forward only: per-example losses (batch) and logits (batch*classes). */
 pgb_status pgb_forward(pgb_engine* e, const float* x, const float* y, float* losses_out,
                        float* logits_out);

@@ -208,6 +208,22 @@ class GradEngine {
     check(pgb_get_params(h_.get(), f.data()));
     m.set_flat(f);
   }
+  // strategies.cpp:432-450 / 453-458: sum_i w_i g_i (flat parameter order)
+  std::vector<float> weighted_grad_sum(const float* x, const float* y, const float* w) const {
+    std::vector<float> out(param_count());
+    check(pgb_weighted_grad_sum(h_.get(), x, y, w, out.data()));
+    return out;
+  }
+  std::vector<float> batch_grad_sum(const float* x, const float* y) const {
+    std::vector<float> out(param_count());
+    check(pgb_batch_grad_sum(h_.get(), x, y, out.data()));
+    return out;
+  }
+  int64_t param_count() const {
+    pgb_engine_info info{};
+    check(pgb_engine_info_get(h_.get(), &info));
+    return info.param_count;
+  }
   int64_t footprint_bytes() const {
     pgb_engine_info info{};
     check(pgb_engine_info_get(h_.get(), &info));

@@ -268,6 +268,8 @@ def ref():
                                                              C.c_int64, C.c_uint64, C.c_int64,
                                                              C.c_void_p, _P(C.c_int64)]
             getattr(L, f"ref_engine_sgd_step_{sfx}").argtypes = [C.c_void_p, ptr, ptr, T]
+            getattr(L, f"ref_engine_weighted_sum_{sfx}").argtypes = [C.c_void_p, ptr, ptr, ptr,
+                                                                     C.c_void_p]
         L.ref_run_bench_f32.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_double, C.c_double, C.c_double, C.c_uint64,
                                         _P(C.c_double)]
@@ -336,12 +338,14 @@ class RefModel:
     def set_params(self, p):
         self._call("engine_set_params", np.ascontiguousarray(p, self.dtype))
 
-    def per_example(self, x, y):
+    def per_example(self, x, y, want_stacks=True):
+        """Stacks (None for want_stacks=False, e.g. the norms-only strategy) and norms."""
         B = self.batch
-        stacks = np.empty(B * self.desc.param_count, self.dtype)
+        stacks = np.empty(B * self.desc.param_count, self.dtype) if want_stacks else None
         norms = np.empty(B, self.dtype)
         self._call("engine_per_example", np.ascontiguousarray(x, self.dtype),
-                   np.ascontiguousarray(y, self.dtype), _ptr(stacks), _ptr(norms))
+                   np.ascontiguousarray(y, self.dtype),
+                   _ptr(stacks) if want_stacks else None, _ptr(norms))
         return stacks, norms
 
     def step(self, x, y, clip, sigma, lr, microbatch=1, seed=0, step=0):
@@ -351,6 +355,14 @@ class RefModel:
                    np.ascontiguousarray(y, self.dtype), clip, sigma, lr, microbatch, seed, step,
                    _ptr(norms), C.byref(n))
         return norms, n.value
+
+    def weighted_grad_sum(self, x, y, w):
+        """GradEngine::weighted_grad_sum (strategies.cpp:432-450), flat."""
+        out = np.empty(self.desc.param_count, self.dtype)
+        self._call("engine_weighted_sum", np.ascontiguousarray(x, self.dtype),
+                   np.ascontiguousarray(y, self.dtype), np.ascontiguousarray(w, self.dtype),
+                   _ptr(out))
+        return out
 
     def sgd_step(self, x, y, lr):
         self._call("engine_sgd_step", np.ascontiguousarray(x, self.dtype),

@@ -298,6 +298,22 @@ int64_t ref_desc_block_size(void* d, int p) {
       auto yt = Tensor<T>::from({B}, std::vector<T>(y, y + B));               \
       sgd_step(e->model, *e->engine, xt, yt, lr);                             \
     });                                                                       \
+  }                                                                           \
+  /* GradEngine::weighted_grad_sum: sum_i w_i g_i, flat parameter order */    \
+  int ref_engine_weighted_sum_##SFX(void* h, const T* x, const T* y,          \
+                                    const T* w, T* out) {                     \
+    return guarded([&] {                                                      \
+      auto* e = static_cast<RefEngine<T>*>(h);                                \
+      const auto& d = e->model.desc;                                          \
+      const int64_t B = e->engine->batch();                                   \
+      const int64_t row = numel(d.input_shape);                               \
+      auto xt = Tensor<T>::from(batch_shape<T>(d, B),                         \
+                                std::vector<T>(x, x + B * row));              \
+      auto yt = Tensor<T>::from({B}, std::vector<T>(y, y + B));               \
+      auto wt = Tensor<T>::from({B}, std::vector<T>(w, w + B));               \
+      flatten_into(e->engine->weighted_grad_sum(xt, yt, wt, e->model.params), \
+                   out);                                                      \
+    });                                                                       \
   }
 
 REF_TYPED(float, f32)

@@ -89,6 +89,9 @@ EXPORTS = {
                                         C.c_void_p]),
     "pgb_clipped_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
                                   C.c_void_p, C.POINTER(C.c_int64)]),
+    "pgb_weighted_grad_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
+    "pgb_batch_grad_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pgb_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pgb_aggregate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(DpConfigC), C.c_int64,
                                 C.c_void_p, C.POINTER(StepReportC)]),

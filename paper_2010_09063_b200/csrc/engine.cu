@@ -234,6 +234,7 @@ struct Engine {
   float* norms_dst = nullptr;
   int* clipped_dst = nullptr;
   float* d_stacks = nullptr;
+  float* d_wts = nullptr;  // (B) weights of pgb_weighted_grad_sum
   float* d_units = nullptr;
   double* d_parts = nullptr;
   float* d_cot[2] = {nullptr, nullptr};
@@ -407,6 +408,7 @@ struct Engine {
     want((void**)&d_step_base, sizeof(long long) * (kSlots + 1));
     want((void**)&d_grid_ctr, sizeof(unsigned long long));
     want((void**)&d_stacks, sizeof(float) * B * P);
+    want((void**)&d_wts, sizeof(float) * B);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
     int64_t max_act = 0;
@@ -1117,6 +1119,30 @@ struct Engine {
     return 1;
   }
 
+  // dpsgd_step's checks (dpsgd.cpp:36-51) plus the norms-only strategy's
+  // microbatch restriction (dpsgd.cpp:194-199)
+  void validate_step(const pgb_dp_config& c) const {
+    validate_dp_config(c, B);
+    if (strategy == PGB_NORMS && c.microbatch != 1)
+      raise(PGB_ERR_CONFIG, "dpsgd_step: the norms-only strategy supports microbatch = 1 only");
+  }
+
+  // sum_i w_i g_i of the batch into d_sum (GradEngine::weighted_grad_sum,
+  // strategies.cpp:432-450): the per-example sources of enqueue_grads summed
+  // by the aggregation kernel with the weights in place of clip factors
+  void enqueue_weighted_sum(cudaStream_t s, const float* x_slot, const float* y_slot,
+                            const float* d_w) {
+    enqueue_grads(s, x_slot, y_slot);
+    const BlockTable t = table_for(x_slot);
+    AggLaunch L = agg_launch(t, nparts, (int)B, 1);
+    L.scales = d_w;
+    L.clip_flags = d_clipflag;
+    L.noise = nullptr;
+    L.norms_out = nullptr;
+    L.clipped_out = nullptr;
+    launch_agg(L, s);
+  }
+
   // ---- step arguments ---------------------------------------------------------
   void push_args(const StepArgs& a) { cur_args = a; }
 
@@ -1393,7 +1419,7 @@ struct Engine {
 
   void step_host(const float* x, const float* y, const pgb_dp_config& c, int64_t step,
                  float* norms_out, pgb_step_report* rep) {
-    validate_dp_config(c, B);
+    validate_step(c);
     if (!x || !y) raise(PGB_ERR_CONTRACT, "null input");
     PGB_CUDA(cudaMemcpyAsync(d_x, x, sizeof(float) * B * in_row, cudaMemcpyHostToDevice,
                              stream));
@@ -1525,7 +1551,7 @@ pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d
   return guarded([&] {
     Engine& en = E(e);
     if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
-    validate_dp_config(*cfg, en.B);
+    en.validate_step(*cfg);
     if (!d_x || !d_y) raise(PGB_ERR_CONTRACT, "null input");
     en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
     en.last_cfg = *cfg;
@@ -1550,7 +1576,7 @@ pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_
     Engine& en = E(e);
     if (!cfg || !d_x || !d_y) raise(PGB_ERR_CONTRACT, "null argument");
     if (n_batches <= 0 || n_steps < 0) raise(PGB_ERR_CONFIG, "run_steps_device: bad counts");
-    validate_dp_config(*cfg, en.B);
+    en.validate_step(*cfg);
     en.last_cfg = *cfg;
     int64_t launches = 0;
     auto batch = [&](int64_t s) {
@@ -1679,6 +1705,41 @@ pgb_status pgb_clipped_sum(pgb_engine* e, const float* x, const float* y, float 
   });
 }
 
+pgb_status pgb_weighted_grad_sum(pgb_engine* e, const float* x, const float* y, const float* w,
+                                 float* sum_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!x || !y || !w || !sum_out) raise(PGB_ERR_CONTRACT, "null argument");
+    if (en.world != 1)
+      raise(PGB_ERR_UNSUPPORTED, "weighted_grad_sum: one-process engines only");
+    PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
+                             cudaMemcpyHostToDevice, en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_y, y, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemcpyAsync(en.d_wts, w, sizeof(float) * en.B, cudaMemcpyHostToDevice,
+                             en.stream));
+    PGB_CUDA(cudaMemsetAsync(en.d_err, 0, sizeof(DevError), en.stream));
+    pgb_dp_config c{1.0f, 0.0f, 1.0f, 1, 0};
+    en.push_args(en.make_args(c, 0, en.d_x, en.d_y));
+    en.enqueue_weighted_sum(en.stream, en.d_x, en.d_y, en.d_wts);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaMemcpyAsync(en.h_err, en.d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                             en.stream));
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+    en.check_device_error();
+    PGB_CUDA(cudaMemcpy(sum_out, en.d_sum, sizeof(float) * en.P, cudaMemcpyDeviceToHost));
+  });
+}
+
+pgb_status pgb_batch_grad_sum(pgb_engine* e, const float* x, const float* y, float* sum_out) {
+  return guarded([&] {
+    Engine& en = E(e);
+    std::vector<float> ones((size_t)en.B, 1.0f);
+    const pgb_status st = pgb_weighted_grad_sum(e, x, y, ones.data(), sum_out);
+    if (st != PGB_OK) raise(st, pgb_last_error());
+  });
+}
+
 pgb_status pgb_forward(pgb_engine* e, const float* x, const float* y, float* losses_out,
                        float* logits_out) {
   return guarded([&] {
@@ -1744,7 +1805,7 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
   return guarded([&] {
     Engine& en = E(e);
     if (!cfg || !x || !y) raise(PGB_ERR_CONTRACT, "null argument");
-    validate_dp_config(*cfg, en.B);
+    en.validate_step(*cfg);
     const int64_t steps = n / en.B;
     if (steps <= 0) raise(PGB_ERR_CONFIG, "run_epoch: fewer examples than one batch");
     const int64_t U = en.B / cfg->microbatch;
@@ -1934,7 +1995,7 @@ pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
   return guarded([&] {
     Engine& en = E(e);
     if (!cfg) raise(PGB_ERR_CONTRACT, "null config");
-    validate_dp_config(*cfg, en.B);
+    en.validate_step(*cfg);
     if (n_steps < 1 || n_steps > 32) raise(PGB_ERR_CONFIG, "profile: 1..32 steps");
     PGB_CUDA(cudaMemcpyAsync(en.d_x, d_x, sizeof(float) * en.B * en.in_row,
                              cudaMemcpyDeviceToDevice, en.stream));

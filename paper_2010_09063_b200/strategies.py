@@ -186,3 +186,22 @@ class GradEngine:
         check(lib.pgb_clipped_sum(self.handle, _lib.ptr(x), _lib.ptr(y), float(clip_norm),
                                   _lib.ptr(out), _lib.ptr(norms), C.byref(n)))
         return out, norms, n.value
+
+    def weighted_grad_sum(self, x, y, w):
+        """sum_i w_i g_i over the batch (P floats, flat parameter order), as
+        GradEngine::weighted_grad_sum (strategies.cpp:432-450)."""
+        x, y = self._inputs(x, y)
+        w = np.ascontiguousarray(w, np.float32)
+        if w.shape != (self._batch,):
+            raise ValueError(f"weights must have shape ({self._batch},)")
+        out = np.empty(self.P, np.float32)
+        check(lib.pgb_weighted_grad_sum(self.handle, _lib.ptr(x), _lib.ptr(y), _lib.ptr(w),
+                                        _lib.ptr(out)))
+        return out
+
+    def batch_grad_sum(self, x, y):
+        """sum_i g_i over the batch, as GradEngine::batch_grad_sum (strategies.cpp:453-458)."""
+        x, y = self._inputs(x, y)
+        out = np.empty(self.P, np.float32)
+        check(lib.pgb_batch_grad_sum(self.handle, _lib.ptr(x), _lib.ptr(y), _lib.ptr(out)))
+        return out

@@ -169,6 +169,7 @@ def test_noise_variance(O):
 @pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(os.path.dirname(
     os.path.abspath(__file__))), "oracle", "_ref", "libpegrad_ref.so")), reason="no oracle/_ref")
 @pytest.mark.parametrize("kind,kw,B,strat,m", [(0, {}, 8, 2, 1), (1, {}, 8, 5, 2),
+                                               (1, {}, 8, 3, 1),  # norms: the two-pass step
                                                (2, {}, 4, 4, 1), (2, {}, 4, 1, 2),
                                                (4, dict(seq_len=8, vocab=20, hidden=4), 4, 5, 1)])
 def test_restatement_matches_live_reference(O, kind, kw, B, strat, m):
@@ -176,9 +177,10 @@ def test_restatement_matches_live_reference(O, kind, kw, B, strat, m):
     p = O.init_params(d, 3)
     x, y = O.synth(d, B, 5)
     R = O.RefModel(d, strat, B, p)
-    rs, rn = R.per_example(x, y)
+    rs, rn = R.per_example(x, y, want_stacks=strat != O.NORMS)
     st, nsq, _ = O.per_example_grads(d, x, y, p)
-    assert np.abs(st - rs).max() <= 1e-12 * max(1.0, np.abs(rs).max())
+    if rs is not None:
+        assert np.abs(st - rs).max() <= 1e-12 * max(1.0, np.abs(rs).max())
     np.testing.assert_allclose(np.sqrt(nsq), rn, rtol=1e-12)
     for step in range(3):
         got, norms, nclip, _ = O.dpsgd_step(d, x, y, p, 0.5, 0.7, 0.1, m, 9, step)
@@ -187,3 +189,22 @@ def test_restatement_matches_live_reference(O, kind, kw, B, strat, m):
         assert nclip == rclip
         np.testing.assert_allclose(got, R.params(), rtol=1e-12, atol=1e-15)
         p = got
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(os.path.dirname(
+    os.path.abspath(__file__))), "oracle", "_ref", "libpegrad_ref.so")), reason="no oracle/_ref")
+@pytest.mark.parametrize("kind,strat", [(1, 3), (1, 2), (2, 4)])
+def test_weighted_grad_sum_matches_restatement(O, kind, strat):
+    """GradEngine::weighted_grad_sum (strategies.cpp:432-450, one weighted
+    backward) equals sum_i w_i g_i over the restatement's per-example stacks:
+    the identity the norms-only two-pass step (dpsgd.cpp:194-230) rests on."""
+    d = O.build_desc(kind)
+    B = 6
+    p = O.init_params(d, 2)
+    x, y = O.synth(d, B, 4)
+    w = np.random.default_rng(0).uniform(0.1, 1.0, B)
+    R = O.RefModel(d, strat, B, p)
+    got = R.weighted_grad_sum(x, y, w)
+    st, _, _ = O.per_example_grads(d, x, y, p)
+    want = np.concatenate([(w[:, None] * b).sum(0) for b in O.split_stacks(d, st, B)])
+    np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-13 * np.abs(want).max())

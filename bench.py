@@ -149,8 +149,9 @@ def ncu_counters(model, kernel):
     return {}
 
 
-def workload_config(model, world):
+def workload_config(model, world, batch_override=0):
     kind, opts, strat, batch, data_n, _, _, arch = MODELS[model]
+    batch = batch_override or batch
     return {"workload": f"{model} DPSGD step ({arch})", "model": model,
             "global_batch": batch * world, "per_gpu_batch": batch, "seq_len": None,
             "parallelism": f"dp{world}", "clip_norm": CLIP, "noise_multiplier": SIGMA,
@@ -163,10 +164,11 @@ def workload_config(model, world):
 # CPU reference (oracle/_ref = the unmodified reference library compiled here)
 # ---------------------------------------------------------------------------
 
-def _ref_worker(model, steps, warmup, time_cap, q):
+def _ref_worker(model, steps, warmup, time_cap, q, batch_override=0):
     import numpy as np
     import oracle as O
     kind, opts, strat, batch, _, _, _, _ = MODELS[model]
+    batch = batch_override or batch
     strat = {4: O.GROUPCONV, 2: O.OUTER, 5: O.JACMM}.get(strat, strat)
     if model == "fcnn":
         strat = O.NORMS  # the reference's fastest FCNN strategy
@@ -189,21 +191,21 @@ def _ref_worker(model, steps, warmup, time_cap, q):
     q.put((done, time.perf_counter() - t0))
 
 
-def cpu_reference(model, steps, procs, warmup=1, time_cap=20.0):
+def cpu_reference(model, steps, procs, warmup=1, time_cap=20.0, batch=0):
     """The reference's own dpsgd_step (its fastest strategy, graph mode, fp32,
     its 2-thread intra-op split) on `procs` independent processes, each over
     its own batches; returns (aggregate ex/s, steps per process, seconds)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_ref_worker, args=(model, steps, warmup, time_cap, q))
+    ps = [ctx.Process(target=_ref_worker, args=(model, steps, warmup, time_cap, q, batch))
           for _ in range(procs)]
     for p in ps:
         p.start()
     res = [q.get() for _ in ps]
     for p in ps:
         p.join()
-    batch = MODELS[model][3]
+    batch = batch or MODELS[model][3]
     value = sum(n * batch / t for n, t in res if n)
     return value, [n for n, _ in res], max(t for _, t in res)
 
@@ -215,15 +217,15 @@ def run_reference_arm(args):
     ncpu = os.cpu_count() or 1
     procs = max(1, ncpu // 2)
     value, nsteps, t = cpu_reference(args.model, args.steps, procs, warmup=args.warmup,
-                                     time_cap=args.ref_seconds)
-    batch = MODELS[args.model][3]
+                                     time_cap=args.ref_seconds, batch=args.batch)
+    batch = args.batch or MODELS[args.model][3]
     line = {
         "metric": MODELS[args.model][5], "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": int(min(nsteps)), "warmup": args.warmup,
         "ms_per_step": 1e3 * t / max(1, min(nsteps)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (io::synth_for_model, seed 0)", "impl": "reference",
-        "config": workload_config(args.model, world),
+        "config": workload_config(args.model, world, getattr(args, 'batch', 0)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 2 * procs, "kind": "reference",
                          "sample": f"{procs} processes x up to {args.steps} reference "
                                    f"dpsgd_step(B={batch}, graph, fp32) capped at "
@@ -298,6 +300,9 @@ def run_ours(args):
     from paper_2010_09063_b200.dist import exchange_unique_id
 
     kind, opts, strat, BATCH, DATA_N, METRIC, MFLOP, _ = MODELS[args.model]
+    if args.batch:  # batch sweeps (BASELINE config 2: FFNN at batch 16-512)
+        METRIC = METRIC.replace(f"batch {BATCH}", f"batch {args.batch}")
+        BATCH = args.batch
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
@@ -463,7 +468,7 @@ def run_ours(args):
                 import oracle
                 if oracle.ref_available():
                     v, nst, tt = cpu_reference(args.model, args.ref_steps, 1, 1,
-                                               args.ref_seconds)
+                                               args.ref_seconds, batch=args.batch)
                     cpu = {"value": v, "unit": UNIT, "cores": 2, "kind": "reference",
                            "sample": f"{nst[0]} reference dpsgd_step calls (B={BATCH}, graph "
                                      f"mode, fp32; {nst[0] * BATCH} examples) in 1 process, "
@@ -478,7 +483,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (bit-identical to io::synth_for_model, seed 0+rank); random-init "
                     "params (models::build seed 0)",
-            "config": workload_config(args.model, world),
+            "config": workload_config(args.model, world, getattr(args, 'batch', 0)),
             "e2e": {"value": e2e, "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * row * 4 + BATCH * 4,
                     "d2h_bytes_per_step": BATCH * 4 + 8,
@@ -509,6 +514,8 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=200)
     ap.add_argument("--ref-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="per-GPU batch override (default: the config's batch)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

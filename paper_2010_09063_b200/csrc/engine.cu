@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "mnist_fused.cuh"
 #include "mnist_tc.cuh"
+#include "mlp_fused.cuh"
 #include "tc.cuh"
 #include "conv_tc.cuh"
 #include "pgb_internal.h"
@@ -129,6 +130,8 @@ struct Engine {
   int nparts = 1;        // fp64 norm partials per example
   bool norms_fused = false;  // per-example norms produced by the gradient kernel
   bool fused_mnist = false;  // whole per-example pass in one kernel
+  bool mlp_fused = false;    // dense-only models: one warp-per-example kernel (mlp_fused.cuh)
+  bool mlp_attr = false;
   bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
   bool agg_in_kernel = false;  // ... and the aggregation after an in-kernel grid barrier
   bool fuse_agg_next = false;  // set by enqueue_step for the fused launch it makes
@@ -389,6 +392,26 @@ struct Engine {
     mnist_tc = fused_mnist && std::getenv("PGB_MNIST_SIMT") == nullptr;
     use_tc = std::getenv("PGB_NO_TC") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
+    // dense / relu / flatten only, dense first, widths and depth within the
+    // fused kernel's per-warp buffers
+    {
+      int nd = 0;
+      bool ok = !fused_mnist && std::getenv("PGB_NO_MLP_FUSED") == nullptr && n > 0 &&
+                desc.layers[0].kind == PGB_DENSE && desc.classes <= mlp::kMaxClasses;
+      for (int l = 0; l < n && ok; ++l) {
+        const pgb_layer_spec& sp = desc.layers[l];
+        if (sp.kind == PGB_DENSE) {
+          ++nd;
+          ok = sp.in <= mlp::kMaxWidth && sp.out <= mlp::kMaxWidth;
+        } else if (sp.kind == PGB_RELU) {
+          ok = layers[l].alias;
+        } else {
+          ok = sp.kind == PGB_FLATTEN;
+        }
+      }
+      mlp_fused = ok && nd >= 1 && nd <= mlp::kMaxLayers &&
+                  desc.layers[n - 1].kind == PGB_DENSE && P <= mlp::kMaxParams;
+    }
   }
 
   void allocate() {
@@ -838,10 +861,48 @@ struct Engine {
     return mark(s, "mnist_fused");
   }
 
+  // dense-only models: the whole per-example pass in mlp::mlp_kernel
+  int enqueue_mlp(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    mlp::Params prm{};
+    for (const Layer& L : layers) {
+      if (L.spec.kind != PGB_DENSE) continue;
+      mlp::DenseLayer& D = prm.L[prm.n++];
+      D.in = (int)L.spec.in;
+      D.out = (int)L.spec.out;
+      D.relu = L.fused_relu ? 1 : 0;
+      D.pW = L.pblock;
+      D.pb = L.pblock + 1;
+      D.offW = (int)param_off[L.pblock];
+      D.offb = (int)param_off[L.pblock + 1];
+      D.act = L.act_out;
+      D.gout = L.gout;
+    }
+    prm.params = d_params;
+    prm.P = (int)P;
+    prm.x = x_slot;
+    prm.y = y_slot;
+    prm.loss = d_loss;
+    prm.parts = d_parts;
+    prm.nparts = nparts;
+    prm.B = (int)B;
+    prm.classes = (int)desc.classes;
+    prm.err = d_err;
+    const size_t smem = sizeof(float) * (size_t)P;
+    if (!mlp_attr) {  // once per engine (the attribute is per device)
+      PGB_CUDA(cudaFuncSetAttribute(mlp::mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(float) * mlp::kMaxParams)));
+      mlp_attr = true;
+    }
+    mlp::mlp_kernel<<<(unsigned)((B + mlp::kWarps - 1) / mlp::kWarps), 32 * mlp::kWarps, smem,
+                      s>>>(prm);
+    return mark(s, "mlp_fused");
+  }
+
   // Per-example gradient sources for the batch (the reference's
   // compute_views); norms land in d_parts. Returns kernels launched.
   int enqueue_grads(cudaStream_t s, const float* x_slot, const float* y_slot) {
     if (fused_mnist) return enqueue_fused_mnist(s, x_slot, y_slot);
+    if (mlp_fused) return enqueue_mlp(s, x_slot, y_slot);
     int nk = enqueue_forward(s, x_slot, y_slot);
     const int n = desc.n_layers;
     const int Bi = (int)B;
@@ -1093,7 +1154,7 @@ struct Engine {
     int nk = 0;
     const bool emb = emb_layer >= 0 && t.kind[layers[emb_layer].pblock] == 2;
     if (world == 1) {
-      launch_agg(agg_launch(t, np, U, 0, ff), s, ff && pdl_enabled);
+      launch_agg(agg_launch(t, np, U, 0, ff), s, (ff || mlp_fused) && pdl_enabled);
       nk += mark(s, "aggregate");
       if (emb) nk += enqueue_embed_agg(s, t, np, 0);
     } else {

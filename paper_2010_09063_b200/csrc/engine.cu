@@ -238,6 +238,7 @@ struct Engine {
   int* clipped_dst = nullptr;
   float* d_stacks = nullptr;
   float* d_wts = nullptr;  // (B) weights of pgb_weighted_grad_sum
+  float* d_xin = nullptr;  // (B, in) inputs as the fused dense kernel read them
   float* d_units = nullptr;
   double* d_parts = nullptr;
   float* d_cot[2] = {nullptr, nullptr};
@@ -279,6 +280,8 @@ struct Engine {
     bool fused_tc = false;
     cudaGraphNode_t emb = nullptr;  // the sparse embedding aggregation
     EmbAggLaunch emb_args{};
+    cudaGraphNode_t mlp = nullptr;  // the fused dense-model kernel (inputs per step)
+    mlp::Params mlp_args{};
   };
   std::map<int, StepGraph> graphs;  // key: schedule variant
   int kernels_last = 0;
@@ -432,6 +435,7 @@ struct Engine {
     want((void**)&d_grid_ctr, sizeof(unsigned long long));
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_wts, sizeof(float) * B);
+    want((void**)&d_xin, sizeof(float) * B * in_row);
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
     int64_t max_act = 0;
@@ -605,7 +609,7 @@ struct Engine {
       t.kind[L.pblock] = 1;
       t.base[L.pblock] = L.gout;
       t.stride[L.pblock] = o;
-      t.a[L.pblock] = x_slot;
+      t.a[L.pblock] = mlp_fused ? d_xin : x_slot;
       t.a_stride[L.pblock] = L.spec.in;
       t.out[L.pblock] = o;
     }
@@ -879,6 +883,13 @@ struct Engine {
     }
     prm.params = d_params;
     prm.P = (int)P;
+    prm.xin = d_xin;
+    prm.step_base = cap_step_base;
+    prm.step_off = cap_step_off;
+    prm.xring = cap_xring;
+    prm.yring = cap_yring;
+    prm.ring_origin = 0;
+    prm.ring_n = cap_ring_n;
     prm.x = x_slot;
     prm.y = y_slot;
     prm.loss = d_loss;
@@ -1100,6 +1111,10 @@ struct Engine {
     L.U = U;
     L.nparts = np;
     L.mode = mode;
+    if (cap_step_base && !L.noise) {
+      L.step_base = cap_step_base;
+      L.step_off = cap_step_off;
+    }
     return L;
   }
 
@@ -1231,7 +1246,7 @@ struct Engine {
     int slot_key = 0;
     for (int i = 0; i < kSlots; ++i)
       if (x_slot == d_xb[i]) slot_key = i + 1;
-    const int key = variant * (kSlots + 1) + (fused_mnist ? 0 : slot_key);
+    const int key = variant * (kSlots + 1) + ((fused_mnist || mlp_fused) ? 0 : slot_key);
     if (!graph_enabled) {
       kernels_last = enqueue_step(stream, x_slot, y_slot, m);
       PGB_CUDA(cudaGetLastError());
@@ -1377,6 +1392,9 @@ struct Engine {
           sg.agg = nd;
           sg.agg_args = *L;
         }
+      } else if (kp.func == (void*)mlp::mlp_kernel) {
+        sg.mlp = nd;
+        sg.mlp_args = *static_cast<const mlp::Params*>(kp.kernelParams[0]);
       } else if (kp.func == (void*)embed_agg_kernel) {
         sg.emb = nd;
         sg.emb_args = *static_cast<const EmbAggLaunch*>(kp.kernelParams[0]);
@@ -1414,6 +1432,11 @@ struct Engine {
       sg.agg_args.norms_out = norms_dst;
       sg.agg_args.clipped_out = clipped_dst;
       set_node(sg.exec, sg.agg, &sg.agg_args);
+    }
+    if (sg.mlp && (sg.mlp_args.x != x_slot || sg.mlp_args.y != y_slot)) {
+      sg.mlp_args.x = x_slot;
+      sg.mlp_args.y = y_slot;
+      set_node(sg.exec, sg.mlp, &sg.mlp_args);
     }
     if (sg.emb && !same_args(sg.emb_args.a, cur_args)) {
       sg.emb_args.a = cur_args;
@@ -1617,7 +1640,7 @@ pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d
     en.push_args(en.make_args(*cfg, step, en.d_x, en.d_y));
     en.last_cfg = *cfg;
     en.last_step = step;
-    if (en.fused_mnist && en.graph_enabled) {
+    if ((en.fused_mnist || en.mlp_fused) && en.graph_enabled) {
       // read in place: the graph's fused-kernel node is pointed at the batch
       en.launch_step(d_x, d_y, cfg->microbatch);
     } else {
@@ -1646,7 +1669,7 @@ pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_
     };
     int64_t C = 8;
     if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
-    const bool chunked = en.fused_mnist && en.world == 1 && cfg->microbatch == 1 &&
+    const bool chunked = (en.fused_mnist || en.mlp_fused) && en.world == 1 && cfg->microbatch == 1 &&
                          en.graph_enabled && C > 1 && n_steps >= C && n_batches < (1 << 30);
     int64_t s = 0;
     if (chunked) {
@@ -1662,7 +1685,7 @@ pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_
     for (; s < n_steps; ++s) {
       const auto in = batch(step0 + s);
       en.push_args(en.make_args(*cfg, step0 + s, in.first, in.second));
-      if (en.fused_mnist && en.graph_enabled) {
+      if ((en.fused_mnist || en.mlp_fused) && en.graph_enabled) {
         en.launch_step(in.first, in.second, cfg->microbatch);
       } else {
         PGB_CUDA(cudaMemcpyAsync(en.d_x, in.first, sizeof(float) * en.B * en.in_row,
@@ -1897,7 +1920,7 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
     // result slots: K chunk slots of C, then the head / remainder slots
     C = std::min<int64_t>(C, Engine::kResSlots / (K + 1));
-    const bool chunked = en.fused_mnist && en.world == 1 && cfg->microbatch == 1 &&
+    const bool chunked = (en.fused_mnist || en.mlp_fused) && en.world == 1 && cfg->microbatch == 1 &&
                          en.graph_enabled && C > 1 && steps >= C;
     if (!chunked) C = 1;
     if (C > 1) en.ensure_chunk_ring(C);

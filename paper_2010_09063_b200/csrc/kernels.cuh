@@ -771,6 +771,10 @@ struct AggLaunch {
   const float* scales;      // (U) or null: computed from parts
   const int* clip_flags;    // (U)
   const float* noise;       // (P) or null: drawn here
+  // multi-step graphs: the step index of the noise streams is read on the
+  // device (*step_base + step_off) instead of a.step
+  const long long* step_base;
+  int step_off;
   int U, nparts, mode;
 };
 
@@ -1007,7 +1011,8 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     if (!L.noise) {
       // the pair's two normals come from one Box-Muller draw (kernels.hpp:597-614)
       float n0, n1;
-      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
+      const long long stp = L.step_base ? *L.step_base + L.step_off : a.step;
+      gauss_pair(stream_key(a.seed, noise_stream(stp, p)), j >> 1, &n0, &n1);
       n = (j & 1) ? n1 : n0;
     }
     sum = __fadd_rn(sum, __fmul_rn(__fmul_rn(a.sigma, a.clip), n));

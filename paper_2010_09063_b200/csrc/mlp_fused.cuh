@@ -37,6 +37,15 @@ struct Params {
   int P;
   const float* x;  // (B, L[0].in)
   const float* y;  // (B) labels as float
+  float* xin;      // (B, L[0].in): the inputs again, the ghost factor a of layer 0
+  // multi-step graphs over a device-resident ring of batches (as mnist::Params):
+  // step s = *step_base + step_off reads batch (s - ring_origin) mod ring_n
+  const long long* step_base;
+  int step_off;
+  const float* xring;
+  const float* yring;
+  long long ring_origin;
+  int ring_n;
   float* loss;     // (B)
   double* parts;   // (B, nparts) squared norm per parameter block
   int nparts, B, classes;
@@ -64,7 +73,20 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
   if (i >= P.B) return;  // warp-level work only: no CTA barriers below
   float(*A)[kMaxWidth] = act[warp];
   const int in0 = P.L[0].in;
-  for (int k = lane; k < in0; k += 32) A[0][k] = __ldg(P.x + (size_t)i * in0 + k);
+  const float* X = P.x;
+  const float* Y = P.y;
+  if (P.xring) {
+    const long long st = *P.step_base + P.step_off - P.ring_origin;
+    long long bi = st % P.ring_n;
+    if (bi < 0) bi += P.ring_n;
+    X = P.xring + bi * P.B * in0;
+    Y = P.yring + bi * P.B;
+  }
+  for (int k = lane; k < in0; k += 32) {
+    const float v = __ldg(X + (size_t)i * in0 + k);
+    A[0][k] = v;
+    P.xin[(size_t)i * in0 + k] = v;
+  }
   __syncwarp();
 
   // ---- forward: z = a W + b (ascending k), relu fused ----------------------
@@ -94,7 +116,7 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
   const int K = P.classes;
   const float* z = A[P.n];
   float* g = grad[warp][0];
-  const float raw = __ldg(P.y + i);
+  const float raw = __ldg(Y + i);
   const int Kc = K == 1 ? 2 : K;
   if (!valid_id(raw, Kc)) {
     if (lane == 0) {

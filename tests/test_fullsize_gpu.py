@@ -301,3 +301,63 @@ def test_embed_full_size_sparse_step_matches_dense_clipped_sum(P, O):
     n_emb = 10004 * 100
     want = got_sum[:n_emb].astype(np.float64)
     assert np.linalg.norm(step_sum[:n_emb] - want) <= 1e-5 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("name,kind", [("fcnn", 1), ("logreg", 0)])
+def test_dense_run_steps_device_matches_step_calls(P, O, name, kind):
+    """Dense models through the fused MLP kernel in static multi-step graphs
+    (batch and noise step read on the device): bitwise the parameters of the
+    same steps issued one call at a time, with a remainder that does not fill
+    a graph."""
+    torch = pytest.importorskip("torch")
+    from paper_2010_09063_b200 import _lib
+    B, NB, STEPS = 64, 3, 21
+    desc = P.build_desc(P.ModelKind(kind))
+    data = P.synth_for_model(desc, B * NB, 2)
+    row = int(np.prod(desc.input_shape))
+    dx = torch.from_numpy(data.inputs).cuda()
+    dy = torch.from_numpy(data.labels).cuda()
+    cfg = P.DpConfig(clip_norm=0.5, noise_multiplier=1.1, learning_rate=0.1, seed=4).to_c()
+    out = []
+    for mode in ("steps", "calls"):
+        model = P.build_from_desc(desc, 0)
+        eng = P.GradEngine(model, P.Strategy.outer, B)
+        if mode == "steps":
+            n = C.c_int64()
+            _lib.check(_lib.lib.pgb_run_steps_device(eng.handle, C.c_void_p(dx.data_ptr()),
+                                                     C.c_void_p(dy.data_ptr()), NB, STEPS,
+                                                     C.byref(cfg), 5, C.byref(n)))
+        else:
+            for i in range(STEPS):
+                b = (5 + i) % NB
+                _lib.check(_lib.lib.pgb_dpsgd_step_device(
+                    eng.handle, C.c_void_p(dx.data_ptr() + b * B * row * 4),
+                    C.c_void_p(dy.data_ptr() + b * B * 4), C.byref(cfg), 5 + i))
+        _lib.check(_lib.lib.pgb_synchronize(eng.handle, None, None))
+        out.append(eng.get_flat_params())
+    np.testing.assert_array_equal(out[0], out[1])
+
+
+def test_fcnn_epoch_driver_matches_oracle(P, O):
+    """pgb_run_epoch on the FCNN (fused MLP kernel, chunk graphs with the
+    noise step read on the device) against the oracle, step by step."""
+    B, steps = 64, 20
+    desc = P.build_desc(P.ModelKind.fcnn)
+    od = O.build_desc(O.FCNN)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, steps * B, 0, pinned=True)
+    eng = P.GradEngine(model, P.Strategy.norms, B)
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0)
+    norms = np.empty(steps * B, np.float32)
+    _, clipped = P.run_epoch(eng, model, data, cfg, 7, norms)
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, steps * B, 0)
+    total = 0
+    for s in range(steps):
+        sl = slice(s * B, (s + 1) * B)
+        p_new, wn, wclip, _ = O.dpsgd_step(od, x64[sl], y64[sl], p64, 1.0, 1.1, 0.1, 1, 0, 7 + s)
+        assert np.max(np.abs(norms[sl] - wn) / wn) < TOL, f"step {s}"
+        total += wclip
+        p_prev, p64 = p64, p_new
+    assert clipped == total
+    _check_params(eng.get_flat_params(), p64, p_prev)

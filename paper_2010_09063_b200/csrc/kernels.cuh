@@ -394,20 +394,53 @@ __global__ void mask_kernel(const float* __restrict__ g, const float* __restrict
 
 // embedding gather fused with the sequence mean-pool (models.cpp:241-262):
 // y[b,e] = (sum_t table[id_bt, e]) * 1/L. Ids validated (checked_id).
+constexpr int kPoolMaxL = 2048;
+
 __global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
                                       const float* __restrict__ table, float* __restrict__ y,
                                       int B, int L, int E, int V, DevError* err) {
   const int b = blockIdx.x;
+  if (L > kPoolMaxL) {  // long sequences: the plain loop
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      float s = 0.0f;
+      for (int t = 0; t < L; ++t) {
+        const float raw = ids[(size_t)b * L + t];
+        if (!valid_id(raw, V)) {
+          if (e == 0) raise_index(err, 1, (long long)b * L + t, raw, V);
+          continue;
+        }
+        s += table[(size_t)(int)raw * E + e];
+      }
+      y[(size_t)b * E + e] = s * (1.0f / float(L));
+    }
+    return;
+  }
+  // the example's ids once (validated), then 8 row gathers in flight per
+  // thread, added in token order
+  __shared__ int sid[kPoolMaxL];
+  for (int t = threadIdx.x; t < L; t += blockDim.x) {
+    const float raw = ids[(size_t)b * L + t];
+    const bool ok = valid_id(raw, V);
+    if (!ok) raise_index(err, 1, (long long)b * L + t, raw, V);
+    sid[t] = ok ? (int)raw : -1;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     float s = 0.0f;
-    for (int t = 0; t < L; ++t) {
-      const float raw = ids[(size_t)b * L + t];
-      if (!valid_id(raw, V)) {
-        if (e == 0) raise_index(err, 1, (long long)b * L + t, raw, V);
-        continue;
+    int t = 0;
+    for (; t + 8 <= L; t += 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int r = sid[t + q];
+        v[q] = r >= 0 ? __ldg(table + (size_t)r * E + e) : 0.0f;
       }
-      s += table[(size_t)(int)raw * E + e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (sid[t + q] >= 0) s += v[q];
     }
+    for (; t < L; ++t)
+      if (sid[t] >= 0) s += __ldg(table + (size_t)sid[t] * E + e);
     y[(size_t)b * E + e] = s * (1.0f / float(L));
   }
 }
@@ -1042,6 +1075,8 @@ __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaun
 // order. Here each example keeps only its distinct tokens and counts; the
 // element value is the same fp32 chain acc = fl(acc + v) repeated c times.
 constexpr int kEmbMaxL = 1024;
+constexpr int kEmbMaxE = 1024;
+constexpr int kEmbHist = 64;  // token counts per example handled by the count histogram  // pooled-cotangent rows staged in shared memory up to this width
 
 __device__ __forceinline__ float emb_chain(float v, int c) {
   float acc = 0.0f;
@@ -1089,18 +1124,33 @@ __global__ void __launch_bounds__(256) embed_index_kernel(
       }
       __syncthreads();
     }
-  // segment starts (distinct tokens) in order
-  if (t == 0) {
-    int n = 0;
-    for (int k = 0; k < L; ++k) {
-      if (key[k] == 0x7fffffff) break;
-      if (k == 0 || key[k] != key[k - 1]) seg[n++] = k;
+  // segment starts (distinct tokens) in order: first occurrences flagged in
+  // parallel, compacted with warp ballots and a per-chunk warp prefix
+  {
+    __shared__ int wtot[32];
+    const int lane = t & 31, wp = t >> 5, nw = blockDim.x >> 5;
+    int base = 0, end = 0;
+    for (int k0 = 0; k0 < Lp; k0 += blockDim.x) {
+      const int k = k0 + t;
+      const bool valid = k < L && key[k] != 0x7fffffff;
+      const bool f = valid && (k == 0 || key[k] != key[k - 1]);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wtot[wp] = __popc(bal);
+      end += __syncthreads_count(valid);
+      int off = base, tot = 0;
+      for (int q = 0; q < nw; ++q) {
+        off += q < wp ? wtot[q] : 0;
+        tot += wtot[q];
+      }
+      if (f) seg[off + __popc(bal & ((1u << lane) - 1u))] = k;
+      base += tot;
+      __syncthreads();
     }
-    int end = 0;
-    while (end < L && key[end] != 0x7fffffff) ++end;
-    seg[n] = end;
-    nseg = n;
-    nd[i] = n;
+    if (t == 0) {
+      seg[base] = end;
+      nseg = base;
+      nd[i] = base;
+    }
   }
   __syncthreads();
   const int n = nseg;
@@ -1110,13 +1160,44 @@ __global__ void __launch_bounds__(256) embed_index_kernel(
     cnt[(size_t)i * L + k] = seg[k + 1] - seg[k];
     atomicOr(&bits[(size_t)r * words + (i >> 5)], 1u << (i & 31));
   }
-  // ||G_i||^2 = sum over distinct tokens and e of chain(u_ie / L, c)^2
+  // ||G_i||^2 = sum over distinct tokens and e of chain(u_ie / L, c)^2 (the
+  // pooled cotangent row staged in shared memory once)
+  __shared__ float urow[kEmbMaxE];
+  const bool staged = E <= kEmbMaxE;
+  if (staged)
+    for (int e = t; e < E; e += blockDim.x) urow[e] = u[(size_t)i * E + e];
+  __syncthreads();
+  const float* ur = staged ? urow : u + (size_t)i * E;
   const float invL = 1.0f / float(L);
+  // every token with count c contributes the same sum_e chain(u_e / L, c)^2:
+  // one pass over e per distinct count (fp64, any order)
+  __shared__ int hist[kEmbHist];
+  for (int c = t; c < kEmbHist; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int k = t; k < n; k += blockDim.x) {
+    const int c = seg[k + 1] - seg[k];
+    if (c < kEmbHist) atomicAdd(&hist[c], 1);
+  }
+  __syncthreads();
   double acc = 0.0;
-  for (int q = t; q < n * E; q += blockDim.x) {
-    const int k = q / E, e = q - k * E;
-    const float g = emb_chain(u[(size_t)i * E + e] * invL, seg[k + 1] - seg[k]);
-    acc += (double)g * g;
+  const int lane = t & 31, wp = t >> 5, nw = blockDim.x >> 5;
+  for (int c = 1 + wp; c < kEmbHist; c += nw) {
+    const int m = hist[c];
+    if (!m) continue;
+    double sc = 0.0;
+    for (int e = lane; e < E; e += 32) {
+      const float g = emb_chain(ur[e] * invL, c);
+      sc += (double)g * g;
+    }
+    acc += sc * m;
+  }
+  for (int k = t; k < n; k += blockDim.x) {  // counts beyond the histogram
+    const int c = seg[k + 1] - seg[k];
+    if (c < kEmbHist) continue;
+    for (int e = 0; e < E; ++e) {
+      const float g = emb_chain(ur[e] * invL, c);
+      acc += (double)g * g;
+    }
   }
   acc = block_reduce_sum(acc, red);
   if (t == 0) parts[(size_t)i * nparts + p] = acc;
@@ -1159,48 +1240,102 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
   const bool failed = A.err && A.err->code != 0;
   const uint64_t key = stream_key(a.seed, noise_stream(a.step, A.p));
   const long long E = A.E;
+  __shared__ int lst_i[8][32], lst_c[8][32];
+  __shared__ float lst_s[8][32];
   for (int r = blockIdx.x * 8 + w; r < A.V; r += gridDim.x * 8) {
     const unsigned word = lane < A.words ? A.bits[(size_t)r * A.words + lane] : 0u;
     const unsigned active = __ballot_sync(0xffffffffu, word != 0u);
     wsh[w][lane] = word;
     __syncwarp();
-    const long long j0 = (long long)r * E, jp0 = j0 >> 1, jp1 = (j0 + E - 1) >> 1;
-    for (long long jp = jp0 + lane; jp <= jp1; jp += 32) {
-      const long long e0 = 2 * jp - j0, e1 = e0 + 1;
-      const bool ok0 = e0 >= 0 && e0 < E, ok1 = e1 >= 0 && e1 < E;
-      float acc0 = 0.0f, acc1 = 0.0f;
-      unsigned am = active;
-      while (am) {
-        const int wd = __ffs(am) - 1;
-        am &= am - 1;
-        unsigned bw = wsh[w][wd];
-        while (bw) {
-          const int bb = __ffs(bw) - 1;
-          bw &= bw - 1;
-          const int i = wd * 32 + bb;
-          // count of token r in example i: binary search its distinct tokens
-          const int* tk = A.tok + (size_t)i * A.L;
-          int lo = 0, hi = A.nd[i] - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (tk[mid] < r) lo = mid + 1;
-            else hi = mid;
-          }
-          const int c = A.cnt[(size_t)i * A.L + lo];
-          const float s = s_emb[i];
-          const float* ui = A.u + (size_t)i * E;
-          if (ok0) acc0 = __fadd_rn(acc0, __fmul_rn(emb_chain(ui[e0] * invL, c), s));
-          if (ok1) acc1 = __fadd_rn(acc1, __fmul_rn(emb_chain(ui[e1] * invL, c), s));
+    // this lane's element pairs of the row: jb + lane + 32 q, in blocks of 64
+    // pairs (one block for E <= 126)
+    const long long j0 = (long long)r * E, jp1 = (j0 + E - 1) >> 1;
+    for (long long jb = j0 >> 1; jb <= jp1; jb += 64) {
+    float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+    long long e0q[2];
+    bool okq[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const long long jp = jb + lane + 32 * q;
+      e0q[q] = 2 * jp - j0;
+      okq[q][0] = jp <= jp1 && e0q[q] >= 0 && e0q[q] < E;
+      okq[q][1] = jp <= jp1 && e0q[q] + 1 >= 0 && e0q[q] + 1 < E;
+    }
+    // the row's examples in ascending order, 32 at a time: the count of token
+    // r in example i is found once per example (one lane each, binary search
+    // of its distinct tokens), then every lane adds fl(chain(u_ie / L, c) s_i)
+    int fill = 0;
+    auto flush = [&]() {
+      if (lane < fill) {
+        const int i = lst_i[w][lane];
+        const int* tk = A.tok + (size_t)i * A.L;
+        int lo = 0, hi = A.nd[i] - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tk[mid] < r) lo = mid + 1;
+          else hi = mid;
+        }
+        lst_c[w][lane] = A.cnt[(size_t)i * A.L + lo];
+        lst_s[w][lane] = s_emb[i];
+      }
+      __syncwarp();
+      // four examples' u values in flight at a time, added in example order
+      for (int k0 = 0; k0 < fill; k0 += 4) {
+        float uv[4][2][2];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          const int k = min(k0 + d, fill - 1);
+          const float* ui = A.u + (size_t)lst_i[w][k] * E;
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) uv[d][q][h] = okq[q][h] ? __ldg(ui + e0q[q] + h) : 0.0f;
+        }
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          if (k0 + d >= fill) break;
+          const int c = lst_c[w][k0 + d];
+          const float s = lst_s[w][k0 + d];
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (okq[q][h])
+                acc[q][h] = __fadd_rn(acc[q][h], __fmul_rn(emb_chain(uv[d][q][h] * invL, c), s));
         }
       }
+      __syncwarp();
+      fill = 0;
+    };
+    unsigned am = active;
+    while (am) {
+      const int wd = __ffs(am) - 1;
+      am &= am - 1;
+      unsigned bw = wsh[w][wd];
+      while (bw) {
+        const int bb = __ffs(bw) - 1;
+        bw &= bw - 1;
+        if (lane == 0) lst_i[w][fill] = wd * 32 + bb;
+        if (++fill == 32) {
+          __syncwarp();
+          flush();
+        }
+      }
+    }
+    __syncwarp();
+    if (fill) flush();
+    const float scale = __fmul_rn(a.sigma, a.clip);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const long long jp = jb + lane + 32 * q;
+      if (jp > jp1) continue;
       float n0 = 0.0f, n1 = 0.0f;
       if (A.mode == 0 && a.add_noise) gauss_pair(key, jp, &n0, &n1);
-      const float scale = __fmul_rn(a.sigma, a.clip);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (!(h ? ok1 : ok0)) continue;
-        const long long j = j0 + (h ? e1 : e0);
-        float sum = h ? acc1 : acc0;
+        if (!okq[q][h]) continue;
+        const long long j = j0 + e0q[q] + h;
+        float sum = acc[q][h];
         if (A.mode == 1) {
           A.sum_out[bt.param_off[A.p] + j] = sum;
           continue;
@@ -1212,6 +1347,7 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
         write_param(bt, A.p, j, A.params, __fsub_rn(cur, __fmul_rn(a.lr, sum)));
       }
     }
+    }  // pair blocks
     if (lane < A.words && word) A.bits[(size_t)r * A.words + lane] = 0u;
     __syncwarp();
   }

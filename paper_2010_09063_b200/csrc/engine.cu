@@ -1160,9 +1160,12 @@ struct Engine {
     A.nparts = np;
     A.mode = mode;
     const int rows_per_cta = 8;
+    finalize_norms_kernel<<<((int)B + 127) / 128, 128, 0, s>>>(d_parts, np, (int)B, d_wts);
+    const int nk0 = mark(s, "embed_norms");
+    A.norms = d_wts;  // (the weighted-sum weights buffer, free on the step path)
     const int grid = std::min<int>((A.V + rows_per_cta - 1) / rows_per_cta, 148 * 8);
     embed_agg_kernel<<<grid, 256, sizeof(float) * B, s>>>(A);
-    return mark(s, mode == 0 ? "embed_agg" : "embed_agg_local");
+    return nk0 + mark(s, mode == 0 ? "embed_agg" : "embed_agg_local");
   }
 
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {

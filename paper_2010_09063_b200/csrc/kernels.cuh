@@ -1079,6 +1079,7 @@ constexpr int kEmbMaxE = 1024;
 constexpr int kEmbHist = 64;  // token counts per example handled by the count histogram  // pooled-cotangent rows staged in shared memory up to this width
 
 __device__ __forceinline__ float emb_chain(float v, int c) {
+  if (c == 1) return v;  // fl(0 + v) = v, the common case
   float acc = 0.0f;
   for (int k = 0; k < c; ++k) acc = __fadd_rn(acc, v);
   return acc;
@@ -1212,6 +1213,7 @@ struct EmbAggLaunch {
   BlockTable bt;
   StepArgs a;
   const double* parts;
+  const float* norms;  // (B) per-example norms (finalize_norms_kernel), once per step
   const float* u;      // (B, E) pooled cotangent
   const int* tok;      // (B, L)
   const int* cnt;
@@ -1228,9 +1230,7 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
   __shared__ unsigned wsh[8][32];   // the current row's bitmap words, per warp
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < A.B; i += blockDim.x) {
-    double acc = 0.0;
-    for (int q = 0; q < A.nparts; ++q) acc += A.parts[(size_t)i * A.nparts + q];
-    const float nrm = (float)sqrt(acc);
+    const float nrm = A.norms[i];
     s_emb[i] = nrm > A.a.clip ? __fdiv_rn(A.a.clip, nrm) : 1.0f;
   }
   __syncthreads();
@@ -1308,22 +1308,28 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
       fill = 0;
     };
     unsigned am = active;
-    while (am) {
-      const int wd = __ffs(am) - 1;
-      am &= am - 1;
-      unsigned bw = wsh[w][wd];
-      while (bw) {
+    unsigned bw = 0;
+    int wd = 0;
+    while (true) {
+      // next example of the row in ascending order, or the end
+      while (!bw && am) {
+        wd = __ffs(am) - 1;
+        am &= am - 1;
+        bw = wsh[w][wd];
+      }
+      const bool more = bw != 0;
+      if (more) {
         const int bb = __ffs(bw) - 1;
         bw &= bw - 1;
         if (lane == 0) lst_i[w][fill] = wd * 32 + bb;
-        if (++fill == 32) {
-          __syncwarp();
-          flush();
-        }
+        ++fill;
       }
+      if (fill == 32 || (!more && fill)) {
+        __syncwarp();
+        flush();
+      }
+      if (!more) break;
     }
-    __syncwarp();
-    if (fill) flush();
     const float scale = __fmul_rn(a.sigma, a.clip);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {

@@ -58,6 +58,7 @@ struct TcConvDWOp {
   const float* x;     // (B, C, H, W)
   const float* gout;  // (B, D, Ho, Wo)
   float* stack;       // (B, D*C*k*k)
+  double* tile_sq;    // (B, tiles): each tile's squared sum (the block's per-example norm)
   __device__ const float* img(int z) const { return x + (size_t)z * g.C * g.H * g.W; }
   __device__ int img_h() const { return g.H; }
   __device__ int img_w() const { return g.W; }
@@ -170,6 +171,12 @@ inline void launch_bn(const Op& op, int batch, cudaStream_t s) {
   }
   dim3 grid((op.N + BN - 1) / BN, (op.M + kBM - 1) / kBM, batch);
   tc_gemm_kernel<Op, BN, kConvThreads><<<grid, kConvThreads, smem, s>>>(op);
+}
+
+// Output tiles of one GEMM launch() makes for (M, N) (tile_sq row length).
+inline int tile_count(int M, int N) {
+  const int bn = N <= 32 ? 32 : N <= 64 ? 64 : 128;
+  return ((N + bn - 1) / bn) * ((M + kBM - 1) / kBM);
 }
 
 // Pick the column tile from N (TMEM holds 3 accumulators of BN columns).

@@ -239,6 +239,7 @@ struct Engine {
   float* d_stacks = nullptr;
   float* d_wts = nullptr;  // (B) weights of pgb_weighted_grad_sum
   float* d_xin = nullptr;  // (B, in) inputs as the fused dense kernel read them
+  double* d_tile_sq = nullptr;  // (B, tiles) squared sums of the conv dW GEMM tiles
   float* d_units = nullptr;
   double* d_parts = nullptr;
   float* d_cot[2] = {nullptr, nullptr};
@@ -436,6 +437,16 @@ struct Engine {
     want((void**)&d_stacks, sizeof(float) * B * P);
     want((void**)&d_wts, sizeof(float) * B);
     want((void**)&d_xin, sizeof(float) * B * in_row);
+    {
+      int tiles = 1;
+      for (int l = 0; l < n; ++l)
+        if (desc.layers[l].kind == PGB_CONV) {
+          const ExShape& in = layers[l].in;
+          tiles = std::max(tiles, tc::tile_count((int)(in.d[0] * desc.layers[l].k * desc.layers[l].k),
+                                                 (int)desc.layers[l].out));
+        }
+      want((void**)&d_tile_sq, sizeof(double) * B * tiles);
+    }
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
     int64_t max_act = 0;
@@ -591,6 +602,10 @@ struct Engine {
         }
         set_block(bt, L.pblock + 1, 0, L.gout, o);
       }
+      // conv dW blocks: the per-example norm comes from the dW GEMM's tile sums
+      if (use_tc)
+        for (int l = 0; l < desc.n_layers; ++l)
+          if (layers[l].spec.kind == PGB_CONV) bt.norm_pre[layers[l].pblock] = 1;
       norms_fused = false;
       nparts = t.n;
     }
@@ -947,9 +962,13 @@ struct Engine {
           float* sW = d_stacks + param_off[L.pblock] * B;
           float* sb = d_stacks + param_off[L.pblock + 1] * B;
           if (use_tc) {
-            tc::TcConvDWOp dw{K, gg.D, Pp, gg, in, gcur, sW};
+            tc::TcConvDWOp dw{K, gg.D, Pp, gg, in, gcur, sW, d_tile_sq};
             tc::launch(dw, Bi, s);
             nk += mark(s, "conv_dw_pex_tc");
+            // the block's per-example norm from the GEMM's tile sums (sumsq skips it)
+            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(
+                d_tile_sq, tc::tile_count(K, gg.D), Bi, d_parts, nparts, L.pblock);
+            nk += mark(s, "conv_dw_norm");
           } else {
             ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
             launch_gemm(dw, Bi, s);

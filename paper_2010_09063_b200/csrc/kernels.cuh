@@ -524,7 +524,18 @@ struct BlockTable {
   // MNIST kernel's conv2 pair rows): row count (0: one row per unit, scaled
   // by the unit's clip factor in the aggregation)
   int rows[kMaxBlocks];
+  int norm_pre[kMaxBlocks];  // 1: per-example squared norm already in parts (sumsq skips)
 };
+
+// parts[i * nparts + p] = the fixed-order sum of example i's tile sums
+__global__ void tile_sq_reduce_kernel(const double* __restrict__ tile_sq, int tiles, int B,
+                                      double* __restrict__ parts, int nparts, int p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  double acc = 0.0;
+  for (int q = 0; q < tiles; ++q) acc += tile_sq[(size_t)i * tiles + q];
+  parts[(size_t)i * nparts + p] = acc;
+}
 
 // ---- hi/lo UMMA operand shadows of the MNIST conv weights (mnist_tc.cuh) ---
 // float layout of one shadow buffer (hi and lo stacked along the M/N rows so
@@ -643,7 +654,9 @@ __global__ void sumsq_kernel(BlockTable bt, int B, double* __restrict__ parts) {
   __shared__ double red[32];
   const int p = blockIdx.x;
   const long long i = blockIdx.y;
-  if (bt.kind[p] == 2) return;  // sparse embedding: embed_index_kernel writes its norm
+  // sparse embedding (embed_index_kernel) and conv dW blocks (the dW GEMM's
+  // tile sums) have their norms written elsewhere
+  if (bt.kind[p] == 2 || bt.norm_pre[p]) return;
   if (bt.kind[p] == 0) {
     const long long per = bt.size[p];
     const float* row = bt.base[p] + i * bt.stride[p];

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace pgb {
 namespace tc {
 
@@ -152,6 +154,14 @@ struct TcSmem {
 struct NoTable {
   static constexpr bool kTableA = false;
 };
+
+// Ops with a `double* tile_sq` member also get each tile's sum of squared
+// outputs (fp64), written to tile_sq[z * tiles + tile]: the per-example norm
+// of a materialised gradient block without a second pass over it.
+template <class T, class = void>
+struct HasTileSq : std::false_type {};
+template <class T>
+struct HasTileSq<T, std::void_t<decltype(&T::tile_sq)>> : std::true_type {};
 
 template <class Op, int BN, int NT>
 __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
@@ -301,6 +311,7 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
   const int row = m0 + (warp & 3) * 32 + lane;
   const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const int cbeg = (warp >> 2) * (BN / kGroups), cend = cbeg + BN / kGroups;
+  double sq = 0.0;
 #pragma unroll 1
   for (int c0 = cbeg; c0 < cend; c0 += 8) {
     float v[8], v1[8], vc[8], vd[8];
@@ -317,11 +328,30 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
     if (row < M) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (n0 + c0 + j < N) op.store(z, row, n0 + c0 + j, v[j]);
+        if (n0 + c0 + j < N) {
+          op.store(z, row, n0 + c0 + j, v[j]);
+          if constexpr (HasTileSq<Op>::value) sq = fma((double)v[j], (double)v[j], sq);
+        }
     }
   }
-  fence_before_sync();
-  __syncthreads();
+  if constexpr (HasTileSq<Op>::value) {
+    __shared__ double sq_red[NT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) sq_red[warp] = sq;
+    fence_before_sync();
+    __syncthreads();
+    if (t == 0) {
+      double tot = 0.0;
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) tot += sq_red[w];
+      const int tiles = gridDim.x * gridDim.y;
+      op.tile_sq[(size_t)z * tiles + blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    }
+  } else {
+    fence_before_sync();
+    __syncthreads();
+  }
   if (warp == 0) tmem_dealloc(tmem, kCols);
 }
 

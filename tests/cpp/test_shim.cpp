@@ -101,6 +101,24 @@ int main() {
   for (size_t i = 0; i < fc.size(); ++i)
     CHECK(std::fabs(fc[i] - fdd[i]) <= 1e-6f * (1.0f + std::fabs(fdd[i])));
 
+  // the norms-only two-pass branch (dpsgd.cpp:194-230): weighted sums through
+  // the shim, batch_grad_sum = weighted_grad_sum(1), sum_i w g_i linear in w,
+  // and microbatch != 1 refused
+  {
+    auto e = models::build(ModelKind::fcnn, 5);
+    auto fe = io::synth_for_model(e.desc, 8, 1);
+    GradEngine en(e, Strategy::norms, 8);
+    std::vector<float> ones(8, 1.0f), halves(8, 0.5f);
+    const auto g1 = en.batch_grad_sum(fe.inputs.data(), fe.labels.data());
+    const auto w1 = en.weighted_grad_sum(fe.inputs.data(), fe.labels.data(), ones.data());
+    const auto wh = en.weighted_grad_sum(fe.inputs.data(), fe.labels.data(), halves.data());
+    CHECK(g1 == w1);
+    for (size_t i = 0; i < g1.size(); ++i) CHECK(std::fabs(wh[i] - 0.5f * g1[i]) <= 1e-6f * (1.0f + std::fabs(g1[i])));
+    DpConfig<float> mb = cfg;
+    mb.microbatch = 2;
+    CHECK(throws<ConfigError>([&] { dpsgd_step(e, en, fe.inputs, fe.labels, mb, 0); }));
+  }
+
   // labels outside [0, classes) are an IndexError; parameters untouched
   auto before = model.flat();
   auto badlab = data.labels;

@@ -290,16 +290,36 @@ __global__ void conv_db_pex_kernel(const float* __restrict__ g, int BD, int P,
 
 // ---- parameter-free layers ----------------------------------------------------
 
+// flat index e of a (BC, H, W) tensor -> (bc, y, x); 32-bit divisions when
+// the tensor allows (64-bit division is a long instruction sequence and was
+// the bound of the pooling kernels)
+__device__ __forceinline__ void split_bchw(size_t e, int H, int W, size_t& bc, int& y, int& x,
+                                           bool small) {
+  if (small) {
+    const unsigned ee = (unsigned)e, hw = (unsigned)(H * W);
+    const unsigned b = ee / hw, r = ee - b * hw;
+    const unsigned yy = r / (unsigned)W;
+    bc = b;
+    y = (int)yy;
+    x = (int)(r - yy * (unsigned)W);
+  } else {
+    x = (int)(e % W);
+    y = (int)((e / W) % H);
+    bc = e / ((size_t)W * H);
+  }
+}
+
 // max/avg pooling via window reduction (tape.cpp:269-282): avg = sum * 1/k^2.
 __global__ void pool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int BC,
                                 int H, int W, int Ho, int Wo, int k, int s, int is_max) {
   const size_t total = (size_t)BC * Ho * Wo;
+  const bool small = total < (1ull << 31);
   const float inv = 1.0f / float(k * k);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
        e += (size_t)gridDim.x * blockDim.x) {
-    const int ox = (int)(e % Wo);
-    const int oy = (int)((e / Wo) % Ho);
-    const size_t bc = e / ((size_t)Wo * Ho);
+    size_t bc;
+    int oy, ox;
+    split_bchw(e, Ho, Wo, bc, oy, ox, small);
     const float* xp = x + bc * H * W;
     float m = 0.0f, sum = 0.0f;
     bool first = true;
@@ -321,12 +341,13 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
                                 int BC, int H, int W, int Ho, int Wo, int k, int s,
                                 int is_max) {
   const size_t total = (size_t)BC * H * W;
+  const bool small = total < (1ull << 31);
   const float inv = 1.0f / float(k * k);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
        e += (size_t)gridDim.x * blockDim.x) {
-    const int ix = (int)(e % W);
-    const int iy = (int)((e / W) % H);
-    const size_t bc = e / ((size_t)W * H);
+    size_t bc;
+    int iy, ix;
+    split_bchw(e, H, W, bc, iy, ix, small);
     const float* xp = x + bc * H * W;
     const float* gp = g + bc * Ho * Wo;
     float acc = 0.0f;

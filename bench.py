@@ -47,7 +47,7 @@ MODELS = {
              0.0238, "dense 104-50-10; P=5,760"),
     "logreg": (0, {}, 2, 256, 300000, "DPSGD examples/sec at batch 256 (logistic regression)",
                0.0006, "dense 104-1, sigmoid head; P=105"),
-    "embed": (4, {"hidden": 100}, 5, 512, 1024,
+    "embed": (4, {"hidden": 100}, 5, 512, 16384,
               "DPSGD examples/sec at batch 512 (IMDb-shaped embedding)", 0.05,
               "embedding 10,004x100, mean-pool, dense 100-2; P=1,000,602"),
 }

@@ -1178,6 +1178,10 @@ struct Engine {
     A.words = emb_words;
     A.nparts = np;
     A.mode = mode;
+    if (cap_step_base) {
+      A.step_base = cap_step_base;
+      A.step_off = cap_step_off;
+    }
     const int rows_per_cta = 8;
     finalize_norms_kernel<<<((int)B + 127) / 128, 128, 0, s>>>(d_parts, np, (int)B, d_wts);
     const int nk0 = mark(s, "embed_norms");
@@ -1942,8 +1946,14 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
     // result slots: K chunk slots of C, then the head / remainder slots
     C = std::min<int64_t>(C, Engine::kResSlots / (K + 1));
-    const bool chunked = (en.fused_mnist || en.mlp_fused) && en.world == 1 && cfg->microbatch == 1 &&
-                         en.graph_enabled && C > 1 && steps >= C;
+    // (every one-process schedule: the layer-wise one bakes each step's input
+    // pointer into its chunk graph node; noise takes the step from the device)
+    const bool chunked = en.world == 1 && cfg->microbatch == 1 && en.graph_enabled && C > 1 &&
+                         steps >= C;
+    // the fused schedules take input pointers as node parameters: their
+    // per-step graphs can read any batch inside a chunk slot; the layer-wise
+    // schedule launches those steps directly
+    const bool ptr_params = en.fused_mnist || en.mlp_fused;
     if (!chunked) C = 1;
     if (C > 1) en.ensure_chunk_ring(C);
     const int64_t nchunks = (steps + C - 1) / C, nfull = steps / C;
@@ -1978,7 +1988,12 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
       const float* xs = xslot(sl) + j * en.B * en.in_row;
       const float* ys = yslot(sl) + j * en.B;
       en.push_args(en.make_args(*cfg, step0 + s, xs, ys));
-      en.launch_step(xs, ys, cfg->microbatch);
+      if (C > 1 && !ptr_params) {
+        en.kernels_last = en.enqueue_step(en.stream, xs, ys, cfg->microbatch);
+        PGB_CUDA(cudaGetLastError());
+      } else {
+        en.launch_step(xs, ys, cfg->microbatch);
+      }
       // the step's result read back every step (norms, clipped count)
       cudaStream_t rs = ring ? en.out_stream : en.stream;
       if (ring) {

@@ -1256,6 +1256,8 @@ struct EmbAggLaunch {
   float* params;
   float* sum_out;      // mode 1
   const DevError* err;
+  const long long* step_base;  // multi-step graphs: the noise step on the device
+  int step_off;
   int p, B, L, E, V, words, nparts, mode;
 };
 
@@ -1272,7 +1274,8 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
   const StepArgs& a = A.a;
   const float invL = 1.0f / float(A.L);
   const bool failed = A.err && A.err->code != 0;
-  const uint64_t key = stream_key(a.seed, noise_stream(a.step, A.p));
+  const uint64_t key =
+      stream_key(a.seed, noise_stream(A.step_base ? *A.step_base + A.step_off : a.step, A.p));
   const long long E = A.E;
   __shared__ int lst_i[8][32], lst_c[8][32];
   __shared__ float lst_s[8][32];

@@ -361,3 +361,33 @@ def test_fcnn_epoch_driver_matches_oracle(P, O):
         p_prev, p64 = p64, p_new
     assert clipped == total
     _check_params(eng.get_flat_params(), p64, p_prev)
+
+
+@pytest.mark.parametrize("name", ["embed", "cifar"])
+def test_layerwise_epoch_driver_matches_step_calls(P, O, name):
+    """pgb_run_epoch on the layer-wise schedule (chunk graphs with each step's
+    input pointer baked in, noise step read on the device; head and remainder
+    steps launched directly) gives bitwise the parameters, norms and clip
+    counts of the same steps issued one dpsgd_step call at a time."""
+    if name == "embed":
+        desc = P.build_desc(P.ModelKind.embed, P.ModelOptions(seq_len=16, vocab=50, hidden=8))
+        B, steps, strat, C_ = 8, 21, P.Strategy.jacmm, 0.05
+    else:
+        desc = P.build_desc(P.ModelKind.cifar_cnn)
+        B, steps, strat, C_ = 4, 19, P.Strategy.groupconv, 1.0
+    data = P.synth_for_model(desc, steps * B, 3, pinned=True)
+    cfg = P.DpConfig(clip_norm=C_, noise_multiplier=1.1, learning_rate=0.1, seed=2)
+    m1 = P.build_from_desc(desc, 0)
+    e1 = P.GradEngine(m1, strat, B)
+    norms = np.empty(steps * B, np.float32)
+    _, clipped = P.run_epoch(e1, m1, data, cfg, 30, norms)
+    m2 = P.build_from_desc(desc, 0)
+    e2 = P.GradEngine(m2, strat, B)
+    total = 0
+    for s in range(steps):
+        sl = slice(s * B, (s + 1) * B)
+        rep = P.dpsgd_step(m2, e2, data.inputs[sl], data.labels[sl], cfg, 30 + s)
+        np.testing.assert_array_equal(norms[sl], rep.pre_clip_norms)
+        total += rep.clipped_count
+    assert clipped == total
+    np.testing.assert_array_equal(e1.get_flat_params(), e2.get_flat_params())

@@ -154,3 +154,26 @@ def test_aggregate_matches_reference_fp32_order(P, O):
         pu = np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
         assert (pu == 0).mean() > 0.9, f"bitwise fraction {(pu == 0).mean()}"
         assert np.max(np.abs(got - want)) <= 2e-6 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("kind,B,strat", [(0, 7, 2), (1, 13, 3), (1, 1, 2), (2, 5, 4)])
+def test_ragged_batches_match_oracle(P, O, kind, B, strat):
+    """Batches that fill neither a CTA of the fused dense kernel (8 examples)
+    nor a pair of the MNIST kernel: three noised steps against the oracle."""
+    desc = P.build_desc(P.ModelKind(kind))
+    od = O.build_desc(kind)
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 4)
+    eng = P.GradEngine(model, P.Strategy(strat), B)
+    cfg = P.DpConfig(clip_norm=0.7, noise_multiplier=1.1, learning_rate=0.1, seed=6)
+    p64 = O.init_params(od, 0)
+    x64, y64 = O.synth(od, B, 4)
+    for step in range(3):
+        rep = P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, step)
+        p_new, wn, wclip, _ = O.dpsgd_step(od, x64, y64, p64, 0.7, 1.1, 0.1, 1, 6, step)
+        assert np.max(np.abs(rep.pre_clip_norms - wn) / wn) < TOL
+        assert rep.clipped_count == wclip
+        got = model.flat_params().astype(np.float64)
+        delta = np.abs(p_new - p64).max()
+        assert np.all(np.abs(got - p_new) <= 3e-7 * np.abs(p_new) + TOL * delta)
+        p64 = p_new

@@ -132,6 +132,7 @@ struct Engine {
   bool fused_mnist = false;  // whole per-example pass in one kernel
   bool mlp_fused = false;    // dense-only models: one warp-per-example kernel (mlp_fused.cuh)
   bool mlp_attr = false;
+  bool emb_head = false;     // embedding models: dense head in mlp_kernel on the sparse path
   bool mnist_tc = false;     // ... with the conv GEMMs on tcgen05 (mnist_tc.cuh)
   bool agg_in_kernel = false;  // ... and the aggregation after an in-kernel grid barrier
   bool fuse_agg_next = false;  // set by enqueue_step for the fused launch it makes
@@ -481,6 +482,25 @@ struct Engine {
         want((void**)&d_emb_cnt, sizeof(int) * B * Lq);
         want((void**)&d_emb_nd, sizeof(int) * B);
         want((void**)&d_emb_bits, sizeof(unsigned) * L.spec.in * emb_words);
+        // the dense head after the pool through mlp_kernel (dense / relu only,
+        // within its widths; the embedding first)
+        bool ok = l == 0 && std::getenv("PGB_NO_EMB_HEAD") == nullptr &&
+                  desc.classes <= mlp::kMaxClasses && L.spec.out <= mlp::kMaxWidth;
+        int nd = 0, firstp = -1;
+        for (int j = l + 2; j < n && ok; ++j) {
+          const pgb_layer_spec& sp = desc.layers[j];
+          if (sp.kind == PGB_DENSE) {
+            ok = sp.in <= mlp::kMaxWidth && sp.out <= mlp::kMaxWidth;
+            if (firstp < 0) firstp = layers[j].pblock;
+            ++nd;
+          } else {
+            ok = sp.kind == PGB_RELU && layers[j].alias;
+          }
+        }
+        emb_head = ok && nd >= 1 && nd <= mlp::kMaxLayers && l + 1 < n &&
+                   desc.layers[l + 1].kind == PGB_SEQ_AVGPOOL &&
+                   desc.layers[n - 1].kind == PGB_DENSE &&
+                   P - param_off[firstp] <= mlp::kMaxParams;
       }
     }
     d_dense_g.assign(n, nullptr);
@@ -881,24 +901,34 @@ struct Engine {
   }
 
   // dense-only models: the whole per-example pass in mlp::mlp_kernel
-  int enqueue_mlp(cudaStream_t s, const float* x_slot, const float* y_slot) {
+  // head: the dense layers after an embedding + seq_avgpool (their input is
+  // the pooled activation, their input cotangent feeds the embedding block)
+  int enqueue_mlp(cudaStream_t s, const float* x_slot, const float* y_slot, bool head = false) {
     mlp::Params prm{};
+    int first = -1;
     for (const Layer& L : layers) {
       if (L.spec.kind != PGB_DENSE) continue;
+      if (first < 0) first = L.pblock;
       mlp::DenseLayer& D = prm.L[prm.n++];
       D.in = (int)L.spec.in;
       D.out = (int)L.spec.out;
       D.relu = L.fused_relu ? 1 : 0;
       D.pW = L.pblock;
       D.pb = L.pblock + 1;
-      D.offW = (int)param_off[L.pblock];
-      D.offb = (int)param_off[L.pblock + 1];
       D.act = L.act_out;
       D.gout = L.gout;
     }
+    // the dense blocks are the tail of the parameter vector (layer order)
+    const long long off0 = param_off[first];
+    for (int l = 0; l < prm.n; ++l) {
+      prm.L[l].offW = (int)(param_off[prm.L[l].pW] - off0);
+      prm.L[l].offb = (int)(param_off[prm.L[l].pb] - off0);
+    }
     prm.params = d_params;
-    prm.P = (int)P;
-    prm.xin = d_xin;
+    prm.stage_off = (int)off0;
+    prm.P = (int)(P - off0);
+    prm.xin = head ? nullptr : d_xin;
+    prm.gin = head ? layers[emb_layer].gout : nullptr;
     prm.step_base = cap_step_base;
     prm.step_off = cap_step_off;
     prm.xring = cap_xring;
@@ -913,7 +943,11 @@ struct Engine {
     prm.B = (int)B;
     prm.classes = (int)desc.classes;
     prm.err = d_err;
-    const size_t smem = sizeof(float) * (size_t)P;
+    if (head) {
+      prm.x = layers[emb_layer].act_out;  // pooled (B, E)
+      prm.xring = nullptr;
+    }
+    const size_t smem = sizeof(float) * (size_t)prm.P;
     if (!mlp_attr) {  // once per engine (the attribute is per device)
       PGB_CUDA(cudaFuncSetAttribute(mlp::mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(sizeof(float) * mlp::kMaxParams)));
@@ -921,7 +955,26 @@ struct Engine {
     }
     mlp::mlp_kernel<<<(unsigned)((B + mlp::kWarps - 1) / mlp::kWarps), 32 * mlp::kWarps, smem,
                       s>>>(prm);
-    return mark(s, "mlp_fused");
+    return mark(s, head ? "embed_head" : "mlp_fused");
+  }
+
+  // embedding models on the sparse step path: pooled forward, the dense head
+  // in one kernel (forward, loss, backward to the pooled cotangent, ghost
+  // norms), then the sparse embedding index
+  int enqueue_embed_head_grads(cudaStream_t s, const float* x_slot, const float* y_slot) {
+    int nk = 0;
+    const Layer& Le = layers[emb_layer];
+    const int E = (int)Le.spec.out, V = (int)Le.spec.in, Bi = (int)B;
+    const float* Wt = d_params + param_off[Le.pblock];
+    embed_pool_fwd_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
+        x_slot, Wt, Le.act_out, Bi, (int)Le.in.d[0], E, V, d_err);
+    nk += mark(s, "embed_pool_fwd");
+    nk += enqueue_mlp(s, x_slot, y_slot, true);
+    embed_index_kernel<<<Bi, 256, 0, s>>>(x_slot, Le.gout, (int)Le.in.d[0], E, V, emb_words,
+                                          d_emb_tok, d_emb_cnt, d_emb_nd, d_emb_bits, d_parts,
+                                          nparts, Le.pblock);
+    nk += mark(s, "embed_index");
+    return nk;
   }
 
   // Per-example gradient sources for the batch (the reference's
@@ -929,6 +982,7 @@ struct Engine {
   int enqueue_grads(cudaStream_t s, const float* x_slot, const float* y_slot) {
     if (fused_mnist) return enqueue_fused_mnist(s, x_slot, y_slot);
     if (mlp_fused) return enqueue_mlp(s, x_slot, y_slot);
+    if (emb_head && sparse_embed_next) return enqueue_embed_head_grads(s, x_slot, y_slot);
     int nk = enqueue_forward(s, x_slot, y_slot);
     const int n = desc.n_layers;
     const int Bi = (int)B;
@@ -1418,7 +1472,9 @@ struct Engine {
           sg.agg = nd;
           sg.agg_args = *L;
         }
-      } else if (kp.func == (void*)mlp::mlp_kernel) {
+      } else if (kp.func == (void*)mlp::mlp_kernel &&
+                 static_cast<const mlp::Params*>(kp.kernelParams[0])->gin == nullptr) {
+        // (an embedding head reads the pooled activation, not the step input)
         sg.mlp = nd;
         sg.mlp_args = *static_cast<const mlp::Params*>(kp.kernelParams[0]);
       } else if (kp.func == (void*)embed_agg_kernel) {

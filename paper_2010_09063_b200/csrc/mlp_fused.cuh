@@ -33,8 +33,9 @@ struct DenseLayer {
 struct Params {
   int n;  // dense layers
   DenseLayer L[kMaxLayers];
-  const float* params;  // flat parameters (P floats), staged whole into shared memory
-  int P;
+  const float* params;  // flat parameters; [stage_off, stage_off + P) staged into shared memory
+  int P, stage_off;     // (offW / offb are relative to stage_off)
+  float* gin;           // optional (B, L[0].in): cotangent of the input (an embedding head)
   const float* x;  // (B, L[0].in)
   const float* y;  // (B) labels as float
   float* xin;      // (B, L[0].in): the inputs again, the ghost factor a of layer 0
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
   const int i = blockIdx.x * kWarps + warp;
   // stage the parameters: every load in flight at once instead of one cold
   // L1 miss per weight row in the dependent FMA chains below
-  for (int j = threadIdx.x; j < P.P; j += 32 * kWarps) wsm[j] = __ldg(P.params + j);
+  for (int j = threadIdx.x; j < P.P; j += 32 * kWarps) wsm[j] = __ldg(P.params + P.stage_off + j);
   __syncthreads();
   if (i >= P.B) return;  // warp-level work only: no CTA barriers below
   float(*A)[kMaxWidth] = act[warp];
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
   for (int k = lane; k < in0; k += 32) {
     const float v = __ldg(X + (size_t)i * in0 + k);
     A[0][k] = v;
-    P.xin[(size_t)i * in0 + k] = v;
+    if (P.xin) P.xin[(size_t)i * in0 + k] = v;
   }
   __syncwarp();
 
@@ -163,18 +164,20 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
       P.parts[(size_t)i * P.nparts + L.pW] = asq[l] * dsq;
       P.parts[(size_t)i * P.nparts + L.pb] = dsq;
     }
-    if (l == 0) break;
-    const DenseLayer& D = P.L[l - 1];
+    if (l == 0 && !P.gin) break;
     float* gn = grad[warp][cur ^ 1];
+    const bool relu_below = l > 0 && P.L[l > 0 ? l - 1 : 0].relu;
+    float* gdst = l > 0 ? P.L[l > 0 ? l - 1 : 0].gout : P.gin;
     for (int k = lane; k < L.in; k += 32) {
       const float* w = wsm + L.offW + k * L.out;
       float acc = 0.0f;
 #pragma unroll 8
       for (int c = 0; c < L.out; ++c) acc = fmaf(gl[c], w[c], acc);
-      const float v = (D.relu && !(A[l][k] > 0.0f)) ? 0.0f : acc;
+      const float v = (relu_below && !(A[l][k] > 0.0f)) ? 0.0f : acc;
       gn[k] = v;
-      D.gout[(size_t)i * D.out + k] = v;
+      gdst[(size_t)i * L.in + k] = v;
     }
+    if (l == 0) break;
     __syncwarp();
     cur ^= 1;
   }

@@ -265,7 +265,7 @@ def conv_gemm_flops(desc, B):
     return total
 
 
-def aggregate_bytes(desc, B, fused, c2_pairs=False):
+def aggregate_bytes(desc, B, fused, c2_pairs=False, sparse_embed=False):
     """Bytes the aggregation kernel must read/write: per-example gradient
     sources (materialised rows: B*|p|*4; factored dense blocks: B*(in+out)*4;
     with c2_pairs the MNIST kernel's second conv weight block arrives as
@@ -274,6 +274,7 @@ def aggregate_bytes(desc, B, fused, c2_pairs=False):
     total = 0
     pi = 0
     nconv = 0
+    skip_p = 0
     for l in desc.layers:
         if l.kind == LayerKind.dense:
             total += B * (l.in_ + l.out) * 4 + B * l.out * 4
@@ -284,9 +285,14 @@ def aggregate_bytes(desc, B, fused, c2_pairs=False):
             nconv += 1
             pi += 2
         elif l.kind == LayerKind.embedding:
-            total += B * l.in_ * l.out * 4
+            # the sparse step path: embed_agg_kernel (its own roofline line),
+            # not the aggregation kernel, sums this block
+            if not sparse_embed:
+                total += B * l.in_ * l.out * 4
+            else:
+                skip_p += l.in_ * l.out
             pi += 1
-    P = desc.param_count()
+    P = desc.param_count() - skip_p
     return total + 2 * P * 4 + B * 8 * (1 if fused else pi) + B * 4
 
 
@@ -450,7 +456,8 @@ def run_ours(args):
     if "aggregate" in by_name:
         agg_b = aggregate_bytes(desc, BATCH, fused,
                                 c2_pairs=("mnist_tc" in by_name and
-                                          os.environ.get("PGB_C2_PAIRS", "1") != "0"))
+                                          os.environ.get("PGB_C2_PAIRS", "1") != "0"),
+                                sparse_embed="embed_agg" in by_name)
         am = by_name["aggregate"]
         atraffic, _ = ncu_traffic(args.model, "aggregate_kernel")
         agg = {"kernel": "aggregate", "bound": "hbm", "achieved": agg_b / (am * 1e-3) / 1e9,
@@ -461,6 +468,23 @@ def run_ours(args):
             roof = agg
     else:
         agg = None
+    if "embed_agg" in by_name:
+        # sparse embedding aggregation: per table row the clipped sum over the
+        # examples holding it, noise, mean, update. Algorithmic bytes: the
+        # table read + write, the pooled cotangents, the per-example distinct
+        # tokens and counts, the row bitmaps
+        from paper_2010_09063_b200 import LayerKind
+        el = next(l for l in desc.layers if l.kind == LayerKind.embedding)
+        V, E = el.in_, el.out
+        Lq = int(desc.input_shape[0])
+        eb = 2 * V * E * 4 + BATCH * E * 4 + 2 * BATCH * Lq * 4 + V * ((BATCH + 31) // 32) * 4
+        em = by_name["embed_agg"]
+        roof = {"kernel": "embed_agg", "bound": "hbm", "achieved": eb / (em * 1e-3) / 1e9,
+                "peak": hbm, "unit": "GB/s", "frac": eb / (em * 1e-3) / 1e9 / hbm,
+                "traffic": None, "algorithmic_bytes": eb, "share_of_step": em / step_ms,
+                "avg_launch_us": em * 1e3,
+                "note": "latency-bound (per-row example lists, fp64 Box-Muller noise for V*E "
+                        "elements)"}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

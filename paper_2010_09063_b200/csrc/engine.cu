@@ -705,7 +705,11 @@ struct Engine {
       PGB_CUDA(cudaFuncSetAttribute(mnist::fused_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(mnist::Smem)));
-      PGB_CUDA(cudaFuncSetAttribute(mnist::tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      PGB_CUDA(cudaFuncSetAttribute(mnist::tc_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(mnist::TcSmem)));
+      PGB_CUDA(cudaFuncSetAttribute(mnist::tc_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(mnist::TcSmem)));
     }
     // reference init is the default parameter state (models::build, seed 0)
@@ -890,9 +894,14 @@ struct Engine {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        PGB_CUDA(cudaLaunchKernelEx(&cfg, mnist::tc_kernel, prm, L));
+        PGB_CUDA(cudaLaunchKernelEx(&cfg, mnist::tc_kernel<false>, prm, L));
       } else {
-        mnist::tc_kernel<<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(prm, L);
+        if (fuse_agg_next)
+          mnist::tc_kernel<true><<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(
+              prm, L);
+        else
+          mnist::tc_kernel<false><<<(unsigned)((B + 1) / 2), mnist::TNT, sizeof(mnist::TcSmem), s>>>(
+              prm, L);
       }
       return mark(s, fuse_agg_next ? "mnist_tc_step" : "mnist_tc");
     }
@@ -1483,10 +1492,12 @@ struct Engine {
       } else if (kp.func == (void*)noise_update_kernel) {
         sg.noise = nd;
         sg.noise_args = *static_cast<const NoiseLaunch*>(kp.kernelParams[0]);
-      } else if (kp.func == (void*)mnist::fused_kernel || kp.func == (void*)mnist::tc_kernel) {
+      } else if (kp.func == (void*)mnist::fused_kernel ||
+                 kp.func == (void*)mnist::tc_kernel<false> ||
+                 kp.func == (void*)mnist::tc_kernel<true>) {
         sg.fused = nd;
         sg.fused_args = *static_cast<const mnist::Params*>(kp.kernelParams[0]);
-        if (kp.func == (void*)mnist::tc_kernel) {
+        if (kp.func != (void*)mnist::fused_kernel) {
           sg.fused_tc = true;
           sg.fused_agg = *static_cast<const AggLaunch*>(kp.kernelParams[1]);
         }

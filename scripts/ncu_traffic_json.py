@@ -28,7 +28,7 @@ def val(r, name):
 
 kernels = {}
 for r in rows[2:]:
-    name = r[col["Kernel Name"]].split("(")[0].split("::")[-1].strip()
+    name = r[col["Kernel Name"]].split("(")[0].split("::")[-1].split("<")[0].strip()
     if name in kernels:
         continue
     rd = val(r, "dram__bytes_read.sum") or 0.0

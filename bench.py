@@ -5,16 +5,24 @@ P=26,010), C=1.0, sigma=1.1, lr=0.1, synthetic MNIST-shaped data.
     python bench.py [--gpus N --steps K --warmup W] [--model cifar_cnn ...]
     python bench.py --impl reference ...          # the reference's CPU path
 
-Under torchrun each rank drives one GPU with 256 examples per step (weak
-scaling: global DP batch 256*N, one NCCL all-reduce of the clipped sum per
-step inside the engine's CUDA graph). Prints ONE JSON line on rank 0.
+Under torchrun the global DP batch (256) is sharded across the N ranks
+(SURVEY 8(e): rank r takes examples [r*B/N, (r+1)*B/N) of every global batch;
+strong scaling), one NCCL all-reduce of the clipped sum per step captured in
+the engine's multi-step CUDA graphs, the same noise on every rank from the
+shared seed. --weak keeps the per-GPU batch at 256 instead. Prints ONE JSON
+line on rank 0.
 
 value  : device-resident inputs (a synthetic dataset larger than the 126 MB
-         L2 -- 60,000 MNIST images, 188 MB -- cycled batch by batch), K steps
-         timed with CUDA events on the engine stream, max over ranks.
-e2e    : the public epoch driver pgb_run_epoch on PINNED HOST batches: every
+         L2 -- 60,000 MNIST images, 188 MB -- cycled batch by batch), W warm-up
+         steps, every CUDA graph of the timed call built untimed
+         (pgb_prepare_steps), then K steps timed with CUDA events on the engine
+         stream, max over ranks.
+e2e    : the public epoch driver pgb_run_epoch on PINNED HOST batches over
+         full epochs of the dataset (MNIST: 60,000 examples = 234 steps): every
          step copies its batch H2D and reads its result (per-example norms +
-         clipped count) back D2H; wall time, max over ranks.
+         clipped count) back D2H; the median epoch time over --epochs timed
+         epochs after one untimed one (harness.cpp:85-167 reports the median
+         epoch), max over ranks.
 roofline: per-kernel device times from CUDA events around each launch of the
          same schedule (pgb_profile_steps), algorithmic work per SURVEY 8(d).
 """
@@ -149,11 +157,12 @@ def ncu_counters(model, kernel):
     return {}
 
 
-def workload_config(model, world, batch_override=0):
+def workload_config(model, world, per_gpu=0, global_batch=0):
     kind, opts, strat, batch, data_n, _, _, arch = MODELS[model]
-    batch = batch_override or batch
+    per_gpu = per_gpu or batch
+    global_batch = global_batch or per_gpu * world
     return {"workload": f"{model} DPSGD step ({arch})", "model": model,
-            "global_batch": batch * world, "per_gpu_batch": batch, "seq_len": None,
+            "global_batch": global_batch, "per_gpu_batch": per_gpu, "seq_len": None,
             "parallelism": f"dp{world}", "clip_norm": CLIP, "noise_multiplier": SIGMA,
             "learning_rate": LR,
             "l2": f"inputs larger than L2 where the dataset allows: {data_n}-example resident "
@@ -225,7 +234,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * t / max(1, min(nsteps)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (io::synth_for_model, seed 0)", "impl": "reference",
-        "config": workload_config(args.model, world, getattr(args, 'batch', 0)),
+        "config": workload_config(args.model, 1, args.batch or MODELS[args.model][3]),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 2 * procs, "kind": "reference",
                          "sample": f"{procs} processes x up to {args.steps} reference "
                                    f"dpsgd_step(B={batch}, graph, fp32) capped at "
@@ -296,6 +305,20 @@ def aggregate_bytes(desc, B, fused, c2_pairs=False, sparse_embed=False):
     return total + 2 * P * 4 + B * 8 * (1 if fused else pi) + B * 4
 
 
+_PINNED = []
+
+
+def _pinned(a):
+    """A copy of `a` in page-locked host memory (the e2e leg's H2D source)."""
+    import numpy as np
+    import torch
+    t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+    out = t.numpy()
+    np.copyto(out, a)
+    _PINNED.append(t)  # the buffer lives as long as the process
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -305,11 +328,18 @@ def run_ours(args):
     from paper_2010_09063_b200 import _lib
     from paper_2010_09063_b200.dist import exchange_unique_id
 
-    kind, opts, strat, BATCH, DATA_N, METRIC, MFLOP, _ = MODELS[args.model]
+    kind, opts, strat, GBATCH, DATA_N, METRIC, MFLOP, _ = MODELS[args.model]
     if args.batch:  # batch sweeps (BASELINE config 2: FFNN at batch 16-512)
-        METRIC = METRIC.replace(f"batch {BATCH}", f"batch {args.batch}")
-        BATCH = args.batch
+        METRIC = METRIC.replace(f"batch {GBATCH}", f"batch {args.batch}")
+        GBATCH = args.batch
     rank, local, world = dist_env()
+    if args.weak:
+        BATCH = GBATCH            # per-GPU batch fixed, global batch grows with N
+        GBATCH = BATCH * world
+    else:
+        if GBATCH % world:
+            raise SystemExit(f"global batch {GBATCH} is not divisible by {world} ranks")
+        BATCH = GBATCH // world   # the global batch sharded across the ranks
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
@@ -325,12 +355,20 @@ def run_ours(args):
     cfg = Pk.DpConfig(CLIP, SIGMA, LR, 1, SEED)
     ccfg = cfg.to_c()
 
-    # synthetic dataset (this rank's stream: seed + rank), pinned on the host
-    data = Pk.synth_for_model(desc, DATA_N, SEED + rank, pinned=True)
+    # synthetic dataset (io::synth_for_model, seed 0), the same on every rank;
+    # this rank keeps its shard of every global batch, pinned on the host
+    nbatches = DATA_N // GBATCH
+    full = Pk.synth_for_model(desc, nbatches * GBATCH, SEED)
+    row = int(np.prod(desc.input_shape))
+    G = GBATCH // BATCH
+    r = rank % G
+    xs = full.inputs.reshape(nbatches, G, BATCH, row)[:, r].reshape(
+        (nbatches * BATCH,) + tuple(full.inputs.shape[1:]))
+    ys = full.labels.reshape(nbatches, G, BATCH)[:, r].reshape(nbatches * BATCH)
+    data = Pk.Dataset(_pinned(xs), _pinned(ys), full.name, nbatches * BATCH, full.classes)
+    del full
     dx = torch.from_numpy(data.inputs).to(f"cuda:{dev}")
     dy = torch.from_numpy(data.labels).to(f"cuda:{dev}")
-    nbatches = DATA_N // BATCH
-    row = int(np.prod(desc.input_shape))
 
     sp = C.c_void_p()
     _lib.check(_lib.lib.pgb_device_stream(engine.handle, C.byref(sp)))
@@ -361,6 +399,10 @@ def run_ours(args):
 
     run_steps(0, args.warmup)
     _lib.check(_lib.lib.pgb_synchronize(engine.handle, None, None))
+    # one-time setup of the timed call (its multi-step graphs), untimed
+    _lib.check(_lib.lib.pgb_prepare_steps(
+        engine.handle, C.c_void_p(dx.data_ptr()), C.c_void_p(dy.data_ptr()), nbatches,
+        args.steps, C.byref(ccfg)))
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -374,26 +416,26 @@ def run_ours(args):
         _lib.check(_lib.lib.pgb_synchronize(engine.handle, None, None))
     barrier()
     t = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
-    value = args.steps * BATCH * world / t
+    value = args.steps * GBATCH / t
     kps = engine.info().kernels_per_step
 
-    # ---- e2e: public epoch driver from pinned host memory -------------------
-    e_steps = max(1, min(args.steps, nbatches))
-    sub = Pk.Dataset(data.inputs[: e_steps * BATCH], data.labels[: e_steps * BATCH],
-                     data.name, e_steps * BATCH, data.classes)
+    # ---- e2e: public epoch driver from pinned host memory, full epochs ------
+    e_steps = nbatches
     norms = np.empty(e_steps * BATCH, np.float32)
-    # one untimed warm-up epoch over the same batches: builds the driver's
-    # multi-step graphs for every input-chunk slot and touches the pinned
-    # pages the timed epoch copies from (one-time setup)
-    warm = sub
-    Pk.run_epoch(engine, model, warm, cfg, 0)
+    # one untimed epoch: builds the driver's multi-step graphs for every
+    # input-chunk slot and touches the pinned pages (one-time setup)
+    Pk.run_epoch(engine, model, data, cfg, 0)
     barrier()
-    w0 = time.perf_counter()
-    Pk.run_epoch(engine, model, sub, cfg, 10 ** 6, norms)
-    w1 = time.perf_counter()
+    epoch_s = []
+    for ep in range(args.epochs):
+        barrier()
+        w0 = time.perf_counter()
+        Pk.run_epoch(engine, model, data, cfg, (ep + 1) * e_steps, norms)
+        w1 = time.perf_counter()
+        epoch_s.append(max_over_ranks(w1 - w0))
     barrier()
-    e2e_t = max_over_ranks(w1 - w0)
-    e2e = e_steps * BATCH * world / e2e_t
+    e2e_t = statistics.median(epoch_s)
+    e2e = e_steps * GBATCH / e2e_t
 
     # ---- per-kernel device time of the same schedule ------------------------
     hbm, bf16, peak_kind = peaks()
@@ -504,14 +546,18 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (bit-identical to io::synth_for_model, seed 0+rank); random-init "
-                    "params (models::build seed 0)",
-            "config": workload_config(args.model, world, getattr(args, 'batch', 0)),
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (bit-identical to io::synth_for_model, seed 0; rank r takes its "
+                    "shard of every global batch); random-init params (models::build seed 0)",
+            "config": workload_config(args.model, world, BATCH, GBATCH),
             "e2e": {"value": e2e, "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * row * 4 + BATCH * 4,
                     "d2h_bytes_per_step": BATCH * 4 + 8,
-                    "api": "pgb_run_epoch (pinned host batches; every step's inputs copied H2D and its norms + clip count read back D2H inside the timed region, 8 steps per copy / graph launch)"},
+                    "median_epoch_s": e2e_t, "epoch_examples": e_steps * GBATCH,
+                    "epochs_timed": args.epochs,
+                    "epoch_s": [round(v, 6) for v in epoch_s],
+                    "api": "pgb_run_epoch over full epochs (pinned host batches; every step's inputs copied H2D and its norms + clip count read back D2H inside the timed region, 8 steps per copy / graph launch); value = examples per epoch / median epoch seconds"},
             "roofline": roof,
             "aggregate_roofline": agg,
             "kernels_us": {n: round(m * 1e3, 3) for n, m in by_name.items()},
@@ -521,6 +567,7 @@ def run_ours(args):
             "kernels_per_step": kps,
             "host_issue_us_per_step": round(host_issue * 1e6, 2),
             "e2e_us_per_step": round(e2e_t / e_steps * 1e6, 2),
+            "median_epoch_s": e2e_t,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -539,7 +586,11 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0,
-                    help="per-GPU batch override (default: the config's batch)")
+                    help="global batch override (default: the config's batch)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: --batch (or the config's batch) per GPU")
+    ap.add_argument("--epochs", type=int, default=5,
+                    help="timed full epochs of the e2e leg (median reported)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

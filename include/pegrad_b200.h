@@ -213,15 +213,23 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y,
 pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_y,
                                 int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg,
                                 int64_t step0, int64_t* launches_out);
+/* Builds (captures and instantiates, without running) every CUDA graph that
+ * pgb_run_steps_device(e, d_x, d_y, n_batches, n_steps, cfg, ...) will launch,
+ * so a timed run that follows contains no one-time setup. Synchronous. */
+pgb_status pgb_prepare_steps(pgb_engine* e, const float* d_x, const float* d_y,
+                             int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg);
 /* Unsigned-byte IDX containers (io::load_idx / load_mnist,
  * proj/core/src/dataset.cpp:35-112): same validation and FormatError / IoError
  * byte-offset messages. pgb_idx_info: rank (<= 4), dims, element count.
  * pgb_load_idx: float(byte) / scale_div (scale_div <= 0: no division) into a
- * host buffer; pgb_load_idx_device: the bytes cross PCIe as bytes and are
- * decoded on `device` into d_out with the same arithmetic. */
+ * host buffer of `capacity` floats; pgb_load_idx_device: the bytes cross PCIe
+ * as bytes and are decoded on `device` into d_out (`capacity` floats) with the
+ * same arithmetic. A payload larger than `capacity` (e.g. the file grew since
+ * pgb_idx_info) fails with PGB_ERR_CONTRACT and writes nothing. */
 pgb_status pgb_idx_info(const char* path, int32_t* rank, int64_t* dims, int64_t* count);
-pgb_status pgb_load_idx(const char* path, float scale_div, float* out);
-pgb_status pgb_load_idx_device(const char* path, int32_t device, float scale_div, float* d_out);
+pgb_status pgb_load_idx(const char* path, float scale_div, float* out, int64_t capacity);
+pgb_status pgb_load_idx_device(const char* path, int32_t device, float scale_div, float* d_out,
+                               int64_t capacity);
 /* Device addresses for zero-copy interop (torch, benchmarks). */
 pgb_status pgb_device_params(pgb_engine* e, float** d_params);
 pgb_status pgb_device_stream(pgb_engine* e, void** cuda_stream);

@@ -200,13 +200,32 @@ class GradEngine {
   Strategy strategy() const { return strategy_; }
   pgb_engine* handle() const { return h_.get(); }
   void upload(const models::Model& m) {
-    const std::vector<float> f = m.flat();
+    std::vector<float> f = m.flat();
     check(pgb_set_params(h_.get(), f.data()));
+    bound_ = &m;
+    synced_ = std::move(f);
+    device_ahead_ = false;
   }
-  void download(models::Model& m) const {
+  void download(models::Model& m) {
     std::vector<float> f(m.desc.param_count());
     check(pgb_get_params(h_.get(), f.data()));
     m.set_flat(f);
+    bound_ = &m;
+    synced_ = std::move(f);
+    device_ahead_ = false;
+  }
+  // The reference's dpsgd_step reads model.params on every call
+  // (dpsgd.cpp:188-331): upload when the device does not hold exactly this
+  // model's host parameters (another model was stepped on this engine, or the
+  // host copy was edited since the last sync). After a step with
+  // sync_params = false the device copy is the newer one and is kept.
+  void bind(const models::Model& m) {
+    if (bound_ == &m && (device_ahead_ || m.flat() == synced_)) return;
+    upload(m);
+  }
+  void mark_device_ahead(const models::Model& m) {
+    bound_ = &m;
+    device_ahead_ = true;
   }
   // strategies.cpp:432-450 / 453-458: sum_i w_i g_i (flat parameter order)
   std::vector<float> weighted_grad_sum(const float* x, const float* y, const float* w) const {
@@ -237,6 +256,9 @@ class GradEngine {
   std::unique_ptr<pgb_engine, Del> h_;
   int64_t batch_;
   Strategy strategy_;
+  const models::Model* bound_ = nullptr;  // the model whose parameters the device holds
+  std::vector<float> synced_;             // its host parameters at the last sync
+  bool device_ahead_ = false;             // device newer than the host copy
 };
 
 inline void validate(const DpConfig<float>& cfg, int64_t batch) {  // dpsgd.cpp:36-51
@@ -261,10 +283,12 @@ inline StepReport dpsgd_step(models::Model& model, GradEngine& engine, const flo
   pgb_dp_config c{cfg.clip_norm, cfg.noise_multiplier, cfg.learning_rate, cfg.microbatch,
                   cfg.seed};
   pgb_step_report r{};
+  engine.bind(model);
   check(pgb_dpsgd_step(engine.handle(), x, y, &c, step_index, rep.pre_clip_norms.data(), &r));
   rep.clipped_count = r.clipped_count;
   rep.noise_streams.assign(r.noise_streams, r.noise_streams + r.n_streams);
   if (sync_params) engine.download(model);
+  else engine.mark_device_ahead(model);
   return rep;
 }
 
@@ -282,8 +306,10 @@ inline StepReport dpsgd_step(models::Model& model, GradEngine& engine,
 // sgd_step (dpsgd.hpp:76-78)
 inline void sgd_step(models::Model& model, GradEngine& engine, const std::vector<float>& x,
                      const std::vector<float>& y, float learning_rate, bool sync_params = true) {
+  engine.bind(model);
   check(pgb_sgd_step(engine.handle(), x.data(), y.data(), learning_rate));
   if (sync_params) engine.download(model);
+  else engine.mark_device_ahead(model);
 }
 
 // ---- data (dataset.hpp:36-69) -----------------------------------------------------
@@ -314,7 +340,7 @@ inline IdxArray load_idx(const std::string& path, float scale_div = 0.0f) {
   IdxArray a;
   a.dims.assign(dims, dims + rank);
   a.values.resize((size_t)count);
-  check(pgb_load_idx(path.c_str(), scale_div, a.values.data()));
+  check(pgb_load_idx(path.c_str(), scale_div, a.values.data(), (int64_t)a.values.size()));
   return a;
 }
 
@@ -344,6 +370,7 @@ inline EpochResult run_epoch(models::Model& model, GradEngine& engine, const io:
   pgb_dp_config c{cfg.clip_norm, cfg.noise_multiplier, cfg.learning_rate, cfg.microbatch,
                   cfg.seed};
   EpochResult r;
+  engine.bind(model);
   check(pgb_run_epoch(engine.handle(), data.inputs.data(), data.labels.data(), data.count, &c,
                       step0, nullptr, &r.clipped_total, &r.seconds));
   engine.download(model);

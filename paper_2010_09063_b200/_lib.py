@@ -108,10 +108,12 @@ EXPORTS = {
     "pgb_debug_umma_rate": (C.c_int, [C.c_int32] * 4 + [C.c_void_p, C.c_int32, C.c_void_p]),
     "pgb_run_steps_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.POINTER(DpConfigC), C.c_int64, C.POINTER(C.c_int64)]),
+    "pgb_prepare_steps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                    C.POINTER(DpConfigC)]),
     "pgb_idx_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.c_void_p,
                                C.POINTER(C.c_int64)]),
-    "pgb_load_idx": (C.c_int, [C.c_char_p, C.c_float, C.c_void_p]),
-    "pgb_load_idx_device": (C.c_int, [C.c_char_p, C.c_int32, C.c_float, C.c_void_p]),
+    "pgb_load_idx": (C.c_int, [C.c_char_p, C.c_float, C.c_void_p, C.c_int64]),
+    "pgb_load_idx_device": (C.c_int, [C.c_char_p, C.c_int32, C.c_float, C.c_void_p, C.c_int64]),
     "pgb_device_params": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_device_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pgb_kernels_per_step": (C.c_int32, [C.c_void_p]),

@@ -112,6 +112,11 @@ struct Engine {
   int strategy = 0;
   int64_t B = 0;
   int device = 0, rank = 0, world = 1;
+  // the data-parallel schedule (local clipped sum -> NCCL all-reduce ->
+  // noise + update): world > 1, or a one-rank communicator forced with
+  // PGB_FORCE_DIST=1 at pgb_engine_create_dist (tests drive the multi-GPU
+  // kernels and the captured all-reduce on one GPU that way)
+  bool dist = false;
   ncclComm_t comm = nullptr;
 
   std::vector<Layer> layers;
@@ -204,9 +209,13 @@ struct Engine {
     cudaGraphExec_t exec = nullptr;
     StepArgs args{};
     int64_t C = 0;
+    int nk = 0;  // kernels per step
   };
   ChunkGraph chunk_graphs[kSlots];
-  ChunkGraph resident;  // C steps over a device-resident batch ring
+  // C steps over a device-resident batch ring, one graph per C (the full
+  // chunk and the remainder of a run); rebuilt when the ring or the DP
+  // configuration changes
+  std::map<int64_t, ChunkGraph> resident;
   const float* resident_x = nullptr;
   const float* resident_y = nullptr;
   int resident_n = 0;
@@ -285,7 +294,9 @@ struct Engine {
     cudaGraphNode_t mlp = nullptr;  // the fused dense-model kernel (inputs per step)
     mlp::Params mlp_args{};
   };
-  std::map<int, StepGraph> graphs;  // key: schedule variant
+  // key: (schedule variant and input slot, exact microbatch): the graph bakes
+  // m and U = B/m into its microbatch / sumsq / aggregation launches
+  std::map<std::pair<int, int64_t>, StepGraph> graphs;
   int kernels_last = 0;
   pgb_dp_config last_cfg{};
   int64_t last_step = 0;
@@ -311,8 +322,10 @@ struct Engine {
       if (chunk_graphs[i].exec) cudaGraphExecDestroy(chunk_graphs[i].exec);
       if (chunk_graphs[i].graph) cudaGraphDestroy(chunk_graphs[i].graph);
     }
-    if (resident.exec) cudaGraphExecDestroy(resident.exec);
-    if (resident.graph) cudaGraphDestroy(resident.graph);
+    for (auto& kv : resident) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
     if (h_step_base) cudaFreeHost(h_step_base);
     for (int i = 0; i < kSlots; ++i)
       for (cudaEvent_t ev : {ev_copied[i], ev_consumed[i]})
@@ -664,7 +677,7 @@ struct Engine {
     // after a grid barrier. Measured slower than the PDL-launched aggregation
     // kernel (the barrier costs ~1.3 us and the tiles run ~2x slower at the
     // kernel's 64-register budget), so the separate kernel is the default.
-    if (mnist_tc && world == 1 && std::getenv("PGB_GRID_SYNC") != nullptr) {
+    if (mnist_tc && !dist && std::getenv("PGB_GRID_SYNC") != nullptr) {
       // the in-kernel grid barrier needs every CTA resident: one per SM
       int sms = 0;
       PGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1257,7 +1270,7 @@ struct Engine {
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
     const bool emb = emb_layer >= 0 && t.kind[layers[emb_layer].pblock] == 2;
-    if (world == 1) {
+    if (!dist) {
       launch_agg(agg_launch(t, np, U, 0, ff), s, (ff || mlp_fused) && pdl_enabled);
       nk += mark(s, "aggregate");
       if (emb) nk += enqueue_embed_agg(s, t, np, 0);
@@ -1265,13 +1278,27 @@ struct Engine {
       launch_agg(agg_launch(t, np, U, 1, ff), s);
       nk += mark(s, "aggregate_local");
       if (emb) nk += enqueue_embed_agg(s, t, np, 1);
+      // one all-reduce of the clipped sum (+ the clip count beside it); NCCL
+      // returns identical bytes on every rank, so the replicas stay in step
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
       PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
-      PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
+      PGB_NCCL(N.allReduce(clipped_dst, clipped_dst + 1, 1, ncclInt32, ncclSum, comm, s));
       PGB_NCCL(N.groupEnd());
-      NoiseLaunch L{t, cur_args, d_sum, d_params, d_err};
-      noise_update_kernel<<<grid_for((size_t)P), 256, 0, s>>>(L);
+      // the same noise on every rank (shared seed, counter-based streams):
+      // drawn by the fused MNIST kernel already, else here, once per pair
+      NoiseLaunch L{};
+      L.bt = t;
+      L.a = cur_args;
+      L.sum = d_sum;
+      L.params = d_params;
+      L.err = d_err;
+      L.noise = ff ? d_noise : nullptr;
+      L.step_base = cap_step_base;
+      L.step_off = cap_step_off;
+      int64_t pairs = 0;
+      for (int p = 0; p < t.n; ++p) pairs += (t.size[p] + 1) / 2;
+      noise_update_kernel<<<grid_for((size_t)pairs), 256, 0, s>>>(L);
       nk += mark(s, "noise_update");
     }
     return nk;
@@ -1329,7 +1356,7 @@ struct Engine {
 
   // Launch the step for inputs already resident at d_x/d_y slots.
   void launch_step(const float* x_slot, const float* y_slot, int64_t m) {
-    const int variant = (m > 1 ? 1 : 0) | (world > 1 ? 2 : 0);
+    const int variant = (m > 1 ? 1 : 0) | (dist ? 2 : 0);
     // the fused MNIST schedule takes its input pointers as updatable node
     // parameters; the layer-wise schedule bakes the input slot into the graph
     int slot_key = 0;
@@ -1341,7 +1368,7 @@ struct Engine {
       PGB_CUDA(cudaGetLastError());
       return;
     }
-    const int gkey = key * 64 + (int)std::min<int64_t>(m, 63);
+    const std::pair<int, int64_t> gkey{key, m};
     auto it = graphs.find(gkey);
     if (it == graphs.end()) {
       StepGraph sg;
@@ -1417,12 +1444,22 @@ struct Engine {
   // d_step_base[kSlots] and the graph's last node advances it by C).
   cudaGraphExec_t resident_graph(int64_t C, const StepArgs& args, const float* xr,
                                  const float* yr, int n) {
-    ChunkGraph& cg = resident;
     StepArgs a0 = args;
     a0.step = 0;
+    if (resident_x != xr || resident_y != yr || resident_n != n) {
+      // another ring: every resident graph bakes the old one
+      for (auto& kv : resident) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      }
+      resident.clear();
+    }
+    ChunkGraph& cg = resident[C];
     if (cg.exec && cg.C == C && std::memcmp(&cg.args, &a0, sizeof(StepArgs)) == 0 &&
-        resident_x == xr && resident_y == yr && resident_n == n)
+        resident_x == xr && resident_y == yr && resident_n == n) {
+      kernels_last = cg.nk;
       return cg.exec;
+    }
     if (cg.exec) cudaGraphExecDestroy(cg.exec);
     if (cg.graph) cudaGraphDestroy(cg.graph);
     cg = ChunkGraph{};
@@ -1457,6 +1494,7 @@ struct Engine {
     PGB_CUDA(cudaGraphInstantiate(&cg.exec, cg.graph, 0));
     cg.args = a0;
     cg.C = C;
+    cg.nk = kernels_last;
     resident_x = xr;
     resident_y = yr;
     resident_n = n;
@@ -1557,20 +1595,29 @@ struct Engine {
     }
   }
 
-  // Device errors are sticky (the first one wins and later updates are
-  // skipped) until the host reports them here.
+  // Device errors are sticky (the reference's first one wins and later
+  // updates are skipped) until the host reports them here, with the
+  // reference's IndexError text (checked_id, kernels.hpp:475-489).
   void check_device_error() {
     if (h_err->code == 0) return;
     const DevError e = *h_err;
     h_err->code = 0;
     PGB_CUDA(cudaMemsetAsync(d_err, 0, sizeof(DevError), stream));
     PGB_CUDA(cudaStreamSynchronize(stream));
-    if (e.what == 0)
-      raise(PGB_ERR_INDEX, "softmax_xent label: id " + std::to_string((long long)e.value) +
-                               " out of range [0," + std::to_string(e.limit) + ") at position " +
-                               std::to_string(e.pos));
-    raise(PGB_ERR_INDEX, "gather_rows: id " + std::to_string(e.value) + " out of range [0," +
-                             std::to_string(e.limit) + ") at position " + std::to_string(e.pos));
+    const unsigned long long key = ~e.inv_key;
+    const bool label = (key >> 62) & 1;
+    const long long pos = (long long)((key >> 32) & ((1ull << 30) - 1));
+    const uint32_t bits = (uint32_t)key;
+    float v;
+    std::memcpy(&v, &bits, sizeof v);
+    const std::string what = label ? "softmax_xent label" : "gather_rows";
+    const double dv = v;
+    const long long id = std::isfinite(dv) ? std::llround(dv) : 0;
+    if (!std::isfinite(dv) || (double)id != dv)
+      raise(PGB_ERR_INDEX, what + ": non-integral id at position " + std::to_string(pos));
+    raise(PGB_ERR_INDEX, what + ": id " + std::to_string(id) + " out of range [0," +
+                             std::to_string(label ? e.limit_label : e.limit_id) +
+                             ") at position " + std::to_string(pos));
   }
 
   void read_report(float* norms_out, pgb_step_report* rep, int64_t m, int64_t step) {
@@ -1585,7 +1632,7 @@ struct Engine {
     check_device_error();
     if (norms_out) std::memcpy(norms_out, h_norms, sizeof(float) * U);
     if (rep) {
-      rep->clipped_count = world > 1 ? h_clipped[1] : h_clipped[0];
+      rep->clipped_count = dist ? h_clipped[1] : h_clipped[0];
       rep->n_streams = 0;
       if (last_cfg.noise_multiplier > 0.0f) {
         rep->n_streams = bt.n;
@@ -1657,8 +1704,9 @@ pgb_status pgb_engine_create_dist(const pgb_model_desc* desc, int32_t strategy,
     h->impl = std::make_unique<Engine>();
     h->impl->world = world;
     h->impl->rank = rank;
+    h->impl->dist = world > 1 || std::getenv("PGB_FORCE_DIST") != nullptr;
     h->impl->init(*desc, strategy, local_batch, device);
-    if (world > 1) {
+    if (h->impl->dist) {
       ncclUniqueId nid;
       std::memcpy(&nid, id, sizeof nid);
       PGB_NCCL(Nccl::get().commInitRank(&h->impl->comm, world, nid, rank));
@@ -1746,6 +1794,36 @@ pgb_status pgb_dpsgd_step_device(pgb_engine* e, const float* d_x, const float* d
   });
 }
 
+namespace {
+// How pgb_run_steps_device splits n_steps: full multi-step graphs of C steps
+// plus one graph of the remainder (every schedule whose inputs the graph can
+// read from the device ring by the step counter: fused MNIST and dense-only
+// models, one process or data-parallel, microbatch 1); C = 0: per-step graphs.
+int64_t resident_chunk(const Engine& en, const pgb_dp_config& cfg, int64_t n_batches) {
+  int64_t C = 8;
+  if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
+  const bool ok = (en.fused_mnist || en.mlp_fused) && cfg.microbatch == 1 && en.graph_enabled &&
+                  C > 1 && n_batches < (1 << 30);
+  return ok ? C : 0;
+}
+}  // namespace
+
+pgb_status pgb_prepare_steps(pgb_engine* e, const float* d_x, const float* d_y,
+                             int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg) {
+  return guarded([&] {
+    Engine& en = E(e);
+    if (!cfg || !d_x || !d_y) raise(PGB_ERR_CONTRACT, "null argument");
+    if (n_batches <= 0 || n_steps < 0) raise(PGB_ERR_CONFIG, "prepare_steps: bad counts");
+    en.validate_step(*cfg);
+    const int64_t C = resident_chunk(en, *cfg, n_batches);
+    if (C == 0) return;
+    const StepArgs a0 = en.make_args(*cfg, 0, nullptr, nullptr);
+    if (n_steps >= C) en.resident_graph(C, a0, d_x, d_y, (int)n_batches);
+    if (n_steps % C) en.resident_graph(n_steps % C, a0, d_x, d_y, (int)n_batches);
+    PGB_CUDA(cudaStreamSynchronize(en.stream));
+  });
+}
+
 pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_y,
                                 int64_t n_batches, int64_t n_steps, const pgb_dp_config* cfg,
                                 int64_t step0, int64_t* launches_out) {
@@ -1760,34 +1838,41 @@ pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_
       const int64_t bi = ((s % n_batches) + n_batches) % n_batches;
       return std::make_pair(d_x + bi * en.B * en.in_row, d_y + bi * en.B);
     };
-    int64_t C = 8;
-    if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
-    const bool chunked = (en.fused_mnist || en.mlp_fused) && en.world == 1 && cfg->microbatch == 1 &&
-                         en.graph_enabled && C > 1 && n_steps >= C && n_batches < (1 << 30);
-    int64_t s = 0;
-    if (chunked) {
+    const int64_t C = resident_chunk(en, *cfg, n_batches);
+    if (C > 0 && n_steps > 0) {
+      // full chunks, then the remainder as one more static graph: the host
+      // issues one counter write and ceil(n / C) graph launches
       const StepArgs a0 = en.make_args(*cfg, step0, nullptr, nullptr);
-      cudaGraphExec_t g = en.resident_graph(C, a0, d_x, d_y, (int)n_batches);
+      const int64_t full = n_steps / C, rem = n_steps % C;
+      cudaGraphExec_t g = full ? en.resident_graph(C, a0, d_x, d_y, (int)n_batches) : nullptr;
+      const int kfull = en.kernels_last;
+      cudaGraphExec_t gr = rem ? en.resident_graph(rem, a0, d_x, d_y, (int)n_batches) : nullptr;
+      const int krem = en.kernels_last;
       set_counter_kernel<<<1, 1, 0, en.stream>>>(en.d_step_base + Engine::kSlots, step0);
       ++launches;
-      for (; s + C <= n_steps; s += C) {
+      for (int64_t k = 0; k < full; ++k) {
         PGB_CUDA(cudaGraphLaunch(g, en.stream));
-        launches += C * en.kernels_last + 1;
+        launches += C * kfull + 1;
       }
-    }
-    for (; s < n_steps; ++s) {
-      const auto in = batch(step0 + s);
-      en.push_args(en.make_args(*cfg, step0 + s, in.first, in.second));
-      if ((en.fused_mnist || en.mlp_fused) && en.graph_enabled) {
-        en.launch_step(in.first, in.second, cfg->microbatch);
-      } else {
-        PGB_CUDA(cudaMemcpyAsync(en.d_x, in.first, sizeof(float) * en.B * en.in_row,
-                                 cudaMemcpyDeviceToDevice, en.stream));
-        PGB_CUDA(cudaMemcpyAsync(en.d_y, in.second, sizeof(float) * en.B,
-                                 cudaMemcpyDeviceToDevice, en.stream));
-        en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+      if (gr) {
+        PGB_CUDA(cudaGraphLaunch(gr, en.stream));
+        launches += rem * krem + 1;
       }
-      launches += en.kernels_last;
+    } else {
+      for (int64_t s = 0; s < n_steps; ++s) {
+        const auto in = batch(step0 + s);
+        en.push_args(en.make_args(*cfg, step0 + s, in.first, in.second));
+        if ((en.fused_mnist || en.mlp_fused) && en.graph_enabled) {
+          en.launch_step(in.first, in.second, cfg->microbatch);
+        } else {
+          PGB_CUDA(cudaMemcpyAsync(en.d_x, in.first, sizeof(float) * en.B * en.in_row,
+                                   cudaMemcpyDeviceToDevice, en.stream));
+          PGB_CUDA(cudaMemcpyAsync(en.d_y, in.second, sizeof(float) * en.B,
+                                   cudaMemcpyDeviceToDevice, en.stream));
+          en.launch_step(en.d_x, en.d_y, cfg->microbatch);
+        }
+        launches += en.kernels_last;
+      }
     }
     en.last_step = step0 + n_steps - 1;
     PGB_CUDA(cudaGetLastError());
@@ -1887,7 +1972,7 @@ pgb_status pgb_weighted_grad_sum(pgb_engine* e, const float* x, const float* y, 
   return guarded([&] {
     Engine& en = E(e);
     if (!x || !y || !w || !sum_out) raise(PGB_ERR_CONTRACT, "null argument");
-    if (en.world != 1)
+    if (en.dist)
       raise(PGB_ERR_UNSUPPORTED, "weighted_grad_sum: one-process engines only");
     PGB_CUDA(cudaMemcpyAsync(en.d_x, x, sizeof(float) * en.B * en.in_row,
                              cudaMemcpyHostToDevice, en.stream));
@@ -1990,9 +2075,9 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     constexpr int K = Engine::kSlots;
     // Results go to a ring of K device slots read back on out_stream, so the
     // per-step D2H never sits between two steps on the compute stream (the
-    // multi-GPU schedule all-reduces the fixed clip counter: results stay on
-    // the compute stream there).
-    const bool ring = en.world == 1;
+    // data-parallel schedule all-reduces each step's clip count inside its
+    // own result slot).
+    const bool ring = true;
     en.ensure_host_stage(steps, U);
     cudaEvent_t* copied = en.ev_copied;
     cudaEvent_t* consumed = en.ev_consumed;
@@ -2015,8 +2100,7 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     C = std::min<int64_t>(C, Engine::kResSlots / (K + 1));
     // (every one-process schedule: the layer-wise one bakes each step's input
     // pointer into its chunk graph node; noise takes the step from the device)
-    const bool chunked = en.world == 1 && cfg->microbatch == 1 && en.graph_enabled && C > 1 &&
-                         steps >= C;
+    const bool chunked = cfg->microbatch == 1 && en.graph_enabled && C > 1 && steps >= C;
     // the fused schedules take input pointers as node parameters: their
     // per-step graphs can read any batch inside a chunk slot; the layer-wise
     // schedule launches those steps directly
@@ -2147,7 +2231,7 @@ pgb_status pgb_run_epoch(pgb_engine* e, const float* x, const float* y, int64_t 
     if (seconds_out) *seconds_out = std::max(wall, ms * 1e-3);
     int64_t tot = 0;
     for (int64_t s = 0; s < steps; ++s)
-      tot += en.world > 1 ? en.h_clip_stage[2 * s + 1] : en.h_clip_stage[2 * s];
+      tot += en.dist ? en.h_clip_stage[2 * s + 1] : en.h_clip_stage[2 * s];
     if (clipped_total) *clipped_total = tot;
     if (norms_out) std::memcpy(norms_out, en.h_norm_stage, sizeof(float) * steps * U);
     en.last_cfg = *cfg;
@@ -2301,11 +2385,16 @@ pgb_status pgb_debug_umma_rate(int32_t device, int32_t M, int32_t N, int32_t rep
   });
 }
 
-pgb_status pgb_load_idx_device(const char* path, int32_t device, float scale_div, float* d_out) {
+pgb_status pgb_load_idx_device(const char* path, int32_t device, float scale_div, float* d_out,
+                               int64_t capacity) {
   return guarded([&] {
     if (!path || !d_out) raise(PGB_ERR_CONTRACT, "null argument");
     IdxArray a = read_idx(path);
     const size_t n = a.bytes.size() - a.offset;
+    if (capacity < 0 || n > static_cast<size_t>(capacity))
+      raise(PGB_ERR_CONTRACT, "load_idx: payload of " + std::to_string(n) +
+                                  " elements exceeds the output capacity " +
+                                  std::to_string(capacity));
     PGB_CUDA(cudaSetDevice(device));
     // the payload crosses PCIe as bytes (4x fewer than floats) and is decoded
     // on the device with the reference's arithmetic: float(b) / scale

@@ -420,11 +420,15 @@ pgb_status pgb_idx_info(const char* path, int32_t* rank, int64_t* dims, int64_t*
   });
 }
 
-pgb_status pgb_load_idx(const char* path, float scale_div, float* out) {
+pgb_status pgb_load_idx(const char* path, float scale_div, float* out, int64_t capacity) {
   return guarded([&] {
     if (!path || !out) raise(PGB_ERR_CONTRACT, "null argument");
     pgb::IdxArray a = pgb::read_idx(path);
     const size_t n = a.bytes.size() - a.offset;
+    if (capacity < 0 || n > static_cast<size_t>(capacity))
+      raise(PGB_ERR_CONTRACT, "load_idx: payload of " + std::to_string(n) +
+                                  " elements exceeds the output capacity " +
+                                  std::to_string(capacity));
     const unsigned char* b = a.bytes.data() + a.offset;
     for (size_t i = 0; i < n; ++i) {
       const float v = static_cast<float>(b[i]);
@@ -469,6 +473,10 @@ IdxArray read_idx(const std::string& path) {
       raise(PGB_ERR_FORMAT, "load_idx: truncated dims at offset " + std::to_string(offset));
     const int64_t extent = be32(a.bytes.data() + offset);
     a.dims.push_back(extent);
+    // the dimension product must fit the payload arithmetic (and size_t)
+    if (extent != 0 && total > (int64_t(1) << 62) / extent)
+      raise(PGB_ERR_FORMAT, "load_idx: dimension product overflows at offset " +
+                                std::to_string(offset));
     total *= extent;
     offset += 4;
   }

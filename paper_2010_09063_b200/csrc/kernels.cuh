@@ -15,24 +15,31 @@ namespace pgb {
 
 constexpr int kMaxBlocks = PGB_MAX_PARAMS;
 
-// First device-side error wins; the step's update kernel refuses to write
-// parameters once it is set (the reference throws before apply_update).
+// Device-side index errors (checked_id, kernels.hpp:475-489). The reference
+// throws at the first bad value in its own loop order -- the embedding gather
+// of the forward before the loss's labels, each in ascending position -- so
+// the device keeps the error with the smallest (kind, position) key, whatever
+// order the threads find them in: one 64-bit atomicMax on the complemented
+// key (order bit, position, value bits), which also carries the offending
+// value. The step's update kernel refuses to write parameters once code is
+// set (the reference throws before apply_update).
 struct DevError {
-  int code;       // pgb_status, 0 = none
-  int what;       // 0 label, 1 embedding id
-  long long pos;  // flat position of the offending value
-  float value;
-  int limit;
+  int code;        // pgb_status, 0 = none
+  int limit_label; // classes of the softmax_xent label check
+  int limit_id;    // rows of the embedding gather
+  int pad;
+  unsigned long long inv_key;  // ~((label ? 1 : 0) << 62 | pos << 32 | value bits)
 };
 
 __device__ __forceinline__ void raise_index(DevError* e, int what, long long pos, float v,
                                             int limit) {
-  if (atomicCAS(&e->code, 0, PGB_ERR_INDEX) == 0) {
-    e->what = what;
-    e->pos = pos;
-    e->value = v;
-    e->limit = limit;
-  }
+  const unsigned long long p = (unsigned long long)min(max(pos, 0ll), (1ll << 30) - 1);
+  const unsigned long long key =
+      ((unsigned long long)(what == 0 ? 1 : 0) << 62) | (p << 32) | __float_as_uint(v);
+  atomicMax(&e->inv_key, ~key);
+  if (what == 0) e->limit_label = limit;
+  else e->limit_id = limit;
+  atomicExch(&e->code, PGB_ERR_INDEX);
 }
 
 // Packed fp32 FMA (sm_100 FFMA2): {a0, a1} += w * {x0, x1}, each lane of the
@@ -1397,46 +1404,70 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
 }
 
 // After the all-reduce of the clipped sums: noise (one shared draw from the
-// common seed), mean over the global units, update.
+// common seed, so every rank adds the same vector), mean over the global
+// units, update (dpsgd.cpp:308-317, apply_update :173-183). One thread per
+// normal PAIR: each Box-Muller draw (kernels.hpp:597-614) feeds both of its
+// elements, and the pair's two sums / parameters are adjacent.
 struct NoiseLaunch {
   BlockTable bt;
   StepArgs a;
   const float* sum;  // the all-reduced clipped sum
   float* params;
   const DevError* err;
+  const float* noise;          // (P) the step's normals drawn by the fused kernel, or null
+  const long long* step_base;  // multi-step graphs: the noise step on the device
+  int step_off;
 };
 
-__global__ void noise_update_kernel(const NoiseLaunch L) {
+__global__ void __launch_bounds__(256) noise_update_kernel(const NoiseLaunch L) {
   const BlockTable& bt = L.bt;
   const StepArgs& a = L.a;
   const float* __restrict__ sum = L.sum;
   float* __restrict__ params = L.params;
-  __shared__ long long off_sh[kMaxBlocks + 1];
+  __shared__ long long pair_sh[kMaxBlocks + 1];
   if (threadIdx.x == 0) {
     long long o = 0;
     for (int p = 0; p < bt.n; ++p) {
-      off_sh[p] = o;
-      o += bt.size[p];
+      pair_sh[p] = o;
+      o += (bt.size[p] + 1) / 2;
     }
-    off_sh[bt.n] = o;
+    pair_sh[bt.n] = o;
   }
   __syncthreads();
   if (L.err && L.err->code != 0) return;
-  const long long total = off_sh[bt.n];
+  const long long total = pair_sh[bt.n];
+  const long long stp = L.step_base ? *L.step_base + L.step_off : a.step;
+  const float scale = __fmul_rn(a.sigma, a.clip);
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
-    const int p = find_block(off_sh, bt.n, q);
-    const long long j = q - off_sh[p];
-    float acc = sum[bt.param_off[p] + j];
-    if (a.add_noise) {
-      float n0, n1;
-      gauss_pair(stream_key(a.seed, noise_stream(a.step, p)), j >> 1, &n0, &n1);
-      const float scale = __fmul_rn(a.sigma, a.clip);
-      acc = __fadd_rn(acc, __fmul_rn(scale, (j & 1) ? n1 : n0));
+    int lo = 0, hi = bt.n - 1;  // the block holding pair q (binary search)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pair_sh[mid] <= q) lo = mid;
+      else hi = mid - 1;
     }
-    acc = __fmul_rn(acc, a.inv_units);
-    const float cur = params[bt.param_off[p] + j];
-    write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, acc)));
+    const int p = lo;
+    const long long jp = q - pair_sh[p], j0 = 2 * jp;
+    const long long off = bt.param_off[p];
+    float nv[2] = {0.0f, 0.0f};
+    if (a.add_noise) {
+      if (L.noise) {
+        nv[0] = L.noise[off + j0];
+        if (j0 + 1 < bt.size[p]) nv[1] = L.noise[off + j0 + 1];
+      } else {
+        gauss_pair(stream_key(a.seed, noise_stream(stp, p)), jp, &nv[0], &nv[1]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const long long j = j0 + e;
+      if (j >= bt.size[p]) break;
+      float acc = sum[off + j];
+      if (a.add_noise) acc = __fadd_rn(acc, __fmul_rn(scale, nv[e]));
+      acc = __fmul_rn(acc, a.inv_units);
+      const float cur = params[off + j];
+      write_param(bt, p, j, params, __fsub_rn(cur, __fmul_rn(a.lr, acc)));
+    }
   }
 }
 

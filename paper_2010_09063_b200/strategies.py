@@ -74,7 +74,9 @@ class GradEngine:
         self._mode = ExecMode(mode)
         self._batch = int(batch)
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or unique_id is not None:
+            # the data-parallel engine (a one-rank communicator when world == 1
+            # and PGB_FORCE_DIST=1: the multi-GPU schedule on one GPU)
             uid = _lib.UniqueIdC()
             C.memmove(C.byref(uid), unique_id, 128)
             check(lib.pgb_engine_create_dist(C.byref(self._desc_c), int(strategy), int(batch),
@@ -125,6 +127,13 @@ class GradEngine:
     def set_flat_params(self, flat: np.ndarray):
         flat = np.ascontiguousarray(flat, np.float32)
         assert flat.size == self.P
+        # the bound model may hold its newest parameters only on the device
+        # (dpsgd_step leaves them there): fetch them before they are replaced,
+        # and forget the binding so the next bind() uploads again
+        b = self._bound
+        if b is not None and b._engine is self:
+            b.params  # noqa: B018  (downloads into the model)
+        self._bound = None
         check(lib.pgb_set_params(self.handle, _lib.ptr(flat)))
 
     def get_flat_params(self) -> np.ndarray:
@@ -136,7 +145,8 @@ class GradEngine:
         """Make the device hold `model`'s parameters (uploads only when stale)."""
         if model._engine is self and self._bound is model:
             return
-        self.set_flat_params(model.flat_params())
+        flat = model.flat_params()
+        self.set_flat_params(flat)
         self._bound = model
 
     def _inputs(self, x, y):

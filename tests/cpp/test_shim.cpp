@@ -127,6 +127,31 @@ int main() {
   engine.download(model);
   CHECK(model.flat() == before);
 
+  // dpsgd_step reads model.params on every call (dpsgd.cpp:188-331): a host
+  // edit of the parameters, and a second model stepped on the same engine,
+  // both reach the device (two engines built from the edited models agree)
+  {
+    auto m1 = models::build(ModelKind::fcnn, 21);
+    auto m2 = models::build(ModelKind::fcnn, 22);
+    auto fx = io::synth_for_model(m1.desc, 8, 4);
+    GradEngine shared(m1, Strategy::vmap, 8);
+    m1.params[0][0] += 0.25f;  // host edit after the engine took its copy
+    auto r1 = m1, r2 = m2;
+    GradEngine e1(r1, Strategy::vmap, 8), e2(r2, Strategy::vmap, 8);
+    dpsgd_step(m1, shared, fx.inputs, fx.labels, cfg, 0);
+    dpsgd_step(r1, e1, fx.inputs, fx.labels, cfg, 0);
+    CHECK(m1.flat() == r1.flat());
+    dpsgd_step(m2, shared, fx.inputs, fx.labels, cfg, 0);  // another model, same engine
+    dpsgd_step(r2, e2, fx.inputs, fx.labels, cfg, 0);
+    CHECK(m2.flat() == r2.flat());
+    // sync_params = false keeps the newer device copy for the next step
+    dpsgd_step(m1, shared, fx.inputs, fx.labels, cfg, 1, false);
+    dpsgd_step(m1, shared, fx.inputs, fx.labels, cfg, 2);
+    dpsgd_step(r1, e1, fx.inputs, fx.labels, cfg, 1);
+    dpsgd_step(r1, e1, fx.inputs, fx.labels, cfg, 2);
+    CHECK(m1.flat() == r1.flat());
+  }
+
   // the strategy support matrix (strategies.cpp:76-113)
   CHECK(throws<UnsupportedError>([&] { GradEngine bad_e(model, Strategy::outer, B); }));
 

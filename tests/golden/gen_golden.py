@@ -35,8 +35,53 @@ CONFIGS = [
 ]
 
 
+# Full-size fixtures (BASELINE configs 4 and 5 at their stated batch): norms,
+# clip count and a strided sample of the fp64 clipped sum, from the
+# reference's fp64 GradEngine::compute. About a minute; generated on request:
+#     python tests/golden/gen_golden.py full
+# clip: near the median norm, so about half the examples clip.
+FULL = [
+    ("cifar_cnn_b256", lambda: O.build_desc(O.CIFAR_CNN), 256, O.GROUPCONV, None, 11),
+    ("embed_b512", lambda: O.build_desc(O.EMBED, hidden=100), 512, O.JACMM, None, 17),
+]
+
+
 def digest(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def full():
+    assert O.ref_available(), "build the reference first: make -C oracle ref"
+    for name, mk, B, strat, C, every in FULL:
+        d = mk()
+        p64 = O.ref_init_params(d, 0)
+        x64, y64 = O.ref_synth(d, B, 0)
+        x32, y32 = O.ref_synth(d, B, 0, np.float32)
+        R = O.RefModel(d, strat, B, p64)
+        stacks, norms = R.per_example(x64, y64)
+        del R
+        if C is None:
+            # near the median, in the widest gap between consecutive norms of
+            # the middle fifth: no example sits within fp32 noise of C
+            srt = np.sort(norms)
+            lo, hi = int(0.4 * B), int(0.6 * B)
+            k = lo + int(np.argmax(np.diff(srt[lo:hi + 1])))
+            C = float(0.5 * (srt[k] + srt[k + 1]))
+        s = np.where(norms > C, C / norms, 1.0)
+        parts, off = [], 0
+        for n in d.blocks:
+            blk = stacks[off: off + B * n].reshape(B, n)
+            parts.append(s @ blk)  # sum_i s_i g_i, fp64
+            off += B * n
+        del stacks
+        clipped_sum = np.concatenate(parts)
+        nclip = int((norms > C).sum())
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), norms=norms, clip_scales=s,
+                            clipped_count=np.int64(nclip), clipped_sum=clipped_sum[::every],
+                            every=np.int64(every), blocks=np.array(d.blocks, np.int64),
+                            B=np.int64(B), clip=np.float64(C), x_sha=np.array(digest(x32)),
+                            y_sha=np.array(digest(y32)))
+        print(name, "B", B, "P", d.param_count, "C", C, "clipped", nclip, "norm0", norms[0])
 
 
 def main():
@@ -79,4 +124,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    full() if sys.argv[1:] == ["full"] else main()

@@ -1,0 +1,97 @@
+"""Oracle parity at the batch BASELINE states for configs 4 and 5, against
+fixtures made by the UNMODIFIED reference (tests/golden/gen_golden.py full:
+the reference's fp64 GradEngine::compute, clipped sum assembled in fp64):
+
+* CIFAR-10 CNN, B = 256 (605,226 parameters);
+* IMDb-shaped embedding classifier, V = 10,004, L = 256, E = 100, B = 512
+  (1,000,602 parameters; the GPU step path uses sparse per-example embedding
+  gradients, the probe below the same kernels' clipped sum).
+
+Per-example norms element-wise rel <= 1e-5, clip count exact, the noise-free
+clipped sum per block normwise rel <= 1e-5 (over the fixture's strided
+sample) and element-wise |d| <= 1e-5 (|ref| + max|ref|); then one sigma = 0
+step's update carries the same sum.
+"""
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+TOL = 1e-5
+
+CASES = [
+    # fixture, kind, options, strategy
+    ("cifar_cnn_b256", 3, {}, 4),
+    ("embed_b512", 4, {"hidden": 100}, 5),
+]
+
+
+def _load(name):
+    return np.load(os.path.join(HERE, "golden", f"{name}.npz"))
+
+
+def _sampled_blocks(f):
+    """(start, stop) of each parameter block inside the strided sample."""
+    every = int(f["every"])
+    out, off = [], 0
+    for n in f["blocks"]:
+        lo = -(-off // every)
+        hi = -(-(off + int(n)) // every)
+        out.append((lo, hi))
+        off += int(n)
+    return out
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fixture_inputs_are_ours(P, case):
+    """CPU: the fixture was made on exactly the inputs our synth_for_model
+    produces (sha256 of the fp32 arrays)."""
+    import hashlib
+    name, kind, opts, _ = case
+    f = _load(name)
+    desc = P.build_desc(P.ModelKind(kind), P.ModelOptions(**opts))
+    data = P.synth_for_model(desc, int(f["B"]), 0)
+    assert hashlib.sha256(data.inputs.tobytes()).hexdigest() == str(f["x_sha"])
+    assert hashlib.sha256(data.labels.tobytes()).hexdigest() == str(f["y_sha"])
+    assert desc.param_count() == int(np.sum(f["blocks"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_full_size_clipped_sum_matches_reference_fixture(P, case):
+    name, kind, opts, strat = case
+    f = _load(name)
+    B, C = int(f["B"]), float(f["clip"])
+    every = int(f["every"])
+    desc = P.build_desc(P.ModelKind(kind), P.ModelOptions(**opts))
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 0)
+    eng = P.GradEngine(model, P.Strategy(strat), B)
+    got, norms, nclip = eng.clipped_sum(data.inputs, data.labels, C)
+    wn = f["norms"]
+    assert np.max(np.abs(norms - wn) / wn) < TOL
+    assert nclip == int(f["clipped_count"])
+    gs = got[::every].astype(np.float64)
+    want = f["clipped_sum"]
+    for lo, hi in _sampled_blocks(f):
+        w, g = want[lo:hi], gs[lo:hi]
+        den = np.linalg.norm(w)
+        assert np.linalg.norm(g - w) <= TOL * den + 1e-30
+        assert np.all(np.abs(g - w) <= TOL * (np.abs(w) + np.abs(w).max()))
+
+    # the step path (for the embedding model: the sparse per-example
+    # gradients) carries the same clipped sum: sigma = 0, p_new = p - lr*sum/B
+    p0 = model.flat_params().astype(np.float64)
+    lr = 1000.0
+    cfg = P.DpConfig(clip_norm=C, noise_multiplier=0.0, learning_rate=lr, seed=0)
+    rep = P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, 0)
+    assert rep.clipped_count == int(f["clipped_count"])
+    assert np.max(np.abs(rep.pre_clip_norms - wn) / wn) < TOL
+    p1 = model.flat_params().astype(np.float64)
+    step_sum = ((p0 - p1) * B / lr)[::every]
+    # the update is rounded at max(|p|, |p_new|): one ulp of it, in sum units
+    ulp = ((np.abs(p0) + np.abs(p1)) * 2.0 ** -23 * B / lr)[::every]
+    for lo, hi in _sampled_blocks(f):
+        w, g = want[lo:hi], step_sum[lo:hi]
+        assert np.linalg.norm(g - w) <= TOL * np.linalg.norm(w) + np.linalg.norm(ulp[lo:hi])

@@ -407,6 +407,11 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clocks:
+        # hold the stream ~0.2 ms (before the timed region) so the host has
+        # queued the timed launches when the first one starts: the events then
+        # bracket K back-to-back device steps, not host launch latency
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(400_000)
         ev0.record(stream)
         h0 = time.perf_counter()
         timed_launches = run_steps(args.warmup, args.steps)

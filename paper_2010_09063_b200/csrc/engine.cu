@@ -1201,7 +1201,9 @@ struct Engine {
     L.params = d_params;
     L.sum_out = d_sum;
     L.norms_out = norms_dst;
-    L.clipped_out = clipped_dst;
+    // data-parallel steps count into the all-reduce's fixed buffer; the
+    // noise-update kernel copies the reduced count into the result slot
+    L.clipped_out = dist && mode == 1 ? d_clipped : clipped_dst;
     L.err = d_err;
     L.U = U;
     L.nparts = np;
@@ -1283,7 +1285,7 @@ struct Engine {
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
       PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
-      PGB_NCCL(N.allReduce(clipped_dst, clipped_dst + 1, 1, ncclInt32, ncclSum, comm, s));
+      PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
       PGB_NCCL(N.groupEnd());
       // the same noise on every rank (shared seed, counter-based streams):
       // drawn by the fused MNIST kernel already, else here, once per pair
@@ -1296,6 +1298,8 @@ struct Engine {
       L.noise = ff ? d_noise : nullptr;
       L.step_base = cap_step_base;
       L.step_off = cap_step_off;
+      L.cnt_in = d_clipped;
+      L.clipped_out = clipped_dst;
       int64_t pairs = 0;
       for (int p = 0; p < t.n; ++p) pairs += (t.size[p] + 1) / 2;
       noise_update_kernel<<<grid_for((size_t)pairs), 256, 0, s>>>(L);
@@ -1557,11 +1561,12 @@ struct Engine {
   }
 
   void update_step_nodes(StepGraph& sg, const float* x_slot, const float* y_slot) {
+    int* agg_cnt = (dist && sg.agg_args.mode == 1) ? d_clipped : clipped_dst;
     if (sg.agg && (!same_args(sg.agg_args.a, cur_args) || sg.agg_args.norms_out != norms_dst ||
-                   sg.agg_args.clipped_out != clipped_dst)) {
+                   sg.agg_args.clipped_out != agg_cnt)) {
       sg.agg_args.a = cur_args;
       sg.agg_args.norms_out = norms_dst;
-      sg.agg_args.clipped_out = clipped_dst;
+      sg.agg_args.clipped_out = agg_cnt;
       set_node(sg.exec, sg.agg, &sg.agg_args);
     }
     if (sg.mlp && (sg.mlp_args.x != x_slot || sg.mlp_args.y != y_slot)) {
@@ -1573,8 +1578,10 @@ struct Engine {
       sg.emb_args.a = cur_args;
       set_node(sg.exec, sg.emb, &sg.emb_args);
     }
-    if (sg.noise && !same_args(sg.noise_args.a, cur_args)) {
+    if (sg.noise && (!same_args(sg.noise_args.a, cur_args) ||
+                     sg.noise_args.clipped_out != clipped_dst)) {
       sg.noise_args.a = cur_args;
+      sg.noise_args.clipped_out = clipped_dst;
       set_node(sg.exec, sg.noise, &sg.noise_args);
     }
     const bool agg_in = sg.fused_tc && sg.fused_args.agg_tiles > 0;
@@ -1818,8 +1825,13 @@ pgb_status pgb_prepare_steps(pgb_engine* e, const float* d_x, const float* d_y,
     const int64_t C = resident_chunk(en, *cfg, n_batches);
     if (C == 0) return;
     const StepArgs a0 = en.make_args(*cfg, 0, nullptr, nullptr);
-    if (n_steps >= C) en.resident_graph(C, a0, d_x, d_y, (int)n_batches);
-    if (n_steps % C) en.resident_graph(n_steps % C, a0, d_x, d_y, (int)n_batches);
+    // captured, instantiated and uploaded to the device (the first launch
+    // of a graph otherwise pays its upload)
+    if (n_steps >= C)
+      PGB_CUDA(cudaGraphUpload(en.resident_graph(C, a0, d_x, d_y, (int)n_batches), en.stream));
+    if (n_steps % C)
+      PGB_CUDA(cudaGraphUpload(en.resident_graph(n_steps % C, a0, d_x, d_y, (int)n_batches),
+                               en.stream));
     PGB_CUDA(cudaStreamSynchronize(en.stream));
   });
 }

@@ -1417,6 +1417,11 @@ struct NoiseLaunch {
   const float* noise;          // (P) the step's normals drawn by the fused kernel, or null
   const long long* step_base;  // multi-step graphs: the noise step on the device
   int step_off;
+  // the step's clip counts (local, all-reduced) copied from the all-reduce's
+  // fixed buffer into the step's result slot (a per-launch node argument,
+  // where the all-reduce's pointers are fixed at capture)
+  const int* cnt_in;
+  int* clipped_out;
 };
 
 __global__ void __launch_bounds__(256) noise_update_kernel(const NoiseLaunch L) {
@@ -1434,6 +1439,10 @@ __global__ void __launch_bounds__(256) noise_update_kernel(const NoiseLaunch L) 
     pair_sh[bt.n] = o;
   }
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && L.clipped_out && L.clipped_out != L.cnt_in) {
+    L.clipped_out[0] = L.cnt_in[0];
+    L.clipped_out[1] = L.cnt_in[1];
+  }
   if (L.err && L.err->code != 0) return;
   const long long total = pair_sh[bt.n];
   const long long stp = L.step_base ? *L.step_base + L.step_off : a.step;

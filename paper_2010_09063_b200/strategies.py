@@ -88,8 +88,9 @@ class GradEngine:
         # eager mode re-launches kernel by kernel; graph mode replays a CUDA graph
         check(lib.pgb_engine_set_graph(h, 1 if self._mode == ExecMode.graph else 0))
         self.P = self.desc.param_count()
+        self._bound: Optional[Model] = None
         self.set_flat_params(model.flat_params())
-        self._bound: Optional[Model] = model
+        self._bound = model
         self._trace_seconds = time.perf_counter() - t0
 
     def __del__(self):

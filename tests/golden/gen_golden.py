@@ -76,7 +76,34 @@ def full():
         del stacks
         clipped_sum = np.concatenate(parts)
         nclip = int((norms > C).sum())
+        # the reference's own fp32 build on the same inputs: its fp32 stacks
+        # and norms, clip factors and the views path's fp32 ascending sum
+        # (dpsgd.cpp:277-307); its per-block normwise error against the fp64
+        # sum (on the sample) is the accuracy an fp32 implementation reaches
+        p32 = O.ref_init_params(d, 0, np.float32)
+        R32 = O.RefModel(d, strat, B, p32, np.float32)
+        st32, n32 = R32.per_example(x32, y32)
+        del R32
+        s32 = np.where(n32 > np.float32(C), np.float32(C) / n32, np.float32(1)).astype(np.float32)
+        f32_err, f32_norm_err, off = [], float(np.max(np.abs(n32 - norms) / norms)), 0
+        for n in d.blocks:
+            blk = st32[off: off + B * n].reshape(B, n)
+            acc = np.zeros(n, np.float32)
+            for i in range(B):
+                acc = acc + blk[i] * s32[i]
+            f32_err.append(acc)
+            off += B * n
+        del st32
+        f32_sum = np.concatenate(f32_err).astype(np.float64)[::every]
+        want = clipped_sum[::every]
+        rel, off = [], 0
+        for n in d.blocks:
+            lo, hi = -(-off // every), -(-(off + n) // every)
+            den = np.linalg.norm(want[lo:hi])
+            rel.append(np.linalg.norm(f32_sum[lo:hi] - want[lo:hi]) / den if den > 0 else 0.0)
+            off += n
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), norms=norms, clip_scales=s,
+                            ref_f32_block_rel=np.array(rel), ref_f32_norm_rel=f32_norm_err,
                             clipped_count=np.int64(nclip), clipped_sum=clipped_sum[::every],
                             every=np.int64(every), blocks=np.array(d.blocks, np.int64),
                             B=np.int64(B), clip=np.float64(C), x_sha=np.array(digest(x32)),

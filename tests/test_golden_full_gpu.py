@@ -8,9 +8,15 @@ the reference's fp64 GradEngine::compute, clipped sum assembled in fp64):
   gradients, the probe below the same kernels' clipped sum).
 
 Per-example norms element-wise rel <= 1e-5, clip count exact, the noise-free
-clipped sum per block normwise rel <= 1e-5 (over the fixture's strided
-sample) and element-wise |d| <= 1e-5 (|ref| + max|ref|); then one sigma = 0
-step's update carries the same sum.
+clipped sum per block normwise rel <= max(1e-5, 3 e_ref) (over the fixture's
+strided sample) and element-wise |d| <= max(1e-5, 3 e_ref) (|ref| + max|ref|),
+where e_ref is the normwise error of the REFERENCE's own fp32 build against
+its fp64 sum on the same inputs (stored in the fixture). For the CIFAR CNN at
+B = 256, e_ref reaches 4.6e-4 on the first conv block: the backward pass
+through eight conv layers in fp32 and the cancellation of 256 clipped
+per-example gradients put 1e-5 out of reach of any fp32 implementation, the
+reference's included; for the embedding model e_ref <= 7e-7 and the 1e-5 bar
+applies. Then one sigma = 0 step's update carries the same sum.
 """
 import os
 
@@ -74,11 +80,14 @@ def test_full_size_clipped_sum_matches_reference_fixture(P, case):
     assert nclip == int(f["clipped_count"])
     gs = got[::every].astype(np.float64)
     want = f["clipped_sum"]
-    for lo, hi in _sampled_blocks(f):
+    bars = np.maximum(TOL, 3.0 * f["ref_f32_block_rel"])
+    for (lo, hi), bar in zip(_sampled_blocks(f), bars):
+        if hi <= lo:
+            continue
         w, g = want[lo:hi], gs[lo:hi]
         den = np.linalg.norm(w)
-        assert np.linalg.norm(g - w) <= TOL * den + 1e-30
-        assert np.all(np.abs(g - w) <= TOL * (np.abs(w) + np.abs(w).max()))
+        assert np.linalg.norm(g - w) <= bar * den + 1e-30, (lo, hi, bar)
+        assert np.all(np.abs(g - w) <= bar * (np.abs(w) + np.abs(w).max()))
 
     # the step path (for the embedding model: the sparse per-example
     # gradients) carries the same clipped sum: sigma = 0, p_new = p - lr*sum/B
@@ -92,6 +101,6 @@ def test_full_size_clipped_sum_matches_reference_fixture(P, case):
     step_sum = ((p0 - p1) * B / lr)[::every]
     # the update is rounded at max(|p|, |p_new|): one ulp of it, in sum units
     ulp = ((np.abs(p0) + np.abs(p1)) * 2.0 ** -23 * B / lr)[::every]
-    for lo, hi in _sampled_blocks(f):
+    for (lo, hi), bar in zip(_sampled_blocks(f), bars):
         w, g = want[lo:hi], step_sum[lo:hi]
-        assert np.linalg.norm(g - w) <= TOL * np.linalg.norm(w) + np.linalg.norm(ulp[lo:hi])
+        assert np.linalg.norm(g - w) <= bar * np.linalg.norm(w) + np.linalg.norm(ulp[lo:hi])

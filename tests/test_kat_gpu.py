@@ -119,8 +119,10 @@ def test_clip_boundary_in_each_step_kernel(P, case, monkeypatch):
     np.testing.assert_array_equal(ra.pre_clip_norms, n)
     assert ra.clipped_count == 0
     np.testing.assert_array_equal(at, loose)
-    below, rb = step(np.nextafter(top, np.float32(0)))
+    # one ulp below clips (the factor fl(C / n) may round the update back)
+    _, rb = step(np.nextafter(top, np.float32(0)))
     assert rb.clipped_count == int((n >= top).sum())
+    below, _ = step(top * np.float32(0.5))
     assert not np.array_equal(below, loose)
     if B > 1:  # the count at an interior boundary: exactly the norms above it
         mid = np.float32(np.sort(n)[B // 2])
@@ -294,5 +296,5 @@ def test_index_messages_match_compiled_reference(P, O):
         with pytest.raises(Exception) as ours:
             P.dpsgd_step(model, eng, x, data.labels,
                          P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1), 0)
-        assert str(ours.value).split(": ", 1)[-1].endswith(
-            str(ref_err.value).split("gather_rows")[-1]), (str(ours.value), str(ref_err.value))
+        ref_msg = str(ref_err.value).split("] ", 1)[1]  # OracleError: "[code] what()"
+        assert str(ours.value) == ref_msg, (str(ours.value), ref_msg)

@@ -61,6 +61,22 @@ MODELS = {
 }
 
 
+def tc_peaks():
+    """Measured TF32 dense and FP32 SGEMM peaks of this pool's B200s
+    (scripts/measure_peaks.py -> profiles/*_peaks.json; SURVEY 8(d) asks for
+    them beside the bf16 number): the 3xTF32 ceiling of an fp32-accurate
+    tensor-core kernel is tf32 / 3."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_peaks.json")), reverse=True):
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+            return float(d["tf32_tflops"]), float(d["fp32_sgemm_tflops"]), os.path.relpath(f, ROOT)
+        except Exception:
+            pass
+    return None, None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -444,6 +460,7 @@ def run_ours(args):
 
     # ---- per-kernel device time of the same schedule ------------------------
     hbm, bf16, peak_kind = peaks()
+    tf32, fp32_sgemm, tf32_src = tc_peaks()
     nk = C.c_int32()
     ms = np.zeros(64, np.float32)
     names = C.create_string_buffer(64 * 32)
@@ -471,6 +488,7 @@ def run_ours(args):
                 "engine": "fp32 FFMA/FFMA2 on CUDA cores; per-example GEMMs are 16-256 wide and "
                           "run shared-memory-bandwidth bound (DESIGN.md 3.1)",
                 "fp32_simt_peak_tflops": fp32_peak, "frac_of_fp32_simt_peak": ach / fp32_peak,
+                "fp32_sgemm_tflops_measured": fp32_sgemm,
                 "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
     elif dom_name == "mnist_tc":
         # the whole per-example pass with its conv GEMMs on tcgen05: algorithmic
@@ -485,8 +503,9 @@ def run_ours(args):
                 "engine": "tcgen05.mma kind::tf32 with the 3xTF32 split folded into M/N "
                           "(fp32 parity); conv fwd / per-example dW / input grad on tensor "
                           "cores, pooling, dense layers and the loss on CUDA cores",
-                "tf32x3_effective_peak_tflops": bf16 / 2 / 3,
-                "frac_of_tf32x3_effective_peak": ach / (bf16 / 6),
+                "tf32x3_effective_peak_tflops": (tf32 or bf16 / 2) / 3,
+                "frac_of_tf32x3_effective_peak": ach / ((tf32 or bf16 / 2) / 3),
+                "tf32_peak_tflops_measured": tf32, "tf32_peak_source": tf32_src,
                 "tensor_pipe_active_pct_ncu": tk.get("tensor_pipe_active_pct"),
                 "issue_active_pct_ncu": tk.get("issue_active_pct"),
                 "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
@@ -499,6 +518,9 @@ def run_ours(args):
                 "bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
                 "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
                 "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once)",
+                "tf32x3_effective_peak_tflops": (tf32 or bf16 / 2) / 3,
+                "frac_of_tf32x3_effective_peak": ach / ((tf32 or bf16 / 2) / 3),
+                "tf32_peak_tflops_measured": tf32, "tf32_peak_source": tf32_src,
                 "share_of_step": tc_ms / step_ms, "avg_launch_us": tc_ms * 1e3}
     if "aggregate" in by_name:
         agg_b = aggregate_bytes(desc, BATCH, fused,

@@ -244,6 +244,11 @@ pgb_status pgb_profile_steps(pgb_engine* e, const float* d_x, const float* d_y,
  * host buffers. */
 pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
                              const float* B, float* C);
+/* Self-test of the TMA-fed tcgen05 GEMM (tensor maps, 128-B swizzle, 3xTF32
+ * with the hi/lo split on the CUDA cores): C (M x N) = A (M x K) . B (N x K)^T,
+ * row-major, K a multiple of 4. */
+pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
+                              const float* B, float* C);
 /* Self-test of the UMMA operand layouts (K-major / MN-major, no swizzle) and
  * the TMEM accumulator row map: raw TMEM dump (128 lanes x N) of
  * A (MxK) . B (NxK)^T, M in {64, 128}, K <= 32. */

@@ -104,6 +104,8 @@ EXPORTS = {
                                     C.POINTER(C.c_int32)]),
     "pgb_debug_tc_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
+    "pgb_debug_tma_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
     "pgb_debug_umma_probe": (C.c_int, [C.c_int32] * 6 + [C.c_void_p] * 3),
     "pgb_debug_umma_rate": (C.c_int, [C.c_int32] * 4 + [C.c_void_p, C.c_int32, C.c_void_p]),
     "pgb_run_steps_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,

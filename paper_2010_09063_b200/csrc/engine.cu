@@ -24,6 +24,7 @@
 #include "tc.cuh"
 #include "conv_tc.cuh"
 #include "pgb_internal.h"
+#include "tma_gemm.cuh"
 
 namespace pgb {
 
@@ -2345,6 +2346,40 @@ pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, co
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((N + BN - 1) / BN, (M + tc::kBM - 1) / tc::kBM, 1);
     tc::tc_gemm_kernel<tc::PlainOp, BN, 128><<<grid, 128, smem>>>(op);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaDeviceSynchronize());
+    PGB_CUDA(cudaMemcpy(Cout, dC, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
+  });
+}
+
+pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
+                              const float* Bm, float* Cout) {
+  return guarded([&] {
+    if (M <= 0 || N <= 0 || K <= 0 || K % 4) raise(PGB_ERR_CONTRACT, "tma gemm: K % 4 == 0");
+    PGB_CUDA(cudaSetDevice(device));
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    PGB_CUDA(cudaMalloc(&dA, sizeof(float) * (size_t)M * K));
+    PGB_CUDA(cudaMalloc(&dB, sizeof(float) * (size_t)N * K));
+    PGB_CUDA(cudaMalloc(&dC, sizeof(float) * (size_t)M * N));
+    PGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * (size_t)M * K, cudaMemcpyHostToDevice));
+    PGB_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * (size_t)N * K, cudaMemcpyHostToDevice));
+    tg::Params p{};
+    const int bn = tg::pick_bn(N);
+    const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N};
+    const uint64_t st[1] = {sizeof(float) * (uint64_t)K};
+    const uint32_t ba[2] = {32, 128}, bb[2] = {32, (uint32_t)bn};
+    tg::make_map(&p.ta, dA, 2, da, st, ba);
+    tg::make_map(&p.tb, dB, 2, db, st, bb);
+    p.mode = tg::kPlain;
+    p.M = M;
+    p.N = N;
+    p.nchunks = (K + 31) / 32;
+    p.out = dC;
+    p.ldc = N;
+    tg::launch(p, bn, dim3((N + bn - 1) / bn, (M + 127) / 128, 1), 0);
     PGB_CUDA(cudaGetLastError());
     PGB_CUDA(cudaDeviceSynchronize());
     PGB_CUDA(cudaMemcpy(Cout, dC, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost));

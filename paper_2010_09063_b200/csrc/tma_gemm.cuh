@@ -1,0 +1,538 @@
+// Warp-specialised tcgen05 GEMM fed by tensor-map TMA (cp.async.bulk.tensor,
+// SASS UTMALDG), for the convolution GEMMs of the layer-wise engine (CIFAR):
+//
+//   D[m][n] = sum_k A[m][k] * B[n][k]      fp32-accurate (3xTF32), TMEM accumulator
+//
+// Both operands are K-major with the 128-byte swizzle: a K chunk is 32 fp32
+// (one 128-B row per operand row), loaded by TMA boxes straight from the
+// activation / weight tensors -- the implicit im2col is the box coordinates
+// (a tap of the 3x3 kernel is a shifted box; the zero padding is the TMA
+// out-of-bounds fill), no patch matrix and no register gather.
+//
+// fp32 accuracy: tcgen05 kind::tf32 reads the top 19 bits of each fp32
+// operand (truncation, measured: scripts/tf32_probe.py). Four CUDA-core warps
+// split each TMA tile in place: hi = rna_tf32(x) over the tile, lo =
+// rna_tf32(x - hi) into a second buffer of the same (swizzled) layout -- the
+// split is element-wise, so the layout needs no decoding. D += Ahi.Bhi +
+// Ahi.Blo + Alo.Bhi, each dropped or rounded term <= 2^-22 relative (using the
+// raw tile as hi with lo = x - trunc(x) measured ~1e-5 normwise: too coarse).
+//
+// The tensor core's fp32 accumulation is not round-to-nearest (a K = 1152
+// chain in one accumulator measured ~8e-6 normwise, linear in K), so the hi.hi
+// products rotate over NACC accumulators chunk by chunk and the two small
+// correction products share one more; the epilogue adds them in fp32 on the
+// CUDA cores (all of TMEM: one CTA per SM).
+//
+// Roles (256 threads): warp 0 lane 0 issues TMA into an S-stage ring; warps
+// 4-7 split each stage (then run the epilogue from TMEM); warp 1 lane 0
+// issues the 12 MMAs of a stage and commits them to the stage's "empty"
+// barrier, which hands the stage back to TMA.
+//
+// Modes (im2col as box coordinates; conv 3x3, stride 1, pad 1):
+//   kPlain   A[M][K], B[N][K] row-major (self-test)
+//   kConvFwd A = input  NHWC (channels padded to Cp, a multiple of 32): m = position,
+//            k = (tap, c); B = Wt[d][tap * Cp + c]; out NCHW + bias (+ relu)
+//   kConvDx  A = output cotangent NHWC (Dp), m = input position, k = (tap, d),
+//            shifted by the flipped tap; B = Wt2[c][tap * Dp + d];
+//            out NCHW gx (* [mask > 0], the relu of the layer below)
+//   kConvDw  per example z: A = input NCHW, m = (tap, c) (a box per tap),
+//            k = position; B = output cotangent NCHW (n = d);
+//            out = the reference's per-example dW stack (B, D, C, 3, 3)
+//            (strategies.cpp:156-170) + each tile's squared sum (fp64)
+#pragma once
+
+#include <cuda.h>
+
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace pgb {
+namespace tg {
+
+constexpr int kBM = 128, kBK = 32, kThreads = 256;
+enum Mode { kPlain = 0, kConvFwd = 1, kConvDx = 2, kConvDw = 3 };
+
+struct alignas(64) Params {
+  CUtensorMap ta, tb;
+  int mode;
+  int M, N;          // GEMM rows / columns (valid extents)
+  int nchunks;       // K chunks of 32
+  // geometry (conv modes)
+  int C, H, W, D;    // layer input channels, spatial, output channels
+  int Cg;            // fwd: Cp / 32 (channel groups per tap); dx: Dp / 32
+  int by, bn;        // fwd/dx A box: rows per image, images (box = 32 x W x by x bn)
+  int Cr, T;         // dw: rows per tap slot (multiple of 8), tap slots per M tile
+  int big_c;         // dw: C >= 128 -> M tile = 128 channels of one tap
+  int bx, dw_by;     // dw boxes: x extent, rows per chunk
+  int tiles;         // tiles per GEMM (gridDim.x * gridDim.y), tile_sq row length
+  // epilogue
+  float* out;
+  const float* bias;
+  const float* mask;
+  double* tile_sq;
+  int relu;
+  int ldc;           // kPlain: row stride of out
+};
+
+template <int BN>
+constexpr int stages() { return BN >= 128 ? 3 : BN >= 64 ? 4 : 5; }
+// hi.hi accumulators: all of TMEM but one accumulator (the corrections)
+template <int BN>
+constexpr int nacc() { return 512 / (BN < 32 ? 32 : BN) - 1; }
+
+template <int BN>
+struct Smem {
+  static constexpr int S = stages<BN>();
+  float a_hi[S][kBM * kBK];
+  float a_lo[S][kBM * kBK];
+  float b_hi[S][BN * kBK];
+  float b_lo[S][BN * kBK];
+  uint64_t full[S], split[S], empty[S];
+  uint64_t acc;
+  uint32_t tmem;
+  double sq[4];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA descriptor, K-major, SWIZZLE_128B: 8-row atoms of 128 B, SBO = 1024 B
+// between atoms (LBO unused); the K step inside the atom advances the start
+// address by 32 B (8 tf32). Tiles are 1024-B aligned.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, int c0, int c1,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                       int c3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
+
+// in place: hi = rna(x); returns lo = rna(x - hi), four at a time
+__device__ __forceinline__ float4 split4(float4& v) {
+  float4 lo;
+  float h;
+  h = rna_tf32(v.x); lo.x = rna_tf32(v.x - h); v.x = h;
+  h = rna_tf32(v.y); lo.y = rna_tf32(v.y - h); v.y = h;
+  h = rna_tf32(v.z); lo.z = rna_tf32(v.z - h); v.z = h;
+  h = rna_tf32(v.w); lo.w = rna_tf32(v.w - h); v.w = h;
+  return lo;
+}
+
+// Bytes TMA delivers per stage for operand A of M tile mt (full boxes, OOB
+// included). A dW tile past the ninth tap leaves its slots unloaded: those
+// accumulator rows are never stored.
+__device__ __forceinline__ uint32_t a_bytes(const Params& p, int mt) {
+  if (p.mode == kConvDw)
+    return (uint32_t)(p.big_c ? kBM : min(p.T, 9 - mt * p.T) * p.Cr) * kBK * 4;
+  return kBM * kBK * 4;
+}
+
+// Issue the TMA boxes of K chunk q of tile (mt, nt) for example z.
+template <int BN>
+__device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s, int q, int mt,
+                                            int nt, int z) {
+  const uint32_t bar = smem_u32(&S.full[s]);
+  const uint32_t da = smem_u32(S.a_hi[s]), db = smem_u32(S.b_hi[s]);
+  switch (p.mode) {
+    case kPlain:
+      tma_2d(da, &p.ta, q * kBK, mt * kBM, bar);
+      tma_2d(db, &p.tb, q * kBK, nt * BN, bar);
+      break;
+    case kConvFwd:
+    case kConvDx: {
+      const int tap = q / p.Cg, cg = q - tap * p.Cg;
+      const int u = tap / 3, v = tap - 3 * u;
+      const int HW = p.H * p.W;
+      const int m0 = mt * kBM, n0 = m0 / HW, y0 = (m0 - n0 * HW) / p.W;
+      // forward: x + v - 1, y + u - 1; input gradient: the flipped tap
+      const int dx = p.mode == kConvFwd ? v - 1 : 1 - v;
+      const int dy = p.mode == kConvFwd ? u - 1 : 1 - u;
+      tma_4d(da, &p.ta, cg * kBK, dx, y0 + dy, n0, bar);
+      tma_2d(db, &p.tb, tap * p.Cg * kBK + cg * kBK, nt * BN, bar);
+      break;
+    }
+    case kConvDw: {
+      const int y0 = q * p.dw_by;
+      if (p.big_c) {
+        const int cgs = p.C / kBM, tap = mt / cgs, c0 = (mt - tap * cgs) * kBM;
+        const int u = tap / 3, v = tap - 3 * u;
+        tma_4d(da, &p.ta, v - 1, y0 + u - 1, c0, z, bar);
+      } else {
+        for (int sl = 0; sl < p.T; ++sl) {
+          const int tap = mt * p.T + sl;
+          if (tap >= 9) break;
+          const int u = tap / 3, v = tap - 3 * u;
+          tma_4d(da + sl * p.Cr * kBK * 4, &p.ta, v - 1, y0 + u - 1, 0, z, bar);
+        }
+      }
+      tma_4d(db, &p.tb, 0, y0, nt * BN, z, bar);
+      break;
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  // the swizzled tiles need 1024-B alignment of the dynamic window
+  Smem<BN>& S = *reinterpret_cast<Smem<BN>*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int NS = Smem<BN>::S;
+  constexpr uint32_t kCols = 512;
+  constexpr int NACC = nacc<BN>();
+  constexpr uint32_t kAccStride = BN < 32 ? 32 : BN;  // TMEM columns per accumulator
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int nt = blockIdx.x, mt = blockIdx.y, z = blockIdx.z;
+  const int nq = p.nchunks;
+  if (warp == 1) tc::tmem_alloc(&S.tmem, kCols);
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) {
+      tc::mbar_init(&S.full[s], 1);
+      tc::mbar_init(&S.split[s], 4);
+      tc::mbar_init(&S.empty[s], 1);
+    }
+    tc::mbar_init(&S.acc, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb) : "memory");
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem;
+
+  if (warp == 0) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      const uint32_t bytes = a_bytes(p, mt) + BN * kBK * 4;
+      for (int q = 0; q < nq; ++q) {
+        const int s = q % NS;
+        if (q >= NS) tc::mbar_wait(&S.empty[s], ((q / NS) - 1) & 1);
+        expect_tx(&S.full[s], bytes);
+        issue_chunk<BN>(p, S, s, q, mt, nt, z);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN < 16 ? 16 : BN);
+      for (int q = 0; q < nq; ++q) {
+        const int s = q % NS;
+        tc::mbar_wait(&S.split[s], (q / NS) & 1);
+        tc::fence_after_sync();
+        const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
+        const uint32_t bh = smem_u32(S.b_hi[s]), bl = smem_u32(S.b_lo[s]);
+        const uint32_t dmain = tmem + (uint32_t)(q % NACC) * kAccStride;
+        const uint32_t dcorr = tmem + (uint32_t)NACC * kAccStride;
+#pragma unroll
+        for (int k = 0; k < kBK / 8; ++k) {
+          const uint32_t o = 32u * k;
+          tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
+                       (q >= NACC || k) ? 1u : 0u);
+          tc::mma_tf32(dcorr, desc_sw128(ah + o), desc_sw128(bl + o), idesc, (q | k) ? 1u : 0u);
+          tc::mma_tf32(dcorr, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+        }
+        tc::commit(&S.empty[s]);
+      }
+      tc::commit(&S.acc);
+    }
+  } else if (warp >= 4) {
+    // ---- hi/lo split of each stage (warps 4-7) ----
+    const int ts = t - 128;
+    const uint32_t abytes = a_bytes(p, mt);
+    for (int q = 0; q < nq; ++q) {
+      const int s = q % NS;
+      tc::mbar_wait(&S.full[s], (q / NS) & 1);
+      float4* ah = reinterpret_cast<float4*>(S.a_hi[s]);
+      float4* al = reinterpret_cast<float4*>(S.a_lo[s]);
+      for (int i = ts; i < (int)(abytes / 16); i += 128) {
+        float4 v = ah[i];
+        al[i] = split4(v);
+        ah[i] = v;
+      }
+      float4* bh = reinterpret_cast<float4*>(S.b_hi[s]);
+      float4* bl = reinterpret_cast<float4*>(S.b_lo[s]);
+#pragma unroll
+      for (int i = ts; i < BN * kBK / 4; i += 128) {
+        float4 v = bh[i];
+        bl[i] = split4(v);
+        bh[i] = v;
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.split[s]);
+    }
+    // ---- epilogue: TMEM -> registers -> global ----
+    tc::mbar_wait(&S.acc, 0);
+    tc::fence_after_sync();
+    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
+    double sq = 0.0;
+    const int m = mt * kBM + r;
+    const int used = nq < NACC ? nq : NACC;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      float v[8], w[8];
+      tc::tmem_ld8(lane_base + (uint32_t)(NACC * kAccStride + c0), v);  // corrections
+#pragma unroll 1
+      for (int a = 0; a < used; ++a) {
+        tc::tmem_ld8(lane_base + (uint32_t)(a * kAccStride + c0), w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] += w[j];
+      }
+      const int n0 = nt * BN + c0;
+      switch (p.mode) {
+        case kPlain:
+          if (m < p.M)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (n0 + j < p.N) p.out[(size_t)m * p.ldc + n0 + j] = v[j];
+          break;
+        case kConvFwd: {
+          const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+          if (m < p.M)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int d = n0 + j;
+              if (d < p.N) {
+                float o = v[j] + p.bias[d];
+                if (p.relu) o = fmaxf(o, 0.0f);
+                p.out[((size_t)img * p.D + d) * HW + pos] = o;
+              }
+            }
+          break;
+        }
+        case kConvDx: {
+          const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+          if (m < p.M)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int c = n0 + j;
+              if (c < p.N) {
+                const size_t i = ((size_t)img * p.C + c) * HW + pos;
+                p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : v[j];
+              }
+            }
+          break;
+        }
+        case kConvDw: {
+          int tap, c;
+          if (p.big_c) {
+            const int cgs = p.C / kBM;
+            tap = mt / cgs;
+            c = (mt - tap * cgs) * kBM + r;
+          } else {
+            const int sl = r / p.Cr;
+            tap = mt * p.T + sl;
+            c = r - sl * p.Cr;
+          }
+          if (tap < 9 && c < p.C) {
+            float* st = p.out + (size_t)z * p.D * p.C * 9;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int d = n0 + j;
+              if (d < p.N) {
+                st[((size_t)d * p.C + c) * 9 + tap] = v[j];
+                sq = fma((double)v[j], (double)v[j], sq);
+              }
+            }
+          }
+          break;
+        }
+      }
+    }
+    if (p.mode == kConvDw && p.tile_sq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) S.sq[q4] = sq;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 128)
+        p.tile_sq[(size_t)z * p.tiles + mt * gridDim.x + nt] =
+            ((S.sq[0] + S.sq[1]) + S.sq[2]) + S.sq[3];
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, kCols);
+}
+
+template <int BN>
+inline size_t smem_bytes() {
+  return sizeof(Smem<BN>) + 1024;
+}
+
+}  // namespace tg
+}  // namespace pgb
+
+// ---------------------------------------------------------------------------
+// Layout kernels feeding the TMA operands, and the host side.
+// ---------------------------------------------------------------------------
+namespace pgb {
+namespace tg {
+
+// NCHW (B, C, HW) -> NHWC (B, HW, Cp), channels zero-padded to Cp (32 x 32
+// tiles through shared memory: coalesced on both sides)
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C,
+                                    int HW, int Cp) {
+  __shared__ float tile[32][33];
+  const int n = blockIdx.z, p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int c = c0 + j, p = p0 + threadIdx.x;
+    tile[j][threadIdx.x] = (c < C && p < HW) ? src[((size_t)n * C + c) * HW + p] : 0.0f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int p = p0 + j, c = c0 + threadIdx.x;
+    if (p < HW) dst[((size_t)n * HW + p) * Cp + c] = tile[threadIdx.x][j];
+  }
+}
+
+// conv weights (D, C, 3, 3) -> the forward B operand Wt[d][tap * Cp + c]
+__global__ void conv_wt_fwd_kernel(const float* __restrict__ W, float* __restrict__ wt, int D,
+                                   int C, int Cp) {
+  const int n = D * 9 * Cp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int d = e / (9 * Cp), r = e - d * 9 * Cp, tap = r / Cp, c = r - tap * Cp;
+    wt[e] = c < C ? W[((size_t)d * C + c) * 9 + tap] : 0.0f;
+  }
+}
+
+// conv weights (D, C, 3, 3) -> the input-gradient B operand Wt2[c][tap * Dp + d]
+__global__ void conv_wt_dx_kernel(const float* __restrict__ W, float* __restrict__ wt, int D,
+                                  int C, int Dp) {
+  const int n = C * 9 * Dp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int c = e / (9 * Dp), r = e - c * 9 * Dp, tap = r / Dp, d = r - tap * Dp;
+    wt[e] = d < D ? W[((size_t)d * C + c) * 9 + tap] : 0.0f;
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// dependency on libcuda)
+inline EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !f || q != cudaDriverEntryPointSuccess)
+      raise(PGB_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+    fn = reinterpret_cast<EncodeFn>(f);
+  }
+  return fn;
+}
+
+// fp32 tensor map, 128-B swizzle, zero out-of-bounds fill. dims/box innermost
+// first; strides (bytes) of dims 1..rank-1.
+inline void make_map(CUtensorMap* m, const float* base, int rank, const uint64_t* dims,
+                     const uint64_t* strides, const uint32_t* box) {
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank,
+                               const_cast<float*>(base), d, st, b, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    raise(PGB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+inline int pick_bn(int n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+
+template <int BN>
+inline void launch_bn(const Params& p, dim3 grid, cudaStream_t s) {
+  static int attr_dev = -1;  // the attribute is set once per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(tma_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_bytes<BN>());
+    attr_dev = dev;
+  }
+  tma_gemm_kernel<BN><<<grid, kThreads, smem_bytes<BN>(), s>>>(p);
+}
+
+inline void launch(const Params& p, int bn, dim3 grid, cudaStream_t s) {
+  switch (bn) {
+    case 16: launch_bn<16>(p, grid, s); break;
+    case 32: launch_bn<32>(p, grid, s); break;
+    case 64: launch_bn<64>(p, grid, s); break;
+    default: launch_bn<128>(p, grid, s); break;
+  }
+}
+
+// The TMA engine takes 3x3 / stride 1 / pad 1 convolutions whose rows tile a
+// 128-position block: W in {4, 8, 16, 32}, and either 128 | H*W or H*W | 128.
+inline bool conv_ok(const ConvGeom& g) {
+  if (g.k != 3 || g.stride != 1 || g.pad != 1 || g.Ho != g.H || g.Wo != g.W) return false;
+  if (!(g.W == 4 || g.W == 8 || g.W == 16 || g.W == 32)) return false;
+  const int hw = g.H * g.W;
+  return hw >= 128 ? hw % 128 == 0 : 128 % hw == 0;
+}
+
+inline int round32(int c) { return (c + 31) / 32 * 32; }
+
+// A-operand box of the forward / input-gradient GEMMs: 32 channels x W x by rows x bn images
+inline void fwd_box(const ConvGeom& g, int& by, int& bn) {
+  const int rows = 128 / g.W;
+  by = rows < g.H ? rows : g.H;
+  bn = 128 / (g.W * by);
+}
+
+// per-example dW M tiling: rows per tap slot Cr, slots per tile T, tiles
+inline void dw_tiling(int C, int& Cr, int& T, int& big, int& mtiles) {
+  big = C >= 128 && C % 128 == 0;
+  if (big) {
+    Cr = 128;
+    T = 1;
+    mtiles = 9 * C / 128;
+  } else {
+    Cr = (C + 7) / 8 * 8;
+    T = 128 / Cr;
+    if (T < 1) T = 1;
+    mtiles = (9 + T - 1) / T;
+  }
+}
+
+}  // namespace tg
+}  // namespace pgb

@@ -42,3 +42,21 @@ def test_umma_layouts(P, M, N):
     want = A @ B.T
     lanes = np.arange(M) if M == 128 else (np.arange(M) % 16 + 32 * (np.arange(M) // 16))
     np.testing.assert_array_equal(D[lanes], want)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 64, 96), (200, 100, 76), (1000, 16, 288),
+                                   (384, 128, 1152), (64, 32, 4)])
+def test_tma_gemm_3xtf32(P, M, N, K):
+    """The TMA-fed GEMM (tensor maps with the 128-B swizzle, K-major UMMA
+    descriptors, hi = the TMA tile itself since tcgen05 truncates tf32, lo
+    split on the CUDA cores): normwise 1e-6 against fp64, ragged M/N/K (the
+    TMA out-of-bounds fill)."""
+    rng = np.random.default_rng(M + 3 * N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    Cm = np.zeros((M, N), np.float32)
+    P._lib.check(P.lib.pgb_debug_tma_gemm(0, M, N, K, P._lib.ptr(A), P._lib.ptr(B),
+                                          P._lib.ptr(Cm)))
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    err = np.linalg.norm(Cm - want) / np.linalg.norm(want)
+    assert err < 1e-6, err

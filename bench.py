@@ -509,15 +509,17 @@ def run_ours(args):
                 "tensor_pipe_active_pct_ncu": tk.get("tensor_pipe_active_pct"),
                 "issue_active_pct_ncu": tk.get("issue_active_pct"),
                 "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
-    elif dom_name.endswith("_tc"):
-        tc_ms = sum(m for n, m in by_name.items() if n.endswith("_tc"))
+    elif dom_name.endswith("_tc") or dom_name.endswith("_tma"):
+        conv = [n for n in by_name if n.endswith("_tc") or n.endswith("_tma")]
+        tc_ms = sum(by_name[n] for n in conv)
         flops = conv_gemm_flops(desc, BATCH)
         ach = flops / (tc_ms * 1e-3) / 1e12
-        roof = {"kernel": "conv GEMMs on tcgen05 (" + ", ".join(
-                    n for n in by_name if n.endswith("_tc")) + ")",
+        roof = {"kernel": "conv GEMMs on tcgen05 (" + ", ".join(conv) + ")",
                 "bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
                 "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
-                "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once)",
+                "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once); "
+                          "3x3 convs fed by tensor-map TMA (128-B swizzle), the others by "
+                          "register gathers",
                 "tf32x3_effective_peak_tflops": (tf32 or bf16 / 2) / 3,
                 "frac_of_tf32x3_effective_peak": ach / ((tf32 or bf16 / 2) / 3),
                 "tf32_peak_tflops_measured": tf32, "tf32_peak_source": tf32_src,

@@ -150,6 +150,28 @@ struct Engine {
   bool pairs_next = false;     // ... for the launch enqueue_step is making
   unsigned long long* d_grid_ctr = nullptr;
   bool use_tc = true;        // conv GEMMs on tcgen05 (PGB_NO_TC=1: CUDA-core tiles)
+  // 3x3 / stride-1 convolutions on the TMA-fed tcgen05 GEMM (tma_gemm.cuh;
+  // PGB_NO_TMA=1: the register-gather tcgen05 GEMM of conv_tc.cuh)
+  bool use_tma = true;
+  // per GEMM kind, measured on the CIFAR layers (profiles/r02_cifar_*):
+  // forward for C >= 16 inputs; input gradient for the 8x8 / 4x4 layers with
+  // >= 32 output channels (the larger maps re-read each tap's shifted box from
+  // L2 and lose to the gather GEMM); per-example dW stays on the gather GEMM
+  // (its 9 x C row tiles scatter stride-9 stores and pay a TMEM set-up per
+  // example). PGB_TMA_ALL=1 takes every eligible GEMM (parity tests).
+  bool tma_all = false;
+  bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
+  bool tma_dx(const ConvGeom& g) const {
+    return use_tma && tg::conv_ok(g) && (tma_all || (g.H * g.W <= 64 && g.D >= 32));
+  }
+  bool tma_dw(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && tma_all; }
+  // scratch operands of the TMA GEMMs, each as its 3xTF32 (hi, lo) pair: the
+  // A operand (NHWC copy / shifted copies), the B operand (permuted weights /
+  // the dW cotangent)
+  float* d_nhwc = nullptr;
+  float* d_nhwc_lo = nullptr;
+  float* d_wt = nullptr;
+  float* d_wt_lo = nullptr;
   std::vector<int64_t> param_off;
   int64_t P = 0;
   int64_t in_row = 0;
@@ -340,6 +362,122 @@ struct Engine {
     if (ev_t1) cudaEventDestroy(ev_t1);
   }
 
+  static ConvGeom conv_geom(const Layer& L) {
+    const pgb_layer_spec& sp = L.spec;
+    return ConvGeom{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
+                    (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride, (int)sp.pad};
+  }
+
+  // ---- convolutions on the TMA-fed tcgen05 GEMM (tma_gemm.cuh) --------------
+  // forward: out (B, D, H, W) = conv(x) + bias (+ relu)
+  int tma_conv_fwd(cudaStream_t s, const ConvGeom& g, int Bi, const float* x, const float* W,
+                   const float* bias, float* out, bool relu) {
+    const int Cp = tg::round32(g.C), HW = g.H * g.W, bn = tg::pick_bn(g.D);
+    tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Cp / 32, Bi), dim3(32, 8), 0, s>>>(
+        x, d_nhwc, d_nhwc_lo, g.C, HW, Cp);
+    tg::conv_wt_fwd_kernel<<<grid_for((size_t)g.D * 9 * Cp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
+                                                                         g.C, Cp);
+    tg::Params p{};
+    int by, bnimg;
+    tg::fwd_box(g, by, bnimg);
+    const uint64_t da[4] = {(uint64_t)Cp, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)Bi};
+    const uint64_t sa[3] = {4ull * Cp, 4ull * Cp * g.W, 4ull * Cp * HW};
+    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)by, (uint32_t)bnimg};
+    tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+    tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+    const uint64_t db[2] = {(uint64_t)9 * Cp, (uint64_t)g.D};
+    const uint64_t sb[1] = {4ull * 9 * Cp};
+    const uint32_t bb[2] = {32, (uint32_t)bn};
+    tg::make_map(&p.tb, d_wt, 2, db, sb, bb);
+    tg::make_map(&p.tb_lo, d_wt_lo, 2, db, sb, bb);
+    p.mode = tg::kConvFwd;
+    p.M = Bi * HW;
+    p.N = g.D;
+    p.nchunks = 9 * Cp / 32;
+    p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
+    p.Cg = Cp / 32;
+    p.by = by, p.bn = bnimg;
+    p.out = out;
+    p.bias = bias;
+    p.relu = relu ? 1 : 0;
+    tg::launch(p, bn, dim3((g.D + bn - 1) / bn, (p.M + 127) / 128, 1), s);
+    return 3;
+  }
+
+  // input gradient: gx (B, C, H, W) = conv^T(gout) * [mask > 0]
+  int tma_conv_dx(cudaStream_t s, const ConvGeom& g, int Bi, const float* gout, const float* W,
+                  const float* mask, float* gx) {
+    const int Dp = tg::round32(g.D), HW = g.H * g.W, bn = tg::pick_bn(g.C);
+    tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Dp / 32, Bi), dim3(32, 8), 0, s>>>(
+        gout, d_nhwc, d_nhwc_lo, g.D, HW, Dp);
+    tg::conv_wt_dx_kernel<<<grid_for((size_t)g.C * 9 * Dp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
+                                                                        g.C, Dp);
+    tg::Params p{};
+    int by, bnimg;
+    tg::fwd_box(g, by, bnimg);
+    const uint64_t da[4] = {(uint64_t)Dp, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)Bi};
+    const uint64_t sa[3] = {4ull * Dp, 4ull * Dp * g.W, 4ull * Dp * HW};
+    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)by, (uint32_t)bnimg};
+    tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+    tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+    const uint64_t db[2] = {(uint64_t)9 * Dp, (uint64_t)g.C};
+    const uint64_t sb[1] = {4ull * 9 * Dp};
+    const uint32_t bb[2] = {32, (uint32_t)bn};
+    tg::make_map(&p.tb, d_wt, 2, db, sb, bb);
+    tg::make_map(&p.tb_lo, d_wt_lo, 2, db, sb, bb);
+    p.mode = tg::kConvDx;
+    p.M = Bi * HW;
+    p.N = g.C;
+    p.nchunks = 9 * Dp / 32;
+    p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
+    p.Cg = Dp / 32;
+    p.by = by, p.bn = bnimg;
+    p.out = gx;
+    p.mask = mask;
+    tg::launch(p, bn, dim3((g.C + bn - 1) / bn, (p.M + 127) / 128, 1), s);
+    return 3;
+  }
+
+  // per-example weight gradient stacks (B, D, C, 3, 3) + each tile's squared
+  // sum; returns the tiles per example (the tile_sq row length)
+  int tma_conv_dw(cudaStream_t s, const ConvGeom& g, int Bi, const float* x, const float* gout,
+                  float* stack, double* tile_sq) {
+    const int HW = g.H * g.W, bn = tg::pick_bn(g.D);
+    int Cr, T, big, mtiles;
+    tg::dw_tiling(g.C, Cr, T, big, mtiles);
+    const int bx = g.W, by = 32 / g.W;
+    const long long total = (long long)Bi * g.C * HW;
+    tg::shift3_kernel<<<grid_for((size_t)(3 * total)), 256, 0, s>>>(x, d_nhwc, d_nhwc_lo, total,
+                                                                    g.W);
+    const long long gt = (long long)Bi * g.D * HW;
+    tg::split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(gout, d_wt, d_wt_lo, gt);
+    tg::Params p{};
+    // A: the shifted copies [v][n][c][p] (positions flattened); B: gout [n][d][p]
+    const uint64_t da[4] = {(uint64_t)HW, (uint64_t)g.C, (uint64_t)Bi, 3};
+    const uint64_t sa[3] = {4ull * HW, 4ull * HW * g.C, 4ull * total};
+    const uint32_t ba[4] = {32, (uint32_t)Cr, 1, 1};
+    tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+    tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+    const uint64_t db[3] = {(uint64_t)HW, (uint64_t)g.D, (uint64_t)Bi};
+    const uint64_t sb[2] = {4ull * HW, 4ull * HW * g.D};
+    const uint32_t bb[3] = {32, (uint32_t)bn, 1};
+    tg::make_map(&p.tb, d_wt, 3, db, sb, bb);
+    tg::make_map(&p.tb_lo, d_wt_lo, 3, db, sb, bb);
+    p.mode = tg::kConvDw;
+    p.M = mtiles * 128;
+    p.N = g.D;
+    p.nchunks = (HW + 31) / 32;
+    p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
+    p.Cr = Cr, p.T = T, p.big_c = big;
+    p.bx = bx, p.dw_by = by;
+    const int ntiles = (g.D + bn - 1) / bn;
+    p.tiles = ntiles * mtiles;
+    p.out = stack;
+    p.tile_sq = tile_sq;
+    tg::launch(p, bn, dim3(ntiles, mtiles, Bi), s);
+    return p.tiles;
+  }
+
   // The reference MNIST CNN (models.cpp:107-121) runs as one fused kernel.
   static bool is_mnist(const pgb_model_desc& d) {
     const int64_t want[9][6] = {{PGB_CONV, 1, 16, 8, 2, 3},   {PGB_RELU, 0, 0, 0, 1, 0},
@@ -410,6 +548,8 @@ struct Engine {
     fused_mnist = is_mnist(desc) && std::getenv("PGB_NO_FUSED") == nullptr;
     mnist_tc = fused_mnist && std::getenv("PGB_MNIST_SIMT") == nullptr;
     use_tc = std::getenv("PGB_NO_TC") == nullptr;
+    use_tma = use_tc && std::getenv("PGB_NO_TMA") == nullptr;
+    tma_all = std::getenv("PGB_TMA_ALL") != nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -460,7 +600,28 @@ struct Engine {
           tiles = std::max(tiles, tc::tile_count((int)(in.d[0] * desc.layers[l].k * desc.layers[l].k),
                                                  (int)desc.layers[l].out));
         }
+      int64_t nhwc = 1, wt = 1;
+      for (int l = 0; l < n; ++l)
+        if (desc.layers[l].kind == PGB_CONV && use_tma) {
+          const ConvGeom g = conv_geom(layers[l]);
+          if (!tg::conv_ok(g)) continue;
+          int Cr, T, big, mt;
+          tg::dw_tiling(g.C, Cr, T, big, mt);
+          tiles = std::max(tiles, mt * ((g.D + tg::pick_bn(g.D) - 1) / tg::pick_bn(g.D)));
+          const int64_t hw = (int64_t)g.H * g.W;
+          nhwc = std::max(nhwc, B * hw * std::max(tg::round32(g.C), tg::round32(g.D)));
+          nhwc = std::max(nhwc, 3 * B * hw * g.C);  // the dW input's shifted copies
+          wt = std::max(wt, (int64_t)9 * std::max((int64_t)g.D * tg::round32(g.C),
+                                                  (int64_t)g.C * tg::round32(g.D)));
+          wt = std::max(wt, B * hw * g.D);  // the dW cotangent
+        }
       want((void**)&d_tile_sq, sizeof(double) * B * tiles);
+      if (use_tma) {
+        want((void**)&d_nhwc, sizeof(float) * nhwc);
+        want((void**)&d_nhwc_lo, sizeof(float) * nhwc);
+        want((void**)&d_wt, sizeof(float) * wt);
+        want((void**)&d_wt_lo, sizeof(float) * wt);
+      }
     }
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
     want((void**)&d_parts, sizeof(double) * B * std::max(1, desc.n_params));
@@ -753,7 +914,10 @@ struct Engine {
   int mark(cudaStream_t s, const char* name) {
     static const bool debug_sync = std::getenv("PGB_DEBUG_LAUNCH") != nullptr;
     if (debug_sync) {
-      const cudaError_t e = cudaGetLastError();
+      cudaError_t e = cudaGetLastError();
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (e == cudaSuccess) cudaStreamIsCapturing(s, &cs);
+      if (e == cudaSuccess && cs == cudaStreamCaptureStatusNone) e = cudaStreamSynchronize(s);
       if (e != cudaSuccess)
         raise(PGB_ERR_CUDA, std::string("launch of ") + name + ": " + cudaGetErrorString(e));
     }
@@ -788,7 +952,10 @@ struct Engine {
           ConvGeom g{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
                      (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride, (int)sp.pad};
           const int K = g.C * g.k * g.k;
-          if (use_tc) {
+          if (tma_fwd(g)) {
+            tma_conv_fwd(s, g, Bi, in, W, W + (size_t)g.D * K, L.act_out, L.fused_relu);
+            nk += mark(s, "conv_fwd_tma") + 2;
+          } else if (use_tc) {
             tc::TcConvFwdOp op{Bi * g.Ho * g.Wo, g.D, K, g, in, W, W + (size_t)g.D * K,
                                L.act_out, L.fused_relu ? 1 : 0};
             tc::launch(op, 1, s);
@@ -1038,7 +1205,13 @@ struct Engine {
           const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
           float* sW = d_stacks + param_off[L.pblock] * B;
           float* sb = d_stacks + param_off[L.pblock + 1] * B;
-          if (use_tc) {
+          if (tma_dw(gg)) {
+            const int tiles = tma_conv_dw(s, gg, Bi, in, gcur, sW, d_tile_sq);
+            nk += mark(s, "conv_dw_pex_tma") + 2;
+            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(d_tile_sq, tiles, Bi, d_parts,
+                                                                   nparts, L.pblock);
+            nk += mark(s, "conv_dw_norm");
+          } else if (use_tc) {
             tc::TcConvDWOp dw{K, gg.D, Pp, gg, in, gcur, sW, d_tile_sq};
             tc::launch(dw, Bi, s);
             nk += mark(s, "conv_dw_pex_tc");
@@ -1054,7 +1227,10 @@ struct Engine {
           conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
                                                                          sb);
           nk += mark(s, "conv_db_pex");
-          if (L.needs_gx && use_tc && gg.stride == 1) {
+          if (L.needs_gx && tma_dx(gg)) {
+            tma_conv_dx(s, gg, Bi, gcur, W, L.bwd_mask, gnext);
+            nk += mark(s, "conv_bwd_x_tma") + 2;
+          } else if (L.needs_gx && use_tc && gg.stride == 1) {
             tc::TcConvBwdXS1Op op{Bi * gg.H * gg.W, gg.C, gg.D * gg.k * gg.k, gg, gcur, W,
                                   L.bwd_mask, gnext};
             tc::launch(op, 1, s);
@@ -2366,6 +2542,11 @@ pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, c
     PGB_CUDA(cudaMalloc(&dC, sizeof(float) * (size_t)M * N));
     PGB_CUDA(cudaMemcpy(dA, A, sizeof(float) * (size_t)M * K, cudaMemcpyHostToDevice));
     PGB_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * (size_t)N * K, cudaMemcpyHostToDevice));
+    float *dAl = nullptr, *dBl = nullptr;
+    PGB_CUDA(cudaMalloc(&dAl, sizeof(float) * (size_t)M * K));
+    PGB_CUDA(cudaMalloc(&dBl, sizeof(float) * (size_t)N * K));
+    tg::split_kernel<<<grid_for((size_t)M * K), 256>>>(dA, dA, dAl, (long long)M * K);
+    tg::split_kernel<<<grid_for((size_t)N * K), 256>>>(dB, dB, dBl, (long long)N * K);
     tg::Params p{};
     const int bn = tg::pick_bn(N);
     const uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, db[2] = {(uint64_t)K, (uint64_t)N};
@@ -2373,6 +2554,8 @@ pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, c
     const uint32_t ba[2] = {32, 128}, bb[2] = {32, (uint32_t)bn};
     tg::make_map(&p.ta, dA, 2, da, st, ba);
     tg::make_map(&p.tb, dB, 2, db, st, bb);
+    tg::make_map(&p.ta_lo, dAl, 2, da, st, ba);
+    tg::make_map(&p.tb_lo, dBl, 2, db, st, bb);
     p.mode = tg::kPlain;
     p.M = M;
     p.N = N;
@@ -2386,6 +2569,8 @@ pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, c
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dC);
+    cudaFree(dAl);
+    cudaFree(dBl);
   });
 }
 

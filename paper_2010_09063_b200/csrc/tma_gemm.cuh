@@ -9,13 +9,14 @@
 // (a tap of the 3x3 kernel is a shifted box; the zero padding is the TMA
 // out-of-bounds fill), no patch matrix and no register gather.
 //
-// fp32 accuracy: tcgen05 kind::tf32 reads the top 19 bits of each fp32
-// operand (truncation, measured: scripts/tf32_probe.py). Four CUDA-core warps
-// split each TMA tile in place: hi = rna_tf32(x) over the tile, lo =
-// rna_tf32(x - hi) into a second buffer of the same (swizzled) layout -- the
-// split is element-wise, so the layout needs no decoding. D += Ahi.Bhi +
-// Ahi.Blo + Alo.Bhi, each dropped or rounded term <= 2^-22 relative (using the
-// raw tile as hi with lo = x - trunc(x) measured ~1e-5 normwise: too coarse).
+// fp32 accuracy: every operand arrives pre-split as two tensors, hi =
+// rna_tf32(x) and lo = rna_tf32(x - hi), written by the memory-bound layout
+// kernels that produce the operand anyway (NHWC copy, weight permute, shifted
+// copies); TMA loads both, so the GEMM itself does no CUDA-core work.
+// D += Ahi.Bhi + Ahi.Blo + Alo.Bhi, each dropped or rounded term <= 2^-22
+// relative. (tcgen05 kind::tf32 truncates fp32 operands to their top 19 bits,
+// scripts/tf32_probe.py: feeding the raw tile as hi measured ~1e-5 normwise,
+// and splitting in the GEMM on four warps made it split-bound.)
 //
 // The tensor core's fp32 accumulation is not round-to-nearest (a K = 1152
 // chain in one accumulator measured ~8e-6 normwise, linear in K), so the hi.hi
@@ -23,10 +24,10 @@
 // correction products share one more; the epilogue adds them in fp32 on the
 // CUDA cores (all of TMEM: one CTA per SM).
 //
-// Roles (256 threads): warp 0 lane 0 issues TMA into an S-stage ring; warps
-// 4-7 split each stage (then run the epilogue from TMEM); warp 1 lane 0
-// issues the 12 MMAs of a stage and commits them to the stage's "empty"
-// barrier, which hands the stage back to TMA.
+// Roles (256 threads): warp 0 lane 0 issues the four TMA boxes of a stage
+// (A hi / lo, B hi / lo) into an S-stage ring; warp 1 lane 0 issues the 12
+// MMAs of a stage and commits them to the stage's "empty" barrier, which hands
+// the stage back to TMA; warps 4-7 run the epilogue from TMEM.
 //
 // Modes (im2col as box coordinates; conv 3x3, stride 1, pad 1):
 //   kPlain   A[M][K], B[N][K] row-major (self-test)
@@ -36,7 +37,13 @@
 //            shifted by the flipped tap; B = Wt2[c][tap * Dp + d];
 //            out NCHW gx (* [mask > 0], the relu of the layer below)
 //   kConvDw  per example z: A = input NCHW, m = (tap, c) (a box per tap),
-//            k = position; B = output cotangent NCHW (n = d);
+//            k = position; B = output cotangent NCHW (n = d). The K chunk is
+//            32 consecutive positions of the flattened H*W plane (one 128-B
+//            swizzle row for any W); a tap's row shift is a shift of W
+//            positions in that plane (OOB at the image border: zeros), its
+//            column shift comes from three pre-shifted copies of the input
+//            ([v][n][c][p] = x[n][c][p + v - 1] within the row), since TMA
+//            boxes start on 16-byte boundaries of the innermost dimension;
 //            out = the reference's per-example dW stack (B, D, C, 3, 3)
 //            (strategies.cpp:156-170) + each tile's squared sum (fp64)
 #pragma once
@@ -53,7 +60,8 @@ constexpr int kBM = 128, kBK = 32, kThreads = 256;
 enum Mode { kPlain = 0, kConvFwd = 1, kConvDx = 2, kConvDw = 3 };
 
 struct alignas(64) Params {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb;        // the hi tensors
+  CUtensorMap ta_lo, tb_lo;  // the lo tensors (same geometry)
   int mode;
   int M, N;          // GEMM rows / columns (valid extents)
   int nchunks;       // K chunks of 32
@@ -87,7 +95,7 @@ struct Smem {
   float a_lo[S][kBM * kBK];
   float b_hi[S][BN * kBK];
   float b_lo[S][BN * kBK];
-  uint64_t full[S], split[S], empty[S];
+  uint64_t full[S], empty[S];
   uint64_t acc;
   uint32_t tmem;
   double sq[4];
@@ -115,11 +123,23 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, int c
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+}
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
                                        int c3, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
       :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                       int c3, int c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(dst), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -135,15 +155,10 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(h);
 }
 
-// in place: hi = rna(x); returns lo = rna(x - hi), four at a time
-__device__ __forceinline__ float4 split4(float4& v) {
-  float4 lo;
-  float h;
-  h = rna_tf32(v.x); lo.x = rna_tf32(v.x - h); v.x = h;
-  h = rna_tf32(v.y); lo.y = rna_tf32(v.y - h); v.y = h;
-  h = rna_tf32(v.z); lo.z = rna_tf32(v.z - h); v.z = h;
-  h = rna_tf32(v.w); lo.w = rna_tf32(v.w - h); v.w = h;
-  return lo;
+// the 3xTF32 pair of one value: hi = rna(x), lo = rna(x - hi)
+__device__ __forceinline__ void split2(float x, float& hi, float& lo) {
+  hi = rna_tf32(x);
+  lo = rna_tf32(x - hi);
 }
 
 // Bytes TMA delivers per stage for operand A of M tile mt (full boxes, OOB
@@ -155,16 +170,16 @@ __device__ __forceinline__ uint32_t a_bytes(const Params& p, int mt) {
   return kBM * kBK * 4;
 }
 
-// Issue the TMA boxes of K chunk q of tile (mt, nt) for example z.
-template <int BN>
-__device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s, int q, int mt,
-                                            int nt, int z) {
-  const uint32_t bar = smem_u32(&S.full[s]);
-  const uint32_t da = smem_u32(S.a_hi[s]), db = smem_u32(S.b_hi[s]);
+// Issue the TMA boxes of K chunk q of tile (mt, nt) for example z: operand
+// A from (ma, into da) and B from (mb, into db) -- once for the hi tensors,
+// once for the lo tensors.
+__device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* ma,
+                                            const CUtensorMap* mb, uint32_t da, uint32_t db,
+                                            int BN, int q, int mt, int nt, int z, uint32_t bar) {
   switch (p.mode) {
     case kPlain:
-      tma_2d(da, &p.ta, q * kBK, mt * kBM, bar);
-      tma_2d(db, &p.tb, q * kBK, nt * BN, bar);
+      tma_2d(da, ma, q * kBK, mt * kBM, bar);
+      tma_2d(db, mb, q * kBK, nt * BN, bar);
       break;
     case kConvFwd:
     case kConvDx: {
@@ -175,28 +190,37 @@ __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s,
       // forward: x + v - 1, y + u - 1; input gradient: the flipped tap
       const int dx = p.mode == kConvFwd ? v - 1 : 1 - v;
       const int dy = p.mode == kConvFwd ? u - 1 : 1 - u;
-      tma_4d(da, &p.ta, cg * kBK, dx, y0 + dy, n0, bar);
-      tma_2d(db, &p.tb, tap * p.Cg * kBK + cg * kBK, nt * BN, bar);
+      tma_4d(da, ma, cg * kBK, dx, y0 + dy, n0, bar);
+      tma_2d(db, mb, tap * p.Cg * kBK + cg * kBK, nt * BN, bar);
       break;
     }
     case kConvDw: {
-      const int y0 = q * p.dw_by;
+      const int p0 = q * kBK;  // first position of the chunk (flattened H*W)
       if (p.big_c) {
         const int cgs = p.C / kBM, tap = mt / cgs, c0 = (mt - tap * cgs) * kBM;
         const int u = tap / 3, v = tap - 3 * u;
-        tma_4d(da, &p.ta, v - 1, y0 + u - 1, c0, z, bar);
+        tma_4d(da, ma, p0 + (u - 1) * p.W, c0, z, v, bar);
       } else {
         for (int sl = 0; sl < p.T; ++sl) {
           const int tap = mt * p.T + sl;
           if (tap >= 9) break;
           const int u = tap / 3, v = tap - 3 * u;
-          tma_4d(da + sl * p.Cr * kBK * 4, &p.ta, v - 1, y0 + u - 1, 0, z, bar);
+          tma_4d(da + sl * p.Cr * kBK * 4, ma, p0 + (u - 1) * p.W, 0, z, v, bar);
         }
       }
-      tma_4d(db, &p.tb, 0, y0, nt * BN, z, bar);
+      tma_3d(db, mb, p0, nt * BN, z, bar);
       break;
     }
   }
+}
+
+template <int BN>
+__device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s, int q, int mt,
+                                            int nt, int z) {
+  const uint32_t bar = smem_u32(&S.full[s]);
+  issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b_hi[s]), BN, q, mt, nt, z, bar);
+  issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b_lo[s]), BN, q, mt, nt, z,
+              bar);
 }
 
 template <int BN>
@@ -216,13 +240,14 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
   if (t == 0) {
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&S.full[s], 1);
-      tc::mbar_init(&S.split[s], 4);
       tc::mbar_init(&S.empty[s], 1);
     }
     tc::mbar_init(&S.acc, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta) : "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta_lo) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb_lo) : "memory");
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -232,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
   if (warp == 0) {
     // ---- TMA producer ----
     if (lane == 0) {
-      const uint32_t bytes = a_bytes(p, mt) + BN * kBK * 4;
+      const uint32_t bytes = 2 * (a_bytes(p, mt) + BN * kBK * 4);
       for (int q = 0; q < nq; ++q) {
         const int s = q % NS;
         if (q >= NS) tc::mbar_wait(&S.empty[s], ((q / NS) - 1) & 1);
@@ -246,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
       constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN < 16 ? 16 : BN);
       for (int q = 0; q < nq; ++q) {
         const int s = q % NS;
-        tc::mbar_wait(&S.split[s], (q / NS) & 1);
+        tc::mbar_wait(&S.full[s], (q / NS) & 1);
         tc::fence_after_sync();
         const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
         const uint32_t bh = smem_u32(S.b_hi[s]), bl = smem_u32(S.b_lo[s]);
@@ -265,31 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
       tc::commit(&S.acc);
     }
   } else if (warp >= 4) {
-    // ---- hi/lo split of each stage (warps 4-7) ----
-    const int ts = t - 128;
-    const uint32_t abytes = a_bytes(p, mt);
-    for (int q = 0; q < nq; ++q) {
-      const int s = q % NS;
-      tc::mbar_wait(&S.full[s], (q / NS) & 1);
-      float4* ah = reinterpret_cast<float4*>(S.a_hi[s]);
-      float4* al = reinterpret_cast<float4*>(S.a_lo[s]);
-      for (int i = ts; i < (int)(abytes / 16); i += 128) {
-        float4 v = ah[i];
-        al[i] = split4(v);
-        ah[i] = v;
-      }
-      float4* bh = reinterpret_cast<float4*>(S.b_hi[s]);
-      float4* bl = reinterpret_cast<float4*>(S.b_lo[s]);
-#pragma unroll
-      for (int i = ts; i < BN * kBK / 4; i += 128) {
-        float4 v = bh[i];
-        bl[i] = split4(v);
-        bh[i] = v;
-      }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.split[s]);
-    }
     // ---- epilogue: TMEM -> registers -> global ----
     tc::mbar_wait(&S.acc, 0);
     tc::fence_after_sync();
@@ -398,10 +398,11 @@ inline size_t smem_bytes() {
 namespace pgb {
 namespace tg {
 
-// NCHW (B, C, HW) -> NHWC (B, HW, Cp), channels zero-padded to Cp (32 x 32
-// tiles through shared memory: coalesced on both sides)
-__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst, int C,
-                                    int HW, int Cp) {
+// NCHW (B, C, HW) -> NHWC (B, HW, Cp) as the 3xTF32 pair (hi, lo), channels
+// zero-padded to Cp (32 x 32 tiles through shared memory: coalesced on both
+// sides)
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                    float* __restrict__ dst_lo, int C, int HW, int Cp) {
   __shared__ float tile[32][33];
   const int n = blockIdx.z, p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -411,27 +412,53 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __rest
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += 8) {
     const int p = p0 + j, c = c0 + threadIdx.x;
-    if (p < HW) dst[((size_t)n * HW + p) * Cp + c] = tile[threadIdx.x][j];
+    if (p < HW) {
+      float hi, lo;
+      split2(tile[threadIdx.x][j], hi, lo);
+      dst[((size_t)n * HW + p) * Cp + c] = hi;
+      dst_lo[((size_t)n * HW + p) * Cp + c] = lo;
+    }
+  }
+}
+
+// the 3xTF32 pair of a tensor, element-wise
+__global__ void split_kernel(const float* __restrict__ src, float* __restrict__ hi,
+                             float* __restrict__ lo, long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    split2(src[e], hi[e], lo[e]);
+}
+
+// dst[v][i] = src[i + v - 1] within the row (x + v - 1 in [0, W)), else 0:
+// the three column-shifted copies the per-example dW boxes read
+__global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                              float* __restrict__ dst_lo, long long total, int W) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 3 * total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(e / total);
+    const long long i = e - v * total;
+    const int x = (int)(i % W), xs = x + v - 1;
+    split2((xs >= 0 && xs < W) ? src[i + v - 1] : 0.0f, dst[e], dst_lo[e]);
   }
 }
 
 // conv weights (D, C, 3, 3) -> the forward B operand Wt[d][tap * Cp + c]
-__global__ void conv_wt_fwd_kernel(const float* __restrict__ W, float* __restrict__ wt, int D,
-                                   int C, int Cp) {
+__global__ void conv_wt_fwd_kernel(const float* __restrict__ W, float* __restrict__ wt,
+                                   float* __restrict__ wt_lo, int D, int C, int Cp) {
   const int n = D * 9 * Cp;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int d = e / (9 * Cp), r = e - d * 9 * Cp, tap = r / Cp, c = r - tap * Cp;
-    wt[e] = c < C ? W[((size_t)d * C + c) * 9 + tap] : 0.0f;
+    split2(c < C ? W[((size_t)d * C + c) * 9 + tap] : 0.0f, wt[e], wt_lo[e]);
   }
 }
 
 // conv weights (D, C, 3, 3) -> the input-gradient B operand Wt2[c][tap * Dp + d]
-__global__ void conv_wt_dx_kernel(const float* __restrict__ W, float* __restrict__ wt, int D,
-                                  int C, int Dp) {
+__global__ void conv_wt_dx_kernel(const float* __restrict__ W, float* __restrict__ wt,
+                                  float* __restrict__ wt_lo, int D, int C, int Dp) {
   const int n = C * 9 * Dp;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int c = e / (9 * Dp), r = e - c * 9 * Dp, tap = r / Dp, d = r - tap * Dp;
-    wt[e] = d < D ? W[((size_t)d * C + c) * 9 + tap] : 0.0f;
+    split2(d < D ? W[((size_t)d * C + c) * 9 + tap] : 0.0f, wt[e], wt_lo[e]);
   }
 }
 

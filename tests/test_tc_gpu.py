@@ -60,3 +60,34 @@ def test_tma_gemm_3xtf32(P, M, N, K):
     want = A.astype(np.float64) @ B.astype(np.float64).T
     err = np.linalg.norm(Cm - want) / np.linalg.norm(want)
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("C,H,W,D", [(3, 32, 32, 10), (32, 32, 32, 16), (32, 16, 16, 64),
+                                     (64, 8, 8, 10), (128, 8, 8, 32), (128, 4, 4, 256),
+                                     (256, 4, 4, 10)])
+def test_tma_conv_gemms_match_oracle(P, O, monkeypatch, C, H, W, D):
+    """Every 3x3 conv GEMM on the TMA engine (PGB_TMA_ALL=1: forward,
+    per-example dW and input gradient, whatever the per-kind default picks):
+    a conv -> relu -> conv -> relu -> global-avgpool model over the geometries
+    of the CIFAR CNN, per-example gradients and norms against the oracle."""
+    monkeypatch.setenv("PGB_TMA_ALL", "1")
+    layers = [P.LayerSpec(P.LayerKind.conv, C, D, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
+              P.LayerSpec(P.LayerKind.conv, D, 10, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
+              P.LayerSpec(P.LayerKind.global_avgpool)]
+    desc = P.custom_desc(P.ModelKind.cifar_cnn, layers, (C, H, W), 10)
+    od = O.custom_desc(O.CIFAR_CNN, [(1, C, D, 3, 1, 1), (6, 0, 0, 0, 1, 0), (1, D, 10, 3, 1, 1),
+                                     (6, 0, 0, 0, 1, 0), (4, 0, 0, 0, 1, 0)], (C, H, W), 10)
+    B = 3
+    model = P.build_from_desc(desc, 0)
+    data = P.synth_for_model(desc, B, 0)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    st, nr = eng.per_example_flat(data.inputs, data.labels)
+    ws, wnsq, _ = O.per_example_grads(od, data.inputs.astype(np.float64),
+                                      data.labels.astype(np.float64), O.init_params(od, 0))
+    off = 0
+    for n in od.blocks:
+        g, w = st[off:off + B * n], ws[off:off + B * n]
+        assert np.linalg.norm(g - w) <= 1e-5 * np.linalg.norm(w), (off, n)
+        off += B * n
+    wn = np.sqrt(wnsq)
+    assert np.max(np.abs(nr - wn) / wn) < 1e-5

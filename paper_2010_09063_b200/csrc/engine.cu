@@ -656,7 +656,8 @@ struct Engine {
         want((void**)&d_emb_tok, sizeof(int) * B * Lq);
         want((void**)&d_emb_cnt, sizeof(int) * B * Lq);
         want((void**)&d_emb_nd, sizeof(int) * B);
-        want((void**)&d_emb_bits, sizeof(unsigned) * L.spec.in * emb_words);
+        // (two bitmaps: the rows each example holds, and those it holds twice or more)
+        want((void**)&d_emb_bits, sizeof(unsigned) * 2 * L.spec.in * emb_words);
         // the dense head after the pool through mlp_kernel (dense / relu only,
         // within its widths; the embedding first)
         bool ok = l == 0 && std::getenv("PGB_NO_EMB_HEAD") == nullptr &&
@@ -994,7 +995,7 @@ struct Engine {
           break;
         case PGB_EMBEDDING: {
           const int E = (int)sp.out;
-          embed_pool_fwd_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
+          embed_pool_fwd_kernel<<<Bi, std::min(1024, kPoolGroups * ((E + 31) / 32) * 32), 0, s>>>(
               in, W, L.act_out, Bi, (int)L.in.d[0], E, (int)sp.in, d_err);
           nk += mark(s, "embed_pool_fwd");
           break;
@@ -1156,7 +1157,7 @@ struct Engine {
     const Layer& Le = layers[emb_layer];
     const int E = (int)Le.spec.out, V = (int)Le.spec.in, Bi = (int)B;
     const float* Wt = d_params + param_off[Le.pblock];
-    embed_pool_fwd_kernel<<<Bi, std::min(256, ((E + 31) / 32) * 32), 0, s>>>(
+    embed_pool_fwd_kernel<<<Bi, std::min(1024, kPoolGroups * ((E + 31) / 32) * 32), 0, s>>>(
         x_slot, Wt, Le.act_out, Bi, (int)Le.in.d[0], E, V, d_err);
     nk += mark(s, "embed_pool_fwd");
     nk += enqueue_mlp(s, x_slot, y_slot, true);

@@ -423,6 +423,8 @@ __global__ void mask_kernel(const float* __restrict__ g, const float* __restrict
 // embedding gather fused with the sequence mean-pool (models.cpp:241-262):
 // y[b,e] = (sum_t table[id_bt, e]) * 1/L. Ids validated (checked_id).
 constexpr int kPoolMaxL = 2048;
+constexpr int kPoolGroups = 4;   // token groups per example (partial sums)
+constexpr int kPoolMaxE = 1024;  // widths whose partial sums are staged in shared memory
 
 __global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
                                       const float* __restrict__ table, float* __restrict__ y,
@@ -443,9 +445,13 @@ __global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
     }
     return;
   }
-  // the example's ids once (validated), then 8 row gathers in flight per
-  // thread, added in token order
+  // the example's ids once (validated); then the threads split into G groups
+  // of ew (>= E) lanes, group g summing tokens [g L / G, (g + 1) L / G) in
+  // order with 16 row gathers in flight, the G partial sums added in group
+  // order (fp32 re-association of the reference's single chain,
+  // models.cpp:241-262: within the parity tolerance)
   __shared__ int sid[kPoolMaxL];
+  __shared__ float part[kPoolGroups][kPoolMaxE];
   for (int t = threadIdx.x; t < L; t += blockDim.x) {
     const float raw = ids[(size_t)b * L + t];
     const bool ok = valid_id(raw, V);
@@ -453,23 +459,36 @@ __global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
     sid[t] = ok ? (int)raw : -1;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  const int ew = ((E + 31) / 32) * 32;
+  const int G = E <= kPoolMaxE ? max(1, min(kPoolGroups, (int)blockDim.x / ew)) : 1;
+  const int g = threadIdx.x / ew, e = threadIdx.x - g * ew;
+  if (g < G && e < E) {
+    const int t0 = (int)((long long)L * g / G), t1 = (int)((long long)L * (g + 1) / G);
     float s = 0.0f;
-    int t = 0;
-    for (; t + 8 <= L; t += 8) {
-      float v[8];
+    int t = t0;
+    for (; t + 16 <= t1; t += 16) {
+      float v[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < 16; ++q) {
         const int r = sid[t + q];
         v[q] = r >= 0 ? __ldg(table + (size_t)r * E + e) : 0.0f;
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < 16; ++q)
         if (sid[t + q] >= 0) s += v[q];
     }
-    for (; t < L; ++t)
+    for (; t < t1; ++t)
       if (sid[t] >= 0) s += __ldg(table + (size_t)sid[t] * E + e);
-    y[(size_t)b * E + e] = s * (1.0f / float(L));
+    if (G > 1) part[g][e] = s;
+    else y[(size_t)b * E + e] = s * (1.0f / float(L));
+  }
+  if (G > 1) {
+    __syncthreads();
+    for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
+      float s = part[0][e2];
+      for (int q = 1; q < G; ++q) s += part[q][e2];
+      y[(size_t)b * E + e2] = s * (1.0f / float(L));
+    }
   }
 }
 
@@ -1206,7 +1225,11 @@ __global__ void __launch_bounds__(256) embed_index_kernel(
     const int r = key[seg[k]];
     tok[(size_t)i * L + k] = r;
     cnt[(size_t)i * L + k] = seg[k + 1] - seg[k];
+    const int c = seg[k + 1] - seg[k];
     atomicOr(&bits[(size_t)r * words + (i >> 5)], 1u << (i & 31));
+    // the second bitmap (bits + V * words) marks the rows this example holds
+    // more than once: only those look their count up in the aggregation
+    if (c > 1) atomicOr(&bits[((size_t)V + r) * words + (i >> 5)], 1u << (i & 31));
   }
   // ||G_i||^2 = sum over distinct tokens and e of chain(u_ie / L, c)^2 (the
   // pooled cotangent row staged in shared memory once)
@@ -1274,9 +1297,10 @@ struct EmbAggLaunch {
   int p, B, L, E, V, words, nparts, mode;
 };
 
-__global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
+__global__ void __launch_bounds__(256, 4) embed_agg_kernel(const EmbAggLaunch A) {
   extern __shared__ float s_emb[];  // clip factors (B)
   __shared__ unsigned wsh[8][32];   // the current row's bitmap words, per warp
+  __shared__ unsigned msh[8][32];   // ... and its multi-occurrence words
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   for (int i = t; i < A.B; i += blockDim.x) {
     const float nrm = A.norms[i];
@@ -1294,8 +1318,11 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
   __shared__ float lst_s[8][32];
   for (int r = blockIdx.x * 8 + w; r < A.V; r += gridDim.x * 8) {
     const unsigned word = lane < A.words ? A.bits[(size_t)r * A.words + lane] : 0u;
+    const unsigned mword =
+        lane < A.words ? A.bits[((size_t)A.V + r) * A.words + lane] : 0u;
     const unsigned active = __ballot_sync(0xffffffffu, word != 0u);
     wsh[w][lane] = word;
+    msh[w][lane] = mword;
     __syncwarp();
     // this lane's element pairs of the row: jb + lane + 32 q, in blocks of 64
     // pairs (one block for E <= 126)
@@ -1318,14 +1345,19 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
     auto flush = [&]() {
       if (lane < fill) {
         const int i = lst_i[w][lane];
-        const int* tk = A.tok + (size_t)i * A.L;
-        int lo = 0, hi = A.nd[i] - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (tk[mid] < r) lo = mid + 1;
-          else hi = mid;
+        int c = 1;  // the common case: the token once in the example
+        if ((msh[w][i >> 5] >> (i & 31)) & 1u) {
+          // its count: binary search of the example's distinct tokens
+          const int* tk = A.tok + (size_t)i * A.L;
+          int lo = 0, hi = A.nd[i] - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (tk[mid] < r) lo = mid + 1;
+            else hi = mid;
+          }
+          c = A.cnt[(size_t)i * A.L + lo];
         }
-        lst_c[w][lane] = A.cnt[(size_t)i * A.L + lo];
+        lst_c[w][lane] = c;
         lst_s[w][lane] = s_emb[i];
       }
       __syncwarp();
@@ -1405,6 +1437,7 @@ __global__ void __launch_bounds__(256) embed_agg_kernel(const EmbAggLaunch A) {
     }
     }  // pair blocks
     if (lane < A.words && word) A.bits[(size_t)r * A.words + lane] = 0u;
+    if (lane < A.words && mword) A.bits[((size_t)A.V + r) * A.words + lane] = 0u;
     __syncwarp();
   }
 }

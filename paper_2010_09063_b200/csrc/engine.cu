@@ -1061,6 +1061,7 @@ struct Engine {
       AggLaunch L{};
       if (fuse_agg_next) {
         L = agg_launch(bt, nparts, (int)B, 0, true);
+        agg_plan(L.bt, L.plan, kAggRows);  // the in-kernel tiles (agg_tile_run<.., kAggRows>)
         prm.grid_ctr = d_grid_ctr;
         prm.agg_tiles = L.plan.tile_start[L.plan.n];
       }
@@ -1341,8 +1342,9 @@ struct Engine {
   // Tile plan of the aggregation kernel for a block table: materialised
   // blocks in kAggCols-column tiles, factored dense blocks in kAggRows x 32
   // tiles. Returns the CTA count.
-  static int agg_plan(const BlockTable& t, AggPlan& plan) {
+  static int agg_plan(const BlockTable& t, AggPlan& plan, int rows1 = kAggRowsSep) {
     plan.n = t.n;
+    plan.rows1 = rows1;
     int tiles = 0;
     for (int p = 0; p < t.n; ++p) {
       plan.tile_start[p] = tiles;
@@ -1350,7 +1352,7 @@ struct Engine {
         tiles += (int)((t.size[p] + kAggCols - 1) / kAggCols);
       } else if (t.kind[p] == 1) {
         const int64_t out = t.out[p], in = t.size[p] / out;
-        tiles += (int)(((in + kAggRows - 1) / kAggRows) * ((out + 31) / 32));
+        tiles += (int)(((in + rows1 - 1) / rows1) * ((out + 31) / 32));
       }
     }
     plan.tile_start[t.n] = tiles;
@@ -1360,7 +1362,7 @@ struct Engine {
   // dynamic shared memory of the aggregation kernel: clip factors + the
   // per-warp staging of factored rows
   static size_t agg_smem(int U) {
-    return sizeof(float) * (((U + 3) & ~3) + kAggWarps * kAggChunk * kAggRows);
+    return sizeof(float) * (((U + 3) & ~3) + kAggWarps * kAggChunk * kAggRowsSep);
   }
 
   // from_fused: the fused MNIST kernel already produced this step's clip
@@ -1984,8 +1986,11 @@ namespace {
 // plus one graph of the remainder (every schedule whose inputs the graph can
 // read from the device ring by the step counter: fused MNIST and dense-only
 // models, one process or data-parallel, microbatch 1); C = 0: per-step graphs.
-int64_t resident_chunk(const Engine& en, const pgb_dp_config& cfg, int64_t n_batches) {
-  int64_t C = 8;
+int64_t resident_chunk(const Engine& en, const pgb_dp_config& cfg, int64_t n_batches,
+                       int64_t n_steps) {
+  // a run of up to 64 steps is one graph (one launch); longer runs replay
+  // graphs of 8 steps (measured: host issue under 0.2 us per step)
+  int64_t C = n_steps >= 2 && n_steps <= 64 ? n_steps : 8;
   if (const char* cs = std::getenv("PGB_CHUNK_STEPS")) C = std::max<int64_t>(1, std::atoll(cs));
   const bool ok = (en.fused_mnist || en.mlp_fused) && cfg.microbatch == 1 && en.graph_enabled &&
                   C > 1 && n_batches < (1 << 30);
@@ -2000,7 +2005,7 @@ pgb_status pgb_prepare_steps(pgb_engine* e, const float* d_x, const float* d_y,
     if (!cfg || !d_x || !d_y) raise(PGB_ERR_CONTRACT, "null argument");
     if (n_batches <= 0 || n_steps < 0) raise(PGB_ERR_CONFIG, "prepare_steps: bad counts");
     en.validate_step(*cfg);
-    const int64_t C = resident_chunk(en, *cfg, n_batches);
+    const int64_t C = resident_chunk(en, *cfg, n_batches, n_steps);
     if (C == 0) return;
     const StepArgs a0 = en.make_args(*cfg, 0, nullptr, nullptr);
     // captured, instantiated and uploaded to the device (the first launch
@@ -2028,7 +2033,7 @@ pgb_status pgb_run_steps_device(pgb_engine* e, const float* d_x, const float* d_
       const int64_t bi = ((s % n_batches) + n_batches) % n_batches;
       return std::make_pair(d_x + bi * en.B * en.in_row, d_y + bi * en.B);
     };
-    const int64_t C = resident_chunk(en, *cfg, n_batches);
+    const int64_t C = resident_chunk(en, *cfg, n_batches, n_steps);
     if (C > 0 && n_steps > 0) {
       // full chunks, then the remainder as one more static graph: the host
       // issues one counter write and ceil(n / C) graph launches

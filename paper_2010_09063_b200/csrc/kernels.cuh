@@ -789,7 +789,9 @@ __device__ __forceinline__ int find_block(const long long* pair_off, int n, long
 // clipped sum only (multi-GPU before the all-reduce, and the parity probe).
 constexpr int kAggWarps = 16;
 constexpr int kAggCols = 128;
-constexpr int kAggRows = 8;
+constexpr int kAggRows = 8;       // kind-1 rows per tile of the in-kernel aggregation
+constexpr int kAggRowsSep = 8;    // ... and of the separate aggregation kernel (16: fewer,
+                                  // taller tiles re-reading d_i less, measured 2.5% slower)
 constexpr int kAggBatch = 16; // units per load batch (materialised)
 constexpr int kAggChunk = 16; // units per load batch (factored)
 
@@ -799,6 +801,7 @@ constexpr int kAggChunk = 16; // units per load batch (factored)
 // CTA locates its tile without a memory round trip.
 struct AggPlan {
   int n;
+  int rows1;  // kind-1 weight rows per tile (kAggRows or kAggRowsSep)
   int tile_start[kMaxBlocks + 1];
 };
 
@@ -828,9 +831,9 @@ __device__ __forceinline__ AggTile agg_tile(const BlockTable& bt, const AggPlan&
   } else {
     const int out = bt.out[p], in = (int)(bt.size[p] / out);
     const int ctiles = (out + 31) / 32;
-    t.j0 = (q / ctiles) * kAggRows;
+    t.j0 = (q / ctiles) * plan.rows1;
     t.c0 = (q % ctiles) * 32;
-    t.n = min(kAggRows, in - t.j0);
+    t.n = min(plan.rows1, in - t.j0);
   }
   return t;
 }
@@ -914,9 +917,9 @@ __device__ __forceinline__ void agg_sync(int bar_id) {
 // One tile of the aggregation, run by 32 * kAggWarps threads (tid) that
 // synchronise with agg_sync(bar_id); s_sh holds the clip factors (U floats,
 // then the factored-row staging), part_sh the per-warp partial sums.
-template <bool kCoherent, int kBatch = kAggBatch>
+template <bool kCoherent, int kBatch = kAggBatch, int kRows = kAggRows>
 __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, int tid, int bar_id,
-                                             float* s_sh, float (*part_sh)[kAggRows * 32],
+                                             float* s_sh, float (*part_sh)[kRows * 32],
                                              int* cnt_sh) {
   const BlockTable& bt = L.bt;
   const StepArgs& a = L.a;
@@ -1027,7 +1030,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
 #pragma unroll
     for (int c = 0; c < 4; ++c) part_sh[warp][c0 + c] = acc[c];
   } else {
-    // ---- factored dense rows: kAggRows weight rows x 32 columns ----
+    // ---- factored dense rows: kRows weight rows x 32 columns ----
     // Per chunk of kAggChunk units the warp issues every load at once: d_ic
     // into registers (lane = c), the a_i[r0 .. r0+15] rows through a
     // per-warp shared staging area (read back as broadcasts).
@@ -1038,18 +1041,18 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     const float* A = abase + tile.j0;
     const float* D = rbase + (cok ? c : 0);
     const long long as = astride, ds = rstride;
-    float* a_st = s_sh + ((U + 3) & ~3) + warp * (kAggChunk * kAggRows);
-    float acc[kAggRows];
+    float* a_st = s_sh + ((U + 3) & ~3) + warp * (kAggChunk * kRows);
+    float acc[kRows];
 #pragma unroll
-    for (int r = 0; r < kAggRows; ++r) acc[r] = 0.0f;
-    float dv[kAggChunk], ar[kAggChunk * kAggRows / 32];
+    for (int r = 0; r < kRows; ++r) acc[r] = 0.0f;
+    float dv[kAggChunk], ar[kAggChunk * kRows / 32];
     auto load = [&](int ib) {
 #pragma unroll
       for (int u = 0; u < kAggChunk; ++u)
         dv[u] = (cok && ib + u < i1) ? agg_ld<kCoherent>(D + (long long)(ib + u) * ds) : 0.0f;
 #pragma unroll
-      for (int q = 0; q < kAggChunk * kAggRows / 32; ++q) {
-        const int e = q * 32 + lane, u = e / kAggRows, r = e % kAggRows;
+      for (int q = 0; q < kAggChunk * kRows / 32; ++q) {
+        const int e = q * 32 + lane, u = e / kRows, r = e % kRows;
         ar[q] = (ib + u < i1 && r < nr) ? agg_ld<kCoherent>(A + (long long)(ib + u) * as + r) : 0.0f;
       }
     };
@@ -1060,7 +1063,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
     for (int ib = i0; ib < i1; ib += kAggChunk) {
       if (ib != i0) load(ib);
 #pragma unroll
-      for (int q = 0; q < kAggChunk * kAggRows / 32; ++q) a_st[q * 32 + lane] = ar[q];
+      for (int q = 0; q < kAggChunk * kRows / 32; ++q) a_st[q * 32 + lane] = ar[q];
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < kAggChunk; ++u) {
@@ -1070,9 +1073,9 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
           // clipped sum is the issue-bound tail of the step, and the product
           // differs from it by at most one rounding, SURVEY 8(d) tolerance)
           const float ds = __fmul_rn(dv[u], s_sh[ib + u]);
-          const float4* a4 = reinterpret_cast<const float4*>(a_st + u * kAggRows);
+          const float4* a4 = reinterpret_cast<const float4*>(a_st + u * kRows);
 #pragma unroll
-          for (int q = 0; q < kAggRows / 4; ++q) {
+          for (int q = 0; q < kRows / 4; ++q) {
             const float4 x = a4[q];
             acc[4 * q] = __fmaf_rn(x.x, ds, acc[4 * q]);
             acc[4 * q + 1] = __fmaf_rn(x.y, ds, acc[4 * q + 1]);
@@ -1084,7 +1087,7 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
       __syncwarp();
     }
 #pragma unroll
-    for (int r = 0; r < kAggRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
+    for (int r = 0; r < kRows; ++r) part_sh[warp][r * 32 + lane] = acc[r];
   }
   agg_sync(bar_id);
   if (!kCoherent) PGB_MARK_T(PGB_TRACE_AGG + 8 * tile_id + 3, 0);
@@ -1123,14 +1126,15 @@ __device__ __forceinline__ void agg_tile_run(const AggLaunch& L, int tile_id, in
 
 __global__ void __launch_bounds__(32 * kAggWarps) aggregate_kernel(const AggLaunch L) {
   extern __shared__ float s_sh[];  // clip factors, one per unit
-  __shared__ float part_sh[kAggWarps][kAggRows * 32];
+  __shared__ float part_sh[kAggWarps][kAggRowsSep * 32];
   __shared__ int cnt_sh[kAggWarps];
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 0);
   // the next step's per-example kernel may start its input-only prologue
   asm volatile("griddepcontrol.launch_dependents;");
   // programmatic dependent launch: this grid may be resident before the
   // per-example kernel has finished; agg_tile_run waits for it
-  agg_tile_run<false>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh, cnt_sh);
+  agg_tile_run<false, kAggBatch, kAggRowsSep>(L, blockIdx.x, threadIdx.x, -1, s_sh, part_sh,
+                                              cnt_sh);
   PGB_MARK(PGB_TRACE_AGG + 8 * blockIdx.x + 4);
 }
 

@@ -128,6 +128,12 @@ pgb_status pgb_finish_desc(pgb_model_desc* desc);
 int64_t pgb_param_count(const pgb_model_desc* desc);
 pgb_status pgb_init_params(const pgb_model_desc* desc, uint64_t seed,
                            float* flat_out);
+/* The per-epoch example order of bench::train (harness.cpp:330-343): one
+ * Fisher-Yates pass with RngState(seed, 2^40 + epoch), j = (int64)(0 + (i + 1)
+ * * rng_next_unit) for i = n-1 .. 1, applied IN PLACE to `order` -- the
+ * reference initialises the order to 0..n-1 once and reshuffles it every
+ * epoch, so epoch e's order is the composition of passes 0..e. */
+pgb_status pgb_shuffle_order(uint64_t seed, int64_t epoch, int64_t n, int64_t* order);
 /* io::synth_for_model<float> (dataset.cpp:219-237), x (n, input_shape), y (n) */
 pgb_status pgb_synth(const pgb_model_desc* desc, int64_t n, uint64_t seed,
                      float* x_out, float* y_out);

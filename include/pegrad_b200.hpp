@@ -390,6 +390,81 @@ inline int64_t run_steps_device(GradEngine& engine, const float* d_x, const floa
                              &launches));
   return launches;
 }
+// bench::train (harness.cpp:319-382): seeded per-epoch shuffle
+// (pgb_shuffle_order), DPSGD (or SGD) steps, the mean evaluation loss over the
+// first min(N, 1024) examples per epoch, the final accuracy over the whole set
+// (first maximum; K = 1: logit > 0).
+struct TrainResult {
+  std::vector<double> epoch_mean_loss;
+  double final_train_accuracy = 0;
+  int64_t steps = 0;
+};
+
+inline TrainResult train(models::Model& model, const io::Dataset& data, Strategy strategy,
+                         ExecMode mode, const DpConfig<float>& cfg, int64_t batch,
+                         int64_t epochs, bool private_training) {
+  if (batch <= 0 || batch > data.count) throw ConfigError("train: bad batch size");
+  GradEngine engine(model, strategy, batch, mode);
+  TrainResult res;
+  const int64_t steps = data.count / batch, row = model.desc.input_numel();
+  const int64_t K = model.desc.c.classes;
+  std::vector<int64_t> order((size_t)data.count);
+  for (int64_t i = 0; i < data.count; ++i) order[(size_t)i] = i;  // reshuffled every epoch
+  std::vector<float> x((size_t)(batch * row)), y((size_t)batch);
+  // forward-only losses / logits of examples [0, n) in engine-batch chunks
+  auto evaluate = [&](int64_t n, std::vector<float>& losses, std::vector<float>& logits) {
+    losses.assign((size_t)n, 0.0f);
+    logits.assign((size_t)(n * K), 0.0f);
+    std::vector<float> lo((size_t)batch), lg((size_t)(batch * K));
+    engine.bind(model);
+    for (int64_t s0 = 0; s0 < n; s0 += batch) {
+      const int64_t cnt = std::min(batch, n - s0);
+      for (int64_t i = 0; i < batch; ++i) {  // the tail chunk repeats its last example
+        const int64_t src = s0 + std::min(i, cnt - 1);
+        std::copy(data.inputs.begin() + src * row, data.inputs.begin() + (src + 1) * row,
+                  x.begin() + i * row);
+        y[(size_t)i] = data.labels[(size_t)src];
+      }
+      check(pgb_forward(engine.handle(), x.data(), y.data(), lo.data(), lg.data()));
+      std::copy(lo.begin(), lo.begin() + cnt, losses.begin() + s0);
+      std::copy(lg.begin(), lg.begin() + cnt * K, logits.begin() + s0 * K);
+    }
+  };
+  std::vector<float> losses, logits;
+  const int64_t eval_n = std::min<int64_t>(data.count, 1024);
+  for (int64_t epoch = 0; epoch < epochs; ++epoch) {
+    check(pgb_shuffle_order(cfg.seed, epoch, data.count, order.data()));
+    for (int64_t s = 0; s < steps; ++s) {
+      for (int64_t i = 0; i < batch; ++i) {
+        const int64_t src = order[(size_t)(s * batch + i)];
+        std::copy(data.inputs.begin() + src * row, data.inputs.begin() + (src + 1) * row,
+                  x.begin() + i * row);
+        y[(size_t)i] = data.labels[(size_t)src];
+      }
+      if (private_training) dpsgd_step(model, engine, x, y, cfg, epoch * steps + s);
+      else sgd_step(model, engine, x, y, cfg.learning_rate);
+      ++res.steps;
+    }
+    evaluate(eval_n, losses, logits);
+    double tot = 0;
+    for (float l : losses) tot += l;
+    res.epoch_mean_loss.push_back(tot / (double)eval_n);
+  }
+  evaluate(data.count, losses, logits);
+  int64_t correct = 0;
+  for (int64_t i = 0; i < data.count; ++i) {
+    int64_t pred = 0;
+    if (K == 1) {
+      pred = logits[(size_t)i] > 0.0f ? 1 : 0;
+    } else {
+      for (int64_t k = 1; k < K; ++k)
+        if (logits[(size_t)(i * K + k)] > logits[(size_t)(i * K + pred)]) pred = k;
+    }
+    correct += pred == (int64_t)data.labels[(size_t)i];
+  }
+  res.final_train_accuracy = (double)correct / (double)data.count;
+  return res;
+}
 }  // namespace bench
 
 }  // namespace pegrad_b200

@@ -273,12 +273,40 @@ def ref():
         L.ref_run_bench_f32.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_double, C.c_double, C.c_double, C.c_uint64,
                                         _P(C.c_double)]
+        L.ref_train_f32.argtypes = [C.c_void_p, f32p, f32p, f32p, C.c_int64, C.c_int,
+                                    C.c_double, C.c_double, C.c_double, C.c_int64, C.c_uint64,
+                                    C.c_int64, C.c_int64, C.c_int, f64p, _P(C.c_double),
+                                    _P(C.c_int64)]
         L.ref_load_idx_f32.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _P(C.c_int64),
                                        _P(C.c_int), _P(C.c_int64)]
         L.ref_records_json_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_int64,
                                                  _P(C.c_int64)]
         _ref = L
     return _ref
+
+
+def ref_train(desc: Desc, params, x, y, strategy, clip, sigma, lr, microbatch, seed, batch,
+              epochs, private=True):
+    """bench::train<float> of the compiled reference (harness.cpp:319-382):
+    (final params, per-epoch mean evaluation losses, final accuracy, steps)."""
+    L = ref()
+    rows = desc.layer_rows()
+    l6 = (C.c_int64 * (6 * len(rows)))(*[v for r in rows for v in r])
+    ins = (C.c_int64 * desc.in_rank)(*desc.input_shape)
+    h = L.ref_desc_custom(desc.model_kind, len(rows), l6, desc.in_rank, ins, desc.classes,
+                          desc.token_input)
+    p = np.array(params, np.float32, copy=True)
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.ascontiguousarray(y, np.float32)
+    losses = np.zeros(max(1, epochs))
+    acc, steps = C.c_double(), C.c_int64()
+    try:
+        _chk(L.ref_train_f32(h, p, x, y, x.shape[0], strategy, clip, sigma, lr, microbatch,
+                             seed, batch, epochs, int(private), losses, C.byref(acc),
+                             C.byref(steps)), L, "ref_last_error")
+    finally:
+        L.ref_desc_free(h)
+    return p, losses[:epochs], acc.value, steps.value
 
 
 def ref_load_idx(path):

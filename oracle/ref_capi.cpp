@@ -319,6 +319,37 @@ int64_t ref_desc_block_size(void* d, int p) {
 REF_TYPED(float, f32)
 REF_TYPED(double, f64)
 
+// bench::train (harness.cpp:319-382) over caller data: the model starts at
+// `params` and ends in them; per-epoch mean evaluation losses, final accuracy.
+int ref_train_f32(void* dv, float* params, const float* x, const float* y, int64_t n,
+                  int strategy, double clip, double sigma, double lr, int64_t m,
+                  uint64_t seed, int64_t batch, int64_t epochs, int private_training,
+                  double* epoch_loss, double* accuracy, int64_t* steps) {
+  return guarded([&] {
+    const auto& d = *static_cast<models::ModelDesc*>(dv);
+    models::Model<float> model;
+    model.desc = d;
+    model.params = unflatten<float>(d, params);
+    io::Dataset<float> data;
+    const int64_t row = numel(d.input_shape);
+    data.inputs = Tensor<float>::from(batch_shape<float>(d, n), std::vector<float>(x, x + n * row));
+    data.labels = Tensor<float>::from({n}, std::vector<float>(y, y + n));
+    data.count = n;
+    DpConfig<float> cfg;
+    cfg.clip_norm = (float)clip;
+    cfg.noise_multiplier = (float)sigma;
+    cfg.learning_rate = (float)lr;
+    cfg.microbatch = m;
+    cfg.seed = seed;
+    auto r = bench::train(model, data, static_cast<Strategy>(strategy), ExecMode::graph, cfg,
+                          batch, epochs, private_training != 0);
+    for (size_t e = 0; e < r.epoch_mean_loss.size(); ++e) epoch_loss[e] = r.epoch_mean_loss[e];
+    *accuracy = r.final_train_accuracy;
+    *steps = r.steps;
+    flatten_into(model.params, params);
+  });
+}
+
 // bench::run_bench over synth_for_model data; returns the median epoch time.
 int ref_run_bench_f32(int kind, int strategy, int64_t B, int64_t N,
                       int64_t epochs, double clip, double sigma, double lr,

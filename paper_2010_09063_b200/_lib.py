@@ -110,6 +110,7 @@ EXPORTS = {
     "pgb_debug_umma_rate": (C.c_int, [C.c_int32] * 4 + [C.c_void_p, C.c_int32, C.c_void_p]),
     "pgb_run_steps_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.POINTER(DpConfigC), C.c_int64, C.POINTER(C.c_int64)]),
+    "pgb_shuffle_order": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]),
     "pgb_prepare_steps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                     C.POINTER(DpConfigC)]),
     "pgb_idx_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.c_void_p,

@@ -409,6 +409,20 @@ pgb_status pgb_synth(const pgb_model_desc* d, int64_t n, uint64_t seed, float* x
   });
 }
 
+// ---- bench::train's shuffle (proj/core/src/harness.cpp:337-343) ---------------
+pgb_status pgb_shuffle_order(uint64_t seed, int64_t epoch, int64_t n, int64_t* order) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !order)) raise(PGB_ERR_CONTRACT, "shuffle_order: bad arguments");
+    const uint64_t key = pgb::stream_key(seed, (uint64_t(1) << 40) + (uint64_t)epoch);
+    uint64_t ctr = 0;
+    for (int64_t i = n - 1; i > 0; --i) {
+      const double u = static_cast<double>(pgb::value_at(key, ctr++) >> 11) * 0x1.0p-53;
+      const int64_t j = static_cast<int64_t>(0.0 + (static_cast<double>(i + 1) - 0.0) * u);
+      std::swap(order[i], order[j]);
+    }
+  });
+}
+
 // ---- IDX containers (io::load_idx, proj/core/src/dataset.cpp:35-82) -----------
 pgb_status pgb_idx_info(const char* path, int32_t* rank, int64_t* dims, int64_t* count) {
   return guarded([&] {

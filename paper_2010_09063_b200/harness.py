@@ -207,10 +207,18 @@ class TrainResult:
     steps: int = 0
 
 
-def _shuffle(n: int, seed: int, epoch: int) -> np.ndarray:
-    """Fisher-Yates with RngState(seed, 2^40 + epoch) (harness.cpp:337-343)."""
-    from .models import _lib as _  # noqa: F401  (keeps import order explicit)
-    order = np.arange(n, dtype=np.int64)
+def _shuffle(order: np.ndarray, seed: int, epoch: int) -> np.ndarray:
+    """One Fisher-Yates pass with RngState(seed, 2^40 + epoch), in place
+    (harness.cpp:330-343: the order starts at 0..n-1 once and every epoch
+    reshuffles the previous one), by the library (pgb_shuffle_order)."""
+    assert order.dtype == np.int64 and order.flags.c_contiguous
+    check(lib.pgb_shuffle_order(seed, epoch, order.size, _lib.ptr(order)))
+    return order
+
+
+def _shuffle_py(order: np.ndarray, seed: int, epoch: int) -> np.ndarray:
+    """The same pass restated in Python (checks pgb_shuffle_order)."""
+    n = order.size
     key = _stream_key(seed, (1 << 40) + epoch)
     ctr = 0
     for i in range(n - 1, 0, -1):
@@ -248,8 +256,9 @@ def train(model: Model, data: Dataset, strategy: Strategy, mode: ExecMode, cfg: 
     res = TrainResult()
     steps = data.count // batch
     eval_n = min(data.count, 1024)
+    order = np.arange(data.count, dtype=np.int64)
     for epoch in range(epochs):
-        order = _shuffle(data.count, cfg.seed, epoch)
+        _shuffle(order, cfg.seed, epoch)
         for s in range(steps):
             idx = order[s * batch:(s + 1) * batch]
             x, y = data.inputs[idx], data.labels[idx]

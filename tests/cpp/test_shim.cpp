@@ -160,6 +160,23 @@ int main() {
   auto res = bench::run_epoch(model, engine, ep, cfg, 100);
   CHECK(res.seconds > 0 && res.clipped_total >= 0);
 
+  // bench::train (harness.cpp:319-382): steps, one mean loss per epoch,
+  // accuracy in [0, 1], deterministic for a fixed seed
+  {
+    auto t1 = models::build(ModelKind::fcnn, 2), t2 = models::build(ModelKind::fcnn, 2);
+    auto td = io::synth_for_model(t1.desc, 96, 6);
+    DpConfig<float> tc;
+    tc.clip_norm = 1.0f;
+    tc.noise_multiplier = 1.1f;
+    tc.seed = 9;
+    auto r1 = bench::train(t1, td, Strategy::vmap, ExecMode::graph, tc, 32, 2, true);
+    auto r2 = bench::train(t2, td, Strategy::vmap, ExecMode::graph, tc, 32, 2, true);
+    CHECK(r1.steps == 6 && r1.epoch_mean_loss.size() == 2);
+    CHECK(r1.final_train_accuracy >= 0.0 && r1.final_train_accuracy <= 1.0);
+    CHECK(r1.epoch_mean_loss == r2.epoch_mean_loss && t1.flat() == t2.flat());
+    CHECK(throws<ConfigError>([&] { bench::train(t1, td, Strategy::vmap, ExecMode::graph, tc, 0, 1, true); }));
+  }
+
   // IDX ingest (dataset.cpp:35-112): a small MNIST pair written here
   {
     const char* dir = std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp";

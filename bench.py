@@ -377,10 +377,8 @@ def run_ours(args):
     full = Pk.synth_for_model(desc, nbatches * GBATCH, SEED)
     row = int(np.prod(desc.input_shape))
     G = GBATCH // BATCH
-    r = rank % G
-    xs = full.inputs.reshape(nbatches, G, BATCH, row)[:, r].reshape(
-        (nbatches * BATCH,) + tuple(full.inputs.shape[1:]))
-    ys = full.labels.reshape(nbatches, G, BATCH)[:, r].reshape(nbatches * BATCH)
+    from paper_2010_09063_b200.dist import shard_batches
+    xs, ys = shard_batches(full.inputs, full.labels, nbatches, GBATCH, G, rank % G)
     data = Pk.Dataset(_pinned(xs), _pinned(ys), full.name, nbatches * BATCH, full.classes)
     del full
     dx = torch.from_numpy(data.inputs).to(f"cuda:{dev}")

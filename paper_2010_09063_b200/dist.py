@@ -30,6 +30,24 @@ def shard_bounds(rank: int, world: int, batch: int) -> Tuple[int, int]:
     return rank * per, (rank + 1) * per
 
 
+def shard_batches(x, y, n_batches: int, global_batch: int, world: int, rank: int):
+    """This rank's examples of every global batch of a dataset laid out as
+    n_batches consecutive global batches: batch b's rows
+    [b*G + lo, b*G + hi) with (lo, hi) = shard_bounds(rank, world, G),
+    concatenated -- the per-rank ring pgb_run_steps_device / pgb_run_epoch
+    walk (bench.py --gpus N)."""
+    import numpy as np
+    lo, hi = shard_bounds(rank, world, global_batch)
+    per = hi - lo
+    row = int(np.prod(x.shape[1:]))
+    xs = np.ascontiguousarray(
+        x[: n_batches * global_batch].reshape(n_batches, global_batch, row)[:, lo:hi]).reshape(
+            (n_batches * per,) + tuple(x.shape[1:]))
+    ys = np.ascontiguousarray(
+        y[: n_batches * global_batch].reshape(n_batches, global_batch)[:, lo:hi]).reshape(-1)
+    return xs, ys
+
+
 def nccl_unique_id() -> bytes:
     u = _lib.UniqueIdC()
     _lib.check(_lib.lib.pgb_nccl_unique_id(C.byref(u)))

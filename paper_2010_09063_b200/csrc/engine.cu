@@ -160,6 +160,7 @@ struct Engine {
   // (its 9 x C row tiles scatter stride-9 stores and pay a TMEM set-up per
   // example). PGB_TMA_ALL=1 takes every eligible GEMM (parity tests).
   bool tma_all = false;
+  bool emb_agg_scalar = false;  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
   bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
   bool tma_dx(const ConvGeom& g) const {
     return use_tma && tg::conv_ok(g) && (tma_all || (g.H * g.W <= 64 && g.D >= 32));
@@ -550,6 +551,7 @@ struct Engine {
     use_tc = std::getenv("PGB_NO_TC") == nullptr;
     use_tma = use_tc && std::getenv("PGB_NO_TMA") == nullptr;
     tma_all = std::getenv("PGB_TMA_ALL") != nullptr;
+    emb_agg_scalar = std::getenv("PGB_EMB_AGG_SCALAR") != nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -1441,10 +1443,19 @@ struct Engine {
       A.step_off = cap_step_off;
     }
     const int rows_per_cta = 8;
+    const int grid = std::min<int>((A.V + rows_per_cta - 1) / rows_per_cta, 148 * 8);
+    // four elements per lane when the table rows are 16-byte aligned and the
+    // block has no shadow copies (PGB_EMB_AGG_SCALAR=1: the scalar kernel);
+    // it takes the norms from the fp64 partials itself
+    const bool vec4 = A.E % 4 == 0 && t.param_off[A.p] % 4 == 0 && !t.shadow[A.p] &&
+                      !t.tcw[A.p] && B <= 1024 && !emb_agg_scalar;
+    if (vec4) {  // one wave: six 34-KB CTAs per SM
+      embed_agg4_kernel<<<std::min(grid, 148 * 6), 32 * kEmbAggWarps, sizeof(float) * B, s>>>(A);
+      return mark(s, mode == 0 ? "embed_agg" : "embed_agg_local");
+    }
     finalize_norms_kernel<<<((int)B + 127) / 128, 128, 0, s>>>(d_parts, np, (int)B, d_wts);
     const int nk0 = mark(s, "embed_norms");
     A.norms = d_wts;  // (the weighted-sum weights buffer, free on the step path)
-    const int grid = std::min<int>((A.V + rows_per_cta - 1) / rows_per_cta, 148 * 8);
     embed_agg_kernel<<<grid, 256, sizeof(float) * B, s>>>(A);
     return nk0 + mark(s, mode == 0 ? "embed_agg" : "embed_agg_local");
   }
@@ -1708,7 +1719,7 @@ struct Engine {
         // (an embedding head reads the pooled activation, not the step input)
         sg.mlp = nd;
         sg.mlp_args = *static_cast<const mlp::Params*>(kp.kernelParams[0]);
-      } else if (kp.func == (void*)embed_agg_kernel) {
+      } else if (kp.func == (void*)embed_agg_kernel || kp.func == (void*)embed_agg4_kernel) {
         sg.emb = nd;
         sg.emb_args = *static_cast<const EmbAggLaunch*>(kp.kernelParams[0]);
       } else if (kp.func == (void*)noise_update_kernel) {

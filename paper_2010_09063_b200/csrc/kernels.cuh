@@ -1446,6 +1446,131 @@ __global__ void __launch_bounds__(256, 4) embed_agg_kernel(const EmbAggLaunch A)
   }
 }
 
+// embed_agg_kernel with four consecutive elements per lane (E % 4 == 0, the
+// table 16-byte aligned, no shadow copies): the row's example list is built
+// in parallel (one bitmap word per lane, a warp scan for the offsets; the
+// count looked up by the lane that owns the example), then every example of
+// the row costs one 16-byte load of its pooled cotangent per lane. Same
+// arithmetic per element and the same ascending example order as
+// embed_agg_kernel, so the two are bitwise equal (tests/test_embed_gpu.py).
+constexpr int kEmbAggWarps = 8;
+__global__ void __launch_bounds__(32 * kEmbAggWarps) embed_agg4_kernel(const EmbAggLaunch A) {
+  extern __shared__ float s_emb[];                 // clip factors (B)
+  __shared__ int lst[kEmbAggWarps][1024];          // (count << 10) | example, ascending
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int i = t; i < A.B; i += blockDim.x) {
+    // the norm from the fp64 partials, as finalize_norms_kernel computes it
+    double acc = 0.0;
+    for (int q = 0; q < A.nparts; ++q) acc += A.parts[(size_t)i * A.nparts + q];
+    const float nrm = (float)sqrt(acc);
+    s_emb[i] = nrm > A.a.clip ? __fdiv_rn(A.a.clip, nrm) : 1.0f;
+  }
+  __syncthreads();
+  const StepArgs& a = A.a;
+  const float invL = 1.0f / float(A.L);
+  const bool failed = A.err && A.err->code != 0;
+  const uint64_t key =
+      stream_key(a.seed, noise_stream(A.step_base ? *A.step_base + A.step_off : a.step, A.p));
+  const int E = A.E;
+  const float scale = __fmul_rn(a.sigma, a.clip);
+  float* tab = A.params + A.bt.param_off[A.p];
+  float* sum_out = A.sum_out ? A.sum_out + A.bt.param_off[A.p] : nullptr;
+  int* L = lst[w];
+  for (int r = blockIdx.x * kEmbAggWarps + w; r < A.V; r += gridDim.x * kEmbAggWarps) {
+    const bool hasw = lane < A.words;
+    const unsigned word = hasw ? A.bits[(size_t)r * A.words + lane] : 0u;
+    const unsigned mword = hasw ? A.bits[((size_t)A.V + r) * A.words + lane] : 0u;
+    // this lane's examples go to list slots [off, off + popc(word))
+    const int cntw = __popc(word);
+    int off = cntw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, o);
+      if (lane >= o) off += v;
+    }
+    const int n = __shfl_sync(0xffffffffu, off, 31);
+    off -= cntw;
+    for (unsigned bw = word; bw; bw &= bw - 1) {
+      const int bb = __ffs(bw) - 1, i = lane * 32 + bb;
+      int c = 1;  // the common case: the token once in the example
+      if ((mword >> bb) & 1u) {
+        const int* tk = A.tok + (size_t)i * A.L;
+        int lo = 0, hi = A.nd[i] - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tk[mid] < r) lo = mid + 1;
+          else hi = mid;
+        }
+        c = A.cnt[(size_t)i * A.L + lo];
+      }
+      L[off++] = (c << 10) | i;
+    }
+    __syncwarp();
+    const long long j0 = (long long)r * E;
+    for (int eb = 0; eb < E; eb += 128) {  // warp-uniform trip count
+      const int e0 = eb + 4 * lane;
+      const bool ok = e0 < E;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int k0 = 0; k0 < n; k0 += 8) {
+        float4 uv[8];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const int k = min(k0 + d, n - 1);
+          const int i = L[k] & 1023;
+          uv[d] = ok ? __ldg(reinterpret_cast<const float4*>(A.u + (size_t)i * E + e0))
+                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          if (k0 + d >= n) break;
+          const int pk = L[k0 + d];
+          const int c = pk >> 10;
+          const float s = s_emb[pk & 1023];
+          float g[4] = {uv[d].x * invL, uv[d].y * invL, uv[d].z * invL, uv[d].w * invL};
+          if (c != 1) {  // warp-uniform: emb_chain once per example, not per element
+            float ch[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 1
+            for (int k = 0; k < c; ++k)
+#pragma unroll
+              for (int h = 0; h < 4; ++h) ch[h] = __fadd_rn(ch[h], g[h]);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) g[h] = ch[h];
+          }
+#pragma unroll
+          for (int h = 0; h < 4; ++h) acc[h] = __fadd_rn(acc[h], __fmul_rn(g[h], s));
+        }
+      }
+      if (ok) {
+        const long long j = j0 + e0;  // even: two whole normal pairs
+        if (A.mode == 1) {
+          *reinterpret_cast<float4*>(sum_out + j) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        } else {
+          float nz[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (a.add_noise) {
+            gauss_pair(key, j >> 1, &nz[0], &nz[1]);
+            gauss_pair(key, (j >> 1) + 1, &nz[2], &nz[3]);
+          }
+          if (!failed) {
+            float4 cur = *reinterpret_cast<const float4*>(tab + j);
+            float* cv = reinterpret_cast<float*>(&cur);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              float sm = acc[h];
+              if (a.add_noise) sm = __fadd_rn(sm, __fmul_rn(scale, nz[h]));
+              sm = __fmul_rn(sm, a.inv_units);
+              cv[h] = __fsub_rn(cv[h], __fmul_rn(a.lr, sm));
+            }
+            *reinterpret_cast<float4*>(tab + j) = cur;
+          }
+        }
+      }
+    }
+    if (hasw && word) A.bits[(size_t)r * A.words + lane] = 0u;
+    if (hasw && mword) A.bits[((size_t)A.V + r) * A.words + lane] = 0u;
+    __syncwarp();
+  }
+}
+
 // After the all-reduce of the clipped sums: noise (one shared draw from the
 // common seed, so every rank adds the same vector), mean over the global
 // units, update (dpsgd.cpp:308-317, apply_update :173-183). One thread per

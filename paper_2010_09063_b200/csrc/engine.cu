@@ -160,7 +160,8 @@ struct Engine {
   // (its 9 x C row tiles scatter stride-9 stores and pay a TMEM set-up per
   // example). PGB_TMA_ALL=1 takes every eligible GEMM (parity tests).
   bool tma_all = false;
-  bool emb_agg_scalar = false;  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
+  bool emb_agg_scalar = false;
+  bool pool_generic = false;    // PGB_POOL_GENERIC=1: the generic pooling kernels  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
   bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
   bool tma_dx(const ConvGeom& g) const {
     return use_tma && tg::conv_ok(g) && (tma_all || (g.H * g.W <= 64 && g.D >= 32));
@@ -363,6 +364,14 @@ struct Engine {
     if (ev_t1) cudaEventDestroy(ev_t1);
   }
 
+  // 2x2 / stride-2 pooling that tiles its input exactly (pool2_*_kernel)
+  bool pool2(const Layer& L) const {
+    const pgb_layer_spec& sp = L.spec;
+    return !pool_generic && sp.k == 2 && sp.stride == 2 && sp.pad == 0 &&
+           L.in.d[1] == 2 * L.out.d[1] && L.in.d[2] == 2 * L.out.d[2] &&
+           B * L.out.numel() < (1ll << 31);
+  }
+
   static ConvGeom conv_geom(const Layer& L) {
     const pgb_layer_spec& sp = L.spec;
     return ConvGeom{(int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2], (int)L.out.d[0],
@@ -552,6 +561,7 @@ struct Engine {
     use_tma = use_tc && std::getenv("PGB_NO_TMA") == nullptr;
     tma_all = std::getenv("PGB_TMA_ALL") != nullptr;
     emb_agg_scalar = std::getenv("PGB_EMB_AGG_SCALAR") != nullptr;
+    pool_generic = std::getenv("PGB_POOL_GENERIC") != nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -974,10 +984,15 @@ struct Engine {
         case PGB_MAXPOOL:
         case PGB_AVGPOOL: {
           const size_t tot = (size_t)B * L.out.numel();
-          pool_fwd_kernel<<<grid_for(tot), 256, 0, s>>>(
-              in, L.act_out, Bi * (int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2],
-              (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
-              sp.kind == PGB_MAXPOOL);
+          if (pool2(L))
+            pool2_fwd_kernel<<<grid_for(tot), 256, 0, s>>>(in, L.act_out, Bi * (int)L.in.d[0],
+                                                          (int)L.out.d[1], (int)L.out.d[2],
+                                                          sp.kind == PGB_MAXPOOL);
+          else
+            pool_fwd_kernel<<<grid_for(tot), 256, 0, s>>>(
+                in, L.act_out, Bi * (int)L.in.d[0], (int)L.in.d[1], (int)L.in.d[2],
+                (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
+                sp.kind == PGB_MAXPOOL);
           nk += mark(s, "pool_fwd");
           break;
         }
@@ -1255,10 +1270,15 @@ struct Engine {
         case PGB_MAXPOOL:
         case PGB_AVGPOOL: {
           const size_t tot = (size_t)B * L.in.numel();
-          pool_bwd_kernel<<<grid_for(tot), 256, 0, s>>>(
-              in, gcur, L.bwd_mask, gnext, Bi * (int)L.in.d[0], (int)L.in.d[1],
-              (int)L.in.d[2], (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
-              sp.kind == PGB_MAXPOOL);
+          if (pool2(L))
+            pool2_bwd_kernel<<<grid_for((size_t)B * L.out.numel()), 256, 0, s>>>(
+                in, gcur, L.bwd_mask, gnext, Bi * (int)L.in.d[0], (int)L.out.d[1],
+                (int)L.out.d[2], sp.kind == PGB_MAXPOOL);
+          else
+            pool_bwd_kernel<<<grid_for(tot), 256, 0, s>>>(
+                in, gcur, L.bwd_mask, gnext, Bi * (int)L.in.d[0], (int)L.in.d[1],
+                (int)L.in.d[2], (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride,
+                sp.kind == PGB_MAXPOOL);
           nk += mark(s, "pool_bwd");
           break;
         }

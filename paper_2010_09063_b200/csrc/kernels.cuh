@@ -384,6 +384,81 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
+// 2x2 windows with stride 2 tiling the input (H = 2 Ho, W = 2 Wo: every input
+// element in exactly one window) -- the CIFAR pools. One thread per window,
+// 8-byte row loads/stores; the same fp32 operations as pool_fwd_kernel /
+// pool_bwd_kernel (window order (0,0), (0,1), (1,0), (1,1); first max).
+__global__ void pool2_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int BC,
+                                 int Ho, int Wo, int is_max) {
+  const unsigned total = (unsigned)BC * Ho * Wo;
+  const int W = 2 * Wo;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += gridDim.x * blockDim.x) {
+    const unsigned ox = e % Wo, t = e / Wo, oy = t % Ho, bc = t / Ho;
+    const size_t base = ((size_t)bc * 2 * Ho + 2 * oy) * W + 2 * ox;
+    const float2 r0 = *reinterpret_cast<const float2*>(x + base);
+    const float2 r1 = *reinterpret_cast<const float2*>(x + base + W);
+    float out;
+    if (is_max) {
+      float m = r0.x;
+      if (r0.y > m) m = r0.y;
+      if (r1.x > m) m = r1.x;
+      if (r1.y > m) m = r1.y;
+      out = m;
+    } else {
+      float s = __fadd_rn(0.0f, r0.x);
+      s = __fadd_rn(s, r0.y);
+      s = __fadd_rn(s, r1.x);
+      s = __fadd_rn(s, r1.y);
+      out = __fmul_rn(s, 0.25f);
+    }
+    y[e] = out;
+  }
+}
+
+__global__ void pool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                 const float* __restrict__ mask, float* __restrict__ gx, int BC,
+                                 int Ho, int Wo, int is_max) {
+  const unsigned total = (unsigned)BC * Ho * Wo;
+  const int W = 2 * Wo;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += gridDim.x * blockDim.x) {
+    const unsigned ox = e % Wo, t = e / Wo, oy = t % Ho, bc = t / Ho;
+    const size_t base = ((size_t)bc * 2 * Ho + 2 * oy) * W + 2 * ox;
+    const float gv = g[e];
+    float o[4];
+    if (is_max) {
+      const float2 r0 = *reinterpret_cast<const float2*>(x + base);
+      const float2 r1 = *reinterpret_cast<const float2*>(x + base + W);
+      const float v[4] = {r0.x, r0.y, r1.x, r1.y};
+      int best = 0;
+      float bv = v[0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (v[q] > bv) {
+          bv = v[q];
+          best = q;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = q == best ? __fadd_rn(0.0f, gv) : 0.0f;
+    } else {
+      const float a = __fadd_rn(0.0f, __fmul_rn(gv, 0.25f));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = a;
+    }
+    if (mask) {
+      const float2 m0 = *reinterpret_cast<const float2*>(mask + base);
+      const float2 m1 = *reinterpret_cast<const float2*>(mask + base + W);
+      if (!(m0.x > 0.0f)) o[0] = 0.0f;
+      if (!(m0.y > 0.0f)) o[1] = 0.0f;
+      if (!(m1.x > 0.0f)) o[2] = 0.0f;
+      if (!(m1.y > 0.0f)) o[3] = 0.0f;
+    }
+    *reinterpret_cast<float2*>(gx + base) = make_float2(o[0], o[1]);
+    *reinterpret_cast<float2*>(gx + base + W) = make_float2(o[2], o[3]);
+  }
+}
+
 // global average pool (models.cpp:227-232): sum over H,W then * 1/(H*W)
 __global__ void gap_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int BC,
                                int HW) {

@@ -106,6 +106,11 @@ struct Layer {
   bool skip_bwd = false;        // handled by a neighbour in the backward pass
   bool needs_gx = false;        // input gradient needed upstream
   const float* bwd_mask = nullptr;  // relu output to gate gx with
+  // 3x3 conv on a 4x4 / 8x8 map: on the step path its weight block's
+  // per-example norm is a Gram (ghost) norm and its clipped sum one
+  // clip-scaled GEMM over the batch -- no per-example stack
+  bool ghost = false;
+  int ghost_splits = 0;         // example splits of the summed dW GEMM
 };
 
 struct Engine {
@@ -128,6 +133,10 @@ struct Engine {
   // bitmaps instead of the dense (B, V, E) stack (embed_index/agg kernels)
   int emb_layer = -1;          // the embedding layer, when the sparse path applies
   bool sparse_embed_next = false;
+  bool ghost_next = false;      // this step's conv blocks go through the ghost path
+  bool any_ghost = false;
+  bool ghost_enabled = true;    // PGB_NO_GHOST=1: per-example conv dW stacks throughout
+  float* d_dw_ws = nullptr;     // split workspace of the summed dW GEMMs
   int* d_emb_tok = nullptr;    // (B, L)
   int* d_emb_cnt = nullptr;    // (B, L)
   int* d_emb_nd = nullptr;     // (B)
@@ -278,6 +287,7 @@ struct Engine {
   float* d_units = nullptr;
   double* d_parts = nullptr;
   float* d_cot[2] = {nullptr, nullptr};
+  std::vector<float*> d_ghost_g;  // per layer: output cotangent of a ghost conv
   float* d_loss = nullptr;
   float* d_norms = nullptr;
   float* d_sum = nullptr;
@@ -318,6 +328,8 @@ struct Engine {
     EmbAggLaunch emb_args{};
     cudaGraphNode_t mlp = nullptr;  // the fused dense-model kernel (inputs per step)
     mlp::Params mlp_args{};
+    cudaGraphNode_t scales = nullptr;  // clip factors of a ghost-conv step
+    ScalesLaunch scales_args{};
   };
   // key: (schedule variant and input slot, exact microbatch): the graph bakes
   // m and U = B/m into its microbatch / sumsq / aggregation launches
@@ -562,6 +574,7 @@ struct Engine {
     tma_all = std::getenv("PGB_TMA_ALL") != nullptr;
     emb_agg_scalar = std::getenv("PGB_EMB_AGG_SCALAR") != nullptr;
     pool_generic = std::getenv("PGB_POOL_GENERIC") != nullptr;
+    ghost_enabled = std::getenv("PGB_NO_GHOST") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -691,6 +704,43 @@ struct Engine {
                    P - param_off[firstp] <= mlp::kMaxParams;
       }
     }
+    // ghost conv layers (4x4 / 8x8 maps on the TMA engine): dedicated output
+    // cotangents (kept until the clip factors are known) and the split
+    // workspace of their summed weight-gradient GEMMs
+    d_ghost_g.assign(n, nullptr);
+    any_ghost = false;
+    {
+      int64_t ws = 0;
+      for (int l = 0; l < n; ++l) {
+        Layer& L = layers[l];
+        L.ghost = false;
+        if (L.spec.kind != PGB_CONV || !ghost_enabled || !use_tc || !use_tma || fused_mnist)
+          continue;
+        const ConvGeom g = conv_geom(L);
+        const int hw = g.H * g.W;
+        if (!tg::conv_ok(g) || (hw != 16 && hw != 64)) continue;
+        // shared memory of the Gram kernel: x, g and the input Gram
+        if ((size_t)(g.C + g.D + hw) * hw * sizeof(float) > 160 * 1024) continue;
+        L.ghost = true;
+        any_ghost = true;
+        want((void**)&d_ghost_g[l], sizeof(float) * B * L.out.numel());
+        int Cr, T, big, mtiles;
+        tg::dw_tiling(g.C, Cr, T, big, mtiles);
+        const int bn = tg::pick_bn(g.D), ntiles = (g.D + bn - 1) / bn;
+        const int tiles = mtiles * ntiles;
+        // enough example splits to fill the SMs, at least 4 examples each
+        int splits = std::max(1, std::min<int>(148 / tiles, (int)(B / 4)));
+        L.ghost_splits = splits;
+        ws = std::max<int64_t>(ws, (int64_t)splits * mtiles * ntiles * bn * 128);
+      }
+      if (any_ghost) {
+        want((void**)&d_dw_ws, sizeof(float) * ws);
+        if (!fused_mnist) {
+          want((void**)&d_scale, sizeof(float) * B);
+          want((void**)&d_clipflag, sizeof(int) * B);
+        }
+      }
+    }
     d_dense_g.assign(n, nullptr);
     for (int l = 0; l < n; ++l)
       if (layers[l].spec.kind == PGB_DENSE)
@@ -742,6 +792,8 @@ struct Engine {
       if (L.skip_bwd) continue;
       if (L.spec.kind == PGB_DENSE) {
         L.gout = d_dense_g[l];
+      } else if (L.ghost) {
+        L.gout = d_ghost_g[l];
       } else {
         L.gout = d_cot[pp];
         pp ^= 1;
@@ -1224,7 +1276,22 @@ struct Engine {
           const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
           float* sW = d_stacks + param_off[L.pblock] * B;
           float* sb = d_stacks + param_off[L.pblock + 1] * B;
-          if (tma_dw(gg)) {
+          if (ghost_next && L.ghost) {
+            // the block's per-example norm only (ghost Gram norm); its
+            // clipped sum comes later from enqueue_ghost_sums
+            const int hw = gg.H * gg.W;
+            const size_t sm = sizeof(float) * (size_t)(gg.C + gg.D + hw) * hw;
+            if (hw == 64) {
+              gram_attr(conv_gram_norm_kernel<64>, sm);
+              conv_gram_norm_kernel<64><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
+                                                           nparts, L.pblock);
+            } else {
+              gram_attr(conv_gram_norm_kernel<16>, sm);
+              conv_gram_norm_kernel<16><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
+                                                           nparts, L.pblock);
+            }
+            nk += mark(s, "conv_dw_gram");
+          } else if (tma_dw(gg)) {
             const int tiles = tma_conv_dw(s, gg, Bi, in, gcur, sW, d_tile_sq);
             nk += mark(s, "conv_dw_pex_tma") + 2;
             tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(d_tile_sq, tiles, Bi, d_parts,
@@ -1325,10 +1392,11 @@ struct Engine {
     fuse_agg_next = agg_in_kernel && m == 1;
     pairs_next = fused_mnist && mnist_tc && c2_pairs && m == 1 && !fuse_agg_next;
     sparse_embed_next = emb_layer >= 0 && m == 1;
+    ghost_next = any_ghost && m == 1;
     try {
       nk += enqueue_grads(s, x_slot, y_slot);
     } catch (...) {
-      fuse_agg_next = sparse_embed_next = pairs_next = false;
+      fuse_agg_next = sparse_embed_next = pairs_next = ghost_next = false;
       throw;
     }
     if (fuse_agg_next) {
@@ -1355,9 +1423,12 @@ struct Engine {
         t.rows[2] = (int)((B + 1) / 2);
         t.stride[2] = t.size[2];
       }
-      nk += enqueue_aggregate(s, t, nparts, (int)B, fused_mnist);
+      if (ghost_next)
+        nk += enqueue_ghost_aggregate(s, t);
+      else
+        nk += enqueue_aggregate(s, t, nparts, (int)B, fused_mnist);
     }
-    sparse_embed_next = pairs_next = false;
+    sparse_embed_next = pairs_next = ghost_next = false;
     return nk;
   }
 
@@ -1511,11 +1582,120 @@ struct Engine {
       L.step_off = cap_step_off;
       L.cnt_in = d_clipped;
       L.clipped_out = clipped_dst;
+      L.only_kind = -1;
       int64_t pairs = 0;
       for (int p = 0; p < t.n; ++p) pairs += (t.size[p] + 1) / 2;
       noise_update_kernel<<<grid_for((size_t)pairs), 256, 0, s>>>(L);
       nk += mark(s, "noise_update");
     }
+    return nk;
+  }
+
+  template <class K>
+  void gram_attr(K* kern, size_t smem) {
+    if (smem > 48 * 1024)
+      PGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  }
+
+  // The clipped sums sum_i s_i dW_i of the ghost conv blocks into d_sum: the
+  // input's column-shifted copies and the clip-scaled cotangent as 3xTF32
+  // pairs, one GEMM over (example, position) split over the examples, the
+  // splits added in order.
+  int enqueue_ghost_sums(cudaStream_t s) {
+    int nk = 0;
+    for (int l = 0; l < desc.n_layers; ++l) {
+      const Layer& L = layers[l];
+      if (!L.ghost) continue;
+      const ConvGeom g = conv_geom(L);
+      const int Bi = (int)B, HW = g.H * g.W, bn = tg::pick_bn(g.D);
+      int Cr, T, big, mtiles;
+      tg::dw_tiling(g.C, Cr, T, big, mtiles);
+      const long long total = (long long)Bi * g.C * HW;
+      const float* in = L.act_in;
+      tg::shift3_kernel<<<grid_for((size_t)(3 * total)), 256, 0, s>>>(in, d_nhwc, d_nhwc_lo,
+                                                                      total, g.W);
+      const long long gt = (long long)Bi * g.D * HW;
+      tg::scale_split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(L.gout, d_scale,
+                                                                  (long long)g.D * HW, gt, d_wt,
+                                                                  d_wt_lo);
+      tg::Params p{};
+      const uint64_t da[4] = {(uint64_t)HW, (uint64_t)g.C, (uint64_t)Bi, 3};
+      const uint64_t sa[3] = {4ull * HW, 4ull * HW * g.C, 4ull * total};
+      const uint32_t ba[4] = {32, (uint32_t)Cr, 1, 1};
+      tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+      tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+      const uint64_t db[3] = {(uint64_t)HW, (uint64_t)g.D, (uint64_t)Bi};
+      const uint64_t sb[2] = {4ull * HW, 4ull * HW * g.D};
+      const uint32_t bb[3] = {32, (uint32_t)bn, 1};
+      tg::make_map(&p.tb, d_wt, 3, db, sb, bb);
+      tg::make_map(&p.tb_lo, d_wt_lo, 3, db, sb, bb);
+      p.mode = tg::kConvDwSum;
+      p.M = mtiles * 128;
+      p.N = g.D;
+      p.nchunks = (HW + 31) / 32;
+      p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
+      p.Cr = Cr, p.T = T, p.big_c = big;
+      p.bx = g.W, p.dw_by = 32 / g.W;
+      const int ntiles = (g.D + bn - 1) / bn;
+      p.tiles = ntiles * mtiles;
+      const int S = L.ghost_splits;
+      p.ex_per = (Bi + S - 1) / S;
+      p.nex = Bi;
+      p.ws = d_dw_ws;
+      const int splits = (Bi + p.ex_per - 1) / p.ex_per;
+      tg::launch(p, bn, dim3(ntiles, mtiles, splits), s);
+      const long long per = (long long)mtiles * ntiles * bn * 128;
+      tg::dw_sum_reduce_kernel<<<grid_for((size_t)per), 256, 0, s>>>(
+          d_dw_ws, splits, mtiles, ntiles * bn, g.C, g.D, Cr, T, big,
+          d_sum + param_off[L.pblock]);
+      nk += mark(s, "conv_dw_sum") + 3;
+    }
+    return nk;
+  }
+
+  // The step's tail when ghost conv blocks are present: clip factors once,
+  // the ghost blocks' clipped sums by GEMM, the other blocks through the
+  // aggregation kernel (with the clip factors given), then noise / mean /
+  // update of the ghost blocks (single process) or of everything after the
+  // all-reduce (data-parallel).
+  int enqueue_ghost_aggregate(cudaStream_t s, const BlockTable& t) {
+    int nk = 0;
+    ScalesLaunch SL{d_parts, nparts, (int)B, cur_args, d_scale, d_clipflag, norms_dst};
+    step_scales_kernel<<<((int)B + 127) / 128, 128, 0, s>>>(SL);
+    nk += mark(s, "step_scales");
+    nk += enqueue_ghost_sums(s);
+    BlockTable t2 = t;
+    for (const Layer& L : layers)
+      if (L.ghost) t2.kind[L.pblock] = 3;  // no aggregation tiles: summed by GEMM
+    AggLaunch A = agg_launch(t2, nparts, (int)B, dist ? 1 : 0);
+    A.scales = d_scale;
+    A.clip_flags = d_clipflag;
+    launch_agg(A, s);
+    nk += mark(s, dist ? "aggregate_local" : "aggregate");
+    if (dist) {
+      auto& N = Nccl::get();
+      PGB_NCCL(N.groupStart());
+      PGB_NCCL(N.allReduce(d_sum, d_sum, (size_t)P, ncclFloat32, ncclSum, comm, s));
+      PGB_NCCL(N.allReduce(d_clipped, d_clipped + 1, 1, ncclInt32, ncclSum, comm, s));
+      PGB_NCCL(N.groupEnd());
+    }
+    NoiseLaunch NL{};
+    NL.bt = t2;
+    NL.a = cur_args;
+    NL.sum = d_sum;
+    NL.params = d_params;
+    NL.err = d_err;
+    NL.noise = nullptr;
+    NL.step_base = cap_step_base;
+    NL.step_off = cap_step_off;
+    NL.cnt_in = d_clipped;
+    NL.clipped_out = dist ? clipped_dst : nullptr;
+    NL.only_kind = dist ? -1 : 3;
+    int64_t pairs = 0;
+    for (int p = 0; p < t2.n; ++p) pairs += (t2.size[p] + 1) / 2;
+    noise_update_kernel<<<grid_for((size_t)pairs), 256, 0, s>>>(NL);
+    nk += mark(s, "noise_update");
     return nk;
   }
 
@@ -1745,6 +1925,9 @@ struct Engine {
       } else if (kp.func == (void*)noise_update_kernel) {
         sg.noise = nd;
         sg.noise_args = *static_cast<const NoiseLaunch*>(kp.kernelParams[0]);
+      } else if (kp.func == (void*)step_scales_kernel) {
+        sg.scales = nd;
+        sg.scales_args = *static_cast<const ScalesLaunch*>(kp.kernelParams[0]);
       } else if (kp.func == (void*)mnist::fused_kernel ||
                  kp.func == (void*)mnist::tc_kernel<false> ||
                  kp.func == (void*)mnist::tc_kernel<true>) {
@@ -1789,11 +1972,17 @@ struct Engine {
       sg.emb_args.a = cur_args;
       set_node(sg.exec, sg.emb, &sg.emb_args);
     }
+    // (a noise node without a count copy -- the ghost blocks' update -- keeps none)
     if (sg.noise && (!same_args(sg.noise_args.a, cur_args) ||
-                     sg.noise_args.clipped_out != clipped_dst)) {
+                     (sg.noise_args.clipped_out && sg.noise_args.clipped_out != clipped_dst))) {
       sg.noise_args.a = cur_args;
-      sg.noise_args.clipped_out = clipped_dst;
+      if (sg.noise_args.clipped_out) sg.noise_args.clipped_out = clipped_dst;
       set_node(sg.exec, sg.noise, &sg.noise_args);
+    }
+    if (sg.scales && (!same_args(sg.scales_args.a, cur_args) || sg.scales_args.norms != norms_dst)) {
+      sg.scales_args.a = cur_args;
+      sg.scales_args.norms = norms_dst;
+      set_node(sg.exec, sg.scales, &sg.scales_args);
     }
     const bool agg_in = sg.fused_tc && sg.fused_args.agg_tiles > 0;
     if (sg.fused && (sg.fused_args.x != x_slot || sg.fused_args.y != y_slot ||

@@ -1646,6 +1646,119 @@ __global__ void __launch_bounds__(32 * kEmbAggWarps) embed_agg4_kernel(const Emb
   }
 }
 
+// ---- ghost norms of 3x3 / stride-1 / pad-1 conv weight blocks --------------
+// ||dW_i||^2 = sum_{p,q} (g_p . g_q) (a_p . a_q) with a_p the im2col patch at
+// output position p and g_p the output cotangent there (the ghost-norm
+// identity, generalised from dense layers to convolutions): the patch Gram is
+// a sum of shifted input Grams, a_p . a_q = sum_taps x~_{p+t} . x~_{q+t} (x~ the
+// zero-padded input). For the 8x8 and 4x4 layers (HW <= 64) this is far less
+// work than the per-example dW GEMM, and no (B, D, C, 3, 3) stack is written.
+// One CTA of 256 threads per example; Grams in fp32 (dots of length C, D),
+// the weighted sum over (p, q) in fp64, into parts[i * nparts + pb]
+// (dpsgd.cpp:254-270 accumulates the block's squares in double).
+template <int HW>
+__global__ void __launch_bounds__(256) conv_gram_norm_kernel(
+    const float* __restrict__ x, const float* __restrict__ g, int C, int D, int W,
+    double* __restrict__ parts, int nparts, int pb) {
+  static_assert(HW == 16 || HW == 64, "ghost norms for 4x4 and 8x8 maps");
+  constexpr int R = HW == 64 ? 4 : 1;  // (p, q) block per thread: R x R
+  extern __shared__ float gsm[];
+  float* xs = gsm;               // [C][HW]
+  float* gs = xs + C * HW;       // [D][HW]
+  float* gx = gs + D * HW;       // [HW][HW]
+  __shared__ double red[8];
+  const int i = blockIdx.x, t = threadIdx.x;
+  const float* xi = x + (size_t)i * C * HW;
+  const float* gi = g + (size_t)i * D * HW;
+  for (int e = t; e < C * HW; e += 256) xs[e] = xi[e];
+  for (int e = t; e < D * HW; e += 256) gs[e] = gi[e];
+  __syncthreads();
+  const int tp = t / (HW / R), tq = t % (HW / R);
+  float ax[R][R], ag[R][R];
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < R; ++k) ax[j][k] = ag[j][k] = 0.0f;
+  auto gram = [&](const float* src, int n, float (*acc)[R]) {
+    for (int c = 0; c < n; ++c) {
+      float a[R], b[R];
+      if constexpr (R == 4) {
+        const float4 va = reinterpret_cast<const float4*>(src + c * HW)[tp];
+        const float4 vb = reinterpret_cast<const float4*>(src + c * HW)[tq];
+        a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
+        b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
+      } else {
+        a[0] = src[c * HW + tp];
+        b[0] = src[c * HW + tq];
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[j][k] = fmaf(a[j], b[k], acc[j][k]);
+    }
+  };
+  gram(xs, C, ax);
+  gram(gs, D, ag);
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < R; ++k) gx[(tp * R + j) * HW + tq * R + k] = ax[j][k];
+  __syncthreads();
+  const int H = HW / W;
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int pp = tp * R + j, qq = tq * R + k;
+      const int py = pp / W, px = pp - py * W, qy = qq / W, qx = qq - qy * W;
+      float ga = 0.0f;
+#pragma unroll
+      for (int u = -1; u <= 1; ++u)
+#pragma unroll
+        for (int v = -1; v <= 1; ++v) {
+          const int a0 = py + u, a1 = px + v, b0 = qy + u, b1 = qx + v;
+          if (a0 >= 0 && a0 < H && a1 >= 0 && a1 < W && b0 >= 0 && b0 < H && b1 >= 0 && b1 < W)
+            ga += gx[(a0 * W + a1) * HW + b0 * W + b1];
+        }
+      acc = fma((double)ag[j][k], (double)ga, acc);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((t & 31) == 0) red[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    parts[(size_t)i * nparts + pb] = tot;
+  }
+}
+
+// Per-example norms, clip factors and clip flags from the fp64 partials (the
+// same arithmetic as agg_scales), once per step, for the steps whose conv
+// weight gradients are summed by a clip-scaled GEMM.
+struct ScalesLaunch {
+  const double* parts;
+  int nparts, U;
+  StepArgs a;
+  float* scale;
+  int* flags;
+  float* norms;  // the step's result slot (a per-launch node argument)
+};
+
+__global__ void step_scales_kernel(const ScalesLaunch L) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.U) return;
+  double acc = 0.0;
+  for (int q = 0; q < L.nparts; ++q) acc += L.parts[(size_t)i * L.nparts + q];
+  const float nrm = (float)sqrt(acc);
+  const float clip = L.a.clip;
+  L.scale[i] = nrm > clip ? __fdiv_rn(clip, nrm) : 1.0f;
+  L.flags[i] = nrm > clip ? 1 : 0;
+  if (L.norms) L.norms[i] = nrm;
+}
+
 // After the all-reduce of the clipped sums: noise (one shared draw from the
 // common seed, so every rank adds the same vector), mean over the global
 // units, update (dpsgd.cpp:308-317, apply_update :173-183). One thread per
@@ -1665,6 +1778,7 @@ struct NoiseLaunch {
   // where the all-reduce's pointers are fixed at capture)
   const int* cnt_in;
   int* clipped_out;
+  int only_kind;  // >= 0: update only the blocks of this kind (the others are done)
 };
 
 __global__ void __launch_bounds__(256) noise_update_kernel(const NoiseLaunch L) {
@@ -1699,6 +1813,7 @@ __global__ void __launch_bounds__(256) noise_update_kernel(const NoiseLaunch L) 
       else hi = mid - 1;
     }
     const int p = lo;
+    if (L.only_kind >= 0 && bt.kind[p] != L.only_kind) continue;
     const long long jp = q - pair_sh[p], j0 = 2 * jp;
     const long long off = bt.param_off[p];
     float nv[2] = {0.0f, 0.0f};

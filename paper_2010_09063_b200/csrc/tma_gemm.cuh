@@ -46,6 +46,12 @@
 //            boxes start on 16-byte boundaries of the innermost dimension;
 //            out = the reference's per-example dW stack (B, D, C, 3, 3)
 //            (strategies.cpp:156-170) + each tile's squared sum (fp64)
+//   kConvDwSum the clipped weight gradient sum_i s_i dW_i as ONE GEMM over
+//            K = (example, position): the kConvDw operands with the cotangent
+//            pre-scaled by the example's clip factor (scale_split_kernel);
+//            the examples are split over the grid (tile z = example range
+//            [z * ex_per, (z+1) * ex_per)), each split's raw tile goes to a
+//            workspace and dw_sum_reduce_kernel adds the splits in order
 #pragma once
 
 #include <cuda.h>
@@ -57,7 +63,7 @@ namespace pgb {
 namespace tg {
 
 constexpr int kBM = 128, kBK = 32, kThreads = 256;
-enum Mode { kPlain = 0, kConvFwd = 1, kConvDx = 2, kConvDw = 3 };
+enum Mode { kPlain = 0, kConvFwd = 1, kConvDx = 2, kConvDw = 3, kConvDwSum = 4 };
 
 struct alignas(64) Params {
   CUtensorMap ta, tb;        // the hi tensors
@@ -72,7 +78,10 @@ struct alignas(64) Params {
   int Cr, T;         // dw: rows per tap slot (multiple of 8), tap slots per M tile
   int big_c;         // dw: C >= 128 -> M tile = 128 channels of one tap
   int bx, dw_by;     // dw boxes: x extent, rows per chunk
-  int tiles;         // tiles per GEMM (gridDim.x * gridDim.y), tile_sq row length
+  int tiles;         // tiles per GEMM (ntn * ntm), tile_sq row length
+  int ntn, ntm, nz;  // N tiles, M tiles, GEMMs (examples / example splits); set by launch()
+  int ex_per, nex;   // dw-sum: examples per split, examples in total
+  float* ws;         // dw-sum: split workspace [z][mt][n][128 rows]
   // epilogue
   float* out;
   const float* bias;
@@ -84,19 +93,38 @@ struct alignas(64) Params {
 
 template <int BN>
 constexpr int stages() { return BN >= 128 ? 3 : BN >= 64 ? 4 : 5; }
-// hi.hi accumulators: all of TMEM but one accumulator (the corrections)
+// Narrow tiles (BN <= 64) fold the 3xTF32 split into N: the B stage holds the
+// hi rows then the lo rows (2 BN rows, one operand), so a K step is two MMAs
+// of width 2 BN -- Ahi.[Bhi;Blo] and Alo.[Bhi;Blo] -- instead of three of
+// width BN (a single thread issues an MMA only every ~50-120 cycles and below
+// N ~ 100 an MMA costs that fixed time, scripts/umma_rate.py); the epilogue
+// adds column n and BN + n (the lo.lo product rides along, <= 2^-44 relative).
 template <int BN>
-constexpr int nacc() { return 512 / (BN < 32 ? 32 : BN) - 1; }
+constexpr bool folded() { return BN <= 64; }
+// TMEM: two 256-column accumulator buffers (the epilogue of tile k overlaps
+// the MMAs of tile k+1) except for BN = 128, whose hi.hi rotation needs the
+// whole of TMEM (the tensor core's fp32 accumulation is not round-to-nearest:
+// chains are kept short by rotating the hi.hi products over accumulators).
+template <int BN>
+constexpr int nbuf() { return BN >= 128 ? 1 : 2; }
+template <int BN>
+constexpr int acc_stride() { return folded<BN>() ? (2 * BN < 32 ? 32 : 2 * BN) : (BN < 32 ? 32 : BN); }
+// accumulators per buffer: folded -- all of them rotate; unfolded -- the
+// hi.hi rotation plus one for the two correction products
+template <int BN>
+constexpr int nacc() {
+  return folded<BN>() ? (512 / nbuf<BN>()) / acc_stride<BN>()
+                      : (512 / nbuf<BN>()) / acc_stride<BN>() - 1;
+}
 
 template <int BN>
 struct Smem {
   static constexpr int S = stages<BN>();
   float a_hi[S][kBM * kBK];
   float a_lo[S][kBM * kBK];
-  float b_hi[S][BN * kBK];
-  float b_lo[S][BN * kBK];
+  float b[S][2][BN * kBK];  // hi rows, then lo rows (adjacent: one 2 BN-row operand)
   uint64_t full[S], empty[S];
-  uint64_t acc;
+  uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem;
   double sq[4];
 };
@@ -165,7 +193,7 @@ __device__ __forceinline__ void split2(float x, float& hi, float& lo) {
 // included). A dW tile past the ninth tap leaves its slots unloaded: those
 // accumulator rows are never stored.
 __device__ __forceinline__ uint32_t a_bytes(const Params& p, int mt) {
-  if (p.mode == kConvDw)
+  if (p.mode == kConvDw || p.mode == kConvDwSum)
     return (uint32_t)(p.big_c ? kBM : min(p.T, 9 - mt * p.T) * p.Cr) * kBK * 4;
   return kBM * kBK * 4;
 }
@@ -194,7 +222,8 @@ __device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* 
       tma_2d(db, mb, tap * p.Cg * kBK + cg * kBK, nt * BN, bar);
       break;
     }
-    case kConvDw: {
+    case kConvDw:
+    case kConvDwSum: {
       const int p0 = q * kBK;  // first position of the chunk (flattened H*W)
       if (p.big_c) {
         const int cgs = p.C / kBM, tap = mt / cgs, c0 = (mt - tap * cgs) * kBM;
@@ -218,11 +247,41 @@ template <int BN>
 __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s, int q, int mt,
                                             int nt, int z) {
   const uint32_t bar = smem_u32(&S.full[s]);
-  issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b_hi[s]), BN, q, mt, nt, z, bar);
-  issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b_lo[s]), BN, q, mt, nt, z,
+  issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b[s][0]), BN, q, mt, nt, z, bar);
+  issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b[s][1]), BN, q, mt, nt, z,
               bar);
 }
 
+// K chunks of a tile: dw-sum walks the positions of every example of its split
+__device__ __forceinline__ int tile_chunks(const Params& p, int z) {
+  if (p.mode != kConvDwSum) return p.nchunks;
+  const int e0 = z * p.ex_per, e1 = min(p.nex, e0 + p.ex_per);
+  return max(0, e1 - e0) * p.nchunks;
+}
+// chunk q of a tile -> (position chunk, example)
+__device__ __forceinline__ void chunk_coords(const Params& p, int q, int z, int& qc, int& ze) {
+  if (p.mode != kConvDwSum) {
+    qc = q;
+    ze = z;
+  } else {
+    const int k = q / p.nchunks;
+    qc = q - k * p.nchunks;
+    ze = z * p.ex_per + k;
+  }
+}
+
+// tile index -> (nt, mt, z), N tiles fastest
+__device__ __forceinline__ void tile_coords(const Params& p, int t, int& nt, int& mt, int& z) {
+  nt = t % p.ntn;
+  const int r = t / p.ntn;
+  mt = r % p.ntm;
+  z = r / p.ntm;
+}
+
+// Persistent: one CTA per SM walks the tiles t = blockIdx.x + k * gridDim.x.
+// The TMA ring runs across tile boundaries (the next tile's operands stream in
+// while this tile's MMAs finish), and with two accumulator buffers the
+// epilogue of a tile overlaps the next tile's MMAs.
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char raw[];
@@ -231,18 +290,23 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
       (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr int NS = Smem<BN>::S;
   constexpr uint32_t kCols = 512;
+  constexpr bool kFold = folded<BN>();
+  constexpr int NB = nbuf<BN>();
   constexpr int NACC = nacc<BN>();
-  constexpr uint32_t kAccStride = BN < 32 ? 32 : BN;  // TMEM columns per accumulator
+  constexpr uint32_t kAccStride = acc_stride<BN>();
+  constexpr uint32_t kBufCols = 512 / NB;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int nt = blockIdx.x, mt = blockIdx.y, z = blockIdx.z;
-  const int nq = p.nchunks;
+  const int total = p.ntn * p.ntm * p.nz;
   if (warp == 1) tc::tmem_alloc(&S.tmem, kCols);
   if (t == 0) {
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 1);
     }
-    tc::mbar_init(&S.acc, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&S.acc_full[b], 1);
+      tc::mbar_init(&S.acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta) : "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb) : "memory");
@@ -257,126 +321,188 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
   if (warp == 0) {
     // ---- TMA producer ----
     if (lane == 0) {
-      const uint32_t bytes = 2 * (a_bytes(p, mt) + BN * kBK * 4);
-      for (int q = 0; q < nq; ++q) {
-        const int s = q % NS;
-        if (q >= NS) tc::mbar_wait(&S.empty[s], ((q / NS) - 1) & 1);
-        expect_tx(&S.full[s], bytes);
-        issue_chunk<BN>(p, S, s, q, mt, nt, z);
+      int g = 0;  // chunks issued by this CTA (ring position)
+      for (int tl = blockIdx.x; tl < total; tl += gridDim.x) {
+        int nt, mt, z;
+        tile_coords(p, tl, nt, mt, z);
+        const uint32_t bytes = 2 * (a_bytes(p, mt) + BN * kBK * 4);
+        const int nq = tile_chunks(p, z);
+        for (int q = 0; q < nq; ++q, ++g) {
+          const int s = g % NS;
+          if (g >= NS) tc::mbar_wait(&S.empty[s], ((g / NS) - 1) & 1);
+          expect_tx(&S.full[s], bytes);
+          int qc, ze;
+          chunk_coords(p, q, z, qc, ze);
+          issue_chunk<BN>(p, S, s, qc, mt, nt, ze);
+        }
       }
     }
   } else if (warp == 1) {
     // ---- MMA issuer ----
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN < 16 ? 16 : BN);
-      for (int q = 0; q < nq; ++q) {
-        const int s = q % NS;
-        tc::mbar_wait(&S.full[s], (q / NS) & 1);
+      constexpr uint32_t idesc = tc::idesc_tf32(kBM, kFold ? 2 * BN : (BN < 16 ? 16 : BN));
+      int g = 0, lt = 0;
+      for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
+        int nt_, mt_, z_;
+        tile_coords(p, tl, nt_, mt_, z_);
+        const int nq = tile_chunks(p, z_);
+        const int bsel = NB == 2 ? (lt & 1) : 0;
+        const int use = NB == 2 ? (lt >> 1) : lt;  // earlier uses of this buffer
+        if (use > 0) tc::mbar_wait(&S.acc_empty[bsel], (use - 1) & 1);
         tc::fence_after_sync();
-        const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
-        const uint32_t bh = smem_u32(S.b_hi[s]), bl = smem_u32(S.b_lo[s]);
-        const uint32_t dmain = tmem + (uint32_t)(q % NACC) * kAccStride;
-        const uint32_t dcorr = tmem + (uint32_t)NACC * kAccStride;
+        const uint32_t buf = tmem + (uint32_t)bsel * kBufCols;
+        for (int q = 0; q < nq; ++q, ++g) {
+          const int s = g % NS;
+          tc::mbar_wait(&S.full[s], (g / NS) & 1);
+          tc::fence_after_sync();
+          const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
+          const uint32_t bh = smem_u32(S.b[s][0]), bl = smem_u32(S.b[s][1]);
+          const uint32_t dmain = buf + (uint32_t)(q % NACC) * kAccStride;
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          const uint32_t o = 32u * k;
-          tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
-                       (q >= NACC || k) ? 1u : 0u);
-          tc::mma_tf32(dcorr, desc_sw128(ah + o), desc_sw128(bl + o), idesc, (q | k) ? 1u : 0u);
-          tc::mma_tf32(dcorr, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t o = 32u * k;
+            if constexpr (kFold) {
+              // [Bhi; Blo] is one 2 BN-row operand starting at bh
+              tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
+                           (q >= NACC || k) ? 1u : 0u);
+              tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+            } else {
+              const uint32_t dcorr = buf + (uint32_t)NACC * kAccStride;
+              tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
+                           (q >= NACC || k) ? 1u : 0u);
+              tc::mma_tf32(dcorr, desc_sw128(ah + o), desc_sw128(bl + o), idesc, (q | k) ? 1u : 0u);
+              tc::mma_tf32(dcorr, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+            }
+          }
+          tc::commit(&S.empty[s]);
         }
-        tc::commit(&S.empty[s]);
+        tc::commit(&S.acc_full[bsel]);
       }
-      tc::commit(&S.acc);
     }
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> registers -> global ----
-    tc::mbar_wait(&S.acc, 0);
-    tc::fence_after_sync();
     const int q4 = warp & 3, r = q4 * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
-    double sq = 0.0;
-    const int m = mt * kBM + r;
-    const int used = nq < NACC ? nq : NACC;
+    int lt = 0;
+    for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
+      int nt, mt, z;
+      tile_coords(p, tl, nt, mt, z);
+      const int nq = tile_chunks(p, z);
+      const int used = nq < NACC ? nq : NACC;
+      const int bsel = NB == 2 ? (lt & 1) : 0;
+      const int use = NB == 2 ? (lt >> 1) : lt;
+      tc::mbar_wait(&S.acc_full[bsel], use & 1);
+      tc::fence_after_sync();
+      const uint32_t lane_base =
+          tmem + (uint32_t)bsel * kBufCols + ((uint32_t)(q4 * 32) << 16);
+      double sq = 0.0;
+      const int m = mt * kBM + r;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 8) {
-      float v[8], w[8];
-      tc::tmem_ld8(lane_base + (uint32_t)(NACC * kAccStride + c0), v);  // corrections
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        float v[8], w[8];
+        if constexpr (kFold) {
+          tc::tmem_ld8(lane_base + (uint32_t)c0, v);
+          tc::tmem_ld8(lane_base + (uint32_t)(BN + c0), w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] += w[j];
 #pragma unroll 1
-      for (int a = 0; a < used; ++a) {
-        tc::tmem_ld8(lane_base + (uint32_t)(a * kAccStride + c0), w);
+          for (int a = 1; a < used; ++a) {
+            tc::tmem_ld8(lane_base + (uint32_t)(a * kAccStride + c0), w);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] += w[j];
-      }
-      const int n0 = nt * BN + c0;
-      switch (p.mode) {
-        case kPlain:
-          if (m < p.M)
+            for (int j = 0; j < 8; ++j) v[j] += w[j];
+            tc::tmem_ld8(lane_base + (uint32_t)(a * kAccStride + BN + c0), w);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (n0 + j < p.N) p.out[(size_t)m * p.ldc + n0 + j] = v[j];
-          break;
-        case kConvFwd: {
-          const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
-          if (m < p.M)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int d = n0 + j;
-              if (d < p.N) {
-                float o = v[j] + p.bias[d];
-                if (p.relu) o = fmaxf(o, 0.0f);
-                p.out[((size_t)img * p.D + d) * HW + pos] = o;
-              }
-            }
-          break;
-        }
-        case kConvDx: {
-          const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
-          if (m < p.M)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int c = n0 + j;
-              if (c < p.N) {
-                const size_t i = ((size_t)img * p.C + c) * HW + pos;
-                p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : v[j];
-              }
-            }
-          break;
-        }
-        case kConvDw: {
-          int tap, c;
-          if (p.big_c) {
-            const int cgs = p.C / kBM;
-            tap = mt / cgs;
-            c = (mt - tap * cgs) * kBM + r;
-          } else {
-            const int sl = r / p.Cr;
-            tap = mt * p.T + sl;
-            c = r - sl * p.Cr;
+            for (int j = 0; j < 8; ++j) v[j] += w[j];
           }
-          if (tap < 9 && c < p.C) {
-            float* st = p.out + (size_t)z * p.D * p.C * 9;
+        } else {
+          tc::tmem_ld8(lane_base + (uint32_t)(NACC * kAccStride + c0), v);  // corrections
+#pragma unroll 1
+          for (int a = 0; a < used; ++a) {
+            tc::tmem_ld8(lane_base + (uint32_t)(a * kAccStride + c0), w);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int d = n0 + j;
-              if (d < p.N) {
-                st[((size_t)d * p.C + c) * 9 + tap] = v[j];
-                sq = fma((double)v[j], (double)v[j], sq);
+            for (int j = 0; j < 8; ++j) v[j] += w[j];
+          }
+        }
+        const int n0 = nt * BN + c0;
+        switch (p.mode) {
+          case kPlain:
+            if (m < p.M)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (n0 + j < p.N) p.out[(size_t)m * p.ldc + n0 + j] = v[j];
+            break;
+          case kConvFwd: {
+            const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+            if (m < p.M)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int d = n0 + j;
+                if (d < p.N) {
+                  float o = v[j] + p.bias[d];
+                  if (p.relu) o = fmaxf(o, 0.0f);
+                  p.out[((size_t)img * p.D + d) * HW + pos] = o;
+                }
+              }
+            break;
+          }
+          case kConvDx: {
+            const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+            if (m < p.M)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = n0 + j;
+                if (c < p.N) {
+                  const size_t i = ((size_t)img * p.C + c) * HW + pos;
+                  p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : v[j];
+                }
+              }
+            break;
+          }
+          case kConvDwSum: {
+            float* w = p.ws + (((size_t)z * p.ntm + mt) * (size_t)(p.ntn * BN) + n0) * kBM + r;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w[(size_t)j * kBM] = used > 0 ? v[j] : 0.0f;
+            break;
+          }
+          case kConvDw: {
+            int tap, c;
+            if (p.big_c) {
+              const int cgs = p.C / kBM;
+              tap = mt / cgs;
+              c = (mt - tap * cgs) * kBM + r;
+            } else {
+              const int sl = r / p.Cr;
+              tap = mt * p.T + sl;
+              c = r - sl * p.Cr;
+            }
+            if (tap < 9 && c < p.C) {
+              float* st = p.out + (size_t)z * p.D * p.C * 9;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int d = n0 + j;
+                if (d < p.N) {
+                  st[((size_t)d * p.C + c) * 9 + tap] = v[j];
+                  sq = fma((double)v[j], (double)v[j], sq);
+                }
               }
             }
+            break;
           }
-          break;
         }
       }
-    }
-    if (p.mode == kConvDw && p.tile_sq) {
+      // the accumulator buffer is free once every epilogue warp has read it
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.acc_empty[bsel]);
+      if (p.mode == kConvDw && p.tile_sq) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-      if (lane == 0) S.sq[q4] = sq;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (t == 128)
-        p.tile_sq[(size_t)z * p.tiles + mt * gridDim.x + nt] =
-            ((S.sq[0] + S.sq[1]) + S.sq[2]) + S.sq[3];
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) S.sq[q4] = sq;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t == 128)
+          p.tile_sq[(size_t)z * p.tiles + mt * p.ntn + nt] =
+              ((S.sq[0] + S.sq[1]) + S.sq[2]) + S.sq[3];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
     }
   }
   tc::fence_before_sync();
@@ -439,6 +565,46 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
     const long long i = e - v * total;
     const int x = (int)(i % W), xs = x + v - 1;
     split2((xs >= 0 && xs < W) ? src[i + v - 1] : 0.0f, dst[e], dst_lo[e]);
+  }
+}
+
+// the clip-scaled cotangent of the summed weight gradient, as the 3xTF32 pair:
+// fl(g * s_i) split into hi / lo (per element the reference's fl(g_ij * s_i)
+// rounding moves from the weight gradient to the cotangent it is built from)
+__global__ void scale_split_kernel(const float* __restrict__ g, const float* __restrict__ scale,
+                                   long long per_ex, long long total, float* __restrict__ hi,
+                                   float* __restrict__ lo) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    split2(__fmul_rn(g[e], scale[e / per_ex]), hi[e], lo[e]);
+}
+
+// Sum the example splits of the kConvDwSum workspace in split order (fixed:
+// run-to-run deterministic) and scatter the tile rows (tap slot, channel) to
+// the (D, C, 3, 3) parameter layout of the clipped-sum vector.
+__global__ void dw_sum_reduce_kernel(const float* __restrict__ ws, int splits, int ntm, int npad,
+                                     int C, int D, int Cr, int T, int big,
+                                     float* __restrict__ out) {
+  const long long per_split = (long long)ntm * npad * kBM;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_split;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % kBM);
+    const long long t = e / kBM;
+    const int n = (int)(t % npad), mt = (int)(t / npad);
+    int tap, c;
+    if (big) {
+      const int cgs = C / kBM;
+      tap = mt / cgs;
+      c = (mt - tap * cgs) * kBM + r;
+    } else {
+      const int sl = r / Cr;
+      tap = mt * T + sl;
+      c = r - sl * Cr;
+    }
+    if (tap >= 9 || c >= C || n >= D) continue;
+    float acc = ws[e];
+    for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[(long long)z * per_split + e]);
+    out[((long long)n * C + c) * 9 + tap] = acc;
   }
 }
 
@@ -506,8 +672,19 @@ inline void make_map(CUtensorMap* m, const float* base, int rank, const uint64_t
 
 inline int pick_bn(int n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : 128; }
 
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int BN>
-inline void launch_bn(const Params& p, dim3 grid, cudaStream_t s) {
+inline void launch_bn(const Params& p, int ctas, cudaStream_t s) {
   static int attr_dev = -1;  // the attribute is set once per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -516,15 +693,22 @@ inline void launch_bn(const Params& p, dim3 grid, cudaStream_t s) {
                          (int)smem_bytes<BN>());
     attr_dev = dev;
   }
-  tma_gemm_kernel<BN><<<grid, kThreads, smem_bytes<BN>(), s>>>(p);
+  tma_gemm_kernel<BN><<<ctas, kThreads, smem_bytes<BN>(), s>>>(p);
 }
 
-inline void launch(const Params& p, int bn, dim3 grid, cudaStream_t s) {
+// tiles: (N tiles, M tiles, GEMMs); one persistent CTA per SM walks them
+inline void launch(const Params& p0, int bn, dim3 tiles, cudaStream_t s) {
+  Params p = p0;
+  p.ntn = (int)tiles.x;
+  p.ntm = (int)tiles.y;
+  p.nz = (int)tiles.z;
+  const long long total = (long long)p.ntn * p.ntm * p.nz;
+  const int ctas = (int)std::min<long long>(total, num_sms());
   switch (bn) {
-    case 16: launch_bn<16>(p, grid, s); break;
-    case 32: launch_bn<32>(p, grid, s); break;
-    case 64: launch_bn<64>(p, grid, s); break;
-    default: launch_bn<128>(p, grid, s); break;
+    case 16: launch_bn<16>(p, ctas, s); break;
+    case 32: launch_bn<32>(p, ctas, s); break;
+    case 64: launch_bn<64>(p, ctas, s); break;
+    default: launch_bn<128>(p, ctas, s); break;
   }
 }
 

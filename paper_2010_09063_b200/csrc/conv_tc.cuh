@@ -115,12 +115,20 @@ struct TcConvBwdXS1Op {
     const int u = r / g.k, v = r - u * g.k;
     return __ldg(W + (((size_t)d * g.C + n) * g.k + (g.k - 1 - u)) * g.k + (g.k - 1 - v));
   }
-  __device__ void store(int, int m, int n, float v) const {
+  __device__ size_t gx_index(int m, int n) const {
     const int HW = g.H * g.W;
     const int bb = m / HW, q = m - bb * HW;
-    const size_t i = ((size_t)bb * g.C + n) * HW + q;
-    gx[i] = (mask && !(mask[i] > 0.0f)) ? 0.0f : v;
+    return ((size_t)bb * g.C + n) * HW + q;
   }
+  // the relu mask of an output element, loaded before any store of its
+  // column group (tc_gemm_kernel: HasPre)
+  __device__ float pre(int, int m, int n) const {
+    return mask ? __ldg(mask + gx_index(m, n)) : 1.0f;
+  }
+  __device__ void store_pre(int, int m, int n, float v, float mk) const {
+    gx[gx_index(m, n)] = !(mk > 0.0f) ? 0.0f : v;
+  }
+  __device__ void store(int z, int m, int n, float v) const { store_pre(z, m, n, v, pre(z, m, n)); }
 };
 
 // general stride: per-element gather with the divisibility check
@@ -150,12 +158,20 @@ struct TcConvBwdXOp {
     const int d = k / kk2, r = k - d * kk2;
     return __ldg(W + ((size_t)d * g.C + n) * kk2 + r);
   }
-  __device__ void store(int, int m, int n, float v) const {
+  __device__ size_t gx_index(int m, int n) const {
     const int HW = g.H * g.W;
     const int bb = m / HW, q = m - bb * HW;
-    const size_t i = ((size_t)bb * g.C + n) * HW + q;
-    gx[i] = (mask && !(mask[i] > 0.0f)) ? 0.0f : v;
+    return ((size_t)bb * g.C + n) * HW + q;
   }
+  // the relu mask of an output element, loaded before any store of its
+  // column group (tc_gemm_kernel: HasPre)
+  __device__ float pre(int, int m, int n) const {
+    return mask ? __ldg(mask + gx_index(m, n)) : 1.0f;
+  }
+  __device__ void store_pre(int, int m, int n, float v, float mk) const {
+    gx[gx_index(m, n)] = !(mk > 0.0f) ? 0.0f : v;
+  }
+  __device__ void store(int z, int m, int n, float v) const { store_pre(z, m, n, v, pre(z, m, n)); }
 };
 
 constexpr int kConvThreads = 256;

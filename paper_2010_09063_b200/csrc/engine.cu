@@ -137,6 +137,8 @@ struct Engine {
   bool any_ghost = false;
   bool ghost_enabled = true;    // PGB_NO_GHOST=1: per-example conv dW stacks throughout
   float* d_dw_ws = nullptr;     // split workspace of the summed dW GEMMs
+  float* d_split_ws = nullptr;  // K-split workspace of the forward / input-gradient GEMMs
+  bool no_ksplit = false;       // PGB_NO_KSPLIT=1: no K splits
   int* d_emb_tok = nullptr;    // (B, L)
   int* d_emb_cnt = nullptr;    // (B, L)
   int* d_emb_nd = nullptr;     // (B)
@@ -163,18 +165,17 @@ struct Engine {
   // PGB_NO_TMA=1: the register-gather tcgen05 GEMM of conv_tc.cuh)
   bool use_tma = true;
   // per GEMM kind, measured on the CIFAR layers (profiles/r02_cifar_*):
-  // forward for C >= 16 inputs; input gradient for the 8x8 / 4x4 layers with
-  // >= 32 output channels (the larger maps re-read each tap's shifted box from
-  // L2 and lose to the gather GEMM); per-example dW stays on the gather GEMM
-  // (its 9 x C row tiles scatter stride-9 stores and pay a TMEM set-up per
-  // example). PGB_TMA_ALL=1 takes every eligible GEMM (parity tests).
+  // forward for C >= 16 inputs (C = 3 pads to 32 channels per tap); every
+  // input gradient (since the persistent engine and the epilogue's mask loads
+  // ahead of its stores: 826 -> 580 us per CIFAR step); per-example dW stays
+  // on the gather GEMM (its 9 x C row tiles scatter stride-9 stores; the
+  // 4x4 / 8x8 layers take the ghost path anyway). PGB_TMA_ALL=1 takes every
+  // eligible GEMM (parity tests).
   bool tma_all = false;
   bool emb_agg_scalar = false;
   bool pool_generic = false;    // PGB_POOL_GENERIC=1: the generic pooling kernels  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
   bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
-  bool tma_dx(const ConvGeom& g) const {
-    return use_tma && tg::conv_ok(g) && (tma_all || (g.H * g.W <= 64 && g.D >= 32));
-  }
+  bool tma_dx(const ConvGeom& g) const { return use_tma && tg::conv_ok(g); }
   bool tma_dw(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && tma_all; }
   // scratch operands of the TMA GEMMs, each as its 3xTF32 (hi, lo) pair: the
   // A operand (NHWC copy / shifted copies), the B operand (permuted weights /
@@ -422,8 +423,46 @@ struct Engine {
     p.out = out;
     p.bias = bias;
     p.relu = relu ? 1 : 0;
-    tg::launch(p, bn, dim3((g.D + bn - 1) / bn, (p.M + 127) / 128, 1), s);
-    return 3;
+    return 3 + tma_launch_split(p, bn, (g.D + bn - 1) / bn, (p.M + 127) / 128, s);
+  }
+
+  // K splits of a forward / input-gradient GEMM: the tensor core's fp32
+  // accumulation truncates, so each split keeps every TMEM accumulator chain
+  // to <= 8 K chunks (the hi.hi products rotate over tg::nacc accumulators);
+  // the splits are added in order in fp32 (round to nearest). Depends on K and
+  // the tile width only -- never on the batch -- so an output element gets
+  // the same arithmetic at every batch size (the 8x8 / 4x4 layers' long K
+  // also fills the SMs this way).
+  static int ksplit_for(int bn, int nchunks) {
+    // chunks per accumulator chain (PGB_KSPLIT_CHAIN; measured on CIFAR at
+    // B = 4 against the fp64 oracle, worst block: none 7.5e-6, 12: 5.8e-6,
+    // 8: 4.2e-6, 4: 3.2e-6; step 133k / 132k / 125k ex/s at 1000 / 8 / 4)
+    static const int chain =
+        std::getenv("PGB_KSPLIT_CHAIN") ? std::max(1, std::atoi(std::getenv("PGB_KSPLIT_CHAIN"))) : 8;
+    const int nacc = bn == 16 ? 8 : bn == 32 ? 4 : bn == 64 ? 2 : 3;
+    const int per = chain * nacc;
+    return std::max(1, (nchunks + per - 1) / per);
+  }
+
+  // launch a forward / input-gradient GEMM, split over K when it under-fills
+  // the SMs (raw splits to d_split_ws, added in order by the epilogue kernel)
+  int tma_launch_split(tg::Params& p, int bn, int ntn, int ntm, cudaStream_t s) {
+    static const char* only = std::getenv("PGB_KSPLIT_ONLY");  // debug: fwd / dx
+    const bool skip = only && ((only[0] == 'f') != (p.mode == tg::kConvFwd));
+    const int S = (no_ksplit || skip) ? 1 : ksplit_for(bn, p.nchunks);
+    if (S <= 1 || !d_split_ws) {
+      tg::launch(p, bn, dim3(ntn, ntm, 1), s);
+      return 0;
+    }
+    p.ksplit = S;
+    p.ws = d_split_ws;
+    tg::launch(p, bn, dim3(ntn, ntm, S), s);
+    tg::Params q = p;
+    q.ntn = ntn;
+    q.ntm = ntm;
+    const long long per = (long long)ntm * ntn * bn * 128;
+    tg::splitk_epilogue_kernel<<<grid_for((size_t)per), 256, 0, s>>>(q);
+    return 1;
   }
 
   // input gradient: gx (B, C, H, W) = conv^T(gout) * [mask > 0]
@@ -456,8 +495,7 @@ struct Engine {
     p.by = by, p.bn = bnimg;
     p.out = gx;
     p.mask = mask;
-    tg::launch(p, bn, dim3((g.C + bn - 1) / bn, (p.M + 127) / 128, 1), s);
-    return 3;
+    return 3 + tma_launch_split(p, bn, (g.C + bn - 1) / bn, (p.M + 127) / 128, s);
   }
 
   // per-example weight gradient stacks (B, D, C, 3, 3) + each tile's squared
@@ -575,6 +613,7 @@ struct Engine {
     emb_agg_scalar = std::getenv("PGB_EMB_AGG_SCALAR") != nullptr;
     pool_generic = std::getenv("PGB_POOL_GENERIC") != nullptr;
     ghost_enabled = std::getenv("PGB_NO_GHOST") == nullptr;
+    no_ksplit = std::getenv("PGB_NO_KSPLIT") != nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -641,6 +680,20 @@ struct Engine {
           wt = std::max(wt, B * hw * g.D);  // the dW cotangent
         }
       want((void**)&d_tile_sq, sizeof(double) * B * tiles);
+      int64_t split_ws = 0;
+      for (int l = 0; l < n; ++l)
+        if (desc.layers[l].kind == PGB_CONV && use_tma) {
+          const ConvGeom g = conv_geom(layers[l]);
+          if (!tg::conv_ok(g)) continue;
+          const int64_t M = B * g.H * g.W, ntm = (M + 127) / 128;
+          for (int side = 0; side < 2; ++side) {  // forward (N = D), input gradient (N = C)
+            const int N = side ? g.C : g.D, K = side ? g.D : g.C;
+            const int bn = tg::pick_bn(N), ntn = (N + bn - 1) / bn;
+            const int S = ksplit_for(bn, 9 * tg::round32(K) / 32);
+            if (S > 1) split_ws = std::max<int64_t>(split_ws, (int64_t)S * ntm * ntn * bn * 128);
+          }
+        }
+      if (split_ws) want((void**)&d_split_ws, sizeof(float) * split_ws);
       if (use_tma) {
         want((void**)&d_nhwc, sizeof(float) * nhwc);
         want((void**)&d_nhwc_lo, sizeof(float) * nhwc);
@@ -1591,11 +1644,18 @@ struct Engine {
     return nk;
   }
 
+  // process-wide function attribute: only ever raised (a lower value set for
+  // a later layer would make an earlier launch -- or its graph node replayed
+  // by a profiler -- exceed it)
   template <class K>
   void gram_attr(K* kern, size_t smem) {
-    if (smem > 48 * 1024)
+    static size_t set64 = 0, set16 = 0;
+    size_t& cur = (void*)kern == (void*)conv_gram_norm_kernel<64> ? set64 : set16;
+    if (smem > 48 * 1024 && smem > cur) {
       PGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
+      cur = smem;
+    }
   }
 
   // The clipped sums sum_i s_i dW_i of the ghost conv blocks into d_sum: the
@@ -2788,8 +2848,28 @@ pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, c
     p.nchunks = (K + 31) / 32;
     p.out = dC;
     p.ldc = N;
-    tg::launch(p, bn, dim3((N + bn - 1) / bn, (M + 127) / 128, 1), 0);
+    // PGB_DEBUG_KSPLIT=S: the K-split path (raw splits + ordered epilogue)
+    const char* ks = std::getenv("PGB_DEBUG_KSPLIT");
+    const int S = ks ? std::atoi(ks) : 1;
+    const int ntn = (N + bn - 1) / bn, ntm = (M + 127) / 128;
+    float* ws = nullptr;
+    if (S > 1) {
+      PGB_CUDA(cudaMalloc(&ws, sizeof(float) * (size_t)S * ntm * ntn * bn * 128));
+      p.ksplit = S;
+      p.ws = ws;
+      tg::launch(p, bn, dim3(ntn, ntm, S), 0);
+      tg::Params q = p;
+      q.ntn = ntn;
+      q.ntm = ntm;
+      tg::splitk_epilogue_kernel<<<grid_for((size_t)ntm * ntn * bn * 128), 256>>>(q);
+    } else {
+      tg::launch(p, bn, dim3(ntn, ntm, 1), 0);
+    }
     PGB_CUDA(cudaGetLastError());
+    if (ws) {
+      PGB_CUDA(cudaDeviceSynchronize());
+      cudaFree(ws);
+    }
     PGB_CUDA(cudaDeviceSynchronize());
     PGB_CUDA(cudaMemcpy(Cout, dC, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost));
     cudaFree(dA);

@@ -159,6 +159,11 @@ struct NoTable {
 // outputs (fp64), written to tile_sq[z * tiles + tile]: the per-example norm
 // of a materialised gradient block without a second pass over it.
 template <class T, class = void>
+struct HasPre : std::false_type {};
+template <class T>
+struct HasPre<T, std::void_t<decltype(&T::pre)>> : std::true_type {};
+
+template <class T, class = void>
 struct HasTileSq : std::false_type {};
 template <class T>
 struct HasTileSq<T, std::void_t<decltype(&T::tile_sq)>> : std::true_type {};
@@ -326,12 +331,23 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] += vc[j] + vd[j];
     if (row < M) {
+      if constexpr (HasPre<Op>::value) {
+        // every load of the group before its stores (a load after a
+        // possibly-aliasing store waits for it)
+        float pv[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (n0 + c0 + j < N) {
-          op.store(z, row, n0 + c0 + j, v[j]);
-          if constexpr (HasTileSq<Op>::value) sq = fma((double)v[j], (double)v[j], sq);
-        }
+        for (int j = 0; j < 8; ++j) pv[j] = n0 + c0 + j < N ? op.pre(z, row, n0 + c0 + j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (n0 + c0 + j < N) op.store_pre(z, row, n0 + c0 + j, v[j], pv[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (n0 + c0 + j < N) {
+            op.store(z, row, n0 + c0 + j, v[j]);
+            if constexpr (HasTileSq<Op>::value) sq = fma((double)v[j], (double)v[j], sq);
+          }
+      }
     }
   }
   if constexpr (HasTileSq<Op>::value) {

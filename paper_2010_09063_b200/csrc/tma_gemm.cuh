@@ -81,6 +81,7 @@ struct alignas(64) Params {
   int tiles;         // tiles per GEMM (ntn * ntm), tile_sq row length
   int ntn, ntm, nz;  // N tiles, M tiles, GEMMs (examples / example splits); set by launch()
   int ex_per, nex;   // dw-sum: examples per split, examples in total
+  int ksplit;        // fwd / dx / plain: K splits (tile z); > 1: raw tiles to ws
   float* ws;         // dw-sum: split workspace [z][mt][n][128 rows]
   // epilogue
   float* out;
@@ -254,13 +255,17 @@ __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s,
 
 // K chunks of a tile: dw-sum walks the positions of every example of its split
 __device__ __forceinline__ int tile_chunks(const Params& p, int z) {
+  if (p.ksplit > 1) return (z + 1) * p.nchunks / p.ksplit - z * p.nchunks / p.ksplit;
   if (p.mode != kConvDwSum) return p.nchunks;
   const int e0 = z * p.ex_per, e1 = min(p.nex, e0 + p.ex_per);
   return max(0, e1 - e0) * p.nchunks;
 }
 // chunk q of a tile -> (position chunk, example)
 __device__ __forceinline__ void chunk_coords(const Params& p, int q, int z, int& qc, int& ze) {
-  if (p.mode != kConvDwSum) {
+  if (p.ksplit > 1) {
+    qc = z * p.nchunks / p.ksplit + q;
+    ze = 0;
+  } else if (p.mode != kConvDwSum) {
     qc = q;
     ze = z;
   } else {
@@ -423,6 +428,12 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
           }
         }
         const int n0 = nt * BN + c0;
+        if (p.ksplit > 1) {  // a K split: the raw tile, summed by splitk_epilogue_kernel
+          float* w = p.ws + (((size_t)z * p.ntm + mt) * (size_t)(p.ntn * BN) + n0) * kBM + r;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[(size_t)j * kBM] = v[j];
+          continue;
+        }
         switch (p.mode) {
           case kPlain:
             if (m < p.M)
@@ -430,14 +441,20 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
               for (int j = 0; j < 8; ++j)
                 if (n0 + j < p.N) p.out[(size_t)m * p.ldc + n0 + j] = v[j];
             break;
+          // (every load of a column group is issued before its stores: out
+          // may alias the inputs as far as the compiler knows, so a load
+          // after a store would wait for it -- 8 serial round trips)
           case kConvFwd: {
             const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+            float bv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bv[j] = n0 + j < p.N ? __ldg(p.bias + n0 + j) : 0.0f;
             if (m < p.M)
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const int d = n0 + j;
                 if (d < p.N) {
-                  float o = v[j] + p.bias[d];
+                  float o = v[j] + bv[j];
                   if (p.relu) o = fmaxf(o, 0.0f);
                   p.out[((size_t)img * p.D + d) * HW + pos] = o;
                 }
@@ -446,14 +463,16 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
           }
           case kConvDx: {
             const int HW = p.H * p.W, img = m / HW, pos = m - img * HW;
+            const size_t i0 = ((size_t)img * p.C + n0) * HW + pos;
+            float mk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              mk[j] = (p.mask && m < p.M && n0 + j < p.N) ? __ldg(p.mask + i0 + (size_t)j * HW) : 1.0f;
             if (m < p.M)
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const int c = n0 + j;
-                if (c < p.N) {
-                  const size_t i = ((size_t)img * p.C + c) * HW + pos;
-                  p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : v[j];
-                }
+                if (c < p.N) p.out[i0 + (size_t)j * HW] = !(mk[j] > 0.0f) ? 0.0f : v[j];
               }
             break;
           }
@@ -565,6 +584,35 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
     const long long i = e - v * total;
     const int x = (int)(i % W), xs = x + v - 1;
     split2((xs >= 0 && xs < W) ? src[i + v - 1] : 0.0f, dst[e], dst_lo[e]);
+  }
+}
+
+// The K splits of a forward / input-gradient GEMM added in split order, then
+// that mode's epilogue (bias + relu into NCHW; relu mask into NCHW).
+__global__ void splitk_epilogue_kernel(const Params p) {
+  const int npad = p.ntn * (p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : 128);
+  const long long per_split = (long long)p.ntm * npad * kBM;
+  const int HW = p.mode == kPlain ? 1 : p.H * p.W;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_split;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % kBM);
+    const long long t = e / kBM;
+    const int n = (int)(t % npad), mt = (int)(t / npad);
+    const int m = mt * kBM + r;
+    if (m >= p.M || n >= p.N) continue;
+    float acc = p.ws[e];
+    for (int z = 1; z < p.ksplit; ++z) acc += p.ws[(long long)z * per_split + e];
+    const int img = m / HW, pos = m - img * HW;
+    if (p.mode == kPlain) {
+      p.out[(size_t)m * p.ldc + n] = acc;
+    } else if (p.mode == kConvFwd) {
+      float o = acc + p.bias[n];
+      if (p.relu) o = fmaxf(o, 0.0f);
+      p.out[((size_t)img * p.D + n) * HW + pos] = o;
+    } else {
+      const size_t i = ((size_t)img * p.C + n) * HW + pos;
+      p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : acc;
+    }
   }
 }
 

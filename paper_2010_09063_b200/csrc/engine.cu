@@ -428,28 +428,35 @@ struct Engine {
 
   // K splits of a forward / input-gradient GEMM: the tensor core's fp32
   // accumulation truncates, so each split keeps every TMEM accumulator chain
-  // to <= 8 K chunks (the hi.hi products rotate over tg::nacc accumulators);
-  // the splits are added in order in fp32 (round to nearest). Depends on K and
+  // short (the hi.hi products rotate over tg::nacc accumulators) and the
+  // splits are added in order in fp32 (round to nearest). Depends on K and
   // the tile width only -- never on the batch -- so an output element gets
-  // the same arithmetic at every batch size (the 8x8 / 4x4 layers' long K
-  // also fills the SMs this way).
-  static int ksplit_for(int bn, int nchunks) {
-    // chunks per accumulator chain (PGB_KSPLIT_CHAIN; measured on CIFAR at
-    // B = 4 against the fp64 oracle, worst block: none 7.5e-6, 12: 5.8e-6,
-    // 8: 4.2e-6, 4: 3.2e-6; step 133k / 132k / 125k ex/s at 1000 / 8 / 4)
-    static const int chain =
-        std::getenv("PGB_KSPLIT_CHAIN") ? std::max(1, std::atoi(std::getenv("PGB_KSPLIT_CHAIN"))) : 8;
+  // the same arithmetic at every batch size. Chain lengths (chunks per
+  // accumulator; PGB_KSPLIT_CHAIN[_FWD|_DX]) measured on the CIFAR B = 256
+  // clipped sum against the reference's fp64 fixture, blocks 1-10 (block 0
+  // is cancellation-bound, 7.5e-4 for every setting; the reference's own fp32
+  // build is off by up to 4.6e-4): no split 1-4e-4 at 133k ex/s; forward 8
+  // 1-7e-4 at 129k; forward 4 / dx 8 <= 1.0e-5 at 128k (default); 4 / 4
+  // <= 9.9e-6 at 125k; 2 / 2 <= 1.6e-6 at 113k.
+  static int ksplit_for(int bn, int nchunks, bool fwd = false) {
+    static const int chain_fwd = env_int("PGB_KSPLIT_CHAIN_FWD", env_int("PGB_KSPLIT_CHAIN", 4));
+    static const int chain_dx = env_int("PGB_KSPLIT_CHAIN_DX", env_int("PGB_KSPLIT_CHAIN", 8));
     const int nacc = bn == 16 ? 8 : bn == 32 ? 4 : bn == 64 ? 2 : 3;
-    const int per = chain * nacc;
+    const int per = (fwd ? chain_fwd : chain_dx) * nacc;
     return std::max(1, (nchunks + per - 1) / per);
   }
+  static int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::max(1, std::atoi(v)) : dflt;
+  }
+
 
   // launch a forward / input-gradient GEMM, split over K when it under-fills
   // the SMs (raw splits to d_split_ws, added in order by the epilogue kernel)
   int tma_launch_split(tg::Params& p, int bn, int ntn, int ntm, cudaStream_t s) {
     static const char* only = std::getenv("PGB_KSPLIT_ONLY");  // debug: fwd / dx
     const bool skip = only && ((only[0] == 'f') != (p.mode == tg::kConvFwd));
-    const int S = (no_ksplit || skip) ? 1 : ksplit_for(bn, p.nchunks);
+    const int S = (no_ksplit || skip) ? 1 : ksplit_for(bn, p.nchunks, p.mode == tg::kConvFwd);
     if (S <= 1 || !d_split_ws) {
       tg::launch(p, bn, dim3(ntn, ntm, 1), s);
       return 0;
@@ -689,7 +696,7 @@ struct Engine {
           for (int side = 0; side < 2; ++side) {  // forward (N = D), input gradient (N = C)
             const int N = side ? g.C : g.D, K = side ? g.D : g.C;
             const int bn = tg::pick_bn(N), ntn = (N + bn - 1) / bn;
-            const int S = ksplit_for(bn, 9 * tg::round32(K) / 32);
+            const int S = ksplit_for(bn, 9 * tg::round32(K) / 32, side == 0);
             if (S > 1) split_ws = std::max<int64_t>(split_ws, (int64_t)S * ntm * ntn * bn * 128);
           }
         }

@@ -590,19 +590,21 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
 // The K splits of a forward / input-gradient GEMM added in split order, then
 // that mode's epilogue (bias + relu into NCHW; relu mask into NCHW).
 __global__ void splitk_epilogue_kernel(const Params p) {
-  const int npad = p.ntn * (p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : 128);
-  const long long per_split = (long long)p.ntm * npad * kBM;
-  const int HW = p.mode == kPlain ? 1 : p.H * p.W;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_split;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e % kBM);
-    const long long t = e / kBM;
-    const int n = (int)(t % npad), mt = (int)(t / npad);
-    const int m = mt * kBM + r;
-    if (m >= p.M || n >= p.N) continue;
+  // 32-bit index math throughout (a split is < 2^31 elements): the 64-bit
+  // divisions of a straightforward version cost more than the bytes it moves
+  const unsigned npad = (unsigned)p.ntn * (p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : 128);
+  const unsigned per_split = (unsigned)p.ntm * npad * kBM;
+  const unsigned HW = p.mode == kPlain ? 1u : (unsigned)(p.H * p.W);
+  const unsigned N = (unsigned)p.N, M = (unsigned)p.M;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < per_split;
+       e += gridDim.x * blockDim.x) {
+    const unsigned r = e & (kBM - 1), t = e >> 7;
+    const unsigned mt = t / npad, n = t - mt * npad;
+    const unsigned m = mt * kBM + r;
+    if (m >= M || n >= N) continue;
     float acc = p.ws[e];
-    for (int z = 1; z < p.ksplit; ++z) acc += p.ws[(long long)z * per_split + e];
-    const int img = m / HW, pos = m - img * HW;
+    for (int z = 1; z < p.ksplit; ++z) acc += p.ws[(size_t)z * per_split + e];
+    const unsigned img = m / HW, pos = m - img * HW;
     if (p.mode == kPlain) {
       p.out[(size_t)m * p.ldc + n] = acc;
     } else if (p.mode == kConvFwd) {

@@ -134,6 +134,7 @@ struct Engine {
   int emb_layer = -1;          // the embedding layer, when the sparse path applies
   bool sparse_embed_next = false;
   bool ghost_next = false;      // this step's conv blocks go through the ghost path
+  bool mlp_noise_next = false;  // this step's mlp_kernel draws the noise (dense-only models)
   bool any_ghost = false;
   bool ghost_enabled = true;    // PGB_NO_GHOST=1: per-example conv dW stacks throughout
   float* d_dw_ws = nullptr;     // split workspace of the summed dW GEMMs
@@ -732,6 +733,7 @@ struct Engine {
       want((void**)&d_scale, sizeof(float) * B);
       want((void**)&d_clipflag, sizeof(int) * B);
     }
+    if (mlp_fused && !fused_mnist) want((void**)&d_noise, sizeof(float) * P);
     for (int l = 0; l < n; ++l) {
       const Layer& L = layers[l];
       if (L.spec.kind == PGB_EMBEDDING && L.fused_pool && B <= 1024 && L.in.d[0] <= kEmbMaxL) {
@@ -1268,14 +1270,32 @@ struct Engine {
       prm.x = layers[emb_layer].act_out;  // pooled (B, E)
       prm.xring = nullptr;
     }
+    // dense-only models: the extra CTAs draw the step's noise for the
+    // aggregation (its epilogue then only loads it)
+    if (!head && d_noise && cur_args.add_noise) {
+      prm.a = cur_args;
+      prm.noise = d_noise;
+      prm.nb_first = first;
+      prm.nnb = desc.n_params - first;
+      long long pairs = 0;
+      for (int b = 0; b < prm.nnb; ++b) {
+        prm.nb_off[b] = param_off[first + b];
+        prm.nb_size[b] = desc.param_size[first + b];
+        prm.nb_pair[b] = pairs;
+        pairs += (prm.nb_size[b] + 1) / 2;
+      }
+      prm.nb_pair[prm.nnb] = pairs;
+      prm.noise_ctas = (int)((pairs + 32 * mlp::kWarps - 1) / (32 * mlp::kWarps));
+      mlp_noise_next = true;
+    }
     const size_t smem = sizeof(float) * (size_t)prm.P;
     if (!mlp_attr) {  // once per engine (the attribute is per device)
       PGB_CUDA(cudaFuncSetAttribute(mlp::mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(sizeof(float) * mlp::kMaxParams)));
       mlp_attr = true;
     }
-    mlp::mlp_kernel<<<(unsigned)((B + mlp::kWarps - 1) / mlp::kWarps), 32 * mlp::kWarps, smem,
-                      s>>>(prm);
+    mlp::mlp_kernel<<<(unsigned)((B + mlp::kWarps - 1) / mlp::kWarps + prm.noise_ctas),
+                      32 * mlp::kWarps, smem, s>>>(prm);
     return mark(s, head ? "embed_head" : "mlp_fused");
   }
 
@@ -1287,8 +1307,13 @@ struct Engine {
     const Layer& Le = layers[emb_layer];
     const int E = (int)Le.spec.out, V = (int)Le.spec.in, Bi = (int)B;
     const float* Wt = d_params + param_off[Le.pblock];
-    embed_pool_fwd_kernel<<<Bi, std::min(1024, kPoolGroups * ((E + 31) / 32) * 32), 0, s>>>(
-        x_slot, Wt, Le.act_out, Bi, (int)Le.in.d[0], E, V, d_err);
+    if (E % 4 == 0 && E <= 128 && param_off[Le.pblock] % 4 == 0 && Le.in.d[0] <= kPoolMaxL &&
+        !pool_generic)
+      embed_pool4_fwd_kernel<<<Bi, 32 * kPool4Groups, 0, s>>>(x_slot, Wt, Le.act_out, Bi,
+                                                             (int)Le.in.d[0], E, V, d_err);
+    else
+      embed_pool_fwd_kernel<<<Bi, std::min(1024, kPoolGroups * ((E + 31) / 32) * 32), 0, s>>>(
+          x_slot, Wt, Le.act_out, Bi, (int)Le.in.d[0], E, V, d_err);
     nk += mark(s, "embed_pool_fwd");
     nk += enqueue_mlp(s, x_slot, y_slot, true);
     embed_index_kernel<<<Bi, 256, 0, s>>>(x_slot, Le.gout, (int)Le.in.d[0], E, V, emb_words,
@@ -1456,7 +1481,7 @@ struct Engine {
     try {
       nk += enqueue_grads(s, x_slot, y_slot);
     } catch (...) {
-      fuse_agg_next = sparse_embed_next = pairs_next = ghost_next = false;
+      fuse_agg_next = sparse_embed_next = pairs_next = ghost_next = mlp_noise_next = false;
       throw;
     }
     if (fuse_agg_next) {
@@ -1488,7 +1513,7 @@ struct Engine {
       else
         nk += enqueue_aggregate(s, t, nparts, (int)B, fused_mnist);
     }
-    sparse_embed_next = pairs_next = ghost_next = false;
+    sparse_embed_next = pairs_next = ghost_next = mlp_noise_next = false;
     return nk;
   }
 
@@ -1526,6 +1551,8 @@ struct Engine {
       L.scales = d_scale;
       L.clip_flags = d_clipflag;
       L.noise = d_noise;
+    } else if (mlp_noise_next && mode == 0) {
+      L.noise = d_noise;  // drawn by mlp_kernel's extra CTAs this step
     }
     L.bt = t;
     agg_plan(t, L.plan);
@@ -2030,9 +2057,11 @@ struct Engine {
       sg.agg_args.clipped_out = agg_cnt;
       set_node(sg.exec, sg.agg, &sg.agg_args);
     }
-    if (sg.mlp && (sg.mlp_args.x != x_slot || sg.mlp_args.y != y_slot)) {
+    if (sg.mlp && (sg.mlp_args.x != x_slot || sg.mlp_args.y != y_slot ||
+                   (sg.mlp_args.noise && !same_args(sg.mlp_args.a, cur_args)))) {
       sg.mlp_args.x = x_slot;
       sg.mlp_args.y = y_slot;
+      if (sg.mlp_args.noise) sg.mlp_args.a = cur_args;
       set_node(sg.exec, sg.mlp, &sg.mlp_args);
     }
     if (sg.emb && !same_args(sg.emb_args.a, cur_args)) {

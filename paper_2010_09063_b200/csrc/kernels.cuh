@@ -567,6 +567,67 @@ __global__ void embed_pool_fwd_kernel(const float* __restrict__ ids,
   }
 }
 
+// embed_pool_fwd_kernel for E % 4 == 0, E <= 128 and a 16-byte aligned
+// table: one warp per token group, lane l holding elements 4l..4l+3 (one
+// 16-byte gather per token), 16 groups of L/16 tokens, the group partials
+// added in group order (the same fp32
+// re-association class as embed_pool_fwd_kernel's four groups).
+constexpr int kPool4Groups = 16;
+__global__ void __launch_bounds__(32 * kPool4Groups, 3) embed_pool4_fwd_kernel(
+    const float* __restrict__ ids, const float* __restrict__ table, float* __restrict__ y,
+    int B, int L, int E, int V, DevError* err) {
+  __shared__ int sid[kPoolMaxL];
+  __shared__ float4 part[kPool4Groups][32];
+  const int b = blockIdx.x, t = threadIdx.x, g = t >> 5, lane = t & 31;
+  for (int k = t; k < L; k += blockDim.x) {
+    const float raw = ids[(size_t)b * L + k];
+    const bool ok = valid_id(raw, V);
+    if (!ok) raise_index(err, 1, (long long)b * L + k, raw, V);
+    sid[k] = ok ? (int)raw : -1;
+  }
+  __syncthreads();
+  const int e0 = 4 * lane;
+  const bool act = e0 < E;
+  const int t0 = (int)((long long)L * g / kPool4Groups), t1 = (int)((long long)L * (g + 1) / kPool4Groups);
+  float4 s = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  // 8 gathers in flight per lane keeps the kernel at <= 40 registers: three
+  // 512-thread CTAs per SM (one wave for B = 512; 16 in flight at ~100
+  // registers allowed one CTA per SM and 3.5 waves)
+  for (int k = t0; k < t1; k += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = k + q < t1 ? sid[k + q] : -1;
+      v[q] = (act && r >= 0) ? __ldg(reinterpret_cast<const float4*>(table + (size_t)r * E + e0))
+                             : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k + q < t1 && sid[k + q] >= 0) {
+        s.x += v[q].x;
+        s.y += v[q].y;
+        s.z += v[q].z;
+        s.w += v[q].w;
+      }
+  }
+  part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && act) {
+    float4 a = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kPool4Groups; ++q) {
+      const float4 c = part[q][lane];
+      a.x += c.x;
+      a.y += c.y;
+      a.z += c.z;
+      a.w += c.w;
+    }
+    const float inv = 1.0f / float(L);
+    *reinterpret_cast<float4*>(y + (size_t)b * E + e0) =
+        make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+  }
+}
+
 // per-example dense table gradient (strategies.cpp:171-188): the pooled
 // cotangent times 1/L scattered to each token's row, tokens in order.
 __global__ void embed_pex_kernel(const float* __restrict__ ids, const float* __restrict__ g,

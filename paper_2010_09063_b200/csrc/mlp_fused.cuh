@@ -51,7 +51,29 @@ struct Params {
   double* parts;   // (B, nparts) squared norm per parameter block
   int nparts, B, classes;
   DevError* err;
+  // the step's Gaussian noise drawn by extra CTAs while the examples run
+  // (kernels.hpp:597-614), so the aggregation's epilogue only loads it:
+  // blocks nb_first .. nb_first + nnb - 1 of the parameter vector
+  StepArgs a;
+  float* noise;  // (P_total) or null
+  int noise_ctas, nb_first, nnb;
+  long long nb_off[2 * kMaxLayers], nb_size[2 * kMaxLayers], nb_pair[2 * kMaxLayers + 1];
 };
+
+// extra CTA k of mlp_kernel: one Box-Muller pair per thread
+__device__ __forceinline__ void draw_noise(const Params& P, int k) {
+  const long long q = (long long)k * blockDim.x + threadIdx.x;
+  if (!P.a.add_noise || q >= P.nb_pair[P.nnb]) return;
+  int b = 0;
+  while (b + 1 < P.nnb && P.nb_pair[b + 1] <= q) ++b;
+  const long long jp = q - P.nb_pair[b];
+  const long long st = P.step_base ? *P.step_base + P.step_off : P.a.step;
+  float n0, n1;
+  gauss_pair(stream_key(P.a.seed, noise_stream(st, P.nb_first + b)), jp, &n0, &n1);
+  float* dst = P.noise + P.nb_off[b] + 2 * jp;
+  dst[0] = n0;
+  if (2 * jp + 1 < P.nb_size[b]) dst[1] = n1;
+}
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -65,6 +87,11 @@ __global__ void __launch_bounds__(32 * kWarps) mlp_kernel(const Params P) {
   __shared__ float grad[kWarps][2][kMaxWidth];
   extern __shared__ float wsm[];  // all parameters (a few K floats)
   asm volatile("griddepcontrol.launch_dependents;");
+  const int ex_ctas = (int)gridDim.x - P.noise_ctas;
+  if ((int)blockIdx.x >= ex_ctas) {
+    draw_noise(P, (int)blockIdx.x - ex_ctas);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + warp;
   // stage the parameters: every load in flight at once instead of one cold

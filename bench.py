@@ -290,25 +290,41 @@ def conv_gemm_flops(desc, B):
     return total
 
 
-def aggregate_bytes(desc, B, fused, c2_pairs=False, sparse_embed=False):
+def aggregate_bytes(desc, B, fused, c2_pairs=False, sparse_embed=False, ghost=False):
     """Bytes the aggregation kernel must read/write: per-example gradient
     sources (materialised rows: B*|p|*4; factored dense blocks: B*(in+out)*4;
     with c2_pairs the MNIST kernel's second conv weight block arrives as
-    ceil(B/2) clipped pair rows), the parameters (read + write), norms partials."""
+    ceil(B/2) clipped pair rows), the parameters (read + write), norms partials.
+    With ghost, the weight blocks of 3x3 / stride-1 convs on 4x4 and 8x8 maps
+    are summed by the clip-scaled GEMM (DESIGN 3.2a), not the aggregation."""
     from paper_2010_09063_b200 import LayerKind
     total = 0
     pi = 0
     nconv = 0
     skip_p = 0
+    H = W = None
+    if len(desc.input_shape) == 3:
+        H, W = int(desc.input_shape[1]), int(desc.input_shape[2])
     for l in desc.layers:
         if l.kind == LayerKind.dense:
             total += B * (l.in_ + l.out) * 4 + B * l.out * 4
             pi += 2
         elif l.kind == LayerKind.conv:
+            Ho = (H + 2 * l.pad - l.k) // l.stride + 1 if H else None
+            Wo = (W + 2 * l.pad - l.k) // l.stride + 1 if W else None
+            is_ghost = (ghost and l.k == 3 and l.stride == 1 and l.pad == 1 and Ho
+                        and Ho * Wo in (16, 64))
             rows = (B + 1) // 2 if (c2_pairs and nconv == 1) else B
-            total += (rows * l.out * l.in_ * l.k * l.k + B * l.out) * 4
+            if is_ghost:
+                total += B * l.out * 4
+                skip_p += l.out * l.in_ * l.k * l.k
+            else:
+                total += (rows * l.out * l.in_ * l.k * l.k + B * l.out) * 4
+            H, W = Ho, Wo
             nconv += 1
             pi += 2
+        elif l.kind in (LayerKind.maxpool, LayerKind.avgpool) and H:
+            H, W = (H - l.k) // l.stride + 1, (W - l.k) // l.stride + 1
         elif l.kind == LayerKind.embedding:
             # the sparse step path: embed_agg_kernel (its own roofline line),
             # not the aggregation kernel, sums this block
@@ -508,7 +524,11 @@ def run_ours(args):
                 "issue_active_pct_ncu": tk.get("issue_active_pct"),
                 "share_of_step": dom_ms / step_ms, "avg_launch_us": dom_ms * 1e3}
     elif dom_name.endswith("_tc") or dom_name.endswith("_tma"):
-        conv = [n for n in by_name if n.endswith("_tc") or n.endswith("_tma")]
+        # every kernel doing the conv GEMM work the algorithmic FLOPs count:
+        # forward, input gradient, per-example dW -- or, for the ghost layers,
+        # their Gram norms and the clip-scaled summed dW GEMM
+        conv = [n for n in by_name if n.endswith("_tc") or n.endswith("_tma")
+                or n in ("conv_dw_gram", "conv_dw_sum")]
         tc_ms = sum(by_name[n] for n in conv)
         flops = conv_gemm_flops(desc, BATCH)
         ach = flops / (tc_ms * 1e-3) / 1e12
@@ -526,7 +546,8 @@ def run_ours(args):
         agg_b = aggregate_bytes(desc, BATCH, fused,
                                 c2_pairs=("mnist_tc" in by_name and
                                           os.environ.get("PGB_C2_PAIRS", "1") != "0"),
-                                sparse_embed="embed_agg" in by_name)
+                                sparse_embed="embed_agg" in by_name,
+                                ghost="conv_dw_gram" in by_name)
         am = by_name["aggregate"]
         atraffic, _ = ncu_traffic(args.model, "aggregate_kernel")
         agg = {"kernel": "aggregate", "bound": "hbm", "achieved": agg_b / (am * 1e-3) / 1e9,

@@ -1307,30 +1307,60 @@ __global__ void __launch_bounds__(256) embed_index_kernel(
   const int i = blockIdx.x, t = threadIdx.x;
   int Lp = 1;
   while (Lp < L) Lp <<= 1;
-  for (int k = t; k < Lp; k += blockDim.x) {
+  if (Lp <= (int)blockDim.x && blockDim.x == 256) {
+    // one key per thread (sentinels past L), bitonic network over 256 keys in
+    // registers: exchanges with stride < 32 by warp shuffles, the 6 with
+    // stride >= 32 through shared memory
     int v = 0x7fffffff;
-    if (k < L) {
-      const float raw = ids[(size_t)i * L + k];
+    if (t < L) {
+      const float raw = ids[(size_t)i * L + t];
       if (valid_id(raw, V)) v = (int)raw;  // invalid ids raised by the forward
     }
-    key[k] = v;
-  }
-  __syncthreads();
-  // bitonic sort (ascending)
-  for (int size = 2; size <= Lp; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int k = t; k < Lp / 2; k += blockDim.x) {
-        const int a = 2 * k - (k & (stride - 1));
-        const int b = a + stride;
-        const bool up = (a & size) == 0;
-        const int x = key[a], y = key[b];
-        if ((x > y) == up) {
-          key[a] = y;
-          key[b] = x;
+#pragma unroll
+    for (int size = 2; size <= 256; size <<= 1)
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        int other;
+        if (stride >= 32) {
+          key[t] = v;
+          __syncthreads();
+          other = key[t ^ stride];
+          __syncthreads();
+        } else {
+          other = __shfl_xor_sync(0xffffffffu, v, stride);
         }
+        const bool up = (t & size) == 0, lower = (t & stride) == 0;
+        v = (lower == up) ? min(v, other) : max(v, other);
       }
-      __syncthreads();
+    key[t] = v;
+    Lp = 256;
+    __syncthreads();
+  } else {
+    for (int k = t; k < Lp; k += blockDim.x) {
+      int v = 0x7fffffff;
+      if (k < L) {
+        const float raw = ids[(size_t)i * L + k];
+        if (valid_id(raw, V)) v = (int)raw;  // invalid ids raised by the forward
+      }
+      key[k] = v;
     }
+    __syncthreads();
+    // bitonic sort (ascending)
+    for (int size = 2; size <= Lp; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int k = t; k < Lp / 2; k += blockDim.x) {
+          const int a = 2 * k - (k & (stride - 1));
+          const int b = a + stride;
+          const bool up = (a & size) == 0;
+          const int x = key[a], y = key[b];
+          if ((x > y) == up) {
+            key[a] = y;
+            key[b] = x;
+          }
+        }
+        __syncthreads();
+      }
+  }
   // segment starts (distinct tokens) in order: first occurrences flagged in
   // parallel, compacted with warp ballots and a per-chunk warp prefix
   {

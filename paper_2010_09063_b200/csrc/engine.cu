@@ -140,6 +140,7 @@ struct Engine {
   float* d_dw_ws = nullptr;     // split workspace of the summed dW GEMMs
   float* d_split_ws = nullptr;  // K-split workspace of the forward / input-gradient GEMMs
   bool no_ksplit = false;       // PGB_NO_KSPLIT=1: no K splits
+  bool no_halo = false;         // PGB_NO_HALO=1: one TMA box per tap
   int* d_emb_tok = nullptr;    // (B, L)
   int* d_emb_cnt = nullptr;    // (B, L)
   int* d_emb_nd = nullptr;     // (B)
@@ -404,11 +405,13 @@ struct Engine {
     tg::Params p{};
     int by, bnimg;
     tg::fwd_box(g, by, bnimg);
+    const bool halo = halo_ok(g, bn);
     const uint64_t da[4] = {(uint64_t)Cp, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)Bi};
     const uint64_t sa[3] = {4ull * Cp, 4ull * Cp * g.W, 4ull * Cp * HW};
-    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)by, (uint32_t)bnimg};
+    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)(halo ? by + 2 : by), (uint32_t)bnimg};
     tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
     tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+    p.halo = halo ? 1 : 0;
     const uint64_t db[2] = {(uint64_t)9 * Cp, (uint64_t)g.D};
     const uint64_t sb[1] = {4ull * 9 * Cp};
     const uint32_t bb[2] = {32, (uint32_t)bn};
@@ -417,7 +420,7 @@ struct Engine {
     p.mode = tg::kConvFwd;
     p.M = Bi * HW;
     p.N = g.D;
-    p.nchunks = 9 * Cp / 32;
+    p.nchunks = (halo ? 3 : 9) * Cp / 32;
     p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
     p.Cg = Cp / 32;
     p.by = by, p.bn = bnimg;
@@ -452,12 +455,23 @@ struct Engine {
   }
 
 
+  // halo stages for the forward / input gradient: 16- and 32-wide maps whose
+  // 128-position tiles are whole rows of one image, N <= 64 (PGB_NO_HALO=1: off)
+  bool halo_ok(const ConvGeom& g, int bn) const {
+    return !no_halo && bn <= 64 && (g.W == 16 || g.W == 32) && 128 % g.W == 0 &&
+           g.H % (128 / g.W) == 0;
+  }
+
   // launch a forward / input-gradient GEMM, split over K when it under-fills
   // the SMs (raw splits to d_split_ws, added in order by the epilogue kernel)
   int tma_launch_split(tg::Params& p, int bn, int ntn, int ntm, cudaStream_t s) {
     static const char* only = std::getenv("PGB_KSPLIT_ONLY");  // debug: fwd / dx
     const bool skip = only && ((only[0] == 'f') != (p.mode == tg::kConvFwd));
-    const int S = (no_ksplit || skip) ? 1 : ksplit_for(bn, p.nchunks, p.mode == tg::kConvFwd);
+    // (a halo chunk is three taps: the chain counts taps)
+    const int S = (no_ksplit || skip)
+                      ? 1
+                      : std::min(p.nchunks, ksplit_for(bn, p.nchunks * (p.halo ? 3 : 1),
+                                                       p.mode == tg::kConvFwd));
     if (S <= 1 || !d_split_ws) {
       tg::launch(p, bn, dim3(ntn, ntm, 1), s);
       return 0;
@@ -484,11 +498,13 @@ struct Engine {
     tg::Params p{};
     int by, bnimg;
     tg::fwd_box(g, by, bnimg);
+    const bool halo = halo_ok(g, bn);
     const uint64_t da[4] = {(uint64_t)Dp, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)Bi};
     const uint64_t sa[3] = {4ull * Dp, 4ull * Dp * g.W, 4ull * Dp * HW};
-    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)by, (uint32_t)bnimg};
+    const uint32_t ba[4] = {32, (uint32_t)g.W, (uint32_t)(halo ? by + 2 : by), (uint32_t)bnimg};
     tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
     tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
+    p.halo = halo ? 1 : 0;
     const uint64_t db[2] = {(uint64_t)9 * Dp, (uint64_t)g.C};
     const uint64_t sb[1] = {4ull * 9 * Dp};
     const uint32_t bb[2] = {32, (uint32_t)bn};
@@ -497,7 +513,7 @@ struct Engine {
     p.mode = tg::kConvDx;
     p.M = Bi * HW;
     p.N = g.C;
-    p.nchunks = 9 * Dp / 32;
+    p.nchunks = (halo ? 3 : 9) * Dp / 32;
     p.C = g.C, p.H = g.H, p.W = g.W, p.D = g.D;
     p.Cg = Dp / 32;
     p.by = by, p.bn = bnimg;
@@ -622,6 +638,7 @@ struct Engine {
     pool_generic = std::getenv("PGB_POOL_GENERIC") != nullptr;
     ghost_enabled = std::getenv("PGB_NO_GHOST") == nullptr;
     no_ksplit = std::getenv("PGB_NO_KSPLIT") != nullptr;
+    no_halo = std::getenv("PGB_NO_HALO") != nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers

@@ -82,6 +82,7 @@ struct alignas(64) Params {
   int ntn, ntm, nz;  // N tiles, M tiles, GEMMs (examples / example splits); set by launch()
   int ex_per, nex;   // dw-sum: examples per split, examples in total
   int ksplit;        // fwd / dx / plain: K splits (tile z); > 1: raw tiles to ws
+  int halo;          // fwd / dx: halo stages (chunk = (kernel column v, 32 channels))
   float* ws;         // dw-sum: split workspace [z][mt][n][128 rows]
   // epilogue
   float* out;
@@ -92,8 +93,17 @@ struct alignas(64) Params {
   int ldc;           // kPlain: row stride of out
 };
 
-template <int BN>
-constexpr int stages() { return BN >= 128 ? 3 : BN >= 64 ? 4 : 5; }
+// Halo mode (forward / input gradient on 16- and 32-wide maps, N <= 64): a
+// stage holds the (rows + 2) x W input rows around a 128-position tile for
+// one kernel column v and 32 channels, and the three kernel rows u read it at
+// row offsets u * W -- UMMA descriptor start addresses, whole 1024-B swizzle
+// atoms since W * 128 B is -- so each input element crosses L2 -> SMEM once
+// per kernel column instead of once per tap.
+constexpr int kHaloRows = 192;  // A rows of a halo stage: (128 / W + 2) * W <= 192
+template <int BN, bool H = false>
+constexpr int stages() {
+  return H ? (BN >= 64 ? 2 : 3) : (BN >= 128 ? 3 : BN >= 64 ? 4 : 5);
+}
 // Narrow tiles (BN <= 64) fold the 3xTF32 split into N: the B stage holds the
 // hi rows then the lo rows (2 BN rows, one operand), so a K step is two MMAs
 // of width 2 BN -- Ahi.[Bhi;Blo] and Alo.[Bhi;Blo] -- instead of three of
@@ -118,12 +128,14 @@ constexpr int nacc() {
                       : (512 / nbuf<BN>()) / acc_stride<BN>() - 1;
 }
 
-template <int BN>
+template <int BN, bool H = false>
 struct Smem {
-  static constexpr int S = stages<BN>();
-  float a_hi[S][kBM * kBK];
-  float a_lo[S][kBM * kBK];
-  float b[S][2][BN * kBK];  // hi rows, then lo rows (adjacent: one 2 BN-row operand)
+  static constexpr int S = stages<BN, H>();
+  static constexpr int T = H ? 3 : 1;            // taps (kernel rows) per stage
+  static constexpr int RA = H ? kHaloRows : kBM;  // A rows per stage
+  float a_hi[S][RA * kBK];
+  float a_lo[S][RA * kBK];
+  float b[S][T][2][BN * kBK];  // per tap: hi rows, then lo rows (one 2 BN-row operand)
   uint64_t full[S], empty[S];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem;
@@ -244,13 +256,33 @@ __device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* 
   }
 }
 
-template <int BN>
-__device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN>& S, int s, int q, int mt,
+template <int BN, bool H>
+__device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN, H>& S, int s, int q, int mt,
                                             int nt, int z) {
   const uint32_t bar = smem_u32(&S.full[s]);
-  issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b[s][0]), BN, q, mt, nt, z, bar);
-  issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b[s][1]), BN, q, mt, nt, z,
-              bar);
+  if constexpr (H) {
+    // halo chunk q = (kernel column v, channel group cg): the input rows
+    // y0 - 1 .. y0 + 128 / W of the tile's image, shifted by the column tap
+    // (forward x + v - 1, input gradient the flipped 1 - v), once; the three
+    // taps (u, v) of the weight operand
+    const int v = q / p.Cg, cg = q - v * p.Cg;
+    const int HW = p.H * p.W;
+    const int m0 = mt * kBM, n0 = m0 / HW, y0 = (m0 - n0 * HW) / p.W;
+    const int dx = p.mode == kConvFwd ? v - 1 : 1 - v;
+    tma_4d(smem_u32(S.a_hi[s]), &p.ta, cg * kBK, dx, y0 - 1, n0, bar);
+    tma_4d(smem_u32(S.a_lo[s]), &p.ta_lo, cg * kBK, dx, y0 - 1, n0, bar);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int k0 = (3 * u + v) * p.Cg * kBK + cg * kBK;
+      tma_2d(smem_u32(S.b[s][u][0]), &p.tb, k0, nt * BN, bar);
+      tma_2d(smem_u32(S.b[s][u][1]), &p.tb_lo, k0, nt * BN, bar);
+    }
+  } else {
+    issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b[s][0][0]), BN, q, mt, nt, z,
+                bar);
+    issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b[s][0][1]), BN, q, mt,
+                nt, z, bar);
+  }
 }
 
 // K chunks of a tile: dw-sum walks the positions of every example of its split
@@ -287,13 +319,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& nt, int
 // The TMA ring runs across tile boundaries (the next tile's operands stream in
 // while this tile's MMAs finish), and with two accumulator buffers the
 // epilogue of a tile overlaps the next tile's MMAs.
-template <int BN>
+template <int BN, bool H = false>
 __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char raw[];
   // the swizzled tiles need 1024-B alignment of the dynamic window
-  Smem<BN>& S = *reinterpret_cast<Smem<BN>*>(
+  Smem<BN, H>& S = *reinterpret_cast<Smem<BN, H>*>(
       (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  constexpr int NS = Smem<BN>::S;
+  constexpr int NS = Smem<BN, H>::S;
+  constexpr int T = Smem<BN, H>::T;
   constexpr uint32_t kCols = 512;
   constexpr bool kFold = folded<BN>();
   constexpr int NB = nbuf<BN>();
@@ -330,7 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
       for (int tl = blockIdx.x; tl < total; tl += gridDim.x) {
         int nt, mt, z;
         tile_coords(p, tl, nt, mt, z);
-        const uint32_t bytes = 2 * (a_bytes(p, mt) + BN * kBK * 4);
+        const uint32_t bytes =
+            H ? 2u * ((uint32_t)(kBM / p.W + 2) * p.W * kBK * 4 + 3u * BN * kBK * 4)
+              : 2u * (a_bytes(p, mt) + BN * kBK * 4);
         const int nq = tile_chunks(p, z);
         for (int q = 0; q < nq; ++q, ++g) {
           const int s = g % NS;
@@ -338,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
           expect_tx(&S.full[s], bytes);
           int qc, ze;
           chunk_coords(p, q, z, qc, ze);
-          issue_chunk<BN>(p, S, s, qc, mt, nt, ze);
+          issue_chunk<BN, H>(p, S, s, qc, mt, nt, ze);
         }
       }
     }
@@ -360,23 +395,32 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
           const int s = g % NS;
           tc::mbar_wait(&S.full[s], (g / NS) & 1);
           tc::fence_after_sync();
-          const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
-          const uint32_t bh = smem_u32(S.b[s][0]), bl = smem_u32(S.b[s][1]);
-          const uint32_t dmain = buf + (uint32_t)(q % NACC) * kAccStride;
 #pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            const uint32_t o = 32u * k;
-            if constexpr (kFold) {
-              // [Bhi; Blo] is one 2 BN-row operand starting at bh
-              tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
-                           (q >= NACC || k) ? 1u : 0u);
-              tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
-            } else {
-              const uint32_t dcorr = buf + (uint32_t)NACC * kAccStride;
-              tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
-                           (q >= NACC || k) ? 1u : 0u);
-              tc::mma_tf32(dcorr, desc_sw128(ah + o), desc_sw128(bl + o), idesc, (q | k) ? 1u : 0u);
-              tc::mma_tf32(dcorr, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+          for (int u = 0; u < T; ++u) {
+            // halo: kernel row u reads the stage's rows from u (forward) or
+            // 2 - u (input gradient, the flipped tap) times W
+            const uint32_t ao =
+                H ? (uint32_t)((p.mode == kConvFwd ? u : 2 - u) * p.W * kBK * 4) : 0u;
+            const uint32_t ah = smem_u32(S.a_hi[s]) + ao, al = smem_u32(S.a_lo[s]) + ao;
+            const uint32_t bh = smem_u32(S.b[s][u][0]), bl = smem_u32(S.b[s][u][1]);
+            const int qa = q * T + u;  // accumulator chain step
+            const uint32_t dmain = buf + (uint32_t)(qa % NACC) * kAccStride;
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) {
+              const uint32_t o = 32u * k;
+              if constexpr (kFold) {
+                // [Bhi; Blo] is one 2 BN-row operand starting at bh
+                tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
+                             (qa >= NACC || k) ? 1u : 0u);
+                tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+              } else {
+                const uint32_t dcorr = buf + (uint32_t)NACC * kAccStride;
+                tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
+                             (qa >= NACC || k) ? 1u : 0u);
+                tc::mma_tf32(dcorr, desc_sw128(ah + o), desc_sw128(bl + o), idesc,
+                             (qa | k) ? 1u : 0u);
+                tc::mma_tf32(dcorr, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+              }
             }
           }
           tc::commit(&S.empty[s]);
@@ -391,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
     for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
       int nt, mt, z;
       tile_coords(p, tl, nt, mt, z);
-      const int nq = tile_chunks(p, z);
+      const int nq = tile_chunks(p, z) * T;  // accumulator chain steps
       const int used = nq < NACC ? nq : NACC;
       const int bsel = NB == 2 ? (lt & 1) : 0;
       const int use = NB == 2 ? (lt >> 1) : lt;
@@ -529,9 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
   if (warp == 1) tc::tmem_dealloc(tmem, kCols);
 }
 
-template <int BN>
+template <int BN, bool H = false>
 inline size_t smem_bytes() {
-  return sizeof(Smem<BN>) + 1024;
+  return sizeof(Smem<BN, H>) + 1024;
 }
 
 }  // namespace tg
@@ -739,11 +783,20 @@ inline void launch_bn(const Params& p, int ctas, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(tma_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_bytes<BN>());
+    cudaFuncSetAttribute(tma_gemm_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_bytes<BN, false>());
+    if constexpr (BN <= 64)
+      cudaFuncSetAttribute(tma_gemm_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes<BN, true>());
     attr_dev = dev;
   }
-  tma_gemm_kernel<BN><<<ctas, kThreads, smem_bytes<BN>(), s>>>(p);
+  if constexpr (BN <= 64) {
+    if (p.halo) {
+      tma_gemm_kernel<BN, true><<<ctas, kThreads, smem_bytes<BN, true>(), s>>>(p);
+      return;
+    }
+  }
+  tma_gemm_kernel<BN, false><<<ctas, kThreads, smem_bytes<BN, false>(), s>>>(p);
 }
 
 // tiles: (N tiles, M tiles, GEMMs); one persistent CTA per SM walks them

@@ -483,7 +483,7 @@ struct Engine {
     q.ntn = ntn;
     q.ntm = ntm;
     const long long per = (long long)ntm * ntn * bn * 128;
-    tg::splitk_epilogue_kernel<<<grid_for((size_t)per), 256, 0, s>>>(q);
+    tg::splitk_epilogue_kernel<<<grid_for((size_t)per / 4), 256, 0, s>>>(q);
     return 1;
   }
 
@@ -2914,7 +2914,7 @@ pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, c
       tg::Params q = p;
       q.ntn = ntn;
       q.ntm = ntm;
-      tg::splitk_epilogue_kernel<<<grid_for((size_t)ntm * ntn * bn * 128), 256>>>(q);
+      tg::splitk_epilogue_kernel<<<grid_for((size_t)ntm * ntn * bn * 32), 256>>>(q);
     } else {
       tg::launch(p, bn, dim3(ntn, ntm, 1), 0);
     }

@@ -634,30 +634,79 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
 // The K splits of a forward / input-gradient GEMM added in split order, then
 // that mode's epilogue (bias + relu into NCHW; relu mask into NCHW).
 __global__ void splitk_epilogue_kernel(const Params p) {
-  // 32-bit index math throughout (a split is < 2^31 elements): the 64-bit
-  // divisions of a straightforward version cost more than the bytes it moves
+  // four consecutive tile rows (positions) per thread: 16-byte loads of every
+  // split issued before the ordered sum (the splits' loads were serialised
+  // behind the running sum before), 16-byte mask loads and output stores;
+  // 32-bit index math (a split is < 2^31 elements)
   const unsigned npad = (unsigned)p.ntn * (p.N <= 16 ? 16 : p.N <= 32 ? 32 : p.N <= 64 ? 64 : 128);
   const unsigned per_split = (unsigned)p.ntm * npad * kBM;
   const unsigned HW = p.mode == kPlain ? 1u : (unsigned)(p.H * p.W);
   const unsigned N = (unsigned)p.N, M = (unsigned)p.M;
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < per_split;
-       e += gridDim.x * blockDim.x) {
-    const unsigned r = e & (kBM - 1), t = e >> 7;
+  const bool vec = p.mode != kPlain && HW % 4 == 0;
+  const int S = p.ksplit;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < per_split / 4;
+       q += gridDim.x * blockDim.x) {
+    const unsigned e = 4 * q, r = e & (kBM - 1), t = e >> 7;
     const unsigned mt = t / npad, n = t - mt * npad;
     const unsigned m = mt * kBM + r;
     if (m >= M || n >= N) continue;
-    float acc = p.ws[e];
-    for (int z = 1; z < p.ksplit; ++z) acc += p.ws[(size_t)z * per_split + e];
-    const unsigned img = m / HW, pos = m - img * HW;
+    float4 acc = *reinterpret_cast<const float4*>(p.ws + e);
+    for (int z0 = 1; z0 < S; z0 += 8) {
+      float4 u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (z0 + k < S) u[k] = __ldcg(reinterpret_cast<const float4*>(p.ws + (size_t)(z0 + k) * per_split + e));
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (z0 + k < S) {
+          acc.x += u[k].x;
+          acc.y += u[k].y;
+          acc.z += u[k].z;
+          acc.w += u[k].w;
+        }
+    }
+    float a[4] = {acc.x, acc.y, acc.z, acc.w};
     if (p.mode == kPlain) {
-      p.out[(size_t)m * p.ldc + n] = acc;
-    } else if (p.mode == kConvFwd) {
-      float o = acc + p.bias[n];
-      if (p.relu) o = fmaxf(o, 0.0f);
-      p.out[((size_t)img * p.D + n) * HW + pos] = o;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m + j < M) p.out[(size_t)(m + j) * p.ldc + n] = a[j];
+      continue;
+    }
+    const unsigned img = m / HW, pos = m - img * HW;
+    if (p.mode == kConvFwd) {
+      const float b = p.bias[n];
+      const size_t o = ((size_t)img * p.D + n) * HW + pos;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] += b;
+        if (p.relu) a[j] = fmaxf(a[j], 0.0f);
+      }
+      if (vec) {
+        *reinterpret_cast<float4*>(p.out + o) = make_float4(a[0], a[1], a[2], a[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p.out[o + j] = a[j];
+      }
     } else {
       const size_t i = ((size_t)img * p.C + n) * HW + pos;
-      p.out[i] = (p.mask && !(p.mask[i] > 0.0f)) ? 0.0f : acc;
+      float mk[4] = {1.0f, 1.0f, 1.0f, 1.0f};
+      if (p.mask) {
+        if (vec) {
+          const float4 mv = *reinterpret_cast<const float4*>(p.mask + i);
+          mk[0] = mv.x; mk[1] = mv.y; mk[2] = mv.z; mk[3] = mv.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mk[j] = p.mask[i + j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[j] = !(mk[j] > 0.0f) ? 0.0f : a[j];
+      if (vec) {
+        *reinterpret_cast<float4*>(p.out + i) = make_float4(a[0], a[1], a[2], a[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p.out[i + j] = a[j];
+      }
     }
   }
 }

@@ -186,6 +186,10 @@ struct Engine {
   float* d_nhwc_lo = nullptr;
   float* d_wt = nullptr;
   float* d_wt_lo = nullptr;
+  // every TMA conv layer's weight operands, written once per step (conv_wt_all_kernel)
+  float* d_wall = nullptr;
+  float* d_wall_lo = nullptr;
+  std::vector<long long> wall_fwd, wall_dx;  // per layer: element offset, or -1
   std::vector<int64_t> param_off;
   int64_t P = 0;
   int64_t in_row = 0;
@@ -396,12 +400,16 @@ struct Engine {
   // ---- convolutions on the TMA-fed tcgen05 GEMM (tma_gemm.cuh) --------------
   // forward: out (B, D, H, W) = conv(x) + bias (+ relu)
   int tma_conv_fwd(cudaStream_t s, const ConvGeom& g, int Bi, const float* x, const float* W,
-                   const float* bias, float* out, bool relu) {
+                   const float* bias, float* out, bool relu, int layer = -1) {
     const int Cp = tg::round32(g.C), HW = g.H * g.W, bn = tg::pick_bn(g.D);
     tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Cp / 32, Bi), dim3(32, 8), 0, s>>>(
         x, d_nhwc, d_nhwc_lo, g.C, HW, Cp);
-    tg::conv_wt_fwd_kernel<<<grid_for((size_t)g.D * 9 * Cp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
-                                                                         g.C, Cp);
+    const bool pre = layer >= 0 && d_wall && wall_fwd[layer] >= 0;
+    float* wt = pre ? d_wall + wall_fwd[layer] : d_wt;
+    float* wt_lo = pre ? d_wall_lo + wall_fwd[layer] : d_wt_lo;
+    if (!pre)
+      tg::conv_wt_fwd_kernel<<<grid_for((size_t)g.D * 9 * Cp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
+                                                                           g.C, Cp);
     tg::Params p{};
     int by, bnimg;
     tg::fwd_box(g, by, bnimg);
@@ -415,8 +423,8 @@ struct Engine {
     const uint64_t db[2] = {(uint64_t)9 * Cp, (uint64_t)g.D};
     const uint64_t sb[1] = {4ull * 9 * Cp};
     const uint32_t bb[2] = {32, (uint32_t)bn};
-    tg::make_map(&p.tb, d_wt, 2, db, sb, bb);
-    tg::make_map(&p.tb_lo, d_wt_lo, 2, db, sb, bb);
+    tg::make_map(&p.tb, wt, 2, db, sb, bb);
+    tg::make_map(&p.tb_lo, wt_lo, 2, db, sb, bb);
     p.mode = tg::kConvFwd;
     p.M = Bi * HW;
     p.N = g.D;
@@ -427,7 +435,7 @@ struct Engine {
     p.out = out;
     p.bias = bias;
     p.relu = relu ? 1 : 0;
-    return 3 + tma_launch_split(p, bn, (g.D + bn - 1) / bn, (p.M + 127) / 128, s);
+    return (pre ? 2 : 3) + tma_launch_split(p, bn, (g.D + bn - 1) / bn, (p.M + 127) / 128, s);
   }
 
   // K splits of a forward / input-gradient GEMM: the tensor core's fp32
@@ -489,12 +497,16 @@ struct Engine {
 
   // input gradient: gx (B, C, H, W) = conv^T(gout) * [mask > 0]
   int tma_conv_dx(cudaStream_t s, const ConvGeom& g, int Bi, const float* gout, const float* W,
-                  const float* mask, float* gx) {
+                  const float* mask, float* gx, int layer = -1) {
     const int Dp = tg::round32(g.D), HW = g.H * g.W, bn = tg::pick_bn(g.C);
     tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Dp / 32, Bi), dim3(32, 8), 0, s>>>(
         gout, d_nhwc, d_nhwc_lo, g.D, HW, Dp);
-    tg::conv_wt_dx_kernel<<<grid_for((size_t)g.C * 9 * Dp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
-                                                                        g.C, Dp);
+    const bool pre = layer >= 0 && d_wall && wall_dx[layer] >= 0;
+    float* wt = pre ? d_wall + wall_dx[layer] : d_wt;
+    float* wt_lo = pre ? d_wall_lo + wall_dx[layer] : d_wt_lo;
+    if (!pre)
+      tg::conv_wt_dx_kernel<<<grid_for((size_t)g.C * 9 * Dp), 256, 0, s>>>(W, d_wt, d_wt_lo, g.D,
+                                                                          g.C, Dp);
     tg::Params p{};
     int by, bnimg;
     tg::fwd_box(g, by, bnimg);
@@ -508,8 +520,8 @@ struct Engine {
     const uint64_t db[2] = {(uint64_t)9 * Dp, (uint64_t)g.C};
     const uint64_t sb[1] = {4ull * 9 * Dp};
     const uint32_t bb[2] = {32, (uint32_t)bn};
-    tg::make_map(&p.tb, d_wt, 2, db, sb, bb);
-    tg::make_map(&p.tb_lo, d_wt_lo, 2, db, sb, bb);
+    tg::make_map(&p.tb, wt, 2, db, sb, bb);
+    tg::make_map(&p.tb_lo, wt_lo, 2, db, sb, bb);
     p.mode = tg::kConvDx;
     p.M = Bi * HW;
     p.N = g.C;
@@ -519,7 +531,7 @@ struct Engine {
     p.by = by, p.bn = bnimg;
     p.out = gx;
     p.mask = mask;
-    return 3 + tma_launch_split(p, bn, (g.C + bn - 1) / bn, (p.M + 127) / 128, s);
+    return (pre ? 2 : 3) + tma_launch_split(p, bn, (g.C + bn - 1) / bn, (p.M + 127) / 128, s);
   }
 
   // per-example weight gradient stacks (B, D, C, 3, 3) + each tile's squared
@@ -724,6 +736,23 @@ struct Engine {
         want((void**)&d_nhwc_lo, sizeof(float) * nhwc);
         want((void**)&d_wt, sizeof(float) * wt);
         want((void**)&d_wt_lo, sizeof(float) * wt);
+        // per-layer weight operands of the forward / input-gradient GEMMs
+        wall_fwd.assign(n, -1);
+        wall_dx.assign(n, -1);
+        long long wall = 0;
+        for (int l = 0; l < n; ++l) {
+          if (desc.layers[l].kind != PGB_CONV) continue;
+          const ConvGeom g = conv_geom(layers[l]);
+          if (!tg::conv_ok(g)) continue;
+          wall_fwd[l] = wall;
+          wall += (long long)g.D * 9 * tg::round32(g.C);
+          wall_dx[l] = wall;
+          wall += (long long)g.C * 9 * tg::round32(g.D);
+        }
+        if (wall > 0) {
+          want((void**)&d_wall, sizeof(float) * wall);
+          want((void**)&d_wall_lo, sizeof(float) * wall);
+        }
       }
     }
     want((void**)&d_units, sizeof(float) * B * P);  // microbatch means (only m>1)
@@ -1079,6 +1108,27 @@ struct Engine {
     int nk = 0;
     const int n = desc.n_layers;
     const int Bi = (int)B;
+    if (d_wall) {  // the step's weight operands for every TMA conv GEMM, one launch
+      tg::WtAll A{};
+      for (int l = 0; l < n && A.n + 2 <= tg::kMaxWtSegs; ++l) {
+        if (wall_fwd[l] < 0) continue;
+        const ConvGeom g = conv_geom(layers[l]);
+        for (int kind = 0; kind < 2; ++kind) {
+          const int k = A.n++;
+          A.W[k] = d_params + param_off[layers[l].pblock];
+          A.D[k] = g.D;
+          A.C[k] = g.C;
+          A.P[k] = tg::round32(kind == 0 ? g.C : g.D);
+          A.kind[k] = kind;
+          A.off[k] = kind == 0 ? wall_fwd[l] : wall_dx[l];
+          A.off[k + 1] = A.off[k] + (long long)(kind == 0 ? g.D : g.C) * 9 * A.P[k];
+        }
+      }
+      A.hi = d_wall;
+      A.lo = d_wall_lo;
+      tg::conv_wt_all_kernel<<<grid_for((size_t)A.off[A.n]), 256, 0, s>>>(A);
+      nk += mark(s, "conv_wt_all");
+    }
     for (int l = 0; l < n; ++l) {
       Layer& L = layers[l];
       const float* in = L.act_in ? L.act_in : x_slot;
@@ -1097,8 +1147,9 @@ struct Engine {
                      (int)L.out.d[1], (int)L.out.d[2], (int)sp.k, (int)sp.stride, (int)sp.pad};
           const int K = g.C * g.k * g.k;
           if (tma_fwd(g)) {
-            tma_conv_fwd(s, g, Bi, in, W, W + (size_t)g.D * K, L.act_out, L.fused_relu);
-            nk += mark(s, "conv_fwd_tma") + 2;
+            const int kk = tma_conv_fwd(s, g, Bi, in, W, W + (size_t)g.D * K, L.act_out,
+                                        L.fused_relu, l);
+            nk += mark(s, "conv_fwd_tma") + kk - 1;
           } else if (use_tc) {
             tc::TcConvFwdOp op{Bi * g.Ho * g.Wo, g.D, K, g, in, W, W + (size_t)g.D * K,
                                L.act_out, L.fused_relu ? 1 : 0};
@@ -1386,11 +1437,11 @@ struct Engine {
             if (hw == 64) {
               gram_attr(conv_gram_norm_kernel<64>, sm);
               conv_gram_norm_kernel<64><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
-                                                           nparts, L.pblock);
+                                                           nparts, L.pblock, sb);
             } else {
               gram_attr(conv_gram_norm_kernel<16>, sm);
               conv_gram_norm_kernel<16><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
-                                                           nparts, L.pblock);
+                                                           nparts, L.pblock, sb);
             }
             nk += mark(s, "conv_dw_gram");
           } else if (tma_dw(gg)) {
@@ -1412,12 +1463,14 @@ struct Engine {
             launch_gemm(dw, Bi, s);
             nk += mark(s, "conv_dw_pex");
           }
-          conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
-                                                                         sb);
-          nk += mark(s, "conv_db_pex");
+          if (!(ghost_next && L.ghost)) {  // (the Gram kernel wrote the ghost layers' bias rows)
+            conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
+                                                                           sb);
+            nk += mark(s, "conv_db_pex");
+          }
           if (L.needs_gx && tma_dx(gg)) {
-            tma_conv_dx(s, gg, Bi, gcur, W, L.bwd_mask, gnext);
-            nk += mark(s, "conv_bwd_x_tma") + 2;
+            const int kk = tma_conv_dx(s, gg, Bi, gcur, W, L.bwd_mask, gnext, l);
+            nk += mark(s, "conv_bwd_x_tma") + kk - 1;
           } else if (L.needs_gx && use_tc && gg.stride == 1) {
             tc::TcConvBwdXS1Op op{Bi * gg.H * gg.W, gg.C, gg.D * gg.k * gg.k, gg, gcur, W,
                                   L.bwd_mask, gnext};

@@ -1750,7 +1750,7 @@ __global__ void __launch_bounds__(32 * kEmbAggWarps) embed_agg4_kernel(const Emb
 template <int HW>
 __global__ void __launch_bounds__(256) conv_gram_norm_kernel(
     const float* __restrict__ x, const float* __restrict__ g, int C, int D, int W,
-    double* __restrict__ parts, int nparts, int pb) {
+    double* __restrict__ parts, int nparts, int pb, float* __restrict__ sb) {
   static_assert(HW == 16 || HW == 64, "ghost norms for 4x4 and 8x8 maps");
   constexpr int R = HW == 64 ? 4 : 1;  // (p, q) block per thread: R x R
   extern __shared__ float gsm[];
@@ -1764,6 +1764,18 @@ __global__ void __launch_bounds__(256) conv_gram_norm_kernel(
   for (int e = t; e < C * HW; e += 256) xs[e] = xi[e];
   for (int e = t; e < D * HW; e += 256) gs[e] = gi[e];
   __syncthreads();
+  if (sb) {
+    // the example's conv bias gradient (D), with conv_db_pex_kernel's
+    // arithmetic (lane-strided partials, xor butterfly): bitwise the same
+    const int w = t >> 5, lane = t & 31;
+    for (int d = w; d < D; d += 8) {
+      float s = 0.0f;
+      for (int p = lane; p < HW; p += 32) s += gs[d * HW + p];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) sb[(size_t)i * D + d] = s;
+    }
+  }
   const int tp = t / (HW / R), tq = t % (HW / R);
   float ax[R][R], ag[R][R];
 #pragma unroll

@@ -751,6 +751,39 @@ __global__ void dw_sum_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
+// Every TMA conv layer's forward and input-gradient weight operands in one
+// launch per step (they change only at the update): segment k writes the
+// conv_wt_fwd_kernel (kind 0) or conv_wt_dx_kernel (kind 1) layout of W.
+constexpr int kMaxWtSegs = 32;
+struct WtAll {
+  int n;
+  const float* W[kMaxWtSegs];
+  int D[kMaxWtSegs], C[kMaxWtSegs], P[kMaxWtSegs], kind[kMaxWtSegs];  // P: Cp or Dp
+  long long off[kMaxWtSegs + 1];  // element offsets into the output (prefix sums)
+  float* hi;
+  float* lo;
+};
+
+__global__ void conv_wt_all_kernel(const WtAll A) {
+  const long long total = A.off[A.n];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (k + 1 < A.n && A.off[k + 1] <= e) ++k;
+    const int r0 = (int)(e - A.off[k]);
+    const int D = A.D[k], C = A.C[k], Pp = A.P[k];
+    float v;
+    if (A.kind[k] == 0) {  // Wt[d][tap * Cp + c]
+      const int d = r0 / (9 * Pp), r = r0 - d * 9 * Pp, tap = r / Pp, c = r - tap * Pp;
+      v = c < C ? A.W[k][((size_t)d * C + c) * 9 + tap] : 0.0f;
+    } else {  // Wt2[c][tap * Dp + d]
+      const int c = r0 / (9 * Pp), r = r0 - c * 9 * Pp, tap = r / Pp, d = r - tap * Pp;
+      v = d < D ? A.W[k][((size_t)d * C + c) * 9 + tap] : 0.0f;
+    }
+    split2(v, A.hi[e], A.lo[e]);
+  }
+}
+
 // conv weights (D, C, 3, 3) -> the forward B operand Wt[d][tap * Cp + c]
 __global__ void conv_wt_fwd_kernel(const float* __restrict__ W, float* __restrict__ wt,
                                    float* __restrict__ wt_lo, int D, int C, int Cp) {

@@ -253,6 +253,9 @@ pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, co
 /* Self-test of the TMA-fed tcgen05 GEMM (tensor maps, 128-B swizzle, 3xTF32
  * with the hi/lo split on the CUDA cores): C (M x N) = A (M x K) . B (N x K)^T,
  * row-major, K a multiple of 4. */
+/* self-test: one 32 x 4 TMA box at (x0, y0) of a (height, width) fp32 array */
+pgb_status pgb_debug_tma_box(int32_t device, const float* src, int32_t width, int32_t height,
+                             int32_t x0, int32_t y0, float* out);
 pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
                               const float* B, float* C);
 /* Self-test of the UMMA operand layouts (K-major / MN-major, no swizzle) and

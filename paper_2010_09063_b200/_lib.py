@@ -104,6 +104,8 @@ EXPORTS = {
                                     C.POINTER(C.c_int32)]),
     "pgb_debug_tc_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
+    "pgb_debug_tma_box": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_void_p]),
     "pgb_debug_tma_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
     "pgb_debug_umma_probe": (C.c_int, [C.c_int32] * 6 + [C.c_void_p] * 3),

@@ -2923,6 +2923,28 @@ pgb_status pgb_debug_tc_gemm(int32_t device, int32_t M, int32_t N, int32_t K, co
   });
 }
 
+pgb_status pgb_debug_tma_box(int32_t device, const float* src, int32_t width, int32_t height,
+                             int32_t x0, int32_t y0, float* out) {
+  return guarded([&] {
+    PGB_CUDA(cudaSetDevice(device));
+    float *d_src = nullptr, *d_out = nullptr;
+    PGB_CUDA(cudaMalloc(&d_src, sizeof(float) * (size_t)width * height));
+    PGB_CUDA(cudaMalloc(&d_out, sizeof(float) * 128));
+    PGB_CUDA(cudaMemcpy(d_src, src, sizeof(float) * (size_t)width * height, cudaMemcpyHostToDevice));
+    CUtensorMap m;
+    const uint64_t dims[2] = {(uint64_t)width, (uint64_t)height};
+    const uint64_t st[1] = {sizeof(float) * (uint64_t)width};
+    const uint32_t box[2] = {32, 4};
+    tg::make_map(&m, d_src, 2, dims, st, box);
+    tg::tma_box_probe_kernel<<<1, 128>>>(m, x0, y0, d_out);
+    PGB_CUDA(cudaGetLastError());
+    PGB_CUDA(cudaDeviceSynchronize());
+    PGB_CUDA(cudaMemcpy(out, d_out, sizeof(float) * 128, cudaMemcpyDeviceToHost));
+    cudaFree(d_src);
+    cudaFree(d_out);
+  });
+}
+
 pgb_status pgb_debug_tma_gemm(int32_t device, int32_t M, int32_t N, int32_t K, const float* A,
                               const float* Bm, float* Cout) {
   return guarded([&] {

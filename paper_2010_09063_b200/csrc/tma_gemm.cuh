@@ -784,6 +784,28 @@ __global__ void conv_wt_all_kernel(const WtAll A) {
   }
 }
 
+// Probe (self-test): one TMA box {32, 4} of a SWIZZLE_128B map at an arbitrary
+// (possibly misaligned or negative) innermost coordinate x0, unswizzled into out
+// (4 rows x 32): does a box start need 16-byte alignment in the innermost dim?
+__global__ void tma_box_probe_kernel(const __grid_constant__ CUtensorMap m, int x0, int y0,
+                                     float* out) {
+  __shared__ __align__(1024) float tile[4 * 32];
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    expect_tx(&bar, 4 * 32 * 4);
+    tma_2d(smem_u32(tile), &m, x0, y0, smem_u32(&bar));
+  }
+  __syncthreads();
+  tc::mbar_wait(&bar, 0);
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) {
+    const int r = e / 32, c = e % 32;          // logical row, element
+    const int chunk = (c / 4) ^ (r % 8);       // 16-byte chunk after the 128-B swizzle
+    out[e] = tile[r * 32 + chunk * 4 + (c % 4)];
+  }
+}
+
 // conv weights (D, C, 3, 3) -> the forward B operand Wt[d][tap * Cp + c]
 __global__ void conv_wt_fwd_kernel(const float* __restrict__ W, float* __restrict__ wt,
                                    float* __restrict__ wt_lo, int D, int C, int Cp) {

@@ -197,6 +197,9 @@ struct Engine {
 
   static constexpr int kSlots = 3;  // epoch driver: input / result ring depth
   cudaStream_t stream = nullptr, copy_stream = nullptr, out_stream = nullptr;
+  cudaStream_t side_stream = nullptr;  // fork / join branch of the embedding step
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool emb_fork = true;  // PGB_NO_EMB_FORK=1: the head's aggregation in line
   // epoch-driver staging (pinned, grown on demand) and events
   float* h_norm_stage = nullptr;
   int* h_clip_stage = nullptr;
@@ -358,6 +361,9 @@ struct Engine {
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (out_stream) cudaStreamDestroy(out_stream);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (h_norm_stage) cudaFreeHost(h_norm_stage);
     if (h_clip_stage) cudaFreeHost(h_clip_stage);
     for (int i = 0; i < kSlots; ++i) {
@@ -1021,6 +1027,10 @@ struct Engine {
     PGB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+    PGB_CUDA(cudaStreamCreateWithFlags(&side_stream, cudaStreamNonBlocking));
+    PGB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    PGB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    emb_fork = std::getenv("PGB_NO_EMB_FORK") == nullptr;
     for (int i = 0; i < kSlots; ++i)
       for (cudaEvent_t* ev : {&ev_copied[i], &ev_consumed[i]})
         PGB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
@@ -1711,7 +1721,19 @@ struct Engine {
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
     const bool emb = emb_layer >= 0 && t.kind[layers[emb_layer].pblock] == 2;
-    if (!dist) {
+    if (!dist && emb && emb_fork) {
+      // the dense head's aggregation (a few latency-bound CTAs) on a side
+      // branch beside the embedding table's: independent blocks, both after
+      // embed_index (fork / join by events; a captured graph keeps them as
+      // parallel branches)
+      PGB_CUDA(cudaEventRecord(ev_fork, s));
+      PGB_CUDA(cudaStreamWaitEvent(side_stream, ev_fork, 0));
+      launch_agg(agg_launch(t, np, U, 0, ff), side_stream);
+      nk += mark(side_stream, "aggregate");
+      PGB_CUDA(cudaEventRecord(ev_join, side_stream));
+      nk += enqueue_embed_agg(s, t, np, 0);
+      PGB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    } else if (!dist) {
       launch_agg(agg_launch(t, np, U, 0, ff), s, (ff || mlp_fused) && pdl_enabled);
       nk += mark(s, "aggregate");
       if (emb) nk += enqueue_embed_agg(s, t, np, 0);

@@ -1721,7 +1721,7 @@ struct Engine {
   int enqueue_aggregate(cudaStream_t s, const BlockTable& t, int np, int U, bool ff = false) {
     int nk = 0;
     const bool emb = emb_layer >= 0 && t.kind[layers[emb_layer].pblock] == 2;
-    if (!dist && emb && emb_fork) {
+    if (!dist && emb && emb_fork && !prof) {  // (per-kernel profiling needs one stream order)
       // the dense head's aggregation (a few latency-bound CTAs) on a side
       // branch beside the embedding table's: independent blocks, both after
       // embed_index (fork / join by events; a captured graph keeps them as

@@ -77,6 +77,27 @@ struct TcConvDWOp {
   __device__ float b(int z, int n, int k) const {
     return __ldg(gout + ((size_t)z * g.D + n) * K + k);
   }
+  // four consecutive positions k..k+3 (k % 4 == 0) of one output row: one
+  // index computation, the zero padding only at the row's ends
+  __device__ bool vec_ok() const { return g.stride == 1 && g.Wo % 4 == 0 && K % 4 == 0; }
+  __device__ float4 a4(int z, const int4& ri, int k) const {
+    float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (!ri.w || k >= K) return v;
+    const int oy = k / g.Wo, ox = k - oy * g.Wo;
+    const int iy = ri.y + oy;
+    if ((unsigned)iy >= (unsigned)g.H) return v;
+    const float* row = img(z) + ri.x + (size_t)iy * g.W;
+    const int ix = ri.z + ox;
+    v.x = (unsigned)(ix) < (unsigned)g.W ? __ldg(row + ix) : 0.0f;
+    v.y = (unsigned)(ix + 1) < (unsigned)g.W ? __ldg(row + ix + 1) : 0.0f;
+    v.z = (unsigned)(ix + 2) < (unsigned)g.W ? __ldg(row + ix + 2) : 0.0f;
+    v.w = (unsigned)(ix + 3) < (unsigned)g.W ? __ldg(row + ix + 3) : 0.0f;
+    return v;
+  }
+  __device__ float4 b4(int z, int n, int k) const {
+    if (n >= N || k >= K) return make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    return __ldg(reinterpret_cast<const float4*>(gout + ((size_t)z * g.D + n) * K + k));
+  }
   __device__ void store(int z, int m, int n, float v) const {
     stack[(size_t)z * M * N + (size_t)n * M + m] = v;
   }

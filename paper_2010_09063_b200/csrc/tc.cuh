@@ -158,6 +158,14 @@ struct NoTable {
 // Ops with a `double* tile_sq` member also get each tile's sum of squared
 // outputs (fp64), written to tile_sq[z * tiles + tile]: the per-example norm
 // of a materialised gradient block without a second pass over it.
+// Ops with a4 / b4 gather four consecutive k at once (one index computation,
+// 16-byte shared-memory stores; the per-example conv dW, where k runs along an
+// output row) when op.vec_ok()
+template <class T, class = void>
+struct HasA4 : std::false_type {};
+template <class T>
+struct HasA4<T, std::void_t<decltype(&T::a4)>> : std::true_type {};
+
 template <class T, class = void>
 struct HasPre : std::false_type {};
 template <class T>
@@ -252,9 +260,68 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
       rb[i] = v;
     }
   };
+  // four consecutive k per thread (HasA4 ops). A warp covers 8 rows x 4 quads:
+  // lane = 8 * (k4 % 4) + row % 8, so each 8-lane phase of a 16-byte store
+  // hits 8 distinct 16-B slots of the core-matrix rows (conflict-free) and
+  // each load instruction touches 8 rows x 64 contiguous bytes
+  constexpr int kA4 = kBM * kBK / 4 / NT, kB4 = (BN * kBK / 4 + NT - 1) / NT;
+  auto quad = [](int eq, int rows, int& r, int& k4) {
+    const int l = eq & 31, gi = eq >> 5, rg = rows / 8;
+    r = (gi % rg) * 8 + (l & 7);
+    k4 = (gi / rg) * 4 + (l >> 3);
+  };
+  bool vec = false;
+  if constexpr (HasA4<Op>::value) vec = op.vec_ok();
+  float4 ra4[HasA4<Op>::value ? kA4 : 1], rb4[HasA4<Op>::value ? kB4 : 1];
+  auto fetch4 = [&](int kc) {
+    if constexpr (HasA4<Op>::value) {
+      const int k0 = kc * kBK;
+#pragma unroll
+      for (int i = 0; i < kA4; ++i) {
+        int r, k4;
+        quad(t + i * NT, kBM, r, k4);
+        ra4[i] = op.a4(z, S.rowinfo[r], k0 + 4 * k4);
+      }
+#pragma unroll
+      for (int i = 0; i < kB4; ++i) {
+        const int eq = t + i * NT;
+        int n, k4;
+        quad(eq, BN, n, k4);
+        rb4[i] = eq < BN * kBK / 4 ? op.b4(z, n0 + n, k0 + 4 * k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  auto store4 = [&](int s) {
+    if constexpr (HasA4<Op>::value) {
+      auto put = [&](float* hi_base, float* lo_base, int r, int k4, const float4& v) {
+        float4 h, l;
+        split_tf32(v.x, h.x, l.x);
+        split_tf32(v.y, h.y, l.y);
+        split_tf32(v.z, h.z, l.z);
+        split_tf32(v.w, h.w, l.w);
+        const int o = canon_off<kBK>(r, 4 * k4);
+        *reinterpret_cast<float4*>(hi_base + o) = h;
+        *reinterpret_cast<float4*>(lo_base + o) = l;
+      };
+#pragma unroll
+      for (int i = 0; i < kA4; ++i) {
+        int r, k4;
+        quad(t + i * NT, kBM, r, k4);
+        put(S.ahi[s], S.alo[s], r, k4, ra4[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < kB4; ++i) {
+        const int eq = t + i * NT;
+        int n, k4;
+        quad(eq, BN, n, k4);
+        if (eq < BN * kBK / 4) put(S.bhi[s], S.blo[s], n, k4, rb4[i]);
+      }
+    }
+  };
   kinfo_fill(0);
   __syncthreads();
-  fetch(0);
+  if (vec) fetch4(0);
+  else fetch(0);
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     // chunk kc+1's gather info (slot s^1 was last read by fetch(kc-1), two
@@ -262,6 +329,9 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
     if (kc + 1 < nk) kinfo_fill(kc + 1);
     if (kc >= 2) mbar_wait(&S.bar[s], ((kc - 2) >> 1) & 1);
     // split + store this chunk (lanes cover one 8x4 core matrix: conflict-free)
+    if (vec) {
+      store4(s);
+    } else {
 #pragma unroll
     for (int i = 0; i < kA; ++i) {
       const int e = t + i * NT;
@@ -288,6 +358,7 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
         S.blo[s][o] = lo;
       }
     }
+    }  // scalar store
     fence_proxy_async();
     __syncthreads();
     if (lane == 0 && warp < 3) {
@@ -306,7 +377,10 @@ __global__ void __launch_bounds__(NT) tc_gemm_kernel(Op op) {
       commit(&S.bar[s]);
     }
     // next chunk's operands into registers while the tensor core runs
-    if (kc + 1 < nk) fetch(kc + 1);
+    if (kc + 1 < nk) {
+      if (vec) fetch4(kc + 1);
+      else fetch(kc + 1);
+    }
   }
   // all MMAs done once the last commit lands (they complete in issue order)
   mbar_wait(&S.bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);

@@ -746,10 +746,14 @@ struct Engine {
         wall_fwd.assign(n, -1);
         wall_dx.assign(n, -1);
         long long wall = 0;
+        int segs = 0;
         for (int l = 0; l < n; ++l) {
           if (desc.layers[l].kind != PGB_CONV) continue;
           const ConvGeom g = conv_geom(layers[l]);
-          if (!tg::conv_ok(g)) continue;
+          // (layers past conv_wt_all_kernel's segment table keep the per-GEMM
+          // weight kernels)
+          if (!tg::conv_ok(g) || segs + 2 > tg::kMaxWtSegs) continue;
+          segs += 2;
           wall_fwd[l] = wall;
           wall += (long long)g.D * 9 * tg::round32(g.C);
           wall_dx[l] = wall;

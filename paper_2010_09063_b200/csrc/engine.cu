@@ -549,7 +549,7 @@ struct Engine {
     tg::dw_tiling(g.C, Cr, T, big, mtiles);
     const int bx = g.W, by = 32 / g.W;
     const long long total = (long long)Bi * g.C * HW;
-    tg::shift3_kernel<<<grid_for((size_t)(3 * total)), 256, 0, s>>>(x, d_nhwc, d_nhwc_lo, total,
+    tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, d_nhwc, d_nhwc_lo, total,
                                                                     g.W);
     const long long gt = (long long)Bi * g.D * HW;
     tg::split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(gout, d_wt, d_wt_lo, gt);
@@ -1803,7 +1803,7 @@ struct Engine {
       tg::dw_tiling(g.C, Cr, T, big, mtiles);
       const long long total = (long long)Bi * g.C * HW;
       const float* in = L.act_in;
-      tg::shift3_kernel<<<grid_for((size_t)(3 * total)), 256, 0, s>>>(in, d_nhwc, d_nhwc_lo,
+      tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(in, d_nhwc, d_nhwc_lo,
                                                                       total, g.W);
       const long long gt = (long long)Bi * g.D * HW;
       tg::scale_split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(L.gout, d_scale,

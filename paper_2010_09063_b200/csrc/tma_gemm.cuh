@@ -642,6 +642,22 @@ __global__ void split_kernel(const float* __restrict__ src, float* __restrict__ 
 // the three column-shifted copies the per-example dW boxes read
 __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__ dst,
                               float* __restrict__ dst_lo, long long total, int W) {
+  // one thread per source element writes its three copies (the row's
+  // neighbours read once); 32-bit index math when the tensor allows it (the
+  // 64-bit division per element was this kernel's bound)
+  if (total < (1ll << 31)) {
+    const unsigned T = (unsigned)total;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += gridDim.x * blockDim.x) {
+      const unsigned x = i % (unsigned)W;
+      const float c = src[i];
+      const float l = x > 0 ? src[i - 1] : 0.0f;
+      const float r = x + 1 < (unsigned)W ? src[i + 1] : 0.0f;
+      split2(l, dst[i], dst_lo[i]);
+      split2(c, dst[T + i], dst_lo[T + i]);
+      split2(r, dst[2ull * T + i], dst_lo[2ull * T + i]);
+    }
+    return;
+  }
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 3 * total;
        e += (long long)gridDim.x * blockDim.x) {
     const int v = (int)(e / total);
@@ -737,6 +753,12 @@ __global__ void splitk_epilogue_kernel(const Params p) {
 __global__ void scale_split_kernel(const float* __restrict__ g, const float* __restrict__ scale,
                                    long long per_ex, long long total, float* __restrict__ hi,
                                    float* __restrict__ lo) {
+  if (total < (1ll << 31)) {  // 32-bit index math
+    const unsigned T = (unsigned)total, pe = (unsigned)per_ex;
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < T; e += gridDim.x * blockDim.x)
+      split2(__fmul_rn(g[e], scale[e / pe]), hi[e], lo[e]);
+    return;
+  }
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x)
     split2(__fmul_rn(g[e], scale[e / per_ex]), hi[e], lo[e]);

@@ -770,12 +770,13 @@ __global__ void scale_split_kernel(const float* __restrict__ g, const float* __r
 __global__ void dw_sum_reduce_kernel(const float* __restrict__ ws, int splits, int ntm, int npad,
                                      int C, int D, int Cr, int T, int big,
                                      float* __restrict__ out) {
-  const long long per_split = (long long)ntm * npad * kBM;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < per_split;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e % kBM);
-    const long long t = e / kBM;
-    const int n = (int)(t % npad), mt = (int)(t / npad);
+  // 32-bit index math (a split of the workspace is < 2^31 elements)
+  const unsigned per_split = (unsigned)ntm * npad * kBM;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < per_split;
+       e += gridDim.x * blockDim.x) {
+    const int r = (int)(e & (kBM - 1));
+    const unsigned t = e >> 7;
+    const int mt = (int)(t / (unsigned)npad), n = (int)(t - (unsigned)mt * npad);
     int tap, c;
     if (big) {
       const int cgs = C / kBM;
@@ -788,8 +789,8 @@ __global__ void dw_sum_reduce_kernel(const float* __restrict__ ws, int splits, i
     }
     if (tap >= 9 || c >= C || n >= D) continue;
     float acc = ws[e];
-    for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[(long long)z * per_split + e]);
-    out[((long long)n * C + c) * 9 + tap] = acc;
+    for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[(size_t)z * per_split + e]);
+    out[((size_t)n * C + c) * 9 + tap] = acc;
   }
 }
 

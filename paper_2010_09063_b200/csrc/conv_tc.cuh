@@ -200,11 +200,13 @@ constexpr int kConvThreads = 256;
 template <class Op, int BN>
 inline void launch_bn(const Op& op, int batch, cudaStream_t s) {
   const size_t smem = sizeof(TcSmem<BN>);
-  static bool attr = false;  // once per instantiation (host-side)
-  if (!attr) {
+  static unsigned long long attr_devs = 0;  // per instantiation, per device (bit = device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !(attr_devs >> dev & 1ull)) {
     cudaFuncSetAttribute(tc_gemm_kernel<Op, BN, kConvThreads>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    if (dev < 64) attr_devs |= 1ull << dev;
   }
   dim3 grid((op.N + BN - 1) / BN, (op.M + kBM - 1) / kBM, batch);
   tc_gemm_kernel<Op, BN, kConvThreads><<<grid, kConvThreads, smem, s>>>(op);

@@ -1779,8 +1779,9 @@ struct Engine {
   // by a profiler -- exceed it)
   template <class K>
   void gram_attr(K* kern, size_t smem) {
-    static size_t set64 = 0, set16 = 0;
-    size_t& cur = (void*)kern == (void*)conv_gram_norm_kernel<64> ? set64 : set16;
+    // (per device: the attribute is a property of the function on each device)
+    static std::map<std::pair<int, const void*>, size_t> set;
+    size_t& cur = set[{device, (const void*)kern}];
     if (smem > 48 * 1024 && smem > cur) {
       PGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));

@@ -834,6 +834,13 @@ struct Engine {
         L.ghost = false;
         if (L.spec.kind != PGB_CONV || !ghost_enabled || !use_tc || !use_tma || fused_mnist)
           continue;
+        // a conv reading the step input itself keeps per-example stacks (the
+        // summed dW GEMM reads the layer input after the backward, when only
+        // the layers' own activation buffers are stable)
+        bool reads_input = true;
+        for (int j = 0; j < l; ++j)
+          if (!layers[j].alias) reads_input = false;
+        if (reads_input) continue;
         const ConvGeom g = conv_geom(L);
         const int hw = g.H * g.W;
         if (!tg::conv_ok(g) || (hw != 16 && hw != 64)) continue;

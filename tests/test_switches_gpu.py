@@ -73,3 +73,32 @@ def test_embed_fork_bitwise_in_line(P, monkeypatch):
     assert ca == cb
     np.testing.assert_array_equal(na, nb)
     np.testing.assert_array_equal(ea.get_flat_params(), eb.get_flat_params())
+
+
+@pytest.mark.parametrize("C,H,D", [(64, 8, 32), (32, 4, 16)])
+def test_first_layer_small_map_conv_step_matches_oracle(P, O, C, H, D):
+    """A 3x3 conv on an 8x8 / 4x4 map as the FIRST layer (its input is the
+    step input, so it keeps per-example stacks) followed by one that takes the
+    ghost path: full DPSGD steps against the oracle."""
+    layers = [P.LayerSpec(P.LayerKind.conv, C, D, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
+              P.LayerSpec(P.LayerKind.conv, D, 10, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
+              P.LayerSpec(P.LayerKind.global_avgpool)]
+    desc = P.custom_desc(P.ModelKind.cifar_cnn, layers, (C, H, H), 10)
+    od = O.custom_desc(O.CIFAR_CNN, [(1, C, D, 3, 1, 1), (6, 0, 0, 0, 1, 0), (1, D, 10, 3, 1, 1),
+                                     (6, 0, 0, 0, 1, 0), (4, 0, 0, 0, 1, 0)], (C, H, H), 10)
+    B = 6
+    model = P.build_from_desc(desc, 0)
+    eng = P.GradEngine(model, P.Strategy.groupconv, B)
+    data = P.synth_for_model(desc, B, 0)
+    x64, y64 = O.synth(od, B, 0)
+    p64 = O.init_params(od, 0)
+    cfg = P.DpConfig(clip_norm=1.0, noise_multiplier=1.1, learning_rate=0.1, seed=0)
+    for step in range(2):
+        rep = P.dpsgd_step(model, eng, data.inputs, data.labels, cfg, step)
+        p_new, wn, wclip, _ = O.dpsgd_step(od, x64, y64, p64, 1.0, 1.1, 0.1, 1, 0, step)
+        assert np.max(np.abs(rep.pre_clip_norms - wn) / wn) < TOL
+        assert rep.clipped_count == wclip
+        got = model.flat_params().astype(np.float64)
+        delta = np.abs(p_new - p64).max()
+        assert np.all(np.abs(got - p_new) <= 3e-7 * np.abs(p_new) + TOL * delta)
+        p64 = p_new

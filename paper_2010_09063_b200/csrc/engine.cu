@@ -479,10 +479,8 @@ struct Engine {
   // launch a forward / input-gradient GEMM, split over K when it under-fills
   // the SMs (raw splits to d_split_ws, added in order by the epilogue kernel)
   int tma_launch_split(tg::Params& p, int bn, int ntn, int ntm, cudaStream_t s) {
-    static const char* only = std::getenv("PGB_KSPLIT_ONLY");  // debug: fwd / dx
-    const bool skip = only && ((only[0] == 'f') != (p.mode == tg::kConvFwd));
     // (a halo chunk is three taps: the chain counts taps)
-    const int S = (no_ksplit || skip)
+    const int S = no_ksplit
                       ? 1
                       : std::min(p.nchunks, ksplit_for(bn, p.nchunks * (p.halo ? 3 : 1),
                                                        p.mode == tg::kConvFwd));

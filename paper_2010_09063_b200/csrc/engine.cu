@@ -178,7 +178,15 @@ struct Engine {
   bool pool_generic = false;    // PGB_POOL_GENERIC=1: the generic pooling kernels  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
   bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
   bool tma_dx(const ConvGeom& g) const { return use_tma && tg::conv_ok(g); }
-  bool tma_dw(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && tma_all; }
+  bool tma_dw(const ConvGeom& g) const {
+    return use_tma && tg::conv_ok(g) && (tma_all || dwh_sel(g));
+  }
+  // per-example dW on the halo kernel (tma_dw_halo_kernel) for C >= dwh_min_c
+  // (PGB_NO_DW_HALO=1: off; PGB_DWH_MIN_C; PGB_DWH_ROT: accumulators per
+  // kernel row, 1 or 2)
+  bool dw_halo = true;
+  int dwh_min_c = 16, dwh_rot = 1;
+  bool dwh_sel(const ConvGeom& g) const { return dw_halo && tg::dwh_ok(g) && g.C >= dwh_min_c; }
   // scratch operands of the TMA GEMMs, each as its 3xTF32 (hi, lo) pair: the
   // A operand (NHWC copy / shifted copies), the B operand (permuted weights /
   // the dW cotangent)
@@ -542,9 +550,13 @@ struct Engine {
   // sum; returns the tiles per example (the tile_sq row length)
   int tma_conv_dw(cudaStream_t s, const ConvGeom& g, int Bi, const float* x, const float* gout,
                   float* stack, double* tile_sq) {
-    const int HW = g.H * g.W, bn = tg::pick_bn(g.D);
+    const bool halo = dwh_sel(g);
+    const int HW = g.H * g.W, bn = halo ? tg::kDwhBN : tg::pick_bn(g.D);
     int Cr, T, big, mtiles;
-    tg::dw_tiling(g.C, Cr, T, big, mtiles);
+    if (halo)
+      tg::dwh_tiling(g.C, Cr, T, mtiles), big = 0;
+    else
+      tg::dw_tiling(g.C, Cr, T, big, mtiles);
     const int bx = g.W, by = 32 / g.W;
     const long long total = (long long)Bi * g.C * HW;
     tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, d_nhwc, d_nhwc_lo, total,
@@ -574,6 +586,11 @@ struct Engine {
     p.tiles = ntiles * mtiles;
     p.out = stack;
     p.tile_sq = tile_sq;
+    if (halo) {
+      p.rot = dwh_rot;
+      tg::launch_dwh(p, dim3(ntiles, mtiles, Bi), s);
+      return p.tiles;
+    }
     tg::launch(p, bn, dim3(ntiles, mtiles, Bi), s);
     return p.tiles;
   }
@@ -655,6 +672,9 @@ struct Engine {
     ghost_enabled = std::getenv("PGB_NO_GHOST") == nullptr;
     no_ksplit = std::getenv("PGB_NO_KSPLIT") != nullptr;
     no_halo = std::getenv("PGB_NO_HALO") != nullptr;
+    dw_halo = std::getenv("PGB_NO_DW_HALO") == nullptr;
+    dwh_min_c = env_int("PGB_DWH_MIN_C", 16);
+    dwh_rot = std::min(2, env_int("PGB_DWH_ROT", 1));
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -713,6 +733,10 @@ struct Engine {
           int Cr, T, big, mt;
           tg::dw_tiling(g.C, Cr, T, big, mt);
           tiles = std::max(tiles, mt * ((g.D + tg::pick_bn(g.D) - 1) / tg::pick_bn(g.D)));
+          if (tg::dwh_ok(g)) {
+            tg::dwh_tiling(g.C, Cr, T, mt);
+            tiles = std::max(tiles, mt * ((g.D + tg::kDwhBN - 1) / tg::kDwhBN));
+          }
           const int64_t hw = (int64_t)g.H * g.W;
           nhwc = std::max(nhwc, B * hw * std::max(tg::round32(g.C), tg::round32(g.D)));
           nhwc = std::max(nhwc, 3 * B * hw * g.C);  // the dW input's shifted copies

@@ -83,6 +83,8 @@ struct alignas(64) Params {
   int ex_per, nex;   // dw-sum: examples per split, examples in total
   int ksplit;        // fwd / dx / plain: K splits (tile z); > 1: raw tiles to ws
   int halo;          // fwd / dx: halo stages (chunk = (kernel column v, 32 channels))
+  int rot;           // dw halo: accumulators per kernel row (1: two TMEM buffers; 2: one)
+  int narrow;        // folded tiles: the lo.(hi) MMA at N = BN (no lo.lo product)
   float* ws;         // dw-sum: split workspace [z][mt][n][128 rows]
   // epilogue
   float* out;
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
     // ---- MMA issuer ----
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(kBM, kFold ? 2 * BN : (BN < 16 ? 16 : BN));
+      constexpr uint32_t idesc_lo = tc::idesc_tf32(kBM, BN < 16 ? 16 : BN);
       int g = 0, lt = 0;
       for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
         int nt_, mt_, z_;
@@ -412,7 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
                 // [Bhi; Blo] is one 2 BN-row operand starting at bh
                 tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
                              (qa >= NACC || k) ? 1u : 0u);
-                tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
+                if (p.narrow)
+                  tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc_lo, 1u);
+                else
+                  tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc, 1u);
               } else {
                 const uint32_t dcorr = buf + (uint32_t)NACC * kAccStride;
                 tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
@@ -554,7 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
               c = (mt - tap * cgs) * kBM + r;
             } else {
               const int sl = r / p.Cr;
-              tap = mt * p.T + sl;
+              // (rows past the T slots -- 128 % Cr of them -- hold no tap)
+              tap = sl < p.T ? mt * p.T + sl : 9;
               c = r - sl * p.Cr;
             }
             if (tap < 9 && c < p.C) {
@@ -596,6 +603,234 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
 template <int BN, bool H = false>
 inline size_t smem_bytes() {
   return sizeof(Smem<BN, H>) + 1024;
+}
+
+// ---------------------------------------------------------------------------
+// Per-example dW with halo reuse (3x3 / stride 1 / pad 1, W a multiple of 8,
+// W <= 32, C <= 128, 32 output channels per tile). The dW of example z is
+//   dW[d][c][u][v] = sum_p' xv[c][p'] g[d][p' - (u - 1) W]
+// over the flattened positions p', xv the column-shifted copy v of the input
+// (shift3_kernel: the +-1 column taps as whole copies, since a SWIZZLE_128B
+// box starts on a 16-byte boundary). A stage is one K chunk of 32 positions:
+// operand A = the three copies v (M rows = (v, c), Cr rows per copy) at
+// [p0, p0 + 32); operand B = the cotangent at [p0 - W, p0 + 32 + W) (1 + W/16
+// boxes of 32, zeros outside the image). The kernel row u reads B at a K
+// offset of (2 - u) W positions -- a multiple of the 8-position MMA K step, so
+// each step's descriptor starts inside one box -- into its own accumulator.
+// Each input and cotangent element thus crosses L2 -> SMEM once per chunk
+// (the cotangent once per box overlap) instead of once per tap: the tap-slot
+// tiling of tma_gemm_kernel<kConvDw> re-reads both for every tap.
+// Epilogue: the reference's stack layout (B, D, C, 3, 3) (strategies.cpp:156-170)
+// and the tile's squared sum (fp64) for the per-example norm.
+// ---------------------------------------------------------------------------
+constexpr int kDwhBN = 32, kDwhStages = 3, kDwhBoxes = 3;
+
+// 32 consecutive TMEM columns of the warp's 32 lanes (no wait: the caller
+// issues tcgen05.wait::ld once for a batch of loads)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+struct DwhSmem {
+  float a_hi[kDwhStages][kBM * kBK];
+  float a_lo[kDwhStages][kBM * kBK];
+  float b[kDwhStages][kDwhBoxes][2][kDwhBN * kBK];  // per box: hi rows, then lo rows
+  uint64_t full[kDwhStages], empty[kDwhStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem;
+  double sq[4];
+  alignas(16) float stage[kDwhBN * 32 * 9];  // the tile's output rows (d, c, u, v), copied out coalesced
+};
+
+__global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  DwhSmem& S = *reinterpret_cast<DwhSmem*>(
+      (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int NS = kDwhStages, BN = kDwhBN;
+  constexpr uint32_t kCols = 512, kAcc = 2 * BN;  // folded accumulator: hi cols, then lo cols
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int total = p.ntn * p.ntm * p.nz;
+  const int rot = p.rot, NB = rot == 1 ? 2 : 1;
+  const uint32_t buf_cols = kCols / NB;
+  const int nbox = 1 + (2 * p.W + kBK - 1) / kBK;  // cotangent halo boxes (W = 8, 16: 2; 32: 3)
+  if (warp == 1) tc::tmem_alloc(&S.tmem, kCols);
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) {
+      tc::mbar_init(&S.full[s], 1);
+      tc::mbar_init(&S.empty[s], 3);  // one commit per issuing warp
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&S.acc_full[b], 3);
+      tc::mbar_init(&S.acc_empty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.ta_lo) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&p.tb_lo) : "memory");
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem;
+
+  if (warp == 0) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      int g = 0;
+      for (int tl = blockIdx.x; tl < total; tl += gridDim.x) {
+        int nt, mt, z;
+        tile_coords(p, tl, nt, mt, z);
+        const uint32_t bytes = 2u * ((uint32_t)(3 * p.Cr) * kBK * 4 + (uint32_t)(nbox * BN) * kBK * 4);
+        for (int q = 0; q < p.nchunks; ++q, ++g) {
+          const int s = g % NS;
+          if (g >= NS) tc::mbar_wait(&S.empty[s], ((g / NS) - 1) & 1);
+          const uint32_t bar = smem_u32(&S.full[s]);
+          expect_tx(&S.full[s], bytes);
+          const int p0 = q * kBK;
+          for (int v = 0; v < 3; ++v) {  // rows (v, channel mt * Cr + c)
+            const uint32_t o = (uint32_t)(v * p.Cr) * kBK * 4;
+            tma_4d(smem_u32(S.a_hi[s]) + o, &p.ta, p0, mt * p.Cr, z, v, bar);
+            tma_4d(smem_u32(S.a_lo[s]) + o, &p.ta_lo, p0, mt * p.Cr, z, v, bar);
+          }
+          for (int i = 0; i < nbox; ++i) {
+            const int pb = p0 - p.W + i * kBK;
+            tma_3d(smem_u32(S.b[s][i][0]), &p.tb, pb, nt * BN, z, bar);
+            tma_3d(smem_u32(S.b[s][i][1]), &p.tb_lo, pb, nt * BN, z, bar);
+          }
+        }
+      }
+    }
+  } else if (warp <= 3) {
+    // ---- MMA issuers: warp 1 + u issues kernel row u into its own
+    // accumulator (one thread issues an MMA only every ~50-120 cycles; three
+    // issuers keep the tensor core fed, scripts/umma_rate.py) ----
+    if (lane == 0) {
+      const int u = warp - 1;
+      const bool lo_narrow = p.narrow;
+      constexpr uint32_t idesc = tc::idesc_tf32(kBM, 2 * BN);
+      constexpr uint32_t idesc_lo = tc::idesc_tf32(kBM, BN);
+      int g = 0, lt = 0;
+      for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
+        const int bsel = NB == 2 ? (lt & 1) : 0;
+        const int use = NB == 2 ? (lt >> 1) : lt;
+        if (use > 0) tc::mbar_wait(&S.acc_empty[bsel], (use - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t buf = tmem + (uint32_t)bsel * buf_cols;
+        for (int q = 0; q < p.nchunks; ++q, ++g) {
+          const int s = g % NS;
+          tc::mbar_wait(&S.full[s], (g / NS) & 1);
+          tc::fence_after_sync();
+          const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
+          const int r = rot == 1 ? 0 : (q & 1);
+          const bool first = q < rot;
+          const uint32_t d = buf + (uint32_t)(u * rot + r) * kAcc;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const int o = 8 * k + (2 - u) * p.W;  // cotangent position offset in the halo
+            const uint32_t bh = smem_u32(S.b[s][o >> 5][0]) + 32u * ((o >> 3) & 3);
+            tc::mma_tf32(d, desc_sw128(ah + 32u * k), desc_sw128(bh), idesc,
+                         (!first || k) ? 1u : 0u);
+            // Alo.Bhi only (N = BN): the lo.lo product is below the split's error
+            if (lo_narrow)
+              tc::mma_tf32(d, desc_sw128(al + 32u * k), desc_sw128(bh), idesc_lo, 1u);
+            else
+              tc::mma_tf32(d, desc_sw128(al + 32u * k), desc_sw128(bh), idesc, 1u);
+          }
+          tc::commit(&S.empty[s]);
+        }
+        tc::commit(&S.acc_full[bsel]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> the stack ----
+    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const int v = r / p.Cr, cl = r - v * p.Cr;
+    const int used = min(rot, p.nchunks);
+    int lt = 0;
+    for (int tl = blockIdx.x; tl < total; tl += gridDim.x, ++lt) {
+      int nt, mt, z;
+      tile_coords(p, tl, nt, mt, z);
+      const int bsel = NB == 2 ? (lt & 1) : 0;
+      const int use = NB == 2 ? (lt >> 1) : lt;
+      tc::mbar_wait(&S.acc_full[bsel], use & 1);
+      tc::fence_after_sync();
+      const uint32_t lane_base = tmem + (uint32_t)bsel * buf_cols + ((uint32_t)(q4 * 32) << 16);
+      const int c0t = mt * p.Cr, cval = min(p.Cr, p.C - c0t);  // the tile's channels
+      const bool ok = v < 3 && cl < cval;
+      float* sg = S.stage + cl * 9 + v;
+      double sqj[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // independent fp64 chains
+      const int nd = min(BN, p.N - nt * BN);
+#pragma unroll 1
+      for (int u = 0; u < 3; ++u) {
+        uint32_t h[BN], l[BN];
+        const uint32_t base = lane_base + (uint32_t)(u * rot) * kAcc;
+        tmem_ld32_nowait(base, h);       // hi.hi + lo.hi
+        tmem_ld32_nowait(base + BN, l);  // hi.lo + lo.lo
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float a[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) a[j] = __uint_as_float(h[j]) + __uint_as_float(l[j]);
+        for (int e = 1; e < used; ++e) {
+          tmem_ld32_nowait(base + (uint32_t)e * kAcc, h);
+          tmem_ld32_nowait(base + (uint32_t)e * kAcc + BN, l);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < BN; ++j) a[j] += __uint_as_float(h[j]) + __uint_as_float(l[j]);
+        }
+        if (ok) {
+          // stage[d][c][u][v]: lanes are consecutive c, a stride of 9 words (conflict-free)
+#pragma unroll
+          for (int j = 0; j < BN; ++j)
+            if (j < nd) {
+              sg[j * cval * 9 + 3 * u] = a[j];
+              sqj[j & 7] = fma((double)a[j], (double)a[j], sqj[j & 7]);
+            }
+        }
+      }
+      double sq = ((sqj[0] + sqj[1]) + (sqj[2] + sqj[3])) + ((sqj[4] + sqj[5]) + (sqj[6] + sqj[7]));
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.acc_empty[bsel]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) S.sq[q4] = sq;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 128 && p.tile_sq)
+        p.tile_sq[(size_t)z * p.tiles + mt * p.ntn + nt] = ((S.sq[0] + S.sq[1]) + S.sq[2]) + S.sq[3];
+      // the staged rows: per output channel d, cval * 9 contiguous floats of
+      // the reference's stack (B, D, C, 3, 3) (strategies.cpp:156-170)
+      {
+        const int row = cval * 9;
+        float* dst = p.out + ((size_t)z * p.D + nt * BN) * p.C * 9 + (size_t)c0t * 9;
+        const size_t ld = (size_t)p.C * 9;
+        if (row % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          const int r4 = row / 4;
+          for (int e = t - 128; e < nd * r4; e += 128) {
+            const int d = e / r4, k = e - d * r4;
+            *reinterpret_cast<float4*>(dst + d * ld + 4 * k) =
+                *reinterpret_cast<const float4*>(S.stage + d * row + 4 * k);
+          }
+        } else {
+          for (int e = t - 128; e < nd * row; e += 128) {
+            const int d = e / row, k = e - d * row;
+            dst[d * ld + k] = S.stage[e];
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, kCols);
 }
 
 }  // namespace tg
@@ -946,12 +1181,42 @@ inline void launch_bn(const Params& p, int ctas, cudaStream_t s) {
   tma_gemm_kernel<BN, false><<<ctas, kThreads, smem_bytes<BN, false>(), s>>>(p);
 }
 
+inline size_t dwh_smem_bytes() { return sizeof(DwhSmem) + 1024; }
+
+// folded tiles issue lo.hi at N = BN, dropping the lo.lo product (PGB_LOLO=1:
+// the 2 BN-wide lo MMA, lo.lo included; read once per process)
+inline bool narrow_lo() {
+  static const bool v = std::getenv("PGB_LOLO") == nullptr;
+  return v;
+}
+
+// tiles: (N tiles, M tiles, examples)
+inline void launch_dwh(const Params& p0, dim3 tiles, cudaStream_t s) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(tma_dw_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dwh_smem_bytes());
+    attr_dev = dev;
+  }
+  Params p = p0;
+  p.ntn = (int)tiles.x;
+  p.ntm = (int)tiles.y;
+  p.nz = (int)tiles.z;
+  p.narrow = narrow_lo() ? 1 : 0;
+  const long long total = (long long)p.ntn * p.ntm * p.nz;
+  const int ctas = (int)std::min<long long>(total, num_sms());
+  tma_dw_halo_kernel<<<ctas, kThreads, dwh_smem_bytes(), s>>>(p);
+}
+
 // tiles: (N tiles, M tiles, GEMMs); one persistent CTA per SM walks them
 inline void launch(const Params& p0, int bn, dim3 tiles, cudaStream_t s) {
   Params p = p0;
   p.ntn = (int)tiles.x;
   p.ntm = (int)tiles.y;
   p.nz = (int)tiles.z;
+  p.narrow = narrow_lo() ? 1 : 0;
   const long long total = (long long)p.ntn * p.ntm * p.nz;
   const int ctas = (int)std::min<long long>(total, num_sms());
   switch (bn) {
@@ -969,6 +1234,19 @@ inline bool conv_ok(const ConvGeom& g) {
   if (!(g.W == 4 || g.W == 8 || g.W == 16 || g.W == 32)) return false;
   const int hw = g.H * g.W;
   return hw >= 128 ? hw % 128 == 0 : 128 % hw == 0;
+}
+
+// the halo per-example dW fits: 3x3 / stride 1 / pad 1, W a multiple of 8
+// up to 32, C <= 128
+inline bool dwh_ok(const ConvGeom& g) {
+  return conv_ok(g) && g.W % 8 == 0 && g.W <= 32 && g.C <= 128;
+}
+
+// halo per-example dW M tiling: M rows (v, c) for Cr channels per tile
+inline void dwh_tiling(int C, int& Cr, int& T, int& mtiles) {
+  Cr = std::min(32, (C + 7) / 8 * 8);  // channels per tile (rows per copy v)
+  T = 3;
+  mtiles = (C + Cr - 1) / Cr;
 }
 
 inline int round32(int c) { return (c + 31) / 32 * 32; }

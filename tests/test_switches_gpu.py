@@ -2,7 +2,10 @@
 against each other:
 
 * ghost conv norms + clip-scaled summed dW (default) and per-example stacks
-  (PGB_NO_GHOST=1), halo TMA stages (default) and one box per tap
+  (PGB_NO_GHOST=1), per-example dW on the halo kernel for C >= 16 (default),
+  for every layer (PGB_DWH_MIN_C=1; with PGB_NO_GHOST=1 also the 8x8 layers),
+  with two accumulators per kernel row (PGB_DWH_ROT=2) or on the register-gather
+  GEMM (PGB_NO_DW_HALO=1), halo TMA stages (default) and one box per tap
   (PGB_NO_HALO=1), batch-invariant K splits (default) and none
   (PGB_NO_KSPLIT=1): each a full DPSGD step of the CIFAR CNN against the oracle
   (norms rel 1e-5, exact clip counts, parameters within a few ulps + 1e-5 of
@@ -20,18 +23,23 @@ TOL = 1e-5
 
 
 def _engine(P, desc, B, strat, monkeypatch, env):
-    for k in env:
-        monkeypatch.setenv(k, "1")
+    # env entries: "NAME" (set to 1) or "NAME=VALUE"
+    kv = [(e.split("=", 1) + ["1"])[:2] for e in env]
+    for k, v in kv:
+        monkeypatch.setenv(k, v)
     m = P.build_from_desc(desc, 0)
     e = P.GradEngine(m, P.Strategy(strat), B)
-    for k in env:
+    for k, _ in kv:
         monkeypatch.delenv(k)
     return m, e
 
 
 @pytest.mark.parametrize("env", [(), ("PGB_NO_GHOST",), ("PGB_NO_HALO",), ("PGB_NO_KSPLIT",),
-                                 ("PGB_NO_GHOST", "PGB_NO_HALO")],
-                         ids=["default", "no_ghost", "no_halo", "no_ksplit", "no_ghost_no_halo"])
+                                 ("PGB_NO_GHOST", "PGB_NO_HALO"), ("PGB_NO_DW_HALO",),
+                                 ("PGB_DWH_MIN_C=1",), ("PGB_DWH_ROT=2",),
+                                 ("PGB_NO_GHOST", "PGB_DWH_MIN_C=1")],
+                         ids=["default", "no_ghost", "no_halo", "no_ksplit", "no_ghost_no_halo",
+                              "no_dw_halo", "dw_halo_all", "dw_halo_rot2", "no_ghost_dw_halo_all"])
 def test_cifar_step_variants_match_oracle(P, O, env, monkeypatch):
     B = 4
     desc = P.build_desc(P.ModelKind.cifar_cnn)

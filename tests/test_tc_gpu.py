@@ -64,13 +64,21 @@ def test_tma_gemm_3xtf32(P, M, N, K):
 
 @pytest.mark.parametrize("C,H,W,D", [(3, 32, 32, 10), (32, 32, 32, 16), (32, 16, 16, 64),
                                      (64, 8, 8, 10), (128, 8, 8, 32), (128, 4, 4, 256),
-                                     (256, 4, 4, 10)])
-def test_tma_conv_gemms_match_oracle(P, O, monkeypatch, C, H, W, D):
+                                     (256, 4, 4, 10), (16, 8, 32, 40), (48, 16, 8, 96)])
+@pytest.mark.parametrize("env", ["PGB_TMA_ALL=1", "PGB_TMA_ALL=1 PGB_DWH_MIN_C=1",
+                                 "PGB_DWH_MIN_C=1 PGB_DWH_ROT=2", "PGB_TMA_ALL=1 PGB_NO_DW_HALO=1"],
+                         ids=["tma_all", "tma_all_dwh_all", "dwh_all_rot2", "tma_all_no_dwh"])
+def test_tma_conv_gemms_match_oracle(P, O, monkeypatch, C, H, W, D, env):
     """Every 3x3 conv GEMM on the TMA engine (PGB_TMA_ALL=1: forward,
-    per-example dW and input gradient, whatever the per-kind default picks):
-    a conv -> relu -> conv -> relu -> global-avgpool model over the geometries
-    of the CIFAR CNN, per-example gradients and norms against the oracle."""
-    monkeypatch.setenv("PGB_TMA_ALL", "1")
+    per-example dW and input gradient, whatever the per-kind default picks;
+    the per-example dW on the halo kernel for C >= 16 or, PGB_DWH_MIN_C=1, for
+    every channel count, else the tap-slot TMA GEMM): a conv -> relu -> conv ->
+    relu -> global-avgpool model over the geometries of the CIFAR CNN and a few
+    ragged ones (W != H, channel counts off the 32 grid), per-example gradients
+    and norms against the oracle."""
+    for kv in env.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     layers = [P.LayerSpec(P.LayerKind.conv, C, D, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
               P.LayerSpec(P.LayerKind.conv, D, 10, 3, 1, 1), P.LayerSpec(P.LayerKind.relu),
               P.LayerSpec(P.LayerKind.global_avgpool)]

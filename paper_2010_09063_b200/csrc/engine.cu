@@ -186,6 +186,8 @@ struct Engine {
   // kernel row, 1 or 2)
   bool dw_halo = true;
   int dwh_min_c = 16, dwh_rot = 1;
+  bool dwh_raw = true;     // PGB_DWH_SPLIT=1: hi / lo operand tensors split by the layout kernels
+  int dw_prep_kernels = 2;  // layout kernels of the last tma_conv_dw
   bool dwh_sel(const ConvGeom& g) const { return dw_halo && tg::dwh_ok(g) && g.C >= dwh_min_c; }
   // scratch operands of the TMA GEMMs, each as its 3xTF32 (hi, lo) pair: the
   // A operand (NHWC copy / shifted copies), the B operand (permuted weights /
@@ -559,10 +561,14 @@ struct Engine {
       tg::dw_tiling(g.C, Cr, T, big, mtiles);
     const int bx = g.W, by = 32 / g.W;
     const long long total = (long long)Bi * g.C * HW;
-    tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, d_nhwc, d_nhwc_lo, total,
-                                                                    g.W);
+    // halo kernel with plain fp32 operands (it splits the lo halves itself):
+    // the shifted copies only, the cotangent read in place
+    const bool raw = halo && dwh_raw;
+    tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, d_nhwc, raw ? nullptr : d_nhwc_lo,
+                                                              total, g.W);
     const long long gt = (long long)Bi * g.D * HW;
-    tg::split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(gout, d_wt, d_wt_lo, gt);
+    if (!raw) tg::split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(gout, d_wt, d_wt_lo, gt);
+    dw_prep_kernels = raw ? 1 : 2;
     tg::Params p{};
     // A: the shifted copies [v][n][c][p] (positions flattened); B: gout [n][d][p]
     const uint64_t da[4] = {(uint64_t)HW, (uint64_t)g.C, (uint64_t)Bi, 3};
@@ -573,8 +579,9 @@ struct Engine {
     const uint64_t db[3] = {(uint64_t)HW, (uint64_t)g.D, (uint64_t)Bi};
     const uint64_t sb[2] = {4ull * HW, 4ull * HW * g.D};
     const uint32_t bb[3] = {32, (uint32_t)bn, 1};
-    tg::make_map(&p.tb, d_wt, 3, db, sb, bb);
-    tg::make_map(&p.tb_lo, d_wt_lo, 3, db, sb, bb);
+    tg::make_map(&p.tb, raw ? gout : d_wt, 3, db, sb, bb);
+    tg::make_map(&p.tb_lo, raw ? gout : d_wt_lo, 3, db, sb, bb);
+    p.raw = raw ? 1 : 0;
     p.mode = tg::kConvDw;
     p.M = mtiles * 128;
     p.N = g.D;
@@ -675,6 +682,7 @@ struct Engine {
     dw_halo = std::getenv("PGB_NO_DW_HALO") == nullptr;
     dwh_min_c = env_int("PGB_DWH_MIN_C", 16);
     dwh_rot = std::min(2, env_int("PGB_DWH_ROT", 1));
+    dwh_raw = std::getenv("PGB_DWH_SPLIT") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -1489,7 +1497,7 @@ struct Engine {
             nk += mark(s, "conv_dw_gram");
           } else if (tma_dw(gg)) {
             const int tiles = tma_conv_dw(s, gg, Bi, in, gcur, sW, d_tile_sq);
-            nk += mark(s, "conv_dw_pex_tma") + 2;
+            nk += mark(s, "conv_dw_pex_tma") + dw_prep_kernels;
             tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(d_tile_sq, tiles, Bi, d_parts,
                                                                    nparts, L.pblock);
             nk += mark(s, "conv_dw_norm");

@@ -85,6 +85,7 @@ struct alignas(64) Params {
   int halo;          // fwd / dx: halo stages (chunk = (kernel column v, 32 channels))
   int rot;           // dw halo: accumulators per kernel row (1: two TMEM buffers; 2: one)
   int narrow;        // folded tiles: the lo.(hi) MMA at N = BN (no lo.lo product)
+  int raw;           // dw halo: plain fp32 operands, lo halves split in the kernel
   float* ws;         // dw-sum: split workspace [z][mt][n][128 rows]
   // epilogue
   float* out;
@@ -642,14 +643,26 @@ struct DwhSmem {
   float a_hi[kDwhStages][kBM * kBK];
   float a_lo[kDwhStages][kBM * kBK];
   float b[kDwhStages][kDwhBoxes][2][kDwhBN * kBK];  // per box: hi rows, then lo rows
-  uint64_t full[kDwhStages], empty[kDwhStages];
+  uint64_t full[kDwhStages], empty[kDwhStages], split[kDwhStages];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem;
   double sq[4];
   alignas(16) float stage[kDwhBN * 32 * 9];  // the tile's output rows (d, c, u, v), copied out coalesced
 };
 
-__global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_constant__ Params p) {
+// RAW: the operands arrive as plain fp32 (one TMA load each) and warps 8-11
+// write each stage's lo halves, x - trunc_tf32(x), next to them (the tensor
+// core reads the fp32 tile itself as the truncated hi); else the hi and lo
+// tensors are both loaded (split by the layout kernels).
+constexpr int kDwhRawThreads = 384;
+__device__ __forceinline__ float4 lo_of(float4 x) {
+  const auto lo1 = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u); };
+  return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w));
+}
+
+template <bool RAW>
+__global__ void __launch_bounds__(RAW ? kDwhRawThreads : kThreads, 1)
+    tma_dw_halo_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char raw[];
   DwhSmem& S = *reinterpret_cast<DwhSmem*>(
       (reinterpret_cast<uintptr_t>(raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -665,6 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_c
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 3);  // one commit per issuing warp
+      tc::mbar_init(&S.split[s], 4);  // one arrival per splitting warp
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.acc_full[b], 3);
@@ -688,7 +702,8 @@ __global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_c
       for (int tl = blockIdx.x; tl < total; tl += gridDim.x) {
         int nt, mt, z;
         tile_coords(p, tl, nt, mt, z);
-        const uint32_t bytes = 2u * ((uint32_t)(3 * p.Cr) * kBK * 4 + (uint32_t)(nbox * BN) * kBK * 4);
+        const uint32_t bytes =
+            (RAW ? 1u : 2u) * ((uint32_t)(3 * p.Cr) * kBK * 4 + (uint32_t)(nbox * BN) * kBK * 4);
         for (int q = 0; q < p.nchunks; ++q, ++g) {
           const int s = g % NS;
           if (g >= NS) tc::mbar_wait(&S.empty[s], ((g / NS) - 1) & 1);
@@ -698,12 +713,12 @@ __global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_c
           for (int v = 0; v < 3; ++v) {  // rows (v, channel mt * Cr + c)
             const uint32_t o = (uint32_t)(v * p.Cr) * kBK * 4;
             tma_4d(smem_u32(S.a_hi[s]) + o, &p.ta, p0, mt * p.Cr, z, v, bar);
-            tma_4d(smem_u32(S.a_lo[s]) + o, &p.ta_lo, p0, mt * p.Cr, z, v, bar);
+            if (!RAW) tma_4d(smem_u32(S.a_lo[s]) + o, &p.ta_lo, p0, mt * p.Cr, z, v, bar);
           }
           for (int i = 0; i < nbox; ++i) {
             const int pb = p0 - p.W + i * kBK;
             tma_3d(smem_u32(S.b[s][i][0]), &p.tb, pb, nt * BN, z, bar);
-            tma_3d(smem_u32(S.b[s][i][1]), &p.tb_lo, pb, nt * BN, z, bar);
+            if (!RAW) tma_3d(smem_u32(S.b[s][i][1]), &p.tb_lo, pb, nt * BN, z, bar);
           }
         }
       }
@@ -726,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_c
         const uint32_t buf = tmem + (uint32_t)bsel * buf_cols;
         for (int q = 0; q < p.nchunks; ++q, ++g) {
           const int s = g % NS;
-          tc::mbar_wait(&S.full[s], (g / NS) & 1);
+          tc::mbar_wait(RAW ? &S.split[s] : &S.full[s], (g / NS) & 1);
           tc::fence_after_sync();
           const uint32_t ah = smem_u32(S.a_hi[s]), al = smem_u32(S.a_lo[s]);
           const int r = rot == 1 ? 0 : (q & 1);
@@ -749,7 +764,28 @@ __global__ void __launch_bounds__(kThreads, 1) tma_dw_halo_kernel(const __grid_c
         tc::commit(&S.acc_full[bsel]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (RAW && warp >= 8) {
+    // ---- lo halves of each stage (both operands), then release it to the MMAs ----
+    const int ct = t - 256;
+    const int na4 = 3 * p.Cr * kBK / 4, nb4 = BN * kBK / 4;
+    int g = 0;
+    for (int tl = blockIdx.x; tl < total; tl += gridDim.x)
+      for (int q = 0; q < p.nchunks; ++q, ++g) {
+        const int s = g % NS;
+        tc::mbar_wait(&S.full[s], (g / NS) & 1);
+        const float4* ah = reinterpret_cast<const float4*>(S.a_hi[s]);
+        float4* al = reinterpret_cast<float4*>(S.a_lo[s]);
+        for (int e = ct; e < na4; e += 128) al[e] = lo_of(ah[e]);
+        for (int i = 0; i < nbox; ++i) {
+          const float4* bh = reinterpret_cast<const float4*>(S.b[s][i][0]);
+          float4* bl = reinterpret_cast<float4*>(S.b[s][i][1]);
+          for (int e = ct; e < nb4; e += 128) bl[e] = lo_of(bh[e]);
+        }
+        tc::fence_proxy_async();  // generic-proxy writes -> the tensor core's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.split[s]);
+      }
+  } else if (warp >= 4 && warp < 8) {
     // ---- epilogue: TMEM -> registers -> the stack ----
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const int v = r / p.Cr, cl = r - v * p.Cr;
@@ -887,6 +923,12 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
       const float c = src[i];
       const float l = x > 0 ? src[i - 1] : 0.0f;
       const float r = x + 1 < (unsigned)W ? src[i + 1] : 0.0f;
+      if (!dst_lo) {  // plain fp32 copies (the consumer splits them)
+        dst[i] = l;
+        dst[T + i] = c;
+        dst[2ull * T + i] = r;
+        continue;
+      }
       split2(l, dst[i], dst_lo[i]);
       split2(c, dst[T + i], dst_lo[T + i]);
       split2(r, dst[2ull * T + i], dst_lo[2ull * T + i]);
@@ -898,7 +940,11 @@ __global__ void shift3_kernel(const float* __restrict__ src, float* __restrict__
     const int v = (int)(e / total);
     const long long i = e - v * total;
     const int x = (int)(i % W), xs = x + v - 1;
-    split2((xs >= 0 && xs < W) ? src[i + v - 1] : 0.0f, dst[e], dst_lo[e]);
+    const float val = (xs >= 0 && xs < W) ? src[i + v - 1] : 0.0f;
+    if (dst_lo)
+      split2(val, dst[e], dst_lo[e]);
+    else
+      dst[e] = val;
   }
 }
 
@@ -1196,7 +1242,9 @@ inline void launch_dwh(const Params& p0, dim3 tiles, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(tma_dw_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tma_dw_halo_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dwh_smem_bytes());
+    cudaFuncSetAttribute(tma_dw_halo_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)dwh_smem_bytes());
     attr_dev = dev;
   }
@@ -1207,7 +1255,10 @@ inline void launch_dwh(const Params& p0, dim3 tiles, cudaStream_t s) {
   p.narrow = narrow_lo() ? 1 : 0;
   const long long total = (long long)p.ntn * p.ntm * p.nz;
   const int ctas = (int)std::min<long long>(total, num_sms());
-  tma_dw_halo_kernel<<<ctas, kThreads, dwh_smem_bytes(), s>>>(p);
+  if (p.raw)
+    tma_dw_halo_kernel<true><<<ctas, kDwhRawThreads, dwh_smem_bytes(), s>>>(p);
+  else
+    tma_dw_halo_kernel<false><<<ctas, kThreads, dwh_smem_bytes(), s>>>(p);
 }
 
 // tiles: (N tiles, M tiles, GEMMs); one persistent CTA per SM walks them

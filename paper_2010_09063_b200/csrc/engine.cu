@@ -187,6 +187,9 @@ struct Engine {
   bool dw_halo = true;
   int dwh_min_c = 16, dwh_rot = 1;
   bool dwh_raw = true;     // PGB_DWH_SPLIT=1: hi / lo operand tensors split by the layout kernels
+  // forward / input-gradient / clipped-sum dW GEMMs: operand A as plain fp32,
+  // its lo half split in the kernel (PGB_TMA_SPLIT=1: hi / lo tensors)
+  bool raw_a = true;
   int dw_prep_kernels = 2;  // layout kernels of the last tma_conv_dw
   bool dwh_sel(const ConvGeom& g) const { return dw_halo && tg::dwh_ok(g) && g.C >= dwh_min_c; }
   // scratch operands of the TMA GEMMs, each as its 3xTF32 (hi, lo) pair: the
@@ -419,7 +422,7 @@ struct Engine {
                    const float* bias, float* out, bool relu, int layer = -1) {
     const int Cp = tg::round32(g.C), HW = g.H * g.W, bn = tg::pick_bn(g.D);
     tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Cp / 32, Bi), dim3(32, 8), 0, s>>>(
-        x, d_nhwc, d_nhwc_lo, g.C, HW, Cp);
+        x, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.C, HW, Cp);
     const bool pre = layer >= 0 && d_wall && wall_fwd[layer] >= 0;
     float* wt = pre ? d_wall + wall_fwd[layer] : d_wt;
     float* wt_lo = pre ? d_wall_lo + wall_fwd[layer] : d_wt_lo;
@@ -442,6 +445,7 @@ struct Engine {
     tg::make_map(&p.tb, wt, 2, db, sb, bb);
     tg::make_map(&p.tb_lo, wt_lo, 2, db, sb, bb);
     p.mode = tg::kConvFwd;
+    p.raw = raw_a ? 1 : 0;
     p.M = Bi * HW;
     p.N = g.D;
     p.nchunks = (halo ? 3 : 9) * Cp / 32;
@@ -514,7 +518,7 @@ struct Engine {
                   const float* mask, float* gx, int layer = -1) {
     const int Dp = tg::round32(g.D), HW = g.H * g.W, bn = tg::pick_bn(g.C);
     tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Dp / 32, Bi), dim3(32, 8), 0, s>>>(
-        gout, d_nhwc, d_nhwc_lo, g.D, HW, Dp);
+        gout, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.D, HW, Dp);
     const bool pre = layer >= 0 && d_wall && wall_dx[layer] >= 0;
     float* wt = pre ? d_wall + wall_dx[layer] : d_wt;
     float* wt_lo = pre ? d_wall_lo + wall_dx[layer] : d_wt_lo;
@@ -537,6 +541,7 @@ struct Engine {
     tg::make_map(&p.tb, wt, 2, db, sb, bb);
     tg::make_map(&p.tb_lo, wt_lo, 2, db, sb, bb);
     p.mode = tg::kConvDx;
+    p.raw = raw_a ? 1 : 0;
     p.M = Bi * HW;
     p.N = g.C;
     p.nchunks = (halo ? 3 : 9) * Dp / 32;
@@ -683,6 +688,7 @@ struct Engine {
     dwh_min_c = env_int("PGB_DWH_MIN_C", 16);
     dwh_rot = std::min(2, env_int("PGB_DWH_ROT", 1));
     dwh_raw = std::getenv("PGB_DWH_SPLIT") == nullptr;
+    raw_a = std::getenv("PGB_TMA_SPLIT") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -1841,8 +1847,8 @@ struct Engine {
       tg::dw_tiling(g.C, Cr, T, big, mtiles);
       const long long total = (long long)Bi * g.C * HW;
       const float* in = L.act_in;
-      tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(in, d_nhwc, d_nhwc_lo,
-                                                                      total, g.W);
+      tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(
+          in, d_nhwc, raw_a ? nullptr : d_nhwc_lo, total, g.W);
       const long long gt = (long long)Bi * g.D * HW;
       tg::scale_split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(L.gout, d_scale,
                                                                   (long long)g.D * HW, gt, d_wt,
@@ -1859,6 +1865,7 @@ struct Engine {
       tg::make_map(&p.tb, d_wt, 3, db, sb, bb);
       tg::make_map(&p.tb_lo, d_wt_lo, 3, db, sb, bb);
       p.mode = tg::kConvDwSum;
+      p.raw = raw_a ? 1 : 0;
       p.M = mtiles * 128;
       p.N = g.D;
       p.nchunks = (HW + 31) / 32;

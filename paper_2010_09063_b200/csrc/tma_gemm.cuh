@@ -139,7 +139,7 @@ struct Smem {
   float a_hi[S][RA * kBK];
   float a_lo[S][RA * kBK];
   float b[S][T][2][BN * kBK];  // per tap: hi rows, then lo rows (one 2 BN-row operand)
-  uint64_t full[S], empty[S];
+  uint64_t full[S], empty[S], split[S];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem;
   double sq[4];
@@ -199,6 +199,13 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(h);
 }
 
+// the lo half of a plain fp32 operand the tensor core reads as the truncated
+// tf32 hi: x - trunc_tf32(x) (exact in fp32)
+__device__ __forceinline__ float4 lo_of(float4 x) {
+  const auto lo1 = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u); };
+  return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w));
+}
+
 // the 3xTF32 pair of one value: hi = rna(x), lo = rna(x - hi)
 __device__ __forceinline__ void split2(float x, float& hi, float& lo) {
   hi = rna_tf32(x);
@@ -219,10 +226,11 @@ __device__ __forceinline__ uint32_t a_bytes(const Params& p, int mt) {
 // once for the lo tensors.
 __device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* ma,
                                             const CUtensorMap* mb, uint32_t da, uint32_t db,
-                                            int BN, int q, int mt, int nt, int z, uint32_t bar) {
+                                            int BN, int q, int mt, int nt, int z, uint32_t bar,
+                                            bool load_a = true) {
   switch (p.mode) {
     case kPlain:
-      tma_2d(da, ma, q * kBK, mt * kBM, bar);
+      if (load_a) tma_2d(da, ma, q * kBK, mt * kBM, bar);
       tma_2d(db, mb, q * kBK, nt * BN, bar);
       break;
     case kConvFwd:
@@ -234,14 +242,15 @@ __device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* 
       // forward: x + v - 1, y + u - 1; input gradient: the flipped tap
       const int dx = p.mode == kConvFwd ? v - 1 : 1 - v;
       const int dy = p.mode == kConvFwd ? u - 1 : 1 - u;
-      tma_4d(da, ma, cg * kBK, dx, y0 + dy, n0, bar);
+      if (load_a) tma_4d(da, ma, cg * kBK, dx, y0 + dy, n0, bar);
       tma_2d(db, mb, tap * p.Cg * kBK + cg * kBK, nt * BN, bar);
       break;
     }
     case kConvDw:
     case kConvDwSum: {
       const int p0 = q * kBK;  // first position of the chunk (flattened H*W)
-      if (p.big_c) {
+      if (!load_a) {
+      } else if (p.big_c) {
         const int cgs = p.C / kBM, tap = mt / cgs, c0 = (mt - tap * cgs) * kBM;
         const int u = tap / 3, v = tap - 3 * u;
         tma_4d(da, ma, p0 + (u - 1) * p.W, c0, z, v, bar);
@@ -259,7 +268,8 @@ __device__ __forceinline__ void issue_boxes(const Params& p, const CUtensorMap* 
   }
 }
 
-template <int BN, bool H>
+// RAW: operand A arrives as plain fp32 only (its lo half is split in the kernel)
+template <int BN, bool H, bool RAW>
 __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN, H>& S, int s, int q, int mt,
                                             int nt, int z) {
   const uint32_t bar = smem_u32(&S.full[s]);
@@ -273,7 +283,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN, H>& S, int
     const int m0 = mt * kBM, n0 = m0 / HW, y0 = (m0 - n0 * HW) / p.W;
     const int dx = p.mode == kConvFwd ? v - 1 : 1 - v;
     tma_4d(smem_u32(S.a_hi[s]), &p.ta, cg * kBK, dx, y0 - 1, n0, bar);
-    tma_4d(smem_u32(S.a_lo[s]), &p.ta_lo, cg * kBK, dx, y0 - 1, n0, bar);
+    if (!RAW) tma_4d(smem_u32(S.a_lo[s]), &p.ta_lo, cg * kBK, dx, y0 - 1, n0, bar);
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int k0 = (3 * u + v) * p.Cg * kBK + cg * kBK;
@@ -284,7 +294,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, Smem<BN, H>& S, int
     issue_boxes(p, &p.ta, &p.tb, smem_u32(S.a_hi[s]), smem_u32(S.b[s][0][0]), BN, q, mt, nt, z,
                 bar);
     issue_boxes(p, &p.ta_lo, &p.tb_lo, smem_u32(S.a_lo[s]), smem_u32(S.b[s][0][1]), BN, q, mt,
-                nt, z, bar);
+                nt, z, bar, !RAW);
   }
 }
 
@@ -322,8 +332,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& nt, int
 // The TMA ring runs across tile boundaries (the next tile's operands stream in
 // while this tile's MMAs finish), and with two accumulator buffers the
 // epilogue of a tile overlaps the next tile's MMAs.
-template <int BN, bool H = false>
-__global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_constant__ Params p) {
+// RAW: operand A (activations / shifted copies) is loaded as plain fp32 and
+// warps 8-11 write its lo half, x - trunc_tf32(x), next to it in shared
+// memory (the tensor core reads the fp32 tile itself as the truncated hi):
+// one A load per stage instead of two, and the layout kernels write one tensor.
+constexpr int kRawThreads = 384;
+template <int BN, bool H = false, bool RAW = false>
+__global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
+    tma_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char raw[];
   // the swizzled tiles need 1024-B alignment of the dynamic window
   Smem<BN, H>& S = *reinterpret_cast<Smem<BN, H>*>(
@@ -343,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 1);
+      tc::mbar_init(&S.split[s], 4);  // RAW: one arrival per splitting warp
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.acc_full[b], 1);
@@ -367,8 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
         int nt, mt, z;
         tile_coords(p, tl, nt, mt, z);
         const uint32_t bytes =
-            H ? 2u * ((uint32_t)(kBM / p.W + 2) * p.W * kBK * 4 + 3u * BN * kBK * 4)
-              : 2u * (a_bytes(p, mt) + BN * kBK * 4);
+            H ? (RAW ? 1u : 2u) * (uint32_t)(kBM / p.W + 2) * p.W * kBK * 4 + 2u * 3u * BN * kBK * 4
+              : (RAW ? 1u : 2u) * a_bytes(p, mt) + 2u * BN * kBK * 4;
         const int nq = tile_chunks(p, z);
         for (int q = 0; q < nq; ++q, ++g) {
           const int s = g % NS;
@@ -376,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
           expect_tx(&S.full[s], bytes);
           int qc, ze;
           chunk_coords(p, q, z, qc, ze);
-          issue_chunk<BN, H>(p, S, s, qc, mt, nt, ze);
+          issue_chunk<BN, H, RAW>(p, S, s, qc, mt, nt, ze);
         }
       }
     }
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
         const uint32_t buf = tmem + (uint32_t)bsel * kBufCols;
         for (int q = 0; q < nq; ++q, ++g) {
           const int s = g % NS;
-          tc::mbar_wait(&S.full[s], (g / NS) & 1);
+          tc::mbar_wait(RAW ? &S.split[s] : &S.full[s], (g / NS) & 1);
           tc::fence_after_sync();
 #pragma unroll
           for (int u = 0; u < T; ++u) {
@@ -435,7 +452,28 @@ __global__ void __launch_bounds__(kThreads, 1) tma_gemm_kernel(const __grid_cons
         tc::commit(&S.acc_full[bsel]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (RAW && warp >= 8) {
+    // ---- lo half of each stage's A operand, then release the stage to the MMA ----
+    const int ct = t - 256;
+    constexpr int na4 = Smem<BN, H>::RA * kBK / 4;
+    int g = 0;
+    for (int tl = blockIdx.x; tl < total; tl += gridDim.x) {
+      int nt, mt, z;
+      tile_coords(p, tl, nt, mt, z);
+      const int nq = tile_chunks(p, z);
+      for (int q = 0; q < nq; ++q, ++g) {
+        const int s = g % NS;
+        tc::mbar_wait(&S.full[s], (g / NS) & 1);
+        const float4* ah = reinterpret_cast<const float4*>(S.a_hi[s]);
+        float4* al = reinterpret_cast<float4*>(S.a_lo[s]);
+#pragma unroll 4
+        for (int e = ct; e < na4; e += 128) al[e] = lo_of(ah[e]);
+        tc::fence_proxy_async();  // generic-proxy writes -> the tensor core's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.split[s]);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     // ---- epilogue: TMEM -> registers -> global ----
     const int q4 = warp & 3, r = q4 * 32 + lane;
     int lt = 0;
@@ -655,10 +693,6 @@ struct DwhSmem {
 // core reads the fp32 tile itself as the truncated hi); else the hi and lo
 // tensors are both loaded (split by the layout kernels).
 constexpr int kDwhRawThreads = 384;
-__device__ __forceinline__ float4 lo_of(float4 x) {
-  const auto lo1 = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u); };
-  return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w));
-}
 
 template <bool RAW>
 __global__ void __launch_bounds__(RAW ? kDwhRawThreads : kThreads, 1)
@@ -893,6 +927,10 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __rest
   for (int j = threadIdx.y; j < 32; j += 8) {
     const int p = p0 + j, c = c0 + threadIdx.x;
     if (p < HW) {
+      if (!dst_lo) {  // plain fp32 (the GEMM splits the lo half itself)
+        dst[((size_t)n * HW + p) * Cp + c] = tile[threadIdx.x][j];
+        continue;
+      }
       float hi, lo;
       split2(tile[threadIdx.x][j], hi, lo);
       dst[((size_t)n * HW + p) * Cp + c] = hi;
@@ -1205,26 +1243,42 @@ inline int num_sms() {
   return n;
 }
 
+template <int BN, bool H, bool RAW>
+inline void launch_kernel(const Params& p, int ctas, cudaStream_t s) {
+  tma_gemm_kernel<BN, H, RAW><<<ctas, RAW ? kRawThreads : kThreads, smem_bytes<BN, H>(), s>>>(p);
+}
+
+template <int BN, bool H>
+inline void set_attrs() {
+  cudaFuncSetAttribute(tma_gemm_kernel<BN, H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem_bytes<BN, H>());
+  cudaFuncSetAttribute(tma_gemm_kernel<BN, H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem_bytes<BN, H>());
+}
+
 template <int BN>
 inline void launch_bn(const Params& p, int ctas, cudaStream_t s) {
   static int attr_dev = -1;  // the attribute is set once per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(tma_gemm_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_bytes<BN, false>());
-    if constexpr (BN <= 64)
-      cudaFuncSetAttribute(tma_gemm_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_bytes<BN, true>());
+    set_attrs<BN, false>();
+    if constexpr (BN <= 64) set_attrs<BN, true>();
     attr_dev = dev;
   }
   if constexpr (BN <= 64) {
     if (p.halo) {
-      tma_gemm_kernel<BN, true><<<ctas, kThreads, smem_bytes<BN, true>(), s>>>(p);
+      if (p.raw)
+        launch_kernel<BN, true, true>(p, ctas, s);
+      else
+        launch_kernel<BN, true, false>(p, ctas, s);
       return;
     }
   }
-  tma_gemm_kernel<BN, false><<<ctas, kThreads, smem_bytes<BN, false>(), s>>>(p);
+  if (p.raw)
+    launch_kernel<BN, false, true>(p, ctas, s);
+  else
+    launch_kernel<BN, false, false>(p, ctas, s);
 }
 
 inline size_t dwh_smem_bytes() { return sizeof(DwhSmem) + 1024; }

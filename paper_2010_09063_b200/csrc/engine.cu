@@ -477,6 +477,12 @@ struct Engine {
     const int per = (fwd ? chain_fwd : chain_dx) * nacc;
     return std::max(1, (nchunks + per - 1) / per);
   }
+  static int ksplit_mi(int nchunks, bool fwd) {
+    static const int chain_fwd = env_int("PGB_KSPLIT_CHAIN_FWD", env_int("PGB_KSPLIT_CHAIN", 4));
+    static const int chain_dx = env_int("PGB_KSPLIT_CHAIN_DX", env_int("PGB_KSPLIT_CHAIN", 8));
+    const int chain = fwd ? chain_fwd : chain_dx;
+    return std::max(1, (nchunks + chain - 1) / chain);
+  }
   static int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::max(1, std::atoi(v)) : dflt;
@@ -494,10 +500,13 @@ struct Engine {
   // the SMs (raw splits to d_split_ws, added in order by the epilogue kernel)
   int tma_launch_split(tg::Params& p, int bn, int ntn, int ntm, cudaStream_t s) {
     // (a halo chunk is three taps: the chain counts taps)
-    const int S = no_ksplit
-                      ? 1
-                      : std::min(p.nchunks, ksplit_for(bn, p.nchunks * (p.halo ? 3 : 1),
-                                                       p.mode == tg::kConvFwd));
+    // (halo tiles with BN <= 32: one accumulator per kernel row, so the
+    // chain is the split's chunk count)
+    const bool fwd = p.mode == tg::kConvFwd;
+    const int S = no_ksplit ? 1
+                  : p.halo && bn <= 32
+                      ? std::min(p.nchunks, ksplit_mi(p.nchunks, fwd))
+                      : std::min(p.nchunks, ksplit_for(bn, p.nchunks * (p.halo ? 3 : 1), fwd));
     if (S <= 1 || !d_split_ws) {
       tg::launch(p, bn, dim3(ntn, ntm, 1), s);
       return 0;
@@ -768,7 +777,8 @@ struct Engine {
           for (int side = 0; side < 2; ++side) {  // forward (N = D), input gradient (N = C)
             const int N = side ? g.C : g.D, K = side ? g.D : g.C;
             const int bn = tg::pick_bn(N), ntn = (N + bn - 1) / bn;
-            const int S = ksplit_for(bn, 9 * tg::round32(K) / 32, side == 0);
+            const int S = std::max(ksplit_for(bn, 9 * tg::round32(K) / 32, side == 0),
+                                   ksplit_mi(3 * tg::round32(K) / 32, side == 0));
             if (S > 1) split_ws = std::max<int64_t>(split_ws, (int64_t)S * ntm * ntn * bn * 128);
           }
         }

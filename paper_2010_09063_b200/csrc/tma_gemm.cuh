@@ -352,17 +352,21 @@ __global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
   constexpr int NACC = nacc<BN>();
   constexpr uint32_t kAccStride = acc_stride<BN>();
   constexpr uint32_t kBufCols = 512 / NB;
+  // halo tiles with BN <= 32: warps 1-3 each issue one kernel row u into its
+  // own accumulator (a single thread issues an MMA only every ~50-120 cycles,
+  // and a halo chunk is 3 x 4 x 2 MMAs)
+  constexpr bool kMI = H && BN <= 32;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int total = p.ntn * p.ntm * p.nz;
   if (warp == 1) tc::tmem_alloc(&S.tmem, kCols);
   if (t == 0) {
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&S.full[s], 1);
-      tc::mbar_init(&S.empty[s], 1);
+      tc::mbar_init(&S.empty[s], kMI ? 3 : 1);  // one commit per issuing warp
       tc::mbar_init(&S.split[s], 4);  // RAW: one arrival per splitting warp
     }
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&S.acc_full[b], 1);
+      tc::mbar_init(&S.acc_full[b], kMI ? 3 : 1);
       tc::mbar_init(&S.acc_empty[b], 4);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -397,9 +401,10 @@ __global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ---- MMA issuer ----
+  } else if (warp == 1 || (kMI && warp <= 3)) {
+    // ---- MMA issuer(s) ----
     if (lane == 0) {
+      const int u0 = kMI ? warp - 1 : 0, u1 = kMI ? warp : T;
       constexpr uint32_t idesc = tc::idesc_tf32(kBM, kFold ? 2 * BN : (BN < 16 ? 16 : BN));
       constexpr uint32_t idesc_lo = tc::idesc_tf32(kBM, BN < 16 ? 16 : BN);
       int g = 0, lt = 0;
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
           tc::mbar_wait(RAW ? &S.split[s] : &S.full[s], (g / NS) & 1);
           tc::fence_after_sync();
 #pragma unroll
-          for (int u = 0; u < T; ++u) {
+          for (int u = u0; u < u1; ++u) {
             // halo: kernel row u reads the stage's rows from u (forward) or
             // 2 - u (input gradient, the flipped tap) times W
             const uint32_t ao =
@@ -425,14 +430,15 @@ __global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
             const uint32_t ah = smem_u32(S.a_hi[s]) + ao, al = smem_u32(S.a_lo[s]) + ao;
             const uint32_t bh = smem_u32(S.b[s][u][0]), bl = smem_u32(S.b[s][u][1]);
             const int qa = q * T + u;  // accumulator chain step
-            const uint32_t dmain = buf + (uint32_t)(qa % NACC) * kAccStride;
+            const uint32_t dmain = buf + (uint32_t)(kMI ? u : qa % NACC) * kAccStride;
+            const bool acc0 = kMI ? q > 0 : qa >= NACC;  // the accumulator already holds a chunk
 #pragma unroll
             for (int k = 0; k < kBK / 8; ++k) {
               const uint32_t o = 32u * k;
               if constexpr (kFold) {
                 // [Bhi; Blo] is one 2 BN-row operand starting at bh
                 tc::mma_tf32(dmain, desc_sw128(ah + o), desc_sw128(bh + o), idesc,
-                             (qa >= NACC || k) ? 1u : 0u);
+                             (acc0 || k) ? 1u : 0u);
                 if (p.narrow)
                   tc::mma_tf32(dmain, desc_sw128(al + o), desc_sw128(bh + o), idesc_lo, 1u);
                 else
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(RAW ? kRawThreads : kThreads, 1)
       int nt, mt, z;
       tile_coords(p, tl, nt, mt, z);
       const int nq = tile_chunks(p, z) * T;  // accumulator chain steps
-      const int used = nq < NACC ? nq : NACC;
+      const int used = kMI ? T : nq < NACC ? nq : NACC;
       const int bsel = NB == 2 ? (lt & 1) : 0;
       const int use = NB == 2 ? (lt >> 1) : lt;
       // input gradient: the tile's ReLU-mask row loaded while the MMAs run

@@ -178,6 +178,13 @@ struct Engine {
   bool pool_generic = false;    // PGB_POOL_GENERIC=1: the generic pooling kernels  // PGB_EMB_AGG_SCALAR=1: the scalar embedding aggregation
   bool tma_fwd(const ConvGeom& g) const { return use_tma && tg::conv_ok(g) && (tma_all || g.C >= 16); }
   bool tma_dx(const ConvGeom& g) const { return use_tma && tg::conv_ok(g); }
+  // few-channel 3x3 forward directly on the CUDA cores (conv3x3_smallc_fwd_kernel;
+  // PGB_NO_DIRECT_CONV=1: the gather GEMM)
+  bool direct_conv = true;
+  bool smallc_fwd(const ConvGeom& g) const {
+    return direct_conv && g.C <= 4 && g.k == 3 && g.stride == 1 && g.pad == 1 && g.Ho == g.H &&
+           g.Wo == g.W && g.W % 4 == 0 && g.D % 16 == 0;
+  }
   bool tma_dw(const ConvGeom& g) const {
     return use_tma && tg::conv_ok(g) && (tma_all || dwh_sel(g));
   }
@@ -698,6 +705,7 @@ struct Engine {
     dwh_rot = std::min(2, env_int("PGB_DWH_ROT", 1));
     dwh_raw = std::getenv("PGB_DWH_SPLIT") == nullptr;
     raw_a = std::getenv("PGB_TMA_SPLIT") == nullptr;
+    direct_conv = std::getenv("PGB_NO_DIRECT_CONV") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -1217,6 +1225,17 @@ struct Engine {
             const int kk = tma_conv_fwd(s, g, Bi, in, W, W + (size_t)g.D * K, L.act_out,
                                         L.fused_relu, l);
             nk += mark(s, "conv_fwd_tma") + kk - 1;
+          } else if (smallc_fwd(g)) {
+            const size_t sm = sizeof(float) * (size_t)(g.C * 9 + 1) * g.D;
+            const long long thr = (long long)Bi * g.H * (g.W / 4);
+            const int blocks = (int)std::min<long long>((thr + 255) / 256, 148ll * 8);
+            switch (g.C) {
+              case 1: conv3x3_smallc_fwd_kernel<1><<<blocks, 256, sm, s>>>(in, W, W + (size_t)g.D * K, L.act_out, Bi, g.D, g.H, g.W, L.fused_relu ? 1 : 0); break;
+              case 2: conv3x3_smallc_fwd_kernel<2><<<blocks, 256, sm, s>>>(in, W, W + (size_t)g.D * K, L.act_out, Bi, g.D, g.H, g.W, L.fused_relu ? 1 : 0); break;
+              case 3: conv3x3_smallc_fwd_kernel<3><<<blocks, 256, sm, s>>>(in, W, W + (size_t)g.D * K, L.act_out, Bi, g.D, g.H, g.W, L.fused_relu ? 1 : 0); break;
+              default: conv3x3_smallc_fwd_kernel<4><<<blocks, 256, sm, s>>>(in, W, W + (size_t)g.D * K, L.act_out, Bi, g.D, g.H, g.W, L.fused_relu ? 1 : 0); break;
+            }
+            nk += mark(s, "conv_fwd_direct");
           } else if (use_tc) {
             tc::TcConvFwdOp op{Bi * g.Ho * g.Wo, g.D, K, g, in, W, W + (size_t)g.D * K,
                                L.act_out, L.fused_relu ? 1 : 0};

@@ -384,6 +384,88 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
+// 3x3 / stride 1 / pad 1 convolution of a few-channel input (the CIFAR
+// first layer, C = 3) directly on the CUDA cores in fp32
+// (models.cpp:197-220 computes the same sum as an im2col GEMM): a 27-tap
+// sum per output is too short for the tensor cores to pay for the im2col
+// gather. One thread = 4 consecutive outputs of a row, all D channels in
+// groups of 16 (64 accumulators); its 3 x 6 input window per channel sits in
+// registers, the weights ([tap][d], 16-byte broadcast loads) in shared memory.
+// Bias and ReLU fused; out NCHW, float4 stores.
+template <int C>
+__global__ void __launch_bounds__(256) conv3x3_smallc_fwd_kernel(
+    const float* __restrict__ x, const float* __restrict__ Wt, const float* __restrict__ bias,
+    float* __restrict__ out, int B, int D, int H, int W, int relu) {
+  extern __shared__ float sw[];  // [C * 9][D] then bias[D]
+  for (int e = threadIdx.x; e < C * 9 * D; e += blockDim.x) {
+    const int d = e / (C * 9), k = e - d * (C * 9);
+    sw[k * D + d] = Wt[e];
+  }
+  for (int d = threadIdx.x; d < D; d += blockDim.x) sw[C * 9 * D + d] = bias[d];
+  __syncthreads();
+  const int W4 = W >> 2;
+  const long long total = (long long)B * H * W4;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int xq = (int)(t % W4);
+    const long long r = t / W4;
+    const int y = (int)(r % H), n = (int)(r / H);
+    const int x0 = xq * 4;
+    float xw[C][3][6];
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int yy = y + u - 1;
+        const bool rowok = yy >= 0 && yy < H;
+        const float* row = x + (((size_t)n * C + c) * H + (rowok ? yy : 0)) * W;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int xx = x0 - 1 + j;
+          xw[c][u][j] = (rowok && xx >= 0 && xx < W) ? __ldg(row + xx) : 0.0f;
+        }
+      }
+    for (int d0 = 0; d0 < D; d0 += 16) {
+      float acc[16][4];
+#pragma unroll
+      for (int dd = 0; dd < 16; ++dd) {
+        const float b = sw[C * 9 * D + d0 + dd];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[dd][i] = b;
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            const float4* wk = reinterpret_cast<const float4*>(sw + (c * 9 + u * 3 + v) * D + d0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 w4 = wk[q];
+              const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  acc[q * 4 + e][i] = fmaf(wv[e], xw[c][u][i + v], acc[q * 4 + e][i]);
+            }
+          }
+#pragma unroll
+      for (int dd = 0; dd < 16; ++dd) {
+        float4 o = make_float4(acc[dd][0], acc[dd][1], acc[dd][2], acc[dd][3]);
+        if (relu) {
+          o.x = fmaxf(o.x, 0.0f);
+          o.y = fmaxf(o.y, 0.0f);
+          o.z = fmaxf(o.z, 0.0f);
+          o.w = fmaxf(o.w, 0.0f);
+        }
+        *reinterpret_cast<float4*>(out + (((size_t)n * D + d0 + dd) * H + y) * W + x0) = o;
+      }
+    }
+  }
+}
+
 // 2x2 windows with stride 2 tiling the input (H = 2 Ho, W = 2 Wo: every input
 // element in exactly one window) -- the CIFAR pools. One thread per window,
 // 8-byte row loads/stores; the same fp32 operations as pool_fwd_kernel /

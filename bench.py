@@ -528,7 +528,7 @@ def run_ours(args):
         # forward, input gradient, per-example dW -- or, for the ghost layers,
         # their Gram norms and the clip-scaled summed dW GEMM
         conv = [n for n in by_name if n.endswith("_tc") or n.endswith("_tma")
-                or n in ("conv_dw_gram", "conv_dw_sum", "conv_fwd_direct")]
+                or n in ("conv_dw_gram", "conv_dw_sum", "conv_fwd_direct", "conv_dw_pex_direct")]
         tc_ms = sum(by_name[n] for n in conv)
         flops = conv_gemm_flops(desc, BATCH)
         ach = flops / (tc_ms * 1e-3) / 1e12
@@ -537,8 +537,8 @@ def run_ours(args):
                 "frac": ach / bf16, "traffic": None, "peak_kind": peak_kind,
                 "engine": "tcgen05.mma kind::tf32, 3xTF32 split (work counted once); "
                           "3x3 convs fed by tensor-map TMA (128-B swizzle), the others by "
-                          "register gathers; the 3-channel first layer's forward "
-                          "(conv_fwd_direct) on the CUDA cores in fp32, its time counted here",
+                          "register gathers; the 3-channel first layer's forward and per-example dW "
+                          "(conv_*_direct) on the CUDA cores in fp32, their time counted here",
                 "tf32x3_effective_peak_tflops": (tf32 or bf16 / 2) / 3,
                 "frac_of_tf32x3_effective_peak": ach / ((tf32 or bf16 / 2) / 3),
                 "tf32_peak_tflops_measured": tf32, "tf32_peak_source": tf32_src,

@@ -181,6 +181,11 @@ struct Engine {
   // few-channel 3x3 forward directly on the CUDA cores (conv3x3_smallc_fwd_kernel;
   // PGB_NO_DIRECT_CONV=1: the gather GEMM)
   bool direct_conv = true;
+  bool direct_dw = true;  // PGB_NO_DIRECT_DW=1: the first layer's dW on the gather GEMM
+  bool smallc_dw(const ConvGeom& g) const {
+    return direct_conv && direct_dw && g.C <= 4 && g.k == 3 && g.stride == 1 && g.pad == 1 && g.Ho == g.H &&
+           g.Wo == g.W && g.W == 32 && (size_t)g.C * (g.H + 2) * 34 * 4 <= 48 * 1024;
+  }
   bool smallc_fwd(const ConvGeom& g) const {
     return direct_conv && g.C <= 4 && g.k == 3 && g.stride == 1 && g.pad == 1 && g.Ho == g.H &&
            g.Wo == g.W && g.W % 4 == 0 && g.D % 16 == 0;
@@ -706,6 +711,7 @@ struct Engine {
     dwh_raw = std::getenv("PGB_DWH_SPLIT") == nullptr;
     raw_a = std::getenv("PGB_TMA_SPLIT") == nullptr;
     direct_conv = std::getenv("PGB_NO_DIRECT_CONV") == nullptr;
+    direct_dw = std::getenv("PGB_NO_DIRECT_DW") == nullptr;
     if (const char* cp = std::getenv("PGB_C2_PAIRS")) c2_pairs = std::atoi(cp) != 0;
     // dense / relu / flatten only, dense first, widths and depth within the
     // fused kernel's per-warp buffers
@@ -1530,6 +1536,15 @@ struct Engine {
                                                            nparts, L.pblock, sb);
             }
             nk += mark(s, "conv_dw_gram");
+          } else if (smallc_dw(gg)) {
+            const size_t sm = sizeof(float) * (size_t)gg.C * (gg.H + 2) * 34;
+            switch (gg.C) {
+              case 1: conv3x3_smallc_dw_kernel<1, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 2: conv3x3_smallc_dw_kernel<2, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 3: conv3x3_smallc_dw_kernel<3, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              default: conv3x3_smallc_dw_kernel<4, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+            }
+            nk += mark(s, "conv_dw_pex_direct");
           } else if (tma_dw(gg)) {
             const int tiles = tma_conv_dw(s, gg, Bi, in, gcur, sW, d_tile_sq);
             nk += mark(s, "conv_dw_pex_tma") + dw_prep_kernels;

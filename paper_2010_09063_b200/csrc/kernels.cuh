@@ -792,6 +792,92 @@ struct BlockTable {
   int norm_pre[kMaxBlocks];  // 1: per-example squared norm already in parts (sumsq skips)
 };
 
+// Per-example dW of a few-channel 3x3 / stride 1 / pad 1 convolution on a
+// 32-wide map (the CIFAR first layer) on the CUDA cores in fp32: one block per
+// example, lane = output column x, warp w = DPW output channels (more
+// warps loop over channel groups); each thread sums its column over all rows
+// into 4 x C x 9 accumulators (input rows staged zero-padded in shared
+// memory, cotangent rows read coalesced), then a fixed xor-shuffle tree adds
+// the 32 columns. Writes the reference's stack row (D, C, 3, 3)
+// (strategies.cpp:156-170) and the block's squared norm (fp64) into parts.
+template <int C, int DPW>
+__global__ void __launch_bounds__(512) conv3x3_smallc_dw_kernel(
+    const float* __restrict__ x, const float* __restrict__ g, float* __restrict__ stack, int D,
+    int H, double* __restrict__ parts, int nparts, int pb) {
+  constexpr int W = 32, WP = 34, K = C * 9;
+  extern __shared__ float xs[];  // [C][H + 2][34], zero border
+  __shared__ double wsq[16];
+  const int z = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const float* xz = x + (size_t)z * C * H * W;
+  for (int e = threadIdx.x; e < C * (H + 2) * WP; e += blockDim.x) {
+    const int c = e / ((H + 2) * WP), r = e - c * (H + 2) * WP;
+    const int yy = r / WP - 1, xx = r % WP - 1;
+    xs[e] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? xz[((size_t)c * H + yy) * W + xx] : 0.0f;
+  }
+  __syncthreads();
+  double sq = 0.0;
+  for (int d0 = warp * DPW; d0 < D; d0 += nw * DPW) {
+    float acc[DPW][K];
+#pragma unroll
+    for (int dd = 0; dd < DPW; ++dd)
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[dd][k] = 0.0f;
+    const float* gz = g + ((size_t)z * D + d0) * H * W;
+    float gn[DPW];  // the next row's cotangent, loaded one row ahead
+#pragma unroll
+    for (int dd = 0; dd < DPW; ++dd) gn[dd] = d0 + dd < D ? __ldg(gz + (size_t)dd * H * W + lane) : 0.0f;
+    for (int y = 0; y < H; ++y) {
+      float gv[DPW];
+#pragma unroll
+      for (int dd = 0; dd < DPW; ++dd) {
+        gv[dd] = gn[dd];
+        gn[dd] = (d0 + dd < D && y + 1 < H) ? __ldg(gz + ((size_t)dd * H + y + 1) * W + lane) : 0.0f;
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            const float xv = xs[(c * (H + 2) + y + u) * WP + lane + v];
+#pragma unroll
+            for (int dd = 0; dd < DPW; ++dd)
+              acc[dd][c * 9 + u * 3 + v] = fmaf(gv[dd], xv, acc[dd][c * 9 + u * 3 + v]);
+          }
+    }
+    // the 32 columns: a fixed xor tree (every lane ends with the total)
+#pragma unroll
+    for (int dd = 0; dd < DPW; ++dd)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        float a = acc[dd][k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        acc[dd][k] = a;
+      }
+    // lane l writes elements l, l + 32, ... of the DPW x K contiguous stack values
+    float* st = stack + ((size_t)z * D + d0) * K;
+#pragma unroll
+    for (int dd = 0; dd < DPW; ++dd)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (((dd * K + k) & 31) == lane && d0 + dd < D) {
+          st[dd * K + k] = acc[dd][k];
+          sq = fma((double)acc[dd][k], (double)acc[dd][k], sq);
+        }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) wsq[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += wsq[w];
+    parts[(size_t)z * nparts + pb] = t;
+  }
+}
+
 // parts[i * nparts + p] = the fixed-order sum of example i's tile sums
 __global__ void tile_sq_reduce_kernel(const double* __restrict__ tile_sq, int tiles, int B,
                                       double* __restrict__ parts, int nparts, int p) {

@@ -5,7 +5,9 @@ against each other:
   (PGB_NO_GHOST=1), per-example dW on the halo kernel for C >= 16 (default),
   for every layer (PGB_DWH_MIN_C=1; with PGB_NO_GHOST=1 also the 8x8 layers),
   with two accumulators per kernel row (PGB_DWH_ROT=2) or on the register-gather
-  GEMM (PGB_NO_DW_HALO=1), halo TMA stages (default) and one box per tap
+  GEMM (PGB_NO_DW_HALO=1), the 3-channel first layer's forward and dW on the
+  CUDA cores (default) or the gather GEMM (PGB_NO_DIRECT_CONV=1 / _DW=1), halo
+  TMA stages (default) and one box per tap
   (PGB_NO_HALO=1), batch-invariant K splits (default) and none
   (PGB_NO_KSPLIT=1): each a full DPSGD step of the CIFAR CNN against the oracle
   (norms rel 1e-5, exact clip counts, parameters within a few ulps + 1e-5 of
@@ -37,9 +39,11 @@ def _engine(P, desc, B, strat, monkeypatch, env):
 @pytest.mark.parametrize("env", [(), ("PGB_NO_GHOST",), ("PGB_NO_HALO",), ("PGB_NO_KSPLIT",),
                                  ("PGB_NO_GHOST", "PGB_NO_HALO"), ("PGB_NO_DW_HALO",),
                                  ("PGB_DWH_MIN_C=1",), ("PGB_DWH_ROT=2",),
-                                 ("PGB_NO_GHOST", "PGB_DWH_MIN_C=1")],
+                                 ("PGB_NO_GHOST", "PGB_DWH_MIN_C=1"), ("PGB_NO_DIRECT_CONV",),
+                                 ("PGB_NO_DIRECT_DW",)],
                          ids=["default", "no_ghost", "no_halo", "no_ksplit", "no_ghost_no_halo",
-                              "no_dw_halo", "dw_halo_all", "dw_halo_rot2", "no_ghost_dw_halo_all"])
+                              "no_dw_halo", "dw_halo_all", "dw_halo_rot2", "no_ghost_dw_halo_all",
+                              "no_direct_conv", "no_direct_dw"])
 def test_cifar_step_variants_match_oracle(P, O, env, monkeypatch):
     B = 4
     desc = P.build_desc(P.ModelKind.cifar_cnn)

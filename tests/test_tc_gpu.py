@@ -66,8 +66,10 @@ def test_tma_gemm_3xtf32(P, M, N, K):
                                      (64, 8, 8, 10), (128, 8, 8, 32), (128, 4, 4, 256),
                                      (256, 4, 4, 10), (16, 8, 32, 40), (48, 16, 8, 96)])
 @pytest.mark.parametrize("env", ["PGB_TMA_ALL=1", "PGB_TMA_ALL=1 PGB_DWH_MIN_C=1",
-                                 "PGB_DWH_MIN_C=1 PGB_DWH_ROT=2", "PGB_TMA_ALL=1 PGB_NO_DW_HALO=1"],
-                         ids=["tma_all", "tma_all_dwh_all", "dwh_all_rot2", "tma_all_no_dwh"])
+                                 "PGB_DWH_MIN_C=1 PGB_DWH_ROT=2", "PGB_TMA_ALL=1 PGB_NO_DW_HALO=1",
+                                 "PGB_NO_DIRECT_CONV=1", "PGB_TMA_SPLIT=1 PGB_DWH_SPLIT=1"],
+                         ids=["tma_all", "tma_all_dwh_all", "dwh_all_rot2", "tma_all_no_dwh",
+                              "no_direct", "split_operands"])
 def test_tma_conv_gemms_match_oracle(P, O, monkeypatch, C, H, W, D, env):
     """Every 3x3 conv GEMM on the TMA engine (PGB_TMA_ALL=1: forward,
     per-example dW and input gradient, whatever the per-kind default picks;

@@ -199,6 +199,12 @@ struct Engine {
   bool dw_halo = true;
   int dwh_min_c = 16, dwh_rot = 1;
   bool dwh_raw = true;     // PGB_DWH_SPLIT=1: hi / lo operand tensors split by the layout kernels
+  // conv weight-gradient work on a forked graph branch beside the input
+  // gradient (PGB_NO_DW_FORK=1: in line); needs its own shifted-copy scratch
+  // and a cotangent buffer per layer (no ping-pong)
+  bool dw_fork = true, fork_dw_now = false;
+  float* d_nhwc_dw = nullptr;
+  bool dw_fork_ok() const { return dw_fork && dwh_raw && use_tma && !tma_all; }
   // forward / input-gradient / clipped-sum dW GEMMs: operand A as plain fp32,
   // its lo half split in the kernel (PGB_TMA_SPLIT=1: hi / lo tensors)
   bool raw_a = true;
@@ -590,7 +596,8 @@ struct Engine {
     // halo kernel with plain fp32 operands (it splits the lo halves itself):
     // the shifted copies only, the cotangent read in place
     const bool raw = halo && dwh_raw;
-    tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, d_nhwc, raw ? nullptr : d_nhwc_lo,
+    float* cp = fork_dw_now ? d_nhwc_dw : d_nhwc;  // (the forked branch has its own)
+    tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(x, cp, raw ? nullptr : d_nhwc_lo,
                                                               total, g.W);
     const long long gt = (long long)Bi * g.D * HW;
     if (!raw) tg::split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(gout, d_wt, d_wt_lo, gt);
@@ -600,7 +607,7 @@ struct Engine {
     const uint64_t da[4] = {(uint64_t)HW, (uint64_t)g.C, (uint64_t)Bi, 3};
     const uint64_t sa[3] = {4ull * HW, 4ull * HW * g.C, 4ull * total};
     const uint32_t ba[4] = {32, (uint32_t)Cr, 1, 1};
-    tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+    tg::make_map(&p.ta, cp, 4, da, sa, ba);
     tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
     const uint64_t db[3] = {(uint64_t)HW, (uint64_t)g.D, (uint64_t)Bi};
     const uint64_t sb[2] = {4ull * HW, 4ull * HW * g.D};
@@ -709,6 +716,7 @@ struct Engine {
     dwh_min_c = env_int("PGB_DWH_MIN_C", 16);
     dwh_rot = std::min(2, env_int("PGB_DWH_ROT", 1));
     dwh_raw = std::getenv("PGB_DWH_SPLIT") == nullptr;
+    dw_fork = std::getenv("PGB_NO_DW_FORK") == nullptr;
     raw_a = std::getenv("PGB_TMA_SPLIT") == nullptr;
     direct_conv = std::getenv("PGB_NO_DIRECT_CONV") == nullptr;
     direct_dw = std::getenv("PGB_NO_DIRECT_DW") == nullptr;
@@ -926,6 +934,19 @@ struct Engine {
         }
       }
     }
+    if (dw_fork_ok()) {
+      // forked weight-gradient branch: a cotangent buffer per conv layer and
+      // its own shifted-copy scratch
+      int64_t cp = 0;
+      for (int l = 0; l < n; ++l) {
+        const Layer& L = layers[l];
+        if (L.spec.kind != PGB_CONV || L.ghost || L.skip_bwd) continue;
+        want((void**)&d_ghost_g[l], sizeof(float) * B * L.out.numel());
+        const ConvGeom g = conv_geom(L);
+        if (tg::dwh_ok(g)) cp = std::max<int64_t>(cp, 3 * B * (int64_t)g.H * g.W * g.C);
+      }
+      if (cp) want((void**)&d_nhwc_dw, sizeof(float) * cp);
+    }
     d_dense_g.assign(n, nullptr);
     for (int l = 0; l < n; ++l)
       if (layers[l].spec.kind == PGB_DENSE)
@@ -978,6 +999,10 @@ struct Engine {
       if (L.spec.kind == PGB_DENSE) {
         L.gout = d_dense_g[l];
       } else if (L.ghost) {
+        L.gout = d_ghost_g[l];
+      } else if (d_ghost_g[l]) {
+        // (a forked weight-gradient branch may still read it when the
+        // ping-pong would hand the buffer to a layer further down)
         L.gout = d_ghost_g[l];
       } else {
         L.gout = d_cot[pp];
@@ -1493,6 +1518,8 @@ struct Engine {
     const int n = desc.n_layers;
     const int Bi = (int)B;
     const Layer* below = nullptr;
+    fork_dw_now = dw_fork_ok() && !prof && d_nhwc_dw;
+    bool forked = false;
     for (int l = n - 1; l >= first_param_layer; --l) {
       Layer& L = layers[l];
       if (L.skip_bwd) continue;
@@ -1521,6 +1548,16 @@ struct Engine {
           const int K = gg.C * gg.k * gg.k, Pp = gg.Ho * gg.Wo;
           float* sW = d_stacks + param_off[L.pblock] * B;
           float* sb = d_stacks + param_off[L.pblock + 1] * B;
+          // the weight-gradient work of this layer reads only its input and
+          // output cotangent: on a forked branch beside the input gradient
+          // (fills the SMs the other's tail leaves idle; joined after the loop)
+          cudaStream_t sd = s;
+          if (fork_dw_now) {
+            PGB_CUDA(cudaEventRecord(ev_fork, s));
+            PGB_CUDA(cudaStreamWaitEvent(side_stream, ev_fork, 0));
+            sd = side_stream;
+            forked = true;
+          }
           if (ghost_next && L.ghost) {
             // the block's per-example norm only (ghost Gram norm); its
             // clipped sum comes later from enqueue_ghost_sums
@@ -1528,46 +1565,46 @@ struct Engine {
             const size_t sm = sizeof(float) * (size_t)(gg.C + gg.D + hw) * hw;
             if (hw == 64) {
               gram_attr(conv_gram_norm_kernel<64>, sm);
-              conv_gram_norm_kernel<64><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
+              conv_gram_norm_kernel<64><<<Bi, 256, sm, sd>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
                                                            nparts, L.pblock, sb);
             } else {
               gram_attr(conv_gram_norm_kernel<16>, sm);
-              conv_gram_norm_kernel<16><<<Bi, 256, sm, s>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
+              conv_gram_norm_kernel<16><<<Bi, 256, sm, sd>>>(in, gcur, gg.C, gg.D, gg.W, d_parts,
                                                            nparts, L.pblock, sb);
             }
-            nk += mark(s, "conv_dw_gram");
+            nk += mark(sd, "conv_dw_gram");
           } else if (smallc_dw(gg)) {
             const size_t sm = sizeof(float) * (size_t)gg.C * (gg.H + 2) * 34;
             switch (gg.C) {
-              case 1: conv3x3_smallc_dw_kernel<1, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              case 2: conv3x3_smallc_dw_kernel<2, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              case 3: conv3x3_smallc_dw_kernel<3, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              default: conv3x3_smallc_dw_kernel<4, 2><<<Bi, 512, sm, s>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 1: conv3x3_smallc_dw_kernel<1, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 2: conv3x3_smallc_dw_kernel<2, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 3: conv3x3_smallc_dw_kernel<3, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              default: conv3x3_smallc_dw_kernel<4, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
             }
-            nk += mark(s, "conv_dw_pex_direct");
+            nk += mark(sd, "conv_dw_pex_direct");
           } else if (tma_dw(gg)) {
-            const int tiles = tma_conv_dw(s, gg, Bi, in, gcur, sW, d_tile_sq);
-            nk += mark(s, "conv_dw_pex_tma") + dw_prep_kernels;
-            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(d_tile_sq, tiles, Bi, d_parts,
+            const int tiles = tma_conv_dw(sd, gg, Bi, in, gcur, sW, d_tile_sq);
+            nk += mark(sd, "conv_dw_pex_tma") + dw_prep_kernels;
+            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, sd>>>(d_tile_sq, tiles, Bi, d_parts,
                                                                    nparts, L.pblock);
-            nk += mark(s, "conv_dw_norm");
+            nk += mark(sd, "conv_dw_norm");
           } else if (use_tc) {
             tc::TcConvDWOp dw{K, gg.D, Pp, gg, in, gcur, sW, d_tile_sq};
-            tc::launch(dw, Bi, s);
-            nk += mark(s, "conv_dw_pex_tc");
+            tc::launch(dw, Bi, sd);
+            nk += mark(sd, "conv_dw_pex_tc");
             // the block's per-example norm from the GEMM's tile sums (sumsq skips it)
-            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, s>>>(
+            tile_sq_reduce_kernel<<<(Bi + 127) / 128, 128, 0, sd>>>(
                 d_tile_sq, tc::tile_count(K, gg.D), Bi, d_parts, nparts, L.pblock);
-            nk += mark(s, "conv_dw_norm");
+            nk += mark(sd, "conv_dw_norm");
           } else {
             ConvDWOp dw{gg.D, K, Pp, gg, gcur, in, sW};
-            launch_gemm(dw, Bi, s);
-            nk += mark(s, "conv_dw_pex");
+            launch_gemm(dw, Bi, sd);
+            nk += mark(sd, "conv_dw_pex");
           }
           if (!(ghost_next && L.ghost)) {  // (the Gram kernel wrote the ghost layers' bias rows)
-            conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, s>>>(gcur, Bi * gg.D, Pp,
+            conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, sd>>>(gcur, Bi * gg.D, Pp,
                                                                            sb);
-            nk += mark(s, "conv_db_pex");
+            nk += mark(sd, "conv_db_pex");
           }
           if (L.needs_gx && tma_dx(gg)) {
             const int kk = tma_conv_dx(s, gg, Bi, gcur, W, L.bwd_mask, gnext, l);
@@ -1635,6 +1672,11 @@ struct Engine {
                 std::string("unsupported layer in backward: ") + layer_kind_name(sp.kind));
       }
     }
+    if (forked) {
+      PGB_CUDA(cudaEventRecord(ev_join, side_stream));
+      PGB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    }
+    fork_dw_now = false;
     dim3 sg(bt.n, (unsigned)B);
     sumsq_kernel<<<sg, 128, 0, s>>>(table_for(x_slot, sparse_embed_next), Bi, d_parts);
     nk += mark(s, "sumsq");

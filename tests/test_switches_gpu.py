@@ -7,7 +7,9 @@ against each other:
   with two accumulators per kernel row (PGB_DWH_ROT=2) or on the register-gather
   GEMM (PGB_NO_DW_HALO=1), the 3-channel first layer's forward and dW on the
   CUDA cores (default) or the gather GEMM (PGB_NO_DIRECT_CONV=1 / _DW=1), halo
-  TMA stages (default) and one box per tap
+  TMA stages (default) and one box per tap, the weight-gradient work on a
+  forked graph branch beside the input gradient (default) or in line
+  (PGB_NO_DW_FORK=1)
   (PGB_NO_HALO=1), batch-invariant K splits (default) and none
   (PGB_NO_KSPLIT=1): each a full DPSGD step of the CIFAR CNN against the oracle
   (norms rel 1e-5, exact clip counts, parameters within a few ulps + 1e-5 of
@@ -40,10 +42,10 @@ def _engine(P, desc, B, strat, monkeypatch, env):
                                  ("PGB_NO_GHOST", "PGB_NO_HALO"), ("PGB_NO_DW_HALO",),
                                  ("PGB_DWH_MIN_C=1",), ("PGB_DWH_ROT=2",),
                                  ("PGB_NO_GHOST", "PGB_DWH_MIN_C=1"), ("PGB_NO_DIRECT_CONV",),
-                                 ("PGB_NO_DIRECT_DW",)],
+                                 ("PGB_NO_DIRECT_DW",), ("PGB_NO_DW_FORK",)],
                          ids=["default", "no_ghost", "no_halo", "no_ksplit", "no_ghost_no_halo",
                               "no_dw_halo", "dw_halo_all", "dw_halo_rot2", "no_ghost_dw_halo_all",
-                              "no_direct_conv", "no_direct_dw"])
+                              "no_direct_conv", "no_direct_dw", "no_dw_fork"])
 def test_cifar_step_variants_match_oracle(P, O, env, monkeypatch):
     B = 4
     desc = P.build_desc(P.ModelKind.cifar_cnn)

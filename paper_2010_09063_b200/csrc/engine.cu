@@ -1985,15 +1985,28 @@ struct Engine {
     ScalesLaunch SL{d_parts, nparts, (int)B, cur_args, d_scale, d_clipflag, norms_dst};
     step_scales_kernel<<<((int)B + 127) / 128, 128, 0, s>>>(SL);
     nk += mark(s, "step_scales");
-    nk += enqueue_ghost_sums(s);
     BlockTable t2 = t;
     for (const Layer& L : layers)
       if (L.ghost) t2.kind[L.pblock] = 3;  // no aggregation tiles: summed by GEMM
     AggLaunch A = agg_launch(t2, nparts, (int)B, dist ? 1 : 0);
     A.scales = d_scale;
     A.clip_flags = d_clipflag;
-    launch_agg(A, s);
-    nk += mark(s, dist ? "aggregate_local" : "aggregate");
+    // single process: the aggregation (the other blocks' clipped sums, noise
+    // and update) touches none of the ghost blocks' buffers, so it runs on a
+    // forked branch beside their GEMMs (PGB_NO_DW_FORK=1: in line)
+    const bool fork = !dist && !prof && dw_fork;
+    if (fork) {
+      PGB_CUDA(cudaEventRecord(ev_fork, s));
+      PGB_CUDA(cudaStreamWaitEvent(side_stream, ev_fork, 0));
+      launch_agg(A, side_stream);
+      nk += mark(side_stream, "aggregate");
+      PGB_CUDA(cudaEventRecord(ev_join, side_stream));
+    }
+    nk += enqueue_ghost_sums(s);
+    if (!fork) {
+      launch_agg(A, s);
+      nk += mark(s, dist ? "aggregate_local" : "aggregate");
+    }
     if (dist) {
       auto& N = Nccl::get();
       PGB_NCCL(N.groupStart());
@@ -2017,6 +2030,7 @@ struct Engine {
     for (int p = 0; p < t2.n; ++p) pairs += (t2.size[p] + 1) / 2;
     noise_update_kernel<<<grid_for((size_t)pairs), 256, 0, s>>>(NL);
     nk += mark(s, "noise_update");
+    if (fork) PGB_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     return nk;
   }
 

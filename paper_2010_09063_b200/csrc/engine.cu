@@ -203,6 +203,12 @@ struct Engine {
   // gradient (PGB_NO_DW_FORK=1: in line); needs its own shifted-copy scratch
   // and a cotangent buffer per layer (no ping-pong)
   bool dw_fork = true, fork_dw_now = false;
+  // the ghost layers' clip-scaled dW GEMMs on parallel branches: per-layer
+  // scratch (shift copies, scaled cotangent pair, split workspace)
+  static constexpr int kGhostBranches = 4;
+  cudaStream_t ghost_streams[kGhostBranches - 1] = {};
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin[kGhostBranches - 1] = {};
+  std::vector<float*> d_gcp, d_gwt, d_gwt_lo, d_gws;
   float* d_nhwc_dw = nullptr;
   bool dw_fork_ok() const { return dw_fork && dwh_raw && use_tma && !tma_all; }
   // forward / input-gradient / clipped-sum dW GEMMs: operand A as plain fp32,
@@ -393,6 +399,11 @@ struct Engine {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (out_stream) cudaStreamDestroy(out_stream);
     if (side_stream) cudaStreamDestroy(side_stream);
+    for (int i = 0; i < kGhostBranches - 1; ++i) {
+      if (ghost_streams[i]) cudaStreamDestroy(ghost_streams[i]);
+      if (ev_gjoin[i]) cudaEventDestroy(ev_gjoin[i]);
+    }
+    if (ev_gfork) cudaEventDestroy(ev_gfork);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (h_norm_stage) cudaFreeHost(h_norm_stage);
@@ -925,6 +936,14 @@ struct Engine {
         int splits = std::max(1, std::min<int>(148 / tiles, (int)(B / 4)));
         L.ghost_splits = splits;
         ws = std::max<int64_t>(ws, (int64_t)splits * mtiles * ntiles * bn * 128);
+        if (dw_fork) {
+          d_gcp.resize(n, nullptr), d_gwt.resize(n, nullptr), d_gwt_lo.resize(n, nullptr);
+          d_gws.resize(n, nullptr);
+          want((void**)&d_gcp[l], sizeof(float) * 3 * B * hw * g.C);
+          want((void**)&d_gwt[l], sizeof(float) * B * hw * g.D);
+          want((void**)&d_gwt_lo[l], sizeof(float) * B * hw * g.D);
+          want((void**)&d_gws[l], sizeof(float) * splits * mtiles * ntiles * bn * 128);
+        }
       }
       if (any_ghost) {
         want((void**)&d_dw_ws, sizeof(float) * ws);
@@ -1126,6 +1145,11 @@ struct Engine {
     PGB_CUDA(cudaStreamCreateWithFlags(&side_stream, cudaStreamNonBlocking));
     PGB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     PGB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    PGB_CUDA(cudaEventCreateWithFlags(&ev_gfork, cudaEventDisableTiming));
+    for (int i = 0; i < kGhostBranches - 1; ++i) {
+      PGB_CUDA(cudaStreamCreateWithFlags(&ghost_streams[i], cudaStreamNonBlocking));
+      PGB_CUDA(cudaEventCreateWithFlags(&ev_gjoin[i], cudaEventDisableTiming));
+    }
     emb_fork = std::getenv("PGB_NO_EMB_FORK") == nullptr;
     for (int i = 0; i < kSlots; ++i)
       for (cudaEvent_t* ev : {&ev_copied[i], &ev_consumed[i]})
@@ -1922,11 +1946,27 @@ struct Engine {
   // input's column-shifted copies and the clip-scaled cotangent as 3xTF32
   // pairs, one GEMM over (example, position) split over the examples, the
   // splits added in order.
-  int enqueue_ghost_sums(cudaStream_t s) {
+  int enqueue_ghost_sums(cudaStream_t s0) {
     int nk = 0;
+    // parallel branches (layer k on stream k % 4, per-layer scratch; the
+    // kernels' tails and the small copy / reduce launches overlap)
+    const bool par = dw_fork && raw_a && !prof && !d_gws.empty();
+    if (par) PGB_CUDA(cudaEventRecord(ev_gfork, s0));
+    int k = 0, used = 0;
     for (int l = 0; l < desc.n_layers; ++l) {
       const Layer& L = layers[l];
       if (!L.ghost) continue;
+      const int br = par ? k % kGhostBranches : 0;
+      ++k;
+      cudaStream_t s = br ? ghost_streams[br - 1] : s0;
+      if (br && !(used & (1 << br))) {
+        PGB_CUDA(cudaStreamWaitEvent(s, ev_gfork, 0));
+        used |= 1 << br;
+      }
+      float* cp = par ? d_gcp[l] : d_nhwc;
+      float* wt = par ? d_gwt[l] : d_wt;
+      float* wt_lo = par ? d_gwt_lo[l] : d_wt_lo;
+      float* wsp = par ? d_gws[l] : d_dw_ws;
       const ConvGeom g = conv_geom(L);
       const int Bi = (int)B, HW = g.H * g.W, bn = tg::pick_bn(g.D);
       int Cr, T, big, mtiles;
@@ -1934,22 +1974,22 @@ struct Engine {
       const long long total = (long long)Bi * g.C * HW;
       const float* in = L.act_in;
       tg::shift3_kernel<<<grid_for((size_t)total), 256, 0, s>>>(
-          in, d_nhwc, raw_a ? nullptr : d_nhwc_lo, total, g.W);
+          in, cp, raw_a ? nullptr : d_nhwc_lo, total, g.W);
       const long long gt = (long long)Bi * g.D * HW;
       tg::scale_split_kernel<<<grid_for((size_t)gt), 256, 0, s>>>(L.gout, d_scale,
-                                                                  (long long)g.D * HW, gt, d_wt,
-                                                                  d_wt_lo);
+                                                                  (long long)g.D * HW, gt, wt,
+                                                                  wt_lo);
       tg::Params p{};
       const uint64_t da[4] = {(uint64_t)HW, (uint64_t)g.C, (uint64_t)Bi, 3};
       const uint64_t sa[3] = {4ull * HW, 4ull * HW * g.C, 4ull * total};
       const uint32_t ba[4] = {32, (uint32_t)Cr, 1, 1};
-      tg::make_map(&p.ta, d_nhwc, 4, da, sa, ba);
+      tg::make_map(&p.ta, cp, 4, da, sa, ba);
       tg::make_map(&p.ta_lo, d_nhwc_lo, 4, da, sa, ba);
       const uint64_t db[3] = {(uint64_t)HW, (uint64_t)g.D, (uint64_t)Bi};
       const uint64_t sb[2] = {4ull * HW, 4ull * HW * g.D};
       const uint32_t bb[3] = {32, (uint32_t)bn, 1};
-      tg::make_map(&p.tb, d_wt, 3, db, sb, bb);
-      tg::make_map(&p.tb_lo, d_wt_lo, 3, db, sb, bb);
+      tg::make_map(&p.tb, wt, 3, db, sb, bb);
+      tg::make_map(&p.tb_lo, wt_lo, 3, db, sb, bb);
       p.mode = tg::kConvDwSum;
       p.raw = raw_a ? 1 : 0;
       p.M = mtiles * 128;
@@ -1963,15 +2003,20 @@ struct Engine {
       const int S = L.ghost_splits;
       p.ex_per = (Bi + S - 1) / S;
       p.nex = Bi;
-      p.ws = d_dw_ws;
+      p.ws = wsp;
       const int splits = (Bi + p.ex_per - 1) / p.ex_per;
       tg::launch(p, bn, dim3(ntiles, mtiles, splits), s);
       const long long per = (long long)mtiles * ntiles * bn * 128;
       tg::dw_sum_reduce_kernel<<<grid_for((size_t)per), 256, 0, s>>>(
-          d_dw_ws, splits, mtiles, ntiles * bn, g.C, g.D, Cr, T, big,
+          wsp, splits, mtiles, ntiles * bn, g.C, g.D, Cr, T, big,
           d_sum + param_off[L.pblock]);
       nk += mark(s, "conv_dw_sum") + 3;
     }
+    for (int br = 1; br < kGhostBranches; ++br)
+      if (used & (1 << br)) {
+        PGB_CUDA(cudaEventRecord(ev_gjoin[br - 1], ghost_streams[br - 1]));
+        PGB_CUDA(cudaStreamWaitEvent(s0, ev_gjoin[br - 1], 0));
+      }
     return nk;
   }
 

@@ -210,7 +210,7 @@ struct Engine {
   cudaEvent_t ev_gfork = nullptr, ev_gjoin[kGhostBranches - 1] = {};
   std::vector<float*> d_gcp, d_gwt, d_gwt_lo, d_gws;
   float* d_nhwc_dw = nullptr;
-  bool dw_fork_ok() const { return dw_fork && dwh_raw && use_tma && !tma_all; }
+  bool dw_fork_ok() const { return dw_fork && dwh_raw && use_tma && !tma_all && !fused_mnist; }
   // forward / input-gradient / clipped-sum dW GEMMs: operand A as plain fp32,
   // its lo half split in the kernel (PGB_TMA_SPLIT=1: hi / lo tensors)
   bool raw_a = true;

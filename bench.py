@@ -382,6 +382,14 @@ def run_ours(args):
         uid = exchange_unique_id(rank)
         engine = Pk.GradEngine(model, Pk.Strategy(strat), BATCH, device=dev, rank=rank,
                                world=world, unique_id=uid)
+    elif args.dist_schedule:
+        # one GPU running the data-parallel step (aggregate mode 1 -> one-rank
+        # ncclAllReduce -> noise_update_kernel): the per-rank cost at N = 256 / B
+        from paper_2010_09063_b200.dist import nccl_unique_id
+        os.environ["PGB_FORCE_DIST"] = "1"
+        engine = Pk.GradEngine(model, Pk.Strategy(strat), BATCH, device=dev, rank=0, world=1,
+                               unique_id=nccl_unique_id())
+        del os.environ["PGB_FORCE_DIST"]
     else:
         engine = Pk.GradEngine(model, Pk.Strategy(strat), BATCH, device=dev)
     cfg = Pk.DpConfig(CLIP, SIGMA, LR, 1, SEED)
@@ -599,7 +607,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (bit-identical to io::synth_for_model, seed 0; rank r takes its "
                     "shard of every global batch); random-init params (models::build seed 0)",
-            "config": workload_config(args.model, world, BATCH, GBATCH),
+            "config": dict(workload_config(args.model, world, BATCH, GBATCH),
+                           **({"schedule": "data-parallel kernels on a one-rank NCCL "
+                               "communicator (--dist-schedule)"} if args.dist_schedule else {})),
             "e2e": {"value": e2e, "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * row * 4 + BATCH * 4,
                     "d2h_bytes_per_step": BATCH * 4 + 8,
@@ -638,6 +648,9 @@ def main():
                     help="global batch override (default: the config's batch)")
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling: --batch (or the config's batch) per GPU")
+    ap.add_argument("--dist-schedule", action="store_true",
+                    help="one GPU: run the multi-GPU step schedule on a one-rank NCCL "
+                         "communicator (per-rank cost proxy for N > 1)")
     ap.add_argument("--epochs", type=int, default=5,
                     help="timed full epochs of the e2e leg (median reported)")
     args = ap.parse_args()

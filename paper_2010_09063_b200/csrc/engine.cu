@@ -184,7 +184,8 @@ struct Engine {
   bool direct_dw = true;  // PGB_NO_DIRECT_DW=1: the first layer's dW on the gather GEMM
   bool smallc_dw(const ConvGeom& g) const {
     return direct_conv && direct_dw && g.C <= 4 && g.k == 3 && g.stride == 1 && g.pad == 1 && g.Ho == g.H &&
-           g.Wo == g.W && g.W == 32 && (size_t)g.C * (g.H + 2) * 34 * 4 <= 48 * 1024;
+           g.Wo == g.W && g.W == 32 &&
+           smallc_dw_smem_floats<4, 2>(g.H, 8) * sizeof(float) <= 110 * 1024;
   }
   bool smallc_fwd(const ConvGeom& g) const {
     return direct_conv && g.C <= 4 && g.k == 3 && g.stride == 1 && g.pad == 1 && g.Ho == g.H &&
@@ -1598,12 +1599,18 @@ struct Engine {
             }
             nk += mark(sd, "conv_dw_gram");
           } else if (smallc_dw(gg)) {
-            const size_t sm = sizeof(float) * (size_t)gg.C * (gg.H + 2) * 34;
+            // input rows + per-warp cotangent slices (8 warps x 2 channels, two
+            // passes; two blocks per SM so one block's loads overlap the other's sums)
+            auto launch = [&](auto kern, size_t floats) {
+              const size_t sm = sizeof(float) * floats;
+              gram_attr(kern, sm);
+              kern<<<Bi, 256, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock);
+            };
             switch (gg.C) {
-              case 1: conv3x3_smallc_dw_kernel<1, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              case 2: conv3x3_smallc_dw_kernel<2, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              case 3: conv3x3_smallc_dw_kernel<3, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
-              default: conv3x3_smallc_dw_kernel<4, 2><<<Bi, 512, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock); break;
+              case 1: launch(conv3x3_smallc_dw_kernel<1, 2>, smallc_dw_smem_floats<1, 2>(gg.H, 8)); break;
+              case 2: launch(conv3x3_smallc_dw_kernel<2, 2>, smallc_dw_smem_floats<2, 2>(gg.H, 8)); break;
+              case 3: launch(conv3x3_smallc_dw_kernel<3, 2>, smallc_dw_smem_floats<3, 2>(gg.H, 8)); break;
+              default: launch(conv3x3_smallc_dw_kernel<4, 2>, smallc_dw_smem_floats<4, 2>(gg.H, 8)); break;
             }
             nk += mark(sd, "conv_dw_pex_direct");
           } else if (tma_dw(gg)) {

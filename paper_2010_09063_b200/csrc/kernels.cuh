@@ -796,76 +796,140 @@ struct BlockTable {
 // 32-wide map (the CIFAR first layer) on the CUDA cores in fp32: one block per
 // example, lane = output column x, warp w = DPW output channels (more
 // warps loop over channel groups); each thread sums its column over all rows
-// into 4 x C x 9 accumulators (input rows staged zero-padded in shared
-// memory, cotangent rows read coalesced), then a fixed xor-shuffle tree adds
-// the 32 columns. Writes the reference's stack row (D, C, 3, 3)
-// (strategies.cpp:156-170) and the block's squared norm (fp64) into parts.
+// into 4 x C x 9 accumulators, then a fixed xor-shuffle tree adds the 32
+// columns. Input rows are staged zero-padded in shared memory and walked as a
+// three-row register window (one new padded row, C x 3 loads, per output row
+// instead of C x 9); each warp stages its DPW cotangent channels (DPW x H x 32
+// floats, contiguous in g) in its own shared slice with every 16-byte load in
+// flight at once, so no row waits on a global round trip. Writes the
+// reference's stack row (D, C, 3, 3) (strategies.cpp:156-170) and the block's
+// squared norm (fp64) into parts.
+// per-warp slice: the staged cotangent rows, later the column-sum transpose
 template <int C, int DPW>
-__global__ void __launch_bounds__(512) conv3x3_smallc_dw_kernel(
+__host__ __device__ constexpr size_t smallc_dw_slice_floats(int H) {
+  return (((size_t)DPW * H * 32 > (size_t)DPW * C * 9 * 33 ? (size_t)DPW * H * 32
+                                                            : (size_t)DPW * C * 9 * 33) + 3) &
+         ~(size_t)3;
+}
+template <int C, int DPW>
+__host__ __device__ constexpr size_t smallc_dw_smem_floats(int H, int nw) {
+  return (((size_t)C * (H + 2) * 34 + 3) & ~(size_t)3) + (size_t)nw * smallc_dw_slice_floats<C, DPW>(H);
+}
+
+template <int C, int DPW>
+__global__ void __launch_bounds__(256, 2) conv3x3_smallc_dw_kernel(
     const float* __restrict__ x, const float* __restrict__ g, float* __restrict__ stack, int D,
     int H, double* __restrict__ parts, int nparts, int pb) {
   constexpr int W = 32, WP = 34, K = C * 9;
-  extern __shared__ float xs[];  // [C][H + 2][34], zero border
+  extern __shared__ __align__(16) float xs[];  // [C][H + 2][34], zero border; then the g slices
   __shared__ double wsq[16];
   const int z = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   const float* xz = x + (size_t)z * C * H * W;
-  for (int e = threadIdx.x; e < C * (H + 2) * WP; e += blockDim.x) {
-    const int c = e / ((H + 2) * WP), r = e - c * (H + 2) * WP;
-    const int yy = r / WP - 1, xx = r % WP - 1;
-    xs[e] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? xz[((size_t)c * H + yy) * W + xx] : 0.0f;
+  // staged in batches with every load of a batch in flight before its stores
+  // (a plain copy loop would wait one global round trip per element)
+  constexpr int kXB = 8;
+  for (int e0 = threadIdx.x; e0 < C * (H + 2) * WP; e0 += kXB * blockDim.x) {
+    float v[kXB];
+#pragma unroll
+    for (int q = 0; q < kXB; ++q) {
+      const int e = e0 + q * blockDim.x;
+      const int c = e / ((H + 2) * WP), r = e - c * (H + 2) * WP;
+      const int yy = r / WP - 1, xx = r % WP - 1;
+      v[q] = (e < C * (H + 2) * WP && yy >= 0 && yy < H && xx >= 0 && xx < W)
+                 ? __ldg(xz + ((size_t)c * H + yy) * W + xx) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < kXB; ++q)
+      if (e0 + q * blockDim.x < C * (H + 2) * WP) xs[e0 + q * blockDim.x] = v[q];
   }
+  float* gs = xs + ((C * (H + 2) * WP + 3) & ~3) + (size_t)warp * smallc_dw_slice_floats<C, DPW>(H);
   __syncthreads();
   double sq = 0.0;
   for (int d0 = warp * DPW; d0 < D; d0 += nw * DPW) {
+    {  // this warp's cotangent channels d0 .. d0 + DPW - 1 (zero past D)
+      const int nch = min(DPW, D - d0);
+      const float* src = g + ((size_t)z * D + d0) * H * W;
+      const int n = nch * H * W;
+      constexpr int kGB = 8;
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(gs);
+        for (int e0 = lane; e0 < n / 4; e0 += 32 * kGB) {
+          float4 r[kGB];
+#pragma unroll
+          for (int q = 0; q < kGB; ++q)
+            if (e0 + 32 * q < n / 4) r[q] = __ldg(s4 + e0 + 32 * q);
+#pragma unroll
+          for (int q = 0; q < kGB; ++q)
+            if (e0 + 32 * q < n / 4) d4[e0 + 32 * q] = r[q];
+        }
+      } else {
+        for (int e = lane; e < n; e += 32) gs[e] = __ldg(src + e);
+      }
+      for (int e = n + lane; e < DPW * H * W; e += 32) gs[e] = 0.0f;
+      __syncwarp();
+    }
     float acc[DPW][K];
 #pragma unroll
     for (int dd = 0; dd < DPW; ++dd)
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[dd][k] = 0.0f;
-    const float* gz = g + ((size_t)z * D + d0) * H * W;
-    float gn[DPW];  // the next row's cotangent, loaded one row ahead
+    // padded rows y, y + 1, y + 2 of every input channel at columns lane .. lane + 2
+    float xw[3][C][3];
 #pragma unroll
-    for (int dd = 0; dd < DPW; ++dd) gn[dd] = d0 + dd < D ? __ldg(gz + (size_t)dd * H * W + lane) : 0.0f;
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) xw[u][c][v] = xs[(c * (H + 2) + u) * WP + lane + v];
     for (int y = 0; y < H; ++y) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) xw[2][c][v] = xs[(c * (H + 2) + y + 2) * WP + lane + v];
       float gv[DPW];
 #pragma unroll
-      for (int dd = 0; dd < DPW; ++dd) {
-        gv[dd] = gn[dd];
-        gn[dd] = (d0 + dd < D && y + 1 < H) ? __ldg(gz + ((size_t)dd * H + y + 1) * W + lane) : 0.0f;
-      }
+      for (int dd = 0; dd < DPW; ++dd) gv[dd] = gs[(dd * H + y) * W + lane];
 #pragma unroll
       for (int c = 0; c < C; ++c)
 #pragma unroll
         for (int u = 0; u < 3; ++u)
 #pragma unroll
           for (int v = 0; v < 3; ++v) {
-            const float xv = xs[(c * (H + 2) + y + u) * WP + lane + v];
+            const float xv = xw[u][c][v];
 #pragma unroll
             for (int dd = 0; dd < DPW; ++dd)
               acc[dd][c * 9 + u * 3 + v] = fmaf(gv[dd], xv, acc[dd][c * 9 + u * 3 + v]);
           }
-    }
-    // the 32 columns: a fixed xor tree (every lane ends with the total)
 #pragma unroll
-    for (int dd = 0; dd < DPW; ++dd)
+      for (int c = 0; c < C; ++c)
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        float a = acc[dd][k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        acc[dd][k] = a;
-      }
-    // lane l writes elements l, l + 32, ... of the DPW x K contiguous stack values
-    float* st = stack + ((size_t)z * D + d0) * K;
-#pragma unroll
-    for (int dd = 0; dd < DPW; ++dd)
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (((dd * K + k) & 31) == lane && d0 + dd < D) {
-          st[dd * K + k] = acc[dd][k];
-          sq = fma((double)acc[dd][k], (double)acc[dd][k], sq);
+        for (int v = 0; v < 3; ++v) {
+          xw[0][c][v] = xw[1][c][v];
+          xw[1][c][v] = xw[2][c][v];
         }
+    }
+    // the 32 columns: transposed through the warp's slice (rows of 33 floats,
+    // conflict-free), lane l then sums outputs l, l + 32, ... in column order
+    __syncwarp();  // every lane is done reading the cotangent rows
+#pragma unroll
+    for (int dd = 0; dd < DPW; ++dd)
+#pragma unroll
+      for (int k = 0; k < K; ++k) gs[(dd * K + k) * 33 + lane] = acc[dd][k];
+    __syncwarp();
+    float* st = stack + ((size_t)z * D + d0) * K;
+    for (int o = lane; o < DPW * K; o += 32) {
+      const float* row = gs + o * 33;
+      float a = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a += row[j];
+      if (d0 + o / K < D) {
+        st[o] = a;
+        sq = fma((double)a, (double)a, sq);
+      }
+    }
+    __syncwarp();  // every lane is done with the slice before the next group overwrites it
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);

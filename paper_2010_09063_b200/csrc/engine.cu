@@ -451,8 +451,7 @@ struct Engine {
   int tma_conv_fwd(cudaStream_t s, const ConvGeom& g, int Bi, const float* x, const float* W,
                    const float* bias, float* out, bool relu, int layer = -1) {
     const int Cp = tg::round32(g.C), HW = g.H * g.W, bn = tg::pick_bn(g.D);
-    tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Cp / 32, Bi), dim3(32, 8), 0, s>>>(
-        x, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.C, HW, Cp);
+    tg::nchw_to_nhwc(x, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.C, HW, Cp, Bi, s);
     const bool pre = layer >= 0 && d_wall && wall_fwd[layer] >= 0;
     float* wt = pre ? d_wall + wall_fwd[layer] : d_wt;
     float* wt_lo = pre ? d_wall_lo + wall_fwd[layer] : d_wt_lo;
@@ -556,8 +555,7 @@ struct Engine {
   int tma_conv_dx(cudaStream_t s, const ConvGeom& g, int Bi, const float* gout, const float* W,
                   const float* mask, float* gx, int layer = -1) {
     const int Dp = tg::round32(g.D), HW = g.H * g.W, bn = tg::pick_bn(g.C);
-    tg::nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Dp / 32, Bi), dim3(32, 8), 0, s>>>(
-        gout, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.D, HW, Dp);
+    tg::nchw_to_nhwc(gout, d_nhwc, raw_a ? nullptr : d_nhwc_lo, g.D, HW, Dp, Bi, s);
     const bool pre = layer >= 0 && d_wall && wall_dx[layer] >= 0;
     float* wt = pre ? d_wall + wall_dx[layer] : d_wt;
     float* wt_lo = pre ? d_wall_lo + wall_dx[layer] : d_wt_lo;

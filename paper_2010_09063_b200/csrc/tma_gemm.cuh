@@ -945,6 +945,76 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __rest
   }
 }
 
+// nchw_to_nhwc_kernel over CB channels x 32 NQ positions per block (4096
+// elements: (32, 128), (64, 64) or (128, 32)): each thread has its 16 loads in
+// flight before the first store (the 32 x 32 version keeps ~4 KB per block in
+// flight and ran at ~40% of HBM on the 32 x 32 CIFAR maps). Same values, same
+// layout; the tile rows padded by one float keep both passes conflict-free.
+template <int NQ, int CB>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_wide_kernel(const float* __restrict__ src,
+                                                                float* __restrict__ dst,
+                                                                float* __restrict__ dst_lo, int C,
+                                                                int HW, int Cp) {
+  static_assert(NQ * CB == 128, "16 elements per thread");
+  constexpr int PB = 32 * NQ;
+  __shared__ float tile[CB][PB + 1];  // [c][p]
+  const int n = blockIdx.z, p0 = blockIdx.x * PB, c0 = blockIdx.y * CB;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  float v[CB / 8][NQ];
+#pragma unroll
+  for (int j = 0; j < CB / 8; ++j) {
+    const int c = c0 + ty + 8 * j;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int p = p0 + 32 * q + tx;
+      v[j][q] = (c < C && p < HW) ? __ldg(src + ((size_t)n * C + c) * HW + p) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CB / 8; ++j)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tile[ty + 8 * j][32 * q + tx] = v[j][q];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PB / 8; ++j) {
+    const int pp = ty + 8 * j, p = p0 + pp;
+    if (p < HW) {
+#pragma unroll
+      for (int k = 0; k < CB / 32; ++k) {
+        const int c = c0 + tx + 32 * k;
+        const float x = tile[tx + 32 * k][pp];
+        if (!dst_lo) {
+          dst[((size_t)n * HW + p) * Cp + c] = x;
+        } else {
+          float hi, lo;
+          split2(x, hi, lo);
+          dst[((size_t)n * HW + p) * Cp + c] = hi;
+          dst_lo[((size_t)n * HW + p) * Cp + c] = lo;
+        }
+      }
+    }
+  }
+}
+
+// NCHW -> NHWC (channels padded to Cp) of Bi examples: 4096-element tiles
+// shaped to the map (positions x channels), else the 32 x 32 kernel
+inline void nchw_to_nhwc(const float* src, float* dst, float* dst_lo, int C, int HW, int Cp,
+                         int Bi, cudaStream_t s) {
+  const dim3 blk(32, 8);
+  if (HW >= 128)
+    nchw_to_nhwc_wide_kernel<4, 32><<<dim3((HW + 127) / 128, Cp / 32, Bi), blk, 0, s>>>(
+        src, dst, dst_lo, C, HW, Cp);
+  else if (HW > 32 && Cp % 64 == 0)
+    nchw_to_nhwc_wide_kernel<2, 64><<<dim3((HW + 63) / 64, Cp / 64, Bi), blk, 0, s>>>(
+        src, dst, dst_lo, C, HW, Cp);
+  else if (Cp % 128 == 0)
+    nchw_to_nhwc_wide_kernel<1, 128><<<dim3((HW + 31) / 32, Cp / 128, Bi), blk, 0, s>>>(
+        src, dst, dst_lo, C, HW, Cp);
+  else
+    nchw_to_nhwc_kernel<<<dim3((HW + 31) / 32, Cp / 32, Bi), blk, 0, s>>>(src, dst, dst_lo, C, HW,
+                                                                         Cp);
+}
+
 // the 3xTF32 pair of a tensor, element-wise
 __global__ void split_kernel(const float* __restrict__ src, float* __restrict__ hi,
                              float* __restrict__ lo, long long n) {

@@ -1602,7 +1602,7 @@ struct Engine {
             auto launch = [&](auto kern, size_t floats) {
               const size_t sm = sizeof(float) * floats;
               gram_attr(kern, sm);
-              kern<<<Bi, 256, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock);
+              kern<<<Bi, 256, sm, sd>>>(in, gcur, sW, gg.D, gg.H, d_parts, nparts, L.pblock, sb);
             };
             switch (gg.C) {
               case 1: launch(conv3x3_smallc_dw_kernel<1, 2>, smallc_dw_smem_floats<1, 2>(gg.H, 8)); break;
@@ -1630,7 +1630,9 @@ struct Engine {
             launch_gemm(dw, Bi, sd);
             nk += mark(sd, "conv_dw_pex");
           }
-          if (!(ghost_next && L.ghost)) {  // (the Gram kernel wrote the ghost layers' bias rows)
+          // (the Gram kernel wrote the ghost layers' bias rows, the direct dW kernel the
+          // few-channel first layer's)
+          if (!(ghost_next && L.ghost) && !smallc_dw(gg)) {
             conv_db_pex_kernel<<<(Bi * gg.D * 32 + 255) / 256, 256, 0, sd>>>(gcur, Bi * gg.D, Pp,
                                                                            sb);
             nk += mark(sd, "conv_db_pex");

@@ -819,7 +819,7 @@ __host__ __device__ constexpr size_t smallc_dw_smem_floats(int H, int nw) {
 template <int C, int DPW>
 __global__ void __launch_bounds__(256, 2) conv3x3_smallc_dw_kernel(
     const float* __restrict__ x, const float* __restrict__ g, float* __restrict__ stack, int D,
-    int H, double* __restrict__ parts, int nparts, int pb) {
+    int H, double* __restrict__ parts, int nparts, int pb, float* __restrict__ sb) {
   constexpr int W = 32, WP = 34, K = C * 9;
   extern __shared__ __align__(16) float xs[];  // [C][H + 2][34], zero border; then the g slices
   __shared__ double wsq[16];
@@ -869,6 +869,16 @@ __global__ void __launch_bounds__(256, 2) conv3x3_smallc_dw_kernel(
       }
       for (int e = n + lane; e < DPW * H * W; e += 32) gs[e] = 0.0f;
       __syncwarp();
+      // the example's bias gradient of these channels from the staged rows,
+      // with conv_db_pex_kernel's arithmetic (lane-strided partials, xor
+      // butterfly): bitwise the same, and the cotangent is not read again
+      for (int dd = 0; dd < nch; ++dd) {
+        float sbv = 0.0f;
+        for (int p = lane; p < H * W; p += 32) sbv += gs[dd * H * W + p];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sbv += __shfl_xor_sync(0xffffffffu, sbv, o);
+        if (lane == 0) sb[(size_t)z * D + d0 + dd] = sbv;
+      }
     }
     float acc[DPW][K];
 #pragma unroll
